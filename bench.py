@@ -1,0 +1,449 @@
+"""Benchmark of the quantised tensor-adapter linear hot path (BASELINE.json north star).
+
+Workload (BASELINE.json configs[1], "config 2"): the Llama-2-7B linear set — q/k/v/o 4096x4096,
+gate/up 11008x4096, down 4096x11008 — int8 per-row quantised from ~N(0, 0.02) weights, a TT
+adapter of rank 8 on every linear, 8x2048 = 16384 bf16 tokens ~N(0, 1) per GPU.  One step =
+forward (per-token act-quant, int8 tcgen05 GEMM, dequant epilogue + adapter) and backward with
+recompute (adapter-core gradients + dx) of all seven linears, then (N > 1) the NCCL all-reduce
+of the flat adapter-gradient buffer.  Data is synthetic (seeded); there is no dataset.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 2|3]
+
+N > 1 runs under torchrun (one process per GPU, NCCL); the line is printed by rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "quantized-adapter linear fwd+bwd tokens/s"
+UNIT = "tokens/s"
+
+LINEARS_7B = [  # (name, fan_out, fan_in, input) in forward order (transformer.py:862-874)
+    ("wq", 4096, 4096, "attn"), ("wk", 4096, 4096, "attn"), ("wv", 4096, 4096, "attn"),
+    ("wo", 4096, 4096, "ctx"), ("wu", 11008, 4096, "ffn"), ("wg", 11008, 4096, "ffn"),
+    ("wd", 4096, 11008, "act"),
+]
+BACKWARD_ORDER = ["wd", "wu", "wg", "wo", "wq", "wk", "wv"]  # transformer.py:919-944
+INPUT_DIMS = {"attn": 4096, "ctx": 4096, "ffn": 4096, "act": 11008}
+
+CONFIGS = {
+    "2": {"bits": 8, "rank": 8, "batch": 8, "seq": 2048},
+    "3": {"bits": 4, "rank": 16, "batch": 16, "seq": 4096},  # global tokens; sharded over ranks
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def workload_config(cfg_name, world):
+    c = CONFIGS[cfg_name]
+    if cfg_name == "3":  # [16, 4096] global tokens, strong-scaled over ranks
+        tokens = c["batch"] * c["seq"] // world
+        scaling = "strong"
+    else:
+        tokens = c["batch"] * c["seq"]
+        scaling = "weak"
+    desc = {
+        "workload": (f"llama2-7b linear set q/k/v/o 4096x4096, gate/up 11008x4096, down 4096x11008; int{c['bits']} "
+                     f"per-row weights; TT adapter r={c['rank']} m=(1,N/256,256) n=(K/16,4,4); "
+                     f"{tokens} bf16 tokens/GPU; fwd + bwd-with-recompute (+ NCCL grad all-reduce)"),
+        "baseline_config": int(cfg_name),
+        "tokens_per_gpu": tokens,
+        "bits": c["bits"],
+        "rank": c["rank"],
+        "l2": "inputs larger than L2 (>= 763 MB of layer inputs + 1.4 GB of upstream grads per step)",
+        "parallelism": f"dp{world}",
+    }
+    return c, tokens, scaling, desc
+
+
+def clocks_sampler_start(path):
+    try:
+        return subprocess.Popen(
+            ["nvidia-smi", "--query-gpu=index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+             "--format=csv,noheader,nounits", "-lms", "200"],
+            stdout=open(path, "w"), stderr=subprocess.DEVNULL)
+    except Exception:
+        return None
+
+
+def clocks_sampler_stop(proc, path, device_index):
+    if proc is None:
+        return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+    proc.terminate()
+    try:
+        proc.wait(timeout=5)
+    except Exception:
+        proc.kill()
+    sms, maxes, reasons = [], [], set()
+    names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    for line in open(path):
+        parts = [p.strip() for p in line.split(",")]
+        if len(parts) < 9 or not parts[0].isdigit() or int(parts[0]) != device_index:
+            continue
+        try:
+            sms.append(float(parts[1]))
+            maxes.append(float(parts[2]))
+        except ValueError:
+            continue
+        for nm, flag in zip(names, parts[5:9]):
+            if flag.lower() == "active":
+                reasons.add(nm)
+    return {"sm_mhz": statistics.median(sms) if sms else None, "sm_max_mhz": max(maxes) if maxes else None,
+            "reasons": sorted(reasons), "samples": len(sms)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+# ----------------------------------------------------------------------------- CPU baseline / reference arm
+
+
+def cpu_reference_step_fn(cfg, sample_tokens, seed=0):
+    """The oracle's staged numpy port of the same 7-linear step on `sample_tokens` tokens
+    (TEST/BASELINE INFRASTRUCTURE: used only for the CPU baseline and --impl reference)."""
+    import numpy as np
+
+    import oracle as O
+
+    rng = np.random.default_rng(seed)
+    mats = {}
+    for name, n, k, _ in LINEARS_7B:
+        w = (rng.standard_normal((n, k), dtype=np.float32) * 0.02)
+        q = O.quantize_rows(w, cfg["bits"])
+        shape = O.tt_modes_for(n, k, cfg["rank"])
+        cores = [rng.standard_normal(shape.core_shape(i)) * 0.01 for i in range(shape.d)]
+        mats[name] = (q, cores)
+    xs = {kind: O.to_bf16(rng.standard_normal((sample_tokens, d), dtype=np.float32)) for kind, d in INPUT_DIMS.items()}
+    dys = {name: O.to_bf16(rng.standard_normal((sample_tokens, n), dtype=np.float32)) for name, n, _, _ in LINEARS_7B}
+    inputs = {name: kind for name, _, _, kind in LINEARS_7B}
+
+    def step():
+        for name, _, _, _ in LINEARS_7B:
+            q, cores = mats[name]
+            O.qa_step_staged(xs[inputs[name]], dys[name], q, cores)
+
+    return step
+
+
+def cpu_threads():
+    try:
+        import threadpoolctl
+
+        info = threadpoolctl.threadpool_info()
+        blas = [i for i in info if i.get("internal_api") in ("openblas", "mkl", "blis")]
+        if blas:
+            return int(blas[0]["num_threads"]), f"{blas[0]['internal_api']} {blas[0].get('version', '')}".strip()
+    except Exception:
+        pass
+    return os.cpu_count() or 1, "numpy BLAS"
+
+
+def run_cpu_baseline(cfg, sample_tokens=256, repeats=3):
+    step = cpu_reference_step_fn(cfg, sample_tokens)
+    step()  # warm (BLAS thread start-up, page faults)
+    times = []
+    for _ in range(repeats):
+        t0 = time.perf_counter()
+        step()
+        times.append(time.perf_counter() - t0)
+    sec = statistics.median(times)
+    threads, blas = cpu_threads()
+    return {
+        "value": sample_tokens / sec,
+        "unit": UNIT,
+        "cores": threads,
+        "kind": "port",
+        "sample": (f"{sample_tokens} tokens through all 7 linears (fwd + bwd) with the oracle's staged numpy fp64 "
+                   f"port of the reference path (quant.py quantize_rows/qmatmul/qmatmul_t + TT adapter), median "
+                   f"of {repeats}, {blas}, {threads} threads; weights quantised outside the timed region"),
+    }
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    if rank != 0:
+        return 0
+    cfg, tokens, scaling, desc = workload_config(args.config, world)
+    sample = 256
+    step = cpu_reference_step_fn(cfg, sample)
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    sec = (time.perf_counter() - t0) / max(args.steps, 1)
+    threads, blas = cpu_threads()
+    value = sample / sec
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+        "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": desc,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{sample} tokens/step through the 7 linears, oracle staged numpy fp64 port "
+                                   f"({blas}); the reference lrlm itself cannot travel to the GPU box"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- GPU arm
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2402_13533_b200 import _lib
+    from paper_2402_13533_b200.linear import TTSpec
+    from paper_2402_13533_b200.quant import quantize_rows
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (the product has no CPU path)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg, T, scaling, desc = workload_config(args.config, world)
+    lib = _lib.lib()
+    stream = torch.cuda.current_stream(dev)
+    sptr = stream.cuda_stream
+
+    # --- frozen quantised base + TT adapters (identical on every rank: same seed)
+    gen = torch.Generator(device=dev).manual_seed(1234)
+    mats = {}
+    ws_bytes = 0
+    grad_numel = 0
+    for name, n, k, kind in LINEARS_7B:
+        w = torch.randn((n, k), generator=gen, device=dev, dtype=torch.float32) * 0.02
+        q = quantize_rows(w, cfg["bits"])
+        del w
+        spec = TTSpec.for_shape(n, k, cfg["rank"])
+        cores = [torch.randn(spec.core_shape(i), generator=gen, device=dev) * 0.01 for i in range(spec.d)]
+        wc, ttc = q.as_c(), spec.as_c(cores)
+        ws_bytes = max(ws_bytes, lib.qa_linear_workspace_bytes(ctypes.byref(wc), ctypes.byref(ttc), T))
+        mats[name] = dict(q=q, spec=spec, cores=cores, wc=wc, ttc=ttc, n=n, k=k, kind=kind)
+        grad_numel += spec.param_count()
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    flat_grad = torch.zeros(grad_numel, dtype=torch.float32, device=dev)
+    off = 0
+    for name, n, k, kind in LINEARS_7B:
+        m = mats[name]
+        views = []
+        for i in range(m["spec"].d):
+            numel = int(torch.tensor(m["spec"].core_shape(i)).prod())
+            views.append(flat_grad[off: off + numel])
+            off += numel
+        m["gptr"] = (ctypes.c_void_p * _lib.QA_TT_MAX_D)(*[v.data_ptr() for v in views])
+
+    # --- per-rank synthetic activations / upstream grads (rank-dependent seed: different token shards)
+    dgen = torch.Generator(device=dev).manual_seed(99 + rank)
+
+    def make_inputs():
+        xs = {kd: torch.randn((T, d), generator=dgen, device=dev).to(torch.bfloat16) for kd, d in INPUT_DIMS.items()}
+        dys = {nm: torch.randn((T, n), generator=dgen, device=dev).to(torch.bfloat16) for nm, n, _, _ in LINEARS_7B}
+        return xs, dys
+
+    xs, dys = make_inputs()
+    ys = {nm: torch.empty((T, n), dtype=torch.bfloat16, device=dev) for nm, n, _, _ in LINEARS_7B}
+    dxs = {nm: torch.empty((T, k), dtype=torch.bfloat16, device=dev) for nm, _, k, _ in LINEARS_7B}
+    BF16 = _lib.QA_BF16
+
+    def step(xs, dys):
+        for name, _, _, kind in LINEARS_7B:
+            m = mats[name]
+            st = lib.qa_linear_forward(ctypes.byref(m["wc"]), ctypes.byref(m["ttc"]), xs[kind].data_ptr(), BF16, T,
+                                       ys[name].data_ptr(), None, None, None, ws.data_ptr(), ws_bytes, sptr)
+            if st:
+                _lib.check(st, f"forward {name}")
+        for name in BACKWARD_ORDER:
+            m = mats[name]
+            st = lib.qa_linear_backward(ctypes.byref(m["wc"]), ctypes.byref(m["ttc"]), xs[m["kind"]].data_ptr(), BF16,
+                                        dys[name].data_ptr(), BF16, T, dxs[name].data_ptr(), None,
+                                        ctypes.cast(m["gptr"], ctypes.POINTER(ctypes.c_void_p)), 0, ws.data_ptr(),
+                                        ws_bytes, sptr)
+            if st:
+                _lib.check(st, f"backward {name}")
+        if world > 1:
+            dist.all_reduce(flat_grad, op=dist.ReduceOp.SUM)
+            flat_grad.div_(world)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # --- warm-up, then exactly K timed steps bracketed by barrier + synchronize
+    for _ in range(max(args.warmup, 3)):
+        step(xs, dys)
+    torch.cuda.synchronize(dev)
+    barrier()
+    torch.cuda.synchronize(dev)
+    clk_path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{rank}.csv") if os.path.isdir(
+        os.path.join(ROOT, "gpurun_out")) else f"/tmp/qa_clocks_rank{rank}.csv"
+    sampler = clocks_sampler_start(clk_path) if local == 0 else None
+    time.sleep(0.4 if sampler else 0)
+    n_launch0 = lib.qa_launch_count()
+    lib.qa_timing_enable(1)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step(xs, dys)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    barrier()
+    torch.cuda.synchronize(dev)
+    launches = (lib.qa_launch_count() - n_launch0) // max(args.steps, 1)
+    per_class = {c: _lib.timing_read(c) for c in ("gemm_i8", "gemm_bf16", "quantize", "tt", "dequant")}
+    lib.qa_timing_enable(0)
+    clocks = clocks_sampler_stop(sampler, clk_path, local) if sampler else None
+    ms_total = max_over_ranks(e0.elapsed_time(e1))
+    ms_step = ms_total / args.steps
+    value = T * world / (ms_step / 1e3)
+
+    # --- roofline of the dominant kernel class (live CUDA-event durations of the timed region)
+    peaks, peak_src = measured_peaks()
+    dom = max(per_class, key=lambda c: per_class[c][0])
+    dms, dn, dwork = per_class[dom]
+    kernels = {}
+    for c, (cms, cn, cw) in per_class.items():
+        if cn == 0:
+            continue
+        avg_s = cms / cn / 1e3
+        if c.startswith("gemm"):
+            kernels[c] = {"ms_per_step": cms / args.steps, "launches_per_step": cn / args.steps,
+                          "achieved_tflops": cw / cn / avg_s / 1e12, "share_of_step": cms / ms_total}
+        else:
+            kernels[c] = {"ms_per_step": cms / args.steps, "launches_per_step": cn / args.steps,
+                          "achieved_gbs" if c != "tt" else "achieved_tflops":
+                              (cw / cn / avg_s / 1e9) if c != "tt" else (cw / cn / avg_s / 1e12),
+                          "share_of_step": cms / ms_total}
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tfile):
+        traffic = json.load(open(tfile)).get(dom)
+    if dom.startswith("gemm"):
+        achieved = dwork / dn / (dms / dn / 1e3) / 1e12
+        if dom == "gemm_bf16":
+            peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
+            note = f"bf16 dense, sustained, of {peak_src} (MEASURED_PEAKS.json)"
+        else:
+            peak = 4500.0
+            note = "int8 dense: no measured int8 peak in MEASURED_PEAKS.json; NVIDIA B200 spec 4.5 POPS"
+        roofline = {"kernel": dom, "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                    "frac": achieved / peak, "traffic": traffic, "peak_source": note,
+                    "work_per_launch": dwork / dn, "launch_ms": dms / dn}
+    else:
+        achieved = dwork / dn / (dms / dn / 1e3) / 1e9
+        peak = peaks["hbm_gbs"]
+        roofline = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "traffic": traffic, "peak_source": f"HBM copy, of {peak_src}"}
+
+    # --- end-to-end through the C ABI with host buffers: pinned H2D of every step's inputs
+    # (double-buffered on a copy stream, overlapping the previous step) + D2H of the gradients
+    e2e = None
+    if not args.no_e2e:
+        host_x = {kd: v.cpu().pin_memory() for kd, v in xs.items()}
+        host_dy = {nm: v.cpu().pin_memory() for nm, v in dys.items()}
+        host_grad = torch.empty(grad_numel, dtype=torch.float32).pin_memory()
+        bufs = [(xs, dys), make_inputs()]
+        copy_stream = torch.cuda.Stream(dev)
+        h2d = sum(v.numel() * v.element_size() for v in host_x.values()) + \
+            sum(v.numel() * v.element_size() for v in host_dy.values())
+        d2h = host_grad.numel() * 4
+        uploaded = [torch.cuda.Event() for _ in range(2)]
+        consumed = [torch.cuda.Event() for _ in range(2)]
+
+        def upload(i):
+            bx, bdy = bufs[i % 2]
+            with torch.cuda.stream(copy_stream):
+                copy_stream.wait_event(consumed[i % 2])
+                for kd in bx:
+                    bx[kd].copy_(host_x[kd], non_blocking=True)
+                for nm in bdy:
+                    bdy[nm].copy_(host_dy[nm], non_blocking=True)
+                uploaded[i % 2].record(copy_stream)
+
+        for i in range(2):
+            consumed[i].record(stream)
+        torch.cuda.synchronize(dev)
+        barrier()
+        k_e2e = max(3, min(args.steps, 10))
+        t0 = time.perf_counter()
+        upload(0)
+        for i in range(k_e2e):
+            if i + 1 < k_e2e:
+                upload(i + 1)
+            stream.wait_event(uploaded[i % 2])
+            step(*bufs[i % 2])
+            consumed[i % 2].record(stream)
+            host_grad.copy_(flat_grad, non_blocking=True)
+        torch.cuda.synchronize(dev)
+        barrier()
+        sec = max_over_ranks(time.perf_counter() - t0)
+        e2e = {"value": k_e2e * T * world / sec, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "steps": k_e2e,
+               "note": "C-ABI calls on pinned host inputs; H2D of step i+1 overlaps compute of step i"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = run_cpu_baseline(cfg)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": scaling,
+            "vs_baseline": None, "dtype": "int8 (u8xu8->s32) GEMM + bf16", "data": "synthetic",
+            "config": desc, "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(launches * args.steps), "gpu_launches_per_step": int(launches), "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,154 @@
+/*
+ * qadapter.h — C ABI of the B200-native quantised tensor-adapter linear.
+ *
+ * The reference (`lrlm`, /root/reference/pkg/src/lrlm) is pure Python + numpy and has
+ * no FFI; its drop-in boundary is the duck-typed linear-backend protocol plus the
+ * module functions of quant.py / lowrank.py.  Each entry point below
+ * replaces one of those reference functions; the cited file:line is the interface it
+ * stands in for.  The Python mirror (paper_2402_13533_b200/) binds these with ctypes
+ * (INTEGRATION.md shows the binding).
+ *
+ * Conventions
+ *   - every pointer is a caller-owned DEVICE pointer; the library never allocates or
+ *     frees device memory.  Scratch space is caller-allocated and sized by the
+ *     matching *_workspace_bytes() query.
+ *   - `stream` is a cudaStream_t passed as void*; all work is stream-ordered and the
+ *     functions return without synchronising.
+ *   - weights are stored (rows = fan_out, cols = fan_in) and applied as x · Wᵀ
+ *     (transformer.py:5-7).  Codes use the reference layout exactly: u8 [rows, cols]
+ *     for 8 bits, two codes per byte (even column in the low nibble, odd cols padded)
+ *     [rows, ceil(cols/2)] for 4 bits (quant.py:37-52).
+ *   - return value: QA_OK or a negative qa_status; qa_last_error() describes it.
+ *     Non-finite inputs are detected on the device and reported through a
+ *     caller-provided int32 flag (checked by the caller at its next sync point),
+ *     mirroring QuantError (quant.py:79-80).
+ */
+#ifndef QADAPTER_H
+#define QADAPTER_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define QA_API __attribute__((visibility("default")))
+#else
+#define QA_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  QA_OK = 0,
+  QA_ERR_ARG = -1,         /* bad pointer / shape / stride        (QuantError / ModelError) */
+  QA_ERR_BITS = -2,        /* bits not in {4, 8}                  (quant.py:74-75)          */
+  QA_ERR_CUDA = -3,        /* a CUDA runtime / driver call failed                           */
+  QA_ERR_UNSUPPORTED = -4, /* shape outside the tensor-core path's constraints              */
+  QA_ERR_WORKSPACE = -5    /* workspace smaller than *_workspace_bytes()                    */
+} qa_status;
+
+typedef enum { QA_F32 = 0, QA_BF16 = 1 } qa_dtype;
+
+#define QA_TT_MAX_D 4
+
+/* Frozen quantised base weight (quant.py:55-70 QuantizedMatrix, on the device). */
+typedef struct {
+  int64_t rows;          /* fan_out N */
+  int64_t cols;          /* fan_in  K */
+  int32_t bits;          /* 4 or 8 */
+  const uint8_t* codes;  /* reference layout, see above */
+  const float* scale;    /* [rows] f32, (hi - lo) / (2^bits - 1) rounded to f32 */
+  const float* offset;   /* [rows] f32, row minimum */
+  const int32_t* rowsum; /* [rows] Σ_k code[n, k] (unpacked), written by qa_quantize_rows */
+} qa_qweight;
+
+/* Tensor-train adapter ΔW = W_t.
+ * core k has shape (r[k], m[k], n[k], r[k+1]) row-major fp32, r[0] = r[d] = 1,
+ * W_t[(i1..id), (j1..jd)] = G1[0,i1,j1,:] · G2[:,i2,j2,:] ··· Gd[:,id,jd,0]. */
+typedef struct {
+  int32_t d;
+  int32_t m[QA_TT_MAX_D];
+  int32_t n[QA_TT_MAX_D];
+  int32_t r[QA_TT_MAX_D + 1];
+  const float* cores[QA_TT_MAX_D];
+} qa_tt;
+
+QA_API const char* qa_version(void);
+QA_API const char* qa_last_error(void);
+
+/* quantize_rows (quant.py:73-99), also the per-token activation quantiser
+ * (quantize_rows on x.reshape(-1, K); quantize_activations, quant.py:147-152).
+ * w: [rows, cols] with row stride ld_w elements, dtype QA_F32 or QA_BF16.
+ * codes: reference layout with row stride ld_codes bytes; for bits == 8 the bytes
+ * [cols, pad_cols) of each row are zero-filled (GEMM operand padding; pass
+ * pad_cols = cols for the plain reference layout).
+ * scale/offset: [rows] f32; rowsum: [rows] i32 Σ codes (nullable);
+ * nonfinite_flag: device i32 set to 1 when any input is NaN/Inf (nullable). */
+QA_API int qa_quantize_rows(const void* w, int w_dtype, int64_t rows, int64_t cols, int64_t ld_w, int bits,
+                     uint8_t* codes, int64_t ld_codes, int64_t pad_cols, float* scale, float* offset,
+                     int32_t* rowsum, int32_t* nonfinite_flag, void* stream);
+
+/* dequantize_rows (quant.py:102-105): out = code·scale + offset evaluated in fp64,
+ * rounded to out_dtype (bit-exact with the reference for QA_F32).
+ * transpose != 0 writes outᵀ ([cols, rows], row stride ld_out). */
+QA_API int qa_dequantize_rows(const qa_qweight* w, void* out, int out_dtype, int64_t ld_out, int transpose, void* stream);
+
+/* Workspace for qa_linear_forward / qa_linear_backward at `tokens` tokens. */
+QA_API size_t qa_linear_workspace_bytes(const qa_qweight* w, const qa_tt* tt, int64_t tokens);
+
+/* Forward of the quantised adapter linear (LoraLinear.forward over
+ * QuantizedLinear, transformer.py:266-267 + 304-308; qmatmul, quant.py:123-132):
+ *   per-token 8-bit act-quant of x, int8 tcgen05 GEMM with exact int32 accumulators,
+ *   dequantising epilogue, + y2 = x · W_tᵀ (tt may be NULL: base only).
+ * x: [tokens, cols] (dtype x_dtype, row stride = cols).  y: [tokens, rows] bf16.
+ * Optional debug outputs (NULL to skip): acc_i32 [tokens, rows] raw Σ cx·cw,
+ * y_f32 [tokens, rows] the fp32 pre-rounding y, y2_f32 [tokens, rows] the adapter term. */
+QA_API int qa_linear_forward(const qa_qweight* w, const qa_tt* tt, const void* x, int x_dtype, int64_t tokens,
+                      void* y, int32_t* acc_i32, float* y_f32, float* y2_f32, void* workspace,
+                      size_t workspace_bytes, void* stream);
+
+/* Backward with recompute (LoraLinear.backward, transformer.py:310-318, with
+ * QuantizedLinear.backward -> qmatmul_t, quant.py:135-144): recomputes the TT partial
+ * contractions from the stored layer input x, writes dx = dy · deq(W) + dy · W_t
+ * (bf16, NULL to skip) and the adapter-core gradients dcores[k] (fp32, shapes as the
+ * cores; accumulate != 0 adds into them like _accumulate, transformer.py:150-156).
+ * dx_f32 (nullable) receives the fp32 pre-rounding dx. */
+QA_API int qa_linear_backward(const qa_qweight* w, const qa_tt* tt, const void* x, int x_dtype, const void* dy,
+                       int dy_dtype, int64_t tokens, void* dx, float* dx_f32, float* const* dcores,
+                       int accumulate, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Workspace for qa_merge / qa_tt_materialize. */
+QA_API size_t qa_merge_workspace_bytes(const qa_tt* tt);
+
+/* Merge (lowrank.py:245-257 via the explicit dequantise route lowrank.py:249-252):
+ * out = dequantize_rows(w) + W_t, [rows, cols] in out_dtype (fp64 dequantisation,
+ * fp32 W_t, rounded once to out_dtype). */
+QA_API int qa_merge(const qa_qweight* w, const qa_tt* tt, void* out, int out_dtype, void* workspace,
+             size_t workspace_bytes, void* stream);
+
+/* W_t alone ([N, K] fp32, N = Π m, K = Π n): the contraction of the cores. */
+QA_API int qa_tt_materialize(const qa_tt* tt, float* out, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Launch accounting (benchmark / profiling support, not on the reference's API).
+ * qa_launch_count(): kernels this library has launched since load (all classes).
+ * qa_timing_enable(1) resets and starts per-class CUDA-event timing of every launch on the
+ * launching stream; qa_timing_read() synchronises the recorded events and returns, for the
+ * named class ("gemm_i8", "gemm_bf16", "quantize", "tt", "dequant", "merge"), the summed
+ * device time, the launch count and the summed algorithmic work (int8 ops / flops for GEMMs,
+ * bytes for the memory-bound classes). */
+QA_API int64_t qa_launch_count(void);
+QA_API int qa_timing_enable(int on);
+QA_API int qa_timing_read(const char* kernel_class, double* total_ms, int64_t* launches, double* work);
+
+/* Plain bf16 tensor-core GEMM C[M, N] = A[M, K] · B[N, K]ᵀ (fp32 accumulate): the dense
+ * forward of a merged adapter (LoraLinear.forward merged path, transformer.py:305-306).
+ * Row strides in elements must give 16-byte aligned rows.  out_bf16 / out_f32 nullable. */
+QA_API int qa_gemm_bf16(const void* a, int64_t lda, const void* b, int64_t ldb, int64_t m, int64_t n, int64_t k,
+                        void* out_bf16, float* out_f32, int64_t ld_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QADAPTER_H */

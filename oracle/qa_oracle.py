@@ -39,6 +39,9 @@ __all__ = [
     "mse_grad",
     "dp_mean",
     "rel_err",
+    "tt_apply_staged",
+    "tt_backward_staged",
+    "qa_step_staged",
 ]
 
 
@@ -424,3 +427,60 @@ def rel_err(got, want) -> float:
     denom = np.abs(want) + rms
     denom = np.where(denom > 0, denom, 1.0)
     return float(np.max(np.abs(got - want) / denom))
+
+
+# ---------------------------------------------------------------------------
+# Staged (non-materialising) CPU port: the same left-to-right stage algebra the GPU runs.
+# Used as bench.py's CPU baseline (`cpu_baseline` / `--impl reference`) because materialising
+# W_t per call is not how a CPU implementation would run the layer; it is checked against the
+# materialising oracle above in tests/test_oracle_golden.py.
+# ---------------------------------------------------------------------------
+
+
+def tt_apply_staged(x, cores) -> np.ndarray:
+    x = np.asarray(x, dtype=np.float64)
+    t = x.shape[0]
+    z = x.reshape(t, 1, 1, -1)
+    for g in cores:
+        g = np.asarray(g, dtype=np.float64)
+        a, mk, nk, b = g.shape
+        i0 = z.shape[1]
+        z = z.reshape(t, i0, a, nk, -1)
+        z = np.einsum("tiajq,akjb->tikbq", z, g, optimize=True).reshape(t, i0 * mk, b, -1)
+    return z.reshape(t, -1)
+
+
+def tt_backward_staged(x, dy, cores):
+    """(dx_adapter, [dG_k]) by the right-to-left stage walk (the GPU's qa_linear_backward order)."""
+    x = np.asarray(x, dtype=np.float64)
+    t = x.shape[0]
+    cs = [np.asarray(g, dtype=np.float64) for g in cores]
+    zs = [x.reshape(t, 1, 1, -1)]
+    for g in cs[:-1]:
+        a, mk, nk, b = g.shape
+        z = zs[-1]
+        i0 = z.shape[1]
+        zs.append(np.einsum("tiajq,akjb->tikbq", z.reshape(t, i0, a, nk, -1), g, optimize=True)
+                  .reshape(t, i0 * mk, b, -1))
+    cur = np.asarray(dy, dtype=np.float64)
+    grads = [None] * len(cs)
+    for k in range(len(cs) - 1, -1, -1):
+        g = cs[k]
+        a, mk, nk, b = g.shape
+        zin = zs[k]
+        i0 = zin.shape[1]
+        zin5 = zin.reshape(t, i0, a, nk, -1)
+        dout5 = cur.reshape(t, i0, mk, b, -1)
+        grads[k] = np.einsum("tiajq,tikbq->akjb", zin5, dout5, optimize=True)
+        cur = np.einsum("tikbq,akjb->tiajq", dout5, g, optimize=True).reshape(t, -1)
+    return cur.reshape(t, -1), grads
+
+
+def qa_step_staged(x, dy, qw: OQuant, cores) -> dict:
+    """One forward + backward of the quantised adapter linear on the CPU, staged (no W_t)."""
+    x2 = np.asarray(x, dtype=np.float64).reshape(-1, qw.cols)
+    qx = quantize_rows(x2, 8)
+    y = qmatmul(qw, dequantize_rows(qx)) + tt_apply_staged(x2, cores)
+    dxa, grads = tt_backward_staged(x2, dy, cores)
+    dx = qmatmul_t(qw, dy) + dxa
+    return {"y": y, "dx": dx, "dcores": grads}

@@ -1,0 +1,477 @@
+// extern "C" boundary: argument validation, workspace planning and kernel orchestration.
+// See include/qadapter.h for the contract and the reference interfaces each entry replaces.
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+
+#include "qa_internal.h"
+
+namespace qa {
+
+namespace {
+thread_local char g_err[512] = "";
+}
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int cuda_status(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return QA_OK;
+  set_error("%s: %s", what, cudaGetErrorString(e));
+  return QA_ERR_CUDA;
+}
+
+namespace {
+
+constexpr int kMaxRank = 64;
+
+int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+
+// Bump allocator over the caller's workspace (256-byte aligned slices).
+struct Bump {
+  char* base;
+  size_t off = 0;
+  explicit Bump(void* b) : base(static_cast<char*>(b)) {}
+  template <typename T>
+  T* take(int64_t count) {
+    off = (off + 255) & ~size_t(255);
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += static_cast<size_t>(std::max<int64_t>(count, 0)) * sizeof(T);
+    return p;
+  }
+};
+
+struct LinearPlan {
+  int64_t T = 0, N = 0, K = 0, Kp = 0, Np = 0;
+  bool need_wcodes = false, need_dypad = false;
+  uint8_t* xcodes = nullptr;
+  float* sx = nullptr;
+  float* ox = nullptr;
+  int32_t* rsx = nullptr;
+  uint8_t* wcodes = nullptr;
+  float* z[QA_TT_MAX_D + 1] = {};  // Z_1..Z_{d-1}
+  float* y2 = nullptr;             // [T, N]
+  float* dz[2] = {};               // ping-pong dZ buffers (max Z size)
+  float* dxad = nullptr;           // [T, K]
+  float* partial = nullptr;
+  int nchunks = 1;
+  __nv_bfloat16* wdt = nullptr;   // deq(W)ᵀ [K, Np]
+  __nv_bfloat16* dyb = nullptr;   // dy padded [T, Np]
+  __nv_bfloat16* wdt_lo = nullptr;  // fp32-input path: bf16 residuals of deq(W)ᵀ and dy
+  __nv_bfloat16* dyb_lo = nullptr;
+  float* dxacc = nullptr;           // fp32-input path: partial dx [T, K]
+  size_t bytes = 0;
+};
+
+bool plan_linear(const qa_qweight* w, const TTDims* dd, int64_t T, void* ws, LinearPlan* P, bool f32_path) {
+  P->T = T;
+  P->N = w->rows;
+  P->K = w->cols;
+  P->Kp = round_up(P->K, 16);
+  P->Np = round_up(P->N, 8);
+  P->need_wcodes = w->bits == 4 || P->Kp != P->K;
+  Bump b(ws);
+  P->xcodes = b.take<uint8_t>(T * P->Kp);
+  P->sx = b.take<float>(T);
+  P->ox = b.take<float>(T);
+  P->rsx = b.take<int32_t>(T);
+  if (P->need_wcodes) P->wcodes = b.take<uint8_t>(P->N * P->Kp);
+  if (dd != nullptr) {
+    int64_t zmax = 0;
+    for (int k = 1; k < dd->d; ++k) {
+      P->z[k] = b.take<float>(T * dd->zsize[k]);
+      zmax = std::max(zmax, dd->zsize[k]);
+    }
+    P->y2 = b.take<float>(T * P->N);
+    P->dz[0] = b.take<float>(T * zmax);
+    P->dz[1] = b.take<float>(T * zmax);
+    P->dxad = b.take<float>(T * P->K);
+    int64_t gmax = 0;
+    for (int k = 0; k < dd->d; ++k) gmax = std::max(gmax, dd->core_numel(k));
+    P->nchunks = tt_grad_chunks(T);
+    P->partial = b.take<float>(gmax * P->nchunks);
+  }
+  P->wdt = b.take<__nv_bfloat16>(P->K * P->Np);
+  P->dyb = b.take<__nv_bfloat16>(T * P->Np);
+  if (f32_path) {
+    P->wdt_lo = b.take<__nv_bfloat16>(P->K * P->Np);
+    P->dyb_lo = b.take<__nv_bfloat16>(T * P->Np);
+    P->dxacc = b.take<float>(T * P->K);
+  }
+  P->bytes = b.off + 256;
+  return true;
+}
+
+int check_weight(const qa_qweight* w) {
+  if (w == nullptr || w->codes == nullptr || w->scale == nullptr || w->offset == nullptr) {
+    set_error("qa_qweight: null pointer");
+    return QA_ERR_ARG;
+  }
+  if (w->bits != 4 && w->bits != 8) {
+    set_error("bits must be 4 or 8, got %d", w->bits);
+    return QA_ERR_BITS;
+  }
+  if (w->rows < 1 || w->cols < 1) {
+    set_error("weight grid must be non-empty, got %lldx%lld", (long long)w->rows, (long long)w->cols);
+    return QA_ERR_ARG;
+  }
+  return QA_OK;
+}
+
+int check_tt(const qa_tt* tt, const qa_qweight* w, TTDims* dd) {
+  if (!tt_dims(tt, dd)) {
+    set_error("invalid TT adapter descriptor (d in [1,%d], r[0]=r[d]=1, positive modes, non-null cores)",
+              QA_TT_MAX_D);
+    return QA_ERR_ARG;
+  }
+  for (int k = 0; k <= dd->d; ++k)
+    if (dd->r[k] > kMaxRank) {
+      set_error("TT rank %d exceeds the supported maximum %d", dd->r[k], kMaxRank);
+      return QA_ERR_UNSUPPORTED;
+    }
+  if (w != nullptr && (dd->N != w->rows || dd->K != w->cols)) {
+    set_error("TT modes give %lldx%lld but the base weight is %lldx%lld", (long long)dd->N, (long long)dd->K,
+              (long long)w->rows, (long long)w->cols);
+    return QA_ERR_ARG;
+  }
+  return QA_OK;
+}
+
+#define QA_TRY_CUDA(expr, what)                         \
+  do {                                                  \
+    cudaError_t _e = (expr);                            \
+    if (_e != cudaSuccess) return cuda_status(_e, what); \
+  } while (0)
+#define QA_TRY(expr)            \
+  do {                          \
+    int _s = (expr);            \
+    if (_s != QA_OK) return _s; \
+  } while (0)
+
+// B-operand codes for the int8 GEMM: the reference layout directly when it already is a
+// 16-byte-strided u8 grid, else an unpacked / padded copy in the workspace.
+const uint8_t* weight_operand(const qa_qweight* w, const LinearPlan& P, cudaStream_t s, int* status) {
+  *status = QA_OK;
+  if (!P.need_wcodes) return w->codes;
+  cudaError_t e = launch_unpack_pad(w->codes, w->rows, w->cols, w->bits, P.wcodes, P.Kp, s);
+  if (e != cudaSuccess) *status = cuda_status(e, "unpack_pad");
+  return P.wcodes;
+}
+
+}  // namespace
+}  // namespace qa
+
+using namespace qa;
+
+extern "C" {
+
+const char* qa_version(void) { return "qadapter 0.1 (sm_100a tcgen05)"; }
+
+const char* qa_last_error(void) { return g_err; }
+
+int qa_quantize_rows(const void* w, int w_dtype, int64_t rows, int64_t cols, int64_t ld_w, int bits,
+                     uint8_t* codes, int64_t ld_codes, int64_t pad_cols, float* scale, float* offset,
+                     int32_t* rowsum, int32_t* nonfinite_flag, void* stream) {
+  if (bits != 4 && bits != 8) {
+    set_error("bits must be 4 or 8, got %d", bits);
+    return QA_ERR_BITS;
+  }
+  if (w == nullptr || codes == nullptr || scale == nullptr || offset == nullptr || rows < 0 || cols < 1 ||
+      ld_w < cols || (w_dtype != QA_F32 && w_dtype != QA_BF16)) {
+    set_error("qa_quantize_rows: bad argument");
+    return QA_ERR_ARG;
+  }
+  const int64_t min_ld = bits == 8 ? std::max(cols, pad_cols) : (cols + 1) / 2;
+  if (ld_codes < min_ld || (bits == 4 && pad_cols > cols)) {
+    set_error("qa_quantize_rows: code row stride %lld too small", (long long)ld_codes);
+    return QA_ERR_ARG;
+  }
+  return cuda_status(launch_quantize_rows(w, w_dtype, rows, cols, ld_w, bits, codes, ld_codes, std::max(pad_cols, cols),
+                                          scale, offset, rowsum, nonfinite_flag, static_cast<cudaStream_t>(stream)),
+                     "quantize_rows");
+}
+
+int qa_dequantize_rows(const qa_qweight* w, void* out, int out_dtype, int64_t ld_out, int transpose, void* stream) {
+  QA_TRY(check_weight(w));
+  if (out == nullptr || (out_dtype != QA_F32 && out_dtype != QA_BF16) ||
+      ld_out < (transpose ? w->rows : w->cols)) {
+    set_error("qa_dequantize_rows: bad output");
+    return QA_ERR_ARG;
+  }
+  return cuda_status(launch_dequantize(w->codes, w->scale, w->offset, w->rows, w->cols, w->bits, out, out_dtype,
+                                       ld_out, transpose != 0, static_cast<cudaStream_t>(stream)),
+                     "dequantize");
+}
+
+size_t qa_linear_workspace_bytes(const qa_qweight* w, const qa_tt* tt, int64_t tokens) {
+  if (check_weight(w) != QA_OK) return 0;
+  TTDims dd;
+  const TTDims* pd = nullptr;
+  if (tt != nullptr) {
+    if (check_tt(tt, w, &dd) != QA_OK) return 0;
+    pd = &dd;
+  }
+  LinearPlan P;
+  plan_linear(w, pd, tokens, nullptr, &P, true);  // large enough for the fp32-input backward too
+  return P.bytes;
+}
+
+int qa_linear_forward(const qa_qweight* w, const qa_tt* tt, const void* x, int x_dtype, int64_t tokens,
+                      void* y, int32_t* acc_i32, float* y_f32, float* y2_f32, void* workspace,
+                      size_t workspace_bytes, void* stream) {
+  QA_TRY(check_weight(w));
+  if (x == nullptr || tokens < 0 || (x_dtype != QA_F32 && x_dtype != QA_BF16) || w->rowsum == nullptr) {
+    set_error("qa_linear_forward: bad argument (x, dtype, tokens or weight rowsum)");
+    return QA_ERR_ARG;
+  }
+  if (tokens == 0) return QA_OK;
+  TTDims dd;
+  const TTDims* pd = nullptr;
+  if (tt != nullptr) {
+    QA_TRY(check_tt(tt, w, &dd));
+    pd = &dd;
+  }
+  LinearPlan P;
+  plan_linear(w, pd, tokens, nullptr, &P, false);
+  if (workspace == nullptr || workspace_bytes < P.bytes) {
+    set_error("workspace too small: need %zu bytes", P.bytes);
+    return QA_ERR_WORKSPACE;
+  }
+  plan_linear(w, pd, tokens, workspace, &P, false);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t T = tokens, N = P.N, K = P.K;
+
+  // (2) per-token activation quantisation: quantize_rows on x[T, K] (codes padded to Kp with zeros)
+  QA_TRY_CUDA(launch_quantize_rows(x, x_dtype, T, K, K, 8, P.xcodes, P.Kp, P.Kp, P.sx, P.ox, P.rsx, nullptr, s),
+              "act quantize");
+  int st = QA_OK;
+  const uint8_t* wop = weight_operand(w, P, s, &st);
+  QA_TRY(st);
+
+  // (4) TT adapter y2 = x · W_tᵀ via the left-to-right stage chain
+  float* y2 = nullptr;
+  if (pd != nullptr) {
+    y2 = y2_f32 != nullptr ? y2_f32 : P.y2;
+    const void* zin = x;
+    int zin_dtype = x_dtype;
+    int64_t zin_ld = K;
+    for (int k = 0; k < dd.d; ++k) {
+      float* zout = (k == dd.d - 1) ? y2 : P.z[k + 1];
+      QA_TRY_CUDA(launch_tt_stage_fwd(zin, zin_dtype, zin_ld, tt->cores[k], zout, dd.zsize[k + 1], T, dd.I(k),
+                                      dd.r[k], dd.n[k], dd.J(k + 1), dd.m[k], dd.r[k + 1], s),
+                  "tt stage fwd");
+      zin = zout;
+      zin_dtype = QA_F32;
+      zin_ld = dd.zsize[k + 1];
+    }
+  }
+
+  // (3) int8 tcgen05 GEMM with the dequantising epilogue (+ y2)
+  GemmEpilogue e;
+  e.row_scale = P.sx;
+  e.row_offset = P.ox;
+  e.row_sum = P.rsx;
+  e.col_scale = w->scale;
+  e.col_offset = w->offset;
+  e.col_sum = w->rowsum;
+  e.zp_row = 128;
+  e.zp_col = w->bits == 8 ? 128 : 8;
+  e.k_real = static_cast<int>(K);
+  e.addend = y2;
+  e.ld_add = N;
+  e.out_bf16 = static_cast<__nv_bfloat16*>(y);
+  e.ld_out = N;
+  e.out_f32 = y_f32;
+  e.ld_f32 = N;
+  e.out_acc = acc_i32;
+  e.ld_acc = N;
+  return gemm_tc(0, P.xcodes, P.Kp, wop, P.Kp, T, N, P.Kp, e, s);
+}
+
+int qa_linear_backward(const qa_qweight* w, const qa_tt* tt, const void* x, int x_dtype, const void* dy,
+                       int dy_dtype, int64_t tokens, void* dx, float* dx_f32, float* const* dcores,
+                       int accumulate, void* workspace, size_t workspace_bytes, void* stream) {
+  QA_TRY(check_weight(w));
+  if (dy == nullptr || tokens < 0 || (x_dtype != QA_F32 && x_dtype != QA_BF16) ||
+      (dy_dtype != QA_F32 && dy_dtype != QA_BF16)) {
+    set_error("qa_linear_backward: bad argument");
+    return QA_ERR_ARG;
+  }
+  if (tokens == 0) return QA_OK;
+  TTDims dd;
+  const TTDims* pd = nullptr;
+  if (tt != nullptr) {
+    QA_TRY(check_tt(tt, w, &dd));
+    pd = &dd;
+    if (x == nullptr) {
+      set_error("qa_linear_backward: the adapter backward needs the stored layer input x");
+      return QA_ERR_ARG;
+    }
+  }
+  const bool f32_path = dy_dtype == QA_F32;
+  LinearPlan P;
+  plan_linear(w, pd, tokens, nullptr, &P, f32_path);
+  if (workspace == nullptr || workspace_bytes < P.bytes) {
+    set_error("workspace too small: need %zu bytes", P.bytes);
+    return QA_ERR_WORKSPACE;
+  }
+  plan_linear(w, pd, tokens, workspace, &P, f32_path);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t T = tokens, N = P.N, K = P.K;
+  const bool want_dx = dx != nullptr || dx_f32 != nullptr;
+
+  float* dxad = nullptr;
+  if (pd != nullptr) {
+    // (5) recompute Z_1..Z_{d-1} from the stored layer input
+    for (int k = 0; k + 1 < dd.d; ++k) {
+      const void* zin = k == 0 ? x : static_cast<const void*>(P.z[k]);
+      QA_TRY_CUDA(launch_tt_stage_fwd(zin, k == 0 ? x_dtype : QA_F32, k == 0 ? K : dd.zsize[k], tt->cores[k],
+                                      P.z[k + 1], dd.zsize[k + 1], T, dd.I(k), dd.r[k], dd.n[k], dd.J(k + 1),
+                                      dd.m[k], dd.r[k + 1], s),
+                  "tt recompute");
+    }
+    // walk the stages right to left: dG_k from (Z_k, dZ_{k+1}); dZ_k = stage_bwd(dZ_{k+1})
+    const void* cur = dy;
+    int cur_dtype = dy_dtype;
+    int64_t cur_ld = N;
+    for (int k = dd.d - 1; k >= 0; --k) {
+      const void* zin = k == 0 ? x : static_cast<const void*>(P.z[k]);
+      const int zin_dtype = k == 0 ? x_dtype : QA_F32;
+      const int64_t zin_ld = k == 0 ? K : dd.zsize[k];
+      if (dcores != nullptr && dcores[k] != nullptr) {
+        QA_TRY_CUDA(launch_tt_core_grad(zin, zin_dtype, zin_ld, cur, cur_dtype, cur_ld, P.partial, P.nchunks,
+                                        dcores[k], accumulate != 0, T, dd.I(k), dd.r[k], dd.n[k], dd.J(k + 1),
+                                        dd.m[k], dd.r[k + 1], s),
+                    "tt core grad");
+      }
+      if (k == 0 && !want_dx) break;
+      float* next = k == 0 ? P.dxad : P.dz[k & 1];
+      QA_TRY_CUDA(launch_tt_stage_bwd(cur, cur_dtype, cur_ld, tt->cores[k], next, dd.zsize[k], T, dd.I(k), dd.r[k],
+                                      dd.n[k], dd.J(k + 1), dd.m[k], dd.r[k + 1], s),
+                  "tt stage bwd");
+      cur = next;
+      cur_dtype = QA_F32;
+      cur_ld = dd.zsize[k];
+    }
+    if (want_dx) dxad = P.dxad;
+  }
+
+  if (want_dx) {
+    // dx = dy · deq(W): transient bf16 deq(W)ᵀ [K, Np] + tcgen05 bf16 GEMM (+ adapter dx).
+    // bf16 dy: one GEMM (deq(W) rounded once to bf16).  fp32 dy: 3xbf16 split
+    // (dy_hi·W_hi + dy_hi·W_lo + dy_lo·W_hi) so fp32 callers keep ~2^-16 relative accuracy.
+    if (P.Np != N) {
+      QA_TRY_CUDA(cudaMemsetAsync(P.wdt, 0, sizeof(__nv_bfloat16) * K * P.Np, s), "memset wdt");
+      if (f32_path) QA_TRY_CUDA(cudaMemsetAsync(P.wdt_lo, 0, sizeof(__nv_bfloat16) * K * P.Np, s), "memset wdt_lo");
+    }
+    QA_TRY_CUDA(launch_dequantize(w->codes, w->scale, w->offset, N, K, w->bits, P.wdt, QA_BF16, P.Np, true, s,
+                                  f32_path ? P.wdt_lo : nullptr),
+                "dequantize T");
+    const void* a = dy;
+    int64_t lda = N;
+    if (f32_path || P.Np != N || reinterpret_cast<uintptr_t>(dy) % 16 != 0) {
+      QA_TRY_CUDA(launch_to_bf16_pad(dy, dy_dtype, T, N, P.dyb, P.Np, s, f32_path ? P.dyb_lo : nullptr),
+                  "dy to bf16");
+      a = P.dyb;
+      lda = P.Np;
+    }
+    const float* addend = dxad;
+    if (f32_path) {
+      GemmEpilogue e1;
+      e1.addend = dxad;
+      e1.ld_add = K;
+      e1.out_f32 = P.dxacc;
+      e1.ld_f32 = K;
+      QA_TRY(gemm_tc(1, P.dyb_lo, P.Np, P.wdt, P.Np, T, K, P.Np, e1, s));
+      GemmEpilogue e2;
+      e2.addend = P.dxacc;
+      e2.ld_add = K;
+      e2.out_f32 = P.dxacc;
+      e2.ld_f32 = K;
+      QA_TRY(gemm_tc(1, P.dyb, P.Np, P.wdt_lo, P.Np, T, K, P.Np, e2, s));
+      addend = P.dxacc;
+    }
+    GemmEpilogue e;
+    e.addend = addend;
+    e.ld_add = K;
+    e.out_bf16 = static_cast<__nv_bfloat16*>(dx);
+    e.ld_out = K;
+    e.out_f32 = dx_f32;
+    e.ld_f32 = K;
+    QA_TRY(gemm_tc(1, a, lda, P.wdt, P.Np, T, K, P.Np, e, s));
+  }
+  return QA_OK;
+}
+
+size_t qa_merge_workspace_bytes(const qa_tt* tt) {
+  TTDims dd;
+  if (check_tt(tt, nullptr, &dd) != QA_OK) return 0;
+  int64_t IP = 1, JP = 1;
+  for (int k = 0; k + 1 < dd.d; ++k) {
+    IP *= dd.m[k];
+    JP *= dd.n[k];
+  }
+  return static_cast<size_t>(IP * JP * dd.r[dd.d - 1]) * sizeof(float) + 256;
+}
+
+int qa_merge(const qa_qweight* w, const qa_tt* tt, void* out, int out_dtype, void* workspace,
+             size_t workspace_bytes, void* stream) {
+  QA_TRY(check_weight(w));
+  TTDims dd;
+  QA_TRY(check_tt(tt, w, &dd));
+  if (out == nullptr || (out_dtype != QA_F32 && out_dtype != QA_BF16)) {
+    set_error("qa_merge: bad output");
+    return QA_ERR_ARG;
+  }
+  if (workspace == nullptr || workspace_bytes < qa_merge_workspace_bytes(tt)) {
+    set_error("workspace too small: need %zu bytes", qa_merge_workspace_bytes(tt));
+    return QA_ERR_WORKSPACE;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  float* L = static_cast<float*>(workspace);
+  QA_TRY_CUDA(launch_tt_prefix_full(dd, tt->cores, L, s), "tt prefix");
+  return cuda_status(launch_tt_last_full(dd, L, tt->cores[dd.d - 1], w->codes, w->bits, w->scale, w->offset, out,
+                                         out_dtype, s),
+                     "merge");
+}
+
+int qa_tt_materialize(const qa_tt* tt, float* out, void* workspace, size_t workspace_bytes, void* stream) {
+  TTDims dd;
+  QA_TRY(check_tt(tt, nullptr, &dd));
+  if (out == nullptr) {
+    set_error("qa_tt_materialize: null output");
+    return QA_ERR_ARG;
+  }
+  if (workspace == nullptr || workspace_bytes < qa_merge_workspace_bytes(tt)) {
+    set_error("workspace too small: need %zu bytes", qa_merge_workspace_bytes(tt));
+    return QA_ERR_WORKSPACE;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  float* L = static_cast<float*>(workspace);
+  QA_TRY_CUDA(launch_tt_prefix_full(dd, tt->cores, L, s), "tt prefix");
+  return cuda_status(launch_tt_last_full(dd, L, tt->cores[dd.d - 1], nullptr, 8, nullptr, nullptr, out, QA_F32, s),
+                     "tt materialize");
+}
+
+int qa_gemm_bf16(const void* a, int64_t lda, const void* b, int64_t ldb, int64_t m, int64_t n, int64_t k,
+                 void* out_bf16, float* out_f32, int64_t ld_out, void* stream) {
+  if (a == nullptr || b == nullptr || m < 0 || n < 0 || k < 1 || lda < k || ldb < k || ld_out < n ||
+      (out_bf16 == nullptr && out_f32 == nullptr)) {
+    set_error("qa_gemm_bf16: bad argument");
+    return QA_ERR_ARG;
+  }
+  GemmEpilogue e;
+  e.out_bf16 = static_cast<__nv_bfloat16*>(out_bf16);
+  e.ld_out = ld_out;
+  e.out_f32 = out_f32;
+  e.ld_f32 = ld_out;
+  return gemm_tc(1, a, lda, b, ldb, m, n, k, e, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,295 @@
+// tcgen05 tensor-core GEMM for the quantised adapter linear (sm_100a).
+//
+//   kind 0 (forward, qmatmul quant.py:123-132 with per-token act-quant):
+//       acc[t, n] = Σ_k cx[t, k] · cw[n, k]   u8 x u8 -> exact s32 in TMEM (tcgen05.mma kind::i8)
+//       epilogue: centred dequantisation (SURVEY §7 "epilogue cancellation"):
+//         acc_c = acc - zw·Σcx - zx·Σcw + zx·zw·K       (exact int32)
+//         y     = sx·(sw·acc_c + õw·Σc̃x) + õx·(sw·Σc̃w + K·õw) (+ addend),  õ = offset + z·scale
+//   kind 1 (backward dX, qmatmul_t quant.py:135-144):
+//       dx[t, k] = Σ_n dy[t, n] · deq(W)ᵀ[k, n]   bf16 x bf16 -> f32 in TMEM (kind::f16) (+ addend)
+//
+// Structure: one 128 x 256 output tile per CTA, 4-stage TMA -> shared-memory ring (128-byte
+// swizzled K-major tiles), warp 0 = TMA producer, warp 1 = single-thread MMA issuer,
+// warp 2 = TMEM allocator, warps 4..7 = epilogue (TMEM lane quarter = warp % 4).
+#include <mutex>
+
+#include "qa_common.cuh"
+#include "qa_internal.h"
+#include "qa_timing.h"
+
+namespace qa {
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BN = 256;
+constexpr int BK_BYTES = 128;  // one 128-byte swizzle atom along K per stage
+constexpr int STAGES = 4;
+constexpr int A_BYTES = BM * BK_BYTES;
+constexpr int B_BYTES = BN * BK_BYTES;
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int TMEM_COLS = 256;
+constexpr int THREADS = 256;
+constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 4 * BN * 4 /*column terms*/ + 256;
+
+struct KParams {
+  int64_t M, N, K;  // K in elements
+  GemmEpilogue e;
+};
+
+template <int KIND>
+__global__ void __launch_bounds__(THREADS, 1)
+    k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const KParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_BYTES;
+  float* colA = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES);  // sw
+  float* colB = colA + BN;                                              // õw
+  float* colC = colB + BN;                                              // sw·Σc̃w + K·õw
+  int32_t* colD = reinterpret_cast<int32_t*>(colC + BN);                // zx·Σcw
+  uint64_t* full = reinterpret_cast<uint64_t*>(colD + BN);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tmem_full = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const uint32_t warp = warp_id_sync();
+  const uint32_t lane = lane_id();
+  const int64_t m0 = static_cast<int64_t>(blockIdx.y) * BM;
+  const int64_t n0 = static_cast<int64_t>(blockIdx.x) * BN;
+  constexpr int ELEM_BYTES = KIND == 0 ? 1 : 2;
+  constexpr int BK = BK_BYTES / ELEM_BYTES;
+  const int num_kb = static_cast<int>((p.K + BK - 1) / BK);
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      for (int kb = 0; kb < num_kb; ++kb) {
+        const int s = kb % STAGES;
+        const uint32_t ph = (kb / STAGES) & 1;
+        mbar_wait(&empty[s], ph ^ 1);
+        mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+        tma_load_2d(sA + s * A_BYTES, &tmA, &full[s], kb * BK, static_cast<int32_t>(m0));
+        tma_load_2d(sB + s * B_BYTES, &tmB, &full[s], kb * BK, static_cast<int32_t>(n0));
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (one thread)
+    if (lane == 0) {
+      constexpr uint32_t idesc = KIND == 0 ? make_idesc(/*S32*/ 2, /*u8*/ 0, /*u8*/ 0, BM, BN)
+                                           : make_idesc(/*F32*/ 1, /*bf16*/ 1, /*bf16*/ 1, BM, BN);
+      for (int kb = 0; kb < num_kb; ++kb) {
+        const int s = kb % STAGES;
+        const uint32_t ph = (kb / STAGES) & 1;
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        const uint64_t a0 = smem_desc_kmajor_sw128(sA + s * A_BYTES);
+        const uint64_t b0 = smem_desc_kmajor_sw128(sB + s * B_BYTES);
+#pragma unroll
+        for (int k = 0; k < BK_BYTES / 32; ++k) {  // 32 bytes of K per MMA (32 x i8 or 16 x bf16)
+          const uint64_t adv = static_cast<uint64_t>((k * 32) >> 4);
+          if (KIND == 0)
+            mma_i8(tmem_base, a0 + adv, b0 + adv, idesc, (kb | k) != 0);
+          else
+            mma_f16(tmem_base, a0 + adv, b0 + adv, idesc, (kb | k) != 0);
+        }
+        mma_commit(&empty[s]);  // slot reusable once these MMAs have read it
+      }
+      mma_commit(tmem_full);  // accumulator complete
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue
+    const int et = static_cast<int>(threadIdx.x) - 128;  // 0..127
+    const GemmEpilogue& e = p.e;
+    if (KIND == 0) {
+      const float kf = static_cast<float>(e.k_real);
+      for (int c = et; c < BN; c += 128) {
+        const int64_t n = n0 + c;
+        if (n < p.N) {
+          const float sw = e.col_scale[n];
+          const float ow = e.col_offset[n] + static_cast<float>(e.zp_col) * sw;
+          const int32_t rs = e.col_sum[n];
+          const float rsc = static_cast<float>(rs - e.zp_col * e.k_real);
+          colA[c] = sw;
+          colB[c] = ow;
+          colC[c] = fmaf(sw, rsc, kf * ow);
+          colD[c] = e.zp_row * rs;
+        } else {
+          colA[c] = 0.f;
+          colB[c] = 0.f;
+          colC[c] = 0.f;
+          colD[c] = 0;
+        }
+      }
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+
+    const uint32_t quarter = warp & 3u;
+    const int64_t row = m0 + quarter * 32 + lane;
+    const bool row_ok = row < p.M;
+    float sx = 0.f, ox = 0.f, rsxc = 0.f;
+    int32_t ibase = 0;
+    if (KIND == 0 && row_ok) {
+      sx = e.row_scale[row];
+      ox = e.row_offset[row] + static_cast<float>(e.zp_row) * sx;
+      const int32_t rsx = e.row_sum[row];
+      rsxc = static_cast<float>(rsx - e.zp_row * e.k_real);
+      ibase = e.zp_row * e.zp_col * e.k_real - e.zp_col * rsx;
+    }
+
+    mbar_wait(tmem_full, 0);
+    tc_fence_after();
+
+    const bool vec_out = e.out_bf16 != nullptr && (e.ld_out % 8 == 0) &&
+                         (reinterpret_cast<uintptr_t>(e.out_bf16) % 16 == 0);
+#pragma unroll 1
+    for (int chunk = 0; chunk < BN / 32; ++chunk) {
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(tmem_base + ((quarter * 32u) << 16) + chunk * 32u, v);
+      tmem_ld_wait();
+      const int64_t nb = n0 + chunk * 32;
+      if (!row_ok || nb >= p.N) continue;
+      float y[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if (KIND == 0) {
+          const int c = chunk * 32 + j;
+          const int32_t accc = static_cast<int32_t>(v[j]) + ibase - colD[c];
+          y[j] = fmaf(sx, fmaf(colA[c], static_cast<float>(accc), colB[c] * rsxc), ox * colC[c]);
+        } else {
+          y[j] = __uint_as_float(v[j]);
+        }
+      }
+      const int ncols = static_cast<int>(p.N - nb < 32 ? p.N - nb : 32);
+      if (e.addend != nullptr) {
+        const float* ad = e.addend + row * e.ld_add + nb;
+        for (int j = 0; j < ncols; ++j) y[j] += ad[j];
+      }
+      if (KIND == 0 && e.out_acc != nullptr) {
+        int32_t* dst = e.out_acc + row * e.ld_acc + nb;
+        for (int j = 0; j < ncols; ++j) dst[j] = static_cast<int32_t>(v[j]);
+      }
+      if (e.out_f32 != nullptr) {
+        float* dst = e.out_f32 + row * e.ld_f32 + nb;
+        for (int j = 0; j < ncols; ++j) dst[j] = y[j];
+      }
+      if (e.out_bf16 != nullptr) {
+        __nv_bfloat16* dst = e.out_bf16 + row * e.ld_out + nb;
+        if (vec_out && ncols == 32) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint4 pk;
+            uint32_t* w = reinterpret_cast<uint32_t*>(&pk);
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+              const __nv_bfloat162 b2 = __floats2bfloat162_rn(y[q * 8 + 2 * h], y[q * 8 + 2 * h + 1]);
+              w[h] = *reinterpret_cast<const uint32_t*>(&b2);
+            }
+            *reinterpret_cast<uint4*>(dst + q * 8) = pk;
+          }
+        } else {
+          for (int j = 0; j < ncols; ++j) dst[j] = __float2bfloat16_rn(y[j]);
+        }
+      }
+    }
+    tc_fence_before();
+  }
+
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<TMEM_COLS>(tmem_base);
+  }
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  });
+  return fn;
+}
+
+// Row-major [rows, cols] operand with row stride ld (elements), box = box_rows x 128 bytes, 128B swizzle.
+bool make_tmap(CUtensorMap* m, const void* base, int elem_bytes, int64_t rows, int64_t cols, int64_t ld,
+               int box_rows) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (enc == nullptr) return false;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * elem_bytes)};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(BK_BYTES / elem_bytes), static_cast<cuuint32_t>(box_rows)};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUtensorMapDataType dt = elem_bytes == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  return enc(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int KIND>
+int launch(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
+           const GemmEpilogue& epi, cudaStream_t s) {
+  constexpr int eb = KIND == 0 ? 1 : 2;
+  CUtensorMap ta, tb;
+  if (!make_tmap(&ta, A, eb, M, K, lda, BM) || !make_tmap(&tb, B, eb, N, K, ldb, BN)) {
+    set_error("cuTensorMapEncodeTiled failed (M=%lld N=%lld K=%lld lda=%lld ldb=%lld)", (long long)M, (long long)N,
+              (long long)K, (long long)lda, (long long)ldb);
+    return QA_ERR_CUDA;
+  }
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_gemm_tc<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(gemm)");
+    attr_set = true;
+  }
+  KParams p;
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.e = epi;
+  const dim3 grid(static_cast<unsigned>((N + BN - 1) / BN), static_cast<unsigned>((M + BM - 1) / BM));
+  const double kalg = KIND == 0 && epi.k_real > 0 ? double(epi.k_real) : double(K);
+  LaunchScope scope(KIND == 0 ? kGemmI8 : kGemmBF16, 2.0 * double(M) * double(N) * kalg, s);
+  count_launches(1);
+  k_gemm_tc<KIND><<<grid, THREADS, SMEM_BYTES, s>>>(ta, tb, p);
+  return cuda_status(cudaGetLastError(), "k_gemm_tc launch");
+}
+
+}  // namespace
+
+int gemm_tc(int kind, const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
+            const GemmEpilogue& epi, cudaStream_t s) {
+  if (M == 0 || N == 0) return QA_OK;
+  const int eb = kind == 0 ? 1 : 2;
+  if ((lda * eb) % 16 || (ldb * eb) % 16 || reinterpret_cast<uintptr_t>(A) % 16 || reinterpret_cast<uintptr_t>(B) % 16) {
+    set_error("gemm_tc: operands must be 16-byte aligned with 16-byte row strides");
+    return QA_ERR_UNSUPPORTED;
+  }
+  return kind == 0 ? launch<0>(A, lda, B, ldb, M, N, K, epi, s) : launch<1>(A, lda, B, ldb, M, N, K, epi, s);
+}
+
+}  // namespace qa

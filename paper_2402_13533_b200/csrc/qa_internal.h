@@ -1,0 +1,90 @@
+// Internal launcher declarations shared by the kernel translation units and the C ABI.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include "../../include/qadapter.h"
+
+namespace qa {
+
+void set_error(const char* fmt, ...);
+int cuda_status(cudaError_t e, const char* what);
+
+// ------------------------------------------------------------ quantisation
+cudaError_t launch_quantize_rows(const void* w, int w_dtype, int64_t rows, int64_t cols, int64_t ld_w, int bits,
+                                 uint8_t* codes, int64_t ld_codes, int64_t pad_cols, float* scale, float* offset,
+                                 int32_t* rowsum, int32_t* flag, cudaStream_t s);
+cudaError_t launch_dequantize(const uint8_t* codes, const float* scale, const float* offset, int64_t rows,
+                              int64_t cols, int bits, void* out, int out_dtype, int64_t ld_out, bool transpose,
+                              cudaStream_t s, __nv_bfloat16* out_lo = nullptr);
+// 4-bit packed / unpadded codes -> u8 codes [rows, ld_out] with zero padding in [cols, ld_out).
+cudaError_t launch_unpack_pad(const uint8_t* codes, int64_t rows, int64_t cols, int bits, uint8_t* out,
+                              int64_t ld_out, cudaStream_t s);
+// f32 / bf16 [rows, cols] -> bf16 [rows, ld_out] zero padded; out_lo (nullable) = bf16(v - hi).
+cudaError_t launch_to_bf16_pad(const void* in, int in_dtype, int64_t rows, int64_t cols, __nv_bfloat16* out,
+                               int64_t ld_out, cudaStream_t s, __nv_bfloat16* out_lo = nullptr);
+
+// ------------------------------------------------------------ tensor-train adapter
+struct TTDims {
+  int d;
+  int m[QA_TT_MAX_D], n[QA_TT_MAX_D], r[QA_TT_MAX_D + 1];
+  int64_t N, K;
+  // per-token size of the left-to-right partial contraction Z_k, k = 0..d
+  int64_t zsize[QA_TT_MAX_D + 1];
+  int64_t I(int k) const;  // Π_{q<k} m_q
+  int64_t J(int k) const;  // Π_{q>=k} n_q  (J(d) = 1)
+  int64_t core_numel(int k) const { return (int64_t)r[k] * m[k] * n[k] * r[k + 1]; }
+};
+bool tt_dims(const qa_tt* tt, TTDims* out);
+
+// out[t, i, ik, b, q] = Σ_{a,j} in[t, i, a, j, q] G[a, ik, j, b]   (stage k of the forward contraction)
+cudaError_t launch_tt_stage_fwd(const void* in, int in_dtype, int64_t in_ld, const float* G, float* out,
+                                int64_t out_ld, int64_t T, int64_t I, int A, int nk, int64_t Q, int mk, int B,
+                                cudaStream_t s);
+// din[t, i, a, j, q] = Σ_{ik,b} dout[t, i, ik, b, q] G[a, ik, j, b]
+cudaError_t launch_tt_stage_bwd(const void* dout, int dout_dtype, int64_t dout_ld, const float* G, float* din,
+                                int64_t din_ld, int64_t T, int64_t I, int A, int nk, int64_t Q, int mk, int B,
+                                cudaStream_t s);
+// dG[a, ik, j, b] (+)= Σ_{t,i,q} in[t, i, a, j, q] dout[t, i, ik, b, q]; deterministic two-phase reduction.
+cudaError_t launch_tt_core_grad(const void* in, int in_dtype, int64_t in_ld, const void* dout, int dout_dtype,
+                                int64_t dout_ld, float* partial, int nchunks, float* dG, bool accumulate,
+                                int64_t T, int64_t I, int A, int nk, int64_t Q, int mk, int B, cudaStream_t s);
+int tt_grad_chunks(int64_t T);
+// L[ip, jp, b]: contraction of cores 0..d-2 with the last rank left open (ip < I(d-1), jp < n_0..n_{d-2}).
+cudaError_t launch_tt_prefix_full(const TTDims& dd, const float* const* cores, float* L, cudaStream_t s);
+// out[(h, i), (jp, j)] = Σ_b L[h, jp, b] Gd[b, i, j]  (+ deq(codes) when codes != NULL)
+cudaError_t launch_tt_last_full(const TTDims& dd, const float* L, const float* Gd, const uint8_t* codes,
+                                int bits, const float* scale, const float* offset, void* out, int out_dtype,
+                                cudaStream_t s);
+
+// ------------------------------------------------------------ tcgen05 GEMM
+struct GemmEpilogue {
+  // int8 path: per-row (activation) and per-column (weight) quantisation terms
+  const float* row_scale = nullptr;
+  const float* row_offset = nullptr;
+  const int32_t* row_sum = nullptr;
+  const float* col_scale = nullptr;
+  const float* col_offset = nullptr;
+  const int32_t* col_sum = nullptr;
+  int zp_row = 128, zp_col = 128;
+  int k_real = 0;
+  const float* addend = nullptr;  // fp32 [M, N]
+  int64_t ld_add = 0;
+  __nv_bfloat16* out_bf16 = nullptr;
+  int64_t ld_out = 0;
+  float* out_f32 = nullptr;
+  int64_t ld_f32 = 0;
+  int32_t* out_acc = nullptr;
+  int64_t ld_acc = 0;
+};
+
+// C[M, N] = A[M, K] · B[N, K]ᵀ, both operands K-major with row strides lda / ldb (elements).
+// kind 0: u8 x u8 -> s32 (dequantising epilogue); kind 1: bf16 x bf16 -> f32.
+int gemm_tc(int kind, const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
+            const GemmEpilogue& epi, cudaStream_t s);
+
+}  // namespace qa

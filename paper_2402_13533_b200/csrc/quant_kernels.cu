@@ -1,0 +1,314 @@
+// Per-row min/max quantisation, dequantisation and operand-layout kernels.
+//
+// Bit-exactness contract (quant.py:73-99): lo/hi are exact, the step is the fp64 quotient
+// (hi - lo) / (2^b - 1), a code is floor(v + 0.5) of the fp64 quotient v = (w - lo) / step,
+// clipped.  The kernel evaluates v in fp32 (|v32 - v64| <= ~5e-5 for v <= 255) and replays
+// the exact fp64 sequence (__dsub_rn, __ddiv_rn, __dadd_rn, floor) only for elements whose
+// fp32 quotient lies within 2.5e-4 of a rounding boundary (~0.05% of elements), so every
+// code equals the reference's while the kernel stays HBM-bound.
+#include <math.h>
+
+#include "qa_common.cuh"
+#include "qa_internal.h"
+#include "qa_timing.h"
+
+namespace qa {
+
+namespace {
+
+constexpr float kTieBand = 2.5e-4f;
+
+template <int BITS>
+QA_DEV uint32_t code_of(float v, float lo, float inv, double lo64, double step64) {
+  constexpr float kTop = float((1 << BITS) - 1);
+  const float q = (v - lo) * inv;
+  const float fl = floorf(q);
+  const float fr = q - fl;
+  float c;
+  if (fabsf(fr - 0.5f) < kTieBand) {
+    const double v64 = __ddiv_rn(__dsub_rn(static_cast<double>(v), lo64), step64);
+    c = static_cast<float>(floor(__dadd_rn(v64, 0.5)));
+  } else {
+    c = fr > 0.5f ? fl + 1.0f : fl;
+  }
+  return static_cast<uint32_t>(fminf(fmaxf(c, 0.0f), kTop));
+}
+
+template <typename T>
+QA_DEV void load8(const T* p, float (&f)[8]);
+template <>
+QA_DEV void load8<float>(const float* p, float (&f)[8]) {
+  const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+  const float4 b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+  f[0] = a.x, f[1] = a.y, f[2] = a.z, f[3] = a.w, f[4] = b.x, f[5] = b.y, f[6] = b.z, f[7] = b.w;
+}
+template <>
+QA_DEV void load8<__nv_bfloat16>(const __nv_bfloat16* p, float (&f)[8]) {
+  const uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    f[2 * i] = __uint_as_float(w[i] << 16);
+    f[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+  }
+}
+
+// One warp per row.  Pass 1: exact min/max (+ finiteness); pass 2 re-reads the row (L1/L2
+// resident) and writes codes, the reference's packed layout for 4 bits, and Σ codes.
+template <typename InT, int BITS>
+__global__ void __launch_bounds__(256) k_quantize_rows(const InT* __restrict__ w, int64_t rows, int64_t cols,
+                                                       int64_t ldw, uint8_t* __restrict__ codes, int64_t ldc,
+                                                       int64_t pad_cols, float* __restrict__ scale,
+                                                       float* __restrict__ offset, int32_t* __restrict__ rowsum,
+                                                       int32_t* __restrict__ flag, int vec_ok) {
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const uint32_t lane = threadIdx.x & 31u;
+  const InT* src = w + row * ldw;
+  uint8_t* dst = codes + row * ldc;
+  const int64_t nvec = vec_ok ? cols / 8 : 0;  // full 8-element chunks on the vector path
+
+  float lo = INFINITY, hi = -INFINITY;
+  bool bad = false;
+  for (int64_t c = lane; c < nvec; c += 32) {
+    float f[8];
+    load8<InT>(src + c * 8, f);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      lo = fminf(lo, f[i]);
+      hi = fmaxf(hi, f[i]);
+      bad |= !isfinite(f[i]);
+    }
+  }
+  for (int64_t k = nvec * 8 + lane; k < cols; k += 32) {
+    const float v = to_f32(src[k]);
+    lo = fminf(lo, v);
+    hi = fmaxf(hi, v);
+    bad |= !isfinite(v);
+  }
+  lo = warp_min(lo);
+  hi = warp_max(hi);
+  const bool any_bad = __any_sync(0xffffffffu, bad);
+  if (any_bad && lane == 0 && flag != nullptr) atomicOr(flag, 1);
+
+  constexpr int kTop = (1 << BITS) - 1;
+  const double lo64 = static_cast<double>(lo);
+  const double step64 = __ddiv_rn(__dsub_rn(static_cast<double>(hi), lo64), static_cast<double>(kTop));
+  const bool flat = !(step64 > 0.0) || any_bad;
+  const float inv = flat ? 0.0f : static_cast<float>(1.0 / step64);
+
+  int sum = 0;
+  for (int64_t c = lane; c < nvec; c += 32) {
+    float f[8];
+    load8<InT>(src + c * 8, f);
+    uint32_t q[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      q[i] = flat ? 0u : code_of<BITS>(f[i], lo, inv, lo64, step64);
+      sum += static_cast<int>(q[i]);
+    }
+    if (BITS == 8) {
+      uint2 packed;
+      packed.x = q[0] | (q[1] << 8) | (q[2] << 16) | (q[3] << 24);
+      packed.y = q[4] | (q[5] << 8) | (q[6] << 16) | (q[7] << 24);
+      *reinterpret_cast<uint2*>(dst + c * 8) = packed;
+    } else {
+      const uint32_t packed = (q[0] | (q[1] << 4)) | ((q[2] | (q[3] << 4)) << 8) | ((q[4] | (q[5] << 4)) << 16) |
+                              ((q[6] | (q[7] << 4)) << 24);
+      *reinterpret_cast<uint32_t*>(dst + c * 4) = packed;
+    }
+  }
+  // scalar tail, in (even, odd) pairs so 4-bit bytes are formed by one lane
+  for (int64_t k = nvec * 8 + 2 * lane; k < cols; k += 64) {
+    const uint32_t q0 = flat ? 0u : code_of<BITS>(to_f32(src[k]), lo, inv, lo64, step64);
+    const bool has1 = k + 1 < cols;
+    const uint32_t q1 = (flat || !has1) ? 0u : code_of<BITS>(to_f32(src[k + 1]), lo, inv, lo64, step64);
+    sum += static_cast<int>(q0 + q1);
+    if (BITS == 8) {
+      dst[k] = static_cast<uint8_t>(q0);
+      if (has1) dst[k + 1] = static_cast<uint8_t>(q1);
+    } else {
+      dst[k >> 1] = static_cast<uint8_t>(q0 | (q1 << 4));
+    }
+  }
+  if (BITS == 8) {
+    for (int64_t k = cols + lane; k < pad_cols; k += 32) dst[k] = 0;
+  }
+  sum = warp_sum_i(sum);
+  if (lane == 0) {
+    scale[row] = flat ? 0.0f : __double2float_rn(step64);
+    offset[row] = lo;
+    if (rowsum != nullptr) rowsum[row] = sum;
+  }
+}
+
+QA_DEV uint32_t unpack_code(const uint8_t* row, int64_t k, int bits) {
+  if (bits == 8) return row[k];
+  const uint32_t b = row[k >> 1];
+  return (k & 1) ? (b >> 4) : (b & 0xFu);
+}
+
+template <typename OutT>
+QA_DEV OutT from_f64(double v);
+template <>
+QA_DEV float from_f64<float>(double v) {
+  return __double2float_rn(v);
+}
+template <>
+QA_DEV __nv_bfloat16 from_f64<__nv_bfloat16>(double v) {
+  return __float2bfloat16_rn(__double2float_rn(v));
+}
+
+// out[n, k] (or out[k, n]) = code · scale + offset in fp64 (quant.py:102-105), 32x32 tiles.
+template <typename OutT, bool TRANS>
+__global__ void __launch_bounds__(256) k_dequantize(const uint8_t* __restrict__ codes, int64_t ldc,
+                                                    const float* __restrict__ scale,
+                                                    const float* __restrict__ offset, int64_t rows, int64_t cols,
+                                                    int bits, OutT* __restrict__ out, int64_t ld_out,
+                                                    __nv_bfloat16* __restrict__ out_lo) {
+  __shared__ OutT tile[32][33];
+  __shared__ __nv_bfloat16 tile_lo[32][34];
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * 32, c0 = static_cast<int64_t>(blockIdx.x) * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  for (int i = ty; i < 32; i += 8) {
+    const int64_t r = r0 + i, c = c0 + tx;
+    if (r < rows && c < cols) {
+      const double v = __dadd_rn(__dmul_rn(static_cast<double>(unpack_code(codes + r * ldc, c, bits)),
+                                           static_cast<double>(scale[r])),
+                                 static_cast<double>(offset[r]));
+      const OutT hi = from_f64<OutT>(v);
+      // bf16 split: lo = bf16(v - hi), so hi + lo carries ~16 mantissa bits (3xbf16 fp32 path)
+      const __nv_bfloat16 lo = __float2bfloat16_rn(__double2float_rn(v - static_cast<double>(to_f32(hi))));
+      if (TRANS) {
+        tile[i][tx] = hi;
+        tile_lo[i][tx] = lo;
+      } else {
+        out[r * ld_out + c] = hi;
+        if (out_lo != nullptr) out_lo[r * ld_out + c] = lo;
+      }
+    }
+  }
+  if (TRANS) {
+    __syncthreads();
+    for (int i = ty; i < 32; i += 8) {
+      const int64_t c = c0 + i, r = r0 + tx;
+      if (r < rows && c < cols) {
+        out[c * ld_out + r] = tile[tx][i];
+        if (out_lo != nullptr) out_lo[c * ld_out + r] = tile_lo[tx][i];
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_unpack_pad(const uint8_t* __restrict__ codes, int64_t ldc, int64_t rows,
+                                                    int64_t cols, int bits, uint8_t* __restrict__ out,
+                                                    int64_t ld_out) {
+  const int64_t row = blockIdx.y;
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < ld_out;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    out[row * ld_out + k] = k < cols ? static_cast<uint8_t>(unpack_code(codes + row * ldc, k, bits)) : 0;
+  }
+}
+
+template <typename InT>
+__global__ void __launch_bounds__(256) k_to_bf16_pad(const InT* __restrict__ in, int64_t rows, int64_t cols,
+                                                     __nv_bfloat16* __restrict__ out, int64_t ld_out,
+                                                     __nv_bfloat16* __restrict__ out_lo) {
+  const int64_t row = blockIdx.y;
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < ld_out;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float v = k < cols ? to_f32(in[row * cols + k]) : 0.f;
+    const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+    out[row * ld_out + k] = hi;
+    if (out_lo != nullptr) out_lo[row * ld_out + k] = __float2bfloat16_rn(v - __bfloat162float(hi));
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_quantize_rows(const void* w, int w_dtype, int64_t rows, int64_t cols, int64_t ld_w, int bits,
+                                 uint8_t* codes, int64_t ld_codes, int64_t pad_cols, float* scale, float* offset,
+                                 int32_t* rowsum, int32_t* flag, cudaStream_t s) {
+  if (rows == 0) return cudaSuccess;
+  const size_t in_bytes = w_dtype == QA_F32 ? 4 : 2;
+  LaunchScope scope(kQuantize, double(rows) * cols * in_bytes + double(rows) * ld_codes + 12.0 * rows, s);
+  count_launches(1);
+  const int warps = 8;
+  const dim3 grid(static_cast<unsigned>((rows + warps - 1) / warps));
+  const size_t esz = w_dtype == QA_F32 ? 4 : 2;
+  const bool vec_in = (reinterpret_cast<uintptr_t>(w) % 16 == 0) && ((ld_w * esz) % 16 == 0);
+  const bool vec_out = bits == 8 ? ((reinterpret_cast<uintptr_t>(codes) % 8 == 0) && (ld_codes % 8 == 0))
+                                 : ((reinterpret_cast<uintptr_t>(codes) % 4 == 0) && (ld_codes % 4 == 0));
+  const int vec_ok = vec_in && vec_out;
+  if (w_dtype == QA_F32) {
+    if (bits == 8)
+      k_quantize_rows<float, 8><<<grid, warps * 32, 0, s>>>(static_cast<const float*>(w), rows, cols, ld_w, codes,
+                                                            ld_codes, pad_cols, scale, offset, rowsum, flag, vec_ok);
+    else
+      k_quantize_rows<float, 4><<<grid, warps * 32, 0, s>>>(static_cast<const float*>(w), rows, cols, ld_w, codes,
+                                                            ld_codes, pad_cols, scale, offset, rowsum, flag, vec_ok);
+  } else {
+    if (bits == 8)
+      k_quantize_rows<__nv_bfloat16, 8><<<grid, warps * 32, 0, s>>>(static_cast<const __nv_bfloat16*>(w), rows,
+                                                                    cols, ld_w, codes, ld_codes, pad_cols, scale,
+                                                                    offset, rowsum, flag, vec_ok);
+    else
+      k_quantize_rows<__nv_bfloat16, 4><<<grid, warps * 32, 0, s>>>(static_cast<const __nv_bfloat16*>(w), rows,
+                                                                    cols, ld_w, codes, ld_codes, pad_cols, scale,
+                                                                    offset, rowsum, flag, vec_ok);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dequantize(const uint8_t* codes, const float* scale, const float* offset, int64_t rows,
+                              int64_t cols, int bits, void* out, int out_dtype, int64_t ld_out, bool transpose,
+                              cudaStream_t s, __nv_bfloat16* out_lo) {
+  if (rows == 0 || cols == 0) return cudaSuccess;
+  const int64_t ldc = bits == 8 ? cols : (cols + 1) / 2;
+  LaunchScope scope(kDequant, double(rows) * ldc + double(rows) * cols * (out_dtype == QA_F32 ? 4 : 2) * (out_lo ? 2 : 1), s);
+  count_launches(1);
+  const dim3 grid(static_cast<unsigned>((cols + 31) / 32), static_cast<unsigned>((rows + 31) / 32));
+  if (out_dtype == QA_F32) {
+    if (transpose)
+      k_dequantize<float, true><<<grid, 256, 0, s>>>(codes, ldc, scale, offset, rows, cols, bits,
+                                                     static_cast<float*>(out), ld_out, nullptr);
+    else
+      k_dequantize<float, false><<<grid, 256, 0, s>>>(codes, ldc, scale, offset, rows, cols, bits,
+                                                      static_cast<float*>(out), ld_out, nullptr);
+  } else {
+    if (transpose)
+      k_dequantize<__nv_bfloat16, true><<<grid, 256, 0, s>>>(codes, ldc, scale, offset, rows, cols, bits,
+                                                             static_cast<__nv_bfloat16*>(out), ld_out, out_lo);
+    else
+      k_dequantize<__nv_bfloat16, false><<<grid, 256, 0, s>>>(codes, ldc, scale, offset, rows, cols, bits,
+                                                              static_cast<__nv_bfloat16*>(out), ld_out, out_lo);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_unpack_pad(const uint8_t* codes, int64_t rows, int64_t cols, int bits, uint8_t* out,
+                              int64_t ld_out, cudaStream_t s) {
+  if (rows == 0) return cudaSuccess;
+  const int64_t ldc = bits == 8 ? cols : (cols + 1) / 2;
+  LaunchScope scope(kDequant, double(rows) * (ldc + ld_out), s);
+  count_launches(1);
+  const dim3 grid(static_cast<unsigned>(std::min<int64_t>((ld_out + 255) / 256, 64)), static_cast<unsigned>(rows));
+  k_unpack_pad<<<grid, 256, 0, s>>>(codes, ldc, rows, cols, bits, out, ld_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_to_bf16_pad(const void* in, int in_dtype, int64_t rows, int64_t cols, __nv_bfloat16* out,
+                               int64_t ld_out, cudaStream_t s, __nv_bfloat16* out_lo) {
+  if (rows == 0) return cudaSuccess;
+  LaunchScope scope(kDequant, double(rows) * cols * (in_dtype == QA_F32 ? 4 : 2) + double(rows) * ld_out * (out_lo ? 4 : 2), s);
+  count_launches(1);
+  const dim3 grid(static_cast<unsigned>(std::min<int64_t>((ld_out + 255) / 256, 64)), static_cast<unsigned>(rows));
+  if (in_dtype == QA_F32)
+    k_to_bf16_pad<float><<<grid, 256, 0, s>>>(static_cast<const float*>(in), rows, cols, out, ld_out, out_lo);
+  else
+    k_to_bf16_pad<__nv_bfloat16><<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(in), rows, cols, out,
+                                                      ld_out, out_lo);
+  return cudaGetLastError();
+}
+
+}  // namespace qa

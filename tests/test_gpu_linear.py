@@ -1,0 +1,206 @@
+"""GPU parity of the quantised tensor-adapter linear (forward / backward-with-recompute / merge)
+against the oracle, through the C ABI.
+
+Tolerances: |got - want| <= rtol (|want| + rms(want)), reported by oracle.rel_err.
+  exact : act/weight codes and the int32 accumulators
+  1e-5  : fp32 outputs of fp32 arithmetic (y before bf16 rounding, merge in fp32)
+  1e-2  : bf16 outputs and everything computed from bf16 operands (y, dx, adapter grads)
+"""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import paper_2402_13533_b200 as qa
+from paper_2402_13533_b200 import linear as L
+
+pytestmark = pytest.mark.gpu
+
+TOL_F32 = 1e-5
+TOL_BF16 = 1e-2
+
+
+def _np(t):
+    return t.detach().float().cpu().numpy() if t.dtype == torch.bfloat16 else t.detach().cpu().numpy()
+
+
+def _case(N, K, T, bits, r, seed, spec=None, xdtype=torch.bfloat16):
+    W = O.seeded_random(N, K, seed, std=0.02)
+    Xf = O.seeded_random(T, K, seed + 1)
+    x = torch.from_numpy(Xf).cuda().to(xdtype)
+    xs = x.float().cpu().numpy()  # exact values the GPU sees
+    q = qa.quantize_rows(W, bits)
+    oq = O.quantize_rows(W, bits)
+    if spec is None:
+        spec = L.TTSpec.for_shape(N, K, r)
+    shape = O.TTShape(spec.m, spec.n, spec.ranks)
+    cores_np = O.tt_init_cores(shape, seed + 2, std=0.01)
+    cores = [torch.from_numpy(c).cuda() for c in cores_np]
+    return q, oq, x, xs, spec, cores, cores_np
+
+
+CASES = [
+    # (N, K, T, bits, r, spec)  — config 1 and ragged / padded / int4 shapes
+    (1024, 1024, 512, 8, 8, None),
+    (1024, 1024, 512, 4, 8, None),
+    (512, 768, 77, 8, 4, L.TTSpec((1, 2, 256), (48, 4, 4), (1, 4, 4, 1))),
+    (320, 200, 130, 4, 3, L.TTSpec((4, 80), (20, 10), (1, 3, 1))),
+    (256, 4096, 300, 8, 8, None),
+]
+
+
+@pytest.mark.parametrize("N,K,T,bits,r,spec", CASES)
+def test_forward_parity(N, K, T, bits, r, spec):
+    q, oq, x, xs, spec, cores, cores_np = _case(N, K, T, bits, r, 11, spec)
+    out = L.linear_forward(q, (spec, cores), x, debug=True)
+    ref = O.qa_linear_forward(xs, oq, cores_np)
+    acc = _np(out["acc"]).astype(np.int64)
+    assert np.array_equal(acc, ref["acc"]), f"int32 accumulators differ at {np.argwhere(acc != ref['acc'])[:5]}"
+    y2 = _np(out["y2"])
+    e_y2 = O.rel_err(y2, ref["y2"])
+    e_y1 = O.rel_err(_np(out["y_f32"]) - y2, ref["y1"])
+    e_y = O.rel_err(_np(out["y_bf16"]), ref["y"])
+    assert e_y1 <= TOL_F32, e_y1
+    assert e_y2 <= TOL_BF16, e_y2
+    assert e_y <= TOL_BF16, e_y
+
+
+@pytest.mark.parametrize("N,K,T,bits,r,spec", CASES)
+def test_backward_parity(N, K, T, bits, r, spec):
+    q, oq, x, xs, spec, cores, cores_np = _case(N, K, T, bits, r, 21, spec)
+    dy = torch.from_numpy(O.seeded_random(T, N, 99)).cuda().to(torch.bfloat16)
+    dys = dy.float().cpu().numpy()
+    dx, dcores, dx32 = L.linear_backward(q, (spec, cores), x, dy, debug=True)
+    ref = O.qa_linear_backward(xs, dys, oq, cores_np)
+    assert O.rel_err(_np(dx32), ref["dx"]) <= TOL_BF16
+    assert O.rel_err(_np(dx), ref["dx"]) <= TOL_BF16
+    for k, (g, gr) in enumerate(zip(dcores, ref["dcores"])):
+        e = O.rel_err(_np(g), gr)
+        assert e <= TOL_BF16, (k, e)
+
+
+def test_base_only_paths_match_reference_functions():
+    # qmatmul with per-token act-quant == qmatmul(qw, deq(Q(x))) ; qmatmul_t == reference qmatmul_t
+    W = O.seeded_random(384, 640, 5, std=0.02)
+    X = O.seeded_random(200, 640, 6)
+    dY = O.seeded_random(200, 384, 7)
+    for bits in (4, 8):
+        q, oq = qa.quantize_rows(W, bits), O.quantize_rows(W, bits)
+        y = qa.qmatmul(q, torch.from_numpy(X).cuda())
+        assert y.dtype == torch.float32
+        want = O.qmatmul(oq, O.dequantize_rows(O.quantize_rows(X, 8)))
+        assert O.rel_err(_np(y), want) <= TOL_F32
+        dx = qa.qmatmul_t(q, torch.from_numpy(dY).cuda())
+        assert O.rel_err(_np(dx), O.qmatmul_t(oq, dY)) <= TOL_BF16
+
+
+def test_lora_backend_is_drop_in_for_reference_loralinear(golden_dir):
+    g = np.load(os.path.join(golden_dir, "lora_cases.npz"))
+    for bits in (4, 8):
+        base = L.QuantizedLinear("w.base", qa.quantize_rows(g[f"b{bits}__w"], bits))
+        ad = L.LoraLinear("w", base, g[f"b{bits}__down"], g[f"b{bits}__up"])
+        x = torch.from_numpy(g[f"b{bits}__x"].astype(np.float32)).cuda()
+        dy = torch.from_numpy(g[f"b{bits}__dy"].astype(np.float32)).cuda()
+        grads = {}
+        dx = ad.backward(x, dy, grads)
+        # the reference's own LoraLinear.backward outputs (transformer.py:310-318)
+        assert set(grads) == {"w.down", "w.up"}
+        assert O.rel_err(_np(dx), g[f"b{bits}__dx"]) <= TOL_BF16
+        assert O.rel_err(_np(grads["w.down"]), g[f"b{bits}__gdown"]) <= TOL_BF16
+        assert O.rel_err(_np(grads["w.up"]), g[f"b{bits}__gup"]) <= TOL_BF16
+        # _accumulate semantics: a second backward adds
+        ad.backward(x, dy, grads)
+        assert O.rel_err(_np(grads["w.up"]), 2 * g[f"b{bits}__gup"]) <= TOL_BF16
+        # forward = reference adapter + the paper's per-token act-quant of the base product
+        y = ad.forward(x)
+        oq = O.quantize_rows(g[f"b{bits}__w"], bits)
+        _, cores = O.lora_as_tt(g[f"b{bits}__down"].astype(np.float64), g[f"b{bits}__up"].astype(np.float64))
+        want = O.qa_linear_forward(x.cpu().numpy(), oq, cores)["y"]
+        assert O.rel_err(_np(y), want) <= TOL_F32
+
+
+@pytest.mark.parametrize("bits", [8, 4])
+def test_merge_parity_and_merged_inference(bits):
+    q, oq, x, xs, spec, cores, cores_np = _case(1024, 1024, 64, bits, 8, 31)
+    base = L.QuantizedLinear("w.base", q)
+    ad = L.TTLinear("w", base, spec, cores)
+    wt = L.tt_materialize(spec, cores)
+    assert O.rel_err(_np(wt), O.tt_full(cores_np)) <= TOL_F32
+    merged = L.tt_merge(ad)
+    assert O.rel_err(_np(merged), O.qa_merge(oq, cores_np)) <= TOL_F32
+    with pytest.raises(qa.ModelError, match="already merged"):
+        L.tt_merge(ad)
+    with pytest.raises(qa.ModelError, match="inference-only"):
+        ad.backward(x, torch.zeros(64, 1024, device="cuda"), {})
+    y = ad.forward(x)  # dense bf16 GEMM on W'
+    assert O.rel_err(_np(y), xs.astype(np.float64) @ O.qa_merge(oq, cores_np).T) <= TOL_BF16
+
+
+def test_edge_cases():
+    q = qa.quantize_rows(O.seeded_random(256, 512, 3, std=0.02), 8)
+    spec = L.TTSpec.for_shape(256, 512, 4)
+    cores = [torch.randn(spec.core_shape(k), device="cuda") * 0.01 for k in range(spec.d)]
+    # empty token batch
+    y = L.linear_forward(q, (spec, cores), torch.zeros(0, 512, device="cuda", dtype=torch.bfloat16))
+    assert y.shape == (0, 256)
+    # single token, 3-D input shape preserved
+    x = torch.randn(1, 1, 512, device="cuda", dtype=torch.bfloat16)
+    y = L.linear_forward(q, (spec, cores), x)
+    assert y.shape == (1, 1, 256)
+    # constant token rows (scale 0) go through the offset path exactly
+    xc = torch.full((3, 512), 0.75, device="cuda")
+    out = L.linear_forward(q, None, xc, debug=True)
+    oq = O.quantize_rows(O.seeded_random(256, 512, 3, std=0.02), 8)
+    assert O.rel_err(_np(out["y_f32"]), O.qmatmul(oq, np.full((3, 512), 0.75))) <= TOL_F32
+    # shape mismatch and bad cores raise the reference's exception classes
+    with pytest.raises(qa.QuantError):
+        L.linear_forward(q, None, torch.zeros(4, 100, device="cuda"))
+    with pytest.raises(qa.ModelError):
+        L.linear_forward(q, (spec, cores[:2]), x)
+
+
+def test_determinism():
+    q, oq, x, xs, spec, cores, _ = _case(1024, 1024, 512, 8, 8, 41)
+    dy = torch.randn(512, 1024, device="cuda", dtype=torch.bfloat16)
+    a = L.linear_forward(q, (spec, cores), x)
+    b = L.linear_forward(q, (spec, cores), x)
+    assert torch.equal(a, b)
+    dx1, g1 = L.linear_backward(q, (spec, cores), x, dy)
+    dx2, g2 = L.linear_backward(q, (spec, cores), x, dy)
+    assert torch.equal(dx1, dx2)
+    assert all(torch.equal(u, v) for u, v in zip(g1, g2))
+
+
+def test_full_size_properties():
+    # config-2 shape (4096x4096, 16384 tokens): exact accumulators on sampled entries, sampled
+    # tokens against the oracle, and linearity of the backward in dy.
+    N = K = 4096
+    T = 16384
+    torch.manual_seed(3)
+    W = (torch.randn(N, K, device="cuda") * 0.02)
+    q = qa.quantize_rows(W, 8)
+    spec = L.TTSpec.for_shape(N, K, 8)
+    cores = [torch.randn(spec.core_shape(k), device="cuda") * 0.01 for k in range(spec.d)]
+    x = torch.randn(T, K, device="cuda").to(torch.bfloat16)
+    out = L.linear_forward(q, (spec, cores), x, debug=True)
+    qx = qa.quantize_rows(x, 8)
+    rows = torch.randint(0, T, (64,), device="cuda")
+    cx = qx.codes[rows].long()
+    exact = cx @ q.codes.long().t()
+    assert torch.equal(exact, out["acc"][rows].long())
+    oq = O.quantize_rows(W.cpu().numpy(), 8)
+    cores_np = [c.cpu().numpy() for c in cores]
+    ref = O.qa_linear_forward(x[rows].float().cpu().numpy(), oq, cores_np)
+    assert O.rel_err(_np(out["y_bf16"][rows]), ref["y"]) <= TOL_BF16
+    dy1 = torch.randn(T, N, device="cuda").to(torch.bfloat16)
+    dy2 = torch.randn(T, N, device="cuda").to(torch.bfloat16)
+    dsum = (dy1.float() + dy2.float()).to(torch.bfloat16)
+    a, ga = L.linear_backward(q, (spec, cores), x, dy1)
+    b, gb = L.linear_backward(q, (spec, cores), x, dy2)
+    c, gc = L.linear_backward(q, (spec, cores), x, dsum)
+    assert O.rel_err(_np(c), _np(a) + _np(b)) <= 2 * TOL_BF16
+    for u, v, w in zip(ga, gb, gc):
+        assert O.rel_err(_np(w), _np(u) + _np(v)) <= 2 * TOL_BF16

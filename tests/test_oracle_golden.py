@@ -183,3 +183,17 @@ def test_dp_mean_fixed_order():
     a = {"g": np.array([1.0, 2.0])}
     b = {"g": np.array([3.0, 6.0])}
     np.testing.assert_array_equal(O.dp_mean([a, b])["g"], [2.0, 4.0])
+
+
+def test_staged_cpu_port_equals_materialised_oracle():
+    for shape in (O.TTShape((1, 4, 8), (8, 2, 2), (1, 3, 3, 1)), O.TTShape((4, 16, 16), (4, 16, 16), (1, 8, 8, 1)),
+                  O.TTShape((1, 32), (48, 1), (1, 4, 1))):
+        rng = np.random.default_rng(7)
+        cores = [rng.standard_normal(shape.core_shape(k)) for k in range(shape.d)]
+        x = rng.standard_normal((9, shape.K))
+        dy = rng.standard_normal((9, shape.N))
+        np.testing.assert_allclose(O.tt_apply_staged(x, cores), O.tt_apply(x, cores), rtol=1e-10, atol=1e-10)
+        dxa, grads = O.tt_backward_staged(x, dy, cores)
+        np.testing.assert_allclose(dxa, O.tt_dx(dy, cores), rtol=1e-10, atol=1e-10)
+        for g, gr in zip(grads, O.tt_core_grads(x, dy, cores)):
+            np.testing.assert_allclose(g, gr, rtol=1e-10, atol=1e-9)
