@@ -65,7 +65,7 @@ def workload_config(cfg_name, world):
         scaling = "weak"
     desc = {
         "workload": (f"llama2-7b linear set q/k/v/o 4096x4096, gate/up 11008x4096, down 4096x11008; int{c['bits']} "
-                     f"per-row weights; TT adapter r={c['rank']} m=(1,N/256,256) n=(K/16,4,4); "
+                     f"per-row weights; TT adapter r={c['rank']} m=(1,N/256,256) n=(K/4,4,1); "
                      f"{tokens} bf16 tokens/GPU; fwd + bwd-with-recompute (+ NCCL grad all-reduce)"),
         "baseline_config": int(cfg_name),
         "tokens_per_gpu": tokens,

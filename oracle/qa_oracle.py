@@ -253,15 +253,15 @@ def tt_modes_for(N: int, K: int, r: int) -> TTShape:
     """The mode factorisation pinned for each BASELINE shape (BASELINE.json leaves 7B/70B open).
 
     Config 1 (1024x1024): balanced (4,16,16)x(4,16,16) as BASELINE.json states.
-    Llama shapes: m = (1, N/256, 256), n = (K/16, 4, 4): the heavy contractions
-    touch x once with rank r (like LoRA's down projection) and the last core
-    couples a 256-wide output block with a 4-wide input block, which is what
-    lets the forward fuse its last stage into the GEMM epilogue.
+    Llama shapes: m = (1, N/256, 256), n = (K/4, 4, 1): the first core is
+    input-only and the last output-only, so the contractions that touch x or dy
+    have rank r on their small side (like LoRA's down / up projections) while
+    the middle core couples 16..112 output blocks with 4 input blocks.
     """
     if N == 1024 and K == 1024:
         return TTShape((4, 16, 16), (4, 16, 16), (1, r, r, 1))
-    if N % 256 == 0 and K % 16 == 0:
-        return TTShape((1, N // 256, 256), (K // 16, 4, 4), (1, r, r, 1))
+    if N % 256 == 0 and K % 4 == 0:
+        return TTShape((1, N // 256, 256), (K // 4, 4, 1), (1, r, r, 1))
     raise OracleError(f"no pinned TT modes for {N}x{K}")
 
 

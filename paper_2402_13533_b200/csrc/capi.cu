@@ -66,8 +66,45 @@ struct LinearPlan {
   __nv_bfloat16* wdt_lo = nullptr;  // fp32-input path: bf16 residuals of deq(W)ᵀ and dy
   __nv_bfloat16* dyb_lo = nullptr;
   float* dxacc = nullptr;           // fp32-input path: partial dx [T, K]
+  // fast TT family (m_1 = 1, n_d = 1, d in {2, 3}): see tt_fast.cu
+  bool fast = false;
+  int fd = 0, R1 = 0, J1 = 0, K2 = 0, K2p = 0, H = 0, M = 0, C = 0, S_dy = 1, S_dg1 = 1;
+  __nv_bfloat16* zb = nullptr;    // Z1 bf16 [T, K2p] (GEMM extension operand)
+  __nv_bfloat16* v = nullptr;     // V bf16 [N, K2p]
+  float* zf = nullptr;            // Z1 fp32 [T, K2]
+  float* z2 = nullptr;            // Z2 fp32 [T, H*C] (d = 3)
+  float* dzp = nullptr;           // dZ_{d-1} partials [M/256][T][H*C]
+  float* dzd = nullptr;           // dZ_{d-1} [T][H*C] (summed)
+  float* dz1 = nullptr;           // dZ1 fp32 [T, K2]
+  __nv_bfloat16* dz1b = nullptr;  // dZ1 bf16 [T, K2p]
+  __nv_bfloat16* bext = nullptr;  // B_ext bf16 [K, K2p]
+  float* gpart = nullptr;         // core-gradient partials
+  float* g1i = nullptr;           // G1 interleaved for the x pass
   size_t bytes = 0;
 };
+
+// The fast TT family: first core input-only, last core output-only (LoRA is d = 2).
+bool plan_fast(const TTDims& dd, int64_t N, int64_t K, LinearPlan* P) {
+  const int d = dd.d;
+  if ((d != 2 && d != 3) || dd.m[0] != 1 || dd.n[d - 1] != 1) return false;
+  const int R1 = dd.r[1];
+  const int64_t J1 = K / dd.n[0];
+  if (J1 > 64 || !fast_tt_supported(static_cast<int>(J1), R1)) return false;
+  const int H = d == 3 ? dd.m[1] : 1;
+  const int M = dd.m[d - 1];
+  const int C = dd.r[d - 1];
+  if ((C != 8 && C != 16) || M % 256 != 0 || N % 8 != 0 || K % 8 != 0) return false;
+  P->fast = true;
+  P->fd = d;
+  P->R1 = R1;
+  P->J1 = static_cast<int>(J1);
+  P->K2 = R1 * static_cast<int>(J1);
+  P->K2p = static_cast<int>(round_up(3 * P->K2, 64));  // 3-term bf16 split of Z1 / dZ1 (tt_fast.cu)
+  P->H = H;
+  P->M = M;
+  P->C = C;
+  return true;
+}
 
 bool plan_linear(const qa_qweight* w, const TTDims* dd, int64_t T, void* ws, LinearPlan* P, bool f32_path) {
   P->T = T;
@@ -82,7 +119,26 @@ bool plan_linear(const qa_qweight* w, const TTDims* dd, int64_t T, void* ws, Lin
   P->ox = b.take<float>(T);
   P->rsx = b.take<int32_t>(T);
   if (P->need_wcodes) P->wcodes = b.take<uint8_t>(P->N * P->Kp);
-  if (dd != nullptr) {
+  if (dd != nullptr && plan_fast(*dd, P->N, P->K, P)) {
+    const int64_t HC = static_cast<int64_t>(P->H) * P->C;
+    const int ncb = P->M / 256;
+    P->g1i = b.take<float>(static_cast<int64_t>(g1i_floats(P->K, P->J1, P->R1)));
+    P->zb = b.take<__nv_bfloat16>(T * P->K2p);
+    P->v = b.take<__nv_bfloat16>(P->N * P->K2p);
+    P->zf = b.take<float>(T * P->K2);
+    if (P->fd == 3) P->z2 = b.take<float>(T * HC);
+    P->dzp = b.take<float>(int64_t(ncb) * T * HC);
+    P->dzd = b.take<float>(T * HC);
+    P->dz1 = b.take<float>(T * P->K2);
+    P->dz1b = b.take<__nv_bfloat16>(T * P->K2p);
+    P->bext = b.take<__nv_bfloat16>(P->K * P->K2p);
+    P->S_dy = tt_dy_splits(T, ncb * P->H);
+    P->S_dg1 = tt_dg1_splits(T, P->K, P->J1);
+    P->nchunks = tt_grad_chunks(T);
+    int64_t gp = std::max<int64_t>(int64_t(P->H) * P->S_dy * P->C * P->M, int64_t(P->S_dg1) * P->K * P->R1);
+    if (P->fd == 3) gp = std::max<int64_t>(gp, dd->core_numel(1) * P->nchunks);
+    P->gpart = b.take<float>(gp);
+  } else if (dd != nullptr) {
     int64_t zmax = 0;
     for (int k = 1; k < dd->d; ++k) {
       P->z[k] = b.take<float>(T * dd->zsize[k]);
@@ -226,11 +282,11 @@ int qa_linear_forward(const qa_qweight* w, const qa_tt* tt, const void* x, int x
                       void* y, int32_t* acc_i32, float* y_f32, float* y2_f32, void* workspace,
                       size_t workspace_bytes, void* stream) {
   QA_TRY(check_weight(w));
+  if (tokens == 0) return QA_OK;  // empty batch: nothing to do (pointers may be null)
   if (x == nullptr || tokens < 0 || (x_dtype != QA_F32 && x_dtype != QA_BF16) || w->rowsum == nullptr) {
     set_error("qa_linear_forward: bad argument (x, dtype, tokens or weight rowsum)");
     return QA_ERR_ARG;
   }
-  if (tokens == 0) return QA_OK;
   TTDims dd;
   const TTDims* pd = nullptr;
   if (tt != nullptr) {
@@ -247,16 +303,34 @@ int qa_linear_forward(const qa_qweight* w, const qa_tt* tt, const void* x, int x
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t T = tokens, N = P.N, K = P.K;
 
-  // (2) per-token activation quantisation: quantize_rows on x[T, K] (codes padded to Kp with zeros)
-  QA_TRY_CUDA(launch_quantize_rows(x, x_dtype, T, K, K, 8, P.xcodes, P.Kp, P.Kp, P.sx, P.ox, P.rsx, nullptr, s),
-              "act quantize");
+  GemmExt ext;
+  const bool x_vec = reinterpret_cast<uintptr_t>(x) % 16 == 0;
+  if (P.fast && x_vec) {
+    // (2)+(4a) one pass over x: bit-exact per-token act-quant + Z1 = first TT stage
+    QA_TRY_CUDA(launch_actquant_z1(x, x_dtype, T, K, true, P.xcodes, P.Kp, P.sx, P.ox, P.rsx, tt->cores[0], P.J1,
+                                   P.R1, P.zb, P.K2p, nullptr, P.g1i, s),
+                "act quantize + TT stage 1");
+    // (4b) V = cores 2..d contracted; y2 = Z1 · Vᵀ runs as extension k-blocks of the GEMM
+    QA_TRY_CUDA(launch_build_v(P.fd, P.R1, P.H, P.J1, P.C, P.M, tt->cores[1], P.fd == 3 ? tt->cores[2] : nullptr,
+                               P.v, N, P.K2p, s),
+                "build V");
+    ext.A2 = P.zb;
+    ext.lda2 = P.K2p;
+    ext.B2 = P.v;
+    ext.ldb2 = P.K2p;
+    ext.K2 = P.K2p;
+  } else {
+    // (2) per-token activation quantisation: quantize_rows on x[T, K] (codes padded to Kp with zeros)
+    QA_TRY_CUDA(launch_quantize_rows(x, x_dtype, T, K, K, 8, P.xcodes, P.Kp, P.Kp, P.sx, P.ox, P.rsx, nullptr, s),
+                "act quantize");
+  }
   int st = QA_OK;
   const uint8_t* wop = weight_operand(w, P, s, &st);
   QA_TRY(st);
 
-  // (4) TT adapter y2 = x · W_tᵀ via the left-to-right stage chain
+  // (4) generic TT adapter y2 = x · W_tᵀ via the left-to-right stage chain
   float* y2 = nullptr;
-  if (pd != nullptr) {
+  if (pd != nullptr && ext.K2 == 0) {
     y2 = y2_f32 != nullptr ? y2_f32 : P.y2;
     const void* zin = x;
     int zin_dtype = x_dtype;
@@ -291,19 +365,34 @@ int qa_linear_forward(const qa_qweight* w, const qa_tt* tt, const void* x, int x
   e.ld_f32 = N;
   e.out_acc = acc_i32;
   e.ld_acc = N;
-  return gemm_tc(0, P.xcodes, P.Kp, wop, P.Kp, T, N, P.Kp, e, s);
+  if (ext.K2 > 0) {
+    e.out_y2 = y2_f32;
+    e.ld_y2 = N;
+  }
+  return gemm_tc(0, P.xcodes, P.Kp, wop, P.Kp, T, N, P.Kp, e, s, ext.K2 > 0 ? &ext : nullptr);
 }
 
 int qa_linear_backward(const qa_qweight* w, const qa_tt* tt, const void* x, int x_dtype, const void* dy,
                        int dy_dtype, int64_t tokens, void* dx, float* dx_f32, float* const* dcores,
                        int accumulate, void* workspace, size_t workspace_bytes, void* stream) {
   QA_TRY(check_weight(w));
+  if (tokens == 0) {
+    // empty batch: gradients of an empty sum are zero (unless accumulating)
+    if (tt != nullptr && dcores != nullptr && accumulate == 0) {
+      TTDims dz;
+      QA_TRY(check_tt(tt, w, &dz));
+      for (int k = 0; k < dz.d; ++k)
+        if (dcores[k] != nullptr)
+          QA_TRY_CUDA(cudaMemsetAsync(dcores[k], 0, sizeof(float) * dz.core_numel(k), static_cast<cudaStream_t>(stream)),
+                      "memset dcores");
+    }
+    return QA_OK;
+  }
   if (dy == nullptr || tokens < 0 || (x_dtype != QA_F32 && x_dtype != QA_BF16) ||
       (dy_dtype != QA_F32 && dy_dtype != QA_BF16)) {
     set_error("qa_linear_backward: bad argument");
     return QA_ERR_ARG;
   }
-  if (tokens == 0) return QA_OK;
   TTDims dd;
   const TTDims* pd = nullptr;
   if (tt != nullptr) {
@@ -327,7 +416,92 @@ int qa_linear_backward(const qa_qweight* w, const qa_tt* tt, const void* x, int 
   const bool want_dx = dx != nullptr || dx_f32 != nullptr;
 
   float* dxad = nullptr;
-  if (pd != nullptr) {
+  GemmExt ext;
+  // bf16 view of dy: the dX GEMM operand and the fast dy pass read it through 16-byte copies
+  const void* dyb16 = dy;
+  int64_t ld_dyb = N;
+  bool dy_converted = false;
+  auto convert_dy = [&]() -> int {
+    if (dy_converted) return QA_OK;
+    QA_TRY_CUDA(launch_to_bf16_pad(dy, dy_dtype, T, N, P.dyb, P.Np, s, f32_path ? P.dyb_lo : nullptr), "dy to bf16");
+    dyb16 = P.dyb;
+    ld_dyb = P.Np;
+    dy_converted = true;
+    return QA_OK;
+  };
+  if (f32_path || P.Np != N || reinterpret_cast<uintptr_t>(dy) % 16 != 0) QA_TRY(convert_dy());
+
+  const bool fast = pd != nullptr && P.fast && reinterpret_cast<uintptr_t>(x) % 16 == 0;
+  if (fast) {
+    // (5) recompute Z1 from the stored layer input, then Z_{d-1}
+    const int d = P.fd;
+    QA_TRY_CUDA(launch_actquant_z1(x, x_dtype, T, K, false, nullptr, 0, nullptr, nullptr, nullptr, tt->cores[0], P.J1,
+                                   P.R1, nullptr, 0, P.zf, P.g1i, s),
+                "TT stage 1 recompute");
+    const float* zd = P.zf;
+    int64_t zs = P.K2;
+    const bool mid_fast = d == 3 && mid_fast_ok(P.K2, P.H * P.C);
+    if (d == 3) {
+      if (mid_fast)
+        QA_TRY_CUDA(launch_mid_fwd(P.zf, T, P.K2, P.J1, P.H * P.C, P.C, tt->cores[1], P.z2, s), "TT stage 2 recompute");
+      else
+        QA_TRY_CUDA(launch_tt_stage_fwd(P.zf, QA_F32, P.K2, tt->cores[1], P.z2, int64_t(P.H) * P.C, T, 1, P.R1, P.J1,
+                                        1, P.H, P.C, s),
+                    "TT stage 2 recompute");
+      zd = P.z2;
+      zs = int64_t(P.H) * P.C;
+    }
+    // dy pass: dZ_{d-1} = dy · G_dᵀ and dG_d = Σ Z_{d-1}ᵀ dy (one read of dy)
+    const int ncb = P.M / 256;
+    QA_TRY_CUDA(launch_tt_dy(static_cast<const __nv_bfloat16*>(dyb16), T, ld_dyb, P.H, P.M, zd, zs, P.C,
+                             tt->cores[d - 1], P.dzp, P.gpart, P.S_dy, s),
+                "TT dy pass");
+    if (dcores != nullptr && dcores[d - 1] != nullptr)
+      QA_TRY_CUDA(launch_sum_partials(P.gpart, P.H * P.S_dy, int64_t(P.C) * P.M, dcores[d - 1], accumulate != 0, s),
+                  "reduce dG_d");
+    float* dzd = P.dzp;
+    if (ncb > 1) {
+      QA_TRY_CUDA(launch_sum_partials(P.dzp, ncb, T * P.H * P.C, P.dzd, false, s), "reduce dZ");
+      dzd = P.dzd;
+    }
+    float* dz1 = dzd;
+    if (d == 3) {
+      const bool want_g2 = dcores != nullptr && dcores[1] != nullptr;
+      if (mid_fast) {
+        const int nctas = mid_bwd_ctas(T);
+        QA_TRY_CUDA(launch_mid_bwd(dzd, P.zf, T, P.K2, P.J1, P.H * P.C, P.C, tt->cores[1], P.dz1,
+                                   want_g2 ? P.gpart : nullptr, nctas, s),
+                    "dZ1 + dG2");
+        if (want_g2)
+          QA_TRY_CUDA(launch_sum_partials(P.gpart, nctas, int64_t(P.K2) * P.H * P.C, dcores[1], accumulate != 0, s),
+                      "reduce dG2");
+      } else {
+        if (want_g2)
+          QA_TRY_CUDA(launch_tt_core_grad(P.zf, QA_F32, P.K2, dzd, QA_F32, int64_t(P.H) * P.C, P.gpart, P.nchunks,
+                                          dcores[1], accumulate != 0, T, 1, P.R1, P.J1, 1, P.H, P.C, s),
+                      "dG2");
+        QA_TRY_CUDA(launch_tt_stage_bwd(dzd, QA_F32, int64_t(P.H) * P.C, tt->cores[1], P.dz1, P.K2, T, 1, P.R1,
+                                        P.J1, 1, P.H, P.C, s),
+                    "dZ1");
+      }
+      dz1 = P.dz1;
+    }
+    // x pass: dG1 = Σ_t x ⊗ dZ1
+    if (dcores != nullptr && dcores[0] != nullptr) {
+      QA_TRY_CUDA(launch_tt_dg1(x, x_dtype, T, K, dz1, P.J1, P.R1, P.gpart, P.S_dg1, s), "TT x pass");
+      QA_TRY_CUDA(launch_sum_partials(P.gpart, P.S_dg1, K / P.J1 * P.R1, dcores[0], accumulate != 0, s), "reduce dG1");
+    }
+    if (want_dx) {
+      // adapter dx = dZ1 · B_extᵀ as extension k-blocks of the dX GEMM
+      QA_TRY_CUDA(launch_split_rows(dz1, T, P.K2, P.dz1b, P.K2p, s), "dZ1 to bf16 hi/lo");
+      QA_TRY_CUDA(launch_build_bext(P.R1, P.J1, tt->cores[0], P.bext, K, P.K2p, s), "build B_ext");
+      ext.A2 = P.dz1b;
+      ext.lda2 = P.K2p;
+      ext.B2 = P.bext;
+      ext.ldb2 = P.K2p;
+      ext.K2 = P.K2p;
+    }
+  } else if (pd != nullptr) {
     // (5) recompute Z_1..Z_{d-1} from the stored layer input
     for (int k = 0; k + 1 < dd.d; ++k) {
       const void* zin = k == 0 ? x : static_cast<const void*>(P.z[k]);
@@ -373,14 +547,8 @@ int qa_linear_backward(const qa_qweight* w, const qa_tt* tt, const void* x, int 
     QA_TRY_CUDA(launch_dequantize(w->codes, w->scale, w->offset, N, K, w->bits, P.wdt, QA_BF16, P.Np, true, s,
                                   f32_path ? P.wdt_lo : nullptr),
                 "dequantize T");
-    const void* a = dy;
-    int64_t lda = N;
-    if (f32_path || P.Np != N || reinterpret_cast<uintptr_t>(dy) % 16 != 0) {
-      QA_TRY_CUDA(launch_to_bf16_pad(dy, dy_dtype, T, N, P.dyb, P.Np, s, f32_path ? P.dyb_lo : nullptr),
-                  "dy to bf16");
-      a = P.dyb;
-      lda = P.Np;
-    }
+    const void* a = dyb16;
+    const int64_t lda = ld_dyb;
     const float* addend = dxad;
     if (f32_path) {
       GemmEpilogue e1;
@@ -404,7 +572,7 @@ int qa_linear_backward(const qa_qweight* w, const qa_tt* tt, const void* x, int 
     e.ld_out = K;
     e.out_f32 = dx_f32;
     e.ld_f32 = K;
-    QA_TRY(gemm_tc(1, a, lda, P.wdt, P.Np, T, K, P.Np, e, s));
+    QA_TRY(gemm_tc(1, a, lda, P.wdt, P.Np, T, K, P.Np, e, s, ext.K2 > 0 ? &ext : nullptr));
   }
   return QA_OK;
 }

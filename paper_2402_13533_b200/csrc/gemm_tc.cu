@@ -4,13 +4,17 @@
 //       acc[t, n] = Σ_k cx[t, k] · cw[n, k]   u8 x u8 -> exact s32 in TMEM (tcgen05.mma kind::i8)
 //       epilogue: centred dequantisation (SURVEY §7 "epilogue cancellation"):
 //         acc_c = acc - zw·Σcx - zx·Σcw + zx·zw·K       (exact int32)
-//         y     = sx·(sw·acc_c + õw·Σc̃x) + õx·(sw·Σc̃w + K·õw) (+ addend),  õ = offset + z·scale
+//         y     = sx·(sw·acc_c + õw·Σc̃x) + õx·(sw·Σc̃w + K·õw) (+ y2),  õ = offset + z·scale
+//       y2 (the TT adapter) comes from extension k-blocks: bf16 MMAs (kind::f16)
+//       of U = Z1[t, :] against V[n, :] into a second fp32 TMEM accumulator (columns 256..511).
 //   kind 1 (backward dX, qmatmul_t quant.py:135-144):
-//       dx[t, k] = Σ_n dy[t, n] · deq(W)ᵀ[k, n]   bf16 x bf16 -> f32 in TMEM (kind::f16) (+ addend)
+//       dx[t, k] = Σ_n dy[t, n] · deq(W)ᵀ[k, n] (+ Σ_c dZ1[t, c] · B_ext[k, c])   bf16 -> f32 in TMEM
+//       the extension k-blocks accumulate the adapter's dx into the same accumulator.
 //
 // Structure: one 128 x 256 output tile per CTA, 4-stage TMA -> shared-memory ring (128-byte
-// swizzled K-major tiles), warp 0 = TMA producer, warp 1 = single-thread MMA issuer,
-// warp 2 = TMEM allocator, warps 4..7 = epilogue (TMEM lane quarter = warp % 4).
+// swizzled K-major tiles; extension k-blocks travel through the same ring), warp 0 = TMA
+// producer, warp 1 = single-thread MMA issuer, warp 2 = TMEM allocator, warps 4..7 = epilogue
+// (TMEM lane quarter = warp % 4).
 #include <mutex>
 
 #include "qa_common.cuh"
@@ -28,18 +32,55 @@ constexpr int STAGES = 4;
 constexpr int A_BYTES = BM * BK_BYTES;
 constexpr int B_BYTES = BN * BK_BYTES;
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int TMEM_COLS = 256;
 constexpr int THREADS = 256;
 constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 4 * BN * 4 /*column terms*/ + 256;
 
+template <int KIND>
+struct Cfg {
+  static constexpr uint32_t kTmemCols = KIND == 0 ? 512 : 256;  // kind 0: s32 acc + fp32 y2 acc
+};
+
 struct KParams {
-  int64_t M, N, K;  // K in elements
+  int64_t M, N, K;  // K in elements of the main operands
+  int num_ext;      // extension k-blocks (bf16, 64 elements each)
   GemmEpilogue e;
 };
 
+QA_DEV void store_row_chunk(const GemmEpilogue& e, int64_t row, int64_t nb, int ncols, const float (&y)[32],
+                            bool vec_out) {
+  if (e.out_f32 != nullptr) {
+    float* dst = e.out_f32 + row * e.ld_f32 + nb;
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < ncols) dst[j] = y[j];
+  }
+  if (e.out_bf16 != nullptr) {
+    __nv_bfloat16* dst = e.out_bf16 + row * e.ld_out + nb;
+    if (vec_out && ncols == 32) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 pk;
+        uint32_t* w = reinterpret_cast<uint32_t*>(&pk);
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const __nv_bfloat162 b2 = __floats2bfloat162_rn(y[q * 8 + 2 * h], y[q * 8 + 2 * h + 1]);
+          w[h] = *reinterpret_cast<const uint32_t*>(&b2);
+        }
+        *reinterpret_cast<uint4*>(dst + q * 8) = pk;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j < ncols) dst[j] = __float2bfloat16_rn(y[j]);
+    }
+  }
+}
+
 template <int KIND>
 __global__ void __launch_bounds__(THREADS, 1)
-    k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const KParams p) {
+    k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+              const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2, const KParams p) {
+  constexpr uint32_t TMEM_COLS = Cfg<KIND>::kTmemCols;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -59,11 +100,16 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int64_t n0 = static_cast<int64_t>(blockIdx.x) * BN;
   constexpr int ELEM_BYTES = KIND == 0 ? 1 : 2;
   constexpr int BK = BK_BYTES / ELEM_BYTES;
-  const int num_kb = static_cast<int>((p.K + BK - 1) / BK);
+  const int num_main = static_cast<int>((p.K + BK - 1) / BK);
+  const int num_kb = num_main + p.num_ext;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
+    if (p.num_ext > 0) {
+      tma_prefetch_desc(&tmA2);
+      tma_prefetch_desc(&tmB2);
+    }
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -85,8 +131,14 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t ph = (kb / STAGES) & 1;
         mbar_wait(&empty[s], ph ^ 1);
         mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
-        tma_load_2d(sA + s * A_BYTES, &tmA, &full[s], kb * BK, static_cast<int32_t>(m0));
-        tma_load_2d(sB + s * B_BYTES, &tmB, &full[s], kb * BK, static_cast<int32_t>(n0));
+        if (kb < num_main) {
+          tma_load_2d(sA + s * A_BYTES, &tmA, &full[s], kb * BK, static_cast<int32_t>(m0));
+          tma_load_2d(sB + s * B_BYTES, &tmB, &full[s], kb * BK, static_cast<int32_t>(n0));
+        } else {
+          const int ke = (kb - num_main) * 64;  // 64 bf16 = 128 bytes
+          tma_load_2d(sA + s * A_BYTES, &tmA2, &full[s], ke, static_cast<int32_t>(m0));
+          tma_load_2d(sB + s * B_BYTES, &tmB2, &full[s], ke, static_cast<int32_t>(n0));
+        }
       }
     }
   } else if (warp == 1) {
@@ -94,6 +146,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (lane == 0) {
       constexpr uint32_t idesc = KIND == 0 ? make_idesc(/*S32*/ 2, /*u8*/ 0, /*u8*/ 0, BM, BN)
                                            : make_idesc(/*F32*/ 1, /*bf16*/ 1, /*bf16*/ 1, BM, BN);
+      constexpr uint32_t idesc_ext = make_idesc(/*F32*/ 1, /*bf16*/ 1, /*bf16*/ 1, BM, BN);
+      const uint32_t ext_tmem = KIND == 0 ? tmem_base + 256 : tmem_base;
       for (int kb = 0; kb < num_kb; ++kb) {
         const int s = kb % STAGES;
         const uint32_t ph = (kb / STAGES) & 1;
@@ -101,17 +155,27 @@ __global__ void __launch_bounds__(THREADS, 1)
         tc_fence_after();
         const uint64_t a0 = smem_desc_kmajor_sw128(sA + s * A_BYTES);
         const uint64_t b0 = smem_desc_kmajor_sw128(sB + s * B_BYTES);
+        if (kb < num_main) {
 #pragma unroll
-        for (int k = 0; k < BK_BYTES / 32; ++k) {  // 32 bytes of K per MMA (32 x i8 or 16 x bf16)
-          const uint64_t adv = static_cast<uint64_t>((k * 32) >> 4);
-          if (KIND == 0)
-            mma_i8(tmem_base, a0 + adv, b0 + adv, idesc, (kb | k) != 0);
-          else
-            mma_f16(tmem_base, a0 + adv, b0 + adv, idesc, (kb | k) != 0);
+          for (int k = 0; k < BK_BYTES / 32; ++k) {  // 32 bytes of K per MMA (32 x i8 or 16 x bf16)
+            const uint64_t adv = static_cast<uint64_t>((k * 32) >> 4);
+            if (KIND == 0)
+              mma_i8(tmem_base, a0 + adv, b0 + adv, idesc, (kb | k) != 0);
+            else
+              mma_f16(tmem_base, a0 + adv, b0 + adv, idesc, (kb | k) != 0);
+          }
+        } else {
+          const bool first_ext = kb == num_main;
+#pragma unroll
+          for (int k = 0; k < BK_BYTES / 32; ++k) {
+            const uint64_t adv = static_cast<uint64_t>((k * 32) >> 4);
+            const uint32_t acc = KIND == 0 ? (!first_ext || k != 0) : 1u;
+            mma_f16(ext_tmem, a0 + adv, b0 + adv, idesc_ext, acc);
+          }
         }
         mma_commit(&empty[s]);  // slot reusable once these MMAs have read it
       }
-      mma_commit(tmem_full);  // accumulator complete
+      mma_commit(tmem_full);  // accumulators complete
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
@@ -152,19 +216,24 @@ __global__ void __launch_bounds__(THREADS, 1)
       rsxc = static_cast<float>(rsx - e.zp_row * e.k_real);
       ibase = e.zp_row * e.zp_col * e.k_real - e.zp_col * rsx;
     }
+    const bool has_y2 = KIND == 0 && p.num_ext > 0;
 
     mbar_wait(tmem_full, 0);
     tc_fence_after();
 
     const bool vec_out = e.out_bf16 != nullptr && (e.ld_out % 8 == 0) &&
                          (reinterpret_cast<uintptr_t>(e.out_bf16) % 16 == 0);
+    const uint32_t lane_base = (quarter * 32u) << 16;
 #pragma unroll 1
     for (int chunk = 0; chunk < BN / 32; ++chunk) {
       uint32_t v[32];
-      tmem_ld_32x32b_x32(tmem_base + ((quarter * 32u) << 16) + chunk * 32u, v);
+      uint32_t v2[32];
+      tmem_ld_32x32b_x32(tmem_base + lane_base + chunk * 32u, v);
+      if (has_y2) tmem_ld_32x32b_x32(tmem_base + lane_base + 256u + chunk * 32u, v2);
       tmem_ld_wait();
       const int64_t nb = n0 + chunk * 32;
       if (!row_ok || nb >= p.N) continue;
+      const int ncols = static_cast<int>(p.N - nb < 32 ? p.N - nb : 32);
       float y[32];
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
@@ -176,37 +245,30 @@ __global__ void __launch_bounds__(THREADS, 1)
           y[j] = __uint_as_float(v[j]);
         }
       }
-      const int ncols = static_cast<int>(p.N - nb < 32 ? p.N - nb : 32);
+      if (has_y2) {
+        float* y2o = e.out_y2;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) y[j] += __uint_as_float(v2[j]);
+        if (y2o != nullptr) {
+          float* dst = y2o + row * e.ld_y2 + nb;
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (j < ncols) dst[j] = __uint_as_float(v2[j]);
+        }
+      }
       if (e.addend != nullptr) {
         const float* ad = e.addend + row * e.ld_add + nb;
-        for (int j = 0; j < ncols; ++j) y[j] += ad[j];
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (j < ncols) y[j] += ad[j];
       }
       if (KIND == 0 && e.out_acc != nullptr) {
         int32_t* dst = e.out_acc + row * e.ld_acc + nb;
-        for (int j = 0; j < ncols; ++j) dst[j] = static_cast<int32_t>(v[j]);
-      }
-      if (e.out_f32 != nullptr) {
-        float* dst = e.out_f32 + row * e.ld_f32 + nb;
-        for (int j = 0; j < ncols; ++j) dst[j] = y[j];
-      }
-      if (e.out_bf16 != nullptr) {
-        __nv_bfloat16* dst = e.out_bf16 + row * e.ld_out + nb;
-        if (vec_out && ncols == 32) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            uint4 pk;
-            uint32_t* w = reinterpret_cast<uint32_t*>(&pk);
-#pragma unroll
-            for (int h = 0; h < 4; ++h) {
-              const __nv_bfloat162 b2 = __floats2bfloat162_rn(y[q * 8 + 2 * h], y[q * 8 + 2 * h + 1]);
-              w[h] = *reinterpret_cast<const uint32_t*>(&b2);
-            }
-            *reinterpret_cast<uint4*>(dst + q * 8) = pk;
-          }
-        } else {
-          for (int j = 0; j < ncols; ++j) dst[j] = __float2bfloat16_rn(y[j]);
-        }
+        for (int j = 0; j < 32; ++j)
+          if (j < ncols) dst[j] = static_cast<int32_t>(v[j]);
       }
+      store_row_chunk(e, row, nb, ncols, y, vec_out);
     }
     tc_fence_before();
   }
@@ -250,15 +312,31 @@ bool make_tmap(CUtensorMap* m, const void* base, int elem_bytes, int64_t rows, i
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+bool aligned_operand(const void* p, int64_t ld, int eb) {
+  return p != nullptr && reinterpret_cast<uintptr_t>(p) % 16 == 0 && (ld * eb) % 16 == 0;
+}
+
 template <int KIND>
 int launch(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
-           const GemmEpilogue& epi, cudaStream_t s) {
+           const GemmEpilogue& epi, const GemmExt* ext, cudaStream_t s) {
   constexpr int eb = KIND == 0 ? 1 : 2;
-  CUtensorMap ta, tb;
+  CUtensorMap ta, tb, ta2, tb2;
   if (!make_tmap(&ta, A, eb, M, K, lda, BM) || !make_tmap(&tb, B, eb, N, K, ldb, BN)) {
     set_error("cuTensorMapEncodeTiled failed (M=%lld N=%lld K=%lld lda=%lld ldb=%lld)", (long long)M, (long long)N,
               (long long)K, (long long)lda, (long long)ldb);
     return QA_ERR_CUDA;
+  }
+  int num_ext = 0;
+  if (ext != nullptr && ext->K2 > 0) {
+    if (!make_tmap(&ta2, ext->A2, 2, M, ext->K2, ext->lda2, BM) ||
+        !make_tmap(&tb2, ext->B2, 2, N, ext->K2, ext->ldb2, BN)) {
+      set_error("cuTensorMapEncodeTiled failed for the extension operands (K2=%lld)", (long long)ext->K2);
+      return QA_ERR_CUDA;
+    }
+    num_ext = static_cast<int>((ext->K2 + 63) / 64);
+  } else {
+    ta2 = ta;
+    tb2 = tb;
   }
   static bool attr_set = false;
   if (!attr_set) {
@@ -270,26 +348,28 @@ int launch(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, in
   p.M = M;
   p.N = N;
   p.K = K;
+  p.num_ext = num_ext;
   p.e = epi;
   const dim3 grid(static_cast<unsigned>((N + BN - 1) / BN), static_cast<unsigned>((M + BM - 1) / BM));
   const double kalg = KIND == 0 && epi.k_real > 0 ? double(epi.k_real) : double(K);
   LaunchScope scope(KIND == 0 ? kGemmI8 : kGemmBF16, 2.0 * double(M) * double(N) * kalg, s);
   count_launches(1);
-  k_gemm_tc<KIND><<<grid, THREADS, SMEM_BYTES, s>>>(ta, tb, p);
+  k_gemm_tc<KIND><<<grid, THREADS, SMEM_BYTES, s>>>(ta, tb, ta2, tb2, p);
   return cuda_status(cudaGetLastError(), "k_gemm_tc launch");
 }
 
 }  // namespace
 
 int gemm_tc(int kind, const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
-            const GemmEpilogue& epi, cudaStream_t s) {
+            const GemmEpilogue& epi, cudaStream_t s, const GemmExt* ext) {
   if (M == 0 || N == 0) return QA_OK;
   const int eb = kind == 0 ? 1 : 2;
-  if ((lda * eb) % 16 || (ldb * eb) % 16 || reinterpret_cast<uintptr_t>(A) % 16 || reinterpret_cast<uintptr_t>(B) % 16) {
+  if (!aligned_operand(A, lda, eb) || !aligned_operand(B, ldb, eb) ||
+      (ext != nullptr && ext->K2 > 0 && (!aligned_operand(ext->A2, ext->lda2, 2) || !aligned_operand(ext->B2, ext->ldb2, 2)))) {
     set_error("gemm_tc: operands must be 16-byte aligned with 16-byte row strides");
     return QA_ERR_UNSUPPORTED;
   }
-  return kind == 0 ? launch<0>(A, lda, B, ldb, M, N, K, epi, s) : launch<1>(A, lda, B, ldb, M, N, K, epi, s);
+  return kind == 0 ? launch<0>(A, lda, B, ldb, M, N, K, epi, ext, s) : launch<1>(A, lda, B, ldb, M, N, K, epi, ext, s);
 }
 
 }  // namespace qa

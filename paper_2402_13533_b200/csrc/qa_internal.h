@@ -61,6 +61,34 @@ cudaError_t launch_tt_last_full(const TTDims& dd, const float* L, const float* G
                                 int bits, const float* scale, const float* offset, void* out, int out_dtype,
                                 cudaStream_t s);
 
+// out[i] (+)= Σ_p partial[p][i] in fixed order (deterministic reduction of per-CTA partials)
+cudaError_t launch_sum_partials(const float* partial, int nparts, int64_t numel, float* out, bool accumulate,
+                                cudaStream_t s);
+
+// ------------------------------------------------------------ fast TT family (tt_fast.cu)
+bool fast_tt_supported(int J1, int R1);
+size_t g1i_floats(int64_t K, int J1, int R1);  // workspace for the interleaved G1 copy
+cudaError_t launch_actquant_z1(const void* x, int x_dtype, int64_t T, int64_t K, bool want_codes, uint8_t* codes,
+                               int64_t ldc, float* sx, float* ox, int32_t* rsx, const float* G1, int J1, int R1,
+                               __nv_bfloat16* zb, int64_t ldzb, float* zf, float* g1i_ws, cudaStream_t s);
+cudaError_t launch_build_v(int d, int R1, int H, int J1, int C, int M, const float* G2, const float* G3,
+                           __nv_bfloat16* V, int64_t N, int64_t ldv, cudaStream_t s);
+cudaError_t launch_build_bext(int R1, int J1, const float* G1, __nv_bfloat16* B, int64_t K, int64_t ldb,
+                              cudaStream_t s);
+cudaError_t launch_split_rows(const float* in, int64_t T, int K2, __nv_bfloat16* out, int64_t ld, cudaStream_t s);
+bool mid_fast_ok(int K2, int HC);
+int mid_bwd_ctas(int64_t T);
+cudaError_t launch_mid_fwd(const float* z1, int64_t T, int K2, int J1, int HC, int C, const float* G2, float* z2,
+                           cudaStream_t s);
+cudaError_t launch_mid_bwd(const float* dz2, const float* z1, int64_t T, int K2, int J1, int HC, int C,
+                           const float* G2, float* dz1, float* gpart, int nctas, cudaStream_t s);
+int tt_dy_splits(int64_t T, int blocks_per_split);
+cudaError_t launch_tt_dy(const __nv_bfloat16* dy, int64_t T, int64_t N, int H, int M, const float* Z, int64_t zs,
+                         int C, const float* Gd, float* dz_part, float* dg_part, int S, cudaStream_t s);
+int tt_dg1_splits(int64_t T, int64_t K, int J1);
+cudaError_t launch_tt_dg1(const void* x, int x_dtype, int64_t T, int64_t K, const float* dz1, int J1, int R1,
+                          float* part, int S, cudaStream_t s);
+
 // ------------------------------------------------------------ tcgen05 GEMM
 struct GemmEpilogue {
   // int8 path: per-row (activation) and per-column (weight) quantisation terms
@@ -80,11 +108,23 @@ struct GemmEpilogue {
   int64_t ld_f32 = 0;
   int32_t* out_acc = nullptr;
   int64_t ld_acc = 0;
+  float* out_y2 = nullptr;  // kind 0 with extension: the fp32 adapter term (debug)
+  int64_t ld_y2 = 0;
+};
+
+// Extension k-blocks: bf16 A2[M, K2] · B2[N, K2]ᵀ, issued after the main k-loop.  kind 0 puts them
+// in a separate fp32 accumulator added in the epilogue (y2); kind 1 adds them to the main one.
+struct GemmExt {
+  const void* A2 = nullptr;
+  int64_t lda2 = 0;
+  const void* B2 = nullptr;
+  int64_t ldb2 = 0;
+  int64_t K2 = 0;  // multiple of 64 expected (zero padded)
 };
 
 // C[M, N] = A[M, K] · B[N, K]ᵀ, both operands K-major with row strides lda / ldb (elements).
 // kind 0: u8 x u8 -> s32 (dequantising epilogue); kind 1: bf16 x bf16 -> f32.
 int gemm_tc(int kind, const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
-            const GemmEpilogue& epi, cudaStream_t s);
+            const GemmEpilogue& epi, cudaStream_t s, const GemmExt* ext = nullptr);
 
 }  // namespace qa

@@ -11,47 +11,11 @@
 #include "qa_common.cuh"
 #include "qa_internal.h"
 #include "qa_timing.h"
+#include "quant_row.cuh"
 
 namespace qa {
 
 namespace {
-
-constexpr float kTieBand = 2.5e-4f;
-
-template <int BITS>
-QA_DEV uint32_t code_of(float v, float lo, float inv, double lo64, double step64) {
-  constexpr float kTop = float((1 << BITS) - 1);
-  const float q = (v - lo) * inv;
-  const float fl = floorf(q);
-  const float fr = q - fl;
-  float c;
-  if (fabsf(fr - 0.5f) < kTieBand) {
-    const double v64 = __ddiv_rn(__dsub_rn(static_cast<double>(v), lo64), step64);
-    c = static_cast<float>(floor(__dadd_rn(v64, 0.5)));
-  } else {
-    c = fr > 0.5f ? fl + 1.0f : fl;
-  }
-  return static_cast<uint32_t>(fminf(fmaxf(c, 0.0f), kTop));
-}
-
-template <typename T>
-QA_DEV void load8(const T* p, float (&f)[8]);
-template <>
-QA_DEV void load8<float>(const float* p, float (&f)[8]) {
-  const float4 a = __ldg(reinterpret_cast<const float4*>(p));
-  const float4 b = __ldg(reinterpret_cast<const float4*>(p) + 1);
-  f[0] = a.x, f[1] = a.y, f[2] = a.z, f[3] = a.w, f[4] = b.x, f[5] = b.y, f[6] = b.z, f[7] = b.w;
-}
-template <>
-QA_DEV void load8<__nv_bfloat16>(const __nv_bfloat16* p, float (&f)[8]) {
-  const uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
-  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    f[2 * i] = __uint_as_float(w[i] << 16);
-    f[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
-  }
-}
 
 // One warp per row.  Pass 1: exact min/max (+ finiteness); pass 2 re-reads the row (L1/L2
 // resident) and writes codes, the reference's packed layout for 4 bits, and Σ codes.
@@ -200,6 +164,51 @@ __global__ void __launch_bounds__(256) k_dequantize(const uint8_t* __restrict__ 
   }
 }
 
+// Transposed bf16 dequantisation for the dX GEMM operand: outᵀ[k, n] = bf16(code·scale + offset),
+// 64 x 64 tiles, 16-byte code loads and 16-byte stores (full tiles; edges go through k_dequantize).
+template <int BITS>
+__global__ void __launch_bounds__(256) k_dequant_t64(const uint8_t* __restrict__ codes, int64_t ldc,
+                                                     const float* __restrict__ scale,
+                                                     const float* __restrict__ offset,
+                                                     __nv_bfloat16* __restrict__ out, int64_t ld_out,
+                                                     __nv_bfloat16* __restrict__ out_lo) {
+  __shared__ __align__(16) __nv_bfloat16 sh[64][72];
+  __shared__ __align__(16) __nv_bfloat16 sl[64][72];
+  const int64_t n0 = static_cast<int64_t>(blockIdx.y) * 64, k0 = static_cast<int64_t>(blockIdx.x) * 64;
+  const int t = threadIdx.x;
+  const int r = t >> 2, seg = t & 3;  // row n0 + r, columns k0 + 16 seg .. + 15
+  const int64_t n = n0 + r;
+  uint32_t c[16];
+  if (BITS == 8) {
+    const uint4 u = __ldg(reinterpret_cast<const uint4*>(codes + n * ldc + k0 + seg * 16));
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 16; ++i) c[i] = (w[i >> 2] >> (8 * (i & 3))) & 0xFFu;
+  } else {
+    const uint2 u = __ldg(reinterpret_cast<const uint2*>(codes + n * ldc + (k0 + seg * 16) / 2));
+    const uint32_t w[2] = {u.x, u.y};
+#pragma unroll
+    for (int i = 0; i < 16; ++i) c[i] = (w[i >> 3] >> (4 * (i & 7))) & 0xFu;
+  }
+  const double s = static_cast<double>(scale[n]), o = static_cast<double>(offset[n]);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const double v = __dadd_rn(__dmul_rn(static_cast<double>(c[i]), s), o);
+    const __nv_bfloat16 hi = __float2bfloat16_rn(__double2float_rn(v));
+    sh[seg * 16 + i][r] = hi;
+    if (out_lo != nullptr) sl[seg * 16 + i][r] = __float2bfloat16_rn(__double2float_rn(v - double(__bfloat162float(hi))));
+  }
+  __syncthreads();
+#pragma unroll
+  for (int pass = 0; pass < 2; ++pass) {
+    const int kk = (t >> 3) + pass * 32, ch = t & 7;
+    *reinterpret_cast<uint4*>(out + (k0 + kk) * ld_out + n0 + ch * 8) = *reinterpret_cast<const uint4*>(&sh[kk][ch * 8]);
+    if (out_lo != nullptr)
+      *reinterpret_cast<uint4*>(out_lo + (k0 + kk) * ld_out + n0 + ch * 8) =
+          *reinterpret_cast<const uint4*>(&sl[kk][ch * 8]);
+  }
+}
+
 __global__ void __launch_bounds__(256) k_unpack_pad(const uint8_t* __restrict__ codes, int64_t ldc, int64_t rows,
                                                     int64_t cols, int bits, uint8_t* __restrict__ out,
                                                     int64_t ld_out) {
@@ -276,7 +285,19 @@ cudaError_t launch_dequantize(const uint8_t* codes, const float* scale, const fl
       k_dequantize<float, false><<<grid, 256, 0, s>>>(codes, ldc, scale, offset, rows, cols, bits,
                                                       static_cast<float*>(out), ld_out, nullptr);
   } else {
-    if (transpose)
+    const bool fast_t = transpose && rows % 64 == 0 && cols % 64 == 0 && ld_out % 8 == 0 &&
+                        reinterpret_cast<uintptr_t>(out) % 16 == 0 &&
+                        (out_lo == nullptr || reinterpret_cast<uintptr_t>(out_lo) % 16 == 0) &&
+                        reinterpret_cast<uintptr_t>(codes) % 16 == 0 && (ldc % 16 == 0);
+    if (fast_t) {
+      const dim3 g64(static_cast<unsigned>(cols / 64), static_cast<unsigned>(rows / 64));
+      if (bits == 8)
+        k_dequant_t64<8><<<g64, 256, 0, s>>>(codes, ldc, scale, offset, static_cast<__nv_bfloat16*>(out), ld_out,
+                                             out_lo);
+      else
+        k_dequant_t64<4><<<g64, 256, 0, s>>>(codes, ldc, scale, offset, static_cast<__nv_bfloat16*>(out), ld_out,
+                                             out_lo);
+    } else if (transpose)
       k_dequantize<__nv_bfloat16, true><<<grid, 256, 0, s>>>(codes, ldc, scale, offset, rows, cols, bits,
                                                              static_cast<__nv_bfloat16*>(out), ld_out, out_lo);
     else

@@ -1,0 +1,791 @@
+// Fast path for the tensor-train adapters whose first core is input-only and last core is
+// output-only (m_1 = 1, n_d = 1; d = 2 is LoRA, d = 3 is the pinned Llama modes
+// m = (1, N/256, 256), n = (K/4, 4, 1)).  With that shape every contraction that touches a
+// big tensor has a small rank side, so each is a single streaming pass:
+//
+//   forward  x-pass  : act-quant codes + Z1[t, a, J] = Σ_j1 x[t, j1, J] G1[j1, a]  (one read of x)
+//                      y2 = Z1 · Vᵀ runs inside the int8 GEMM as bf16 extension k-blocks, with
+//                      V[n, (a, J)] the contraction of cores 2..d (k_build_v)
+//   backward dy-pass : dZ_{d-1} = dy · G_dᵀ and dG_d = Σ Z_{d-1}ᵀ dy (warp-level bf16 MMA, one read of dy)
+//            x-pass  : dG1 = Σ_t x ⊗ dZ1 (one read of x); dx_adapter = dZ1 · B_extᵀ as extension
+//                      k-blocks of the dX GEMM (k_build_bext)
+// Middle-core work is per-token and tiny (generic kernels in tt_kernels.cu).
+#include "qa_common.cuh"
+#include "qa_internal.h"
+#include "qa_timing.h"
+#include "quant_row.cuh"
+
+namespace qa {
+
+namespace {
+
+// Sum of 32 per-lane values across the warp; afterwards lane l holds the total of value l.
+template <int NV>
+QA_DEV void warp_reduce_scatter32(float (&z)[NV], int base) {
+  const uint32_t lane = lane_id();
+#pragma unroll
+  for (int o = 16, half = 16; o > 0; o >>= 1, half >>= 1) {
+    const bool up = lane & o;
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      const float send = up ? z[base + i] : z[base + i + half];
+      const float keep = up ? z[base + i + half] : z[base + i];
+      z[base + i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Per-token act-quant (bit-exact, quant.py:73-99) fused with the first TT stage.
+// One warp per token row (lane l takes the 8-element chunks l, l + 32, ...), so a warp's row
+// (<= 22 KB) stays L1/L2-resident between the stats pass and the codes pass.  The G1 rows a chunk
+// needs (8 R1 / J1 floats) come from an interleaved copy G1i[c / 32][q][c % 32] (float4), so each
+// warp-wide G1 load is one contiguous 512-byte line.  Vector path only (K % 8 == 0, aligned rows).
+template <int J1, int R1>
+__global__ void __launch_bounds__(256) k_g1_interleave(const float* __restrict__ G1, float4* __restrict__ G1i,
+                                                       int64_t nvec) {
+  constexpr int NQ = 2 * R1 / J1;  // float4 pieces per 8-element chunk
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= nvec * NQ) return;
+  const int64_t c = idx / NQ;
+  const int q = static_cast<int>(idx % NQ);
+  const float* src = G1 + c * (8 / J1) * R1 + 4 * q;
+  G1i[((c / 32) * NQ + q) * 32 + (c % 32)] = make_float4(src[0], src[1], src[2], src[3]);
+}
+
+template <typename InT, int J1, int R1, bool CODES>
+__global__ void __launch_bounds__(256) k_actquant_z1(const InT* __restrict__ x, int64_t T, int64_t K,
+                                                     uint8_t* __restrict__ codes, int64_t ldc,
+                                                     float* __restrict__ sx, float* __restrict__ ox,
+                                                     int32_t* __restrict__ rsx, const float4* __restrict__ G1i,
+                                                     __nv_bfloat16* __restrict__ zb, int64_t ldzb,
+                                                     float* __restrict__ zf) {
+  constexpr int K2 = J1 * R1;
+  static_assert(K2 == 8 || K2 == 16 || K2 == 32 || K2 == 64, "unsupported Z1 width");
+  constexpr int NQ = 2 * R1 / J1;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= T) return;
+  const uint32_t lane = lane_id();
+  const InT* src = x + row * K;
+  const int64_t nvec = K / 8;
+
+  float z[K2];
+#pragma unroll
+  for (int i = 0; i < K2; ++i) z[i] = 0.f;
+  float lo = INFINITY, hi = -INFINITY;
+  constexpr int UNR = 4;  // chunks in flight per lane
+  for (int64_t i0 = 0; i0 * 32 + lane < nvec; i0 += UNR) {
+    float f[UNR][8];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int64_t c = (i0 + u) * 32 + lane;
+      if (c < nvec) load8<InT>(src + c * 8, f[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int64_t c = (i0 + u) * 32 + lane;
+      if (c >= nvec) break;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        lo = fminf(lo, f[u][i]);
+        hi = fmaxf(hi, f[u][i]);
+      }
+      float g[4 * NQ];  // [8 / J1 rows][R1]
+      const float4* gp = G1i + ((i0 + u) * NQ) * 32 + lane;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const float4 v = __ldg(gp + q * 32);
+        g[4 * q] = v.x, g[4 * q + 1] = v.y, g[4 * q + 2] = v.z, g[4 * q + 3] = v.w;
+      }
+#pragma unroll
+      for (int jj = 0; jj < 8 / J1; ++jj)
+#pragma unroll
+        for (int J = 0; J < J1; ++J) {
+          const float xv = f[u][jj * J1 + J];
+#pragma unroll
+          for (int a = 0; a < R1; ++a) z[a * J1 + J] = fmaf(xv, g[jj * R1 + a], z[a * J1 + J]);
+        }
+    }
+  }
+  // Z1 row: reduce across lanes, write fp32 and/or the 3-term bf16 split [hi | lo | hi | 0]
+  if (K2 >= 32) {
+#pragma unroll
+    for (int b = 0; b < K2; b += 32) warp_reduce_scatter32<K2>(z, b);
+#pragma unroll
+    for (int b = 0; b < K2; b += 32) {
+      const float v = z[b];
+      if (zf != nullptr) zf[row * K2 + b + lane] = v;
+      if (zb != nullptr) {
+        const __nv_bfloat16 hv = __float2bfloat16_rn(v);
+        zb[row * ldzb + b + lane] = hv;
+        zb[row * ldzb + K2 + b + lane] = __float2bfloat16_rn(v - __bfloat162float(hv));
+        zb[row * ldzb + 2 * K2 + b + lane] = hv;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < K2; ++i) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) z[i] += __shfl_xor_sync(0xffffffffu, z[i], o);
+    }
+#pragma unroll
+    for (int i = 0; i < K2; ++i) {
+      if (lane == static_cast<uint32_t>(i)) {
+        if (zf != nullptr) zf[row * K2 + i] = z[i];
+        if (zb != nullptr) {
+          const __nv_bfloat16 hv = __float2bfloat16_rn(z[i]);
+          zb[row * ldzb + i] = hv;
+          zb[row * ldzb + K2 + i] = __float2bfloat16_rn(z[i] - __bfloat162float(hv));
+          zb[row * ldzb + 2 * K2 + i] = hv;
+        }
+      }
+    }
+  }
+  if (zb != nullptr)
+    for (int64_t i = 3 * K2 + lane; i < ldzb; i += 32) zb[row * ldzb + i] = __float2bfloat16_rn(0.f);
+  if constexpr (CODES) {
+    lo = warp_min(lo);
+    hi = warp_max(hi);
+    const double lo64 = static_cast<double>(lo);
+    const double step64 = __ddiv_rn(__dsub_rn(static_cast<double>(hi), lo64), 255.0);
+    const bool flat = !(step64 > 0.0);
+    const float inv = flat ? 0.0f : static_cast<float>(1.0 / step64);
+    uint8_t* dst = codes + row * ldc;
+    int sum = 0;
+    for (int64_t i0 = 0; i0 * 32 + lane < nvec; i0 += UNR) {
+      float f[UNR][8];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const int64_t c = (i0 + u) * 32 + lane;
+        if (c < nvec) load8<InT>(src + c * 8, f[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const int64_t c = (i0 + u) * 32 + lane;
+        if (c >= nvec) break;
+        uint32_t q[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          q[i] = flat ? 0u : code_of<8>(f[u][i], lo, inv, lo64, step64);
+          sum += static_cast<int>(q[i]);
+        }
+        uint2 packed;
+        packed.x = q[0] | (q[1] << 8) | (q[2] << 16) | (q[3] << 24);
+        packed.y = q[4] | (q[5] << 8) | (q[6] << 16) | (q[7] << 24);
+        *reinterpret_cast<uint2*>(dst + c * 8) = packed;
+      }
+    }
+    for (int64_t k = K + lane; k < ldc; k += 32) dst[k] = 0;
+    sum = warp_sum_i(sum);
+    if (lane == 0) {
+      sx[row] = flat ? 0.0f : __double2float_rn(step64);
+      ox[row] = lo;
+      rsx[row] = sum;
+    }
+  }
+}
+
+// V[n, c] (bf16, zero padded to ldv): contraction of cores 2..d with the left rank open.
+//   d = 2: V[i, a] = G2[a, i];  d = 3: V[(i2, i3), (a, j2)] = Σ_b G2[a, i2, j2, b] G3[b, i3]
+__global__ void __launch_bounds__(256) k_build_v(int d, int R1, int H, int J1, int C, int M,
+                                                 const float* __restrict__ G2, const float* __restrict__ G3,
+                                                 __nv_bfloat16* __restrict__ V, int64_t N, int64_t ldv) {
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= N * ldv) return;
+  const int64_t n = idx / ldv;
+  const int c = static_cast<int>(idx - n * ldv);
+  // [V_hi | V_hi | V_lo] against [Z_hi | Z_lo | Z_hi]: the three leading terms of the bf16 split
+  // product, so y2 carries ~16 mantissa bits although the MMA operands are bf16
+  const int K2 = R1 * J1;
+  float v = 0.f;
+  if (c < 3 * K2) {
+    const int cc = c % K2;
+    const int a = cc / J1, j2 = cc % J1;
+    if (d == 2) {
+      v = G2[static_cast<int64_t>(a) * N + n];
+    } else {
+      const int i2 = static_cast<int>(n / M), i3 = static_cast<int>(n % M);
+      const float* g2 = G2 + ((static_cast<int64_t>(a) * H + i2) * J1 + j2) * C;
+      for (int b = 0; b < C; ++b) v = fmaf(g2[b], G3[static_cast<int64_t>(b) * M + i3], v);
+    }
+    if (c >= 2 * K2) v -= __bfloat162float(__float2bfloat16_rn(v));
+  }
+  V[idx] = __float2bfloat16_rn(v);
+}
+
+// B_ext[k = (j1, J), c = (a, J')] = G1[j1, a] δ(J, J')  (bf16, zero padded to ldb)
+__global__ void __launch_bounds__(256) k_build_bext(int R1, int J1, const float* __restrict__ G1,
+                                                    __nv_bfloat16* __restrict__ B, int64_t K, int64_t ldb) {
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= K * ldb) return;
+  const int64_t k = idx / ldb;
+  const int c = static_cast<int>(idx - k * ldb);
+  // [B_hi | B_hi | B_lo] against [dZ1_hi | dZ1_lo | dZ1_hi] (see k_build_v)
+  const int K2 = R1 * J1;
+  float v = 0.f;
+  if (c < 3 * K2) {
+    const int cc = c % K2;
+    const int a = cc / J1, Jp = cc % J1;
+    const int64_t j1 = k / J1;
+    const int J = static_cast<int>(k % J1);
+    if (J == Jp) v = G1[j1 * R1 + a];
+    if (c >= 2 * K2) v -= __bfloat162float(__float2bfloat16_rn(v));
+  }
+  B[idx] = __float2bfloat16_rn(v);
+}
+
+// f32 [T, K2] -> bf16 [T, ld] laid out [hi | lo | 0]: hi + lo carries ~16 mantissa bits, so the
+// bf16 extension MMA against [B | B] rounds only the constant operand.
+__global__ void __launch_bounds__(256) k_split_rows(const float* __restrict__ in, int64_t T, int K2,
+                                                    __nv_bfloat16* __restrict__ out, int64_t ld) {
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= T * ld) return;
+  const int64_t t = idx / ld;
+  const int c = static_cast<int>(idx - t * ld);
+  float v = 0.f;
+  if (c < 3 * K2) {  // [hi | lo | hi]
+    const float f = in[t * K2 + c % K2];
+    v = __bfloat162float(__float2bfloat16_rn(f));
+    if (c >= K2 && c < 2 * K2) v = f - v;
+  }
+  out[idx] = __float2bfloat16_rn(v);
+}
+
+// ---------------------------------------------------------------------------------------------
+// dy pass: for one (h, 256-column block) and a token range:
+//   dZ[t, h, c]  = Σ_col dy[t, h, col] · Gd[c, col]          (partial per column block)
+//   dGd[c, col] += Σ_t  Z[t, h, c] · dy[t, h, col]           (partial per (h, token split))
+constexpr int DY_TT = 32, DY_COLS = 256, DY_LDY = DY_COLS + 8;
+
+template <int C>
+__global__ void __launch_bounds__(256) k_tt_dy(const __nv_bfloat16* __restrict__ dy, int64_t T, int64_t N, int H,
+                                               int M, const float* __restrict__ Z, int64_t zs,
+                                               const float* __restrict__ Gd, float* __restrict__ dz_part,
+                                               float* __restrict__ dg_part, int S) {
+  static_assert(C == 8 || C == 16, "rank into the last core must be 8 or 16");
+  constexpr int NT = C / 8;
+  constexpr int KW = 8 / (2 * NT);  // warps sharing one 16 x 8 dZ output tile (split over K)
+  extern __shared__ __align__(16) uint8_t dy_smem[];
+  auto sdy = reinterpret_cast<__nv_bfloat16(*)[DY_TT][DY_LDY]>(dy_smem);
+  auto sz = reinterpret_cast<__nv_bfloat16(*)[C][DY_TT + 8]>(dy_smem + sizeof(__nv_bfloat16) * 2 * DY_TT * DY_LDY);
+  auto sg = reinterpret_cast<__nv_bfloat16(*)[DY_COLS + 8]>(dy_smem + sizeof(__nv_bfloat16) * 2 * DY_TT * DY_LDY +
+                                                             sizeof(__nv_bfloat16) * 2 * C * (DY_TT + 8));
+  auto sred = reinterpret_cast<float(*)[DY_TT][C]>(dy_smem + sizeof(__nv_bfloat16) * 2 * DY_TT * DY_LDY +
+                                                    sizeof(__nv_bfloat16) * 2 * C * (DY_TT + 8) +
+                                                    sizeof(__nv_bfloat16) * C * (DY_COLS + 8));
+
+  const int ncb = M / DY_COLS;
+  const int cb = blockIdx.x % ncb, h = blockIdx.x / ncb, s = blockIdx.y;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t col0 = static_cast<int64_t>(h) * M + static_cast<int64_t>(cb) * DY_COLS;
+  const int64_t tiles = (T + DY_TT - 1) / DY_TT;
+  const int64_t per = (tiles + S - 1) / S;
+  const int64_t tile0 = s * per, tile1 = tile0 + per < tiles ? tile0 + per : tiles;
+
+  for (int i = tid; i < C * DY_COLS; i += 256) {
+    const int c = i / DY_COLS, col = i % DY_COLS;
+    sg[c][col] = __float2bfloat16_rn(Gd[static_cast<int64_t>(c) * M + cb * DY_COLS + col]);
+  }
+
+  auto load_tile = [&](int64_t tile, int buf) {
+    const int64_t t0 = tile * DY_TT;
+    for (int i = tid; i < DY_TT * (DY_COLS / 8); i += 256) {
+      const int r = i / (DY_COLS / 8), ch = i % (DY_COLS / 8);
+      const int64_t t = t0 + r;
+      const bool ok = t < T;
+      cp_async16(&sdy[buf][r][ch * 8], dy + (ok ? t : 0) * N + col0 + ch * 8, ok);
+    }
+    for (int i = tid; i < DY_TT * C; i += 256) {
+      const int r = i / C, c = i % C;
+      const int64_t t = t0 + r;
+      sz[buf][c][r] = __float2bfloat16_rn(t < T ? Z[t * zs + static_cast<int64_t>(h) * C + c] : 0.f);
+    }
+  };
+
+  float acc2[2][NT][4];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc2[i][nt][q] = 0.f;
+
+  if (tile0 < tile1) load_tile(tile0, 0);
+  cp_async_commit();
+  const int g = lane >> 2, tq = lane & 3;
+  for (int64_t tile = tile0; tile < tile1; ++tile) {
+    const int buf = static_cast<int>((tile - tile0) & 1);
+    if (tile + 1 < tile1) load_tile(tile + 1, buf ^ 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+
+    // (1) dZ partial: warp -> (m-tile, n-tile) output tile, K (256 columns) split over KW warps
+    {
+      const int ti = warp / KW, kq = warp % KW;
+      const int mt = ti / NT, nt = ti % NT;
+      float d1[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int ks = 0; ks < 16 / KW; ++ks) {
+        const int kc = (kq * (16 / KW) + ks) * 16;
+        uint32_t b0, b1, a0, a1, a2, a3;
+        ldsm_x2(&sg[nt * 8 + (lane & 7)][kc + ((lane >> 3) & 1) * 8], b0, b1);
+        ldsm_x4(&sdy[buf][mt * 16 + (lane & 7) + ((lane >> 3) & 1) * 8][kc + (lane >> 4) * 8], a0, a1, a2, a3);
+        mma_16816(d1, a0, a1, a2, a3, b0, b1);
+      }
+      sred[kq][mt * 16 + g][nt * 8 + 2 * tq] = d1[0];
+      sred[kq][mt * 16 + g][nt * 8 + 2 * tq + 1] = d1[1];
+      sred[kq][mt * 16 + g + 8][nt * 8 + 2 * tq] = d1[2];
+      sred[kq][mt * 16 + g + 8][nt * 8 + 2 * tq + 1] = d1[3];
+    }
+
+    // (2) dGd^T[cols x C] += dy_tile^T [cols x 32 tokens] · Z [32 tokens x C]
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      uint32_t b[NT][2];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+        ldsm_x2(&sz[buf][nt * 8 + (lane & 7)][ks * 16 + ((lane >> 3) & 1) * 8], b[nt][0], b[nt][1]);
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int c0 = warp * 32 + i * 16;
+        const int q = lane >> 3;
+        uint32_t a0, a1, a2, a3;
+        ldsm_x4_t(&sdy[buf][ks * 16 + (q >> 1) * 8 + (lane & 7)][c0 + (q & 1) * 8], a0, a1, a2, a3);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) mma_16816(acc2[i][nt], a0, a1, a2, a3, b[nt][0], b[nt][1]);
+      }
+    }
+    __syncthreads();
+    for (int i = tid; i < DY_TT * C; i += 256) {
+      const int r = i / C, c = i % C;
+      float v = 0.f;
+#pragma unroll
+      for (int w = 0; w < KW; ++w) v += sred[w][r][c];
+      const int64_t t = tile * DY_TT + r;
+      if (t < T) dz_part[(static_cast<int64_t>(cb) * T + t) * (static_cast<int64_t>(H) * C) + static_cast<int64_t>(h) * C + c] = v;
+    }
+  }
+  cp_async_wait<0>();
+  // dGd partial for (h, s): element (col = c0 + g (+8), c = nt*8 + 2tq (+1))
+  float* dst = dg_part + (static_cast<int64_t>(h) * S + s) * (static_cast<int64_t>(C) * M);
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const int col = cb * DY_COLS + warp * 32 + i * 16 + g;
+      const int c = nt * 8 + 2 * tq;
+      dst[static_cast<int64_t>(c) * M + col] = acc2[i][nt][0];
+      dst[static_cast<int64_t>(c + 1) * M + col] = acc2[i][nt][1];
+      dst[static_cast<int64_t>(c) * M + col + 8] = acc2[i][nt][2];
+      dst[static_cast<int64_t>(c + 1) * M + col + 8] = acc2[i][nt][3];
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// x pass of the backward: dG1[j1, a] partial = Σ_{t in split} Σ_J x[t, j1 J1 + J] dZ1[t, a, J]
+template <typename InT, int J1, int R1>
+__global__ void __launch_bounds__(256) k_tt_dg1(const InT* __restrict__ x, int64_t T, int64_t K,
+                                                const float* __restrict__ dz1, float* __restrict__ part, int S) {
+  constexpr int K2 = J1 * R1;
+  constexpr int E = J1 == 1 ? 4 : 8;  // x elements per thread
+  constexpr int NJ = E / J1;
+  constexpr int TB = 32;
+  __shared__ __align__(16) float sdz[TB][K2];
+  const int64_t col0 = (static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x) * E;
+  const bool active = col0 < K;
+  const int s = blockIdx.y;
+  const int64_t per = (T + S - 1) / S;
+  const int64_t t0 = s * per, t1 = t0 + per < T ? t0 + per : T;
+  float acc[NJ][R1];
+#pragma unroll
+  for (int j = 0; j < NJ; ++j)
+#pragma unroll
+    for (int a = 0; a < R1; ++a) acc[j][a] = 0.f;
+  for (int64_t tb = t0; tb < t1; tb += TB) {
+    const int nt = static_cast<int>(t1 - tb < TB ? t1 - tb : TB);
+    __syncthreads();
+    for (int i = threadIdx.x; i < nt * K2; i += 256) sdz[i / K2][i % K2] = dz1[(tb + i / K2) * K2 + i % K2];
+    __syncthreads();
+    if (!active) continue;
+    constexpr int UNR = 4;  // token rows of x in flight per thread
+    for (int r0 = 0; r0 < nt; r0 += UNR) {
+      float f[UNR][8];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        if (r0 + u < nt) {
+          if (E == 8) {
+            load8<InT>(x + (tb + r0 + u) * K + col0, f[u]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) f[u][i] = to_f32(x[(tb + r0 + u) * K + col0 + i]);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        if (r0 + u >= nt) break;
+#pragma unroll
+        for (int j = 0; j < NJ; ++j)
+#pragma unroll
+          for (int J = 0; J < J1; ++J) {
+            const float xv = f[u][j * J1 + J];
+#pragma unroll
+            for (int a = 0; a < R1; ++a) acc[j][a] = fmaf(xv, sdz[r0 + u][a * J1 + J], acc[j][a]);
+          }
+      }
+    }
+  }
+  if (!active) return;
+  const int64_t n1 = K / J1;
+  float* dst = part + static_cast<int64_t>(s) * n1 * R1;
+#pragma unroll
+  for (int j = 0; j < NJ; ++j)
+#pragma unroll
+    for (int a = 0; a < R1; ++a) dst[(col0 / J1 + j) * R1 + a] = acc[j][a];
+}
+
+// ---------------------------------------------------------------------------------------------
+// Middle core (d = 3) as register-tiled small GEMMs over token tiles of 64.  G2 [R1][H][J1][C]
+// is gathered once per CTA into shared memory as the dense matrix Gm[aj][hc] (aj = a*J1 + j2,
+// hc = i2*C + b), or its transpose.
+//   fwd : Z2 = Z1 · Gm                 [T, HC]
+//   bwd : dZ1 = dZ2 · Gmᵀ              [T, K2]   and   dG2 (+)= Z1ᵀ · dZ2 (per-CTA partial)
+constexpr int MID_TT = 64, MID_LD = MID_TT + 4;
+
+QA_DEV int g2_index(int aj, int hc, int J1, int C, int HC) {
+  const int a = aj / J1, j2 = aj % J1, i2 = hc / C, b = hc % C;
+  return ((a * (HC / C) + i2) * J1 + j2) * C + b;
+}
+
+__global__ void __launch_bounds__(256) k_mid_fwd(const float* __restrict__ z1, int64_t T, int K2, int J1, int HC,
+                                                 int C, const float* __restrict__ G2, float* __restrict__ z2) {
+  extern __shared__ __align__(16) float mid_smem[];
+  float* gm = mid_smem;                  // [K2][HC]
+  float* zt = mid_smem + K2 * HC;        // [K2][MID_LD]  (Z1 tile, transposed)
+  for (int i = threadIdx.x; i < K2 * HC; i += 256) gm[i] = G2[g2_index(i / HC, i % HC, J1, C, HC)];
+  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * MID_TT;
+  const int nt = static_cast<int>(T - t0 < MID_TT ? T - t0 : MID_TT);
+  for (int i = threadIdx.x; i < MID_TT * K2; i += 256) {
+    const int r = i / K2, aj = i % K2;
+    zt[aj * MID_LD + r] = r < nt ? z1[(t0 + r) * K2 + aj] : 0.f;
+  }
+  __syncthreads();
+  const int ntile = (MID_TT / 4) * (HC / 4);
+  for (int mt = threadIdx.x; mt < ntile; mt += 256) {
+    const int r0 = (mt % (MID_TT / 4)) * 4, c0 = (mt / (MID_TT / 4)) * 4;
+    float acc[4][4] = {};
+    for (int aj = 0; aj < K2; ++aj) {
+      const float4 zv = *reinterpret_cast<const float4*>(zt + aj * MID_LD + r0);
+      const float4 gv = *reinterpret_cast<const float4*>(gm + aj * HC + c0);
+      const float zz[4] = {zv.x, zv.y, zv.z, zv.w}, gg[4] = {gv.x, gv.y, gv.z, gv.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(zz[i], gg[j], acc[i][j]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (r0 + i < nt)
+        *reinterpret_cast<float4*>(z2 + (t0 + r0 + i) * HC + c0) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+  }
+}
+
+template <int MAXT>  // dG2 micro-tiles (4 x 4) per thread
+__global__ void __launch_bounds__(256) k_mid_bwd(const float* __restrict__ dz2, const float* __restrict__ z1,
+                                                 int64_t T, int K2, int J1, int HC, int C,
+                                                 const float* __restrict__ G2, float* __restrict__ dz1,
+                                                 float* __restrict__ gpart, int tiles_per_cta) {
+  extern __shared__ __align__(16) float mid_smem[];
+  float* gt = mid_smem;                        // [HC][K2]
+  float* dt = mid_smem + HC * K2;              // [HC][MID_LD]  dZ2 tile, transposed
+  float* zt = dt + HC * MID_LD;                // [K2][MID_LD]  Z1 tile, transposed
+  for (int i = threadIdx.x; i < K2 * HC; i += 256) gt[i] = G2[g2_index(i % K2, i / K2, J1, C, HC)];
+  const bool want_g = gpart != nullptr;
+  const int gtiles = (K2 / 4) * (HC / 4);
+  float gacc[MAXT][4][4];
+#pragma unroll
+  for (int u = 0; u < MAXT; ++u)
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) gacc[u][i][j] = 0.f;
+  for (int tile = 0; tile < tiles_per_cta; ++tile) {
+    const int64_t t0 = (static_cast<int64_t>(blockIdx.x) * tiles_per_cta + tile) * MID_TT;
+    if (t0 >= T) break;
+    const int nt = static_cast<int>(T - t0 < MID_TT ? T - t0 : MID_TT);
+    __syncthreads();
+    for (int i = threadIdx.x; i < MID_TT * HC; i += 256) {
+      const int r = i / HC, hc = i % HC;
+      dt[hc * MID_LD + r] = r < nt ? dz2[(t0 + r) * HC + hc] : 0.f;
+    }
+    if (want_g)
+      for (int i = threadIdx.x; i < MID_TT * K2; i += 256) {
+        const int r = i / K2, aj = i % K2;
+        zt[aj * MID_LD + r] = r < nt ? z1[(t0 + r) * K2 + aj] : 0.f;
+      }
+    __syncthreads();
+    // dZ1 tile [64 x K2]: micro-tile 4 tokens x 4 aj
+    for (int mt = threadIdx.x; mt < (MID_TT / 4) * (K2 / 4); mt += 256) {
+      const int r0 = (mt % (MID_TT / 4)) * 4, c0 = (mt / (MID_TT / 4)) * 4;
+      float acc[4][4] = {};
+      for (int hc = 0; hc < HC; ++hc) {
+        const float4 dv = *reinterpret_cast<const float4*>(dt + hc * MID_LD + r0);
+        const float4 gv = *reinterpret_cast<const float4*>(gt + hc * K2 + c0);
+        const float dd[4] = {dv.x, dv.y, dv.z, dv.w}, gg[4] = {gv.x, gv.y, gv.z, gv.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(dd[i], gg[j], acc[i][j]);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (r0 + i < nt)
+          *reinterpret_cast<float4*>(dz1 + (t0 + r0 + i) * K2 + c0) =
+              make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+    }
+    // dG2 partial [K2 x HC] += Z1ᵀ · dZ2 over this tile's tokens: micro-tile 4 aj x 4 hc
+    if (want_g) {
+#pragma unroll
+      for (int u = 0; u < MAXT; ++u) {
+        const int mt = threadIdx.x + 256 * u;
+        if (mt >= gtiles) break;
+        const int a0 = (mt % (K2 / 4)) * 4, h0 = (mt / (K2 / 4)) * 4;
+        for (int r = 0; r < MID_TT; r += 4) {
+          float4 zv[4], dv[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) zv[i] = *reinterpret_cast<const float4*>(zt + (a0 + i) * MID_LD + r);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dv[j] = *reinterpret_cast<const float4*>(dt + (h0 + j) * MID_LD + r);
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              gacc[u][i][j] = fmaf(zv[i].x, dv[j].x,
+                                   fmaf(zv[i].y, dv[j].y, fmaf(zv[i].z, dv[j].z, fmaf(zv[i].w, dv[j].w, gacc[u][i][j]))));
+        }
+      }
+    }
+  }
+  if (want_g) {
+    const int numel = K2 * HC;
+#pragma unroll
+    for (int u = 0; u < MAXT; ++u) {
+      const int mt = threadIdx.x + 256 * u;
+      if (mt >= gtiles) break;
+      const int a0 = (mt % (K2 / 4)) * 4, h0 = (mt / (K2 / 4)) * 4;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          gpart[static_cast<int64_t>(blockIdx.x) * numel + g2_index(a0 + i, h0 + j, J1, C, HC)] = gacc[u][i][j];
+    }
+  }
+}
+
+}  // namespace
+
+size_t mid_fwd_smem(int K2, int HC) { return sizeof(float) * (size_t(K2) * HC + size_t(K2) * MID_LD); }
+size_t mid_bwd_smem(int K2, int HC) {
+  return sizeof(float) * (size_t(K2) * HC + size_t(HC) * MID_LD + size_t(K2) * MID_LD);
+}
+
+bool mid_fast_ok(int K2, int HC) {
+  return K2 % 4 == 0 && HC % 4 == 0 && (K2 / 4) * (HC / 4) <= 256 * 4 && mid_bwd_smem(K2, HC) <= 200 * 1024;
+}
+
+int mid_bwd_ctas(int64_t T) {
+  const int64_t tiles = (T + MID_TT - 1) / MID_TT;
+  return static_cast<int>(tiles < 148 ? (tiles > 0 ? tiles : 1) : 148);
+}
+
+cudaError_t launch_mid_fwd(const float* z1, int64_t T, int K2, int J1, int HC, int C, const float* G2, float* z2,
+                           cudaStream_t s) {
+  if (T == 0) return cudaSuccess;
+  LaunchScope scope(kTT, 2.0 * double(T) * K2 * HC, s);
+  count_launches(1);
+  const unsigned grid = static_cast<unsigned>((T + MID_TT - 1) / MID_TT);
+  const size_t smem = mid_fwd_smem(K2, HC);
+  cudaFuncSetAttribute(k_mid_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  k_mid_fwd<<<grid, 256, smem, s>>>(z1, T, K2, J1, HC, C, G2, z2);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mid_bwd(const float* dz2, const float* z1, int64_t T, int K2, int J1, int HC, int C,
+                           const float* G2, float* dz1, float* gpart, int nctas, cudaStream_t s) {
+  if (T == 0) return cudaSuccess;
+  LaunchScope scope(kTT, 2.0 * double(T) * K2 * HC * (gpart ? 2 : 1), s);
+  count_launches(1);
+  const int64_t tiles = (T + MID_TT - 1) / MID_TT;
+  const int per = static_cast<int>((tiles + nctas - 1) / nctas);
+  const size_t smem = mid_bwd_smem(K2, HC);
+  const int gtiles = (K2 / 4) * (HC / 4);
+#define QA_MB(U)                                                                                                    cudaFuncSetAttribute(k_mid_bwd<U>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));        k_mid_bwd<U><<<static_cast<unsigned>(nctas), 256, smem, s>>>(dz2, z1, T, K2, J1, HC, C, G2, dz1, gpart, per)
+  if (gtiles <= 256) {
+    QA_MB(1);
+  } else if (gtiles <= 512) {
+    QA_MB(2);
+  } else {
+    QA_MB(4);
+  }
+#undef QA_MB
+  return cudaGetLastError();
+}
+
+bool fast_tt_supported(int J1, int R1) {
+  return (J1 == 1 && (R1 == 8 || R1 == 16)) || (J1 == 4 && (R1 == 8 || R1 == 16));
+}
+
+size_t g1i_floats(int64_t K, int J1, int R1) {
+  const int64_t nvec = K / 8;
+  return static_cast<size_t>(((nvec + 31) / 32) * 32) * 8 * R1 / J1;
+}
+
+cudaError_t launch_actquant_z1(const void* x, int x_dtype, int64_t T, int64_t K, bool want_codes, uint8_t* codes,
+                               int64_t ldc, float* sx, float* ox, int32_t* rsx, const float* G1, int J1, int R1,
+                               __nv_bfloat16* zb, int64_t ldzb, float* zf, float* g1i_ws, cudaStream_t s) {
+  if (T == 0) return cudaSuccess;
+  const int64_t nvec = K / 8;
+  {
+    const int64_t n = nvec * (2 * R1 / J1);
+    LaunchScope scope(kTT, double(n) * 32, s);
+    count_launches(1);
+    const unsigned g = static_cast<unsigned>((n + 255) / 256);
+    float4* G1i = reinterpret_cast<float4*>(g1i_ws);
+    if (J1 == 1 && R1 == 8)
+      k_g1_interleave<1, 8><<<g, 256, 0, s>>>(G1, G1i, nvec);
+    else if (J1 == 1 && R1 == 16)
+      k_g1_interleave<1, 16><<<g, 256, 0, s>>>(G1, G1i, nvec);
+    else if (J1 == 4 && R1 == 8)
+      k_g1_interleave<4, 8><<<g, 256, 0, s>>>(G1, G1i, nvec);
+    else
+      k_g1_interleave<4, 16><<<g, 256, 0, s>>>(G1, G1i, nvec);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  const float4* G1i = reinterpret_cast<const float4*>(g1i_ws);
+  const size_t esz = x_dtype == QA_F32 ? 4 : 2;
+  LaunchScope scope(kQuantize, double(T) * K * esz + (want_codes ? double(T) * ldc + 12.0 * T : 0.0) +
+                                   double(T) * (zb ? ldzb * 2 : 0) + double(T) * (zf ? J1 * R1 * 4 : 0),
+                    s);
+  count_launches(1);
+  const dim3 grid(static_cast<unsigned>((T + 7) / 8));  // 8 warps = 8 token rows per CTA
+#define QA_AQ(TI, JJ, RR)                                                                                           \
+  if (want_codes)                                                                                                   \
+    k_actquant_z1<TI, JJ, RR, true><<<grid, 256, 0, s>>>(static_cast<const TI*>(x), T, K, codes, ldc, sx, ox, rsx,  \
+                                                         G1i, zb, ldzb, zf);                                        \
+  else                                                                                                              \
+    k_actquant_z1<TI, JJ, RR, false><<<grid, 256, 0, s>>>(static_cast<const TI*>(x), T, K, codes, ldc, sx, ox, rsx, \
+                                                          G1i, zb, ldzb, zf);
+#define QA_AQ_T(TI)                  \
+  if (J1 == 1 && R1 == 8) {          \
+    QA_AQ(TI, 1, 8)                  \
+  } else if (J1 == 1 && R1 == 16) {  \
+    QA_AQ(TI, 1, 16)                 \
+  } else if (J1 == 4 && R1 == 8) {   \
+    QA_AQ(TI, 4, 8)                  \
+  } else {                           \
+    QA_AQ(TI, 4, 16)                 \
+  }
+  if (x_dtype == QA_F32) {
+    QA_AQ_T(float)
+  } else {
+    QA_AQ_T(__nv_bfloat16)
+  }
+#undef QA_AQ_T
+#undef QA_AQ
+  return cudaGetLastError();
+}
+
+cudaError_t launch_build_v(int d, int R1, int H, int J1, int C, int M, const float* G2, const float* G3,
+                           __nv_bfloat16* V, int64_t N, int64_t ldv, cudaStream_t s) {
+  const int64_t total = N * ldv;
+  LaunchScope scope(kTT, double(total) * 2 + double(N) * R1 * J1 * C * 2, s);
+  count_launches(1);
+  k_build_v<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(d, R1, H, J1, C, M, G2, G3, V, N, ldv);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_build_bext(int R1, int J1, const float* G1, __nv_bfloat16* B, int64_t K, int64_t ldb,
+                              cudaStream_t s) {
+  const int64_t total = K * ldb;
+  LaunchScope scope(kTT, double(total) * 2, s);
+  count_launches(1);
+  k_build_bext<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(R1, J1, G1, B, K, ldb);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_split_rows(const float* in, int64_t T, int K2, __nv_bfloat16* out, int64_t ld, cudaStream_t s) {
+  const int64_t total = T * ld;
+  if (total == 0) return cudaSuccess;
+  LaunchScope scope(kTT, double(T) * K2 * 4 + double(total) * 2, s);
+  count_launches(1);
+  k_split_rows<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(in, T, K2, out, ld);
+  return cudaGetLastError();
+}
+
+int tt_dy_splits(int64_t T, int blocks_per_split) {
+  const int64_t tiles = (T + DY_TT - 1) / DY_TT;
+  int64_t S = (4 * 148 + blocks_per_split - 1) / blocks_per_split;  // ~4 resident CTAs per SM
+  if (S > tiles) S = tiles;
+  return static_cast<int>(S < 1 ? 1 : S);
+}
+
+cudaError_t launch_tt_dy(const __nv_bfloat16* dy, int64_t T, int64_t N, int H, int M, const float* Z, int64_t zs,
+                         int C, const float* Gd, float* dz_part, float* dg_part, int S, cudaStream_t s) {
+  if (T == 0) return cudaSuccess;
+  LaunchScope scope(kTT, 4.0 * double(T) * N * C, s);
+  count_launches(1);
+  const dim3 grid(static_cast<unsigned>((M / DY_COLS) * H), static_cast<unsigned>(S));
+  const size_t smem = sizeof(__nv_bfloat16) * (2 * DY_TT * DY_LDY + 2 * C * (DY_TT + 8) + C * (DY_COLS + 8)) +
+                      sizeof(float) * (8 / (2 * (C / 8))) * DY_TT * C;
+  static bool attr8 = false, attr16 = false;
+  if (C == 8) {
+    if (!attr8) cudaFuncSetAttribute(k_tt_dy<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    attr8 = true;
+    k_tt_dy<8><<<grid, 256, smem, s>>>(dy, T, N, H, M, Z, zs, Gd, dz_part, dg_part, S);
+  } else {
+    if (!attr16) cudaFuncSetAttribute(k_tt_dy<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    attr16 = true;
+    k_tt_dy<16><<<grid, 256, smem, s>>>(dy, T, N, H, M, Z, zs, Gd, dz_part, dg_part, S);
+  }
+  return cudaGetLastError();
+}
+
+int tt_dg1_splits(int64_t T, int64_t K, int J1) {
+  const int E = J1 == 1 ? 4 : 8;
+  const int64_t gx = (K + 256 * E - 1) / (256 * E);
+  int64_t S = (2 * 148 + gx - 1) / gx;
+  if (S > T) S = T;
+  return static_cast<int>(S < 1 ? 1 : S);
+}
+
+cudaError_t launch_tt_dg1(const void* x, int x_dtype, int64_t T, int64_t K, const float* dz1, int J1, int R1,
+                          float* part, int S, cudaStream_t s) {
+  if (T == 0) return cudaSuccess;
+  LaunchScope scope(kTT, 2.0 * double(T) * K * R1, s);
+  count_launches(1);
+  const int E = J1 == 1 ? 4 : 8;
+  const dim3 grid(static_cast<unsigned>((K + 256 * E - 1) / (256 * E)), static_cast<unsigned>(S));
+#define QA_DG(TI, JJ, RR) \
+  k_tt_dg1<TI, JJ, RR><<<grid, 256, 0, s>>>(static_cast<const TI*>(x), T, K, dz1, part, S)
+#define QA_DG_T(TI)                 \
+  if (J1 == 1 && R1 == 8)           \
+    QA_DG(TI, 1, 8);                \
+  else if (J1 == 1 && R1 == 16)     \
+    QA_DG(TI, 1, 16);               \
+  else if (J1 == 4 && R1 == 8)      \
+    QA_DG(TI, 4, 8);                \
+  else                              \
+    QA_DG(TI, 4, 16);
+  if (x_dtype == QA_F32) {
+    QA_DG_T(float)
+  } else {
+    QA_DG_T(__nv_bfloat16)
+  }
+#undef QA_DG_T
+#undef QA_DG
+  return cudaGetLastError();
+}
+
+}  // namespace qa

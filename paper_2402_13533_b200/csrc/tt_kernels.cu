@@ -148,14 +148,36 @@ __global__ void __launch_bounds__(256) k_core_grad_partial(const InT* __restrict
   partial[static_cast<int64_t>(chunk) * numel + g] = acc;
 }
 
-// Phase 2: fixed-order sum over chunks.
+// Phase 2: fixed-order sum over chunks.  A block owns 32 consecutive outputs; warp w sums chunks
+// w, w+8, ... (lane = output), then lanes combine the 8 warp sums in warp order.
 __global__ void __launch_bounds__(256) k_core_grad_reduce(const float* __restrict__ partial, int nchunks,
                                                           int64_t numel, float* __restrict__ dG, int accumulate) {
-  const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (g >= numel) return;
+  __shared__ float red[8][33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t g = static_cast<int64_t>(blockIdx.x) * 32 + lane;
   float s = 0.f;
-  for (int c = 0; c < nchunks; ++c) s += partial[static_cast<int64_t>(c) * numel + g];
-  dG[g] = accumulate ? dG[g] + s : s;
+  if (g < numel) {
+    int c = warp;
+    for (; c + 24 < nchunks; c += 32) {  // 4 independent loads in flight
+      const float a0 = partial[static_cast<int64_t>(c) * numel + g];
+      const float a1 = partial[static_cast<int64_t>(c + 8) * numel + g];
+      const float a2 = partial[static_cast<int64_t>(c + 16) * numel + g];
+      const float a3 = partial[static_cast<int64_t>(c + 24) * numel + g];
+      s += a0;
+      s += a1;
+      s += a2;
+      s += a3;
+    }
+    for (; c < nchunks; c += 8) s += partial[static_cast<int64_t>(c) * numel + g];
+  }
+  red[warp][lane] = s;
+  __syncthreads();
+  if (warp == 0 && g < numel) {
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += red[w][lane];
+    dG[g] = accumulate ? dG[g] + t : t;
+  }
 }
 
 // L[ip, jp, b] = (G_0 ··· G_{d-2})[ip, jp, b]; one thread per element, chain of small vector-matrix products.
@@ -274,6 +296,16 @@ cudaError_t launch_tt_stage_bwd(const void* dout, int dout_dtype, int64_t dout_l
   return cudaGetLastError();
 }
 
+cudaError_t launch_sum_partials(const float* partial, int nparts, int64_t numel, float* out, bool accumulate,
+                                cudaStream_t s) {
+  if (numel == 0) return cudaSuccess;
+  LaunchScope scope(kTT, 4.0 * double(numel) * (nparts + 1), s);
+  count_launches(1);
+  k_core_grad_reduce<<<static_cast<unsigned>((numel + 31) / 32), 256, 0, s>>>(partial, nparts, numel, out,
+                                                                                accumulate ? 1 : 0);
+  return cudaGetLastError();
+}
+
 int tt_grad_chunks(int64_t T) { return static_cast<int>(T < 296 ? (T > 0 ? T : 1) : 296); }
 
 cudaError_t launch_tt_core_grad(const void* in, int in_dtype, int64_t in_ld, const void* dout, int dout_dtype,
@@ -297,7 +329,7 @@ cudaError_t launch_tt_core_grad(const void* in, int in_dtype, int64_t in_ld, con
 #undef QA_CG
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  k_core_grad_reduce<<<static_cast<unsigned>((numel + 255) / 256), 256, 0, s>>>(partial, nchunks, numel, dG,
+  k_core_grad_reduce<<<static_cast<unsigned>((numel + 31) / 32), 256, 0, s>>>(partial, nchunks, numel, dG,
                                                                                 accumulate ? 1 : 0);
   return cudaGetLastError();
 }

@@ -98,11 +98,12 @@ class TTSpec:
     @staticmethod
     def for_shape(fan_out: int, fan_in: int, r: int) -> "TTSpec":
         """Pinned modes (DESIGN.md §TT modes): BASELINE config 1 is balanced (4,16,16)²;
-        Llama shapes use m = (1, N/256, 256), n = (K/16, 4, 4)."""
+        Llama shapes use m = (1, N/256, 256), n = (K/4, 4, 1): first core input-only, last core
+        output-only, so every contraction touching x or dy has rank r on its small side."""
         if fan_out == 1024 and fan_in == 1024:
             return TTSpec((4, 16, 16), (4, 16, 16), (1, r, r, 1))
-        if fan_out % 256 == 0 and fan_in % 16 == 0:
-            return TTSpec((1, fan_out // 256, 256), (fan_in // 16, 4, 4), (1, r, r, 1))
+        if fan_out % 256 == 0 and fan_in % 4 == 0:
+            return TTSpec((1, fan_out // 256, 256), (fan_in // 4, 4, 1), (1, r, r, 1))
         raise ModelError(f"no pinned TT modes for {fan_out}x{fan_in}; pass a TTSpec")
 
     @staticmethod

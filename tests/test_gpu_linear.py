@@ -43,12 +43,18 @@ def _case(N, K, T, bits, r, seed, spec=None, xdtype=torch.bfloat16):
 
 
 CASES = [
-    # (N, K, T, bits, r, spec)  — config 1 and ragged / padded / int4 shapes
+    # (N, K, T, bits, r, spec)
+    # generic TT path: config 1 (balanced modes), ragged / padded / int4 shapes
     (1024, 1024, 512, 8, 8, None),
     (1024, 1024, 512, 4, 8, None),
     (512, 768, 77, 8, 4, L.TTSpec((1, 2, 256), (48, 4, 4), (1, 4, 4, 1))),
     (320, 200, 130, 4, 3, L.TTSpec((4, 80), (20, 10), (1, 3, 1))),
+    # fast TT family (first core input-only, last core output-only): pinned Llama modes and LoRA
     (256, 4096, 300, 8, 8, None),
+    (4096, 1024, 200, 8, 16, None),
+    (2048, 512, 97, 4, 8, None),
+    (1024, 512, 150, 8, 8, L.TTSpec.lora(1024, 512, 8)),
+    (768, 256, 64, 4, 16, L.TTSpec.lora(768, 256, 16)),
 ]
 
 
@@ -188,8 +194,8 @@ def test_full_size_properties():
     out = L.linear_forward(q, (spec, cores), x, debug=True)
     qx = qa.quantize_rows(x, 8)
     rows = torch.randint(0, T, (64,), device="cuda")
-    cx = qx.codes[rows].long()
-    exact = cx @ q.codes.long().t()
+    cx = qx.codes[rows].double()
+    exact = (cx @ q.codes.double().t()).long()  # fp64 is exact below 2^53
     assert torch.equal(exact, out["acc"][rows].long())
     oq = O.quantize_rows(W.cpu().numpy(), 8)
     cores_np = [c.cpu().numpy() for c in cores]
