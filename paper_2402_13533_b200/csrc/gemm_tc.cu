@@ -15,6 +15,8 @@
 // swizzled K-major tiles; extension k-blocks travel through the same ring), warp 0 = TMA
 // producer, warp 1 = single-thread MMA issuer, warp 2 = TMEM allocator, warps 4..7 = epilogue
 // (TMEM lane quarter = warp % 4).
+#include <stdlib.h>
+
 #include <mutex>
 
 #include "qa_common.cuh"
@@ -280,6 +282,604 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Persistent variant (production path): one CTA per SM walks tiles t = blockIdx.x + i * gridDim.x
+// (n-fastest, so concurrently running tiles share A rows and B stays L2-resident).  The TMA ring
+// runs continuously across tiles and the TMEM accumulator is double-buffered (2 x 256 columns), so
+// tile i's epilogue overlaps tile i+1's main loop.
+//   kind 1: extension k-blocks accumulate into the same buffer inside the k-loop.
+//   kind 0: the y2 extension is folded in place — the epilogue converts the s32 accumulator to fp32
+//           y1 and stores it back into TMEM (pass A), the MMA thread then runs the bf16 extension
+//           MMAs of tile i on top of it (ring order M0 M1 E0 M2 E1 ...), and pass B reads y1 + y2.
+template <int KIND>
+__global__ void __launch_bounds__(THREADS, 1)
+    k_gemm_tc_p(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2, const KParams p) {
+  constexpr uint32_t TMEM_COLS = 512;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_BYTES;
+  float* colA = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES);
+  float* colB = colA + BN;
+  float* colC = colB + BN;
+  int32_t* colD = reinterpret_cast<int32_t*>(colC + BN);
+  uint64_t* full = reinterpret_cast<uint64_t*>(colD + BN);
+  uint64_t* empty = full + STAGES;
+  uint64_t* acc_full = empty + STAGES;  // [2]
+  uint64_t* y1_ready = acc_full + 2;    // [2]
+  uint64_t* y_full = y1_ready + 2;      // [2]
+  uint64_t* tmem_empty = y_full + 2;    // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+
+  const uint32_t warp = warp_id_sync();
+  const uint32_t lane = lane_id();
+  constexpr int ELEM_BYTES = KIND == 0 ? 1 : 2;
+  constexpr int BK = BK_BYTES / ELEM_BYTES;
+  const int num_main = static_cast<int>((p.K + BK - 1) / BK);
+  const int num_ext = p.num_ext;
+  const int64_t n_tn = (p.N + BN - 1) / BN;
+  const int64_t total = ((p.M + BM - 1) / BM) * n_tn;
+  const int my_tiles =
+      blockIdx.x < total ? static_cast<int>((total - blockIdx.x + gridDim.x - 1) / gridDim.x) : 0;
+  auto coords = [&](int i, int64_t& m0, int64_t& n0) {
+    const int64_t t = blockIdx.x + static_cast<int64_t>(i) * gridDim.x;
+    m0 = (t / n_tn) * BM;
+    n0 = (t % n_tn) * BN;
+  };
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    if (num_ext > 0) {
+      tma_prefetch_desc(&tmA2);
+      tma_prefetch_desc(&tmB2);
+    }
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&y1_ready[b], 4);
+      mbar_init(&y_full[b], 1);
+      mbar_init(&tmem_empty[b], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const bool fold_ext = KIND == 0 && num_ext > 0;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      uint32_t q = 0;
+      auto load = [&](const CUtensorMap* ta, const CUtensorMap* tb, int kcoord, int64_t m0, int64_t n0) {
+        const int s = q % STAGES;
+        mbar_wait(&empty[s], ((q / STAGES) & 1) ^ 1);
+        mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+        tma_load_2d(sA + s * A_BYTES, ta, &full[s], kcoord, static_cast<int32_t>(m0));
+        tma_load_2d(sB + s * B_BYTES, tb, &full[s], kcoord, static_cast<int32_t>(n0));
+        ++q;
+      };
+      for (int i = 0; i < my_tiles; ++i) {
+        int64_t m0, n0;
+        coords(i, m0, n0);
+        for (int kb = 0; kb < num_main; ++kb) load(&tmA, &tmB, kb * BK, m0, n0);
+        if (KIND == 1) {
+          for (int e = 0; e < num_ext; ++e) load(&tmA2, &tmB2, e * 64, m0, n0);
+        } else if (fold_ext && i > 0) {
+          coords(i - 1, m0, n0);
+          for (int e = 0; e < num_ext; ++e) load(&tmA2, &tmB2, e * 64, m0, n0);
+        }
+      }
+      if (fold_ext && my_tiles > 0) {
+        int64_t m0, n0;
+        coords(my_tiles - 1, m0, n0);
+        for (int e = 0; e < num_ext; ++e) load(&tmA2, &tmB2, e * 64, m0, n0);
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (one thread)
+    if (lane == 0) {
+      constexpr uint32_t idesc = KIND == 0 ? make_idesc(2, 0, 0, BM, BN) : make_idesc(1, 1, 1, BM, BN);
+      constexpr uint32_t idesc_ext = make_idesc(1, 1, 1, BM, BN);
+      uint32_t q = 0;
+      auto block = [&](uint32_t dcol, bool ext, bool first) {
+        const int s = q % STAGES;
+        mbar_wait(&full[s], (q / STAGES) & 1);
+        tc_fence_after();
+        const uint64_t a0 = smem_desc_kmajor_sw128(sA + s * A_BYTES);
+        const uint64_t b0 = smem_desc_kmajor_sw128(sB + s * B_BYTES);
+#pragma unroll
+        for (int k = 0; k < BK_BYTES / 32; ++k) {
+          const uint64_t adv = static_cast<uint64_t>((k * 32) >> 4);
+          const uint32_t acc = (first && k == 0) ? 0u : 1u;
+          if (!ext && KIND == 0)
+            mma_i8(dcol, a0 + adv, b0 + adv, idesc, acc);
+          else
+            mma_f16(dcol, a0 + adv, b0 + adv, ext ? idesc_ext : idesc, acc);
+        }
+        mma_commit(&empty[s]);
+        ++q;
+      };
+      auto fold = [&](int i) {  // kind 0: y2 MMAs of tile i onto its fp32 y1
+        const uint32_t pb = i & 1;
+        mbar_wait(&y1_ready[pb], (i >> 1) & 1);
+        tc_fence_after();
+        for (int e = 0; e < num_ext; ++e) block(tmem_base + pb * 256, true, false);
+        mma_commit(&y_full[pb]);
+      };
+      for (int i = 0; i < my_tiles; ++i) {
+        const uint32_t b = i & 1;
+        mbar_wait(&tmem_empty[b], ((i >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + b * 256;
+        for (int kb = 0; kb < num_main; ++kb) block(d, false, kb == 0);
+        if (KIND == 1)
+          for (int e = 0; e < num_ext; ++e) block(d, true, false);
+        mma_commit(&acc_full[b]);
+        if (fold_ext && i > 0) fold(i - 1);
+      }
+      if (fold_ext && my_tiles > 0) fold(my_tiles - 1);
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue
+    const int et = static_cast<int>(threadIdx.x) - 128;
+    const GemmEpilogue& e = p.e;
+    const uint32_t quarter = warp & 3u;
+    const uint32_t lane_base = (quarter * 32u) << 16;
+    const bool vec_out = e.out_bf16 != nullptr && (e.ld_out % 8 == 0) &&
+                         (reinterpret_cast<uintptr_t>(e.out_bf16) % 16 == 0);
+    for (int i = 0; i < my_tiles; ++i) {
+      const uint32_t b = i & 1, ph = (i >> 1) & 1;
+      const uint32_t d = tmem_base + lane_base + b * 256;
+      int64_t m0, n0;
+      coords(i, m0, n0);
+      const int64_t row = m0 + quarter * 32 + lane;
+      const bool row_ok = row < p.M;
+      float sx = 0.f, ox = 0.f, rsxc = 0.f;
+      int32_t ibase = 0;
+      if (KIND == 0) {
+        named_bar_sync(1, 128);  // previous tile's pass A is done with the column terms
+        const float kf = static_cast<float>(e.k_real);
+        for (int c = et; c < BN; c += 128) {
+          const int64_t n = n0 + c;
+          if (n < p.N) {
+            const float sw = e.col_scale[n];
+            const float ow = e.col_offset[n] + static_cast<float>(e.zp_col) * sw;
+            const int32_t rs = e.col_sum[n];
+            colA[c] = sw;
+            colB[c] = ow;
+            colC[c] = fmaf(sw, static_cast<float>(rs - e.zp_col * e.k_real), kf * ow);
+            colD[c] = e.zp_row * rs;
+          } else {
+            colA[c] = 0.f;
+            colB[c] = 0.f;
+            colC[c] = 0.f;
+            colD[c] = 0;
+          }
+        }
+        named_bar_sync(1, 128);
+        if (row_ok) {
+          sx = e.row_scale[row];
+          ox = e.row_offset[row] + static_cast<float>(e.zp_row) * sx;
+          const int32_t rsx = e.row_sum[row];
+          rsxc = static_cast<float>(rsx - e.zp_row * e.k_real);
+          ibase = e.zp_row * e.zp_col * e.k_real - e.zp_col * rsx;
+        }
+        mbar_wait(&acc_full[b], ph);
+        tc_fence_after();
+        if (fold_ext) {
+          // pass A: s32 -> fp32 y1 in place
+#pragma unroll 1
+          for (int chunk = 0; chunk < BN / 32; ++chunk) {
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(d + chunk * 32u, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const int c = chunk * 32 + j;
+              const int32_t accc = static_cast<int32_t>(v[j]) + ibase - colD[c];
+              v[j] = __float_as_uint(fmaf(sx, fmaf(colA[c], static_cast<float>(accc), colB[c] * rsxc), ox * colC[c]));
+            }
+            tmem_st_32x32b_x32(d + chunk * 32u, v);
+          }
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&y1_ready[b]);
+          mbar_wait(&y_full[b], ph);
+          tc_fence_after();
+        }
+      } else {
+        mbar_wait(&acc_full[b], ph);
+        tc_fence_after();
+      }
+      // pass B: drain the buffer into registers (bf16 pairs), release TMEM, then store
+      uint32_t packed[BN / 2];
+#pragma unroll
+      for (int chunk = 0; chunk < BN / 32; ++chunk) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(d + chunk * 32u, v);
+        tmem_ld_wait();
+        float y[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          if (KIND == 0 && !fold_ext) {  // no adapter: dequantise the s32 accumulator here
+            const int c = chunk * 32 + j;
+            const int32_t accc = static_cast<int32_t>(v[j]) + ibase - colD[c];
+            y[j] = fmaf(sx, fmaf(colA[c], static_cast<float>(accc), colB[c] * rsxc), ox * colC[c]);
+          } else {
+            y[j] = __uint_as_float(v[j]);
+          }
+        }
+        const int64_t nb = n0 + chunk * 32;
+        const int ncols = static_cast<int>(p.N - nb < 32 ? (p.N - nb > 0 ? p.N - nb : 0) : 32);
+        if (row_ok && e.addend != nullptr) {
+          const float* ad = e.addend + row * e.ld_add + nb;
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (j < ncols) y[j] += ad[j];
+        }
+        if (row_ok && e.out_f32 != nullptr) {
+          float* dst = e.out_f32 + row * e.ld_f32 + nb;
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (j < ncols) dst[j] = y[j];
+        }
+#pragma unroll
+        for (int h = 0; h < 16; ++h) {
+          const __nv_bfloat162 b2 = __floats2bfloat162_rn(y[2 * h], y[2 * h + 1]);
+          packed[chunk * 16 + h] = *reinterpret_cast<const uint32_t*>(&b2);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tmem_empty[b]);
+      if (row_ok && e.out_bf16 != nullptr) {
+        __nv_bfloat16* dst = e.out_bf16 + row * e.ld_out + n0;
+        const int ncols = static_cast<int>(p.N - n0 < BN ? p.N - n0 : BN);
+#pragma unroll
+        for (int q = 0; q < BN / 8; ++q) {
+          if (vec_out && q * 8 + 8 <= ncols) {
+            *reinterpret_cast<uint4*>(dst + q * 8) =
+                make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+          } else {
+#pragma unroll
+            for (int h = 0; h < 8; ++h) {
+              const uint32_t w = packed[4 * q + h / 2];
+              if (q * 8 + h < ncols)
+                dst[q * 8 + h] = __ushort_as_bfloat16(static_cast<uint16_t>((h & 1) ? (w >> 16) : (w & 0xFFFFu)));
+            }
+          }
+        }
+      }
+    }
+  }
+
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<TMEM_COLS>(tmem_base);
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2): a cluster of 2 CTAs computes 256 x 256 tiles.  Each CTA
+// loads its own 128 rows of A and 128 of the 256 B rows; the leader issues M=256 MMAs that read
+// both CTAs' shared memory, and each CTA's TMEM holds the accumulator of its own 128 rows.
+// Per CTA that is 32 KB of operands per k-block instead of 48 KB (L2 feed was the limit), so the
+// ring holds 6 stages.  Same persistent schedule, double-buffered TMEM and kind-0 fold as above.
+constexpr int STAGES2 = 6;
+constexpr int BH_BYTES = 128 * BK_BYTES;  // half of B per CTA
+constexpr int STAGE2_BYTES = A_BYTES + BH_BYTES;
+constexpr int SMEM2_BYTES = 1024 + STAGES2 * STAGE2_BYTES + 4 * BN * 4 + 512;
+
+template <int KIND>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+    k_gemm_tc_2sm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                  const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
+                  const KParams p) {
+  constexpr uint32_t TMEM_COLS = 512;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES2 * A_BYTES;
+  float* colA = reinterpret_cast<float*>(smem + STAGES2 * STAGE2_BYTES);
+  float* colB = colA + BN;
+  float* colC = colB + BN;
+  int32_t* colD = reinterpret_cast<int32_t*>(colC + BN);
+  uint64_t* full = reinterpret_cast<uint64_t*>(colD + BN);
+  uint64_t* empty = full + STAGES2;
+  uint64_t* acc_full = empty + STAGES2;
+  uint64_t* y1_ready = acc_full + 2;
+  uint64_t* y_full = y1_ready + 2;
+  uint64_t* tmem_empty = y_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+
+  const uint32_t warp = warp_id_sync();
+  const uint32_t lane = lane_id();
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  constexpr int ELEM_BYTES = KIND == 0 ? 1 : 2;
+  constexpr int BK = BK_BYTES / ELEM_BYTES;
+  constexpr int BM2 = 2 * BM;
+  const int num_main = static_cast<int>((p.K + BK - 1) / BK);
+  const int num_ext = p.num_ext;
+  const int64_t n_tn = (p.N + BN - 1) / BN;
+  const int64_t total = ((p.M + BM2 - 1) / BM2) * n_tn;
+  const int64_t cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+  const int my_tiles = cluster < total ? static_cast<int>((total - cluster + nclusters - 1) / nclusters) : 0;
+  auto coords = [&](int i, int64_t& m0, int64_t& n0) {
+    const int64_t t = cluster + static_cast<int64_t>(i) * nclusters;
+    m0 = (t / n_tn) * BM2;
+    n0 = (t % n_tn) * BN;
+  };
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    if (num_ext > 0) {
+      tma_prefetch_desc(&tmA2);
+      tma_prefetch_desc(&tmB2);
+    }
+    for (int s = 0; s < STAGES2; ++s) {
+      mbar_init(&full[s], 2);   // leader: its own expect_tx arrive + the peer's remote arrive
+      mbar_init(&empty[s], 1);  // multicast commit from the leader's MMA
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&y1_ready[b], 8);    // leader: 4 epilogue warps x 2 CTAs
+      mbar_init(&y_full[b], 1);
+      mbar_init(&tmem_empty[b], 8);  // leader: 4 epilogue warps x 2 CTAs
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc_2sm<TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const bool fold_ext = KIND == 0 && num_ext > 0;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer (both CTAs)
+    if (lane == 0) {
+      uint32_t q = 0;
+      auto load = [&](const CUtensorMap* ta, const CUtensorMap* tb, int kcoord, int64_t m0, int64_t n0) {
+        const int s = q % STAGES2;
+        mbar_wait(&empty[s], ((q / STAGES2) & 1) ^ 1);
+        if (leader)
+          mbar_arrive_expect_tx(&full[s], 2 * STAGE2_BYTES);
+        else
+          mbar_arrive_cluster(&full[s], 0);
+        tma_load_2d_2sm(sA + s * A_BYTES, ta, &full[s], kcoord, static_cast<int32_t>(m0 + BM * rank));
+        tma_load_2d_2sm(sB + s * BH_BYTES, tb, &full[s], kcoord, static_cast<int32_t>(n0 + 128 * rank));
+        ++q;
+      };
+      for (int i = 0; i < my_tiles; ++i) {
+        int64_t m0, n0;
+        coords(i, m0, n0);
+        for (int kb = 0; kb < num_main; ++kb) load(&tmA, &tmB, kb * BK, m0, n0);
+        if (KIND == 1) {
+          for (int e = 0; e < num_ext; ++e) load(&tmA2, &tmB2, e * 64, m0, n0);
+        } else if (fold_ext && i > 0) {
+          coords(i - 1, m0, n0);
+          for (int e = 0; e < num_ext; ++e) load(&tmA2, &tmB2, e * 64, m0, n0);
+        }
+      }
+      if (fold_ext && my_tiles > 0) {
+        int64_t m0, n0;
+        coords(my_tiles - 1, m0, n0);
+        for (int e = 0; e < num_ext; ++e) load(&tmA2, &tmB2, e * 64, m0, n0);
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (leader, one thread)
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = KIND == 0 ? make_idesc(2, 0, 0, BM2, BN) : make_idesc(1, 1, 1, BM2, BN);
+      constexpr uint32_t idesc_ext = make_idesc(1, 1, 1, BM2, BN);
+      uint32_t q = 0;
+      auto block = [&](uint32_t dcol, bool ext, bool first) {
+        const int s = q % STAGES2;
+        mbar_wait(&full[s], (q / STAGES2) & 1);
+        tc_fence_after();
+        const uint64_t a0 = smem_desc_kmajor_sw128(sA + s * A_BYTES);
+        const uint64_t b0 = smem_desc_kmajor_sw128(sB + s * BH_BYTES);
+#pragma unroll
+        for (int k = 0; k < BK_BYTES / 32; ++k) {
+          const uint64_t adv = static_cast<uint64_t>((k * 32) >> 4);
+          const uint32_t acc = (first && k == 0) ? 0u : 1u;
+          if (!ext && KIND == 0)
+            mma_i8_2sm(dcol, a0 + adv, b0 + adv, idesc, acc);
+          else
+            mma_f16_2sm(dcol, a0 + adv, b0 + adv, ext ? idesc_ext : idesc, acc);
+        }
+        mma_commit_2sm(&empty[s]);
+        ++q;
+      };
+      auto fold = [&](int i) {
+        const uint32_t pb = i & 1;
+        mbar_wait(&y1_ready[pb], (i >> 1) & 1);
+        tc_fence_after();
+        for (int e = 0; e < num_ext; ++e) block(tmem_base + pb * 256, true, false);
+        mma_commit_2sm(&y_full[pb]);
+      };
+      for (int i = 0; i < my_tiles; ++i) {
+        const uint32_t b = i & 1;
+        mbar_wait(&tmem_empty[b], ((i >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + b * 256;
+        for (int kb = 0; kb < num_main; ++kb) block(d, false, kb == 0);
+        if (KIND == 1)
+          for (int e = 0; e < num_ext; ++e) block(d, true, false);
+        mma_commit_2sm(&acc_full[b]);
+        if (fold_ext && i > 0) fold(i - 1);
+      }
+      if (fold_ext && my_tiles > 0) fold(my_tiles - 1);
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue (both CTAs, own 128 rows)
+    const int et = static_cast<int>(threadIdx.x) - 128;
+    const GemmEpilogue& e = p.e;
+    const uint32_t quarter = warp & 3u;
+    const uint32_t lane_base = (quarter * 32u) << 16;
+    const bool vec_out = e.out_bf16 != nullptr && (e.ld_out % 8 == 0) &&
+                         (reinterpret_cast<uintptr_t>(e.out_bf16) % 16 == 0);
+    auto arrive_leader = [&](uint64_t* bar) {
+      __syncwarp();
+      if (lane == 0) {
+        if (leader)
+          mbar_arrive(bar);
+        else
+          mbar_arrive_cluster(bar, 0);
+      }
+    };
+    for (int i = 0; i < my_tiles; ++i) {
+      const uint32_t b = i & 1, ph = (i >> 1) & 1;
+      const uint32_t d = tmem_base + lane_base + b * 256;
+      int64_t m0, n0;
+      coords(i, m0, n0);
+      const int64_t row = m0 + BM * rank + quarter * 32 + lane;
+      const bool row_ok = row < p.M;
+      float sx = 0.f, ox = 0.f, rsxc = 0.f;
+      int32_t ibase = 0;
+      if (KIND == 0) {
+        named_bar_sync(1, 128);
+        const float kf = static_cast<float>(e.k_real);
+        for (int c = et; c < BN; c += 128) {
+          const int64_t n = n0 + c;
+          if (n < p.N) {
+            const float sw = e.col_scale[n];
+            const float ow = e.col_offset[n] + static_cast<float>(e.zp_col) * sw;
+            const int32_t rs = e.col_sum[n];
+            colA[c] = sw;
+            colB[c] = ow;
+            colC[c] = fmaf(sw, static_cast<float>(rs - e.zp_col * e.k_real), kf * ow);
+            colD[c] = e.zp_row * rs;
+          } else {
+            colA[c] = 0.f;
+            colB[c] = 0.f;
+            colC[c] = 0.f;
+            colD[c] = 0;
+          }
+        }
+        named_bar_sync(1, 128);
+        if (row_ok) {
+          sx = e.row_scale[row];
+          ox = e.row_offset[row] + static_cast<float>(e.zp_row) * sx;
+          const int32_t rsx = e.row_sum[row];
+          rsxc = static_cast<float>(rsx - e.zp_row * e.k_real);
+          ibase = e.zp_row * e.zp_col * e.k_real - e.zp_col * rsx;
+        }
+        mbar_wait(&acc_full[b], ph);
+        tc_fence_after();
+        if (fold_ext) {
+#pragma unroll 1
+          for (int chunk = 0; chunk < BN / 32; ++chunk) {
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(d + chunk * 32u, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const int c = chunk * 32 + j;
+              const int32_t accc = static_cast<int32_t>(v[j]) + ibase - colD[c];
+              v[j] = __float_as_uint(fmaf(sx, fmaf(colA[c], static_cast<float>(accc), colB[c] * rsxc), ox * colC[c]));
+            }
+            tmem_st_32x32b_x32(d + chunk * 32u, v);
+          }
+          tmem_st_wait();
+          tc_fence_before();
+          arrive_leader(&y1_ready[b]);
+          mbar_wait(&y_full[b], ph);
+          tc_fence_after();
+        }
+      } else {
+        mbar_wait(&acc_full[b], ph);
+        tc_fence_after();
+      }
+      uint32_t packed[BN / 2];
+#pragma unroll
+      for (int chunk = 0; chunk < BN / 32; ++chunk) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(d + chunk * 32u, v);
+        tmem_ld_wait();
+        float y[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          if (KIND == 0 && !fold_ext) {
+            const int c = chunk * 32 + j;
+            const int32_t accc = static_cast<int32_t>(v[j]) + ibase - colD[c];
+            y[j] = fmaf(sx, fmaf(colA[c], static_cast<float>(accc), colB[c] * rsxc), ox * colC[c]);
+          } else {
+            y[j] = __uint_as_float(v[j]);
+          }
+        }
+        const int64_t nb = n0 + chunk * 32;
+        const int ncols = static_cast<int>(p.N - nb < 32 ? (p.N - nb > 0 ? p.N - nb : 0) : 32);
+        if (row_ok && e.addend != nullptr) {
+          const float* ad = e.addend + row * e.ld_add + nb;
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (j < ncols) y[j] += ad[j];
+        }
+        if (row_ok && e.out_f32 != nullptr) {
+          float* dst = e.out_f32 + row * e.ld_f32 + nb;
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (j < ncols) dst[j] = y[j];
+        }
+#pragma unroll
+        for (int h = 0; h < 16; ++h) {
+          const __nv_bfloat162 b2 = __floats2bfloat162_rn(y[2 * h], y[2 * h + 1]);
+          packed[chunk * 16 + h] = *reinterpret_cast<const uint32_t*>(&b2);
+        }
+      }
+      tc_fence_before();
+      arrive_leader(&tmem_empty[b]);
+      if (row_ok && e.out_bf16 != nullptr) {
+        __nv_bfloat16* dst = e.out_bf16 + row * e.ld_out + n0;
+        const int ncols = static_cast<int>(p.N - n0 < BN ? p.N - n0 : BN);
+#pragma unroll
+        for (int q = 0; q < BN / 8; ++q) {
+          if (vec_out && q * 8 + 8 <= ncols) {
+            *reinterpret_cast<uint4*>(dst + q * 8) =
+                make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+          } else {
+#pragma unroll
+            for (int h = 0; h < 8; ++h) {
+              const uint32_t w = packed[4 * q + h / 2];
+              if (q * 8 + h < ncols)
+                dst[q * 8 + h] = __ushort_as_bfloat16(static_cast<uint16_t>((h & 1) ? (w >> 16) : (w & 0xFFFFu)));
+            }
+          }
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_2sm<TMEM_COLS>(tmem_base);
+  }
+}
+
+// QA_GEMM_2SM=0 keeps the single-CTA persistent kernel (A/B comparisons, triage).
+bool pair_disabled() {
+  static const bool off = [] {
+    const char* v = getenv("QA_GEMM_2SM");
+    return v != nullptr && v[0] == '0';
+  }();
+  return off;
+}
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -312,6 +912,15 @@ bool make_tmap(CUtensorMap* m, const void* base, int elem_bytes, int64_t rows, i
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// QA_GEMM_PERSISTENT=0 selects the one-tile-per-CTA kernel everywhere (A/B comparisons, triage).
+bool persistent_disabled() {
+  static const bool off = [] {
+    const char* v = getenv("QA_GEMM_PERSISTENT");
+    return v != nullptr && v[0] == '0';
+  }();
+  return off;
+}
+
 bool aligned_operand(const void* p, int64_t ld, int eb) {
   return p != nullptr && reinterpret_cast<uintptr_t>(p) % 16 == 0 && (ld * eb) % 16 == 0;
 }
@@ -339,9 +948,15 @@ int launch(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, in
     tb2 = tb;
   }
   static bool attr_set = false;
+  static int num_sms = 148;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(k_gemm_tc<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(gemm)");
+    e = cudaFuncSetAttribute(k_gemm_tc_p<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(gemm_p)");
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
     attr_set = true;
   }
   KParams p;
@@ -350,11 +965,37 @@ int launch(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, in
   p.K = K;
   p.num_ext = num_ext;
   p.e = epi;
-  const dim3 grid(static_cast<unsigned>((N + BN - 1) / BN), static_cast<unsigned>((M + BM - 1) / BM));
   const double kalg = KIND == 0 && epi.k_real > 0 ? double(epi.k_real) : double(K);
   LaunchScope scope(KIND == 0 ? kGemmI8 : kGemmBF16, 2.0 * double(M) * double(N) * kalg, s);
   count_launches(1);
-  k_gemm_tc<KIND><<<grid, THREADS, SMEM_BYTES, s>>>(ta, tb, ta2, tb2, p);
+  const int64_t tiles = ((N + BN - 1) / BN) * ((M + BM - 1) / BM);
+  const bool debug = epi.out_acc != nullptr || epi.out_y2 != nullptr;
+  if (debug || persistent_disabled()) {
+    // one tile per CTA; also the only variant that can expose the raw s32 accumulators / y2
+    const dim3 grid(static_cast<unsigned>((N + BN - 1) / BN), static_cast<unsigned>((M + BM - 1) / BM));
+    k_gemm_tc<KIND><<<grid, THREADS, SMEM_BYTES, s>>>(ta, tb, ta2, tb2, p);
+  } else if (!pair_disabled() && M > BM) {
+    static bool attr2 = false;
+    if (!attr2) {
+      cudaError_t e = cudaFuncSetAttribute(k_gemm_tc_2sm<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES);
+      if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(gemm_2sm)");
+      attr2 = true;
+    }
+    // each CTA of the pair loads 128 of the tile's 256 B rows
+    CUtensorMap tbh, tb2h;
+    if (!make_tmap(&tbh, B, eb, N, K, ldb, 128) ||
+        (num_ext > 0 && !make_tmap(&tb2h, ext->B2, 2, N, ext->K2, ext->ldb2, 128))) {
+      set_error("cuTensorMapEncodeTiled failed for the CTA-pair B operand");
+      return QA_ERR_CUDA;
+    }
+    if (num_ext == 0) tb2h = tbh;
+    const int64_t pair_tiles = ((N + BN - 1) / BN) * ((M + 2 * BM - 1) / (2 * BM));
+    const int64_t clusters = pair_tiles < num_sms / 2 ? pair_tiles : num_sms / 2;
+    k_gemm_tc_2sm<KIND><<<static_cast<unsigned>(2 * clusters), THREADS, SMEM2_BYTES, s>>>(ta, tbh, ta2, tb2h, p);
+  } else {
+    const unsigned grid = static_cast<unsigned>(tiles < num_sms ? tiles : num_sms);
+    k_gemm_tc_p<KIND><<<grid, THREADS, SMEM_BYTES, s>>>(ta, tb, ta2, tb2, p);
+  }
   return cuda_status(cudaGetLastError(), "k_gemm_tc launch");
 }
 

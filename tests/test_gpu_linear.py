@@ -72,6 +72,10 @@ def test_forward_parity(N, K, T, bits, r, spec):
     assert e_y1 <= TOL_F32, e_y1
     assert e_y2 <= TOL_BF16, e_y2
     assert e_y <= TOL_BF16, e_y
+    # production path (persistent GEMM, adapter folded in TMEM) against the oracle and the debug path
+    y_prod = L.linear_forward(q, (spec, cores), x)
+    assert O.rel_err(_np(y_prod), ref["y"]) <= TOL_BF16
+    assert O.rel_err(_np(y_prod), _np(out["y_bf16"])) <= 2 ** -7
 
 
 @pytest.mark.parametrize("N,K,T,bits,r,spec", CASES)
