@@ -35,6 +35,10 @@ constexpr int A_BYTES = BM * BK_BYTES;
 constexpr int B_BYTES = BN * BK_BYTES;
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int THREADS = 256;
+// kind 0 persistent kernels issue tile i-1's y2 extension this many k-blocks into tile i's main
+// loop: late enough for the epilogue's in-place s32 -> fp32 pass, early enough that tile i-1's TMEM
+// buffer is drained before tile i+1 needs it.
+constexpr int kFoldAt = 16;
 constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 4 * BN * 4 /*column terms*/ + 256;
 
 template <int KIND>
@@ -367,15 +371,17 @@ __global__ void __launch_bounds__(THREADS, 1)
         ++q;
       };
       for (int i = 0; i < my_tiles; ++i) {
-        int64_t m0, n0;
+        int64_t m0, n0, pm0, pn0;
         coords(i, m0, n0);
-        for (int kb = 0; kb < num_main; ++kb) load(&tmA, &tmB, kb * BK, m0, n0);
-        if (KIND == 1) {
-          for (int e = 0; e < num_ext; ++e) load(&tmA2, &tmB2, e * 64, m0, n0);
-        } else if (fold_ext && i > 0) {
-          coords(i - 1, m0, n0);
-          for (int e = 0; e < num_ext; ++e) load(&tmA2, &tmB2, e * 64, m0, n0);
+        const int split = (fold_ext && i > 0) ? (num_main < kFoldAt ? num_main : kFoldAt) : num_main;
+        for (int kb = 0; kb < split; ++kb) load(&tmA, &tmB, kb * BK, m0, n0);
+        if (fold_ext && i > 0) {  // y2 operands of tile i-1, a fixed distance into tile i's k-loop
+          coords(i - 1, pm0, pn0);
+          for (int e = 0; e < num_ext; ++e) load(&tmA2, &tmB2, e * 64, pm0, pn0);
         }
+        for (int kb = split; kb < num_main; ++kb) load(&tmA, &tmB, kb * BK, m0, n0);
+        if (KIND == 1)
+          for (int e = 0; e < num_ext; ++e) load(&tmA2, &tmB2, e * 64, m0, n0);
       }
       if (fold_ext && my_tiles > 0) {
         int64_t m0, n0;
@@ -419,11 +425,13 @@ __global__ void __launch_bounds__(THREADS, 1)
         mbar_wait(&tmem_empty[b], ((i >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + b * 256;
-        for (int kb = 0; kb < num_main; ++kb) block(d, false, kb == 0);
+        const int split = (fold_ext && i > 0) ? (num_main < kFoldAt ? num_main : kFoldAt) : num_main;
+        for (int kb = 0; kb < split; ++kb) block(d, false, kb == 0);
+        if (fold_ext && i > 0) fold(i - 1);
+        for (int kb = split; kb < num_main; ++kb) block(d, false, false);
         if (KIND == 1)
           for (int e = 0; e < num_ext; ++e) block(d, true, false);
         mma_commit(&acc_full[b]);
-        if (fold_ext && i > 0) fold(i - 1);
       }
       if (fold_ext && my_tiles > 0) fold(my_tiles - 1);
     }
@@ -663,15 +671,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         ++q;
       };
       for (int i = 0; i < my_tiles; ++i) {
-        int64_t m0, n0;
+        int64_t m0, n0, pm0, pn0;
         coords(i, m0, n0);
-        for (int kb = 0; kb < num_main; ++kb) load(&tmA, &tmB, kb * BK, m0, n0);
-        if (KIND == 1) {
-          for (int e = 0; e < num_ext; ++e) load(&tmA2, &tmB2, e * 64, m0, n0);
-        } else if (fold_ext && i > 0) {
-          coords(i - 1, m0, n0);
-          for (int e = 0; e < num_ext; ++e) load(&tmA2, &tmB2, e * 64, m0, n0);
+        const int split = (fold_ext && i > 0) ? (num_main < kFoldAt ? num_main : kFoldAt) : num_main;
+        for (int kb = 0; kb < split; ++kb) load(&tmA, &tmB, kb * BK, m0, n0);
+        if (fold_ext && i > 0) {
+          coords(i - 1, pm0, pn0);
+          for (int e = 0; e < num_ext; ++e) load(&tmA2, &tmB2, e * 64, pm0, pn0);
         }
+        for (int kb = split; kb < num_main; ++kb) load(&tmA, &tmB, kb * BK, m0, n0);
+        if (KIND == 1)
+          for (int e = 0; e < num_ext; ++e) load(&tmA2, &tmB2, e * 64, m0, n0);
       }
       if (fold_ext && my_tiles > 0) {
         int64_t m0, n0;
@@ -715,11 +725,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         mbar_wait(&tmem_empty[b], ((i >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + b * 256;
-        for (int kb = 0; kb < num_main; ++kb) block(d, false, kb == 0);
+        const int split = (fold_ext && i > 0) ? (num_main < kFoldAt ? num_main : kFoldAt) : num_main;
+        for (int kb = 0; kb < split; ++kb) block(d, false, kb == 0);
+        if (fold_ext && i > 0) fold(i - 1);
+        for (int kb = split; kb < num_main; ++kb) block(d, false, false);
         if (KIND == 1)
           for (int e = 0; e < num_ext; ++e) block(d, true, false);
         mma_commit_2sm(&acc_full[b]);
-        if (fold_ext && i > 0) fold(i - 1);
       }
       if (fold_ext && my_tiles > 0) fold(my_tiles - 1);
     }

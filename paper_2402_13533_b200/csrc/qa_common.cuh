@@ -86,6 +86,15 @@ QA_DEV void tma_load_2d(void* smem_dst, const CUtensorMap* m, uint64_t* bar, int
       : "memory");
 }
 
+// 1-D bulk async copy global -> shared (16-byte aligned, size multiple of 16), completing on `bar`.
+QA_DEV void bulk_load(void* smem_dst, const void* gmem_src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(gmem_src)), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // ---------------------------------------------------------------- tcgen05 / TMEM
 template <uint32_t kCols>
 QA_DEV void tmem_alloc(uint32_t* dst_smem) {

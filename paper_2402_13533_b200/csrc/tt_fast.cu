@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(256) k_g1_interleave(const float* __restrict__
 }
 
 template <typename InT, int J1, int R1, bool CODES>
-__global__ void __launch_bounds__(256) k_actquant_z1(const InT* __restrict__ x, int64_t T, int64_t K,
+__global__ void __launch_bounds__(256, 3) k_actquant_z1(const InT* __restrict__ x, int64_t T, int64_t K,
                                                      uint8_t* __restrict__ codes, int64_t ldc,
                                                      float* __restrict__ sx, float* __restrict__ ox,
                                                      int32_t* __restrict__ rsx, const float4* __restrict__ G1i,
@@ -63,50 +63,99 @@ __global__ void __launch_bounds__(256) k_actquant_z1(const InT* __restrict__ x, 
   constexpr int K2 = J1 * R1;
   static_assert(K2 == 8 || K2 == 16 || K2 == 32 || K2 == 64, "unsupported Z1 width");
   constexpr int NQ = 2 * R1 / J1;
+  constexpr int RP = R1 / 2;  // rank pairs: Z1 accumulates with packed fp32 FMAs (FFMA2)
+  constexpr bool BF = sizeof(InT) == 2;
   const int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= T) return;
   const uint32_t lane = lane_id();
   const InT* src = x + row * K;
   const int64_t nvec = K / 8;
 
-  float z[K2];
+  unsigned long long zz[J1][RP];  // zz[J][p] = (z[2p, J], z[2p+1, J])
 #pragma unroll
-  for (int i = 0; i < K2; ++i) z[i] = 0.f;
+  for (int J = 0; J < J1; ++J)
+#pragma unroll
+    for (int p = 0; p < RP; ++p) zz[J][p] = 0ull;
   float lo = INFINITY, hi = -INFINITY;
-  constexpr int UNR = 4;  // chunks in flight per lane
-  for (int64_t i0 = 0; i0 * 32 + lane < nvec; i0 += UNR) {
-    float f[UNR][8];
+  __nv_bfloat162 lo2 = __floats2bfloat162_rn(INFINITY, INFINITY), hi2 = __floats2bfloat162_rn(-INFINITY, -INFINITY);
+  constexpr int UNR = 4;  // chunks per batch; the next batch's loads are in flight while this one computes
+  uint4 nxt[UNR];
+  if (BF) {
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
-      const int64_t c = (i0 + u) * 32 + lane;
-      if (c < nvec) load8<InT>(src + c * 8, f[u]);
+      const int64_t c = u * 32 + lane;
+      if (c < nvec) nxt[u] = __ldg(reinterpret_cast<const uint4*>(src + c * 8));
+    }
+  }
+  for (int64_t i0 = 0; i0 * 32 + lane < nvec; i0 += UNR) {
+    float f[UNR][8];
+    uint4 raw[UNR];
+    if (BF) {
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        raw[u] = nxt[u];
+        const int64_t c = (i0 + UNR + u) * 32 + lane;
+        if (c < nvec) nxt[u] = __ldg(reinterpret_cast<const uint4*>(src + c * 8));
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const int64_t c = (i0 + u) * 32 + lane;
+        if (c < nvec) load8<InT>(src + c * 8, f[u]);
+      }
     }
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
       const int64_t c = (i0 + u) * 32 + lane;
       if (c >= nvec) break;
+      if (BF) {
+        const uint32_t w[4] = {raw[u].x, raw[u].y, raw[u].z, raw[u].w};
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        lo = fminf(lo, f[u][i]);
-        hi = fmaxf(hi, f[u][i]);
+        for (int i = 0; i < 4; ++i) {
+          const __nv_bfloat162 b2 = *reinterpret_cast<const __nv_bfloat162*>(&w[i]);
+          lo2 = __hmin2(lo2, b2);
+          hi2 = __hmax2(hi2, b2);
+          f[u][2 * i] = __uint_as_float(w[i] << 16);
+          f[u][2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          lo = fminf(lo, f[u][i]);
+          hi = fmaxf(hi, f[u][i]);
+        }
       }
-      float g[4 * NQ];  // [8 / J1 rows][R1]
+      unsigned long long g2[2 * NQ];  // [8 / J1 rows][RP] rank pairs of G1
       const float4* gp = G1i + ((i0 + u) * NQ) * 32 + lane;
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
         const float4 v = __ldg(gp + q * 32);
-        g[4 * q] = v.x, g[4 * q + 1] = v.y, g[4 * q + 2] = v.z, g[4 * q + 3] = v.w;
+        g2[2 * q] = f2pack(v.x, v.y);
+        g2[2 * q + 1] = f2pack(v.z, v.w);
       }
 #pragma unroll
       for (int jj = 0; jj < 8 / J1; ++jj)
 #pragma unroll
         for (int J = 0; J < J1; ++J) {
           const float xv = f[u][jj * J1 + J];
+          const unsigned long long xb = f2pack(xv, xv);
 #pragma unroll
-          for (int a = 0; a < R1; ++a) z[a * J1 + J] = fmaf(xv, g[jj * R1 + a], z[a * J1 + J]);
+          for (int p = 0; p < RP; ++p) ffma2(zz[J][p], xb, g2[jj * RP + p]);
         }
     }
   }
+  if (BF) {
+    lo = fminf(__low2float(lo2), __high2float(lo2));
+    hi = fmaxf(__low2float(hi2), __high2float(hi2));
+  }
+  float z[K2];  // z[a * J1 + J]
+#pragma unroll
+  for (int J = 0; J < J1; ++J)
+#pragma unroll
+    for (int p = 0; p < RP; ++p) {
+      z[(2 * p) * J1 + J] = f2lo(zz[J][p]);
+      z[(2 * p + 1) * J1 + J] = f2hi(zz[J][p]);
+    }
   // Z1 row: reduce across lanes, write fp32 and/or the 3-term bf16 split [hi | lo | hi | 0]
   if (K2 >= 32) {
 #pragma unroll
@@ -163,15 +212,8 @@ __global__ void __launch_bounds__(256) k_actquant_z1(const InT* __restrict__ x, 
       for (int u = 0; u < UNR; ++u) {
         const int64_t c = (i0 + u) * 32 + lane;
         if (c >= nvec) break;
-        uint32_t q[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          q[i] = flat ? 0u : code_of<8>(f[u][i], lo, inv, lo64, step64);
-          sum += static_cast<int>(q[i]);
-        }
-        uint2 packed;
-        packed.x = q[0] | (q[1] << 8) | (q[2] << 16) | (q[3] << 24);
-        packed.y = q[4] | (q[5] << 8) | (q[6] << 16) | (q[7] << 24);
+        uint2 packed = make_uint2(0u, 0u);
+        if (!flat) codes8(f[u], lo, inv, lo64, step64, packed.x, packed.y, sum);
         *reinterpret_cast<uint2*>(dst + c * 8) = packed;
       }
     }
@@ -181,6 +223,225 @@ __global__ void __launch_bounds__(256) k_actquant_z1(const InT* __restrict__ x, 
       sx[row] = flat ? 0.0f : __double2float_rn(step64);
       ox[row] = lo;
       rsx[row] = sum;
+    }
+  }
+}
+
+// Shared-memory-staged variant (production path for bf16 rows): every warp owns one row slot in
+// shared memory; lane 0 fetches the warp's next row with a single cp.async.bulk completing on the
+// warp's mbarrier, so HBM reads need no registers and both passes (stats + Z1, then codes) read
+// shared memory.  Rows are strided over all warps of the grid.
+//   Z1 (J1 >= 2): accumulators are paired over J (zz[a][J/2]) so each bf16 word of x is directly a
+//   packed fp32 operand; G1 comes pre-broadcast ((g, g) pairs, k_g1_bcast).  J1 == 1 (LoRA) pairs
+//   over the rank instead and broadcasts x.
+//   Codes: magic-number rounding; chunks with an element near a rounding tie are recorded in a
+//   per-lane bitmask and replayed exactly in fp64 after the row (rare, ~0.4% of lane-chunks).
+template <int J1, int R1>
+__global__ void __launch_bounds__(256) k_g1_bcast(const float* __restrict__ G1, float4* __restrict__ G1b,
+                                                  int64_t nvec) {
+  constexpr int NQB = (8 / J1) * R1 / 2;  // float4 (g_a, g_a, g_a+1, g_a+1) per chunk
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= nvec * NQB) return;
+  const int64_t c = idx / NQB;
+  const int q = static_cast<int>(idx % NQB);
+  const int jj = q / (R1 / 2), a = 2 * (q % (R1 / 2));
+  const float* g = G1 + (c * (8 / J1) + jj) * R1 + a;
+  G1b[((c / 32) * NQB + q) * 32 + (c % 32)] = make_float4(g[0], g[0], g[1], g[1]);
+}
+
+template <int J1, int R1, bool CODES>
+__global__ void __launch_bounds__(512) k_actquant_z1_s(const __nv_bfloat16* __restrict__ x, int64_t T, int64_t K,
+                                                       uint8_t* __restrict__ codes, int64_t ldc,
+                                                       float* __restrict__ sx, float* __restrict__ ox,
+                                                       int32_t* __restrict__ rsx, const float4* __restrict__ G1g,
+                                                       __nv_bfloat16* __restrict__ zb, int64_t ldzb,
+                                                       float* __restrict__ zf) {
+  constexpr int K2 = J1 * R1;
+  static_assert(K2 == 8 || K2 == 16 || K2 == 32 || K2 == 64, "unsupported Z1 width");
+  constexpr int NQ = 2 * R1 / J1;  // float4 G1 pieces per chunk (interleaved layout, k_g1_interleave)
+  extern __shared__ __align__(128) uint8_t aq_smem[];
+  __shared__ uint64_t aq_bar[16];
+  const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
+  const uint32_t rowbytes = static_cast<uint32_t>(K * 2);
+  const uint32_t slot_bytes = (rowbytes + 127u) & ~127u;
+  uint8_t* slot = aq_smem + warp * slot_bytes;
+  uint64_t* bar = &aq_bar[warp];
+  const int64_t nwarps_grid = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + warp;
+  const uint32_t nvec = static_cast<uint32_t>(K / 8);
+  if (lane == 0) {
+    mbar_init(bar, 1);
+    fence_barrier_init();
+    if (row < T) {
+      mbar_arrive_expect_tx(bar, rowbytes);
+      bulk_load(slot, x + row * K, rowbytes, bar);
+    }
+  }
+  __syncwarp();
+  const uint4* srow = reinterpret_cast<const uint4*>(slot);
+  for (uint32_t it = 0; row < T; ++it, row += nwarps_grid) {
+    mbar_wait(bar, it & 1);
+    // ---- pass 1: exact bf16 min/max and Z1
+    float z[K2];
+    __nv_bfloat162 lo2 = __floats2bfloat162_rn(INFINITY, INFINITY), hi2 = __floats2bfloat162_rn(-INFINITY, -INFINITY);
+    {
+      constexpr int RP = R1 / 2;
+      unsigned long long zz[J1][RP];  // zz[J][p] = (z[2p, J], z[2p+1, J]): pairs over the rank
+#pragma unroll
+      for (int J = 0; J < J1; ++J)
+#pragma unroll
+        for (int p = 0; p < RP; ++p) zz[J][p] = 0ull;
+#pragma unroll 2
+      for (uint32_t c = lane; c < nvec; c += 32) {
+        const uint4 raw = srow[c];
+        const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+        float f[8];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const __nv_bfloat162 b2 = *reinterpret_cast<const __nv_bfloat162*>(&w[i]);
+          lo2 = __hmin2(lo2, b2);
+          hi2 = __hmax2(hi2, b2);
+          f[2 * i] = __uint_as_float(w[i] << 16);
+          f[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+        }
+        const float4* gp = G1g + ((c >> 5) * NQ) * 32 + (c & 31);
+        unsigned long long g2[2 * NQ];  // [8 / J1 rows][RP]
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          const float4 v = __ldg(gp + q * 32);
+          g2[2 * q] = f2pack(v.x, v.y);
+          g2[2 * q + 1] = f2pack(v.z, v.w);
+        }
+#pragma unroll
+        for (int jj = 0; jj < 8 / J1; ++jj)
+#pragma unroll
+          for (int J = 0; J < J1; ++J) {
+            const unsigned long long xb = f2pack(f[jj * J1 + J], f[jj * J1 + J]);
+#pragma unroll
+            for (int p = 0; p < RP; ++p) ffma2(zz[J][p], xb, g2[jj * RP + p]);
+          }
+      }
+#pragma unroll
+      for (int J = 0; J < J1; ++J)
+#pragma unroll
+        for (int p = 0; p < RP; ++p) {
+          z[(2 * p) * J1 + J] = f2lo(zz[J][p]);
+          z[(2 * p + 1) * J1 + J] = f2hi(zz[J][p]);
+        }
+    }
+    if (K2 >= 32) {
+#pragma unroll
+      for (int b = 0; b < K2; b += 32) warp_reduce_scatter32<K2>(z, b);
+#pragma unroll
+      for (int b = 0; b < K2; b += 32) {
+        const float v = z[b];
+        if (zf != nullptr) zf[row * K2 + b + lane] = v;
+        if (zb != nullptr) {
+          const __nv_bfloat16 hv = __float2bfloat16_rn(v);
+          zb[row * ldzb + b + lane] = hv;
+          zb[row * ldzb + K2 + b + lane] = __float2bfloat16_rn(v - __bfloat162float(hv));
+          zb[row * ldzb + 2 * K2 + b + lane] = hv;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < K2; ++i) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) z[i] += __shfl_xor_sync(0xffffffffu, z[i], o);
+      }
+#pragma unroll
+      for (int i = 0; i < K2; ++i) {
+        if (lane == static_cast<uint32_t>(i)) {
+          if (zf != nullptr) zf[row * K2 + i] = z[i];
+          if (zb != nullptr) {
+            const __nv_bfloat16 hv = __float2bfloat16_rn(z[i]);
+            zb[row * ldzb + i] = hv;
+            zb[row * ldzb + K2 + i] = __float2bfloat16_rn(z[i] - __bfloat162float(hv));
+            zb[row * ldzb + 2 * K2 + i] = hv;
+          }
+        }
+      }
+    }
+    if (zb != nullptr)
+      for (int64_t i = 3 * K2 + lane; i < ldzb; i += 32) zb[row * ldzb + i] = __float2bfloat16_rn(0.f);
+    if constexpr (CODES) {
+      // ---- pass 2: codes (reference rule, bit-exact) from the same shared-memory row
+      float lo = fminf(__low2float(lo2), __high2float(lo2));
+      float hi = fmaxf(__low2float(hi2), __high2float(hi2));
+      lo = warp_min(lo);
+      hi = warp_max(hi);
+      const double lo64 = static_cast<double>(lo);
+      const double step64 = __ddiv_rn(__dsub_rn(static_cast<double>(hi), lo64), 255.0);
+      const bool flat = !(step64 > 0.0);
+      const float inv = flat ? 0.0f : static_cast<float>(1.0 / step64);
+      const float nb = -lo * inv;
+      const unsigned long long inv2 = f2pack(inv, inv), nb2 = f2pack(nb, nb);
+      uint8_t* dst = codes + row * ldc;
+      int sum = 0;
+      if (flat) {
+        for (uint32_t c = lane; c < nvec; c += 32) *reinterpret_cast<uint2*>(dst + c * 8) = make_uint2(0u, 0u);
+      } else {
+        unsigned long long near_mask[2] = {0ull, 0ull};
+        uint32_t k = 0;
+#pragma unroll 2
+        for (uint32_t c = lane; c < nvec; c += 32, ++k) {
+          const uint4 raw = srow[c];
+          const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+          float f[8];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            f[2 * i] = __uint_as_float(w[i] << 16);
+            f[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+          }
+          uint2 packed;
+          if (codes8_fast(f, inv2, nb2, packed.x, packed.y)) {
+            if (k < 64)
+              near_mask[0] |= 1ull << k;
+            else
+              near_mask[1] |= 1ull << (k - 64);
+          }
+          sum = static_cast<int>(__dp4a(packed.x, 0x01010101u, static_cast<unsigned int>(sum)));
+          sum = static_cast<int>(__dp4a(packed.y, 0x01010101u, static_cast<unsigned int>(sum)));
+          *reinterpret_cast<uint2*>(dst + c * 8) = packed;
+        }
+        // exact fp64 replay of the flagged chunks (same lane, so program order covers the rewrite)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          while (near_mask[h] != 0ull) {
+            const int bit = __ffsll(static_cast<long long>(near_mask[h])) - 1;
+            near_mask[h] &= near_mask[h] - 1;
+            const uint32_t c = lane + 32u * (static_cast<uint32_t>(h) * 64u + static_cast<uint32_t>(bit));
+            const uint4 raw = srow[c];
+            const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+            float f[8];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              f[2 * i] = __uint_as_float(w[i] << 16);
+              f[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+            }
+            uint2 old = *reinterpret_cast<const uint2*>(dst + c * 8);
+            uint2 fixed = old;
+            codes8_exact(f, inv, nb, lo64, step64, fixed.x, fixed.y);
+            sum += static_cast<int>(__dp4a(fixed.x, 0x01010101u, 0u) + __dp4a(fixed.y, 0x01010101u, 0u)) -
+                   static_cast<int>(__dp4a(old.x, 0x01010101u, 0u) + __dp4a(old.y, 0x01010101u, 0u));
+            *reinterpret_cast<uint2*>(dst + c * 8) = fixed;
+          }
+        }
+      }
+      for (int64_t kk = K + lane; kk < ldc; kk += 32) dst[kk] = 0;
+      sum = warp_sum_i(sum);
+      if (lane == 0) {
+        sx[row] = flat ? 0.0f : __double2float_rn(step64);
+        ox[row] = lo;
+        rsx[row] = sum;
+      }
+    }
+    // all lanes are done with the slot: fetch this warp's next row into it
+    __syncwarp();
+    if (lane == 0 && row + nwarps_grid < T) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive_expect_tx(bar, rowbytes);
+      bulk_load(slot, x + (row + nwarps_grid) * K, rowbytes, bar);
     }
   }
 }
@@ -636,9 +897,18 @@ bool fast_tt_supported(int J1, int R1) {
   return (J1 == 1 && (R1 == 8 || R1 == 16)) || (J1 == 4 && (R1 == 8 || R1 == 16));
 }
 
+// QA_AQ_STAGED=0 selects the register-streaming act-quant kernel (A/B comparisons).
+bool staged_disabled() {
+  static const bool off = [] {
+    const char* v = getenv("QA_AQ_STAGED");
+    return v != nullptr && v[0] == '0';
+  }();
+  return off;
+}
+
 size_t g1i_floats(int64_t K, int J1, int R1) {
   const int64_t nvec = K / 8;
-  return static_cast<size_t>(((nvec + 31) / 32) * 32) * 8 * R1 / J1;
+  return static_cast<size_t>(((nvec + 31) / 32) * 32) * 8 * R1 / J1 * 2;  // broadcast layout is 2x
 }
 
 cudaError_t launch_actquant_z1(const void* x, int x_dtype, int64_t T, int64_t K, bool want_codes, uint8_t* codes,
@@ -646,8 +916,11 @@ cudaError_t launch_actquant_z1(const void* x, int x_dtype, int64_t T, int64_t K,
                                __nv_bfloat16* zb, int64_t ldzb, float* zf, float* g1i_ws, cudaStream_t s) {
   if (T == 0) return cudaSuccess;
   const int64_t nvec = K / 8;
+  const uint32_t slot_bytes = static_cast<uint32_t>((K * 2 + 127) & ~int64_t(127));
+  const bool staged = x_dtype == QA_BF16 && !staged_disabled() && slot_bytes <= 100 * 1024 && K <= 32768;
   {
-    const int64_t n = nvec * (2 * R1 / J1);
+    const bool bcast = false;  // broadcast G1 layout (k_g1_bcast) measured slower: 2x the L1 loads
+    const int64_t n = nvec * (bcast ? (8 / J1) * R1 / 2 : 2 * R1 / J1);
     LaunchScope scope(kTT, double(n) * 32, s);
     count_launches(1);
     const unsigned g = static_cast<unsigned>((n + 255) / 256);
@@ -657,9 +930,10 @@ cudaError_t launch_actquant_z1(const void* x, int x_dtype, int64_t T, int64_t K,
     else if (J1 == 1 && R1 == 16)
       k_g1_interleave<1, 16><<<g, 256, 0, s>>>(G1, G1i, nvec);
     else if (J1 == 4 && R1 == 8)
-      k_g1_interleave<4, 8><<<g, 256, 0, s>>>(G1, G1i, nvec);
+      bcast ? k_g1_bcast<4, 8><<<g, 256, 0, s>>>(G1, G1i, nvec) : k_g1_interleave<4, 8><<<g, 256, 0, s>>>(G1, G1i, nvec);
     else
-      k_g1_interleave<4, 16><<<g, 256, 0, s>>>(G1, G1i, nvec);
+      bcast ? k_g1_bcast<4, 16><<<g, 256, 0, s>>>(G1, G1i, nvec)
+            : k_g1_interleave<4, 16><<<g, 256, 0, s>>>(G1, G1i, nvec);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
@@ -669,6 +943,30 @@ cudaError_t launch_actquant_z1(const void* x, int x_dtype, int64_t T, int64_t K,
                                    double(T) * (zb ? ldzb * 2 : 0) + double(T) * (zf ? J1 * R1 * 4 : 0),
                     s);
   count_launches(1);
+  if (staged) {
+    int warps = static_cast<int>((200 * 1024) / slot_bytes);
+    warps = warps > 16 ? 16 : warps;
+    const size_t smem = static_cast<size_t>(warps) * slot_bytes;
+    const int64_t ctas_needed = (T + warps - 1) / warps;
+    const unsigned grid = static_cast<unsigned>(ctas_needed < 148 ? ctas_needed : 148);
+#define QA_AQS(JJ, RR)                                                                                              \
+  {                                                                                                                 \
+    auto kern = want_codes ? k_actquant_z1_s<JJ, RR, true> : k_actquant_z1_s<JJ, RR, false>;                       \
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));               \
+    kern<<<grid, warps * 32, smem, s>>>(static_cast<const __nv_bfloat16*>(x), T, K, codes, ldc, sx, ox, rsx, G1i, \
+                                        zb, ldzb, zf);                                                              \
+  }
+    if (J1 == 1 && R1 == 8)
+      QA_AQS(1, 8)
+    else if (J1 == 1 && R1 == 16)
+      QA_AQS(1, 16)
+    else if (J1 == 4 && R1 == 8)
+      QA_AQS(4, 8)
+    else
+      QA_AQS(4, 16)
+#undef QA_AQS
+    return cudaGetLastError();
+  }
   const dim3 grid(static_cast<unsigned>((T + 7) / 8));  // 8 warps = 8 token rows per CTA
 #define QA_AQ(TI, JJ, RR)                                                                                           \
   if (want_codes)                                                                                                   \
