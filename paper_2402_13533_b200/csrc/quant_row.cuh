@@ -76,66 +76,22 @@ QA_DEV unsigned long long fsub2(unsigned long long a, unsigned long long b) {
   return d;
 }
 
-// Fast codes for 8 elements without any tie handling: returns the packed codes and whether any
-// element lies within the tie band (the caller replays those chunks exactly, see codes8_exact).
-QA_DEV bool codes8_fast(const float (&f)[8], unsigned long long inv2, unsigned long long nb2, uint32_t& w0,
-                        uint32_t& w1) {
-  constexpr float kMagic = 12582912.0f;
-  const unsigned long long m2 = f2pack(kMagic, kMagic);
-  uint32_t r[8];
-  float dmax = 0.f;
-#pragma unroll
-  for (int i = 0; i < 8; i += 2) {
-    const unsigned long long q2 = ffma2r(f2pack(f[i], f[i + 1]), inv2, nb2);
-    const unsigned long long s2 = fadd2(q2, m2);
-    const unsigned long long d2 = fsub2(q2, fsub2(s2, m2));
-    dmax = fmaxf(dmax, fmaxf(fabsf(__uint_as_float(static_cast<uint32_t>(d2))),
-                             fabsf(__uint_as_float(static_cast<uint32_t>(d2 >> 32)))));
-    r[i] = static_cast<uint32_t>(s2);
-    r[i + 1] = static_cast<uint32_t>(s2 >> 32);
-  }
-  w0 = __byte_perm(__byte_perm(r[0], r[1], 0x0040), __byte_perm(r[2], r[3], 0x0040), 0x5410);
-  w1 = __byte_perm(__byte_perm(r[4], r[5], 0x0040), __byte_perm(r[6], r[7], 0x0040), 0x5410);
-  return dmax > 0.5f - kTieBand;
-}
-
-// Exact codes (the reference's fp64 rule) for the elements of a flagged chunk that are near a tie.
-QA_DEV void codes8_exact(const float (&f)[8], float inv, float nb, double lo64, double step64, uint32_t& w0,
-                         uint32_t& w1) {
-  constexpr float kMagic = 12582912.0f;
-  uint32_t c[8];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    c[i] = (w0 >> (8 * i)) & 0xFFu;
-    c[i + 4] = (w1 >> (8 * i)) & 0xFFu;
-  }
-  for (int i = 0; i < 8; ++i) {
-    const float q = fmaf(f[i], inv, nb);
-    if (fabsf(q - ((q + kMagic) - kMagic)) > 0.5f - 2.0f * kTieBand) {
-      const double v64 = __ddiv_rn(__dsub_rn(static_cast<double>(f[i]), lo64), step64);
-      c[i] = static_cast<uint32_t>(fmin(fmax(floor(__dadd_rn(v64, 0.5)), 0.0), 255.0));
-    }
-  }
-  w0 = c[0] | (c[1] << 8) | (c[2] << 16) | (c[3] << 24);
-  w1 = c[4] | (c[5] << 8) | (c[6] << 16) | (c[7] << 24);
-}
-
 // Rounding uses the magic constant 1.5 * 2^23: for 0 <= q < 2^22, q + M rounds q to the nearest
 // integer (ties to even) in the low mantissa bits, so the code is the low byte of the sum and
 // rint(q) = (q + M) - M — plain FP32 adds instead of the quarter-rate F2I / FRND pipe.  Exact
-// ties and everything within the band of one are replayed in fp64 below.
+// ties and everything within the band of one are replayed in fp64 below.  q = (v - lo) * inv is
+// formed by subtraction first (as code_of does): v * inv - lo * inv would lose the tie band when
+// |lo| >> hi - lo.
 QA_DEV void codes8(const float (&f)[8], float lo, float inv, double lo64, double step64, uint32_t& w0, uint32_t& w1,
                    int& sum) {
   constexpr float kMagic = 12582912.0f;
-  const unsigned long long inv2 = f2pack(inv, inv);
-  const float nb = -lo * inv;
-  const unsigned long long nb2 = f2pack(nb, nb);
+  const unsigned long long inv2 = f2pack(inv, inv), nlo2 = f2pack(-lo, -lo);
   const unsigned long long m2 = f2pack(kMagic, kMagic), nm2 = f2pack(-kMagic, -kMagic);
   uint32_t r[8];
   bool near = false;
 #pragma unroll
   for (int i = 0; i < 8; i += 2) {
-    const unsigned long long q2 = ffma2r(f2pack(f[i], f[i + 1]), inv2, nb2);
+    const unsigned long long q2 = ffma2r(fadd2(f2pack(f[i], f[i + 1]), nlo2), inv2, 0ull);
     const unsigned long long s2 = fadd2(q2, m2);            // q + M: rounded integer in the low bits
     const unsigned long long d2 = fadd2(q2, fadd2(s2, nm2) ^ 0x8000000080000000ull);  // q - rint(q)
     near |= fabsf(f2lo(d2)) > 0.5f - kTieBand;
@@ -155,7 +111,7 @@ QA_DEV void codes8(const float (&f)[8], float lo, float inv, double lo64, double
     }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const float q = fmaf(f[i], inv, nb);
+      const float q = (f[i] - lo) * inv;
       if (fabsf(q - ((q + kMagic) - kMagic)) > 0.5f - 2.0f * kTieBand) {
         const double v64 = __ddiv_rn(__dsub_rn(static_cast<double>(f[i]), lo64), step64);
         c[i] = static_cast<uint32_t>(fmin(fmax(floor(__dadd_rn(v64, 0.5)), 0.0), 255.0));

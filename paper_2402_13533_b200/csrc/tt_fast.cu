@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(256) k_g1_interleave(const float* __restrict__
 }
 
 template <typename InT, int J1, int R1, bool CODES>
-__global__ void __launch_bounds__(256, 3) k_actquant_z1(const InT* __restrict__ x, int64_t T, int64_t K,
+__global__ void __launch_bounds__(256, 2) k_actquant_z1(const InT* __restrict__ x, int64_t T, int64_t K,
                                                      uint8_t* __restrict__ codes, int64_t ldc,
                                                      float* __restrict__ sx, float* __restrict__ ox,
                                                      int32_t* __restrict__ rsx, const float4* __restrict__ G1i,
@@ -227,222 +227,577 @@ __global__ void __launch_bounds__(256, 3) k_actquant_z1(const InT* __restrict__ 
   }
 }
 
-// Shared-memory-staged variant (production path for bf16 rows): every warp owns one row slot in
-// shared memory; lane 0 fetches the warp's next row with a single cp.async.bulk completing on the
-// warp's mbarrier, so HBM reads need no registers and both passes (stats + Z1, then codes) read
-// shared memory.  Rows are strided over all warps of the grid.
-//   Z1 (J1 >= 2): accumulators are paired over J (zz[a][J/2]) so each bf16 word of x is directly a
-//   packed fp32 operand; G1 comes pre-broadcast ((g, g) pairs, k_g1_bcast).  J1 == 1 (LoRA) pairs
-//   over the rank instead and broadcasts x.
-//   Codes: magic-number rounding; chunks with an element near a rounding tie are recorded in a
-//   per-lane bitmask and replayed exactly in fp64 after the row (rare, ~0.4% of lane-chunks).
+// ---------------------------------------------------------------------------------------------
+// Tensor-core act-quant + Z1 (production path for bf16 rows, J1 in {1, 4}).
+// A CTA of 4 warps owns a tile of TOK token rows staged in shared memory by cp.async.bulk (one
+// copy per row, rows padded so the fragment loads below are bank-conflict free).
+//   pass 1: Z1 on the tensor cores.  Per J, Z1[:, :, J] = X_J · G1 with X_J[t, j1] = x[t, j1 J1 + J]
+//           is an (R1 x 8 tokens) mma.sync m16n8k16 tile: A = [G1_hi | G1_lo]ᵀ (the fp32 core
+//           split into two bf16 terms; x is exact in bf16, products are exact, accumulation fp32),
+//           B = the x row read straight from shared memory (J1 = 4: one PRMT per pair of x words
+//           regroups (j1, j1 + 1) of the same J).  The k-steps are strided over the 4 warps, which
+//           also take the exact bf16 min/max of what they read; partials meet in shared memory
+//           and are summed in fixed warp order (deterministic).
+//   pass 2: per-token codes (reference rule, bit-exact) from the same shared-memory rows.
+// G1 reaches the MMAs as pre-built fragments (k_g1_frag): one 16-byte load per lane per k-step.
 template <int J1, int R1>
-__global__ void __launch_bounds__(256) k_g1_bcast(const float* __restrict__ G1, float4* __restrict__ G1b,
-                                                  int64_t nvec) {
-  constexpr int NQB = (8 / J1) * R1 / 2;  // float4 (g_a, g_a, g_a+1, g_a+1) per chunk
+__global__ void __launch_bounds__(256) k_g1_frag(const float* __restrict__ G1, uint4* __restrict__ frag,
+                                                 int64_t nsteps) {
+  constexpr int MT = R1 / 8;  // m16 tiles: R1 = 8 -> rows (hi a | lo a); R1 = 16 -> tile 0 hi, tile 1 lo
   const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (idx >= nvec * NQB) return;
-  const int64_t c = idx / NQB;
-  const int q = static_cast<int>(idx % NQB);
-  const int jj = q / (R1 / 2), a = 2 * (q % (R1 / 2));
-  const float* g = G1 + (c * (8 / J1) + jj) * R1 + a;
-  G1b[((c / 32) * NQB + q) * 32 + (c % 32)] = make_float4(g[0], g[0], g[1], g[1]);
+  if (idx >= nsteps * MT * 32) return;
+  const int lane = static_cast<int>(idx % 32), mt = static_cast<int>((idx / 32) % MT);
+  const int64_t s = idx / (32 * MT);
+  const int g = lane >> 2, c = lane & 3;
+  uint32_t w[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int m = g + 8 * (q & 1);  // a0a1: (g, 2c), a2a3: (g+8, 2c), a4a5: (g, 2c+8), a6a7: (g+8, 2c+8)
+    const int term = R1 == 8 ? (m >> 3) : mt;
+    const int a = R1 == 8 ? (m & 7) : m;
+    uint32_t packed = 0;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int kk = 2 * c + 8 * (q >> 1) + e;
+      int64_t j;
+      if (J1 == 4) {
+        j = 16 * s + kk;
+      } else {  // LoRA: MMA u of super-step S reads x[64 S + 16 c' + 4 u + {0,1}] (b0) and {2,3} (b1)
+        const int64_t S = s >> 2;
+        const int u = static_cast<int>(s & 3);
+        j = 64 * S + 16 * ((kk & 7) >> 1) + 4 * u + 2 * (kk >> 3) + (kk & 1);
+      }
+      const float v = G1[j * R1 + a];
+      const __nv_bfloat16 hv = __float2bfloat16_rn(v);
+      const __nv_bfloat16 t = term == 0 ? hv : __float2bfloat16_rn(v - __bfloat162float(hv));
+      packed |= static_cast<uint32_t>(__bfloat16_as_ushort(t)) << (16 * e);
+    }
+    w[q] = packed;
+  }
+  frag[idx] = make_uint4(w[0], w[1], w[2], w[3]);
 }
 
-template <int J1, int R1, bool CODES>
-__global__ void __launch_bounds__(512) k_actquant_z1_s(const __nv_bfloat16* __restrict__ x, int64_t T, int64_t K,
-                                                       uint8_t* __restrict__ codes, int64_t ldc,
-                                                       float* __restrict__ sx, float* __restrict__ ox,
-                                                       int32_t* __restrict__ rsx, const float4* __restrict__ G1g,
-                                                       __nv_bfloat16* __restrict__ zb, int64_t ldzb,
-                                                       float* __restrict__ zf) {
-  constexpr int K2 = J1 * R1;
-  static_assert(K2 == 8 || K2 == 16 || K2 == 32 || K2 == 64, "unsupported Z1 width");
-  constexpr int NQ = 2 * R1 / J1;  // float4 G1 pieces per chunk (interleaved layout, k_g1_interleave)
-  extern __shared__ __align__(128) uint8_t aq_smem[];
-  __shared__ uint64_t aq_bar[16];
-  const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
-  const uint32_t rowbytes = static_cast<uint32_t>(K * 2);
-  const uint32_t slot_bytes = (rowbytes + 127u) & ~127u;
-  uint8_t* slot = aq_smem + warp * slot_bytes;
-  uint64_t* bar = &aq_bar[warp];
-  const int64_t nwarps_grid = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
-  int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + warp;
-  const uint32_t nvec = static_cast<uint32_t>(K / 8);
-  if (lane == 0) {
-    mbar_init(bar, 1);
+// Per-row constants of the act-quant rule for the byte-grid code path below.
+struct AqRow {
+  float lo, inv, nbh;   // nbh = 1/2 - lo * inv
+  double lo64, step64;  // the reference's fp64 quantities (tie replays)
+};
+
+// q' = (v - lo) / step + 1/2 for the two bf16 of w, packed.  SUB = false evaluates v * inv + nbh
+// (one FFMA2; used when |lo * inv| <= 512, error < 1e-4), SUB = true subtracts first (rows whose
+// offset dwarfs their range, where v * inv - lo * inv would cancel catastrophically).
+template <bool SUB>
+QA_DEV unsigned long long aq_q2(uint32_t w, unsigned long long inv2, unsigned long long nbh2,
+                                unsigned long long nlo2) {
+  const unsigned long long v2 = f2pack(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
+  if constexpr (SUB)
+    return ffma2r(fadd2(v2, nlo2), inv2, f2pack(0.5f, 0.5f));
+  else
+    return ffma2r(v2, inv2, nbh2);
+}
+template <bool SUB>
+QA_DEV float aq_q1(float v, const AqRow& r) {
+  return SUB ? fmaf(v - r.lo, r.inv, 0.5f) : fmaf(v, r.inv, r.nbh);
+}
+
+// Codes of 8 elements: s = q' + 1.5 * 2^15 puts q' on a 2^-8 grid inside the mantissa, so byte 1
+// of s is floor(q') (the code, round half up) and byte 0 the fraction.  A zero fraction byte means
+// q' is within 2^-9 of an integer — possibly a rounding tie of the reference — and flags the chunk
+// for aq_codes_fix.
+template <bool SUB>
+QA_DEV void aq_codes8(const uint4 raw, unsigned long long inv2, unsigned long long nbh2, unsigned long long nlo2,
+                      uint32_t& c0, uint32_t& c1, bool& near) {
+  const unsigned long long m2 = f2pack(49152.0f, 49152.0f);
+  const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+  uint32_t s[8];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const unsigned long long s2 = fadd2(aq_q2<SUB>(w[i], inv2, nbh2, nlo2), m2);
+    s[2 * i] = static_cast<uint32_t>(s2);
+    s[2 * i + 1] = static_cast<uint32_t>(s2 >> 32);
+  }
+  c0 = __byte_perm(__byte_perm(s[0], s[1], 0x0051), __byte_perm(s[2], s[3], 0x0051), 0x5410);
+  c1 = __byte_perm(__byte_perm(s[4], s[5], 0x0051), __byte_perm(s[6], s[7], 0x0051), 0x5410);
+  const uint32_t f0 = __byte_perm(__byte_perm(s[0], s[1], 0x0040), __byte_perm(s[2], s[3], 0x0040), 0x5410);
+  const uint32_t f1 = __byte_perm(__byte_perm(s[4], s[5], 0x0040), __byte_perm(s[6], s[7], 0x0040), 0x5410);
+  near = (((f0 - 0x01010101u) & ~f0) | ((f1 - 0x01010101u) & ~f1)) & 0x80808080u;
+}
+
+// Resolve the flagged elements of a chunk.  With s rounded to the integer n, floor(q') is n when
+// q' >= n and n - 1 otherwise; the fp32 q' decides that unless it lies within kTieBand of n (far
+// above its error), where the reference's fp64 arithmetic is replayed exactly.
+template <bool SUB>
+QA_DEV void aq_codes_fix(const uint4 raw, const AqRow& r, uint32_t& c0, uint32_t& c1) {
+  const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float v = __uint_as_float((i & 1) ? (w[i >> 1] & 0xFFFF0000u) : (w[i >> 1] << 16));
+    const float q = aq_q1<SUB>(v, r);
+    const float s = q + 49152.0f;
+    if ((__float_as_uint(s) & 0xFFu) != 0u) continue;
+    const float n = s - 49152.0f;  // exact
+    const float d = q - n;         // exact (Sterbenz)
+    uint32_t code;
+    if (fabsf(d) < kTieBand) {
+      const double v64 = __ddiv_rn(__dsub_rn(static_cast<double>(v), r.lo64), r.step64);
+      code = static_cast<uint32_t>(fmin(fmax(floor(__dadd_rn(v64, 0.5)), 0.0), 255.0));
+    } else {
+      code = static_cast<uint32_t>(n) - (d < 0.0f ? 1u : 0u);
+    }
+    uint32_t& word = i < 4 ? c0 : c1;
+    const int sh = 8 * (i & 3);
+    word = (word & ~(0xFFu << sh)) | (code << sh);
+  }
+}
+
+// Codes for one warp's chunk range [cb, ce) of a shared-memory bf16 row (8 elements per chunk);
+// returns the lane's code sum.  Flags are kept per lane in a bitmask (bit k = the lane's k-th
+// chunk) and resolved after the streaming loop, so the loop itself stays branch-free.
+template <bool SUB>
+QA_DEV uint32_t aq_codes_run(const uint4* srow, uint32_t cb, uint32_t ce, const AqRow& r, uint8_t* dst) {
+  const uint32_t lane = lane_id();
+  const unsigned long long inv2 = f2pack(r.inv, r.inv), nbh2 = f2pack(r.nbh, r.nbh), nlo2 = f2pack(-r.lo, -r.lo);
+  const uint32_t first = cb + lane;
+  const uint32_t cnt = first < ce ? (ce - first + 31) / 32 : 0;
+  const uint4* src = srow + first;
+  uint2* out = reinterpret_cast<uint2*>(dst) + first;
+  unsigned long long mask = 0ull;
+  uint32_t sum = 0;
+  uint32_t k0 = 0;
+  for (; k0 + 4 <= cnt; k0 += 4) {  // unguarded groups: four independent chains per iteration
+    uint4 raw[4];
+#pragma unroll
+    for (uint32_t u = 0; u < 4; ++u) raw[u] = src[(k0 + u) * 32];
+    uint32_t m4 = 0;
+#pragma unroll
+    for (uint32_t u = 0; u < 4; ++u) {
+      uint2 packed;
+      bool near;
+      aq_codes8<SUB>(raw[u], inv2, nbh2, nlo2, packed.x, packed.y, near);
+      m4 |= static_cast<uint32_t>(near) << u;
+      sum = __dp4a(packed.x, 0x01010101u, sum);
+      sum = __dp4a(packed.y, 0x01010101u, sum);
+      out[(k0 + u) * 32] = packed;
+    }
+    mask |= static_cast<unsigned long long>(m4) << k0;
+  }
+  for (; k0 < cnt; ++k0) {
+    uint2 packed;
+    bool near;
+    aq_codes8<SUB>(src[k0 * 32], inv2, nbh2, nlo2, packed.x, packed.y, near);
+    mask |= static_cast<unsigned long long>(near) << k0;
+    sum = __dp4a(packed.x, 0x01010101u, sum);
+    sum = __dp4a(packed.y, 0x01010101u, sum);
+    out[k0 * 32] = packed;
+  }
+  while (mask != 0ull) {
+    const uint32_t k = static_cast<uint32_t>(__ffsll(static_cast<long long>(mask)) - 1);
+    mask &= mask - 1;
+    const uint4 raw = src[k * 32];
+    uint2 old;  // recomputed rather than read back from global memory (a full L2 round trip)
+    bool near;
+    aq_codes8<SUB>(raw, inv2, nbh2, nlo2, old.x, old.y, near);
+    uint2 fixed = old;
+    aq_codes_fix<SUB>(raw, r, fixed.x, fixed.y);
+    sum += (__dp4a(fixed.x, 0x01010101u, 0u) + __dp4a(fixed.y, 0x01010101u, 0u)) -
+           (__dp4a(old.x, 0x01010101u, 0u) + __dp4a(old.y, 0x01010101u, 0u));
+    out[k * 32] = fixed;
+  }
+  return sum;
+}
+
+QA_DEV int aq_codes_range(const uint4* srow, uint32_t cb, uint32_t ce, float lo, float hi, uint8_t* dst) {
+  const uint32_t lane = lane_id();
+  AqRow r;
+  r.lo = lo;
+  r.lo64 = static_cast<double>(lo);
+  r.step64 = __ddiv_rn(__dsub_rn(static_cast<double>(hi), r.lo64), 255.0);
+  if (!(r.step64 > 0.0)) {  // flat row: every code is 0
+    for (uint32_t c = cb + lane; c < ce; c += 32) *reinterpret_cast<uint2*>(dst + c * 8) = make_uint2(0u, 0u);
+    return 0;
+  }
+  r.inv = static_cast<float>(1.0 / r.step64);
+  const float nb = -lo * r.inv;
+  r.nbh = nb + 0.5f;
+  const uint32_t sum = fabsf(nb) <= 512.0f ? aq_codes_run<false>(srow, cb, ce, r, dst)
+                                           : aq_codes_run<true>(srow, cb, ce, r, dst);
+  return static_cast<int>(sum);
+}
+
+template <int J1>
+__host__ __device__ constexpr uint32_t aq_row_pad() {
+  return J1 == 4 ? 64u : 16u;
+}
+
+// CTA: 8 warps, tiles of TOK = 4 token rows (the n8 MMA columns 4..7 repeat rows 0..3), NBUF tile
+// buffers in a ring so the next tiles stream in while one is processed.
+constexpr int AQ_TOK = 4, AQ_NW = 8;
+
+template <int J1, int R1, int NBUF, bool CODES>
+__global__ void __launch_bounds__(AQ_NW * 32) k_aq_mma(const __nv_bfloat16* __restrict__ x, int64_t T, int64_t K,
+                                                      uint8_t* __restrict__ codes, int64_t ldc,
+                                                      float* __restrict__ sx, float* __restrict__ ox,
+                                                      int32_t* __restrict__ rsx, const uint4* __restrict__ frag,
+                                                      __nv_bfloat16* __restrict__ zb, int64_t ldzb,
+                                                      float* __restrict__ zf) {
+  constexpr int K2 = J1 * R1, MT = R1 / 8, NJ = J1 == 4 ? 4 : 1, TOK = AQ_TOK, NW = AQ_NW, PARTS = NW / TOK;
+  static_assert(J1 == 1 || J1 == 4, "J1");
+  static_assert(R1 == 8 || R1 == 16, "R1");
+  extern __shared__ __align__(128) uint8_t aq_tile[];
+  __shared__ uint64_t bars[NBUF];
+  __shared__ float s_lo[NW][TOK], s_hi[NW][TOK];
+  __shared__ float s_red[NW][TOK * K2];
+  __shared__ int s_sum[TOK][PARTS];
+  const uint32_t warp = threadIdx.x >> 5, lane = lane_id(), g = lane >> 2, c = lane & 3;
+  const uint32_t rowbytes = static_cast<uint32_t>(K * 2), stride = rowbytes + aq_row_pad<J1>();
+  const uint32_t nsteps = static_cast<uint32_t>(K / 64), nvec = static_cast<uint32_t>(K / 8);
+  const int64_t ntiles = (T + TOK - 1) / TOK;
+  auto issue = [&](int64_t t, int b) {
+    const int nr = static_cast<int>(T - t * TOK < TOK ? T - t * TOK : TOK);
+    mbar_arrive_expect_tx(&bars[b], static_cast<uint32_t>(nr) * rowbytes);
+    for (int r = 0; r < nr; ++r)
+      bulk_load(aq_tile + (b * TOK + r) * stride, x + (t * TOK + r) * K, rowbytes, &bars[b]);
+  };
+  int64_t tile = blockIdx.x;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int b = 0; b < NBUF; ++b) mbar_init(&bars[b], 1);
     fence_barrier_init();
-    if (row < T) {
-      mbar_arrive_expect_tx(bar, rowbytes);
-      bulk_load(slot, x + row * K, rowbytes, bar);
+#pragma unroll
+    for (int b = 0; b < NBUF; ++b)
+      if (tile + static_cast<int64_t>(b) * gridDim.x < ntiles) issue(tile + static_cast<int64_t>(b) * gridDim.x, b);
+  }
+  __syncthreads();
+  for (uint32_t it = 0; tile < ntiles; ++it, tile += gridDim.x) {
+    const int b = static_cast<int>(it % NBUF);
+    const uint8_t* buf = aq_tile + b * TOK * stride;
+    const int64_t r0 = tile * TOK;
+    const int nr = static_cast<int>(T - r0 < TOK ? T - r0 : TOK);
+    mbar_wait(&bars[b], (it / NBUF) & 1);
+    // ---- pass 1: Z1 partials on the tensor cores (+ exact bf16 min/max when codes are wanted)
+    const uint8_t* myrow = buf + (g % TOK) * stride;
+    float acc[NJ][MT][4];
+#pragma unroll
+    for (int J = 0; J < NJ; ++J)
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[J][mt][i] = 0.f;
+    __nv_bfloat162 lo2 = __floats2bfloat162_rn(INFINITY, INFINITY), hi2 = __floats2bfloat162_rn(-INFINITY, -INFINITY);
+#pragma unroll 2
+    for (uint32_t st = warp; st < nsteps; st += NW) {
+      const uint8_t* p = myrow + 128u * st;
+      const uint4 p0 = *reinterpret_cast<const uint4*>(p + (J1 == 4 ? 16u * c : 32u * c));
+      const uint4 p1 = *reinterpret_cast<const uint4*>(p + (J1 == 4 ? 64u + 16u * c : 32u * c + 16u));
+      const uint32_t w[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+      if constexpr (CODES) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const __nv_bfloat162 b2 = *reinterpret_cast<const __nv_bfloat162*>(&w[i]);
+          lo2 = __hmin2(lo2, b2);
+          hi2 = __hmax2(hi2, b2);
+        }
+      }
+      if constexpr (J1 == 4) {
+        uint4 fr[MT];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) fr[mt] = __ldg(frag + (static_cast<size_t>(st) * MT + mt) * 32 + lane);
+#pragma unroll
+        for (int J = 0; J < 4; ++J) {
+          const uint32_t sel = (J & 1) ? 0x7632u : 0x5410u;
+          const uint32_t b0 = __byte_perm(w[J >> 1], w[2 + (J >> 1)], sel);
+          const uint32_t b1 = __byte_perm(w[4 + (J >> 1)], w[6 + (J >> 1)], sel);
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) mma_16816(acc[J][mt], fr[mt].x, fr[mt].y, fr[mt].z, fr[mt].w, b0, b1);
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) {
+            const uint4 fr = __ldg(frag + ((static_cast<size_t>(st) * 4 + u) * MT + mt) * 32 + lane);
+            mma_16816(acc[0][mt], fr.x, fr.y, fr.z, fr.w, w[2 * u], w[2 * u + 1]);
+          }
+        }
+      }
+    }
+    if constexpr (CODES) {  // per-token stats: the 4 lanes of a group share token g % TOK
+      float lo = fminf(__low2float(lo2), __high2float(lo2)), hi = fmaxf(__low2float(hi2), __high2float(hi2));
+#pragma unroll
+      for (int o = 1; o < 4; o <<= 1) {
+        lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+      }
+      if (c == 0 && g < TOK) {
+        s_lo[warp][g] = lo;
+        s_hi[warp][g] = hi;
+      }
+    }
+    if (2 * c < TOK) {  // D columns 2c, 2c + 1 are tokens 2c, 2c + 1
+#pragma unroll
+      for (int J = 0; J < NJ; ++J)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t t = 2 * c + h;
+          if constexpr (MT == 1) {
+            s_red[warp][t * K2 + g * J1 + J] = acc[J][0][h] + acc[J][0][2 + h];
+          } else {
+            s_red[warp][t * K2 + g * J1 + J] = acc[J][0][h] + acc[J][1][h];
+            s_red[warp][t * K2 + (g + 8) * J1 + J] = acc[J][0][2 + h] + acc[J][1][2 + h];
+          }
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < nr * K2; i += NW * 32) {
+      float v = s_red[0][i];
+#pragma unroll
+      for (int w = 1; w < NW; ++w) v += s_red[w][i];
+      const int64_t row = r0 + i / K2;
+      const int col = i % K2;
+      if (zf != nullptr) zf[row * K2 + col] = v;
+      if (zb != nullptr) {
+        const __nv_bfloat16 hv = __float2bfloat16_rn(v);
+        zb[row * ldzb + col] = hv;
+        zb[row * ldzb + K2 + col] = __float2bfloat16_rn(v - __bfloat162float(hv));
+        zb[row * ldzb + 2 * K2 + col] = hv;
+      }
+    }
+    if (zb != nullptr && ldzb > 3 * K2) {
+      const int padw = static_cast<int>(ldzb - 3 * K2);
+      for (int i = threadIdx.x; i < nr * padw; i += NW * 32)
+        zb[(r0 + i / padw) * ldzb + 3 * K2 + i % padw] = __float2bfloat16_rn(0.f);
+    }
+    if constexpr (CODES) {
+      // ---- pass 2: codes; warp w takes part w / TOK of token w % TOK
+      const int t = static_cast<int>(warp % TOK), part = static_cast<int>(warp / TOK);
+      if (t < nr) {
+        float tlo = s_lo[0][t], thi = s_hi[0][t];
+#pragma unroll
+        for (int w = 1; w < NW; ++w) {
+          tlo = fminf(tlo, s_lo[w][t]);
+          thi = fmaxf(thi, s_hi[w][t]);
+        }
+        const uint32_t cb = (nvec * part) / PARTS, ce = (nvec * (part + 1)) / PARTS;
+        uint8_t* dst = codes + (r0 + t) * ldc;
+        int sum = aq_codes_range(reinterpret_cast<const uint4*>(buf + t * stride), cb, ce, tlo, thi, dst);
+        sum = warp_sum_i(sum);
+        if (lane == 0) s_sum[t][part] = sum;
+        if (part == PARTS - 1)
+          for (int64_t kk = K + lane; kk < ldc; kk += 32) dst[kk] = 0;
+        if (part == 0 && lane == 0) {
+          const double step64 = __ddiv_rn(__dsub_rn(static_cast<double>(thi), static_cast<double>(tlo)), 255.0);
+          sx[r0 + t] = step64 > 0.0 ? __double2float_rn(step64) : 0.0f;
+          ox[r0 + t] = tlo;
+        }
+      }
+    }
+    __syncthreads();  // the tile buffer, s_red, s_lo/s_hi are free again
+    if constexpr (CODES) {
+      if (threadIdx.x < static_cast<uint32_t>(nr)) {
+        int sum = 0;
+#pragma unroll
+        for (int p = 0; p < PARTS; ++p) sum += s_sum[threadIdx.x][p];
+        rsx[r0 + threadIdx.x] = sum;
+      }
+    }
+    const int64_t next = tile + static_cast<int64_t>(NBUF) * gridDim.x;
+    if (threadIdx.x == 0 && next < ntiles) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(next, b);
     }
   }
-  __syncwarp();
-  const uint4* srow = reinterpret_cast<const uint4*>(slot);
-  for (uint32_t it = 0; row < T; ++it, row += nwarps_grid) {
-    mbar_wait(bar, it & 1);
-    // ---- pass 1: exact bf16 min/max and Z1
-    float z[K2];
-    __nv_bfloat162 lo2 = __floats2bfloat162_rn(INFINITY, INFINITY), hi2 = __floats2bfloat162_rn(-INFINITY, -INFINITY);
+}
+
+// Barrier-free pipelined variant (rows up to ~4.6K elements): a producer warp streams tiles of 8
+// token rows into an NBUF-deep ring (full/empty mbarriers); each of the 8 consumer warps takes
+// 1/8 of the tile's Z1 k-steps on the tensor cores, publishes its partial (zred mbarrier), then
+// owns one token row end to end — exact bf16 min/max scan and codes.  The warp it % 8 sums the
+// partials in fixed order (deterministic) and writes Z1.  Warps never wait for each other's codes,
+// so the per-row cost variance (tie replays) is absorbed by the ring instead of a CTA barrier.
+constexpr int AQP_TOK = 8, AQP_NC = 8;
+
+template <int J1>
+__host__ __device__ constexpr uint32_t aqp_row_pad() {
+  return J1 == 4 ? 64u : 16u;
+}
+
+template <int J1, int R1, int NBUF, bool CODES>
+__global__ void __launch_bounds__((AQP_NC + 1) * 32, 1)
+    k_aq_pipe(const __nv_bfloat16* __restrict__ x, int64_t T, int64_t K, uint8_t* __restrict__ codes, int64_t ldc,
+              float* __restrict__ sx, float* __restrict__ ox, int32_t* __restrict__ rsx,
+              const uint4* __restrict__ frag, __nv_bfloat16* __restrict__ zb, int64_t ldzb, float* __restrict__ zf) {
+  constexpr int K2 = J1 * R1, MT = R1 / 8, NJ = J1 == 4 ? 4 : 1, TOK = AQP_TOK, NC = AQP_NC;
+  static_assert(J1 == 1 || J1 == 4, "J1");
+  static_assert(R1 == 8 || R1 == 16, "R1");
+  extern __shared__ __align__(128) uint8_t aq_tile[];
+  __shared__ uint64_t full[NBUF], empty[NBUF], zred[NBUF];
+  const uint32_t warp = threadIdx.x >> 5, lane = lane_id(), g = lane >> 2, c = lane & 3;
+  const uint32_t rowbytes = static_cast<uint32_t>(K * 2), stride = rowbytes + aqp_row_pad<J1>();
+  const uint32_t nsteps = static_cast<uint32_t>(K / 64), nvec = static_cast<uint32_t>(K / 8);
+  const int64_t ntiles = (T + TOK - 1) / TOK;
+  float* s_red = reinterpret_cast<float*>(aq_tile + static_cast<size_t>(NBUF) * TOK * stride);  // [NBUF][NC][TOK*K2]
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int b = 0; b < NBUF; ++b) {
+      mbar_init(&full[b], 1);
+      mbar_init(&empty[b], NC);
+      mbar_init(&zred[b], NC);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (warp == NC) {  // ---- producer
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+        const int b = static_cast<int>(it % NBUF);
+        if (it >= static_cast<uint32_t>(NBUF)) mbar_wait(&empty[b], ((it / NBUF) - 1) & 1);
+        const int nr = static_cast<int>(T - tile * TOK < TOK ? T - tile * TOK : TOK);
+        mbar_arrive_expect_tx(&full[b], static_cast<uint32_t>(nr) * rowbytes);
+        for (int r = 0; r < nr; ++r)
+          bulk_load(aq_tile + (b * TOK + r) * stride, x + (tile * TOK + r) * K, rowbytes, &full[b]);
+      }
+    }
+    return;
+  }
+  uint32_t it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int b = static_cast<int>(it % NBUF);
+    const uint32_t ph = (it / NBUF) & 1;
+    const uint8_t* buf = aq_tile + b * TOK * stride;
+    const int64_t r0 = tile * TOK;
+    const int nr = static_cast<int>(T - r0 < TOK ? T - r0 : TOK);
+    mbar_wait(&full[b], ph);
+    // ---- Z1 partial over this warp's k-steps
     {
-      constexpr int RP = R1 / 2;
-      unsigned long long zz[J1][RP];  // zz[J][p] = (z[2p, J], z[2p+1, J]): pairs over the rank
+      const uint8_t* myrow = buf + g * stride;
+      float acc[NJ][MT][4];
 #pragma unroll
-      for (int J = 0; J < J1; ++J)
+      for (int J = 0; J < NJ; ++J)
 #pragma unroll
-        for (int p = 0; p < RP; ++p) zz[J][p] = 0ull;
-#pragma unroll 2
-      for (uint32_t c = lane; c < nvec; c += 32) {
-        const uint4 raw = srow[c];
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) acc[J][mt][i] = 0.f;
+      auto kstep = [&](uint32_t st) {
+        const uint8_t* p = myrow + 128u * st;
+        const uint4 p0 = *reinterpret_cast<const uint4*>(p + (J1 == 4 ? 16u * c : 32u * c));
+        const uint4 p1 = *reinterpret_cast<const uint4*>(p + (J1 == 4 ? 64u + 16u * c : 32u * c + 16u));
+        const uint32_t w[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+        if constexpr (J1 == 4) {
+          uint4 fr[MT];
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) fr[mt] = __ldg(frag + (static_cast<size_t>(st) * MT + mt) * 32 + lane);
+#pragma unroll
+          for (int J = 0; J < 4; ++J) {
+            const uint32_t sel = (J & 1) ? 0x7632u : 0x5410u;
+            const uint32_t b0 = __byte_perm(w[J >> 1], w[2 + (J >> 1)], sel);
+            const uint32_t b1 = __byte_perm(w[4 + (J >> 1)], w[6 + (J >> 1)], sel);
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) mma_16816(acc[J][mt], fr[mt].x, fr[mt].y, fr[mt].z, fr[mt].w, b0, b1);
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+              const uint4 fr = __ldg(frag + ((static_cast<size_t>(st) * 4 + u) * MT + mt) * 32 + lane);
+              mma_16816(acc[0][mt], fr.x, fr.y, fr.z, fr.w, w[2 * u], w[2 * u + 1]);
+            }
+          }
+        }
+      };
+      uint32_t st = warp;
+      for (; st + NC < nsteps; st += 2 * NC) {  // two independent steps per iteration, no guards
+        kstep(st);
+        kstep(st + NC);
+      }
+      if (st < nsteps) kstep(st);
+      float* red = s_red + (static_cast<size_t>(b) * NC + warp) * (TOK * K2);
+#pragma unroll
+      for (int J = 0; J < NJ; ++J)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t t = 2 * c + h;  // D columns 2c, 2c + 1 are tokens 2c, 2c + 1
+          if constexpr (MT == 1) {
+            red[t * K2 + g * J1 + J] = acc[J][0][h] + acc[J][0][2 + h];
+          } else {
+            red[t * K2 + g * J1 + J] = acc[J][0][h] + acc[J][1][h];
+            red[t * K2 + (g + 8) * J1 + J] = acc[J][0][2 + h] + acc[J][1][2 + h];
+          }
+        }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&zred[b]);
+    }
+    // ---- codes of token row `warp`
+    if (CODES && static_cast<int>(warp) < nr) {
+      const uint4* srow = reinterpret_cast<const uint4*>(buf + warp * stride);
+      __nv_bfloat162 lo2 = __floats2bfloat162_rn(INFINITY, INFINITY), hi2 = __floats2bfloat162_rn(-INFINITY, -INFINITY);
+      uint32_t cc = lane;
+      for (; cc + 96 < nvec; cc += 128) {
+        uint4 raw[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) raw[u] = srow[cc + 32 * u];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t w[4] = {raw[u].x, raw[u].y, raw[u].z, raw[u].w};
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const __nv_bfloat162 b2 = *reinterpret_cast<const __nv_bfloat162*>(&w[i]);
+            lo2 = __hmin2(lo2, b2);
+            hi2 = __hmax2(hi2, b2);
+          }
+        }
+      }
+      for (; cc < nvec; cc += 32) {
+        const uint4 raw = srow[cc];
         const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
-        float f[8];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const __nv_bfloat162 b2 = *reinterpret_cast<const __nv_bfloat162*>(&w[i]);
           lo2 = __hmin2(lo2, b2);
           hi2 = __hmax2(hi2, b2);
-          f[2 * i] = __uint_as_float(w[i] << 16);
-          f[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
-        }
-        const float4* gp = G1g + ((c >> 5) * NQ) * 32 + (c & 31);
-        unsigned long long g2[2 * NQ];  // [8 / J1 rows][RP]
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-          const float4 v = __ldg(gp + q * 32);
-          g2[2 * q] = f2pack(v.x, v.y);
-          g2[2 * q + 1] = f2pack(v.z, v.w);
-        }
-#pragma unroll
-        for (int jj = 0; jj < 8 / J1; ++jj)
-#pragma unroll
-          for (int J = 0; J < J1; ++J) {
-            const unsigned long long xb = f2pack(f[jj * J1 + J], f[jj * J1 + J]);
-#pragma unroll
-            for (int p = 0; p < RP; ++p) ffma2(zz[J][p], xb, g2[jj * RP + p]);
-          }
-      }
-#pragma unroll
-      for (int J = 0; J < J1; ++J)
-#pragma unroll
-        for (int p = 0; p < RP; ++p) {
-          z[(2 * p) * J1 + J] = f2lo(zz[J][p]);
-          z[(2 * p + 1) * J1 + J] = f2hi(zz[J][p]);
-        }
-    }
-    if (K2 >= 32) {
-#pragma unroll
-      for (int b = 0; b < K2; b += 32) warp_reduce_scatter32<K2>(z, b);
-#pragma unroll
-      for (int b = 0; b < K2; b += 32) {
-        const float v = z[b];
-        if (zf != nullptr) zf[row * K2 + b + lane] = v;
-        if (zb != nullptr) {
-          const __nv_bfloat16 hv = __float2bfloat16_rn(v);
-          zb[row * ldzb + b + lane] = hv;
-          zb[row * ldzb + K2 + b + lane] = __float2bfloat16_rn(v - __bfloat162float(hv));
-          zb[row * ldzb + 2 * K2 + b + lane] = hv;
         }
       }
-    } else {
-#pragma unroll
-      for (int i = 0; i < K2; ++i) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) z[i] += __shfl_xor_sync(0xffffffffu, z[i], o);
-      }
-#pragma unroll
-      for (int i = 0; i < K2; ++i) {
-        if (lane == static_cast<uint32_t>(i)) {
-          if (zf != nullptr) zf[row * K2 + i] = z[i];
-          if (zb != nullptr) {
-            const __nv_bfloat16 hv = __float2bfloat16_rn(z[i]);
-            zb[row * ldzb + i] = hv;
-            zb[row * ldzb + K2 + i] = __float2bfloat16_rn(z[i] - __bfloat162float(hv));
-            zb[row * ldzb + 2 * K2 + i] = hv;
-          }
-        }
-      }
-    }
-    if (zb != nullptr)
-      for (int64_t i = 3 * K2 + lane; i < ldzb; i += 32) zb[row * ldzb + i] = __float2bfloat16_rn(0.f);
-    if constexpr (CODES) {
-      // ---- pass 2: codes (reference rule, bit-exact) from the same shared-memory row
-      float lo = fminf(__low2float(lo2), __high2float(lo2));
-      float hi = fmaxf(__low2float(hi2), __high2float(hi2));
-      lo = warp_min(lo);
-      hi = warp_max(hi);
-      const double lo64 = static_cast<double>(lo);
-      const double step64 = __ddiv_rn(__dsub_rn(static_cast<double>(hi), lo64), 255.0);
-      const bool flat = !(step64 > 0.0);
-      const float inv = flat ? 0.0f : static_cast<float>(1.0 / step64);
-      const float nb = -lo * inv;
-      const unsigned long long inv2 = f2pack(inv, inv), nb2 = f2pack(nb, nb);
+      const float lo = warp_min(fminf(__low2float(lo2), __high2float(lo2)));
+      const float hi = warp_max(fmaxf(__low2float(hi2), __high2float(hi2)));
+      const int64_t row = r0 + warp;
       uint8_t* dst = codes + row * ldc;
-      int sum = 0;
-      if (flat) {
-        for (uint32_t c = lane; c < nvec; c += 32) *reinterpret_cast<uint2*>(dst + c * 8) = make_uint2(0u, 0u);
-      } else {
-        unsigned long long near_mask[2] = {0ull, 0ull};
-        uint32_t k = 0;
-#pragma unroll 2
-        for (uint32_t c = lane; c < nvec; c += 32, ++k) {
-          const uint4 raw = srow[c];
-          const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
-          float f[8];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            f[2 * i] = __uint_as_float(w[i] << 16);
-            f[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
-          }
-          uint2 packed;
-          if (codes8_fast(f, inv2, nb2, packed.x, packed.y)) {
-            if (k < 64)
-              near_mask[0] |= 1ull << k;
-            else
-              near_mask[1] |= 1ull << (k - 64);
-          }
-          sum = static_cast<int>(__dp4a(packed.x, 0x01010101u, static_cast<unsigned int>(sum)));
-          sum = static_cast<int>(__dp4a(packed.y, 0x01010101u, static_cast<unsigned int>(sum)));
-          *reinterpret_cast<uint2*>(dst + c * 8) = packed;
-        }
-        // exact fp64 replay of the flagged chunks (same lane, so program order covers the rewrite)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          while (near_mask[h] != 0ull) {
-            const int bit = __ffsll(static_cast<long long>(near_mask[h])) - 1;
-            near_mask[h] &= near_mask[h] - 1;
-            const uint32_t c = lane + 32u * (static_cast<uint32_t>(h) * 64u + static_cast<uint32_t>(bit));
-            const uint4 raw = srow[c];
-            const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
-            float f[8];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              f[2 * i] = __uint_as_float(w[i] << 16);
-              f[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
-            }
-            uint2 old = *reinterpret_cast<const uint2*>(dst + c * 8);
-            uint2 fixed = old;
-            codes8_exact(f, inv, nb, lo64, step64, fixed.x, fixed.y);
-            sum += static_cast<int>(__dp4a(fixed.x, 0x01010101u, 0u) + __dp4a(fixed.y, 0x01010101u, 0u)) -
-                   static_cast<int>(__dp4a(old.x, 0x01010101u, 0u) + __dp4a(old.y, 0x01010101u, 0u));
-            *reinterpret_cast<uint2*>(dst + c * 8) = fixed;
-          }
-        }
-      }
+      int sum = aq_codes_range(srow, 0, nvec, lo, hi, dst);
       for (int64_t kk = K + lane; kk < ldc; kk += 32) dst[kk] = 0;
       sum = warp_sum_i(sum);
       if (lane == 0) {
-        sx[row] = flat ? 0.0f : __double2float_rn(step64);
+        const double step64 = __ddiv_rn(__dsub_rn(static_cast<double>(hi), static_cast<double>(lo)), 255.0);
+        sx[row] = step64 > 0.0 ? __double2float_rn(step64) : 0.0f;
         ox[row] = lo;
         rsx[row] = sum;
       }
     }
-    // all lanes are done with the slot: fetch this warp's next row into it
-    __syncwarp();
-    if (lane == 0 && row + nwarps_grid < T) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive_expect_tx(bar, rowbytes);
-      bulk_load(slot, x + (row + nwarps_grid) * K, rowbytes, bar);
+    // ---- Z1 of the tile (rotating finalizer), then release the buffer
+    if (warp == it % NC) {
+      mbar_wait(&zred[b], ph);
+      const float* red = s_red + static_cast<size_t>(b) * NC * (TOK * K2);
+      for (int i = static_cast<int>(lane); i < nr * K2; i += 32) {
+        float v = red[i];
+#pragma unroll
+        for (int w = 1; w < NC; ++w) v += red[w * (TOK * K2) + i];
+        const int64_t row = r0 + i / K2;
+        const int col = i % K2;
+        if (zf != nullptr) zf[row * K2 + col] = v;
+        if (zb != nullptr) {
+          const __nv_bfloat16 hv = __float2bfloat16_rn(v);
+          zb[row * ldzb + col] = hv;
+          zb[row * ldzb + K2 + col] = __float2bfloat16_rn(v - __bfloat162float(hv));
+          zb[row * ldzb + 2 * K2 + col] = hv;
+        }
+      }
+      if (zb != nullptr && ldzb > 3 * K2) {
+        const int padw = static_cast<int>(ldzb - 3 * K2);
+        for (int i = static_cast<int>(lane); i < nr * padw; i += 32)
+          zb[(r0 + i / padw) * ldzb + 3 * K2 + i % padw] = __float2bfloat16_rn(0.f);
+      }
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[b]);
   }
 }
 
@@ -897,10 +1252,19 @@ bool fast_tt_supported(int J1, int R1) {
   return (J1 == 1 && (R1 == 8 || R1 == 16)) || (J1 == 4 && (R1 == 8 || R1 == 16));
 }
 
-// QA_AQ_STAGED=0 selects the register-streaming act-quant kernel (A/B comparisons).
-bool staged_disabled() {
+// QA_AQ_MMA=0 selects the register-streaming act-quant kernel (A/B comparisons).
+bool aq_mma_disabled() {
   static const bool off = [] {
-    const char* v = getenv("QA_AQ_STAGED");
+    const char* v = getenv("QA_AQ_MMA");
+    return v != nullptr && v[0] == '0';
+  }();
+  return off;
+}
+
+// QA_AQ_PIPE=0 selects the CTA-barrier tensor-core act-quant kernel (A/B comparisons).
+bool aq_pipe_disabled() {
+  static const bool off = [] {
+    const char* v = getenv("QA_AQ_PIPE");
     return v != nullptr && v[0] == '0';
   }();
   return off;
@@ -908,7 +1272,7 @@ bool staged_disabled() {
 
 size_t g1i_floats(int64_t K, int J1, int R1) {
   const int64_t nvec = K / 8;
-  return static_cast<size_t>(((nvec + 31) / 32) * 32) * 8 * R1 / J1 * 2;  // broadcast layout is 2x
+  return static_cast<size_t>(((nvec + 31) / 32) * 32) * 8 * R1 / J1 * 2;  // >= the k_g1_frag fragments
 }
 
 cudaError_t launch_actquant_z1(const void* x, int x_dtype, int64_t T, int64_t K, bool want_codes, uint8_t* codes,
@@ -916,11 +1280,101 @@ cudaError_t launch_actquant_z1(const void* x, int x_dtype, int64_t T, int64_t K,
                                __nv_bfloat16* zb, int64_t ldzb, float* zf, float* g1i_ws, cudaStream_t s) {
   if (T == 0) return cudaSuccess;
   const int64_t nvec = K / 8;
-  const uint32_t slot_bytes = static_cast<uint32_t>((K * 2 + 127) & ~int64_t(127));
-  const bool staged = x_dtype == QA_BF16 && !staged_disabled() && slot_bytes <= 100 * 1024 && K <= 32768;
+  // ---- tensor-core path (bf16 rows): TOK = 8 rows per tile when two tiles fit an SM, else 4
+  if (x_dtype == QA_BF16 && !aq_mma_disabled() && K % 64 == 0 && K <= 32768 && (J1 == 1 || J1 == 4)) {
+    const uint32_t pad = J1 == 4 ? aq_row_pad<4>() : aq_row_pad<1>();
+    const size_t tile_bytes = (static_cast<size_t>(K) * 2 + pad) * AQ_TOK;
+    const int nbuf = 3 * tile_bytes <= 200 * 1024 ? 3 : 2;
+    const size_t smem = nbuf * tile_bytes;
+    if (smem <= 200 * 1024) {
+      const int MT = R1 / 8;
+      const int64_t nfrag = (J1 == 4 ? K / 64 : K / 16);
+      {
+        LaunchScope scope(kTT, double(nfrag) * MT * 32 * 16 + double(K) * R1 * 4, s);
+        count_launches(1);
+        const int64_t n = nfrag * MT * 32;
+        const unsigned g = static_cast<unsigned>((n + 255) / 256);
+        uint4* fr = reinterpret_cast<uint4*>(g1i_ws);
+        if (J1 == 1 && R1 == 8)
+          k_g1_frag<1, 8><<<g, 256, 0, s>>>(G1, fr, nfrag);
+        else if (J1 == 1)
+          k_g1_frag<1, 16><<<g, 256, 0, s>>>(G1, fr, nfrag);
+        else if (R1 == 8)
+          k_g1_frag<4, 8><<<g, 256, 0, s>>>(G1, fr, nfrag);
+        else
+          k_g1_frag<4, 16><<<g, 256, 0, s>>>(G1, fr, nfrag);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+      }
+      LaunchScope scope(kQuantize, double(T) * K * 2 + (want_codes ? double(T) * ldc + 12.0 * T : 0.0) +
+                                       double(T) * (zb ? ldzb * 2 : 0) + double(T) * (zf ? J1 * R1 * 4 : 0),
+                        s);
+      count_launches(1);
+      const uint4* fr = reinterpret_cast<const uint4*>(g1i_ws);
+      // barrier-free pipelined kernel when a 2- or 3-deep ring of 8-row tiles fits
+      const size_t ptile = (static_cast<size_t>(K) * 2 + pad) * AQP_TOK;
+      const size_t pred = static_cast<size_t>(AQP_NC) * AQP_TOK * J1 * R1 * 4;
+      const int pbuf = 3 * (ptile + pred) <= 220 * 1024 ? 3 : (2 * (ptile + pred) <= 220 * 1024 ? 2 : 0);
+      if (pbuf > 0 && K <= 16384 && !aq_pipe_disabled()) {
+        const size_t psmem = pbuf * (ptile + pred);
+        const int64_t pt = (T + AQP_TOK - 1) / AQP_TOK;
+        const unsigned grid = static_cast<unsigned>(pt < 148 ? pt : 148);
+#define QA_AQP(JJ, RR, NB)                                                                                     \
+  {                                                                                                            \
+    auto kern = want_codes ? k_aq_pipe<JJ, RR, NB, true> : k_aq_pipe<JJ, RR, NB, false>;                       \
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(psmem));         \
+    kern<<<grid, (AQP_NC + 1) * 32, psmem, s>>>(static_cast<const __nv_bfloat16*>(x), T, K, codes, ldc, sx, ox, \
+                                                rsx, fr, zb, ldzb, zf);                                        \
+  }
+#define QA_AQP_T(JJ, RR) \
+  if (pbuf == 3)         \
+    QA_AQP(JJ, RR, 3)    \
+  else                   \
+    QA_AQP(JJ, RR, 2)
+        if (J1 == 1 && R1 == 8)
+          QA_AQP_T(1, 8)
+        else if (J1 == 1)
+          QA_AQP_T(1, 16)
+        else if (R1 == 8)
+          QA_AQP_T(4, 8)
+        else
+          QA_AQP_T(4, 16)
+#undef QA_AQP_T
+#undef QA_AQP
+        return cudaGetLastError();
+      }
+      const int64_t ntiles = (T + AQ_TOK - 1) / AQ_TOK;
+#define QA_AQM(JJ, RR, NB)                                                                                      \
+  {                                                                                                             \
+    auto kern = want_codes ? k_aq_mma<JJ, RR, NB, true> : k_aq_mma<JJ, RR, NB, false>;                          \
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));           \
+    int per_sm = 1;                                                                                             \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, AQ_NW * 32, smem);                             \
+    const int64_t cap = static_cast<int64_t>(per_sm < 1 ? 1 : per_sm) * 148;                                    \
+    const unsigned grid = static_cast<unsigned>(ntiles < cap ? ntiles : cap);                                   \
+    kern<<<grid, AQ_NW * 32, smem, s>>>(static_cast<const __nv_bfloat16*>(x), T, K, codes, ldc, sx, ox, rsx, fr, \
+                                        zb, ldzb, zf);                                                          \
+  }
+#define QA_AQM_T(JJ, RR) \
+  if (nbuf == 3)         \
+    QA_AQM(JJ, RR, 3)    \
+  else                   \
+    QA_AQM(JJ, RR, 2)
+      if (J1 == 1 && R1 == 8)
+        QA_AQM_T(1, 8)
+      else if (J1 == 1)
+        QA_AQM_T(1, 16)
+      else if (R1 == 8)
+        QA_AQM_T(4, 8)
+      else
+        QA_AQM_T(4, 16)
+#undef QA_AQM_T
+#undef QA_AQM
+      return cudaGetLastError();
+    }
+  }
   {
-    const bool bcast = false;  // broadcast G1 layout (k_g1_bcast) measured slower: 2x the L1 loads
-    const int64_t n = nvec * (bcast ? (8 / J1) * R1 / 2 : 2 * R1 / J1);
+    const int64_t n = nvec * 2 * R1 / J1;
     LaunchScope scope(kTT, double(n) * 32, s);
     count_launches(1);
     const unsigned g = static_cast<unsigned>((n + 255) / 256);
@@ -930,10 +1384,9 @@ cudaError_t launch_actquant_z1(const void* x, int x_dtype, int64_t T, int64_t K,
     else if (J1 == 1 && R1 == 16)
       k_g1_interleave<1, 16><<<g, 256, 0, s>>>(G1, G1i, nvec);
     else if (J1 == 4 && R1 == 8)
-      bcast ? k_g1_bcast<4, 8><<<g, 256, 0, s>>>(G1, G1i, nvec) : k_g1_interleave<4, 8><<<g, 256, 0, s>>>(G1, G1i, nvec);
+      k_g1_interleave<4, 8><<<g, 256, 0, s>>>(G1, G1i, nvec);
     else
-      bcast ? k_g1_bcast<4, 16><<<g, 256, 0, s>>>(G1, G1i, nvec)
-            : k_g1_interleave<4, 16><<<g, 256, 0, s>>>(G1, G1i, nvec);
+      k_g1_interleave<4, 16><<<g, 256, 0, s>>>(G1, G1i, nvec);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
@@ -943,30 +1396,6 @@ cudaError_t launch_actquant_z1(const void* x, int x_dtype, int64_t T, int64_t K,
                                    double(T) * (zb ? ldzb * 2 : 0) + double(T) * (zf ? J1 * R1 * 4 : 0),
                     s);
   count_launches(1);
-  if (staged) {
-    int warps = static_cast<int>((200 * 1024) / slot_bytes);
-    warps = warps > 16 ? 16 : warps;
-    const size_t smem = static_cast<size_t>(warps) * slot_bytes;
-    const int64_t ctas_needed = (T + warps - 1) / warps;
-    const unsigned grid = static_cast<unsigned>(ctas_needed < 148 ? ctas_needed : 148);
-#define QA_AQS(JJ, RR)                                                                                              \
-  {                                                                                                                 \
-    auto kern = want_codes ? k_actquant_z1_s<JJ, RR, true> : k_actquant_z1_s<JJ, RR, false>;                       \
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));               \
-    kern<<<grid, warps * 32, smem, s>>>(static_cast<const __nv_bfloat16*>(x), T, K, codes, ldc, sx, ox, rsx, G1i, \
-                                        zb, ldzb, zf);                                                              \
-  }
-    if (J1 == 1 && R1 == 8)
-      QA_AQS(1, 8)
-    else if (J1 == 1 && R1 == 16)
-      QA_AQS(1, 16)
-    else if (J1 == 4 && R1 == 8)
-      QA_AQS(4, 8)
-    else
-      QA_AQS(4, 16)
-#undef QA_AQS
-    return cudaGetLastError();
-  }
   const dim3 grid(static_cast<unsigned>((T + 7) / 8));  // 8 warps = 8 token rows per CTA
 #define QA_AQ(TI, JJ, RR)                                                                                           \
   if (want_codes)                                                                                                   \

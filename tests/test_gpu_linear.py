@@ -172,6 +172,36 @@ def test_edge_cases():
         L.linear_forward(q, (spec, cores[:2]), x)
 
 
+@pytest.mark.parametrize("xdtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("N,K,T,spec", [(512, 512, 97, None), (512, 256, 70, L.TTSpec.lora(512, 256, 8))])
+def test_activation_codes_offset_and_tie_rows(N, K, T, spec, xdtype):
+    # Rows whose offset dwarfs their range (|lo| / step >> 255: a fused v*inv - lo*inv would cancel),
+    # rows on a coarse grid (many exact rounding ties), constant rows and a one-hot row: the int32
+    # accumulators (which see every activation code) must still match the reference bit for bit.
+    q, oq, x, xs, spec, cores, cores_np = _case(N, K, T, 8, 8, 61, spec, xdtype)
+    g = torch.Generator().manual_seed(5)
+    base = torch.randn(T, K, generator=g)
+    rows = [
+        1000.0 + base[0:16] * 0.5,  # offset rows
+        -3000.0 + base[16:24] * 4.0,
+        torch.round(base[24:48] * 8.0) / 8.0,  # coarse grid: frequent exact ties
+        torch.round(base[48:56] * 2.0) * 0.25 + 7.0,
+        torch.full((4, K), 2.5),  # constant rows (step 0)
+        torch.zeros(4, K),
+        base[64:],
+    ]
+    X = torch.cat(rows)[:T]
+    X[60] = 0.0
+    X[60, 7] = 1.0  # one-hot
+    x = X.to(xdtype).cuda()
+    xs = x.float().cpu().numpy()
+    out = L.linear_forward(q, (spec, cores), x, debug=True)
+    ref = O.qa_linear_forward(xs, oq, cores_np)
+    acc = _np(out["acc"]).astype(np.int64)
+    assert np.array_equal(acc, ref["acc"]), f"accumulators differ in rows {np.unique(np.argwhere(acc != ref['acc'])[:, 0])[:10]}"
+    assert O.rel_err(_np(L.linear_forward(q, (spec, cores), x)), ref["y"]) <= TOL_BF16
+
+
 def test_determinism():
     q, oq, x, xs, spec, cores, _ = _case(1024, 1024, 512, 8, 8, 41)
     dy = torch.randn(512, 1024, device="cuda", dtype=torch.bfloat16)
