@@ -258,7 +258,10 @@ def main():
         cores = [torch.randn(spec.core_shape(i), generator=gen, device=dev) * 0.01 for i in range(spec.d)]
         wc, ttc = q.as_c(), spec.as_c(cores)
         ws_bytes = max(ws_bytes, lib.qa_linear_workspace_bytes(ctypes.byref(wc), ctypes.byref(ttc), T))
-        mats[name] = dict(q=q, spec=spec, cores=cores, wc=wc, ttc=ttc, n=n, k=k, kind=kind)
+        nsaved = lib.qa_linear_saved_bytes(ctypes.byref(wc), ctypes.byref(ttc), T)
+        saved = torch.empty(max(nsaved, 4), dtype=torch.uint8, device=dev)
+        mats[name] = dict(q=q, spec=spec, cores=cores, wc=wc, ttc=ttc, n=n, k=k, kind=kind, saved=saved,
+                          nsaved=nsaved)
         grad_numel += spec.param_count()
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     flat_grad = torch.zeros(grad_numel, dtype=torch.float32, device=dev)
@@ -288,16 +291,18 @@ def main():
     def step(xs, dys):
         for name, _, _, kind in LINEARS_7B:
             m = mats[name]
-            st = lib.qa_linear_forward(ctypes.byref(m["wc"]), ctypes.byref(m["ttc"]), xs[kind].data_ptr(), BF16, T,
-                                       ys[name].data_ptr(), None, None, None, ws.data_ptr(), ws_bytes, sptr)
+            st = lib.qa_linear_forward_save(ctypes.byref(m["wc"]), ctypes.byref(m["ttc"]), xs[kind].data_ptr(), BF16,
+                                            T, ys[name].data_ptr(), m["saved"].data_ptr(), m["nsaved"],
+                                            ws.data_ptr(), ws_bytes, sptr)
             if st:
                 _lib.check(st, f"forward {name}")
         for name in BACKWARD_ORDER:
             m = mats[name]
-            st = lib.qa_linear_backward(ctypes.byref(m["wc"]), ctypes.byref(m["ttc"]), xs[m["kind"]].data_ptr(), BF16,
-                                        dys[name].data_ptr(), BF16, T, dxs[name].data_ptr(), None,
-                                        ctypes.cast(m["gptr"], ctypes.POINTER(ctypes.c_void_p)), 0, ws.data_ptr(),
-                                        ws_bytes, sptr)
+            st = lib.qa_linear_backward_saved(ctypes.byref(m["wc"]), ctypes.byref(m["ttc"]),
+                                              xs[m["kind"]].data_ptr(), BF16, dys[name].data_ptr(), BF16, T,
+                                              dxs[name].data_ptr(),
+                                              ctypes.cast(m["gptr"], ctypes.POINTER(ctypes.c_void_p)), 0,
+                                              m["saved"].data_ptr(), m["nsaved"], ws.data_ptr(), ws_bytes, sptr)
             if st:
                 _lib.check(st, f"backward {name}")
         if world > 1:

@@ -118,6 +118,29 @@ QA_API int qa_linear_backward(const qa_qweight* w, const qa_tt* tt, const void* 
                        int dy_dtype, int64_t tokens, void* dx, float* dx_f32, float* const* dcores,
                        int accumulate, void* workspace, size_t workspace_bytes, void* stream);
 
+/* Saved state of the recompute window (PER_LAYER recompute, transformer.py:613-637 / 888-897).
+ * The reference re-runs a layer's forward from its stored input right before that layer's
+ * backward; the intermediates of that recompute-forward live only until the backward.  For the
+ * fast TT family (m_1 = 1, n_d = 1) the only adapter intermediate the backward needs is
+ * Z1 = x · G1 ([tokens, n_1-remainder x r_1] fp32, 0.8% of x at the Llama shapes), so the
+ * recompute-forward can hand it over instead of the backward reading x a third time.
+ * qa_linear_saved_bytes returns 0 when the adapter has no savable state (the *_saved / *_save
+ * entry points then behave exactly like qa_linear_forward / qa_linear_backward). */
+QA_API size_t qa_linear_saved_bytes(const qa_qweight* w, const qa_tt* tt, int64_t tokens);
+
+/* qa_linear_forward (no debug outputs) that also writes the saved state (nullable). */
+QA_API int qa_linear_forward_save(const qa_qweight* w, const qa_tt* tt, const void* x, int x_dtype,
+                                  int64_t tokens, void* y, void* saved, size_t saved_bytes, void* workspace,
+                                  size_t workspace_bytes, void* stream);
+
+/* qa_linear_backward that takes the saved state of qa_linear_forward_save on the SAME x and cores
+ * (nullable: recompute from x). */
+QA_API int qa_linear_backward_saved(const qa_qweight* w, const qa_tt* tt, const void* x, int x_dtype,
+                                    const void* dy, int dy_dtype, int64_t tokens, void* dx,
+                                    float* const* dcores, int accumulate, const void* saved,
+                                    size_t saved_bytes, void* workspace, size_t workspace_bytes,
+                                    void* stream);
+
 /* Workspace for qa_merge / qa_tt_materialize. */
 QA_API size_t qa_merge_workspace_bytes(const qa_tt* tt);
 

@@ -31,6 +31,9 @@ EXPORTS = (
     "qa_linear_workspace_bytes",
     "qa_linear_forward",
     "qa_linear_backward",
+    "qa_linear_saved_bytes",
+    "qa_linear_forward_save",
+    "qa_linear_backward_saved",
     "qa_merge_workspace_bytes",
     "qa_merge",
     "qa_tt_materialize",
@@ -84,6 +87,12 @@ def _declare(lib):
     lib.qa_linear_forward.argtypes = [PW, PT, P, I32, I64, P, P, P, P, P, SZ, P]
     lib.qa_linear_backward.restype = I32
     lib.qa_linear_backward.argtypes = [PW, PT, P, I32, P, I32, I64, P, P, ctypes.POINTER(P), I32, P, SZ, P]
+    lib.qa_linear_saved_bytes.restype = SZ
+    lib.qa_linear_saved_bytes.argtypes = [PW, PT, I64]
+    lib.qa_linear_forward_save.restype = I32
+    lib.qa_linear_forward_save.argtypes = [PW, PT, P, I32, I64, P, P, SZ, P, SZ, P]
+    lib.qa_linear_backward_saved.restype = I32
+    lib.qa_linear_backward_saved.argtypes = [PW, PT, P, I32, P, I32, I64, P, ctypes.POINTER(P), I32, P, SZ, P, SZ, P]
     lib.qa_merge_workspace_bytes.restype = SZ
     lib.qa_merge_workspace_bytes.argtypes = [PT]
     lib.qa_merge.restype = I32

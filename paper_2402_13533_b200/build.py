@@ -37,13 +37,16 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
+    """defines / out: development variants (extra -D flags, another output path; see tools/)."""
+    lib_path = out or LIB
+    if not force and not defines and out is None and not _stale():
         return LIB
-    objdir = os.path.join(HERE, "build")
+    objdir = os.path.join(HERE, "build", "variant_" + "_".join(d.replace("=", "") for d in defines)) if defines \
+        else os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
     common = [nvcc(), "-std=c++17", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC,-fvisibility=hidden",
-              "-Xptxas", "-v" if verbose else "-O3", "--expt-relaxed-constexpr"]
+              "-Xptxas", "-v" if verbose else "-O3", "--expt-relaxed-constexpr", *["-D" + d for d in defines]]
     objs = []
     for src in SOURCES:
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
@@ -52,12 +55,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
             cmd.insert(1, "-DQA_EXPORTS")
         subprocess.run(cmd, check=True)
         objs.append(obj)
-    tmp = LIB + ".tmp"
+    tmp = lib_path + ".tmp"
     subprocess.run([nvcc(), "-shared", *ARCH, "-o", tmp, *objs, "-lcudart_static", "-ldl", "-lrt", "-lpthread"],
                    check=True)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib_path)
+    return lib_path
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    outs = [a[6:] for a in sys.argv[1:] if a.startswith("--out=")]
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, defines=defs, out=outs[0] if outs else None))

@@ -278,9 +278,13 @@ size_t qa_linear_workspace_bytes(const qa_qweight* w, const qa_tt* tt, int64_t t
   return P.bytes;
 }
 
-int qa_linear_forward(const qa_qweight* w, const qa_tt* tt, const void* x, int x_dtype, int64_t tokens,
-                      void* y, int32_t* acc_i32, float* y_f32, float* y2_f32, void* workspace,
-                      size_t workspace_bytes, void* stream) {
+}  // extern "C"
+
+namespace qa {
+namespace {
+int linear_forward_impl(const qa_qweight* w, const qa_tt* tt, const void* x, int x_dtype, int64_t tokens, void* y,
+                        int32_t* acc_i32, float* y_f32, float* y2_f32, float* z1_save, void* workspace,
+                        size_t workspace_bytes, void* stream) {
   QA_TRY(check_weight(w));
   if (tokens == 0) return QA_OK;  // empty batch: nothing to do (pointers may be null)
   if (x == nullptr || tokens < 0 || (x_dtype != QA_F32 && x_dtype != QA_BF16) || w->rowsum == nullptr) {
@@ -308,7 +312,7 @@ int qa_linear_forward(const qa_qweight* w, const qa_tt* tt, const void* x, int x
   if (P.fast && x_vec) {
     // (2)+(4a) one pass over x: bit-exact per-token act-quant + Z1 = first TT stage
     QA_TRY_CUDA(launch_actquant_z1(x, x_dtype, T, K, true, P.xcodes, P.Kp, P.sx, P.ox, P.rsx, tt->cores[0], P.J1,
-                                   P.R1, P.zb, P.K2p, nullptr, P.g1i, s),
+                                   P.R1, P.zb, P.K2p, z1_save, P.g1i, s),
                 "act quantize + TT stage 1");
     // (4b) V = cores 2..d contracted; y2 = Z1 · Vᵀ runs as extension k-blocks of the GEMM
     QA_TRY_CUDA(launch_build_v(P.fd, P.R1, P.H, P.J1, P.C, P.M, tt->cores[1], P.fd == 3 ? tt->cores[2] : nullptr,
@@ -372,9 +376,9 @@ int qa_linear_forward(const qa_qweight* w, const qa_tt* tt, const void* x, int x
   return gemm_tc(0, P.xcodes, P.Kp, wop, P.Kp, T, N, P.Kp, e, s, ext.K2 > 0 ? &ext : nullptr);
 }
 
-int qa_linear_backward(const qa_qweight* w, const qa_tt* tt, const void* x, int x_dtype, const void* dy,
-                       int dy_dtype, int64_t tokens, void* dx, float* dx_f32, float* const* dcores,
-                       int accumulate, void* workspace, size_t workspace_bytes, void* stream) {
+int linear_backward_impl(const qa_qweight* w, const qa_tt* tt, const void* x, int x_dtype, const void* dy,
+                         int dy_dtype, int64_t tokens, void* dx, float* dx_f32, float* const* dcores, int accumulate,
+                         const float* z1_saved, void* workspace, size_t workspace_bytes, void* stream) {
   QA_TRY(check_weight(w));
   if (tokens == 0) {
     // empty batch: gradients of an empty sum are zero (unless accumulating)
@@ -435,17 +439,21 @@ int qa_linear_backward(const qa_qweight* w, const qa_tt* tt, const void* x, int 
   if (fast) {
     // (5) recompute Z1 from the stored layer input, then Z_{d-1}
     const int d = P.fd;
-    QA_TRY_CUDA(launch_actquant_z1(x, x_dtype, T, K, false, nullptr, 0, nullptr, nullptr, nullptr, tt->cores[0], P.J1,
-                                   P.R1, nullptr, 0, P.zf, P.g1i, s),
-                "TT stage 1 recompute");
-    const float* zd = P.zf;
+    const float* zf = z1_saved;  // Z1 of this very input, exported by the recompute forward
+    if (zf == nullptr) {
+      QA_TRY_CUDA(launch_actquant_z1(x, x_dtype, T, K, false, nullptr, 0, nullptr, nullptr, nullptr, tt->cores[0],
+                                     P.J1, P.R1, nullptr, 0, P.zf, P.g1i, s),
+                  "TT stage 1 recompute");
+      zf = P.zf;
+    }
+    const float* zd = zf;
     int64_t zs = P.K2;
     const bool mid_fast = d == 3 && mid_fast_ok(P.K2, P.H * P.C);
     if (d == 3) {
       if (mid_fast)
-        QA_TRY_CUDA(launch_mid_fwd(P.zf, T, P.K2, P.J1, P.H * P.C, P.C, tt->cores[1], P.z2, s), "TT stage 2 recompute");
+        QA_TRY_CUDA(launch_mid_fwd(zf, T, P.K2, P.J1, P.H * P.C, P.C, tt->cores[1], P.z2, s), "TT stage 2 recompute");
       else
-        QA_TRY_CUDA(launch_tt_stage_fwd(P.zf, QA_F32, P.K2, tt->cores[1], P.z2, int64_t(P.H) * P.C, T, 1, P.R1, P.J1,
+        QA_TRY_CUDA(launch_tt_stage_fwd(zf, QA_F32, P.K2, tt->cores[1], P.z2, int64_t(P.H) * P.C, T, 1, P.R1, P.J1,
                                         1, P.H, P.C, s),
                     "TT stage 2 recompute");
       zd = P.z2;
@@ -469,7 +477,7 @@ int qa_linear_backward(const qa_qweight* w, const qa_tt* tt, const void* x, int 
       const bool want_g2 = dcores != nullptr && dcores[1] != nullptr;
       if (mid_fast) {
         const int nctas = mid_bwd_ctas(T);
-        QA_TRY_CUDA(launch_mid_bwd(dzd, P.zf, T, P.K2, P.J1, P.H * P.C, P.C, tt->cores[1], P.dz1,
+        QA_TRY_CUDA(launch_mid_bwd(dzd, zf, T, P.K2, P.J1, P.H * P.C, P.C, tt->cores[1], P.dz1,
                                    want_g2 ? P.gpart : nullptr, nctas, s),
                     "dZ1 + dG2");
         if (want_g2)
@@ -477,7 +485,7 @@ int qa_linear_backward(const qa_qweight* w, const qa_tt* tt, const void* x, int 
                       "reduce dG2");
       } else {
         if (want_g2)
-          QA_TRY_CUDA(launch_tt_core_grad(P.zf, QA_F32, P.K2, dzd, QA_F32, int64_t(P.H) * P.C, P.gpart, P.nchunks,
+          QA_TRY_CUDA(launch_tt_core_grad(zf, QA_F32, P.K2, dzd, QA_F32, int64_t(P.H) * P.C, P.gpart, P.nchunks,
                                           dcores[1], accumulate != 0, T, 1, P.R1, P.J1, 1, P.H, P.C, s),
                       "dG2");
         QA_TRY_CUDA(launch_tt_stage_bwd(dzd, QA_F32, int64_t(P.H) * P.C, tt->cores[1], P.dz1, P.K2, T, 1, P.R1,
@@ -575,6 +583,60 @@ int qa_linear_backward(const qa_qweight* w, const qa_tt* tt, const void* x, int 
     QA_TRY(gemm_tc(1, a, lda, P.wdt, P.Np, T, K, P.Np, e, s, ext.K2 > 0 ? &ext : nullptr));
   }
   return QA_OK;
+}
+
+}  // namespace
+}  // namespace qa
+
+extern "C" {
+
+int qa_linear_forward(const qa_qweight* w, const qa_tt* tt, const void* x, int x_dtype, int64_t tokens,
+                      void* y, int32_t* acc_i32, float* y_f32, float* y2_f32, void* workspace,
+                      size_t workspace_bytes, void* stream) {
+  return linear_forward_impl(w, tt, x, x_dtype, tokens, y, acc_i32, y_f32, y2_f32, nullptr, workspace,
+                             workspace_bytes, stream);
+}
+
+int qa_linear_backward(const qa_qweight* w, const qa_tt* tt, const void* x, int x_dtype, const void* dy,
+                       int dy_dtype, int64_t tokens, void* dx, float* dx_f32, float* const* dcores,
+                       int accumulate, void* workspace, size_t workspace_bytes, void* stream) {
+  return linear_backward_impl(w, tt, x, x_dtype, dy, dy_dtype, tokens, dx, dx_f32, dcores, accumulate, nullptr,
+                              workspace, workspace_bytes, stream);
+}
+
+size_t qa_linear_saved_bytes(const qa_qweight* w, const qa_tt* tt, int64_t tokens) {
+  if (tt == nullptr || check_weight(w) != QA_OK || tokens <= 0) return 0;
+  TTDims dd;
+  if (check_tt(tt, w, &dd) != QA_OK) return 0;
+  LinearPlan P;
+  plan_linear(w, &dd, tokens, nullptr, &P, false);
+  return P.fast ? sizeof(float) * static_cast<size_t>(tokens) * P.K2 : 0;
+}
+
+int qa_linear_forward_save(const qa_qweight* w, const qa_tt* tt, const void* x, int x_dtype, int64_t tokens,
+                           void* y, void* saved, size_t saved_bytes, void* workspace, size_t workspace_bytes,
+                           void* stream) {
+  const size_t need = qa_linear_saved_bytes(w, tt, tokens);
+  if (saved != nullptr && saved_bytes < need) {
+    set_error("qa_linear_forward_save: saved buffer needs %zu bytes", need);
+    return QA_ERR_WORKSPACE;
+  }
+  return linear_forward_impl(w, tt, x, x_dtype, tokens, y, nullptr, nullptr, nullptr,
+                             need > 0 ? static_cast<float*>(saved) : nullptr, workspace, workspace_bytes, stream);
+}
+
+int qa_linear_backward_saved(const qa_qweight* w, const qa_tt* tt, const void* x, int x_dtype, const void* dy,
+                             int dy_dtype, int64_t tokens, void* dx, float* const* dcores, int accumulate,
+                             const void* saved, size_t saved_bytes, void* workspace, size_t workspace_bytes,
+                             void* stream) {
+  const size_t need = qa_linear_saved_bytes(w, tt, tokens);
+  if (saved != nullptr && saved_bytes < need) {
+    set_error("qa_linear_backward_saved: saved buffer holds %zu of %zu bytes", saved_bytes, need);
+    return QA_ERR_WORKSPACE;
+  }
+  return linear_backward_impl(w, tt, x, x_dtype, dy, dy_dtype, tokens, dx, nullptr, dcores, accumulate,
+                              need > 0 ? static_cast<const float*>(saved) : nullptr, workspace, workspace_bytes,
+                              stream);
 }
 
 size_t qa_merge_workspace_bytes(const qa_tt* tt) {

@@ -70,6 +70,11 @@ QA_DEV unsigned long long fadd2(unsigned long long a, unsigned long long b) {
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
   return d;
 }
+QA_DEV unsigned long long fadd2rm(unsigned long long a, unsigned long long b) {  // round toward -inf
+  unsigned long long d;
+  asm("add.rm.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
 QA_DEV unsigned long long fsub2(unsigned long long a, unsigned long long b) {
   unsigned long long d;
   asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));

@@ -323,6 +323,55 @@ QA_DEV void aq_codes8(const uint4 raw, unsigned long long inv2, unsigned long lo
   near = (((f0 - 0x01010101u) & ~f0) | ((f1 - 0x01010101u) & ~f1)) & 0x80808080u;
 }
 
+// Bracketed codes of 8 elements: t = q' + 1/2 is evaluated twice, with the addend shifted by
+// -kTieBand and +kTieBand, and each is floored onto the integer grid by a round-down magic add
+// (byte 1 of M + t, M = 1.5 * 2^15).  Outside the band both floors agree and equal the reference's
+// code (the fp32 error of t is far below kTieBand); a byte where they differ marks an element whose
+// [t - band, t + band] holds an integer — about 2 * kTieBand of all elements — and is replayed in
+// fp64 (aq_replay64).  c0/c1 = codes of elements 0..3 / 4..7, d0/d1 = nonzero bytes to replay.
+template <bool SUB>
+QA_DEV void aq_codes8b(const uint4 raw, unsigned long long inv2, unsigned long long alo2, unsigned long long ahi2,
+                       unsigned long long nlo2, uint32_t& c0, uint32_t& c1, uint32_t& d0, uint32_t& d1) {
+  const unsigned long long m2 = f2pack(49152.0f, 49152.0f);
+  const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+  uint32_t sl[8], sh[8];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    unsigned long long v2 = f2pack(__uint_as_float(w[i] << 16), __uint_as_float(w[i] & 0xFFFF0000u));
+    if constexpr (SUB) v2 = fadd2(v2, nlo2);
+    const unsigned long long tl = ffma2r(v2, inv2, alo2), th = ffma2r(v2, inv2, ahi2);
+    const unsigned long long l2 = fadd2rm(tl, m2), h2 = fadd2rm(th, m2);
+    sl[2 * i] = static_cast<uint32_t>(l2);
+    sl[2 * i + 1] = static_cast<uint32_t>(l2 >> 32);
+    sh[2 * i] = static_cast<uint32_t>(h2);
+    sh[2 * i + 1] = static_cast<uint32_t>(h2 >> 32);
+  }
+  c0 = __byte_perm(__byte_perm(sl[0], sl[1], 0x0051), __byte_perm(sl[2], sl[3], 0x0051), 0x5410);
+  c1 = __byte_perm(__byte_perm(sl[4], sl[5], 0x0051), __byte_perm(sl[6], sl[7], 0x0051), 0x5410);
+  d0 = c0 ^ __byte_perm(__byte_perm(sh[0], sh[1], 0x0051), __byte_perm(sh[2], sh[3], 0x0051), 0x5410);
+  d1 = c1 ^ __byte_perm(__byte_perm(sh[4], sh[5], 0x0051), __byte_perm(sh[6], sh[7], 0x0051), 0x5410);
+}
+
+// The reference's code of element e (0..7) of an 8-element bf16 word, in its own fp64 arithmetic
+// (quant.py:73-99: round_half_away((w - lo) / scale) clipped to [0, 255], w >= lo).
+QA_DEV uint32_t aq_replay64(const uint4 raw, int e, double lo64, double step64) {
+  const uint32_t wa = (e & 2) ? raw.y : raw.x, wb = (e & 2) ? raw.w : raw.z;
+  const uint32_t wd = (e & 4) ? wb : wa;
+  const float v = __uint_as_float((e & 1) ? (wd & 0xFFFF0000u) : (wd << 16));
+  const double q = __ddiv_rn(__dsub_rn(static_cast<double>(v), lo64), step64);
+  return static_cast<uint32_t>(fmin(fmax(floor(__dadd_rn(q, 0.5)), 0.0), 255.0));
+}
+
+// Replays the flagged bytes of one code word (elements e0 .. e0 + 3 of raw).
+QA_DEV uint32_t aq_replay_word(const uint4 raw, int e0, uint32_t code, uint32_t d, double lo64, double step64) {
+  while (d != 0u) {
+    const int b = (__ffs(d) - 1) >> 3;
+    d &= ~(0xFFu << (8 * b));
+    code = (code & ~(0xFFu << (8 * b))) | (aq_replay64(raw, e0 + b, lo64, step64) << (8 * b));
+  }
+  return code;
+}
+
 // Resolve the flagged elements of a chunk.  With s rounded to the integer n, floor(q') is n when
 // q' >= n and n - 1 otherwise; the fp32 q' decides that unless it lies within kTieBand of n (far
 // above its error), where the reference's fp64 arithmetic is replayed exactly.
@@ -801,6 +850,467 @@ __global__ void __launch_bounds__((AQP_NC + 1) * 32, 1)
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// CTA-per-8-token act-quant + Z1 (production path for bf16 rows, K % 64 == 0, J1 in {1, 4}).
+// Nothing is staged in shared memory but the G1 fragments: a CTA of AQC_WARPS warps owns 8 token
+// rows at a time and warp w takes the 64-element segments w, w + AQC_WARPS, ... of all 8 rows.
+// Lane (g, c) = (lane / 4, lane % 4) reads, per segment, exactly the 16 elements of row g that the
+// m16n8k16 B fragment of the Z1 MMA needs from it (J1 = 4: elements 8c..8c+7 and 32+8c..32+8c+7;
+// J1 = 1: 16c..16c+15): two 16-byte loads straight from global memory, 8 rows x 64 contiguous
+// bytes per warp instruction.
+//   pass 1 (the one HBM read of x): Z1 partials on the tensor cores (A = [G1_hi | G1_lo] fragments,
+//          k_g1_frag; B = the x words, exact in bf16) and the exact bf16 min / max, per warp.
+//   reduce : partials meet in shared memory and are summed in fixed warp order (deterministic).
+//   pass 2 : codes by the byte-grid rule (aq_codes8, bit-exact with quant.py:73-99) from a second
+//            read of the same 64-byte pieces by the same warp — a CTA's live rows are 8 x 2K bytes,
+//            so the re-read is served by L1 / L2, not HBM.  Bracketed elements (aq_codes8b) are
+//            replayed in fp64 in place.
+// Splitting the row over the CTA's warps keeps the live footprint per in-flight byte small (the
+// whole row must be seen before its first code), so many CTAs per SM can stream at once.
+constexpr int AQC_WARPS = 8, AQC_UNROLL = 4;
+
+template <int J1>
+QA_DEV void aqc_offsets(uint32_t c, uint32_t& off0, uint32_t& off1) {
+  off0 = J1 == 4 ? 16u * c : 32u * c;
+  off1 = J1 == 4 ? 64u + 16u * c : 32u * c + 16u;
+}
+
+// Codes of one lane's two 8-element words of segment st (bracketed rule, aq_codes8b); writes them
+// and returns their Σ.
+template <int J1, bool SUB>
+QA_DEV uint32_t aqc_codes_seg(const uint4 p0, const uint4 p1, unsigned long long inv2, unsigned long long alo2,
+                              unsigned long long ahi2, unsigned long long nlo2, double lo64, double step64, bool flat,
+                              uint8_t* dst, bool store) {
+  uint32_t cw[4], dw[4];
+  aq_codes8b<SUB>(p0, inv2, alo2, ahi2, nlo2, cw[0], cw[1], dw[0], dw[1]);
+  aq_codes8b<SUB>(p1, inv2, alo2, ahi2, nlo2, cw[2], cw[3], dw[2], dw[3]);
+  if (flat) cw[0] = cw[1] = cw[2] = cw[3] = dw[0] = dw[1] = dw[2] = dw[3] = 0u;
+  if ((dw[0] | dw[1] | dw[2] | dw[3]) != 0u) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (dw[k] != 0u) cw[k] = aq_replay_word(k < 2 ? p0 : p1, (k & 1) * 4, cw[k], dw[k], lo64, step64);
+  }
+  if (store) {
+    if constexpr (J1 == 4) {
+      *reinterpret_cast<uint2*>(dst) = make_uint2(cw[0], cw[1]);
+      *reinterpret_cast<uint2*>(dst + 32) = make_uint2(cw[2], cw[3]);
+    } else {
+      *reinterpret_cast<uint4*>(dst) = make_uint4(cw[0], cw[1], cw[2], cw[3]);
+    }
+  }
+  return __dp4a(cw[0], 0x01010101u, __dp4a(cw[1], 0x01010101u, __dp4a(cw[2], 0x01010101u, __dp4a(cw[3], 0x01010101u, 0u))));
+}
+
+template <int J1, bool SUB>
+QA_DEV uint32_t aqc_codes_row(const uint8_t* xrow, uint8_t* crow, int64_t nseg, uint32_t warp, uint32_t off0,
+                              uint32_t off1, const AqRow& r, bool flat, bool store) {
+  const unsigned long long inv2 = f2pack(r.inv, r.inv), nlo2 = f2pack(-r.lo, -r.lo);
+  const float alo = SUB ? 0.5f - kTieBand : r.nbh - kTieBand, ahi = SUB ? 0.5f + kTieBand : r.nbh + kTieBand;
+  const unsigned long long alo2 = f2pack(alo, alo), ahi2 = f2pack(ahi, ahi);
+  uint32_t sum = 0;
+  int64_t st = warp;
+  for (; st + (AQC_UNROLL - 1) * AQC_WARPS < nseg; st += AQC_UNROLL * AQC_WARPS) {
+    uint4 p[AQC_UNROLL][2];
+#pragma unroll
+    for (int u = 0; u < AQC_UNROLL; ++u) {
+      p[u][0] = __ldg(reinterpret_cast<const uint4*>(xrow + 128 * (st + u * AQC_WARPS) + off0));
+      p[u][1] = __ldg(reinterpret_cast<const uint4*>(xrow + 128 * (st + u * AQC_WARPS) + off1));
+    }
+#pragma unroll
+    for (int u = 0; u < AQC_UNROLL; ++u)
+      sum += aqc_codes_seg<J1, SUB>(p[u][0], p[u][1], inv2, alo2, ahi2, nlo2, r.lo64, r.step64, flat,
+                                    crow + 64 * (st + u * AQC_WARPS) + off0 / 2, store);
+  }
+  for (; st < nseg; st += AQC_WARPS) {
+    const uint4 p0 = __ldg(reinterpret_cast<const uint4*>(xrow + 128 * st + off0));
+    const uint4 p1 = __ldg(reinterpret_cast<const uint4*>(xrow + 128 * st + off1));
+    sum += aqc_codes_seg<J1, SUB>(p0, p1, inv2, alo2, ahi2, nlo2, r.lo64, r.step64, flat, crow + 64 * st + off0 / 2,
+                                  store);
+  }
+  return sum;
+}
+
+template <int J1, int R1, bool CODES, bool FRAG_SMEM>
+__global__ void __launch_bounds__(AQC_WARPS * 32) k_aq_cta(const __nv_bfloat16* __restrict__ x, int64_t T, int64_t K,
+                                                            uint8_t* __restrict__ codes, int64_t ldc,
+                                                            float* __restrict__ sx, float* __restrict__ ox,
+                                                            int32_t* __restrict__ rsx, const uint4* __restrict__ frag_g,
+                                                            __nv_bfloat16* __restrict__ zb, int64_t ldzb,
+                                                            float* __restrict__ zf) {
+  static_assert(J1 == 1 || J1 == 4, "J1");
+  static_assert(R1 == 8 || R1 == 16, "R1");
+  constexpr int K2 = J1 * R1, MT = R1 / 8, NJ = J1 == 4 ? 4 : 1, W = AQC_WARPS;
+  constexpr int FPS = (J1 == 4 ? 1 : 4) * MT;  // fragments (one uint4 per lane) per 64-element segment
+  extern __shared__ uint4 s_frag[];
+  __shared__ float s_z[W][8][K2];
+  __shared__ float s_lo[W][8], s_hi[W][8];
+  __shared__ int32_t s_sum[W][8];
+  const uint32_t warp = threadIdx.x >> 5, lane = lane_id(), g = lane >> 2, c = lane & 3;
+  const int64_t nseg = K / 64;
+  if constexpr (FRAG_SMEM) {
+    const int64_t n = nseg * FPS * 32;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s_frag[i] = frag_g[i];
+    __syncthreads();
+  }
+  const uint4* frag = FRAG_SMEM ? s_frag : frag_g;
+  uint32_t off0, off1;
+  aqc_offsets<J1>(c, off0, off1);
+  const int64_t ngroups = (T + 7) / 8;
+  for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+    const int64_t t0 = grp * 8;
+    const bool valid = t0 + g < T;
+    const int64_t trow = valid ? t0 + g : T - 1;  // rows past T are computed on a clamped row, never stored
+    const uint8_t* xrow = reinterpret_cast<const uint8_t*>(x + trow * K);
+    // ---- pass 1: Z1 partial + exact min / max over this warp's segments
+    float acc[NJ][MT][4];
+#pragma unroll
+    for (int J = 0; J < NJ; ++J)
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[J][mt][i] = 0.f;
+    __nv_bfloat162 lo2 = __floats2bfloat162_rn(INFINITY, INFINITY), hi2 = __floats2bfloat162_rn(-INFINITY, -INFINITY);
+    auto seg = [&](int64_t st, const uint4 p0, const uint4 p1) {
+      const uint32_t w[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const __nv_bfloat162 b2 = *reinterpret_cast<const __nv_bfloat162*>(&w[i]);
+        lo2 = __hmin2(lo2, b2);
+        hi2 = __hmax2(hi2, b2);
+      }
+      if constexpr (J1 == 4) {
+        uint4 fr[MT];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) fr[mt] = frag[(st * MT + mt) * 32 + lane];
+#pragma unroll
+        for (int J = 0; J < 4; ++J) {
+          const uint32_t sel = (J & 1) ? 0x7632u : 0x5410u;
+          const uint32_t b0 = __byte_perm(w[J >> 1], w[2 + (J >> 1)], sel);
+          const uint32_t b1 = __byte_perm(w[4 + (J >> 1)], w[6 + (J >> 1)], sel);
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) mma_16816(acc[J][mt], fr[mt].x, fr[mt].y, fr[mt].z, fr[mt].w, b0, b1);
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) {
+            const uint4 fr = frag[((st * 4 + u) * MT + mt) * 32 + lane];
+            mma_16816(acc[0][mt], fr.x, fr.y, fr.z, fr.w, w[2 * u], w[2 * u + 1]);
+          }
+      }
+    };
+    int64_t st = warp;
+    for (; st + (AQC_UNROLL - 1) * W < nseg; st += AQC_UNROLL * W) {
+      uint4 p[AQC_UNROLL][2];
+#pragma unroll
+      for (int u = 0; u < AQC_UNROLL; ++u) {
+        p[u][0] = __ldg(reinterpret_cast<const uint4*>(xrow + 128 * (st + u * W) + off0));
+        p[u][1] = __ldg(reinterpret_cast<const uint4*>(xrow + 128 * (st + u * W) + off1));
+      }
+#pragma unroll
+      for (int u = 0; u < AQC_UNROLL; ++u) seg(st + u * W, p[u][0], p[u][1]);
+    }
+    for (; st < nseg; st += W)
+      seg(st, __ldg(reinterpret_cast<const uint4*>(xrow + 128 * st + off0)),
+          __ldg(reinterpret_cast<const uint4*>(xrow + 128 * st + off1)));
+    // D rows m = g (+ 8), columns n = tokens 2c, 2c + 1
+#pragma unroll
+    for (int J = 0; J < NJ; ++J)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if constexpr (MT == 1) {
+          s_z[warp][2 * c + h][g * J1 + J] = acc[J][0][h] + acc[J][0][2 + h];
+        } else {
+          s_z[warp][2 * c + h][g * J1 + J] = acc[J][0][h] + acc[J][1][h];
+          s_z[warp][2 * c + h][(g + 8) * J1 + J] = acc[J][0][2 + h] + acc[J][1][2 + h];
+        }
+      }
+    if (CODES) {
+      float lo = fminf(__low2float(lo2), __high2float(lo2)), hi = fmaxf(__low2float(hi2), __high2float(hi2));
+      lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, 1));
+      lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, 2));
+      hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, 1));
+      hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, 2));
+      if (c == 0) {
+        s_lo[warp][g] = lo;
+        s_hi[warp][g] = hi;
+      }
+    }
+    __syncthreads();
+    // ---- Z1 of the 8 tokens: fixed-order sum of the warp partials
+    for (int i = static_cast<int>(threadIdx.x); i < 8 * K2; i += W * 32) {
+      const int tk = i / K2, col = i % K2;
+      const int64_t row = t0 + tk;
+      float v = s_z[0][tk][col];
+#pragma unroll
+      for (int w2 = 1; w2 < W; ++w2) v += s_z[w2][tk][col];
+      if (row < T) {
+        if (zf != nullptr) zf[row * K2 + col] = v;
+        if (zb != nullptr) {
+          const __nv_bfloat16 hv = __float2bfloat16_rn(v);
+          zb[row * ldzb + col] = hv;
+          zb[row * ldzb + K2 + col] = __float2bfloat16_rn(v - __bfloat162float(hv));
+          zb[row * ldzb + 2 * K2 + col] = hv;
+        }
+      }
+    }
+    if (zb != nullptr && ldzb > 3 * K2) {
+      const int padw = static_cast<int>(ldzb - 3 * K2);
+      for (int i = static_cast<int>(threadIdx.x); i < 8 * padw; i += W * 32) {
+        const int64_t row = t0 + i / padw;
+        if (row < T) zb[row * ldzb + 3 * K2 + i % padw] = __float2bfloat16_rn(0.f);
+      }
+    }
+    if constexpr (CODES) {
+      // ---- pass 2: codes of this warp's segments of row g
+      float lo = s_lo[0][g], hi = s_hi[0][g];
+#pragma unroll
+      for (int w2 = 1; w2 < W; ++w2) {
+        lo = fminf(lo, s_lo[w2][g]);
+        hi = fmaxf(hi, s_hi[w2][g]);
+      }
+      AqRow r;
+      r.lo = lo;
+      r.lo64 = static_cast<double>(lo);
+      r.step64 = __ddiv_rn(__dsub_rn(static_cast<double>(hi), r.lo64), 255.0);
+      const bool flat = !(r.step64 > 0.0);
+      r.inv = flat ? 0.f : static_cast<float>(1.0 / r.step64);
+      const float nb = -lo * r.inv;
+      r.nbh = nb + 0.5f;
+      uint8_t* crow = codes + trow * ldc;
+      const bool sub = __any_sync(0xffffffffu, fabsf(nb) > 512.0f);
+      uint32_t sum = sub ? aqc_codes_row<J1, true>(xrow, crow, nseg, warp, off0, off1, r, flat, valid)
+                         : aqc_codes_row<J1, false>(xrow, crow, nseg, warp, off0, off1, r, flat, valid);
+      sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+      sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+      if (c == 0) s_sum[warp][g] = static_cast<int32_t>(sum);
+      if (warp == 0 && valid) {
+        if (c == 0) {
+          sx[trow] = flat ? 0.0f : __double2float_rn(r.step64);
+          ox[trow] = lo;
+        }
+        for (int64_t kk = K + c; kk < ldc; kk += 4) crow[kk] = 0;  // zero padding [K, ldc) of the codes row
+      }
+      __syncthreads();  // after this only s_sum is read until the next group's first barrier
+      if (threadIdx.x < 8 && t0 + threadIdx.x < T) {
+        int32_t s = 0;
+#pragma unroll
+        for (int w2 = 0; w2 < W; ++w2) s += s_sum[w2][threadIdx.x];
+        rsx[t0 + threadIdx.x] = s;
+      }
+    } else {
+      __syncthreads();
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Register-resident variant of k_aq_cta (rows up to K = 11264): a CTA of W warps owns 8 token rows
+// at a time and warp w holds the S segments w, w + W, ... of all 8 rows in registers (two 16-byte
+// words per lane and segment, loaded up front).  Pass 1 (Z1 MMAs + min / max) and pass 2 (codes)
+// both read those registers: x crosses HBM once and is never re-read.  A bracketed code byte is
+// resolved in
+// place (aq_codes8b / aq_replay_word) while its bf16 inputs are still in registers.
+template <int J1, int R1, int W, int S, bool CODES>
+__global__ void __launch_bounds__(W * 32) k_aq_reg(const __nv_bfloat16* __restrict__ x, int64_t T, int64_t K,
+                                                    uint8_t* __restrict__ codes, int64_t ldc, float* __restrict__ sx,
+                                                    float* __restrict__ ox, int32_t* __restrict__ rsx,
+                                                    const uint4* __restrict__ frag, __nv_bfloat16* __restrict__ zb,
+                                                    int64_t ldzb, float* __restrict__ zf) {
+  static_assert(J1 == 1 || J1 == 4, "J1");
+  static_assert(R1 == 8 || R1 == 16, "R1");
+  constexpr int K2 = J1 * R1, MT = R1 / 8, NJ = J1 == 4 ? 4 : 1;
+  __shared__ float s_z[W][8][K2];
+  __shared__ float s_lo[W][8], s_hi[W][8];
+  __shared__ int32_t s_sum[W][8];
+  const uint32_t warp = threadIdx.x >> 5, lane = lane_id(), g = lane >> 2, c = lane & 3;
+  const int64_t nseg = K / 64;
+  uint32_t off0, off1;
+  aqc_offsets<J1>(c, off0, off1);
+  const int64_t ngroups = (T + 7) / 8;
+  for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+    const int64_t t0 = grp * 8;
+    const bool valid = t0 + g < T;
+    const int64_t trow = valid ? t0 + g : T - 1;  // rows past T are computed on a clamped row, never stored
+    const uint8_t* xrow = reinterpret_cast<const uint8_t*>(x + trow * K);
+    uint4 p[S][2];
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+      const int64_t st = warp + static_cast<int64_t>(W) * i;
+      if (st < nseg) {
+        p[i][0] = __ldg(reinterpret_cast<const uint4*>(xrow + 128 * st + off0));
+        p[i][1] = __ldg(reinterpret_cast<const uint4*>(xrow + 128 * st + off1));
+      } else {
+        p[i][0] = p[i][1] = make_uint4(0u, 0u, 0u, 0u);
+      }
+    }
+    // ---- pass 1: Z1 partial + exact min / max over this warp's segments
+    float acc[NJ][MT][4];
+#pragma unroll
+    for (int J = 0; J < NJ; ++J)
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[J][mt][i] = 0.f;
+    __nv_bfloat162 lo2 = __floats2bfloat162_rn(INFINITY, INFINITY), hi2 = __floats2bfloat162_rn(-INFINITY, -INFINITY);
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+      const int64_t st = warp + static_cast<int64_t>(W) * i;
+      if (st >= nseg) break;
+      const uint32_t w[8] = {p[i][0].x, p[i][0].y, p[i][0].z, p[i][0].w, p[i][1].x, p[i][1].y, p[i][1].z, p[i][1].w};
+      if (CODES) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const __nv_bfloat162 b2 = *reinterpret_cast<const __nv_bfloat162*>(&w[k]);
+          lo2 = __hmin2(lo2, b2);
+          hi2 = __hmax2(hi2, b2);
+        }
+      }
+      if constexpr (J1 == 4) {
+        uint4 fr[MT];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) fr[mt] = __ldg(frag + (st * MT + mt) * 32 + lane);
+#pragma unroll
+        for (int J = 0; J < 4; ++J) {
+          const uint32_t sel = (J & 1) ? 0x7632u : 0x5410u;
+          const uint32_t b0 = __byte_perm(w[J >> 1], w[2 + (J >> 1)], sel);
+          const uint32_t b1 = __byte_perm(w[4 + (J >> 1)], w[6 + (J >> 1)], sel);
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) mma_16816(acc[J][mt], fr[mt].x, fr[mt].y, fr[mt].z, fr[mt].w, b0, b1);
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) {
+            const uint4 fr = __ldg(frag + ((st * 4 + u) * MT + mt) * 32 + lane);
+            mma_16816(acc[0][mt], fr.x, fr.y, fr.z, fr.w, w[2 * u], w[2 * u + 1]);
+          }
+      }
+    }
+#pragma unroll
+    for (int J = 0; J < NJ; ++J)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if constexpr (MT == 1) {
+          s_z[warp][2 * c + h][g * J1 + J] = acc[J][0][h] + acc[J][0][2 + h];
+        } else {
+          s_z[warp][2 * c + h][g * J1 + J] = acc[J][0][h] + acc[J][1][h];
+          s_z[warp][2 * c + h][(g + 8) * J1 + J] = acc[J][0][2 + h] + acc[J][1][2 + h];
+        }
+      }
+    if (CODES) {
+      float lo = fminf(__low2float(lo2), __high2float(lo2)), hi = fmaxf(__low2float(hi2), __high2float(hi2));
+      lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, 1));
+      lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, 2));
+      hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, 1));
+      hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, 2));
+      if (c == 0) {
+        s_lo[warp][g] = lo;
+        s_hi[warp][g] = hi;
+      }
+    }
+    __syncthreads();
+    // ---- Z1 of the 8 tokens: fixed-order sum of the warp partials
+    for (int i = static_cast<int>(threadIdx.x); i < 8 * K2; i += W * 32) {
+      const int tk = i / K2, col = i % K2;
+      const int64_t row = t0 + tk;
+      float v = s_z[0][tk][col];
+#pragma unroll
+      for (int w2 = 1; w2 < W; ++w2) v += s_z[w2][tk][col];
+      if (row < T) {
+        if (zf != nullptr) zf[row * K2 + col] = v;
+        if (zb != nullptr) {
+          const __nv_bfloat16 hv = __float2bfloat16_rn(v);
+          zb[row * ldzb + col] = hv;
+          zb[row * ldzb + K2 + col] = __float2bfloat16_rn(v - __bfloat162float(hv));
+          zb[row * ldzb + 2 * K2 + col] = hv;
+        }
+      }
+    }
+    if (zb != nullptr && ldzb > 3 * K2) {
+      const int padw = static_cast<int>(ldzb - 3 * K2);
+      for (int i = static_cast<int>(threadIdx.x); i < 8 * padw; i += W * 32) {
+        const int64_t row = t0 + i / padw;
+        if (row < T) zb[row * ldzb + 3 * K2 + i % padw] = __float2bfloat16_rn(0.f);
+      }
+    }
+    if constexpr (CODES) {
+      // ---- pass 2: codes of this warp's segments of row g, straight from the registers
+      float lo = s_lo[0][g], hi = s_hi[0][g];
+#pragma unroll
+      for (int w2 = 1; w2 < W; ++w2) {
+        lo = fminf(lo, s_lo[w2][g]);
+        hi = fmaxf(hi, s_hi[w2][g]);
+      }
+      AqRow r;
+      r.lo = lo;
+      r.lo64 = static_cast<double>(lo);
+      r.step64 = __ddiv_rn(__dsub_rn(static_cast<double>(hi), r.lo64), 255.0);
+      const bool flat = !(r.step64 > 0.0);
+      r.inv = flat ? 0.f : static_cast<float>(1.0 / r.step64);
+      const float nb = -lo * r.inv;
+      r.nbh = nb + 0.5f;
+      uint8_t* crow = codes + trow * ldc;
+      const bool sub = __any_sync(0xffffffffu, fabsf(nb) > 512.0f);
+      const unsigned long long inv2 = f2pack(r.inv, r.inv), nlo2 = f2pack(-r.lo, -r.lo);
+      const float alo = sub ? 0.5f - kTieBand : r.nbh - kTieBand, ahi = sub ? 0.5f + kTieBand : r.nbh + kTieBand;
+      const unsigned long long alo2 = f2pack(alo, alo), ahi2 = f2pack(ahi, ahi);
+      uint32_t sum = 0;
+#pragma unroll
+      for (int i = 0; i < S; ++i) {
+        const int64_t st = warp + static_cast<int64_t>(W) * i;
+        if (st >= nseg) break;
+        uint32_t cw[4], dw[4];
+        if (sub) {
+          aq_codes8b<true>(p[i][0], inv2, alo2, ahi2, nlo2, cw[0], cw[1], dw[0], dw[1]);
+          aq_codes8b<true>(p[i][1], inv2, alo2, ahi2, nlo2, cw[2], cw[3], dw[2], dw[3]);
+        } else {
+          aq_codes8b<false>(p[i][0], inv2, alo2, ahi2, nlo2, cw[0], cw[1], dw[0], dw[1]);
+          aq_codes8b<false>(p[i][1], inv2, alo2, ahi2, nlo2, cw[2], cw[3], dw[2], dw[3]);
+        }
+        if (flat) cw[0] = cw[1] = cw[2] = cw[3] = dw[0] = dw[1] = dw[2] = dw[3] = 0u;
+        if ((dw[0] | dw[1] | dw[2] | dw[3]) != 0u) {  // rare: replay the bracketed elements in fp64
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (dw[k] != 0u) cw[k] = aq_replay_word(k < 2 ? p[i][0] : p[i][1], (k & 1) * 4, cw[k], dw[k], r.lo64, r.step64);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) sum = __dp4a(cw[k], 0x01010101u, sum);
+        if (valid) {
+          uint8_t* dst = crow + 64 * st + off0 / 2;
+          if constexpr (J1 == 4) {
+            *reinterpret_cast<uint2*>(dst) = make_uint2(cw[0], cw[1]);
+            *reinterpret_cast<uint2*>(dst + 32) = make_uint2(cw[2], cw[3]);
+          } else {
+            *reinterpret_cast<uint4*>(dst) = make_uint4(cw[0], cw[1], cw[2], cw[3]);
+          }
+        }
+      }
+      sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+      sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+      if (c == 0) s_sum[warp][g] = static_cast<int32_t>(sum);
+      if (warp == 0 && valid) {
+        if (c == 0) {
+          sx[trow] = flat ? 0.0f : __double2float_rn(r.step64);
+          ox[trow] = lo;
+        }
+        for (int64_t kk = K + c; kk < ldc; kk += 4) crow[kk] = 0;  // zero padding [K, ldc) of the codes row
+      }
+      __syncthreads();  // after this only s_sum is read until the next group's first barrier
+      if (threadIdx.x < 8 && t0 + threadIdx.x < T) {
+        int32_t s = 0;
+#pragma unroll
+        for (int w2 = 0; w2 < W; ++w2) s += s_sum[w2][threadIdx.x];
+        rsx[t0 + threadIdx.x] = s;
+      }
+    } else {
+      __syncthreads();
+    }
+  }
+}
+
 // V[n, c] (bf16, zero padded to ldv): contraction of cores 2..d with the left rank open.
 //   d = 2: V[i, a] = G2[a, i];  d = 3: V[(i2, i3), (a, j2)] = Σ_b G2[a, i2, j2, b] G3[b, i3]
 __global__ void __launch_bounds__(256) k_build_v(int d, int R1, int H, int J1, int C, int M,
@@ -1261,6 +1771,25 @@ bool aq_mma_disabled() {
   return off;
 }
 
+// QA_AQ_REG=1 selects the register-resident k_aq_reg kernel (measured slower than k_aq_cta on
+// B200: 2 CTAs / SM at 120 registers; kept for A/B comparisons).
+bool aq_reg_disabled() {
+  static const bool off = [] {
+    const char* v = getenv("QA_AQ_REG");
+    return !(v != nullptr && v[0] == '1');
+  }();
+  return off;
+}
+
+// QA_AQ_CTA=0 falls back to the shared-memory-staged act-quant kernels below (A/B comparisons).
+bool aq_cta_disabled() {
+  static const bool off = [] {
+    const char* v = getenv("QA_AQ_CTA");
+    return v != nullptr && v[0] == '0';
+  }();
+  return off;
+}
+
 // QA_AQ_PIPE=0 selects the CTA-barrier tensor-core act-quant kernel (A/B comparisons).
 bool aq_pipe_disabled() {
   static const bool off = [] {
@@ -1280,6 +1809,105 @@ cudaError_t launch_actquant_z1(const void* x, int x_dtype, int64_t T, int64_t K,
                                __nv_bfloat16* zb, int64_t ldzb, float* zf, float* g1i_ws, cudaStream_t s) {
   if (T == 0) return cudaSuccess;
   const int64_t nvec = K / 8;
+  // ---- production path: CTA-per-8-token kernel, rows read straight from global memory
+  if (x_dtype == QA_BF16 && !aq_cta_disabled() && K % 64 == 0 && (J1 == 1 || J1 == 4) && (R1 == 8 || R1 == 16) &&
+      reinterpret_cast<uintptr_t>(x) % 16 == 0 &&
+      (!want_codes || (ldc % 16 == 0 && reinterpret_cast<uintptr_t>(codes) % 16 == 0)) &&
+      (zf == nullptr || reinterpret_cast<uintptr_t>(zf) % 16 == 0)) {
+    const int MT = R1 / 8;
+    const int64_t nfrag = (J1 == 4 ? K / 64 : K / 16);
+    {
+      LaunchScope scope(kTT, double(nfrag) * MT * 32 * 16 + double(K) * R1 * 4, s);
+      count_launches(1);
+      const int64_t n = nfrag * MT * 32;
+      const unsigned gr = static_cast<unsigned>((n + 255) / 256);
+      uint4* fr = reinterpret_cast<uint4*>(g1i_ws);
+      if (J1 == 1 && R1 == 8)
+        k_g1_frag<1, 8><<<gr, 256, 0, s>>>(G1, fr, nfrag);
+      else if (J1 == 1)
+        k_g1_frag<1, 16><<<gr, 256, 0, s>>>(G1, fr, nfrag);
+      else if (R1 == 8)
+        k_g1_frag<4, 8><<<gr, 256, 0, s>>>(G1, fr, nfrag);
+      else
+        k_g1_frag<4, 16><<<gr, 256, 0, s>>>(G1, fr, nfrag);
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+    }
+    LaunchScope scope(kQuantize, double(T) * K * 2 + (want_codes ? double(T) * ldc + 12.0 * T : 0.0) +
+                                     double(T) * (zb ? ldzb * 2 : 0) + double(T) * (zf ? J1 * R1 * 4 : 0),
+                      s);
+    count_launches(1);
+    const uint4* fr = reinterpret_cast<const uint4*>(g1i_ws);
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t ngroups = (T + 7) / 8;
+    const int64_t nseg = K / 64;
+    if (nseg <= 176 && !aq_reg_disabled()) {  // register-resident rows
+#define QA_AQR(JJ, RR, WW, SS)                                                                                \
+  {                                                                                                           \
+    auto kern = want_codes ? k_aq_reg<JJ, RR, WW, SS, true> : k_aq_reg<JJ, RR, WW, SS, false>;                \
+    int per_sm = 1;                                                                                           \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WW * 32, 0);                                 \
+    const int64_t cap = static_cast<int64_t>(per_sm < 1 ? 1 : per_sm) * nsm;                                  \
+    const unsigned grid = static_cast<unsigned>(ngroups < cap ? ngroups : cap);                               \
+    kern<<<grid, WW * 32, 0, s>>>(static_cast<const __nv_bfloat16*>(x), T, K, codes, ldc, sx, ox, rsx, fr, zb, \
+                                  ldzb, zf);                                                                  \
+  }
+#define QA_AQR_W(JJ, RR)     \
+  if (nseg <= 64)            \
+    QA_AQR(JJ, RR, 8, 8)     \
+  else                       \
+    QA_AQR(JJ, RR, 16, 11)
+      if (J1 == 1 && R1 == 8)
+        QA_AQR_W(1, 8)
+      else if (J1 == 1)
+        QA_AQR_W(1, 16)
+      else if (R1 == 8)
+        QA_AQR_W(4, 8)
+      else
+        QA_AQR_W(4, 16)
+#undef QA_AQR_W
+#undef QA_AQR
+      return cudaGetLastError();
+    }
+    const size_t frag_bytes = static_cast<size_t>(nfrag) * MT * 32 * 16;
+    const bool fsmem = frag_bytes <= 48 * 1024;
+    const size_t smem = fsmem ? frag_bytes : 0;
+#define QA_AQC(JJ, RR, CC, FS)                                                                                  \
+  {                                                                                                             \
+    auto kern = k_aq_cta<JJ, RR, CC, FS>;                                                                       \
+    int per_sm = 1;                                                                                             \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, AQC_WARPS * 32, smem);                          \
+    const int64_t cap = static_cast<int64_t>(per_sm < 1 ? 1 : per_sm) * nsm;                                    \
+    const unsigned grid = static_cast<unsigned>(ngroups < cap ? ngroups : cap);                                 \
+    kern<<<grid, AQC_WARPS * 32, smem, s>>>(static_cast<const __nv_bfloat16*>(x), T, K, codes, ldc, sx, ox, rsx, \
+                                            fr, zb, ldzb, zf);                                                  \
+  }
+#define QA_AQC_C(JJ, RR)          \
+  if (want_codes) {               \
+    if (fsmem)                    \
+      QA_AQC(JJ, RR, true, true)  \
+    else                          \
+      QA_AQC(JJ, RR, true, false) \
+  } else {                        \
+    if (fsmem)                    \
+      QA_AQC(JJ, RR, false, true) \
+    else                          \
+      QA_AQC(JJ, RR, false, false) \
+  }
+    if (J1 == 1 && R1 == 8)
+      QA_AQC_C(1, 8)
+    else if (J1 == 1)
+      QA_AQC_C(1, 16)
+    else if (R1 == 8)
+      QA_AQC_C(4, 8)
+    else
+      QA_AQC_C(4, 16)
+#undef QA_AQC_C
+#undef QA_AQC
+    return cudaGetLastError();
+  }
   // ---- tensor-core path (bf16 rows): TOK = 8 rows per tile when two tiles fit an SM, else 4
   if (x_dtype == QA_BF16 && !aq_mma_disabled() && K % 64 == 0 && K <= 32768 && (J1 == 1 || J1 == 4)) {
     const uint32_t pad = J1 == 4 ? aq_row_pad<4>() : aq_row_pad<1>();

@@ -10,6 +10,7 @@ Backends keep the reference's duck-typed protocol: `kind`, `name`, `fan_in`, `fa
 from __future__ import annotations
 
 import ctypes
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -27,6 +28,7 @@ __all__ = [
     "TTLinear",
     "LoraLinear",
     "linear_forward",
+    "linear_forward_saving",
     "linear_backward",
     "tt_materialize",
     "tt_merge",
@@ -171,8 +173,38 @@ def linear_forward(q: QuantizedMatrix, adapter, x, *, debug: bool = False):
             "acc": acc.reshape(*lead, q.rows), "y2": None if y2 is None else y2.reshape(*lead, q.rows)}
 
 
+def linear_forward_saving(q: QuantizedMatrix, adapter, x):
+    """Forward of the recompute window (qa_linear_forward_save): returns (y, saved), where `saved`
+    is the adapter state the backward of the SAME x and cores can take instead of re-reading x
+    (the fast TT family's Z1; None when the adapter has nothing to save)."""
+    x = _as_device(x, q.device)
+    lead = tuple(x.shape[:-1])
+    if x.shape[-1] != q.cols:
+        raise QuantError(f"qmatmul dimension mismatch: {q.rows}x{q.cols} vs {tuple(x.shape)}")
+    x2 = x.reshape(-1, q.cols).contiguous()
+    if adapter is None or x2.dtype != torch.bfloat16:
+        return linear_forward(q, adapter, x), None
+    T = x2.shape[0]
+    dev = q.device
+    spec, cores = adapter
+    _check_cores(spec, cores)
+    wc, ttc = q.as_c(), spec.as_c(cores)
+    L = _lib.lib()
+    nsaved = L.qa_linear_saved_bytes(ctypes.byref(wc), ctypes.byref(ttc), T)
+    if nsaved == 0:
+        return linear_forward(q, adapter, x), None
+    saved = torch.empty(nsaved // 4, dtype=torch.float32, device=dev)
+    y = torch.empty((T, q.rows), dtype=torch.bfloat16, device=dev)
+    nbytes = L.qa_linear_workspace_bytes(ctypes.byref(wc), ctypes.byref(ttc), T)
+    ws = workspace.get(nbytes, dev)
+    _lib.check(L.qa_linear_forward_save(ctypes.byref(wc), ctypes.byref(ttc), x2.data_ptr(), _dtype_code(x2), T,
+                                        y.data_ptr(), saved.data_ptr(), nsaved, ws.data_ptr(), ws.numel(),
+                                        _stream_ptr(dev)), "qa_linear_forward_save")
+    return y.reshape(*lead, q.rows), saved
+
+
 def linear_backward(q: QuantizedMatrix, adapter, x, dy, *, want_dx: bool = True, want_grads: bool = True,
-                    debug: bool = False):
+                    debug: bool = False, saved: torch.Tensor | None = None):
     """dx = dy·deq(W) + dy·W_t and the adapter-core gradients through qa_linear_backward.
 
     Returns (dx or None, [dG_k] or None[, dx_f32 when debug])."""
@@ -205,6 +237,16 @@ def linear_backward(q: QuantizedMatrix, adapter, x, dy, *, want_dx: bool = True,
     if nbytes == 0:
         raise ModelError(f"invalid linear configuration: {L.qa_last_error().decode()}")
     ws = workspace.get(nbytes, dev)
+    if saved is not None and ttc is not None and dx32 is None:
+        st = L.qa_linear_backward_saved(ctypes.byref(wc), ctypes.byref(ttc), x2.data_ptr(), _dtype_code(x2),
+                                        dy2.data_ptr(), _dtype_code(dy2), T,
+                                        dx.data_ptr() if dx is not None else None,
+                                        ctypes.cast(gptrs, ctypes.POINTER(ctypes.c_void_p)) if gptrs is not None
+                                        else None, 0, saved.data_ptr(), saved.numel() * 4, ws.data_ptr(),
+                                        ws.numel(), _stream_ptr(dev))
+        _lib.check(st, "qa_linear_backward_saved")
+        out_dx = None if dx is None else dx.reshape(*lead, q.cols)
+        return (out_dx, grads, None) if debug else (out_dx, grads)
     st = L.qa_linear_backward(ctypes.byref(wc), ctypes.byref(ttc) if ttc else None,
                               x2.data_ptr() if x2 is not None else None,
                               _dtype_code(x2) if x2 is not None else QA_F32, dy2.data_ptr(), _dtype_code(dy2), T,
@@ -335,15 +377,39 @@ class TTLinear:
         for p, g in zip(self.cores, dcores):
             _accumulate(grads, p, g)
 
+    def _tag(self, x):
+        return (x.data_ptr(), tuple(x.shape), x._version, tuple(p.data._version for p in self._params_for_tag()))
+
+    def _params_for_tag(self):
+        return self.cores
+
     def forward(self, x, step: int = 0):
+        """y = base(x) + adapter(x).  When x is a bf16 CUDA tensor the recompute-window state
+        (Z1, qa_linear_forward_save) is kept for a following backward on the same, unmodified x
+        and cores — the PER_LAYER pattern of re-running a layer's forward right before its
+        backward (transformer.py:888-897); any other backward recomputes it from x."""
         if self.merged:
             return _dense_forward(self._merged_bf16, x)
+        self._saved = None
+        if isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.bfloat16:
+            y, saved = linear_forward_saving(self.base.q, (self.spec, self._core_tensors()), x)
+            if saved is not None:
+                self._saved = (weakref.ref(x), self._tag(x), saved)
+            return y
         return linear_forward(self.base.q, (self.spec, self._core_tensors()), x)
+
+    def _take_saved(self, x):
+        s, self._saved = getattr(self, "_saved", None), None
+        if s is None or not isinstance(x, torch.Tensor):
+            return None
+        ref, tag, saved = s
+        return saved if ref() is x and self._tag(x) == tag else None
 
     def backward(self, x, dy, grads, step: int = 0):
         if self.merged:
             raise ModelError(f"{self.name}: merged adapter is inference-only")
-        dx, dcores = linear_backward(self.base.q, (self.spec, self._core_tensors()), x, dy)
+        saved = self._take_saved(x)
+        dx, dcores = linear_backward(self.base.q, (self.spec, self._core_tensors()), x, dy, saved=saved)
         self._scatter_grads(grads, dcores)
         return dx
 
@@ -378,6 +444,9 @@ class LoraLinear(TTLinear):
     @property
     def rank(self):
         return self.down.data.shape[0]
+
+    def _params_for_tag(self):
+        return [self.down, self.up]
 
     def params(self):
         return self.base.params() + [self.down, self.up]

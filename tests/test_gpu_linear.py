@@ -92,6 +92,34 @@ def test_backward_parity(N, K, T, bits, r, spec):
         assert e <= TOL_BF16, (k, e)
 
 
+@pytest.mark.parametrize("N,K,T,bits,r,spec", CASES[4:])  # the fast TT family
+def test_recompute_window_handoff_is_bit_identical(N, K, T, bits, r, spec):
+    """qa_linear_forward_save + qa_linear_backward_saved (Z1 handed from the recompute-forward)
+    gives exactly the gradients and dx of the backward that recomputes Z1 from x."""
+    q, oq, x, xs, spec, cores, cores_np = _case(N, K, T, bits, r, 31, spec)
+    dy = torch.from_numpy(O.seeded_random(T, N, 98)).cuda().to(torch.bfloat16)
+    y_save, saved = L.linear_forward_saving(q, (spec, cores), x)
+    assert saved is not None and saved.numel() > 0
+    y_plain = L.linear_forward(q, (spec, cores), x)
+    assert torch.equal(y_save, y_plain)
+    dx_a, g_a = L.linear_backward(q, (spec, cores), x, dy, saved=saved)
+    dx_b, g_b = L.linear_backward(q, (spec, cores), x, dy)
+    assert torch.equal(dx_a, dx_b)
+    for a, b in zip(g_a, g_b):
+        assert torch.equal(a, b)
+    # protocol level: TTLinear keeps the state for a backward on the same, unmodified x ...
+    lin = L.TTLinear("w", L.QuantizedLinear("w.base", q), spec, [c.clone() for c in cores])
+    grads = {}
+    lin.forward(x)
+    assert lin._saved is not None
+    dx_c = lin.backward(x, dy, grads)
+    assert torch.equal(dx_c, dx_b) and lin._saved is None
+    # ... and recomputes when x changed in place after the forward
+    lin.forward(x)
+    x.mul_(1.0)
+    assert lin._take_saved(x) is None
+
+
 def test_base_only_paths_match_reference_functions():
     # qmatmul with per-token act-quant == qmatmul(qw, deq(Q(x))) ; qmatmul_t == reference qmatmul_t
     W = O.seeded_random(384, 640, 5, std=0.02)

@@ -1,7 +1,7 @@
 """Summarise an ncu report (or a launch-list CSV) into the plain-text files kept under profiles/.
 
     python tools/ncu_summary.py report.ncu-rep > profiles/rNN_ncu_<what>.txt
-    python tools/ncu_summary.py --launches launches.csv > profiles/rNN_launch_list_summary.txt
+    python tools/ncu_summary.py --launches launches.csv [LAST_N] > profiles/rNN_launch_list_summary.txt
 """
 
 from __future__ import annotations
@@ -30,8 +30,11 @@ METRICS = [
 
 
 def summarise_report(path: str) -> str:
-    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True,
-                         check=True).stdout
+    if path.endswith(".csv"):  # `ncu -i rep --page raw --csv` output saved on the GPU box
+        raw = open(path).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True,
+                             check=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
     out = [f"ncu report: {path}"]
@@ -45,11 +48,13 @@ def summarise_report(path: str) -> str:
     return "\n".join(out) + "\n"
 
 
-def summarise_launches(path: str) -> str:
+def summarise_launches(path: str, last: int = 0) -> str:
     lines = open(path).read().splitlines()
     start = next(i for i, l in enumerate(lines) if "Kernel Name" in l)
     rows = list(csv.reader(io.StringIO("\n".join(lines[start:]))))
     hdr = rows[0]
+    if last:
+        rows = [hdr] + [r for r in rows[1:] if len(r) > 1][-last:]
     ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
     agg = collections.OrderedDict()
     total = 0.0
@@ -73,6 +78,6 @@ def summarise_launches(path: str) -> str:
 
 if __name__ == "__main__":
     if sys.argv[1] == "--launches":
-        sys.stdout.write(summarise_launches(sys.argv[2]))
+        sys.stdout.write(summarise_launches(sys.argv[2], int(sys.argv[3]) if len(sys.argv) > 3 else 0))
     else:
         sys.stdout.write(summarise_report(sys.argv[1]))
