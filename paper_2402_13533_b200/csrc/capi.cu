@@ -80,6 +80,13 @@ struct LinearPlan {
   __nv_bfloat16* bext = nullptr;  // B_ext bf16 [K, K2p]
   float* gpart = nullptr;         // core-gradient partials
   float* g1i = nullptr;           // G1 interleaved for the x pass
+  // fused backward (tt_fast.cu k_tt_bwd_fused): d = 3, J1 = 4, M = 256, R1 = C
+  bool fused = false;
+  int HR = 0, HS = 0, TS = 0;
+  float* dz1p = nullptr;          // dZ1 partials [HS][T][K2]
+  float* g1p = nullptr;           // dG1 partials [S_dg1][K / J1 * R1]
+  float* g2p = nullptr;           // dG2 partials [TS][core-1 numel]
+  float* g3p = nullptr;           // dG3 partials [HS * TS][C * 256]
   size_t bytes = 0;
 };
 
@@ -138,6 +145,14 @@ bool plan_linear(const qa_qweight* w, const TTDims* dd, int64_t T, void* ws, Lin
     int64_t gp = std::max<int64_t>(int64_t(P->H) * P->S_dy * P->C * P->M, int64_t(P->S_dg1) * P->K * P->R1);
     if (P->fd == 3) gp = std::max<int64_t>(gp, dd->core_numel(1) * P->nchunks);
     P->gpart = b.take<float>(gp);
+    if (tt_bwd_fused_ok(P->fd, P->J1, P->R1, P->C, P->M)) {
+      P->fused = true;
+      tt_bwd_fused_plan(T, P->H, P->C, &P->HR, &P->HS, &P->TS);
+      P->dz1p = b.take<float>(int64_t(P->HS) * T * P->K2);
+      P->g1p = b.take<float>(int64_t(P->S_dg1) * (P->K / P->J1) * P->R1);
+      P->g2p = b.take<float>(int64_t(P->TS) * dd->core_numel(1));
+      P->g3p = b.take<float>(int64_t(P->HS) * P->TS * P->C * P->M);
+    }
   } else if (dd != nullptr) {
     int64_t zmax = 0;
     for (int k = 1; k < dd->d; ++k) {
@@ -446,8 +461,36 @@ int linear_backward_impl(const qa_qweight* w, const qa_tt* tt, const void* x, in
                   "TT stage 1 recompute");
       zf = P.zf;
     }
+    if (P.fused) {
+      // one pass over dy: dZ1 partials, dG2 / dG3 partials (Z2 formed on the fly from Z1)
+      QA_TRY_CUDA(launch_tt_bwd_fused(static_cast<const __nv_bfloat16*>(dyb16), ld_dyb, T, P.H, P.C, zf,
+                                      tt->cores[1], tt->cores[2], P.dz1p, P.g3p, P.g2p, s),
+                  "TT fused dy pass");
+      // one pass over x: dG1 partials, dZ1 summed over the h-ranges, its bf16 split for the dX GEMM
+      const bool want_g1 = dcores != nullptr && dcores[0] != nullptr;
+      if (want_g1 || want_dx)
+        QA_TRY_CUDA(launch_tt_dg1(x, x_dtype, T, K, P.dz1p, P.J1, P.R1, P.g1p, P.S_dg1, s, P.HS,
+                                  want_dx ? P.dz1b : nullptr, P.K2p),
+                    "TT x pass");
+      const float* parts[3] = {P.g1p, P.g2p, P.g3p};
+      const int nparts[3] = {P.S_dg1, P.TS, P.HS * P.TS};
+      const int64_t numel[3] = {dd.core_numel(0), dd.core_numel(1), dd.core_numel(2)};
+      float* outs[3] = {want_g1 ? dcores[0] : nullptr, dcores != nullptr ? dcores[1] : nullptr,
+                        dcores != nullptr ? dcores[2] : nullptr};
+      QA_TRY_CUDA(launch_grad_reduce3(parts, nparts, numel, outs, accumulate != 0, P.R1, P.J1, tt->cores[0],
+                                      want_dx ? P.bext : nullptr, K, P.K2p, s),
+                  "reduce core gradients + B_ext");
+      if (want_dx) {
+        ext.A2 = P.dz1b;
+        ext.lda2 = P.K2p;
+        ext.B2 = P.bext;
+        ext.ldb2 = P.K2p;
+        ext.K2 = P.K2p;
+      }
+    }
     const float* zd = zf;
     int64_t zs = P.K2;
+    if (!P.fused) {
     const bool mid_fast = d == 3 && mid_fast_ok(P.K2, P.H * P.C);
     if (d == 3) {
       if (mid_fast)
@@ -509,6 +552,7 @@ int linear_backward_impl(const qa_qweight* w, const qa_tt* tt, const void* x, in
       ext.ldb2 = P.K2p;
       ext.K2 = P.K2p;
     }
+    }  // !P.fused
   } else if (pd != nullptr) {
     // (5) recompute Z_1..Z_{d-1} from the stored layer input
     for (int k = 0; k + 1 < dd.d; ++k) {

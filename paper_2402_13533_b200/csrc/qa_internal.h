@@ -86,8 +86,20 @@ int tt_dy_splits(int64_t T, int blocks_per_split);
 cudaError_t launch_tt_dy(const __nv_bfloat16* dy, int64_t T, int64_t N, int H, int M, const float* Z, int64_t zs,
                          int C, const float* Gd, float* dz_part, float* dg_part, int S, cudaStream_t s);
 int tt_dg1_splits(int64_t T, int64_t K, int J1);
+// dz1: HS partials [HS][T][K2] (summed in fixed order); dz1b (nullable): [hi | lo | hi | 0] split rows
 cudaError_t launch_tt_dg1(const void* x, int x_dtype, int64_t T, int64_t K, const float* dz1, int J1, int R1,
-                          float* part, int S, cudaStream_t s);
+                          float* part, int S, cudaStream_t s, int HS = 1, __nv_bfloat16* dz1b = nullptr,
+                          int64_t ldb = 0);
+// fused backward of the pinned Llama modes (d = 3, J1 = 4, M = 256, R1 = C in {8, 16})
+bool tt_bwd_fused_ok(int d, int J1, int R1, int C, int M);
+void tt_bwd_fused_plan(int64_t T, int H, int C, int* HR, int* HS, int* TS);
+cudaError_t launch_tt_bwd_fused(const __nv_bfloat16* dy, int64_t ldy, int64_t T, int H, int C, const float* Z1,
+                                const float* G2, const float* G3, float* dz1p, float* g3part, float* g2part,
+                                cudaStream_t s);
+// out_i (+)= Σ_p parts_i[p] for three partial sets, plus the B_ext operand (bext nullable), one launch
+cudaError_t launch_grad_reduce3(const float* const* parts, const int* nparts, const int64_t* numel,
+                                float* const* outs, bool accumulate, int R1, int J1, const float* G1,
+                                __nv_bfloat16* bext, int64_t K, int64_t ldb, cudaStream_t s);
 
 // ------------------------------------------------------------ tcgen05 GEMM
 struct GemmEpilogue {

@@ -1509,30 +1509,493 @@ __global__ void __launch_bounds__(256) k_tt_dy(const __nv_bfloat16* __restrict__
 }
 
 // ---------------------------------------------------------------------------------------------
+// Fused backward of the pinned Llama modes (d = 3, m = (1, H, 256), n = (K/4, 4, 1), ranks
+// (1, C, C, 1)): one pass over dy per (h-range, token-range) CTA replaces the stage-2 recompute,
+// the dy pass, the middle-core backward and their partial buffers.  Per 32-token tile and output
+// block h (256 columns of dy, double-buffered with cp.async), all on the tensor cores (mma.sync):
+//   dZ2_h  = dy_h · G3ᵀ       K = 256 split over KW warps, fixed-order sum
+//   dG3   += dy_hᵀ · Z2_h     accumulators in registers for the CTA's lifetime
+//   dZ1   += dZ2_h · Gm_hᵀ    accumulators in registers for the tile (Gm_h[aj][c] = G2[a, h, j2, c])
+//   dG2_h += Z1ᵀ · dZ2_h      per-tile products added to shared-memory accumulators
+//   Z2_h+1 = Z1 · Gm_h+1      (for the next block's dG3)
+// dy, G3 and Z2 enter as bf16 (dy is bf16 already; as in the unfused kernels); Z1, Gm and dZ2 —
+// fp32 values — enter as hi + lo bf16 pairs with three MMAs per product (hi·hi + lo·hi + hi·lo),
+// which keeps those contractions at ~2^-16 relative accuracy.  dZ1 of the h-range is written as a
+// partial ([HS][T][K2]); k_tt_dg1 sums the HS partials in fixed order.
+constexpr int FB_TT = 32, FB_COLS = 256, FB_LDY = FB_COLS + 8, FB_LDZ = FB_TT + 8, FB_NS = 3;
+
+template <int C>
+struct FbLayout {
+  static constexpr int K2 = 4 * C, NT = C / 8, KW = 8 / (2 * NT);
+  static constexpr int LZ1 = K2 + 8;         // Z1 planes: row stride (bf16)
+  static constexpr int LC = C == 8 ? 8 : 24;  // Gm / dZ2 planes: row stride (bf16), ldmatrix conflict-free
+  static constexpr size_t dy = 0;                                                         // bf16 [NS][TT][LDY]
+  static constexpr size_t g3 = dy + sizeof(__nv_bfloat16) * FB_NS * FB_TT * FB_LDY;      // bf16 [C][LDY]
+  static constexpr size_t z2t = g3 + sizeof(__nv_bfloat16) * C * FB_LDY;          // bf16 [C][LDZ]
+  static constexpr size_t red = z2t + sizeof(__nv_bfloat16) * C * FB_LDZ;         // f32 [KW][TT][C]
+  static constexpr size_t z1p = red + sizeof(float) * KW * FB_TT * C;             // bf16 [2][TT][LZ1]
+  static constexpr size_t dz2p = z1p + sizeof(__nv_bfloat16) * 2 * FB_TT * LZ1;   // bf16 [2][TT][LC]
+  static constexpr size_t gmp = dz2p + sizeof(__nv_bfloat16) * 2 * FB_TT * LC;    // bf16 [2][HR][K2][LC]
+  __host__ __device__ static size_t dg2(int hr) { return gmp + sizeof(__nv_bfloat16) * 2 * size_t(hr) * K2 * LC; }  // f32 [HR][K2][C]
+  __host__ __device__ static size_t bytes(int hr) { return dg2(hr) + sizeof(float) * size_t(hr) * K2 * C; }
+};
+
+template <int C>
+__global__ void __launch_bounds__(256) k_tt_bwd_fused(const __nv_bfloat16* __restrict__ dy, int64_t ldy, int64_t T,
+                                                      int H, int HR, const float* __restrict__ Z1,
+                                                      const float* __restrict__ G2, const float* __restrict__ G3,
+                                                      float* __restrict__ dz1p, float* __restrict__ g3part,
+                                                      float* __restrict__ g2part) {
+  using L = FbLayout<C>;
+  constexpr int K2 = L::K2, NT = L::NT, KW = L::KW, LZ1 = L::LZ1, LC = L::LC, J1 = 4;
+  constexpr int MTZ = FB_TT / 16;                        // token m-tiles
+  constexpr int DZT = MTZ * (K2 / 8) / 8;                // dZ1 output tiles per warp
+  extern __shared__ __align__(16) uint8_t fb_smem[];
+  auto sdy = reinterpret_cast<__nv_bfloat16(*)[FB_TT][FB_LDY]>(fb_smem + L::dy);
+  auto sg3 = reinterpret_cast<__nv_bfloat16(*)[FB_LDY]>(fb_smem + L::g3);
+  auto sz2t = reinterpret_cast<__nv_bfloat16(*)[FB_LDZ]>(fb_smem + L::z2t);
+  auto sred = reinterpret_cast<float(*)[FB_TT][C]>(fb_smem + L::red);
+  auto sz1p = reinterpret_cast<__nv_bfloat16(*)[FB_TT][LZ1]>(fb_smem + L::z1p);
+  auto sdz2p = reinterpret_cast<__nv_bfloat16(*)[FB_TT][LC]>(fb_smem + L::dz2p);
+  __nv_bfloat16* sgmp = reinterpret_cast<__nv_bfloat16*>(fb_smem + L::gmp);
+  float* sdg2 = reinterpret_cast<float*>(fb_smem + L::dg2(HR));
+  auto gm = [&](int p, int hl, int aj, int c) -> __nv_bfloat16* {
+    return sgmp + ((static_cast<size_t>(p) * HR + hl) * K2 + aj) * LC + c;
+  };
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, tq = lane & 3;
+  const int hs = blockIdx.x, ts = blockIdx.y, TS = gridDim.y;
+  const int h0 = hs * HR, nh = H - h0 < HR ? H - h0 : HR;
+  const int64_t ntiles = (T + FB_TT - 1) / FB_TT;
+  const int64_t per = (ntiles + TS - 1) / TS;
+  const int64_t tile0 = ts * per, tile1 = tile0 + per < ntiles ? tile0 + per : ntiles;
+
+  for (int i = tid; i < C * FB_COLS; i += 256) sg3[i / FB_COLS][i % FB_COLS] = __float2bfloat16_rn(G3[i]);
+  for (int i = tid; i < nh * K2 * C; i += 256) {
+    const int hl = i / (K2 * C), aj = (i / C) % K2, c = i % C;
+    const int a = aj / J1, j2 = aj % J1;
+    const float v = G2[((static_cast<int64_t>(a) * H + h0 + hl) * J1 + j2) * C + c];
+    const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+    *gm(0, hl, aj, c) = hi;
+    *gm(1, hl, aj, c) = __float2bfloat16_rn(v - __bfloat162float(hi));
+    sdg2[i] = 0.f;
+  }
+  float acc2[2][NT][4];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int n = 0; n < NT; ++n)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc2[i][n][q] = 0.f;
+
+  auto load_dy = [&](int64_t t0, int h, int buf) {
+    for (int i = tid; i < FB_TT * (FB_COLS / 8); i += 256) {
+      const int r = i / (FB_COLS / 8), ch = i % (FB_COLS / 8);
+      const int64_t t = t0 + r;
+      const bool ok = t < T;
+      cp_async16(&sdy[buf][r][ch * 8], dy + (ok ? t : 0) * ldy + static_cast<int64_t>(h) * FB_COLS + ch * 8, ok);
+    }
+  };
+  // Z2_hl = Z1 · Gm_hl (3-term split MMAs) -> bf16, transposed into sz2t; warps 4..7
+  auto z2_phase = [&](int hl) {
+    for (int task = (warp + 4) & 7; task < MTZ * NT; task += 8) {
+      const int mz = task / NT, n8 = task % NT;
+      float d[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int ks = 0; ks < K2 / 16; ++ks) {
+        uint32_t ah[4], al[4], bh[2], bl[2];
+        ldsm_x4(&sz1p[0][mz * 16 + (lane & 15)][ks * 16 + (lane >> 4) * 8], ah[0], ah[1], ah[2], ah[3]);
+        ldsm_x4(&sz1p[1][mz * 16 + (lane & 15)][ks * 16 + (lane >> 4) * 8], al[0], al[1], al[2], al[3]);
+        ldsm_x2_t(gm(0, hl, ks * 16 + (lane & 15), n8 * 8), bh[0], bh[1]);
+        ldsm_x2_t(gm(1, hl, ks * 16 + (lane & 15), n8 * 8), bl[0], bl[1]);
+        mma_16816(d, ah[0], ah[1], ah[2], ah[3], bh[0], bh[1]);
+        mma_16816(d, al[0], al[1], al[2], al[3], bh[0], bh[1]);
+        mma_16816(d, ah[0], ah[1], ah[2], ah[3], bl[0], bl[1]);
+      }
+      sz2t[n8 * 8 + 2 * tq][mz * 16 + g] = __float2bfloat16_rn(d[0]);
+      sz2t[n8 * 8 + 2 * tq + 1][mz * 16 + g] = __float2bfloat16_rn(d[1]);
+      sz2t[n8 * 8 + 2 * tq][mz * 16 + g + 8] = __float2bfloat16_rn(d[2]);
+      sz2t[n8 * 8 + 2 * tq + 1][mz * 16 + g + 8] = __float2bfloat16_rn(d[3]);
+    }
+  };
+
+  // the CTA's (tile, h) items form one stream; dy blocks are prefetched FB_NS - 1 items ahead
+  const int64_t nit = (tile1 - tile0) * nh;
+  auto issue = [&](int64_t it) {
+    if (it < nit) load_dy((tile0 + it / nh) * FB_TT, h0 + static_cast<int>(it % nh), static_cast<int>(it % FB_NS));
+    cp_async_commit();
+  };
+  for (int i = 0; i < FB_NS - 1; ++i) issue(i);
+  float dacc[DZT][4];
+  for (int64_t it = 0; it < nit; ++it) {
+    const int64_t tile = tile0 + it / nh;
+    const int hl = static_cast<int>(it % nh), buf = static_cast<int>(it % FB_NS);
+    const int64_t t0 = tile * FB_TT;
+    const int nt = static_cast<int>(T - t0 < FB_TT ? T - t0 : FB_TT);
+    if (hl == 0) {
+      __syncthreads();  // previous tile's readers of the Z1 planes are done
+      for (int i = tid; i < FB_TT * K2; i += 256) {
+        const int r = i / K2, aj = i % K2;
+        const float f = r < nt ? Z1[(t0 + r) * K2 + aj] : 0.f;
+        const __nv_bfloat16 hi = __float2bfloat16_rn(f);
+        sz1p[0][r][aj] = hi;
+        sz1p[1][r][aj] = __float2bfloat16_rn(f - __bfloat162float(hi));
+      }
+#pragma unroll
+      for (int u = 0; u < DZT; ++u)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) dacc[u][q] = 0.f;
+      __syncthreads();
+      z2_phase(0);
+    }
+    issue(it + FB_NS - 1);  // into the buffer item it - 1 used; its readers passed two barriers since
+    cp_async_wait<FB_NS - 1>();
+    __syncthreads();  // dy_h and Z2_h are in shared memory
+    {  // dZ2_h partial: warp -> (m-tile, n-tile), K split over KW warps
+      const int ti = warp / KW, kq = warp % KW;
+      const int mt = ti / NT, n8 = ti % NT;
+      float d1[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int ks = 0; ks < 16 / KW; ++ks) {
+        const int kc = (kq * (16 / KW) + ks) * 16;
+        uint32_t b0, b1, a0, a1, a2, a3;
+        ldsm_x2(&sg3[n8 * 8 + (lane & 7)][kc + ((lane >> 3) & 1) * 8], b0, b1);
+        ldsm_x4(&sdy[buf][mt * 16 + (lane & 15)][kc + (lane >> 4) * 8], a0, a1, a2, a3);
+        mma_16816(d1, a0, a1, a2, a3, b0, b1);
+      }
+      sred[kq][mt * 16 + g][n8 * 8 + 2 * tq] = d1[0];
+      sred[kq][mt * 16 + g][n8 * 8 + 2 * tq + 1] = d1[1];
+      sred[kq][mt * 16 + g + 8][n8 * 8 + 2 * tq] = d1[2];
+      sred[kq][mt * 16 + g + 8][n8 * 8 + 2 * tq + 1] = d1[3];
+    }
+#pragma unroll
+    for (int ks = 0; ks < FB_TT / 16; ++ks) {  // dG3ᵀ[cols x C] += dy_hᵀ [cols x tokens] · Z2_h [tokens x C]
+      uint32_t b[NT][2];
+#pragma unroll
+      for (int n8 = 0; n8 < NT; ++n8)
+        ldsm_x2(&sz2t[n8 * 8 + (lane & 7)][ks * 16 + ((lane >> 3) & 1) * 8], b[n8][0], b[n8][1]);
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int c0 = warp * 32 + i * 16;
+        const int q = lane >> 3;
+        uint32_t a0, a1, a2, a3;
+        ldsm_x4_t(&sdy[buf][ks * 16 + (q >> 1) * 8 + (lane & 7)][c0 + (q & 1) * 8], a0, a1, a2, a3);
+#pragma unroll
+        for (int n8 = 0; n8 < NT; ++n8) mma_16816(acc2[i][n8], a0, a1, a2, a3, b[n8][0], b[n8][1]);
+      }
+    }
+    __syncthreads();
+    for (int i = tid; i < FB_TT * C; i += 256) {  // dZ2_h: fixed-order sum of the K-split partials, hi/lo
+      const int t = i / C, c = i % C;
+      float v = sred[0][t][c];
+#pragma unroll
+      for (int w = 1; w < KW; ++w) v += sred[w][t][c];
+      const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+      sdz2p[0][t][c] = hi;
+      sdz2p[1][t][c] = __float2bfloat16_rn(v - __bfloat162float(hi));
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < DZT; ++u) {  // dZ1 tile += dZ2_h · Gm_hᵀ
+      const int tl = warp + 8 * u, m = tl / (K2 / 8), n = tl % (K2 / 8);
+      if constexpr (C == 8) {
+        uint32_t ah0, ah1, al0, al1, bh, bl;
+        ldsm_x2(&sdz2p[0][m * 16 + (lane & 15)][0], ah0, ah1);
+        ldsm_x2(&sdz2p[1][m * 16 + (lane & 15)][0], al0, al1);
+        ldsm_x1(gm(0, hl, n * 8 + (lane & 7), 0), bh);
+        ldsm_x1(gm(1, hl, n * 8 + (lane & 7), 0), bl);
+        mma_1688(dacc[u], ah0, ah1, bh);
+        mma_1688(dacc[u], al0, al1, bh);
+        mma_1688(dacc[u], ah0, ah1, bl);
+      } else {
+        uint32_t ah[4], al[4], bh[2], bl[2];
+        ldsm_x4(&sdz2p[0][m * 16 + (lane & 15)][(lane >> 4) * 8], ah[0], ah[1], ah[2], ah[3]);
+        ldsm_x4(&sdz2p[1][m * 16 + (lane & 15)][(lane >> 4) * 8], al[0], al[1], al[2], al[3]);
+        ldsm_x2(gm(0, hl, n * 8 + (lane & 7), ((lane >> 3) & 1) * 8), bh[0], bh[1]);
+        ldsm_x2(gm(1, hl, n * 8 + (lane & 7), ((lane >> 3) & 1) * 8), bl[0], bl[1]);
+        mma_16816(dacc[u], ah[0], ah[1], ah[2], ah[3], bh[0], bh[1]);
+        mma_16816(dacc[u], al[0], al[1], al[2], al[3], bh[0], bh[1]);
+        mma_16816(dacc[u], ah[0], ah[1], ah[2], ah[3], bl[0], bl[1]);
+      }
+    }
+    for (int task = warp; task < (K2 / 16) * NT; task += 8) {  // dG2_h += Z1ᵀ · dZ2_h
+      const int ma = task / NT, n8 = task % NT;
+      float d[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int ks = 0; ks < FB_TT / 16; ++ks) {
+        const int q = lane >> 3;
+        uint32_t ah[4], al[4], bh[2], bl[2];
+        ldsm_x4_t(&sz1p[0][ks * 16 + (q >> 1) * 8 + (lane & 7)][ma * 16 + (q & 1) * 8], ah[0], ah[1], ah[2], ah[3]);
+        ldsm_x4_t(&sz1p[1][ks * 16 + (q >> 1) * 8 + (lane & 7)][ma * 16 + (q & 1) * 8], al[0], al[1], al[2], al[3]);
+        ldsm_x2_t(&sdz2p[0][ks * 16 + (lane & 15)][n8 * 8], bh[0], bh[1]);
+        ldsm_x2_t(&sdz2p[1][ks * 16 + (lane & 15)][n8 * 8], bl[0], bl[1]);
+        mma_16816(d, ah[0], ah[1], ah[2], ah[3], bh[0], bh[1]);
+        mma_16816(d, al[0], al[1], al[2], al[3], bh[0], bh[1]);
+        mma_16816(d, ah[0], ah[1], ah[2], ah[3], bl[0], bl[1]);
+      }
+      float* dst = sdg2 + static_cast<size_t>(hl) * K2 * C;
+      dst[(ma * 16 + g) * C + n8 * 8 + 2 * tq] += d[0];
+      dst[(ma * 16 + g) * C + n8 * 8 + 2 * tq + 1] += d[1];
+      dst[(ma * 16 + g + 8) * C + n8 * 8 + 2 * tq] += d[2];
+      dst[(ma * 16 + g + 8) * C + n8 * 8 + 2 * tq + 1] += d[3];
+    }
+    if (hl + 1 < nh) z2_phase(hl + 1);  // sz2t's readers (the dG3 MMAs of block hl) are done
+    if (hl + 1 < nh) continue;
+    // dZ1 partial of this h-range: D rows = tokens, columns = aj
+#pragma unroll
+    for (int u = 0; u < DZT; ++u) {
+      const int tl = warp + 8 * u, m = tl / (K2 / 8), n = tl % (K2 / 8);
+      const int r0 = m * 16 + g, col = n * 8 + 2 * tq;
+      float* base = dz1p + (static_cast<int64_t>(hs) * T + t0) * K2;
+      if (r0 < nt) *reinterpret_cast<float2*>(base + static_cast<int64_t>(r0) * K2 + col) = make_float2(dacc[u][0], dacc[u][1]);
+      if (r0 + 8 < nt)
+        *reinterpret_cast<float2*>(base + static_cast<int64_t>(r0 + 8) * K2 + col) = make_float2(dacc[u][2], dacc[u][3]);
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+  // dG3 partial of this CTA: element (col = warp*32 + i*16 + g (+8), c = n8*8 + 2tq (+1))
+  float* dst3 = g3part + (static_cast<int64_t>(ts) * gridDim.x + hs) * (C * FB_COLS);
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int n8 = 0; n8 < NT; ++n8) {
+      const int col = warp * 32 + i * 16 + g;
+      const int c = n8 * 8 + 2 * tq;
+      dst3[c * FB_COLS + col] = acc2[i][n8][0];
+      dst3[(c + 1) * FB_COLS + col] = acc2[i][n8][1];
+      dst3[c * FB_COLS + col + 8] = acc2[i][n8][2];
+      dst3[(c + 1) * FB_COLS + col + 8] = acc2[i][n8][3];
+    }
+  // dG2 partial of token split ts, h in [h0, h0 + nh)
+  float* dst2 = g2part + static_cast<int64_t>(ts) * (static_cast<int64_t>(C) * H * J1 * C);
+  for (int i = tid; i < nh * K2 * C; i += 256) {
+    const int hl = i / (K2 * C), aj = (i / C) % K2, c = i % C;
+    const int a = aj / J1, j2 = aj % J1;
+    dst2[((static_cast<int64_t>(a) * H + h0 + hl) * J1 + j2) * C + c] = sdg2[i];
+  }
+}
+
+// Fixed-order reduction of up to three partial sets in one launch, plus (optionally) the B_ext
+// operand of the dX GEMM's adapter extension (k_build_bext).
+struct ReduceSet {
+  const float* part;
+  int nparts;
+  int64_t numel;
+  float* out;
+};
+struct ReduceArgs {
+  ReduceSet set[3];
+  int64_t blocks[3];
+  int accumulate;
+  int R1, J1;
+  const float* G1;
+  __nv_bfloat16* bext;
+  int64_t K, ldb;
+};
+
+__global__ void __launch_bounds__(256) k_grad_reduce3(const ReduceArgs a) {
+  __shared__ float red[8][33];
+  int64_t b = blockIdx.x;
+  int si = 0;
+  while (si < 3 && b >= a.blocks[si]) b -= a.blocks[si++];
+  if (si == 3) {  // B_ext rows
+    const int64_t idx = b * 256 + threadIdx.x;
+    if (a.bext == nullptr || idx >= a.K * a.ldb) return;
+    const int64_t k = idx / a.ldb;
+    const int c = static_cast<int>(idx - k * a.ldb);
+    const int K2 = a.R1 * a.J1;
+    float v = 0.f;
+    if (c < 3 * K2) {  // [B_hi | B_hi | B_lo] against [dZ1_hi | dZ1_lo | dZ1_hi]
+      const int cc = c % K2;
+      const int aa = cc / a.J1, Jp = cc % a.J1;
+      if (static_cast<int>(k % a.J1) == Jp) v = a.G1[(k / a.J1) * a.R1 + aa];
+      if (c >= 2 * K2) v -= __bfloat162float(__float2bfloat16_rn(v));
+    }
+    a.bext[idx] = __float2bfloat16_rn(v);
+    return;
+  }
+  const ReduceSet& S = a.set[si];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t gi = b * 32 + lane;
+  float s = 0.f;
+  if (gi < S.numel) {
+    int c = warp;
+    for (; c + 24 < S.nparts; c += 32) {
+      const float a0 = S.part[static_cast<int64_t>(c) * S.numel + gi];
+      const float a1 = S.part[static_cast<int64_t>(c + 8) * S.numel + gi];
+      const float a2 = S.part[static_cast<int64_t>(c + 16) * S.numel + gi];
+      const float a3 = S.part[static_cast<int64_t>(c + 24) * S.numel + gi];
+      s += a0;
+      s += a1;
+      s += a2;
+      s += a3;
+    }
+    for (; c < S.nparts; c += 8) s += S.part[static_cast<int64_t>(c) * S.numel + gi];
+  }
+  red[warp][lane] = s;
+  __syncthreads();
+  if (warp == 0 && gi < S.numel) {
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += red[w][lane];
+    S.out[gi] = a.accumulate ? S.out[gi] + t : t;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
 // x pass of the backward: dG1[j1, a] partial = Σ_{t in split} Σ_J x[t, j1 J1 + J] dZ1[t, a, J]
+// dz1 may hold HS partials ([HS][T][K2], summed here in fixed order); when dz1b is given, the CTAs
+// of column block 0 also write the [hi | lo | hi | 0] bf16 split of the summed rows (the dX GEMM's
+// extension operand, see k_split_rows).
+// Ring-buffered x pass for bf16 rows (J1 = 4): each thread owns 8 columns and streams its own
+// 16-byte pieces of x through a 3-stage cp.async ring (8 token rows per stage), so the bytes in
+// flight per SM (up to 2 CTAs x 2 stages x 32 KB) no longer depend on registers.  The ring is
+// thread-private: only the dZ1 block (32 tokens) needs CTA barriers.
+constexpr int DG_ROWS = 8, DG_NST = 3;
+
+template <int R1>
+__global__ void __launch_bounds__(256) k_tt_dg1r(const __nv_bfloat16* __restrict__ x, int64_t T, int64_t K,
+                                                 const float* __restrict__ dz1, float* __restrict__ part, int S,
+                                                 int HS, __nv_bfloat16* __restrict__ dz1b, int64_t ldb) {
+  constexpr int J1 = 4, K2 = J1 * R1, NJ = 2, TB = 32;
+  __shared__ __align__(16) float sdz[TB][J1][R1];
+  extern __shared__ __align__(16) uint4 sxr[];  // [DG_NST][DG_ROWS][256]
+  const int tid = threadIdx.x;
+  const int64_t col0 = (static_cast<int64_t>(blockIdx.x) * 256 + tid) * 8;
+  const bool active = col0 < K;
+  const int s = blockIdx.y;
+  const int64_t per = (T + S - 1) / S;
+  const int64_t t0 = s * per, t1 = t0 + per < T ? t0 + per : T;
+  const int64_t nst = t1 > t0 ? (t1 - t0 + DG_ROWS - 1) / DG_ROWS : 0;
+  unsigned long long acc[NJ][R1 / 2];
+#pragma unroll
+  for (int j = 0; j < NJ; ++j)
+#pragma unroll
+    for (int a = 0; a < R1 / 2; ++a) acc[j][a] = 0ull;
+  auto issue = [&](int64_t k) {
+    if (k < nst) {
+#pragma unroll
+      for (int r = 0; r < DG_ROWS; ++r) {
+        const int64_t t = t0 + k * DG_ROWS + r;
+        const bool ok = active && t < t1;
+        cp_async16(&sxr[(static_cast<int>(k % DG_NST) * DG_ROWS + r) * 256 + tid], ok ? x + t * K + col0 : x, ok);
+      }
+    }
+    cp_async_commit();
+  };
+  for (int k = 0; k < DG_NST - 1; ++k) issue(k);
+  for (int64_t k = 0; k < nst; ++k) {
+    if (k % (TB / DG_ROWS) == 0) {
+      const int64_t tb = t0 + k * DG_ROWS;
+      const int nt = static_cast<int>(t1 - tb < TB ? t1 - tb : TB);
+      __syncthreads();
+      for (int i = tid; i < nt * K2; i += 256) {
+        const int r = i / K2, cc = i % K2;
+        const int64_t off = (tb + r) * K2 + cc;
+        float v = dz1[off];
+        for (int h = 1; h < HS; ++h) v += dz1[static_cast<int64_t>(h) * T * K2 + off];
+        sdz[r][cc % J1][cc / J1] = v;
+      }
+      __syncthreads();
+      if (dz1b != nullptr && blockIdx.x == 0) {
+        for (int i = tid; i < nt * static_cast<int>(ldb); i += 256) {
+          const int r = i / static_cast<int>(ldb), c = i % static_cast<int>(ldb);
+          float v = 0.f;
+          if (c < 3 * K2) {  // [hi | lo | hi]
+            const int cc = c % K2;
+            const float f = sdz[r][cc % J1][cc / J1];
+            v = __bfloat162float(__float2bfloat16_rn(f));
+            if (c >= K2 && c < 2 * K2) v = f - v;
+          }
+          dz1b[(tb + r) * ldb + c] = __float2bfloat16_rn(v);
+        }
+      }
+    }
+    issue(k + DG_NST - 1);
+    cp_async_wait<DG_NST - 1>();
+    if (!active) continue;
+    const int rb = static_cast<int>(k % (TB / DG_ROWS)) * DG_ROWS;
+    const int nr = static_cast<int>(t1 - (t0 + k * DG_ROWS) < DG_ROWS ? t1 - (t0 + k * DG_ROWS) : DG_ROWS);
+    for (int r = 0; r < nr; ++r) {
+      const uint4 raw = sxr[(static_cast<int>(k % DG_NST) * DG_ROWS + r) * 256 + tid];
+      const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+      for (int J = 0; J < J1; ++J) {
+        const float4* dz4 = reinterpret_cast<const float4*>(&sdz[rb + r][J][0]);
+        float4 d4[R1 / 4];
+#pragma unroll
+        for (int q = 0; q < R1 / 4; ++q) d4[q] = dz4[q];
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+          const int e = j * J1 + J;  // element e of the 8: bf16 half (e & 1) of word e / 2
+          const float xv = __uint_as_float((e & 1) ? (w[e >> 1] & 0xFFFF0000u) : (w[e >> 1] << 16));
+          const unsigned long long xx = f2pack(xv, xv);
+#pragma unroll
+          for (int q = 0; q < R1 / 4; ++q) {
+            ffma2(acc[j][2 * q], xx, f2pack(d4[q].x, d4[q].y));
+            ffma2(acc[j][2 * q + 1], xx, f2pack(d4[q].z, d4[q].w));
+          }
+        }
+      }
+    }
+  }
+  cp_async_wait<0>();
+  if (!active) return;
+  float* dst = part + static_cast<int64_t>(s) * (K / J1) * R1;
+#pragma unroll
+  for (int j = 0; j < NJ; ++j)
+#pragma unroll
+    for (int a = 0; a < R1 / 2; ++a) {
+      dst[(col0 / J1 + j) * R1 + 2 * a] = f2lo(acc[j][a]);
+      dst[(col0 / J1 + j) * R1 + 2 * a + 1] = f2hi(acc[j][a]);
+    }
+}
+
 template <typename InT, int J1, int R1>
 __global__ void __launch_bounds__(256) k_tt_dg1(const InT* __restrict__ x, int64_t T, int64_t K,
-                                                const float* __restrict__ dz1, float* __restrict__ part, int S) {
+                                                const float* __restrict__ dz1, float* __restrict__ part, int S,
+                                                int HS, __nv_bfloat16* __restrict__ dz1b, int64_t ldb) {
   constexpr int K2 = J1 * R1;
   constexpr int E = J1 == 1 ? 4 : 8;  // x elements per thread
   constexpr int NJ = E / J1;
   constexpr int TB = 32;
-  __shared__ __align__(16) float sdz[TB][K2];
+  static_assert(R1 % 4 == 0, "R1");
+  __shared__ __align__(16) float sdz[TB][J1][R1];  // dZ1 rows as [t][J][a]: (a, a+1) pairs adjacent for FFMA2
   const int64_t col0 = (static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x) * E;
   const bool active = col0 < K;
   const int s = blockIdx.y;
   const int64_t per = (T + S - 1) / S;
   const int64_t t0 = s * per, t1 = t0 + per < T ? t0 + per : T;
-  float acc[NJ][R1];
+  unsigned long long acc[NJ][R1 / 2];
 #pragma unroll
   for (int j = 0; j < NJ; ++j)
 #pragma unroll
-    for (int a = 0; a < R1; ++a) acc[j][a] = 0.f;
+    for (int a = 0; a < R1 / 2; ++a) acc[j][a] = 0ull;
   for (int64_t tb = t0; tb < t1; tb += TB) {
     const int nt = static_cast<int>(t1 - tb < TB ? t1 - tb : TB);
     __syncthreads();
-    for (int i = threadIdx.x; i < nt * K2; i += 256) sdz[i / K2][i % K2] = dz1[(tb + i / K2) * K2 + i % K2];
+    for (int i = threadIdx.x; i < nt * K2; i += 256) {
+      const int r = i / K2, cc = i % K2;
+      const int64_t off = (tb + r) * K2 + cc;
+      float v = dz1[off];
+      for (int h = 1; h < HS; ++h) v += dz1[static_cast<int64_t>(h) * T * K2 + off];
+      sdz[r][cc % J1][cc / J1] = v;
+    }
     __syncthreads();
+    if (dz1b != nullptr && blockIdx.x == 0) {
+      for (int i = threadIdx.x; i < nt * static_cast<int>(ldb); i += 256) {
+        const int r = i / static_cast<int>(ldb), c = i % static_cast<int>(ldb);
+        float v = 0.f;
+        if (c < 3 * K2) {  // [hi | lo | hi]
+          const int cc = c % K2;
+          const float f = sdz[r][cc % J1][cc / J1];
+          v = __bfloat162float(__float2bfloat16_rn(f));
+          if (c >= K2 && c < 2 * K2) v = f - v;
+        }
+        dz1b[(tb + r) * ldb + c] = __float2bfloat16_rn(v);
+      }
+    }
     if (!active) continue;
     constexpr int UNR = 4;  // token rows of x in flight per thread
     for (int r0 = 0; r0 < nt; r0 += UNR) {
@@ -1552,13 +2015,22 @@ __global__ void __launch_bounds__(256) k_tt_dg1(const InT* __restrict__ x, int64
       for (int u = 0; u < UNR; ++u) {
         if (r0 + u >= nt) break;
 #pragma unroll
-        for (int j = 0; j < NJ; ++j)
+        for (int J = 0; J < J1; ++J) {
+          const float4* dz4 = reinterpret_cast<const float4*>(&sdz[r0 + u][J][0]);
+          float4 d4[R1 / 4];
 #pragma unroll
-          for (int J = 0; J < J1; ++J) {
+          for (int q = 0; q < R1 / 4; ++q) d4[q] = dz4[q];
+#pragma unroll
+          for (int j = 0; j < NJ; ++j) {
             const float xv = f[u][j * J1 + J];
+            const unsigned long long xx = f2pack(xv, xv);
 #pragma unroll
-            for (int a = 0; a < R1; ++a) acc[j][a] = fmaf(xv, sdz[r0 + u][a * J1 + J], acc[j][a]);
+            for (int q = 0; q < R1 / 4; ++q) {
+              ffma2(acc[j][2 * q], xx, f2pack(d4[q].x, d4[q].y));
+              ffma2(acc[j][2 * q + 1], xx, f2pack(d4[q].z, d4[q].w));
+            }
           }
+        }
       }
     }
   }
@@ -1568,7 +2040,10 @@ __global__ void __launch_bounds__(256) k_tt_dg1(const InT* __restrict__ x, int64
 #pragma unroll
   for (int j = 0; j < NJ; ++j)
 #pragma unroll
-    for (int a = 0; a < R1; ++a) dst[(col0 / J1 + j) * R1 + a] = acc[j][a];
+    for (int a = 0; a < R1 / 2; ++a) {
+      dst[(col0 / J1 + j) * R1 + 2 * a] = f2lo(acc[j][a]);
+      dst[(col0 / J1 + j) * R1 + 2 * a + 1] = f2hi(acc[j][a]);
+    }
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -1766,6 +2241,15 @@ bool fast_tt_supported(int J1, int R1) {
 bool aq_mma_disabled() {
   static const bool off = [] {
     const char* v = getenv("QA_AQ_MMA");
+    return v != nullptr && v[0] == '0';
+  }();
+  return off;
+}
+
+// QA_FUSED_BWD=0 selects the unfused dy pass / middle-core kernels (A/B comparisons).
+bool fused_bwd_disabled() {
+  static const bool off = [] {
+    const char* v = getenv("QA_FUSED_BWD");
     return v != nullptr && v[0] == '0';
   }();
   return off;
@@ -2107,6 +2591,71 @@ cudaError_t launch_tt_dy(const __nv_bfloat16* dy, int64_t T, int64_t N, int H, i
   return cudaGetLastError();
 }
 
+bool tt_bwd_fused_ok(int d, int J1, int R1, int C, int M) {
+  return d == 3 && J1 == 4 && M == FB_COLS && R1 == C && (C == 8 || C == 16) && !fused_bwd_disabled();
+}
+
+// h-range per CTA: the dG2 accumulators (HR x K2 x C fp32) and Gm_h stay <= 64 KB of shared memory
+void tt_bwd_fused_plan(int64_t T, int H, int C, int* HR, int* HS, int* TS) {
+  const int hr_max = C == 8 ? 16 : 8;
+  *HS = (H + hr_max - 1) / hr_max;
+  *HR = (H + *HS - 1) / *HS;
+  const int64_t tiles = (T + FB_TT - 1) / FB_TT;
+  const int per_sm = C == 8 ? 2 : 1;
+  int64_t ts = (static_cast<int64_t>(per_sm) * 148 + *HS - 1) / *HS;
+  if (ts > tiles) ts = tiles;
+  *TS = static_cast<int>(ts < 1 ? 1 : ts);
+}
+
+cudaError_t launch_tt_bwd_fused(const __nv_bfloat16* dy, int64_t ldy, int64_t T, int H, int C, const float* Z1,
+                                const float* G2, const float* G3, float* dz1p, float* g3part, float* g2part,
+                                cudaStream_t s) {
+  if (T == 0) return cudaSuccess;
+  int HR, HS, TS;
+  tt_bwd_fused_plan(T, H, C, &HR, &HS, &TS);
+  const int64_t N = static_cast<int64_t>(H) * FB_COLS;
+  LaunchScope scope(kTT, 4.0 * double(T) * N * C + 6.0 * double(T) * H * 4 * C * C, s);
+  count_launches(1);
+  const dim3 grid(static_cast<unsigned>(HS), static_cast<unsigned>(TS));
+  if (C == 8) {
+    const size_t smem = FbLayout<8>::bytes(HR);
+    cudaFuncSetAttribute(k_tt_bwd_fused<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    k_tt_bwd_fused<8><<<grid, 256, smem, s>>>(dy, ldy, T, H, HR, Z1, G2, G3, dz1p, g3part, g2part);
+  } else {
+    const size_t smem = FbLayout<16>::bytes(HR);
+    cudaFuncSetAttribute(k_tt_bwd_fused<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    k_tt_bwd_fused<16><<<grid, 256, smem, s>>>(dy, ldy, T, H, HR, Z1, G2, G3, dz1p, g3part, g2part);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_grad_reduce3(const float* const* parts, const int* nparts, const int64_t* numel,
+                                float* const* outs, bool accumulate, int R1, int J1, const float* G1,
+                                __nv_bfloat16* bext, int64_t K, int64_t ldb, cudaStream_t s) {
+  ReduceArgs a;
+  int64_t total = 0;
+  double bytes = 0.0;
+  for (int i = 0; i < 3; ++i) {
+    a.set[i] = ReduceSet{parts[i], nparts[i], numel[i], outs[i]};
+    a.blocks[i] = (parts[i] != nullptr && outs[i] != nullptr) ? (numel[i] + 31) / 32 : 0;
+    total += a.blocks[i];
+    bytes += 4.0 * double(numel[i]) * (nparts[i] + 1);
+  }
+  a.accumulate = accumulate ? 1 : 0;
+  a.R1 = R1;
+  a.J1 = J1;
+  a.G1 = G1;
+  a.bext = bext;
+  a.K = K;
+  a.ldb = ldb;
+  if (bext != nullptr) total += (K * ldb + 255) / 256;
+  if (total == 0) return cudaSuccess;
+  LaunchScope scope(kTT, bytes + (bext ? 2.0 * double(K) * ldb : 0.0), s);
+  count_launches(1);
+  k_grad_reduce3<<<static_cast<unsigned>(total), 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
 int tt_dg1_splits(int64_t T, int64_t K, int J1) {
   const int E = J1 == 1 ? 4 : 8;
   const int64_t gx = (K + 256 * E - 1) / (256 * E);
@@ -2116,14 +2665,25 @@ int tt_dg1_splits(int64_t T, int64_t K, int J1) {
 }
 
 cudaError_t launch_tt_dg1(const void* x, int x_dtype, int64_t T, int64_t K, const float* dz1, int J1, int R1,
-                          float* part, int S, cudaStream_t s) {
+                          float* part, int S, cudaStream_t s, int HS, __nv_bfloat16* dz1b, int64_t ldb) {
   if (T == 0) return cudaSuccess;
   LaunchScope scope(kTT, 2.0 * double(T) * K * R1, s);
   count_launches(1);
   const int E = J1 == 1 ? 4 : 8;
   const dim3 grid(static_cast<unsigned>((K + 256 * E - 1) / (256 * E)), static_cast<unsigned>(S));
+  if (x_dtype == QA_BF16 && J1 == 4 && K % 8 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0) {
+    const size_t smem = sizeof(uint4) * DG_NST * DG_ROWS * 256;
+    if (R1 == 8) {
+      cudaFuncSetAttribute(k_tt_dg1r<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      k_tt_dg1r<8><<<grid, 256, smem, s>>>(static_cast<const __nv_bfloat16*>(x), T, K, dz1, part, S, HS, dz1b, ldb);
+    } else {
+      cudaFuncSetAttribute(k_tt_dg1r<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      k_tt_dg1r<16><<<grid, 256, smem, s>>>(static_cast<const __nv_bfloat16*>(x), T, K, dz1, part, S, HS, dz1b, ldb);
+    }
+    return cudaGetLastError();
+  }
 #define QA_DG(TI, JJ, RR) \
-  k_tt_dg1<TI, JJ, RR><<<grid, 256, 0, s>>>(static_cast<const TI*>(x), T, K, dz1, part, S)
+  k_tt_dg1<TI, JJ, RR><<<grid, 256, 0, s>>>(static_cast<const TI*>(x), T, K, dz1, part, S, HS, dz1b, ldb)
 #define QA_DG_T(TI)                 \
   if (J1 == 1 && R1 == 8)           \
     QA_DG(TI, 1, 8);                \

@@ -20,8 +20,11 @@ for r in rows[2:]:
     if op.startswith("@"):
         op = s.split()[1]
     op = op.split(".")[0]
-    n = float(r[iex] or 0)
-    st = float(r[iss] or 0)
+    try:
+        n = float(r[iex] or 0)
+        st = float(r[iss] or 0)
+    except ValueError:  # a repeated header (several kernels in one export)
+        continue
     ops[op] += n
     stalls[op] += st
     lines.append((n, st, r[ia][-5:], s[:90]))
