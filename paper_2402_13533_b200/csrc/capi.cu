@@ -468,12 +468,13 @@ int linear_backward_impl(const qa_qweight* w, const qa_tt* tt, const void* x, in
                   "TT fused dy pass");
       // one pass over x: dG1 partials, dZ1 summed over the h-ranges, its bf16 split for the dX GEMM
       const bool want_g1 = dcores != nullptr && dcores[0] != nullptr;
+      int s_dg1 = P.S_dg1;
       if (want_g1 || want_dx)
         QA_TRY_CUDA(launch_tt_dg1(x, x_dtype, T, K, P.dz1p, P.J1, P.R1, P.g1p, P.S_dg1, s, P.HS,
-                                  want_dx ? P.dz1b : nullptr, P.K2p),
+                                  want_dx ? P.dz1b : nullptr, P.K2p, &s_dg1),
                     "TT x pass");
       const float* parts[3] = {P.g1p, P.g2p, P.g3p};
-      const int nparts[3] = {P.S_dg1, P.TS, P.HS * P.TS};
+      const int nparts[3] = {s_dg1, P.TS, P.HS * P.TS};
       const int64_t numel[3] = {dd.core_numel(0), dd.core_numel(1), dd.core_numel(2)};
       float* outs[3] = {want_g1 ? dcores[0] : nullptr, dcores != nullptr ? dcores[1] : nullptr,
                         dcores != nullptr ? dcores[2] : nullptr};
@@ -539,8 +540,10 @@ int linear_backward_impl(const qa_qweight* w, const qa_tt* tt, const void* x, in
     }
     // x pass: dG1 = Σ_t x ⊗ dZ1
     if (dcores != nullptr && dcores[0] != nullptr) {
-      QA_TRY_CUDA(launch_tt_dg1(x, x_dtype, T, K, dz1, P.J1, P.R1, P.gpart, P.S_dg1, s), "TT x pass");
-      QA_TRY_CUDA(launch_sum_partials(P.gpart, P.S_dg1, K / P.J1 * P.R1, dcores[0], accumulate != 0, s), "reduce dG1");
+      int s_dg1 = P.S_dg1;
+      QA_TRY_CUDA(launch_tt_dg1(x, x_dtype, T, K, dz1, P.J1, P.R1, P.gpart, P.S_dg1, s, 1, nullptr, 0, &s_dg1),
+                  "TT x pass");
+      QA_TRY_CUDA(launch_sum_partials(P.gpart, s_dg1, K / P.J1 * P.R1, dcores[0], accumulate != 0, s), "reduce dG1");
     }
     if (want_dx) {
       // adapter dx = dZ1 · B_extᵀ as extension k-blocks of the dX GEMM

@@ -267,6 +267,16 @@ QA_DEV void ldsm_x2_t(const void* p, uint32_t& r0, uint32_t& r1) {
 QA_DEV void ldsm_x1(const void* p, uint32_t& r0) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x1.shared.b16 {%0}, [%1];" : "=r"(r0) : "r"(smem_u32(p)));
 }
+// transpose of an 8x8 b16 matrix held as one register per lane (row g, cols 2tq..2tq+1)
+QA_DEV uint32_t movm_t(uint32_t x) {
+  uint32_t y;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+QA_DEV uint32_t pack_bf16(float lo, float hi) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&v);
+}
 // D(16x8 f32) += A(16x8 bf16, row) · B(8x8 bf16, col)
 QA_DEV void mma_1688(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t b0) {
   asm volatile(

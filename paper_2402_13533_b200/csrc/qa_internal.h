@@ -89,7 +89,7 @@ int tt_dg1_splits(int64_t T, int64_t K, int J1);
 // dz1: HS partials [HS][T][K2] (summed in fixed order); dz1b (nullable): [hi | lo | hi | 0] split rows
 cudaError_t launch_tt_dg1(const void* x, int x_dtype, int64_t T, int64_t K, const float* dz1, int J1, int R1,
                           float* part, int S, cudaStream_t s, int HS = 1, __nv_bfloat16* dz1b = nullptr,
-                          int64_t ldb = 0);
+                          int64_t ldb = 0, int* splits_used = nullptr);  // partials written: *splits_used <= S
 // fused backward of the pinned Llama modes (d = 3, J1 = 4, M = 256, R1 = C in {8, 16})
 bool tt_bwd_fused_ok(int d, int J1, int R1, int C, int M);
 void tt_bwd_fused_plan(int64_t T, int H, int C, int* HR, int* HS, int* TS);

@@ -1537,7 +1537,8 @@ struct FbLayout {
   static constexpr size_t dz2p = z1p + sizeof(__nv_bfloat16) * 2 * FB_TT * LZ1;   // bf16 [2][TT][LC]
   static constexpr size_t gmp = dz2p + sizeof(__nv_bfloat16) * 2 * FB_TT * LC;    // bf16 [2][HR][K2][LC]
   __host__ __device__ static size_t dg2(int hr) { return gmp + sizeof(__nv_bfloat16) * 2 * size_t(hr) * K2 * LC; }  // f32 [HR][K2][C]
-  __host__ __device__ static size_t bytes(int hr) { return dg2(hr) + sizeof(float) * size_t(hr) * K2 * C; }
+  __host__ __device__ static size_t z1raw(int hr) { return dg2(hr) + sizeof(float) * size_t(hr) * K2 * C; }  // f32 [2][TT][K2]
+  __host__ __device__ static size_t bytes(int hr) { return z1raw(hr) + sizeof(float) * 2 * FB_TT * K2; }
 };
 
 template <int C>
@@ -1559,6 +1560,7 @@ __global__ void __launch_bounds__(256) k_tt_bwd_fused(const __nv_bfloat16* __res
   auto sdz2p = reinterpret_cast<__nv_bfloat16(*)[FB_TT][LC]>(fb_smem + L::dz2p);
   __nv_bfloat16* sgmp = reinterpret_cast<__nv_bfloat16*>(fb_smem + L::gmp);
   float* sdg2 = reinterpret_cast<float*>(fb_smem + L::dg2(HR));
+  float* sz1raw = reinterpret_cast<float*>(fb_smem + L::z1raw(HR));
   auto gm = [&](int p, int hl, int aj, int c) -> __nv_bfloat16* {
     return sgmp + ((static_cast<size_t>(p) * HR + hl) * K2 + aj) * LC + c;
   };
@@ -1621,10 +1623,22 @@ __global__ void __launch_bounds__(256) k_tt_bwd_fused(const __nv_bfloat16* __res
 
   // the CTA's (tile, h) items form one stream; dy blocks are prefetched FB_NS - 1 items ahead
   const int64_t nit = (tile1 - tile0) * nh;
+  // Z1 rows of a tile are prefetched into sz1raw one tile ahead when a tile spans >= FB_NS items
+  const bool z1_async = nh >= FB_NS;
+  auto load_z1raw = [&](int64_t tile) {
+    if (tile >= tile1) return;
+    float* dst = sz1raw + static_cast<size_t>((tile - tile0) & 1) * FB_TT * K2;
+    for (int i = tid; i < FB_TT * (K2 / 4); i += 256) {
+      const int r = i / (K2 / 4), q = i % (K2 / 4);
+      const bool ok = tile * FB_TT + r < T;
+      cp_async16(dst + r * K2 + 4 * q, ok ? Z1 + (tile * FB_TT + r) * K2 + 4 * q : Z1, ok);
+    }
+  };
   auto issue = [&](int64_t it) {
     if (it < nit) load_dy((tile0 + it / nh) * FB_TT, h0 + static_cast<int>(it % nh), static_cast<int>(it % FB_NS));
     cp_async_commit();
   };
+  if (z1_async) load_z1raw(tile0);
   for (int i = 0; i < FB_NS - 1; ++i) issue(i);
   float dacc[DZT][4];
   for (int64_t it = 0; it < nit; ++it) {
@@ -1634,9 +1648,17 @@ __global__ void __launch_bounds__(256) k_tt_bwd_fused(const __nv_bfloat16* __res
     const int nt = static_cast<int>(T - t0 < FB_TT ? T - t0 : FB_TT);
     if (hl == 0) {
       __syncthreads();  // previous tile's readers of the Z1 planes are done
+      if (z1_async) {  // this tile's Z1 group (issued a tile ahead; tile 0: group 0) has landed ...
+        if (it == 0)
+          cp_async_wait<FB_NS - 2>();
+        else
+          cp_async_wait<FB_NS - 1>();
+      }
+      __syncthreads();                              // ... for every thread
+      const float* zr = sz1raw + static_cast<size_t>((tile - tile0) & 1) * FB_TT * K2;
       for (int i = tid; i < FB_TT * K2; i += 256) {
         const int r = i / K2, aj = i % K2;
-        const float f = r < nt ? Z1[(t0 + r) * K2 + aj] : 0.f;
+        const float f = r < nt ? (z1_async ? zr[i] : Z1[(t0 + r) * K2 + aj]) : 0.f;
         const __nv_bfloat16 hi = __float2bfloat16_rn(f);
         sz1p[0][r][aj] = hi;
         sz1p[1][r][aj] = __float2bfloat16_rn(f - __bfloat162float(hi));
@@ -1648,6 +1670,7 @@ __global__ void __launch_bounds__(256) k_tt_bwd_fused(const __nv_bfloat16* __res
       __syncthreads();
       z2_phase(0);
     }
+    if (z1_async && hl == 0) load_z1raw(tile + 1);  // joins the group below; needed nh >= FB_NS items later
     issue(it + FB_NS - 1);  // into the buffer item it - 1 used; its readers passed two barriers since
     cp_async_wait<FB_NS - 1>();
     __syncthreads();  // dy_h and Z2_h are in shared memory
@@ -1776,6 +1799,255 @@ __global__ void __launch_bounds__(256) k_tt_bwd_fused(const __nv_bfloat16* __res
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Warp-specialised fused backward for C = 8 (the benchmark's rank).  Same contractions as
+// k_tt_bwd_fused, but each warp owns whole output blocks h (local h = warp, warp + 8) and streams
+// its own 16-token x 256-column dy blocks through a private 2-slot cp.async ring, so the only CTA
+// barriers are at 16-token tile boundaries (Z1 planes in, dZ1 partials out).  Every intermediate
+// of a block stays in registers: the m16n8 D fragments of Z2_h and dZ2_h are re-used as the
+// m16n8k8 A fragments (dZ1 += dZ2_h · Gm_hᵀ) and, transposed with movmatrix, as the B fragments
+// of dG3 += dy_hᵀ · Z2_h and dG2_h += Z1ᵀ · dZ2_h.  dG3 / dG2 accumulate in registers per warp.
+constexpr int WS_TT = 16, WS_NHW = 2, WS_LDZ1 = 40;
+
+struct WsLayout {
+  static constexpr size_t dy = 0;                                                         // bf16 [8][2][TT][LDY]
+  static constexpr size_t g3 = dy + sizeof(__nv_bfloat16) * 8 * 2 * WS_TT * FB_LDY;     // bf16 [8][LDY]
+  static constexpr size_t z1p = g3 + sizeof(__nv_bfloat16) * 8 * FB_LDY;                // bf16 [2][TT][LDZ1]
+  static constexpr size_t z1raw = z1p + sizeof(__nv_bfloat16) * 2 * WS_TT * WS_LDZ1;    // f32 [2][TT][32]
+  static constexpr size_t dzs = z1raw + sizeof(float) * 2 * WS_TT * 32;                 // f32 [8][TT][33]
+  static constexpr size_t gmp = dzs + sizeof(float) * 8 * WS_TT * 33;                   // bf16 [2][HR][32][8]
+  __host__ __device__ static size_t bytes(int hr) { return gmp + sizeof(__nv_bfloat16) * 2 * size_t(hr) * 32 * 8; }
+};
+
+__global__ void __launch_bounds__(256, 1) k_tt_bwd_ws(const __nv_bfloat16* __restrict__ dy, int64_t ldy, int64_t T,
+                                                      int H, int HR, const float* __restrict__ Z1,
+                                                      const float* __restrict__ G2, const float* __restrict__ G3,
+                                                      float* __restrict__ dz1p, float* __restrict__ g3part,
+                                                      float* __restrict__ g2part) {
+  constexpr int C = 8, K2 = 32, J1 = 4;
+  extern __shared__ __align__(16) uint8_t ws_smem[];
+  auto sdy = reinterpret_cast<__nv_bfloat16(*)[2][WS_TT][FB_LDY]>(ws_smem + WsLayout::dy);
+  auto sg3 = reinterpret_cast<__nv_bfloat16(*)[FB_LDY]>(ws_smem + WsLayout::g3);
+  auto sz1p = reinterpret_cast<__nv_bfloat16(*)[WS_TT][WS_LDZ1]>(ws_smem + WsLayout::z1p);
+  auto sz1raw = reinterpret_cast<float(*)[WS_TT][K2]>(ws_smem + WsLayout::z1raw);
+  auto sdzs = reinterpret_cast<float(*)[WS_TT][K2 + 1]>(ws_smem + WsLayout::dzs);
+  __nv_bfloat16* sgmp = reinterpret_cast<__nv_bfloat16*>(ws_smem + WsLayout::gmp);
+  auto gm = [&](int p, int hl, int aj) -> __nv_bfloat16* {
+    return sgmp + ((static_cast<size_t>(p) * HR + hl) * K2 + aj) * C;
+  };
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, tq = lane & 3, q = lane >> 3;
+  const int hs = blockIdx.x, ts = blockIdx.y, TS = gridDim.y;
+  const int h0 = hs * HR, nh = H - h0 < HR ? H - h0 : HR;
+  const int64_t ntiles = (T + WS_TT - 1) / WS_TT;
+  const int64_t per = (ntiles + TS - 1) / TS;
+  const int64_t tile0 = ts * per, tile1 = tile0 + per < ntiles ? tile0 + per : ntiles;
+  const int nmine = nh > warp ? (nh - warp + 7) / 8 : 0;  // this warp's h blocks (<= WS_NHW)
+  const int64_t nit = (tile1 > tile0 ? tile1 - tile0 : 0) * nmine;
+
+  for (int i = tid; i < C * FB_COLS; i += 256) sg3[i / FB_COLS][i % FB_COLS] = __float2bfloat16_rn(G3[i]);
+  for (int i = tid; i < nh * K2 * C; i += 256) {
+    const int hl = i / (K2 * C), aj = (i / C) % K2, c = i % C;
+    const int a = aj / J1, j2 = aj % J1;
+    const float v = G2[((static_cast<int64_t>(a) * H + h0 + hl) * J1 + j2) * C + c];
+    const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+    gm(0, hl, aj)[c] = hi;
+    gm(1, hl, aj)[c] = __float2bfloat16_rn(v - __bfloat162float(hi));
+  }
+  auto load_item = [&](int64_t it, int slot) {
+    const int64_t t0 = (tile0 + it / nmine) * WS_TT;
+    const int h = h0 + warp + 8 * static_cast<int>(it % nmine);
+#pragma unroll
+    for (int r = 0; r < WS_TT; ++r) {  // one 512-byte row per warp instruction
+      const int64_t t = t0 + r;
+      const bool ok = t < T;
+      cp_async16(&sdy[warp][slot][r][lane * 8], dy + (ok ? t : 0) * ldy + static_cast<int64_t>(h) * FB_COLS + lane * 8,
+                 ok);
+    }
+  };
+  auto load_z1raw = [&](int64_t tile) {
+    if (tile >= tile1 || tid >= WS_TT * K2 / 4) return;
+    const int r = tid / (K2 / 4), c4 = tid % (K2 / 4);
+    const bool ok = tile * WS_TT + r < T;
+    cp_async16(&sz1raw[(tile - tile0) & 1][r][4 * c4], ok ? Z1 + (tile * WS_TT + r) * K2 + 4 * c4 : Z1, ok);
+  };
+  float acc3[16][4];
+#pragma unroll
+  for (int m = 0; m < 16; ++m)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) acc3[m][k] = 0.f;
+  float g2acc[WS_NHW][2][4];
+#pragma unroll
+  for (int i = 0; i < WS_NHW; ++i)
+#pragma unroll
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) g2acc[i][m][k] = 0.f;
+
+  load_z1raw(tile0);
+  if (nit > 0) load_item(0, 0);
+  cp_async_commit();
+  int64_t it = 0;
+  for (int64_t tile = tile0; tile < tile1; ++tile) {
+    const int64_t t0 = tile * WS_TT;
+    const int nt = static_cast<int>(T - t0 < WS_TT ? T - t0 : WS_TT);
+    __syncthreads();     // previous tile: Z1 planes and dZ1 partial buffers are free
+    cp_async_wait<0>();  // this tile's Z1 rows (and the warp's first dy block) landed ...
+    __syncthreads();     // ... for every thread
+    for (int i = tid; i < WS_TT * K2; i += 256) {
+      const int r = i / K2, aj = i % K2;
+      const float f = r < nt ? sz1raw[(tile - tile0) & 1][r][aj] : 0.f;
+      const __nv_bfloat16 hi = __float2bfloat16_rn(f);
+      sz1p[0][r][aj] = hi;
+      sz1p[1][r][aj] = __float2bfloat16_rn(f - __bfloat162float(hi));
+    }
+    __syncthreads();
+    load_z1raw(tile + 1);
+    cp_async_commit();
+    // Z1 fragments of the tile: A of Z2 = Z1 · Gm (rows t, k = aj) and A of dG2 = Z1ᵀ · dZ2 (rows aj, k = t)
+    uint32_t za[2][2][4], zt[2][2][4];
+#pragma unroll
+    for (int p = 0; p < 2; ++p)
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        ldsm_x4(&sz1p[p][lane & 15][k * 16 + (lane >> 4) * 8], za[p][k][0], za[p][k][1], za[p][k][2], za[p][k][3]);
+        ldsm_x4_t(&sz1p[p][(q >> 1) * 8 + (lane & 7)][k * 16 + (q & 1) * 8], zt[p][k][0], zt[p][k][1], zt[p][k][2],
+                  zt[p][k][3]);
+      }
+    float dz1acc[4][4];
+#pragma unroll
+    for (int n = 0; n < 4; ++n)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) dz1acc[n][k] = 0.f;
+#pragma unroll
+    for (int i = 0; i < WS_NHW; ++i, ++it) {
+      if (i >= nmine) break;
+      const int slot = static_cast<int>(it & 1), hl = warp + 8 * i;
+      if (i == 0)
+        cp_async_wait<1>();
+      else
+        cp_async_wait<0>();
+      __syncwarp();
+      if (it + 1 < nit) load_item(it + 1, slot ^ 1);
+      cp_async_commit();
+      const __nv_bfloat16(*dyw)[FB_LDY] = sdy[warp][slot];
+      // Z2_h = Z1 · Gm_h
+      float z2[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        uint32_t bh0, bh1, bl0, bl1;
+        ldsm_x2_t(gm(0, hl, k * 16 + (lane & 15)), bh0, bh1);
+        ldsm_x2_t(gm(1, hl, k * 16 + (lane & 15)), bl0, bl1);
+        mma_16816(z2, za[0][k][0], za[0][k][1], za[0][k][2], za[0][k][3], bh0, bh1);
+        mma_16816(z2, za[1][k][0], za[1][k][1], za[1][k][2], za[1][k][3], bh0, bh1);
+        mma_16816(z2, za[0][k][0], za[0][k][1], za[0][k][2], za[0][k][3], bl0, bl1);
+      }
+      // dZ2_h = dy_h · G3ᵀ (two accumulator chains, summed in fixed order)
+      float e0[4] = {0.f, 0.f, 0.f, 0.f}, e1[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        uint32_t a0, a1, a2, a3, b0, b1;
+        ldsm_x4(&dyw[lane & 15][k * 16 + (lane >> 4) * 8], a0, a1, a2, a3);
+        ldsm_x2(&sg3[lane & 7][k * 16 + ((lane >> 3) & 1) * 8], b0, b1);
+        if (k & 1)
+          mma_16816(e1, a0, a1, a2, a3, b0, b1);
+        else
+          mma_16816(e0, a0, a1, a2, a3, b0, b1);
+      }
+      float dz2[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) dz2[k] = e0[k] + e1[k];
+      // dG3ᵀ[i3, c] += Σ_t dy[t, i3] Z2[t, c]: B = Z2 (k = t, n = c) from the D fragment via movmatrix
+      {
+        const uint32_t b0 = movm_t(pack_bf16(z2[0], z2[1])), b1 = movm_t(pack_bf16(z2[2], z2[3]));
+#pragma unroll
+        for (int m = 0; m < 16; ++m) {
+          uint32_t a0, a1, a2, a3;
+          ldsm_x4_t(&dyw[(q >> 1) * 8 + (lane & 7)][m * 16 + (q & 1) * 8], a0, a1, a2, a3);
+          mma_16816(acc3[m], a0, a1, a2, a3, b0, b1);
+        }
+      }
+      // dZ2 as hi / lo bf16: A fragments of m16n8k8 (rows t, k = c) are the D layout itself
+      float hv[4];
+      uint32_t ah[2], al[2];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) hv[k] = __bfloat162float(__float2bfloat16_rn(dz2[k]));
+      ah[0] = pack_bf16(hv[0], hv[1]);
+      ah[1] = pack_bf16(hv[2], hv[3]);
+      al[0] = pack_bf16(dz2[0] - hv[0], dz2[1] - hv[1]);
+      al[1] = pack_bf16(dz2[2] - hv[2], dz2[3] - hv[3]);
+#pragma unroll
+      for (int n = 0; n < 4; ++n) {  // dZ1 += dZ2_h · Gm_hᵀ
+        uint32_t bh, bl;
+        ldsm_x1(gm(0, hl, n * 8 + (lane & 7)), bh);
+        ldsm_x1(gm(1, hl, n * 8 + (lane & 7)), bl);
+        mma_1688(dz1acc[n], ah[0], ah[1], bh);
+        mma_1688(dz1acc[n], al[0], al[1], bh);
+        mma_1688(dz1acc[n], ah[0], ah[1], bl);
+      }
+      {  // dG2_h += Z1ᵀ · dZ2_h: B = dZ2 (k = t, n = c), transposed D fragments
+        const uint32_t bh0 = movm_t(ah[0]), bh1 = movm_t(ah[1]), bl0 = movm_t(al[0]), bl1 = movm_t(al[1]);
+#pragma unroll
+        for (int m = 0; m < 2; ++m) {
+          mma_16816(g2acc[i][m], zt[0][m][0], zt[0][m][1], zt[0][m][2], zt[0][m][3], bh0, bh1);
+          mma_16816(g2acc[i][m], zt[1][m][0], zt[1][m][1], zt[1][m][2], zt[1][m][3], bh0, bh1);
+          mma_16816(g2acc[i][m], zt[0][m][0], zt[0][m][1], zt[0][m][2], zt[0][m][3], bl0, bl1);
+        }
+      }
+    }
+    // dZ1 partial of the tile: warp partials -> fixed-order sum
+#pragma unroll
+    for (int n = 0; n < 4; ++n) {
+      sdzs[warp][g][n * 8 + 2 * tq] = dz1acc[n][0];
+      sdzs[warp][g][n * 8 + 2 * tq + 1] = dz1acc[n][1];
+      sdzs[warp][g + 8][n * 8 + 2 * tq] = dz1acc[n][2];
+      sdzs[warp][g + 8][n * 8 + 2 * tq + 1] = dz1acc[n][3];
+    }
+    __syncthreads();
+    for (int i = tid; i < nt * K2; i += 256) {
+      const int r = i / K2, aj = i % K2;
+      float v = sdzs[0][r][aj];
+#pragma unroll
+      for (int w = 1; w < 8; ++w) v += sdzs[w][r][aj];
+      dz1p[(static_cast<int64_t>(hs) * T + t0 + r) * K2 + aj] = v;
+    }
+  }
+  cp_async_wait<0>();
+  // dG2 partial of token split ts for this warp's h blocks (D rows = aj, cols = c)
+  float* dst2 = g2part + static_cast<int64_t>(ts) * (static_cast<int64_t>(C) * H * J1 * C);
+#pragma unroll
+  for (int i = 0; i < WS_NHW; ++i) {
+    if (i >= nmine) break;
+    const int h = h0 + warp + 8 * i;
+#pragma unroll
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int aj = m * 16 + g + (k >> 1) * 8, c = 2 * tq + (k & 1);
+        const int a = aj / J1, j2 = aj % J1;
+        dst2[((static_cast<int64_t>(a) * H + h) * J1 + j2) * C + c] = g2acc[i][m][k];
+      }
+  }
+  // dG3 partial of this CTA: per-warp accumulators summed in warp order through shared memory
+  __syncthreads();
+  float* red = reinterpret_cast<float*>(ws_smem);  // [8][C][256] over the dy ring
+#pragma unroll
+  for (int m = 0; m < 16; ++m) {
+    const int col = m * 16 + g;
+    red[(warp * C + 2 * tq) * FB_COLS + col] = acc3[m][0];
+    red[(warp * C + 2 * tq + 1) * FB_COLS + col] = acc3[m][1];
+    red[(warp * C + 2 * tq) * FB_COLS + col + 8] = acc3[m][2];
+    red[(warp * C + 2 * tq + 1) * FB_COLS + col + 8] = acc3[m][3];
+  }
+  __syncthreads();
+  float* dst3 = g3part + (static_cast<int64_t>(ts) * gridDim.x + hs) * (C * FB_COLS);
+  for (int i = tid; i < C * FB_COLS; i += 256) {
+    float v = red[i];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) v += red[w * C * FB_COLS + i];
+    dst3[i] = v;
+  }
+}
+
 // Fixed-order reduction of up to three partial sets in one launch, plus (optionally) the B_ext
 // operand of the dX GEMM's adapter extension (k_build_bext).
 struct ReduceSet {
@@ -1848,6 +2120,159 @@ __global__ void __launch_bounds__(256) k_grad_reduce3(const ReduceArgs a) {
 // dz1 may hold HS partials ([HS][T][K2], summed here in fixed order); when dz1b is given, the CTAs
 // of column block 0 also write the [hi | lo | hi | 0] bf16 split of the summed rows (the dX GEMM's
 // extension operand, see k_split_rows).
+// x pass on the tensor cores (bf16 rows, J1 = 4):
+//   dG1[j1, a] = Σ_t Σ_J x[t, 4 j1 + J] dZ1[t, a, J] = Σ_k X'[j1, k] D'[k, a],   k = 4 t + J
+// is a GEMM with M = j1, N = a and a reduction over (token, J): the A fragment of an m16n8k16 MMA
+// needs, per lane, the bf16 pair x[t, 4 j1 + J .. + 1] — one 32-bit shared-memory load — and the
+// B fragment the pair dZ1[t, a, J .. J + 1] of the [t][a][J] staged dZ1 rows.  x is exact in bf16;
+// dZ1 enters as hi + lo bf16 (two MMAs), so the sums keep fp32-class accuracy.  A CTA owns 1024
+// columns (16 m-tiles, 2 per warp) of a token range, streamed through a 4-stage cp.async ring of
+// 16-token stages; dZ1 is staged per 64 tokens (HS partials summed in fixed order), and CTAs of
+// column block 0 also emit the [hi | lo | hi | 0] split rows the dX GEMM's extension reads.
+constexpr int DM_COLS = 1024, DM_LDX = DM_COLS + 32, DM_ST = 16, DM_NSTG = 4, DM_DZT = 64;
+
+template <int R1>
+__global__ void __launch_bounds__(256, 1) k_tt_dg1m(const __nv_bfloat16* __restrict__ x, int64_t T, int64_t K,
+                                                    const float* __restrict__ dz1, float* __restrict__ part, int S,
+                                                    int HS, __nv_bfloat16* __restrict__ dz1b, int64_t ldb,
+                                                    int raw_async) {
+  constexpr int J1 = 4, K2 = J1 * R1, NN = R1 / 8;
+  extern __shared__ __align__(16) uint8_t dm_smem[];
+  auto xs = reinterpret_cast<__nv_bfloat16(*)[DM_ST][DM_LDX]>(dm_smem);  // [NSTG]
+  constexpr size_t XS_BYTES = sizeof(__nv_bfloat16) * DM_NSTG * DM_ST * DM_LDX;
+  auto dzs = reinterpret_cast<__nv_bfloat16(*)[DM_DZT][R1][J1]>(dm_smem + XS_BYTES);  // [2 planes]
+  // raw fp32 dZ1 partials of the next 64-token blocks, prefetched by cp.async: [2][HS][DZT][K2]
+  float* raw = reinterpret_cast<float*>(dm_smem + XS_BYTES + sizeof(__nv_bfloat16) * 2 * DM_DZT * R1 * J1);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, tq = lane & 3;
+  const int64_t c0 = static_cast<int64_t>(blockIdx.x) * DM_COLS;
+  const int s = blockIdx.y;
+  const int64_t per = (T + S - 1) / S;
+  const int64_t t0 = s * per, t1 = t0 + per < T ? t0 + per : T;
+  const int64_t nst = t1 > t0 ? (t1 - t0 + DM_ST - 1) / DM_ST : 0;
+  constexpr int SPB = DM_DZT / DM_ST;  // stages per dZ1 block
+  float acc[2][NN][4];
+#pragma unroll
+  for (int m = 0; m < 2; ++m)
+#pragma unroll
+    for (int n = 0; n < NN; ++n)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[m][n][q] = 0.f;
+  auto issue_raw = [&](int64_t blk) {  // 16-byte pieces of HS x [DZT][K2] fp32 rows (tokens past t1 are zero)
+    const int64_t tb = t0 + blk * DM_DZT;
+    if (tb >= t1) return;
+    float* dst = raw + static_cast<size_t>(blk & 1) * HS * DM_DZT * K2;
+    for (int i = tid; i < HS * DM_DZT * (K2 / 4); i += 256) {
+      const int h = i / (DM_DZT * (K2 / 4)), r = (i / (K2 / 4)) % DM_DZT, q = i % (K2 / 4);
+      const bool ok = tb + r < t1;
+      cp_async16(dst + (static_cast<size_t>(h) * DM_DZT + r) * K2 + 4 * q,
+                 ok ? dz1 + (static_cast<int64_t>(h) * T + tb + r) * K2 + 4 * q : dz1, ok);
+    }
+  };
+  auto issue = [&](int64_t k) {
+    if (k < nst) {
+      const int slot = static_cast<int>(k % DM_NSTG);
+      for (int i = tid; i < DM_ST * (DM_COLS / 8); i += 256) {
+        const int r = i / (DM_COLS / 8), ch = i % (DM_COLS / 8);
+        const int64_t t = t0 + k * DM_ST + r, col = c0 + ch * 8;
+        const bool ok = t < t1 && col < K;
+        cp_async16(&xs[slot][r][ch * 8], ok ? x + t * K + col : x, ok);
+      }
+    }
+  };
+  if (raw_async) issue_raw(0);
+  for (int k = 0; k < DM_NSTG - 1; ++k) {
+    issue(k);
+    cp_async_commit();
+  }
+  for (int64_t k = 0; k < nst; ++k) {
+    const int slot = static_cast<int>(k % DM_NSTG);
+    cp_async_wait<DM_NSTG - 2>();
+    __syncthreads();  // stage k (and its dZ1 block) visible to all warps; stage k - 1's readers are done
+    if (k % SPB == 0) {  // dZ1 rows of the next 64 tokens: HS partials summed, hi / lo planes, [t][a][J]
+      const int64_t blk = k / SPB, tb = t0 + k * DM_ST;
+      const int nt = static_cast<int>(t1 - tb < DM_DZT ? t1 - tb : DM_DZT);
+      const float* rb = raw + static_cast<size_t>(blk & 1) * HS * DM_DZT * K2;
+      for (int i = tid; i < DM_DZT * K2; i += 256) {
+        const int r = i / K2, cc = i % K2;  // cc = a * J1 + J (the Z1 / dZ1 column order)
+        float v = 0.f;
+        if (r < nt) {
+          if (raw_async) {
+            v = rb[r * K2 + cc];
+            for (int h = 1; h < HS; ++h) v += rb[(static_cast<size_t>(h) * DM_DZT + r) * K2 + cc];
+          } else {
+            const int64_t off = (tb + r) * K2 + cc;
+            v = dz1[off];
+            for (int h = 1; h < HS; ++h) v += dz1[static_cast<int64_t>(h) * T * K2 + off];
+          }
+        }
+        const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+        dzs[0][r][cc / J1][cc % J1] = hi;
+        dzs[1][r][cc / J1][cc % J1] = __float2bfloat16_rn(v - __bfloat162float(hi));
+        if (dz1b != nullptr && blockIdx.x == 0 && r < nt) {  // [hi | lo | hi] split row for the dX GEMM
+          __nv_bfloat16* row = dz1b + (tb + r) * ldb;
+          row[cc] = hi;
+          row[K2 + cc] = __float2bfloat16_rn(v - __bfloat162float(hi));
+          row[2 * K2 + cc] = hi;
+          if (cc < ldb - 3 * K2) row[3 * K2 + cc] = __float2bfloat16_rn(0.f);
+        }
+      }
+      if (dz1b != nullptr && blockIdx.x == 0 && ldb - 3 * K2 > K2)
+        for (int i = tid; i < nt * static_cast<int>(ldb - 4 * K2); i += 256) {
+          const int r = i / static_cast<int>(ldb - 4 * K2), c = i % static_cast<int>(ldb - 4 * K2);
+          dz1b[(tb + r) * ldb + 4 * K2 + c] = __float2bfloat16_rn(0.f);
+        }
+      __syncthreads();
+    }
+    issue(k + DM_NSTG - 1);  // into the slot stage k - 1 used
+    if (raw_async && k % SPB == 1) issue_raw(k / SPB + 1);  // complete by the next block's first stage
+    cp_async_commit();
+    const int zr = static_cast<int>(k % SPB) * DM_ST;
+#pragma unroll
+    for (int ks = 0; ks < DM_ST / 4; ++ks) {  // 4 tokens x 4 J per k-step
+      const int tr = ks * 4 + (tq >> 1), J = 2 * (tq & 1);
+      uint32_t bh[NN][2], bl[NN][2];
+#pragma unroll
+      for (int n = 0; n < NN; ++n) {
+        bh[n][0] = *reinterpret_cast<const uint32_t*>(&dzs[0][zr + tr][n * 8 + g][J]);
+        bh[n][1] = *reinterpret_cast<const uint32_t*>(&dzs[0][zr + tr + 2][n * 8 + g][J]);
+        bl[n][0] = *reinterpret_cast<const uint32_t*>(&dzs[1][zr + tr][n * 8 + g][J]);
+        bl[n][1] = *reinterpret_cast<const uint32_t*>(&dzs[1][zr + tr + 2][n * 8 + g][J]);
+      }
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+        const int jl = (warp * 2 + m) * 16 + g;
+        const uint32_t a0 = *reinterpret_cast<const uint32_t*>(&xs[slot][tr][4 * jl + J]);
+        const uint32_t a1 = *reinterpret_cast<const uint32_t*>(&xs[slot][tr][4 * (jl + 8) + J]);
+        const uint32_t a2 = *reinterpret_cast<const uint32_t*>(&xs[slot][tr + 2][4 * jl + J]);
+        const uint32_t a3 = *reinterpret_cast<const uint32_t*>(&xs[slot][tr + 2][4 * (jl + 8) + J]);
+#pragma unroll
+        for (int n = 0; n < NN; ++n) {
+          mma_16816(acc[m][n], a0, a1, a2, a3, bh[n][0], bh[n][1]);
+          mma_16816(acc[m][n], a0, a1, a2, a3, bl[n][0], bl[n][1]);
+        }
+      }
+    }
+  }
+  cp_async_wait<0>();
+  float* dst = part + static_cast<int64_t>(s) * (K / J1) * R1;
+  const int64_t nj1 = K / J1;
+#pragma unroll
+  for (int m = 0; m < 2; ++m)
+#pragma unroll
+    for (int n = 0; n < NN; ++n) {
+      const int64_t j1 = c0 / J1 + (warp * 2 + m) * 16 + g;
+      const int a = n * 8 + 2 * tq;
+      if (j1 < nj1) {
+        dst[j1 * R1 + a] = acc[m][n][0];
+        dst[j1 * R1 + a + 1] = acc[m][n][1];
+      }
+      if (j1 + 8 < nj1) {
+        dst[(j1 + 8) * R1 + a] = acc[m][n][2];
+        dst[(j1 + 8) * R1 + a + 1] = acc[m][n][3];
+      }
+    }
+}
+
 // Ring-buffered x pass for bf16 rows (J1 = 4): each thread owns 8 columns and streams its own
 // 16-byte pieces of x through a 3-stage cp.async ring (8 token rows per stage), so the bytes in
 // flight per SM (up to 2 CTAs x 2 stages x 32 KB) no longer depend on registers.  The ring is
@@ -2246,6 +2671,15 @@ bool aq_mma_disabled() {
   return off;
 }
 
+// QA_DG1_MMA=0 selects the FFMA2 x pass (A/B comparisons).
+bool dg1_mma_disabled() {
+  static const bool off = [] {
+    const char* v = getenv("QA_DG1_MMA");
+    return v != nullptr && v[0] == '0';
+  }();
+  return off;
+}
+
 // QA_FUSED_BWD=0 selects the unfused dy pass / middle-core kernels (A/B comparisons).
 bool fused_bwd_disabled() {
   static const bool off = [] {
@@ -2596,12 +3030,21 @@ bool tt_bwd_fused_ok(int d, int J1, int R1, int C, int M) {
 }
 
 // h-range per CTA: the dG2 accumulators (HR x K2 x C fp32) and Gm_h stay <= 64 KB of shared memory
+bool ws_bwd_disabled() {
+  static const bool off = [] {
+    const char* v = getenv("QA_WS_BWD");
+    return v != nullptr && v[0] == '0';
+  }();
+  return off;
+}
+
 void tt_bwd_fused_plan(int64_t T, int H, int C, int* HR, int* HS, int* TS) {
   const int hr_max = C == 8 ? 16 : 8;
   *HS = (H + hr_max - 1) / hr_max;
   *HR = (H + *HS - 1) / *HS;
-  const int64_t tiles = (T + FB_TT - 1) / FB_TT;
-  const int per_sm = C == 8 ? 2 : 1;
+  const bool ws = C == 8 && !ws_bwd_disabled();  // k_tt_bwd_ws: 16-token tiles, one CTA per SM
+  const int64_t tiles = (T + (ws ? WS_TT : FB_TT) - 1) / (ws ? WS_TT : FB_TT);
+  const int per_sm = ws ? 1 : (C == 8 ? 2 : 1);
   int64_t ts = (static_cast<int64_t>(per_sm) * 148 + *HS - 1) / *HS;
   if (ts > tiles) ts = tiles;
   *TS = static_cast<int>(ts < 1 ? 1 : ts);
@@ -2617,7 +3060,11 @@ cudaError_t launch_tt_bwd_fused(const __nv_bfloat16* dy, int64_t ldy, int64_t T,
   LaunchScope scope(kTT, 4.0 * double(T) * N * C + 6.0 * double(T) * H * 4 * C * C, s);
   count_launches(1);
   const dim3 grid(static_cast<unsigned>(HS), static_cast<unsigned>(TS));
-  if (C == 8) {
+  if (C == 8 && !ws_bwd_disabled()) {
+    const size_t smem = WsLayout::bytes(HR);
+    cudaFuncSetAttribute(k_tt_bwd_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    k_tt_bwd_ws<<<grid, 256, smem, s>>>(dy, ldy, T, H, HR, Z1, G2, G3, dz1p, g3part, g2part);
+  } else if (C == 8) {
     const size_t smem = FbLayout<8>::bytes(HR);
     cudaFuncSetAttribute(k_tt_bwd_fused<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     k_tt_bwd_fused<8><<<grid, 256, smem, s>>>(dy, ldy, T, H, HR, Z1, G2, G3, dz1p, g3part, g2part);
@@ -2665,12 +3112,39 @@ int tt_dg1_splits(int64_t T, int64_t K, int J1) {
 }
 
 cudaError_t launch_tt_dg1(const void* x, int x_dtype, int64_t T, int64_t K, const float* dz1, int J1, int R1,
-                          float* part, int S, cudaStream_t s, int HS, __nv_bfloat16* dz1b, int64_t ldb) {
+                          float* part, int S, cudaStream_t s, int HS, __nv_bfloat16* dz1b, int64_t ldb,
+                          int* splits_used) {
+  if (splits_used != nullptr) *splits_used = S;
   if (T == 0) return cudaSuccess;
   LaunchScope scope(kTT, 2.0 * double(T) * K * R1, s);
   count_launches(1);
   const int E = J1 == 1 ? 4 : 8;
   const dim3 grid(static_cast<unsigned>((K + 256 * E - 1) / (256 * E)), static_cast<unsigned>(S));
+  if (x_dtype == QA_BF16 && J1 == 4 && K % 8 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0 && !dg1_mma_disabled()) {
+    const int64_t gx = (K + DM_COLS - 1) / DM_COLS;
+    const int64_t stages = (T + DM_ST - 1) / DM_ST;
+    int64_t Sm = (148 + gx - 1) / gx;
+    if (Sm > stages) Sm = stages;
+    if (Sm < 1) Sm = 1;
+    if (Sm <= S) {  // the caller's partial buffer holds S splits
+      if (splits_used != nullptr) *splits_used = static_cast<int>(Sm);
+      const dim3 gm(static_cast<unsigned>(gx), static_cast<unsigned>(Sm));
+      size_t smem = sizeof(__nv_bfloat16) * (DM_NSTG * DM_ST * DM_LDX + 2 * DM_DZT * R1 * J1);
+      const size_t raw_bytes = sizeof(float) * 2 * HS * DM_DZT * J1 * R1;
+      const int raw_async = smem + raw_bytes <= 220 * 1024 ? 1 : 0;
+      if (raw_async) smem += raw_bytes;
+      if (R1 == 8) {
+        cudaFuncSetAttribute(k_tt_dg1m<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        k_tt_dg1m<8><<<gm, 256, smem, s>>>(static_cast<const __nv_bfloat16*>(x), T, K, dz1, part, static_cast<int>(Sm),
+                                           HS, dz1b, ldb, raw_async);
+      } else {
+        cudaFuncSetAttribute(k_tt_dg1m<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        k_tt_dg1m<16><<<gm, 256, smem, s>>>(static_cast<const __nv_bfloat16*>(x), T, K, dz1, part, static_cast<int>(Sm),
+                                            HS, dz1b, ldb, raw_async);
+      }
+      return cudaGetLastError();
+    }
+  }
   if (x_dtype == QA_BF16 && J1 == 4 && K % 8 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0) {
     const size_t smem = sizeof(uint4) * DG_NST * DG_ROWS * 256;
     if (R1 == 8) {
