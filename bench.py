@@ -360,23 +360,32 @@ def main():
         if c.startswith("gemm"):
             kernels[c] = {"ms_per_step": cms / args.steps, "launches_per_step": cn / args.steps,
                           "achieved_tflops": cw / cn / avg_s / 1e12, "share_of_step": cms / ms_total}
-        else:
+        else:  # HBM-bound classes: work = algorithmic bytes
             kernels[c] = {"ms_per_step": cms / args.steps, "launches_per_step": cn / args.steps,
-                          "achieved_gbs" if c != "tt" else "achieved_tflops":
-                              (cw / cn / avg_s / 1e9) if c != "tt" else (cw / cn / avg_s / 1e12),
-                          "share_of_step": cms / ms_total}
+                          "achieved_gbs": cw / cn / avg_s / 1e9, "share_of_step": cms / ms_total}
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tfile):
         traffic = json.load(open(tfile)).get(dom)
+    # Denominator: the step is ~10 ms and the clocks sampled in the timed region sit at max (no power
+    # throttling), so the burst figures apply (B200_PROFILING.md: burst for a kernel timed in a short
+    # window, sustained for seconds-long loops under the power cap).
+    sustained = bool(clocks and clocks.get("sm_mhz") and clocks.get("sm_max_mhz") and
+                     clocks["sm_mhz"] < 0.9 * clocks["sm_max_mhz"])
+    i8file = os.path.join(ROOT, "profiles", "int8_peak.json")
+    i8 = json.load(open(i8file)) if os.path.exists(i8file) else {}
     if dom.startswith("gemm"):
         achieved = dwork / dn / (dms / dn / 1e3) / 1e12
         if dom == "gemm_bf16":
-            peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
-            note = f"bf16 dense, sustained, of {peak_src} (MEASURED_PEAKS.json)"
+            peak = peaks.get("bf16_tflops_sustained" if sustained else "bf16_tflops", peaks.get("bf16_tflops"))
+            note = (f"bf16 dense cuBLAS, {'sustained' if sustained else 'burst'}, of {peak_src} (MEASURED_PEAKS.json)")
+        elif i8:
+            peak = i8["int8_tops_sustained" if sustained else "int8_tops"]
+            note = (f"int8 dense cuBLASLt (torch._int_mm), {'sustained' if sustained else 'burst'}, measured on this "
+                    f"pool (profiles/int8_peak.json); NVIDIA spec 4.5 POPS")
         else:
             peak = 4500.0
-            note = "int8 dense: no measured int8 peak in MEASURED_PEAKS.json; NVIDIA B200 spec 4.5 POPS"
+            note = "int8 dense: no measured int8 peak; NVIDIA B200 spec 4.5 POPS"
         roofline = {"kernel": dom, "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                     "frac": achieved / peak, "traffic": traffic, "peak_source": note,
                     "work_per_launch": dwork / dn, "launch_ms": dms / dn}
@@ -385,6 +394,17 @@ def main():
         peak = peaks["hbm_gbs"]
         roofline = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                     "frac": achieved / peak, "traffic": traffic, "peak_source": f"HBM copy, of {peak_src}"}
+
+    # per-class fraction of its own roofline (same denominators as the headline roofline)
+    p_bf16 = peaks.get("bf16_tflops_sustained" if sustained else "bf16_tflops", peaks.get("bf16_tflops"))
+    p_i8 = i8.get("int8_tops_sustained" if sustained else "int8_tops", 4500.0) if i8 else 4500.0
+    for c, kd in kernels.items():
+        if c == "gemm_i8":
+            kd["frac_of_peak"] = kd["achieved_tflops"] / p_i8
+        elif c == "gemm_bf16":
+            kd["frac_of_peak"] = kd["achieved_tflops"] / p_bf16
+        else:
+            kd["frac_of_peak"] = kd["achieved_gbs"] / peaks["hbm_gbs"]
 
     # --- end-to-end through the C ABI with host buffers: pinned H2D of every step's inputs
     # (double-buffered on a copy stream, overlapping the previous step) + D2H of the gradients

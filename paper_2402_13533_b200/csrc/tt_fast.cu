@@ -930,8 +930,11 @@ QA_DEV uint32_t aqc_codes_row(const uint8_t* xrow, uint8_t* crow, int64_t nseg, 
   return sum;
 }
 
+#ifndef QA_AQC_MINB
+#define QA_AQC_MINB 3  // <= 85 registers: 3 CTAs (24 warps) per SM; measured best of {1, 3, 4}
+#endif
 template <int J1, int R1, bool CODES, bool FRAG_SMEM>
-__global__ void __launch_bounds__(AQC_WARPS * 32) k_aq_cta(const __nv_bfloat16* __restrict__ x, int64_t T, int64_t K,
+__global__ void __launch_bounds__(AQC_WARPS * 32, QA_AQC_MINB) k_aq_cta(const __nv_bfloat16* __restrict__ x, int64_t T, int64_t K,
                                                             uint8_t* __restrict__ codes, int64_t ldc,
                                                             float* __restrict__ sx, float* __restrict__ ox,
                                                             int32_t* __restrict__ rsx, const uint4* __restrict__ frag_g,
@@ -1170,7 +1173,7 @@ __global__ void __launch_bounds__(W * 32) k_aq_reg(const __nv_bfloat16* __restri
       if constexpr (J1 == 4) {
         uint4 fr[MT];
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt) fr[mt] = __ldg(frag + (st * MT + mt) * 32 + lane);
+        for (int mt = 0; mt < MT; ++mt) fr[mt] = frag[(st * MT + mt) * 32 + lane];
 #pragma unroll
         for (int J = 0; J < 4; ++J) {
           const uint32_t sel = (J & 1) ? 0x7632u : 0x5410u;
@@ -1184,7 +1187,7 @@ __global__ void __launch_bounds__(W * 32) k_aq_reg(const __nv_bfloat16* __restri
         for (int u = 0; u < 4; ++u)
 #pragma unroll
           for (int mt = 0; mt < MT; ++mt) {
-            const uint4 fr = __ldg(frag + ((st * 4 + u) * MT + mt) * 32 + lane);
+            const uint4 fr = frag[((st * 4 + u) * MT + mt) * 32 + lane];
             mma_16816(acc[0][mt], fr.x, fr.y, fr.z, fr.w, w[2 * u], w[2 * u + 1]);
           }
       }
@@ -1309,6 +1312,224 @@ __global__ void __launch_bounds__(W * 32) k_aq_reg(const __nv_bfloat16* __restri
       __syncthreads();
     }
   }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Ring-buffered act-quant + Z1 (production path for bf16 rows, K % 64 == 0): one CTA per SM streams
+// groups of TOKG token rows through a cp.async ring of shared-memory slots (~190 KB in flight per
+// SM: HBM stays busy without relying on register-resident loads or occupancy).  Per group:
+//   pass 1: Z1 partials on the tensor cores + exact bf16 min / max, warp w on the 64-element
+//           segments w, w + 8, ... (lane (g, c) of the m16n8k16 B fragment reads row g % TOKG;
+//           lanes g >= TOKG duplicate a row and are ignored);
+//   reduce: Z1 partials and min / max meet in shared memory (fixed warp order);
+//   pass 2: codes (aq_codes8b, bracketed fp32 + fp64 replay) from the same slot, each lane on a
+//           contiguous 16-element chunk (16 code bytes, one 16-byte store).
+constexpr int AQR_W = 16;
+
+template <int J1, int R1, int TOKG, bool CODES>
+__global__ void __launch_bounds__(AQR_W * 32, 1) k_aq_ring(const __nv_bfloat16* __restrict__ x, int64_t T, int64_t K,
+                                                           uint8_t* __restrict__ codes, int64_t ldc,
+                                                           float* __restrict__ sx, float* __restrict__ ox,
+                                                           int32_t* __restrict__ rsx, const uint4* __restrict__ frag,
+                                                           __nv_bfloat16* __restrict__ zb, int64_t ldzb,
+                                                           float* __restrict__ zf, int NS, int frag_smem) {
+  static_assert(TOKG == 8 || TOKG == 4 || TOKG == 2, "TOKG");
+  constexpr int K2 = J1 * R1, MT = R1 / 8, NJ = J1 == 4 ? 4 : 1, W = AQR_W, LPR = 32 / TOKG;
+  extern __shared__ __align__(16) uint8_t aqr_smem[];
+  __shared__ float s_z[W][8][K2];
+  __shared__ float s_lo[W][8], s_hi[W][8];
+  __shared__ int32_t s_sum[W][8];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, c = lane & 3;
+  const int64_t nseg = K / 64;
+  const int64_t rowb = K * 2 + 64;  // slot row stride in bytes (64-byte pad: conflict-free fragment reads)
+  const int64_t slotb = rowb * TOKG;
+  const int64_t ngroups = (T + TOKG - 1) / TOKG;
+  const int64_t mygroups = blockIdx.x < ngroups ? (ngroups - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  if (frag_smem) {  // G1 fragments next to the ring: the big ring leaves little L1 for __ldg
+    uint4* sf = reinterpret_cast<uint4*>(aqr_smem + NS * slotb);
+    const int64_t nf = nseg * (J1 == 4 ? 1 : 4) * MT * 32;
+    for (int64_t q = tid; q < nf; q += W * 32) sf[q] = frag[q];
+    frag = sf;  // visible after the first loop barrier
+  }
+  auto issue = [&](int64_t i) {
+    if (i < mygroups) {
+      const int64_t t0 = (blockIdx.x + i * gridDim.x) * TOKG;
+      uint8_t* slot = aqr_smem + (i % NS) * slotb;
+      const int chunks = static_cast<int>(K / 8);  // 16-byte pieces per row
+#pragma unroll
+      for (int r = 0; r < TOKG; ++r) {
+        const bool ok = t0 + r < T;
+        const __nv_bfloat16* src = x + (ok ? t0 + r : 0) * K;
+        uint8_t* dst = slot + r * rowb;
+        for (int ch = tid; ch < chunks; ch += W * 32) cp_async16(dst + ch * 16, src + ch * 8, ok);
+      }
+    }
+    cp_async_commit();
+  };
+  auto finish_sums = [&](int64_t i) {  // Σ codes of group i (needs the barrier after its pass 2)
+    const int64_t t0 = (blockIdx.x + i * gridDim.x) * TOKG;
+    if (CODES && tid < TOKG && t0 + tid < T) {
+      int32_t sum = 0;
+#pragma unroll
+      for (int w = 0; w < W; ++w) sum += s_sum[w][tid];
+      rsx[t0 + tid] = sum;
+    }
+  };
+  for (int i = 0; i < NS - 1; ++i) issue(i);
+  for (int64_t i = 0; i < mygroups; ++i) {
+    const int64_t t0 = (blockIdx.x + i * gridDim.x) * TOKG;
+    const int nr = static_cast<int>(T - t0 < TOKG ? T - t0 : TOKG);
+    const uint8_t* slot = aqr_smem + (i % NS) * slotb;
+    cp_async_wait_dyn(NS - 2);
+    __syncthreads();  // slot i landed for every thread; slot i - 1 and the shared partials are free
+    if (i > 0) finish_sums(i - 1);
+    issue(i + NS - 1);
+    // ---- pass 1
+    const uint8_t* myrow = slot + (g % TOKG) * rowb;
+    uint32_t off0, off1;
+    aqc_offsets<J1>(c, off0, off1);
+    float acc[NJ][MT][4];
+#pragma unroll
+    for (int J = 0; J < NJ; ++J)
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc[J][mt][k] = 0.f;
+    __nv_bfloat162 lo2 = __floats2bfloat162_rn(INFINITY, INFINITY), hi2 = __floats2bfloat162_rn(-INFINITY, -INFINITY);
+    for (int64_t st = warp; st < nseg; st += W) {
+      const uint4 p0 = *reinterpret_cast<const uint4*>(myrow + 128 * st + off0);
+      const uint4 p1 = *reinterpret_cast<const uint4*>(myrow + 128 * st + off1);
+      const uint32_t w[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+      if (CODES) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const __nv_bfloat162 b2 = *reinterpret_cast<const __nv_bfloat162*>(&w[k]);
+          lo2 = __hmin2(lo2, b2);
+          hi2 = __hmax2(hi2, b2);
+        }
+      }
+      if constexpr (J1 == 4) {
+        uint4 fr[MT];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) fr[mt] = frag[(st * MT + mt) * 32 + lane];
+#pragma unroll
+        for (int J = 0; J < 4; ++J) {
+          const uint32_t sel = (J & 1) ? 0x7632u : 0x5410u;
+          const uint32_t b0 = __byte_perm(w[J >> 1], w[2 + (J >> 1)], sel);
+          const uint32_t b1 = __byte_perm(w[4 + (J >> 1)], w[6 + (J >> 1)], sel);
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) mma_16816(acc[J][mt], fr[mt].x, fr[mt].y, fr[mt].z, fr[mt].w, b0, b1);
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) {
+            const uint4 fr = frag[((st * 4 + u) * MT + mt) * 32 + lane];
+            mma_16816(acc[0][mt], fr.x, fr.y, fr.z, fr.w, w[2 * u], w[2 * u + 1]);
+          }
+      }
+    }
+#pragma unroll
+    for (int J = 0; J < NJ; ++J)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if constexpr (MT == 1) {
+          s_z[warp][2 * c + h][g * J1 + J] = acc[J][0][h] + acc[J][0][2 + h];
+        } else {
+          s_z[warp][2 * c + h][g * J1 + J] = acc[J][0][h] + acc[J][1][h];
+          s_z[warp][2 * c + h][(g + 8) * J1 + J] = acc[J][0][2 + h] + acc[J][1][2 + h];
+        }
+      }
+    if (CODES) {
+      float lo = fminf(__low2float(lo2), __high2float(lo2)), hi = fmaxf(__low2float(hi2), __high2float(hi2));
+      lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, 1));
+      lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, 2));
+      hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, 1));
+      hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, 2));
+      if (c == 0) {
+        s_lo[warp][g] = lo;
+        s_hi[warp][g] = hi;
+      }
+    }
+    __syncthreads();
+    for (int k = tid; k < nr * K2; k += W * 32) {  // Z1: fixed-order sum of the warp partials
+      const int tk = k / K2, col = k % K2;
+      const int64_t row = t0 + tk;
+      float v = s_z[0][tk][col];
+#pragma unroll
+      for (int w2 = 1; w2 < W; ++w2) v += s_z[w2][tk][col];
+      if (zf != nullptr) zf[row * K2 + col] = v;
+      if (zb != nullptr) {
+        const __nv_bfloat16 hv = __float2bfloat16_rn(v);
+        zb[row * ldzb + col] = hv;
+        zb[row * ldzb + K2 + col] = __float2bfloat16_rn(v - __bfloat162float(hv));
+        zb[row * ldzb + 2 * K2 + col] = hv;
+      }
+    }
+    if (zb != nullptr && ldzb > 3 * K2) {
+      const int padw = static_cast<int>(ldzb - 3 * K2);
+      for (int k = tid; k < nr * padw; k += W * 32) zb[(t0 + k / padw) * ldzb + 3 * K2 + k % padw] = __float2bfloat16_rn(0.f);
+    }
+    if constexpr (CODES) {
+      // ---- pass 2: lane -> (token r, 16-element chunk j of each 512 / TOKG-element super-segment)
+      const int r = lane / LPR, j = lane % LPR;
+      float lo = s_lo[0][r], hi = s_hi[0][r];
+#pragma unroll
+      for (int w2 = 1; w2 < W; ++w2) {
+        lo = fminf(lo, s_lo[w2][r]);
+        hi = fmaxf(hi, s_hi[w2][r]);
+      }
+      const double lo64 = static_cast<double>(lo);
+      const double step64 = __ddiv_rn(__dsub_rn(static_cast<double>(hi), lo64), 255.0);
+      const bool flat = !(step64 > 0.0);
+      const float inv = flat ? 0.f : static_cast<float>(1.0 / step64);
+      const float nb = -lo * inv;
+      const bool sub = __any_sync(0xffffffffu, fabsf(nb) > 512.0f);
+      const float alo = sub ? 0.5f - kTieBand : nb + 0.5f - kTieBand, ahi = sub ? 0.5f + kTieBand : nb + 0.5f + kTieBand;
+      const unsigned long long inv2 = f2pack(inv, inv), nlo2 = f2pack(-lo, -lo), alo2 = f2pack(alo, alo),
+                               ahi2 = f2pack(ahi, ahi);
+      const bool valid = r < nr;
+      const uint8_t* xr = slot + r * rowb;
+      uint8_t* crow = codes + (t0 + (valid ? r : 0)) * ldc;
+      const int64_t nss = K / (512 / TOKG);  // super-segments per row
+      uint32_t sum = 0;
+      for (int64_t ss = warp; ss < nss; ss += W) {
+        const int64_t e0 = ss * (512 / TOKG) + j * 16;  // first element of the lane's chunk
+        const uint4 p0 = *reinterpret_cast<const uint4*>(xr + 2 * e0);
+        const uint4 p1 = *reinterpret_cast<const uint4*>(xr + 2 * e0 + 16);
+        uint32_t cw[4], dw[4];
+        if (sub) {
+          aq_codes8b<true>(p0, inv2, alo2, ahi2, nlo2, cw[0], cw[1], dw[0], dw[1]);
+          aq_codes8b<true>(p1, inv2, alo2, ahi2, nlo2, cw[2], cw[3], dw[2], dw[3]);
+        } else {
+          aq_codes8b<false>(p0, inv2, alo2, ahi2, nlo2, cw[0], cw[1], dw[0], dw[1]);
+          aq_codes8b<false>(p1, inv2, alo2, ahi2, nlo2, cw[2], cw[3], dw[2], dw[3]);
+        }
+        if (flat) cw[0] = cw[1] = cw[2] = cw[3] = dw[0] = dw[1] = dw[2] = dw[3] = 0u;
+        if ((dw[0] | dw[1] | dw[2] | dw[3]) != 0u) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (dw[k] != 0u) cw[k] = aq_replay_word(k < 2 ? p0 : p1, (k & 1) * 4, cw[k], dw[k], lo64, step64);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) sum = __dp4a(cw[k], 0x01010101u, sum);
+        if (valid) *reinterpret_cast<uint4*>(crow + e0) = make_uint4(cw[0], cw[1], cw[2], cw[3]);
+      }
+#pragma unroll
+      for (int o = 1; o < LPR; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      if (j == 0) s_sum[warp][r] = static_cast<int32_t>(sum);
+      if (warp == 0 && valid && j == 0) {
+        sx[t0 + r] = flat ? 0.0f : __double2float_rn(step64);
+        ox[t0 + r] = lo;
+      }
+      if (valid && ldc > K)
+        for (int64_t kk = K + warp * LPR + j; kk < ldc; kk += W * LPR) crow[kk] = 0;  // zero padding [K, ldc)
+    }
+  }
+  cp_async_wait_dyn(0);
+  __syncthreads();
+  if (mygroups > 0) finish_sums(mygroups - 1);
 }
 
 // V[n, c] (bf16, zero padded to ldv): contraction of cores 2..d with the left rank open.
@@ -2689,6 +2910,16 @@ bool fused_bwd_disabled() {
   return off;
 }
 
+// QA_AQ_RING=1 selects the ring-buffered act-quant kernel (measured slower than k_aq_cta on B200:
+// one 16-warp CTA per SM is issue-bound on the codes pass; kept for A/B comparisons).
+bool aq_ring_disabled() {
+  static const bool off = [] {
+    const char* v = getenv("QA_AQ_RING");
+    return !(v != nullptr && v[0] == '1');
+  }();
+  return off;
+}
+
 // QA_AQ_REG=1 selects the register-resident k_aq_reg kernel (measured slower than k_aq_cta on
 // B200: 2 CTAs / SM at 120 registers; kept for A/B comparisons).
 bool aq_reg_disabled() {
@@ -2761,6 +2992,51 @@ cudaError_t launch_actquant_z1(const void* x, int x_dtype, int64_t T, int64_t K,
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     const int64_t ngroups = (T + 7) / 8;
     const int64_t nseg = K / 64;
+    if (!aq_ring_disabled()) {  // ring-buffered rows: pick the widest group whose slot allows >= 3 slots
+      const size_t budget = 180 * 1024;  // dynamic ring; ~40 KB static partials (16 warps)
+      const size_t rowb = static_cast<size_t>(K) * 2 + 64;
+      int tokg = 0;
+      for (int tg : {8, 4, 2})
+        if (3 * rowb * tg <= budget) {
+          tokg = tg;
+          break;
+        }
+      if (tokg > 0 && K % (512 / tokg) == 0) {
+        const size_t slotb = rowb * tokg;
+        const size_t fbytes = static_cast<size_t>(nfrag) * MT * 32 * 16;
+        const int fsm = fbytes <= 64 * 1024 && 3 * slotb + fbytes <= 180 * 1024 ? 1 : 0;
+        int ns = static_cast<int>((180 * 1024 - (fsm ? fbytes : 0)) / slotb);
+        if (ns > 6) ns = 6;
+        const size_t smem = slotb * ns + (fsm ? fbytes : 0);
+        const int64_t groups = (T + tokg - 1) / tokg;
+        const unsigned grid = static_cast<unsigned>(groups < nsm ? groups : nsm);
+#define QA_AQG(JJ, RR, TG)                                                                                     \
+  {                                                                                                            \
+    auto kern = want_codes ? k_aq_ring<JJ, RR, TG, true> : k_aq_ring<JJ, RR, TG, false>;                       \
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));          \
+    kern<<<grid, AQR_W * 32, smem, s>>>(static_cast<const __nv_bfloat16*>(x), T, K, codes, ldc, sx, ox, rsx, fr, \
+                                        zb, ldzb, zf, ns, fsm);                                                \
+  }
+#define QA_AQG_T(JJ, RR) \
+  if (tokg == 8)         \
+    QA_AQG(JJ, RR, 8)    \
+  else if (tokg == 4)    \
+    QA_AQG(JJ, RR, 4)    \
+  else                   \
+    QA_AQG(JJ, RR, 2)
+        if (J1 == 1 && R1 == 8)
+          QA_AQG_T(1, 8)
+        else if (J1 == 1)
+          QA_AQG_T(1, 16)
+        else if (R1 == 8)
+          QA_AQG_T(4, 8)
+        else
+          QA_AQG_T(4, 16)
+#undef QA_AQG_T
+#undef QA_AQG
+        return cudaGetLastError();
+      }
+    }
     if (nseg <= 176 && !aq_reg_disabled()) {  // register-resident rows
 #define QA_AQR(JJ, RR, WW, SS)                                                                                \
   {                                                                                                           \
@@ -3057,7 +3333,8 @@ cudaError_t launch_tt_bwd_fused(const __nv_bfloat16* dy, int64_t ldy, int64_t T,
   int HR, HS, TS;
   tt_bwd_fused_plan(T, H, C, &HR, &HS, &TS);
   const int64_t N = static_cast<int64_t>(H) * FB_COLS;
-  LaunchScope scope(kTT, 4.0 * double(T) * N * C + 6.0 * double(T) * H * 4 * C * C, s);
+  // algorithmic HBM bytes: dy (bf16) + Z1 in, the dZ1 partials out (the kTT class counts bytes)
+  LaunchScope scope(kTT, 2.0 * double(T) * N + 4.0 * double(T) * 4 * C * (1 + HS), s);
   count_launches(1);
   const dim3 grid(static_cast<unsigned>(HS), static_cast<unsigned>(TS));
   if (C == 8 && !ws_bwd_disabled()) {
@@ -3116,7 +3393,9 @@ cudaError_t launch_tt_dg1(const void* x, int x_dtype, int64_t T, int64_t K, cons
                           int* splits_used) {
   if (splits_used != nullptr) *splits_used = S;
   if (T == 0) return cudaSuccess;
-  LaunchScope scope(kTT, 2.0 * double(T) * K * R1, s);
+  // algorithmic HBM bytes: x in, the dZ1 partials in, the split dZ1 rows out
+  LaunchScope scope(kTT, double(T) * K * (x_dtype == QA_F32 ? 4 : 2) + 4.0 * double(T) * J1 * R1 * HS +
+                             (dz1b ? 2.0 * double(T) * ldb : 0.0), s);
   count_launches(1);
   const int E = J1 == 1 ? 4 : 8;
   const dim3 grid(static_cast<unsigned>((K + 256 * E - 1) / (256 * E)), static_cast<unsigned>(S));
