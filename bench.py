@@ -35,6 +35,10 @@ LINEARS_7B = [  # (name, fan_out, fan_in, input) in forward order (transformer.p
     ("wd", 4096, 11008, "act"),
 ]
 BACKWARD_ORDER = ["wd", "wu", "wg", "wo", "wq", "wk", "wv"]  # transformer.py:919-944
+# members that read the same input run as one shared-input group (qa_group_forward / _backward):
+# wq / wk / wv on norm1 and wu / wg on norm2 (transformer.py:862-874)
+GROUPS_FWD = [("wq", "wk", "wv"), ("wo",), ("wu", "wg"), ("wd",)]
+GROUPS_BWD = [("wd",), ("wu", "wg"), ("wo",), ("wq", "wk", "wv")]
 INPUT_DIMS = {"attn": 4096, "ctx": 4096, "ffn": 4096, "act": 11008}
 
 CONFIGS = {
@@ -52,6 +56,7 @@ def parse():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-group", action="store_true", help="run every linear on its own (A/B of the shared x pass)")
     return ap.parse_args()
 
 
@@ -66,7 +71,8 @@ def workload_config(cfg_name, world):
     desc = {
         "workload": (f"llama2-7b linear set q/k/v/o 4096x4096, gate/up 11008x4096, down 4096x11008; int{c['bits']} "
                      f"per-row weights; TT adapter r={c['rank']} m=(1,N/256,256) n=(K/4,4,1); "
-                     f"{tokens} bf16 tokens/GPU; fwd + bwd-with-recompute (+ NCCL grad all-reduce)"),
+                     f"{tokens} bf16 tokens/GPU; fwd + bwd-with-recompute (+ NCCL grad all-reduce); q/k/v and "
+                     f"up/gate as shared-input groups (one x pass per direction, transformer.py:862-874)"),
         "baseline_config": int(cfg_name),
         "tokens_per_gpu": tokens,
         "bits": c["bits"],
@@ -263,6 +269,16 @@ def main():
         mats[name] = dict(q=q, spec=spec, cores=cores, wc=wc, ttc=ttc, n=n, k=k, kind=kind, saved=saved,
                           nsaved=nsaved)
         grad_numel += spec.param_count()
+    # shared-input groups: ctypes argument arrays built once
+    groups = {}
+    for gnames in set(GROUPS_FWD) | set(GROUPS_BWD):
+        if len(gnames) < 2:
+            continue
+        n = len(gnames)
+        W = (ctypes.POINTER(_lib.QWeight) * n)(*[ctypes.pointer(mats[g]["wc"]) for g in gnames])
+        Tt = (ctypes.POINTER(_lib.TT) * n)(*[ctypes.pointer(mats[g]["ttc"]) for g in gnames])
+        ws_bytes = max(ws_bytes, lib.qa_group_workspace_bytes(n, W, Tt, T))
+        groups[gnames] = dict(n=n, W=W, T=Tt)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     flat_grad = torch.zeros(grad_numel, dtype=torch.float32, device=dev)
     off = 0
@@ -288,7 +304,19 @@ def main():
     dxs = {nm: torch.empty((T, k), dtype=torch.bfloat16, device=dev) for nm, _, k, _ in LINEARS_7B}
     BF16 = _lib.QA_BF16
 
+    for gnames, gd in groups.items():  # saved-state, gradient and dy/dx pointer arrays
+        n = gd["n"]
+        gd["S"] = (ctypes.c_void_p * n)(*[mats[g]["saved"].data_ptr() for g in gnames])
+        gd["SB"] = (ctypes.c_size_t * n)(*[mats[g]["nsaved"] for g in gnames])
+        gd["DC"] = (ctypes.POINTER(ctypes.c_void_p) * n)(
+            *[ctypes.cast(mats[g]["gptr"], ctypes.POINTER(ctypes.c_void_p)) for g in gnames])
+        gd["Y"] = (ctypes.c_void_p * n)(*[ys[g].data_ptr() for g in gnames])
+        gd["DX"] = (ctypes.c_void_p * n)(*[dxs[g].data_ptr() for g in gnames])
+        gd["kind"] = mats[gnames[0]]["kind"]
+
     def step(xs, dys):
+        if not args.no_group:
+            return step_grouped(xs, dys)
         for name, _, _, kind in LINEARS_7B:
             m = mats[name]
             st = lib.qa_linear_forward_save(ctypes.byref(m["wc"]), ctypes.byref(m["ttc"]), xs[kind].data_ptr(), BF16,
@@ -305,6 +333,39 @@ def main():
                                               m["saved"].data_ptr(), m["nsaved"], ws.data_ptr(), ws_bytes, sptr)
             if st:
                 _lib.check(st, f"backward {name}")
+        if world > 1:
+            dist.all_reduce(flat_grad, op=dist.ReduceOp.SUM)
+            flat_grad.div_(world)
+
+    def step_grouped(xs, dys):
+        for gnames in GROUPS_FWD:
+            if len(gnames) == 1:
+                m = mats[gnames[0]]
+                st = lib.qa_linear_forward_save(ctypes.byref(m["wc"]), ctypes.byref(m["ttc"]), xs[m["kind"]].data_ptr(),
+                                                BF16, T, ys[gnames[0]].data_ptr(), m["saved"].data_ptr(), m["nsaved"],
+                                                ws.data_ptr(), ws_bytes, sptr)
+            else:
+                gd = groups[gnames]
+                st = lib.qa_group_forward(gd["n"], gd["W"], gd["T"], xs[gd["kind"]].data_ptr(), BF16, T, gd["Y"],
+                                          gd["S"], gd["SB"], ws.data_ptr(), ws_bytes, sptr)
+            if st:
+                _lib.check(st, f"forward {gnames}")
+        for gnames in GROUPS_BWD:
+            if len(gnames) == 1:
+                name = gnames[0]
+                m = mats[name]
+                st = lib.qa_linear_backward_saved(ctypes.byref(m["wc"]), ctypes.byref(m["ttc"]),
+                                                  xs[m["kind"]].data_ptr(), BF16, dys[name].data_ptr(), BF16, T,
+                                                  dxs[name].data_ptr(),
+                                                  ctypes.cast(m["gptr"], ctypes.POINTER(ctypes.c_void_p)), 0,
+                                                  m["saved"].data_ptr(), m["nsaved"], ws.data_ptr(), ws_bytes, sptr)
+            else:
+                gd = groups[gnames]
+                DY = (ctypes.c_void_p * gd["n"])(*[dys[g].data_ptr() for g in gnames])
+                st = lib.qa_group_backward(gd["n"], gd["W"], gd["T"], xs[gd["kind"]].data_ptr(), BF16, DY, BF16, T,
+                                           gd["DX"], gd["DC"], 0, gd["S"], gd["SB"], ws.data_ptr(), ws_bytes, sptr)
+            if st:
+                _lib.check(st, f"backward {gnames}")
         if world > 1:
             dist.all_reduce(flat_grad, op=dist.ReduceOp.SUM)
             flat_grad.div_(world)

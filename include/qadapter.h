@@ -141,6 +141,25 @@ QA_API int qa_linear_backward_saved(const qa_qweight* w, const qa_tt* tt, const 
                                     size_t saved_bytes, void* workspace, size_t workspace_bytes,
                                     void* stream);
 
+/* Shared-input groups (n = 1..3 members with the same fan_in): a decoder layer applies q / k / v to
+ * the same norm1 and up / gate to the same norm2 (_layer_forward, transformer.py:862-874) and sums
+ * their input gradients (_layer_backward, transformer.py:919-944).  The group entry points give
+ * each member's outputs exactly as its own qa_linear_forward_save / qa_linear_backward_saved would
+ * (per-member y, dx and core gradients), but read x once per direction when every member is a
+ * pinned-mode tensor-train adapter (first core input-only with 4-wide last input mode, rank 8);
+ * otherwise they run the members one after another.  saved[i] / saved_bytes[i] as in
+ * qa_linear_forward_save (entries or the arrays themselves may be NULL). */
+QA_API size_t qa_group_workspace_bytes(int n, const qa_qweight* const* w, const qa_tt* const* tt, int64_t tokens);
+QA_API int qa_group_forward(int n, const qa_qweight* const* w, const qa_tt* const* tt, const void* x, int x_dtype,
+                            int64_t tokens, void* const* y, void* const* saved, const size_t* saved_bytes,
+                            void* workspace, size_t workspace_bytes, void* stream);
+/* dcores[i][k]: member i's core-k gradient (all three needed for the shared pass); dx[i] member i's
+ * input gradient (the caller sums them, as _layer_backward does). */
+QA_API int qa_group_backward(int n, const qa_qweight* const* w, const qa_tt* const* tt, const void* x, int x_dtype,
+                             const void* const* dy, int dy_dtype, int64_t tokens, void* const* dx,
+                             float* const* const* dcores, int accumulate, const void* const* saved,
+                             const size_t* saved_bytes, void* workspace, size_t workspace_bytes, void* stream);
+
 /* Workspace for qa_merge / qa_tt_materialize. */
 QA_API size_t qa_merge_workspace_bytes(const qa_tt* tt);
 

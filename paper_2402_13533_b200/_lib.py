@@ -34,6 +34,9 @@ EXPORTS = (
     "qa_linear_saved_bytes",
     "qa_linear_forward_save",
     "qa_linear_backward_saved",
+    "qa_group_workspace_bytes",
+    "qa_group_forward",
+    "qa_group_backward",
     "qa_merge_workspace_bytes",
     "qa_merge",
     "qa_tt_materialize",
@@ -93,6 +96,15 @@ def _declare(lib):
     lib.qa_linear_forward_save.argtypes = [PW, PT, P, I32, I64, P, P, SZ, P, SZ, P]
     lib.qa_linear_backward_saved.restype = I32
     lib.qa_linear_backward_saved.argtypes = [PW, PT, P, I32, P, I32, I64, P, ctypes.POINTER(P), I32, P, SZ, P, SZ, P]
+    PP = ctypes.POINTER(P)
+    lib.qa_group_workspace_bytes.restype = SZ
+    lib.qa_group_workspace_bytes.argtypes = [I32, ctypes.POINTER(PW), ctypes.POINTER(PT), I64]
+    lib.qa_group_forward.restype = I32
+    lib.qa_group_forward.argtypes = [I32, ctypes.POINTER(PW), ctypes.POINTER(PT), P, I32, I64, PP, PP,
+                                     ctypes.POINTER(SZ), P, SZ, P]
+    lib.qa_group_backward.restype = I32
+    lib.qa_group_backward.argtypes = [I32, ctypes.POINTER(PW), ctypes.POINTER(PT), P, I32, PP, I32, I64, PP,
+                                      ctypes.POINTER(PP), I32, PP, ctypes.POINTER(SZ), P, SZ, P]
     lib.qa_merge_workspace_bytes.restype = SZ
     lib.qa_merge_workspace_bytes.argtypes = [PT]
     lib.qa_merge.restype = I32

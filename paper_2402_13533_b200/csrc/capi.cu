@@ -686,6 +686,242 @@ int qa_linear_backward_saved(const qa_qweight* w, const qa_tt* tt, const void* x
                               stream);
 }
 
+// ------------------------------------------------------------------ shared-input groups
+// A decoder layer applies q / k / v to the same norm1 and up / gate to the same norm2
+// (transformer.py:862-874) and sums their input gradients (:919-944).  A group runs those members
+// with one x pass in each direction when every member is a pinned-mode adapter (J1 = 4, r = 8);
+// otherwise it is the members' single-linear calls in sequence.
+}  // extern "C"
+
+namespace qa {
+namespace {
+constexpr int kMaxGroup = 3;
+
+struct GroupPlan {
+  int n = 0;
+  TTDims dd[kMaxGroup];
+  LinearPlan P[kMaxGroup];
+  float* frag = nullptr;
+  size_t bytes = 0;
+  bool fast = false;
+};
+
+int plan_group(int n, const qa_qweight* const* w, const qa_tt* const* tt, int64_t T, void* ws, bool f32_path,
+               const void* x, GroupPlan* G) {
+  if (n < 1 || n > kMaxGroup || w == nullptr || tt == nullptr) {
+    set_error("group of %d members (1..%d supported)", n, kMaxGroup);
+    return QA_ERR_ARG;
+  }
+  G->n = n;
+  size_t off = 0;
+  bool fast = n >= 2;
+  for (int i = 0; i < n; ++i) {
+    QA_TRY(check_weight(w[i]));
+    if (tt[i] == nullptr) {
+      set_error("group member %d has no adapter", i);
+      return QA_ERR_ARG;
+    }
+    QA_TRY(check_tt(tt[i], w[i], &G->dd[i]));
+    if (w[i]->cols != w[0]->cols) {
+      set_error("group members must share fan_in (%lld vs %lld)", (long long)w[i]->cols, (long long)w[0]->cols);
+      return QA_ERR_ARG;
+    }
+    plan_linear(w[i], &G->dd[i], T, ws != nullptr ? static_cast<char*>(ws) + off : nullptr, &G->P[i], f32_path);
+    off += round_up(static_cast<int64_t>(G->P[i].bytes), 256);
+    const LinearPlan& P = G->P[i];
+    fast = fast && P.fast && P.fused && P.fd == 3 && P.J1 == 4 && P.R1 == 8 && P.HS == G->P[0].HS;
+  }
+  G->fast = fast && group_x_pass_ok(4, 8, w[0]->cols, n, x);
+  G->frag = ws != nullptr ? reinterpret_cast<float*>(static_cast<char*>(ws) + off) : nullptr;
+  off += sizeof(float) * kMaxGroup * g1i_floats(w[0]->cols, 4, 8) + 256;
+  G->bytes = off;
+  return QA_OK;
+}
+}  // namespace
+}  // namespace qa
+
+extern "C" {
+
+size_t qa_group_workspace_bytes(int n, const qa_qweight* const* w, const qa_tt* const* tt, int64_t tokens) {
+  GroupPlan G;
+  static const uint64_t aligned_probe = 0;
+  if (plan_group(n, w, tt, tokens, nullptr, true, &aligned_probe, &G) != QA_OK) return 0;
+  return G.bytes;
+}
+
+int qa_group_forward(int n, const qa_qweight* const* w, const qa_tt* const* tt, const void* x, int x_dtype,
+                     int64_t tokens, void* const* y, void* const* saved, const size_t* saved_bytes, void* workspace,
+                     size_t workspace_bytes, void* stream) {
+  GroupPlan G;
+  QA_TRY(plan_group(n, w, tt, tokens, nullptr, false, x, &G));
+  if (tokens == 0) return QA_OK;
+  if (x == nullptr || y == nullptr || tokens < 0) {
+    set_error("qa_group_forward: bad argument");
+    return QA_ERR_ARG;
+  }
+  if (workspace == nullptr || workspace_bytes < G.bytes) {
+    set_error("workspace too small: need %zu bytes", G.bytes);
+    return QA_ERR_WORKSPACE;
+  }
+  QA_TRY(plan_group(n, w, tt, tokens, workspace, false, x, &G));
+  const bool fast = G.fast && x_dtype == QA_BF16;
+  if (!fast) {  // the members' single-linear forwards
+    for (int i = 0; i < n; ++i) {
+      const size_t need = G.P[i].fast ? sizeof(float) * static_cast<size_t>(tokens) * G.P[i].K2 : 0;
+      float* sv = (saved != nullptr && saved[i] != nullptr && need > 0 && saved_bytes != nullptr &&
+                   saved_bytes[i] >= need) ? static_cast<float*>(saved[i]) : nullptr;
+      QA_TRY(linear_forward_impl(w[i], tt[i], x, x_dtype, tokens, y[i], nullptr, nullptr, nullptr, sv,
+                                 reinterpret_cast<char*>(G.P[i].xcodes) - 0, G.P[i].bytes, stream));
+    }
+    return QA_OK;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t T = tokens, K = w[0]->cols;
+  LinearPlan& P0 = G.P[0];
+  const float* G1[kMaxGroup];
+  __nv_bfloat16* zb[kMaxGroup];
+  float* zf[kMaxGroup];
+  for (int i = 0; i < n; ++i) {
+    G1[i] = tt[i]->cores[0];
+    zb[i] = G.P[i].zb;
+    const size_t need = sizeof(float) * static_cast<size_t>(T) * G.P[i].K2;
+    zf[i] = (saved != nullptr && saved[i] != nullptr && saved_bytes != nullptr && saved_bytes[i] >= need)
+                ? static_cast<float*>(saved[i]) : nullptr;
+  }
+  // one pass over x: shared codes + each member's Z1
+  QA_TRY_CUDA(launch_actquant_z1_group(x, T, K, true, P0.xcodes, P0.Kp, P0.sx, P0.ox, P0.rsx, G1, n, zb, P0.K2p, zf,
+                                       G.frag, s),
+              "group act quantize + TT stage 1");
+  for (int i = 0; i < n; ++i) {
+    LinearPlan& P = G.P[i];
+    QA_TRY_CUDA(launch_build_v(P.fd, P.R1, P.H, P.J1, P.C, P.M, tt[i]->cores[1], tt[i]->cores[2], P.v, P.N, P.K2p, s),
+                "build V");
+    int st = QA_OK;
+    const uint8_t* wop = weight_operand(w[i], P, s, &st);
+    QA_TRY(st);
+    GemmEpilogue e;
+    e.row_scale = P0.sx;
+    e.row_offset = P0.ox;
+    e.row_sum = P0.rsx;
+    e.col_scale = w[i]->scale;
+    e.col_offset = w[i]->offset;
+    e.col_sum = w[i]->rowsum;
+    e.zp_row = 128;
+    e.zp_col = w[i]->bits == 8 ? 128 : 8;
+    e.k_real = static_cast<int>(K);
+    e.out_bf16 = static_cast<__nv_bfloat16*>(y[i]);
+    e.ld_out = P.N;
+    GemmExt ext;
+    ext.A2 = P.zb;
+    ext.lda2 = P.K2p;
+    ext.B2 = P.v;
+    ext.ldb2 = P.K2p;
+    ext.K2 = P.K2p;
+    QA_TRY(gemm_tc(0, P0.xcodes, P0.Kp, wop, P.Kp, T, P.N, P0.Kp, e, s, &ext));
+  }
+  return QA_OK;
+}
+
+int qa_group_backward(int n, const qa_qweight* const* w, const qa_tt* const* tt, const void* x, int x_dtype,
+                      const void* const* dy, int dy_dtype, int64_t tokens, void* const* dx,
+                      float* const* const* dcores, int accumulate, const void* const* saved, const size_t* saved_bytes,
+                      void* workspace, size_t workspace_bytes, void* stream) {
+  GroupPlan G;
+  QA_TRY(plan_group(n, w, tt, tokens, nullptr, dy_dtype == QA_F32, x, &G));
+  if (dy == nullptr || x == nullptr || tokens < 0) {
+    set_error("qa_group_backward: bad argument");
+    return QA_ERR_ARG;
+  }
+  if (workspace == nullptr || workspace_bytes < G.bytes) {
+    set_error("workspace too small: need %zu bytes", G.bytes);
+    return QA_ERR_WORKSPACE;
+  }
+  QA_TRY(plan_group(n, w, tt, tokens, workspace, dy_dtype == QA_F32, x, &G));
+  bool fast = G.fast && x_dtype == QA_BF16 && dy_dtype == QA_BF16 && tokens > 0 && dcores != nullptr;
+  for (int i = 0; fast && i < n; ++i)
+    fast = dy[i] != nullptr && reinterpret_cast<uintptr_t>(dy[i]) % 16 == 0 && G.P[i].Np == G.P[i].N &&
+           dcores[i] != nullptr && dcores[i][0] != nullptr && dcores[i][1] != nullptr && dcores[i][2] != nullptr;
+  if (!fast) {  // the members' single-linear backwards
+    for (int i = 0; i < n; ++i) {
+      const size_t need = G.P[i].fast ? sizeof(float) * static_cast<size_t>(tokens) * G.P[i].K2 : 0;
+      const float* sv = (saved != nullptr && saved[i] != nullptr && need > 0 && saved_bytes != nullptr &&
+                         saved_bytes[i] >= need) ? static_cast<const float*>(saved[i]) : nullptr;
+      QA_TRY(linear_backward_impl(w[i], tt[i], x, x_dtype, dy[i], dy_dtype, tokens, dx != nullptr ? dx[i] : nullptr,
+                                  nullptr, dcores != nullptr ? dcores[i] : nullptr, accumulate, sv,
+                                  reinterpret_cast<char*>(G.P[i].xcodes), G.P[i].bytes, stream));
+    }
+    return QA_OK;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t T = tokens, K = w[0]->cols;
+  // Z1 of each member: handed over by the recompute-forward, else recomputed in one shared x pass
+  const float* zfs[kMaxGroup];
+  bool all_saved = true;
+  for (int i = 0; i < n; ++i) {
+    const size_t need = sizeof(float) * static_cast<size_t>(T) * G.P[i].K2;
+    zfs[i] = (saved != nullptr && saved[i] != nullptr && saved_bytes != nullptr && saved_bytes[i] >= need)
+                 ? static_cast<const float*>(saved[i]) : nullptr;
+    all_saved = all_saved && zfs[i] != nullptr;
+  }
+  if (!all_saved) {
+    const float* G1[kMaxGroup];
+    float* zf[kMaxGroup];
+    for (int i = 0; i < n; ++i) {
+      G1[i] = tt[i]->cores[0];
+      zf[i] = G.P[i].zf;
+      zfs[i] = G.P[i].zf;
+    }
+    QA_TRY_CUDA(launch_actquant_z1_group(x, T, K, false, nullptr, 0, nullptr, nullptr, nullptr, G1, n, nullptr, 0, zf,
+                                         G.frag, s),
+                "group TT stage 1 recompute");
+  }
+  // one pass over each dy
+  for (int i = 0; i < n; ++i) {
+    LinearPlan& P = G.P[i];
+    QA_TRY_CUDA(launch_tt_bwd_fused(static_cast<const __nv_bfloat16*>(dy[i]), P.N, T, P.H, P.C, zfs[i], tt[i]->cores[1],
+                                    tt[i]->cores[2], P.dz1p, P.g3p, P.g2p, s),
+                "TT fused dy pass");
+  }
+  // one pass over x for every member's dG1 (+ the dZ1 split rows of the dX GEMMs)
+  const float* dz1[kMaxGroup];
+  float* g1p[kMaxGroup];
+  __nv_bfloat16* dz1b[kMaxGroup];
+  for (int i = 0; i < n; ++i) {
+    dz1[i] = G.P[i].dz1p;
+    g1p[i] = G.P[i].g1p;
+    dz1b[i] = dx != nullptr ? G.P[i].dz1b : nullptr;
+  }
+  int s_dg1 = G.P[0].S_dg1;
+  QA_TRY_CUDA(launch_tt_dg1_group(x, T, K, dz1, g1p, G.P[0].S_dg1, G.P[0].HS, dz1b, G.P[0].K2p, n, &s_dg1, s),
+              "group TT x pass");
+  for (int i = 0; i < n; ++i) {
+    LinearPlan& P = G.P[i];
+    const float* parts[3] = {P.g1p, P.g2p, P.g3p};
+    const int nparts[3] = {s_dg1, P.TS, P.HS * P.TS};
+    const int64_t numel[3] = {G.dd[i].core_numel(0), G.dd[i].core_numel(1), G.dd[i].core_numel(2)};
+    float* outs[3] = {dcores[i][0], dcores[i][1], dcores[i][2]};
+    const bool want_dx = dx != nullptr && dx[i] != nullptr;
+    QA_TRY_CUDA(launch_grad_reduce3(parts, nparts, numel, outs, accumulate != 0, P.R1, P.J1, tt[i]->cores[0],
+                                    want_dx ? P.bext : nullptr, K, P.K2p, s),
+                "reduce core gradients + B_ext");
+    if (!want_dx) continue;
+    QA_TRY_CUDA(launch_dequantize(w[i]->codes, w[i]->scale, w[i]->offset, P.N, K, w[i]->bits, P.wdt, QA_BF16, P.Np,
+                                  true, s, nullptr),
+                "dequantize T");
+    GemmEpilogue e;
+    e.out_bf16 = static_cast<__nv_bfloat16*>(dx[i]);
+    e.ld_out = K;
+    GemmExt ext;
+    ext.A2 = P.dz1b;
+    ext.lda2 = P.K2p;
+    ext.B2 = P.bext;
+    ext.ldb2 = P.K2p;
+    ext.K2 = P.K2p;
+    QA_TRY(gemm_tc(1, dy[i], P.N, P.wdt, P.Np, T, K, P.Np, e, s, &ext));
+  }
+  return QA_OK;
+}
+
 size_t qa_merge_workspace_bytes(const qa_tt* tt) {
   TTDims dd;
   if (check_tt(tt, nullptr, &dd) != QA_OK) return 0;

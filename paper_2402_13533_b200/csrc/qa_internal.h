@@ -96,6 +96,15 @@ void tt_bwd_fused_plan(int64_t T, int H, int C, int* HR, int* HS, int* TS);
 cudaError_t launch_tt_bwd_fused(const __nv_bfloat16* dy, int64_t ldy, int64_t T, int H, int C, const float* Z1,
                                 const float* G2, const float* G3, float* dz1p, float* g3part, float* g2part,
                                 cudaStream_t s);
+// shared-input groups: one x pass for NA in {2, 3} adapters (J1 = 4, R1 = 8)
+bool group_x_pass_ok(int J1, int R1, int64_t K, int NA, const void* x);
+cudaError_t launch_actquant_z1_group(const void* x, int64_t T, int64_t K, bool want_codes, uint8_t* codes,
+                                     int64_t ldc, float* sx, float* ox, int32_t* rsx, const float* const* G1, int NA,
+                                     __nv_bfloat16* const* zb, int64_t ldzb, float* const* zf, float* frag_ws,
+                                     cudaStream_t s);
+cudaError_t launch_tt_dg1_group(const void* x, int64_t T, int64_t K, const float* const* dz1, float* const* part,
+                                int S, int HS, __nv_bfloat16* const* dz1b, int64_t ldb, int NA, int* splits_used,
+                                cudaStream_t s);
 // out_i (+)= Σ_p parts_i[p] for three partial sets, plus the B_ext operand (bext nullable), one launch
 cudaError_t launch_grad_reduce3(const float* const* parts, const int* nparts, const int64_t* numel,
                                 float* const* outs, bool accumulate, int R1, int J1, const float* G1,

@@ -869,6 +869,12 @@ __global__ void __launch_bounds__((AQP_NC + 1) * 32, 1)
 // whole row must be seen before its first code), so many CTAs per SM can stream at once.
 constexpr int AQC_WARPS = 8, AQC_UNROLL = 4;
 
+struct AqAdapters {  // per-adapter outputs of the shared x pass (unused entries null)
+  __nv_bfloat16* zb[3];
+  float* zf[3];
+  int64_t frag_stride;  // uint4 elements between adapters' G1 fragments
+};
+
 template <int J1>
 QA_DEV void aqc_offsets(uint32_t c, uint32_t& off0, uint32_t& off1) {
   off0 = J1 == 4 ? 16u * c : 32u * c;
@@ -933,26 +939,28 @@ QA_DEV uint32_t aqc_codes_row(const uint8_t* xrow, uint8_t* crow, int64_t nseg, 
 #ifndef QA_AQC_MINB
 #define QA_AQC_MINB 3  // <= 85 registers: 3 CTAs (24 warps) per SM; measured best of {1, 3, 4}
 #endif
-template <int J1, int R1, bool CODES, bool FRAG_SMEM>
-__global__ void __launch_bounds__(AQC_WARPS * 32, QA_AQC_MINB) k_aq_cta(const __nv_bfloat16* __restrict__ x, int64_t T, int64_t K,
+// NA adapters share the pass over x (the q / k / v or up / gate linears of a decoder layer read the
+// same input, transformer.py:862-874): one set of codes, NA sets of Z1 (fragments of adapter a at
+// frag + a * ad.frag_stride).
+template <int J1, int R1, bool CODES, bool FRAG_SMEM, int NA = 1>
+__global__ void __launch_bounds__(AQC_WARPS * 32, NA == 1 ? QA_AQC_MINB : 2) k_aq_cta(const __nv_bfloat16* __restrict__ x, int64_t T, int64_t K,
                                                             uint8_t* __restrict__ codes, int64_t ldc,
                                                             float* __restrict__ sx, float* __restrict__ ox,
                                                             int32_t* __restrict__ rsx, const uint4* __restrict__ frag_g,
-                                                            __nv_bfloat16* __restrict__ zb, int64_t ldzb,
-                                                            float* __restrict__ zf) {
+                                                            const AqAdapters ad, int64_t ldzb) {
   static_assert(J1 == 1 || J1 == 4, "J1");
   static_assert(R1 == 8 || R1 == 16, "R1");
   constexpr int K2 = J1 * R1, MT = R1 / 8, NJ = J1 == 4 ? 4 : 1, W = AQC_WARPS;
   constexpr int FPS = (J1 == 4 ? 1 : 4) * MT;  // fragments (one uint4 per lane) per 64-element segment
   extern __shared__ uint4 s_frag[];
-  __shared__ float s_z[W][8][K2];
+  __shared__ float s_z[W][8][NA * K2];
   __shared__ float s_lo[W][8], s_hi[W][8];
   __shared__ int32_t s_sum[W][8];
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id(), g = lane >> 2, c = lane & 3;
   const int64_t nseg = K / 64;
   if constexpr (FRAG_SMEM) {
     const int64_t n = nseg * FPS * 32;
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s_frag[i] = frag_g[i];
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s_frag[i] = frag_g[i];  // NA == 1 only
     __syncthreads();
   }
   const uint4* frag = FRAG_SMEM ? s_frag : frag_g;
@@ -965,13 +973,15 @@ __global__ void __launch_bounds__(AQC_WARPS * 32, QA_AQC_MINB) k_aq_cta(const __
     const int64_t trow = valid ? t0 + g : T - 1;  // rows past T are computed on a clamped row, never stored
     const uint8_t* xrow = reinterpret_cast<const uint8_t*>(x + trow * K);
     // ---- pass 1: Z1 partial + exact min / max over this warp's segments
-    float acc[NJ][MT][4];
+    float acc[NA][NJ][MT][4];
 #pragma unroll
-    for (int J = 0; J < NJ; ++J)
+    for (int aa = 0; aa < NA; ++aa)
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt)
+      for (int J = 0; J < NJ; ++J)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) acc[J][mt][i] = 0.f;
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) acc[aa][J][mt][i] = 0.f;
     __nv_bfloat162 lo2 = __floats2bfloat162_rn(INFINITY, INFINITY), hi2 = __floats2bfloat162_rn(-INFINITY, -INFINITY);
     auto seg = [&](int64_t st, const uint4 p0, const uint4 p1) {
       const uint32_t w[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
@@ -981,26 +991,30 @@ __global__ void __launch_bounds__(AQC_WARPS * 32, QA_AQC_MINB) k_aq_cta(const __
         lo2 = __hmin2(lo2, b2);
         hi2 = __hmax2(hi2, b2);
       }
-      if constexpr (J1 == 4) {
-        uint4 fr[MT];
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt) fr[mt] = frag[(st * MT + mt) * 32 + lane];
+      for (int aa = 0; aa < NA; ++aa) {
+        const uint4* fa = frag + aa * ad.frag_stride;
+        if constexpr (J1 == 4) {
+          uint4 fr[MT];
 #pragma unroll
-        for (int J = 0; J < 4; ++J) {
-          const uint32_t sel = (J & 1) ? 0x7632u : 0x5410u;
-          const uint32_t b0 = __byte_perm(w[J >> 1], w[2 + (J >> 1)], sel);
-          const uint32_t b1 = __byte_perm(w[4 + (J >> 1)], w[6 + (J >> 1)], sel);
+          for (int mt = 0; mt < MT; ++mt) fr[mt] = fa[(st * MT + mt) * 32 + lane];
 #pragma unroll
-          for (int mt = 0; mt < MT; ++mt) mma_16816(acc[J][mt], fr[mt].x, fr[mt].y, fr[mt].z, fr[mt].w, b0, b1);
-        }
-      } else {
+          for (int J = 0; J < 4; ++J) {
+            const uint32_t sel = (J & 1) ? 0x7632u : 0x5410u;
+            const uint32_t b0 = __byte_perm(w[J >> 1], w[2 + (J >> 1)], sel);
+            const uint32_t b1 = __byte_perm(w[4 + (J >> 1)], w[6 + (J >> 1)], sel);
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-          for (int mt = 0; mt < MT; ++mt) {
-            const uint4 fr = frag[((st * 4 + u) * MT + mt) * 32 + lane];
-            mma_16816(acc[0][mt], fr.x, fr.y, fr.z, fr.w, w[2 * u], w[2 * u + 1]);
+            for (int mt = 0; mt < MT; ++mt) mma_16816(acc[aa][J][mt], fr[mt].x, fr[mt].y, fr[mt].z, fr[mt].w, b0, b1);
           }
+        } else {
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+              const uint4 fr = fa[((st * 4 + u) * MT + mt) * 32 + lane];
+              mma_16816(acc[aa][0][mt], fr.x, fr.y, fr.z, fr.w, w[2 * u], w[2 * u + 1]);
+            }
+        }
       }
     };
     int64_t st = warp;
@@ -1019,16 +1033,19 @@ __global__ void __launch_bounds__(AQC_WARPS * 32, QA_AQC_MINB) k_aq_cta(const __
           __ldg(reinterpret_cast<const uint4*>(xrow + 128 * st + off1)));
     // D rows m = g (+ 8), columns n = tokens 2c, 2c + 1
 #pragma unroll
-    for (int J = 0; J < NJ; ++J)
+    for (int aa = 0; aa < NA; ++aa)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        if constexpr (MT == 1) {
-          s_z[warp][2 * c + h][g * J1 + J] = acc[J][0][h] + acc[J][0][2 + h];
-        } else {
-          s_z[warp][2 * c + h][g * J1 + J] = acc[J][0][h] + acc[J][1][h];
-          s_z[warp][2 * c + h][(g + 8) * J1 + J] = acc[J][0][2 + h] + acc[J][1][2 + h];
+      for (int J = 0; J < NJ; ++J)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          float* zrow = &s_z[warp][2 * c + h][aa * K2];
+          if constexpr (MT == 1) {
+            zrow[g * J1 + J] = acc[aa][J][0][h] + acc[aa][J][0][2 + h];
+          } else {
+            zrow[g * J1 + J] = acc[aa][J][0][h] + acc[aa][J][1][h];
+            zrow[(g + 8) * J1 + J] = acc[aa][J][0][2 + h] + acc[aa][J][1][2 + h];
+          }
         }
-      }
     if (CODES) {
       float lo = fminf(__low2float(lo2), __high2float(lo2)), hi = fmaxf(__low2float(hi2), __high2float(hi2));
       lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, 1));
@@ -1042,13 +1059,15 @@ __global__ void __launch_bounds__(AQC_WARPS * 32, QA_AQC_MINB) k_aq_cta(const __
     }
     __syncthreads();
     // ---- Z1 of the 8 tokens: fixed-order sum of the warp partials
-    for (int i = static_cast<int>(threadIdx.x); i < 8 * K2; i += W * 32) {
-      const int tk = i / K2, col = i % K2;
+    for (int i = static_cast<int>(threadIdx.x); i < 8 * NA * K2; i += W * 32) {
+      const int tk = i / (NA * K2), ac = i % (NA * K2), aa = ac / K2, col = ac % K2;
       const int64_t row = t0 + tk;
-      float v = s_z[0][tk][col];
+      float v = s_z[0][tk][ac];
 #pragma unroll
-      for (int w2 = 1; w2 < W; ++w2) v += s_z[w2][tk][col];
+      for (int w2 = 1; w2 < W; ++w2) v += s_z[w2][tk][ac];
       if (row < T) {
+        float* zf = ad.zf[aa];
+        __nv_bfloat16* zb = ad.zb[aa];
         if (zf != nullptr) zf[row * K2 + col] = v;
         if (zb != nullptr) {
           const __nv_bfloat16 hv = __float2bfloat16_rn(v);
@@ -1058,11 +1077,12 @@ __global__ void __launch_bounds__(AQC_WARPS * 32, QA_AQC_MINB) k_aq_cta(const __
         }
       }
     }
-    if (zb != nullptr && ldzb > 3 * K2) {
+    if (ldzb > 3 * K2) {
       const int padw = static_cast<int>(ldzb - 3 * K2);
-      for (int i = static_cast<int>(threadIdx.x); i < 8 * padw; i += W * 32) {
-        const int64_t row = t0 + i / padw;
-        if (row < T) zb[row * ldzb + 3 * K2 + i % padw] = __float2bfloat16_rn(0.f);
+      for (int i = static_cast<int>(threadIdx.x); i < 8 * NA * padw; i += W * 32) {
+        const int aa = i / (8 * padw), ii = i % (8 * padw);
+        const int64_t row = t0 + ii / padw;
+        if (row < T && ad.zb[aa] != nullptr) ad.zb[aa][row * ldzb + 3 * K2 + ii % padw] = __float2bfloat16_rn(0.f);
       }
     }
     if constexpr (CODES) {
@@ -2352,18 +2372,24 @@ __global__ void __launch_bounds__(256) k_grad_reduce3(const ReduceArgs a) {
 // column block 0 also emit the [hi | lo | hi | 0] split rows the dX GEMM's extension reads.
 constexpr int DM_COLS = 1024, DM_LDX = DM_COLS + 32, DM_ST = 16, DM_NSTG = 4, DM_DZT = 64;
 
-template <int R1>
+// NA adapters sharing x (a decoder layer's q / k / v or up / gate) run in one pass: per adapter its
+// own dZ1 planes, B fragments and accumulators.
+struct DgAdapters {
+  const float* dz1[3];
+  float* part[3];
+  __nv_bfloat16* dz1b[3];
+};
+
+template <int R1, int NA = 1>
 __global__ void __launch_bounds__(256, 1) k_tt_dg1m(const __nv_bfloat16* __restrict__ x, int64_t T, int64_t K,
-                                                    const float* __restrict__ dz1, float* __restrict__ part, int S,
-                                                    int HS, __nv_bfloat16* __restrict__ dz1b, int64_t ldb,
-                                                    int raw_async) {
+                                                    const DgAdapters ad, int S, int HS, int64_t ldb, int raw_async) {
   constexpr int J1 = 4, K2 = J1 * R1, NN = R1 / 8;
   extern __shared__ __align__(16) uint8_t dm_smem[];
   auto xs = reinterpret_cast<__nv_bfloat16(*)[DM_ST][DM_LDX]>(dm_smem);  // [NSTG]
   constexpr size_t XS_BYTES = sizeof(__nv_bfloat16) * DM_NSTG * DM_ST * DM_LDX;
-  auto dzs = reinterpret_cast<__nv_bfloat16(*)[DM_DZT][R1][J1]>(dm_smem + XS_BYTES);  // [2 planes]
-  // raw fp32 dZ1 partials of the next 64-token blocks, prefetched by cp.async: [2][HS][DZT][K2]
-  float* raw = reinterpret_cast<float*>(dm_smem + XS_BYTES + sizeof(__nv_bfloat16) * 2 * DM_DZT * R1 * J1);
+  auto dzs = reinterpret_cast<__nv_bfloat16(*)[DM_DZT][R1][J1]>(dm_smem + XS_BYTES);  // [NA][2 planes]
+  // raw fp32 dZ1 partials of the next 64-token blocks, prefetched by cp.async: [2][NA][HS][DZT][K2]
+  float* raw = reinterpret_cast<float*>(dm_smem + XS_BYTES + sizeof(__nv_bfloat16) * NA * 2 * DM_DZT * R1 * J1);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, tq = lane & 3;
   const int64_t c0 = static_cast<int64_t>(blockIdx.x) * DM_COLS;
   const int s = blockIdx.y;
@@ -2371,22 +2397,26 @@ __global__ void __launch_bounds__(256, 1) k_tt_dg1m(const __nv_bfloat16* __restr
   const int64_t t0 = s * per, t1 = t0 + per < T ? t0 + per : T;
   const int64_t nst = t1 > t0 ? (t1 - t0 + DM_ST - 1) / DM_ST : 0;
   constexpr int SPB = DM_DZT / DM_ST;  // stages per dZ1 block
-  float acc[2][NN][4];
+  float acc[2][NA * NN][4];
 #pragma unroll
   for (int m = 0; m < 2; ++m)
 #pragma unroll
-    for (int n = 0; n < NN; ++n)
+    for (int n = 0; n < NA * NN; ++n)
 #pragma unroll
       for (int q = 0; q < 4; ++q) acc[m][n][q] = 0.f;
   auto issue_raw = [&](int64_t blk) {  // 16-byte pieces of HS x [DZT][K2] fp32 rows (tokens past t1 are zero)
     const int64_t tb = t0 + blk * DM_DZT;
     if (tb >= t1) return;
-    float* dst = raw + static_cast<size_t>(blk & 1) * HS * DM_DZT * K2;
-    for (int i = tid; i < HS * DM_DZT * (K2 / 4); i += 256) {
-      const int h = i / (DM_DZT * (K2 / 4)), r = (i / (K2 / 4)) % DM_DZT, q = i % (K2 / 4);
-      const bool ok = tb + r < t1;
-      cp_async16(dst + (static_cast<size_t>(h) * DM_DZT + r) * K2 + 4 * q,
-                 ok ? dz1 + (static_cast<int64_t>(h) * T + tb + r) * K2 + 4 * q : dz1, ok);
+#pragma unroll
+    for (int aa = 0; aa < NA; ++aa) {
+      float* dst = raw + (static_cast<size_t>(blk & 1) * NA + aa) * HS * DM_DZT * K2;
+      const float* dz1 = ad.dz1[aa];
+      for (int i = tid; i < HS * DM_DZT * (K2 / 4); i += 256) {
+        const int h = i / (DM_DZT * (K2 / 4)), r = (i / (K2 / 4)) % DM_DZT, q = i % (K2 / 4);
+        const bool ok = tb + r < t1;
+        cp_async16(dst + (static_cast<size_t>(h) * DM_DZT + r) * K2 + 4 * q,
+                   ok ? dz1 + (static_cast<int64_t>(h) * T + tb + r) * K2 + 4 * q : dz1, ok);
+      }
     }
   };
   auto issue = [&](int64_t k) {
@@ -2412,9 +2442,10 @@ __global__ void __launch_bounds__(256, 1) k_tt_dg1m(const __nv_bfloat16* __restr
     if (k % SPB == 0) {  // dZ1 rows of the next 64 tokens: HS partials summed, hi / lo planes, [t][a][J]
       const int64_t blk = k / SPB, tb = t0 + k * DM_ST;
       const int nt = static_cast<int>(t1 - tb < DM_DZT ? t1 - tb : DM_DZT);
-      const float* rb = raw + static_cast<size_t>(blk & 1) * HS * DM_DZT * K2;
-      for (int i = tid; i < DM_DZT * K2; i += 256) {
-        const int r = i / K2, cc = i % K2;  // cc = a * J1 + J (the Z1 / dZ1 column order)
+      for (int i = tid; i < NA * DM_DZT * K2; i += 256) {
+        const int aa = i / (DM_DZT * K2), r = (i / K2) % DM_DZT, cc = i % K2;  // cc = a * J1 + J
+        const float* rb = raw + (static_cast<size_t>(blk & 1) * NA + aa) * HS * DM_DZT * K2;
+        const float* dz1 = ad.dz1[aa];
         float v = 0.f;
         if (r < nt) {
           if (raw_async) {
@@ -2427,8 +2458,9 @@ __global__ void __launch_bounds__(256, 1) k_tt_dg1m(const __nv_bfloat16* __restr
           }
         }
         const __nv_bfloat16 hi = __float2bfloat16_rn(v);
-        dzs[0][r][cc / J1][cc % J1] = hi;
-        dzs[1][r][cc / J1][cc % J1] = __float2bfloat16_rn(v - __bfloat162float(hi));
+        dzs[2 * aa][r][cc / J1][cc % J1] = hi;
+        dzs[2 * aa + 1][r][cc / J1][cc % J1] = __float2bfloat16_rn(v - __bfloat162float(hi));
+        __nv_bfloat16* dz1b = ad.dz1b[aa];
         if (dz1b != nullptr && blockIdx.x == 0 && r < nt) {  // [hi | lo | hi] split row for the dX GEMM
           __nv_bfloat16* row = dz1b + (tb + r) * ldb;
           row[cc] = hi;
@@ -2437,10 +2469,11 @@ __global__ void __launch_bounds__(256, 1) k_tt_dg1m(const __nv_bfloat16* __restr
           if (cc < ldb - 3 * K2) row[3 * K2 + cc] = __float2bfloat16_rn(0.f);
         }
       }
-      if (dz1b != nullptr && blockIdx.x == 0 && ldb - 3 * K2 > K2)
-        for (int i = tid; i < nt * static_cast<int>(ldb - 4 * K2); i += 256) {
-          const int r = i / static_cast<int>(ldb - 4 * K2), c = i % static_cast<int>(ldb - 4 * K2);
-          dz1b[(tb + r) * ldb + 4 * K2 + c] = __float2bfloat16_rn(0.f);
+      if (blockIdx.x == 0 && ldb - 3 * K2 > K2)
+        for (int i = tid; i < NA * nt * static_cast<int>(ldb - 4 * K2); i += 256) {
+          const int w4 = static_cast<int>(ldb - 4 * K2);
+          const int aa = i / (nt * w4), r = (i / w4) % nt, c = i % w4;
+          if (ad.dz1b[aa] != nullptr) ad.dz1b[aa][(tb + r) * ldb + 4 * K2 + c] = __float2bfloat16_rn(0.f);
         }
       __syncthreads();
     }
@@ -2451,13 +2484,14 @@ __global__ void __launch_bounds__(256, 1) k_tt_dg1m(const __nv_bfloat16* __restr
 #pragma unroll
     for (int ks = 0; ks < DM_ST / 4; ++ks) {  // 4 tokens x 4 J per k-step
       const int tr = ks * 4 + (tq >> 1), J = 2 * (tq & 1);
-      uint32_t bh[NN][2], bl[NN][2];
+      uint32_t bh[NA * NN][2], bl[NA * NN][2];
 #pragma unroll
-      for (int n = 0; n < NN; ++n) {
-        bh[n][0] = *reinterpret_cast<const uint32_t*>(&dzs[0][zr + tr][n * 8 + g][J]);
-        bh[n][1] = *reinterpret_cast<const uint32_t*>(&dzs[0][zr + tr + 2][n * 8 + g][J]);
-        bl[n][0] = *reinterpret_cast<const uint32_t*>(&dzs[1][zr + tr][n * 8 + g][J]);
-        bl[n][1] = *reinterpret_cast<const uint32_t*>(&dzs[1][zr + tr + 2][n * 8 + g][J]);
+      for (int n = 0; n < NA * NN; ++n) {
+        const int aa = n / NN, nn = n % NN;
+        bh[n][0] = *reinterpret_cast<const uint32_t*>(&dzs[2 * aa][zr + tr][nn * 8 + g][J]);
+        bh[n][1] = *reinterpret_cast<const uint32_t*>(&dzs[2 * aa][zr + tr + 2][nn * 8 + g][J]);
+        bl[n][0] = *reinterpret_cast<const uint32_t*>(&dzs[2 * aa + 1][zr + tr][nn * 8 + g][J]);
+        bl[n][1] = *reinterpret_cast<const uint32_t*>(&dzs[2 * aa + 1][zr + tr + 2][nn * 8 + g][J]);
       }
 #pragma unroll
       for (int m = 0; m < 2; ++m) {
@@ -2467,7 +2501,7 @@ __global__ void __launch_bounds__(256, 1) k_tt_dg1m(const __nv_bfloat16* __restr
         const uint32_t a2 = *reinterpret_cast<const uint32_t*>(&xs[slot][tr + 2][4 * jl + J]);
         const uint32_t a3 = *reinterpret_cast<const uint32_t*>(&xs[slot][tr + 2][4 * (jl + 8) + J]);
 #pragma unroll
-        for (int n = 0; n < NN; ++n) {
+        for (int n = 0; n < NA * NN; ++n) {
           mma_16816(acc[m][n], a0, a1, a2, a3, bh[n][0], bh[n][1]);
           mma_16816(acc[m][n], a0, a1, a2, a3, bl[n][0], bl[n][1]);
         }
@@ -2475,14 +2509,14 @@ __global__ void __launch_bounds__(256, 1) k_tt_dg1m(const __nv_bfloat16* __restr
     }
   }
   cp_async_wait<0>();
-  float* dst = part + static_cast<int64_t>(s) * (K / J1) * R1;
   const int64_t nj1 = K / J1;
 #pragma unroll
   for (int m = 0; m < 2; ++m)
 #pragma unroll
-    for (int n = 0; n < NN; ++n) {
+    for (int n = 0; n < NA * NN; ++n) {
+      float* dst = ad.part[n / NN] + static_cast<int64_t>(s) * (K / J1) * R1;
       const int64_t j1 = c0 / J1 + (warp * 2 + m) * 16 + g;
-      const int a = n * 8 + 2 * tq;
+      const int a = (n % NN) * 8 + 2 * tq;
       if (j1 < nj1) {
         dst[j1 * R1 + a] = acc[m][n][0];
         dst[j1 * R1 + a + 1] = acc[m][n][1];
@@ -3076,7 +3110,7 @@ cudaError_t launch_actquant_z1(const void* x, int x_dtype, int64_t T, int64_t K,
     const int64_t cap = static_cast<int64_t>(per_sm < 1 ? 1 : per_sm) * nsm;                                    \
     const unsigned grid = static_cast<unsigned>(ngroups < cap ? ngroups : cap);                                 \
     kern<<<grid, AQC_WARPS * 32, smem, s>>>(static_cast<const __nv_bfloat16*>(x), T, K, codes, ldc, sx, ox, rsx, \
-                                            fr, zb, ldzb, zf);                                                  \
+                                            fr, AqAdapters{{zb, nullptr, nullptr}, {zf, nullptr, nullptr}, 0}, ldzb); \
   }
 #define QA_AQC_C(JJ, RR)          \
   if (want_codes) {               \
@@ -3380,6 +3414,99 @@ cudaError_t launch_grad_reduce3(const float* const* parts, const int* nparts, co
   return cudaGetLastError();
 }
 
+// ---- shared-input groups (a decoder layer's q / k / v and up / gate, transformer.py:862-874):
+// one x pass serves NA in {2, 3} adapters of the pinned modes with J1 = 4, R1 = 8.
+bool group_x_pass_ok(int J1, int R1, int64_t K, int NA, const void* x) {
+  return J1 == 4 && R1 == 8 && NA >= 2 && NA <= 3 && K % 64 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0 &&
+         !aq_cta_disabled() && !dg1_mma_disabled();
+}
+
+cudaError_t launch_actquant_z1_group(const void* x, int64_t T, int64_t K, bool want_codes, uint8_t* codes,
+                                     int64_t ldc, float* sx, float* ox, int32_t* rsx, const float* const* G1, int NA,
+                                     __nv_bfloat16* const* zb, int64_t ldzb, float* const* zf, float* frag_ws,
+                                     cudaStream_t s) {
+  if (T == 0) return cudaSuccess;
+  const int64_t nfrag = K / 64;  // J1 = 4, R1 = 8: one uint4 per lane per 64-element segment
+  const int64_t stride = nfrag * 32;
+  uint4* fr = reinterpret_cast<uint4*>(frag_ws);
+  for (int a = 0; a < NA; ++a) {
+    LaunchScope scope(kTT, double(stride) * 16 + double(K) * 8 * 4, s);
+    count_launches(1);
+    k_g1_frag<4, 8><<<static_cast<unsigned>((stride + 255) / 256), 256, 0, s>>>(G1[a], fr + a * stride, nfrag);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  AqAdapters ad{{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}, stride};
+  for (int a = 0; a < NA; ++a) {
+    ad.zb[a] = zb != nullptr ? zb[a] : nullptr;
+    ad.zf[a] = zf != nullptr ? zf[a] : nullptr;
+  }
+  double out_bytes = 0.0;
+  for (int a = 0; a < NA; ++a) out_bytes += double(T) * ((ad.zb[a] ? ldzb * 2 : 0) + (ad.zf[a] ? 32 * 4 : 0));
+  LaunchScope scope(kQuantize, double(T) * K * 2 + (want_codes ? double(T) * ldc + 12.0 * T : 0.0) + out_bytes, s);
+  count_launches(1);
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t ngroups = (T + 7) / 8;
+#define QA_AQN(CC, NN)                                                                                         \
+  {                                                                                                            \
+    auto kern = k_aq_cta<4, 8, CC, false, NN>;                                                                 \
+    int per_sm = 1;                                                                                            \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, AQC_WARPS * 32, 0);                            \
+    const int64_t cap = static_cast<int64_t>(per_sm < 1 ? 1 : per_sm) * nsm;                                   \
+    kern<<<static_cast<unsigned>(ngroups < cap ? ngroups : cap), AQC_WARPS * 32, 0, s>>>(                      \
+        static_cast<const __nv_bfloat16*>(x), T, K, codes, ldc, sx, ox, rsx, fr, ad, ldzb);                    \
+  }
+  if (NA == 2) {
+    if (want_codes) QA_AQN(true, 2) else QA_AQN(false, 2)
+  } else {
+    if (want_codes) QA_AQN(true, 3) else QA_AQN(false, 3)
+  }
+#undef QA_AQN
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tt_dg1_group(const void* x, int64_t T, int64_t K, const float* const* dz1, float* const* part,
+                                int S, int HS, __nv_bfloat16* const* dz1b, int64_t ldb, int NA, int* splits_used,
+                                cudaStream_t s) {
+  constexpr int R1 = 8, J1 = 4;
+  if (splits_used != nullptr) *splits_used = S;
+  if (T == 0) return cudaSuccess;
+  double bytes = double(T) * K * 2;
+  for (int a = 0; a < NA; ++a) bytes += 4.0 * double(T) * J1 * R1 * HS + (dz1b && dz1b[a] ? 2.0 * double(T) * ldb : 0.0);
+  LaunchScope scope(kTT, bytes, s);
+  count_launches(1);
+  const int64_t gx = (K + DM_COLS - 1) / DM_COLS;
+  const int64_t stages = (T + DM_ST - 1) / DM_ST;
+  int64_t Sm = (148 + gx - 1) / gx;
+  if (Sm > stages) Sm = stages;
+  if (Sm > S) Sm = S;
+  if (Sm < 1) Sm = 1;
+  if (splits_used != nullptr) *splits_used = static_cast<int>(Sm);
+  DgAdapters ad{{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
+  for (int a = 0; a < NA; ++a) {
+    ad.dz1[a] = dz1[a];
+    ad.part[a] = part[a];
+    ad.dz1b[a] = dz1b != nullptr ? dz1b[a] : nullptr;
+  }
+  size_t smem = sizeof(__nv_bfloat16) * (DM_NSTG * DM_ST * DM_LDX + NA * 2 * DM_DZT * R1 * J1);
+  const size_t raw_bytes = sizeof(float) * 2 * NA * HS * DM_DZT * J1 * R1;
+  const int raw_async = smem + raw_bytes <= 220 * 1024 ? 1 : 0;
+  if (raw_async) smem += raw_bytes;
+  const dim3 gm(static_cast<unsigned>(gx), static_cast<unsigned>(Sm));
+  if (NA == 2) {
+    cudaFuncSetAttribute(k_tt_dg1m<8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    k_tt_dg1m<8, 2><<<gm, 256, smem, s>>>(static_cast<const __nv_bfloat16*>(x), T, K, ad, static_cast<int>(Sm), HS,
+                                          ldb, raw_async);
+  } else {
+    cudaFuncSetAttribute(k_tt_dg1m<8, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    k_tt_dg1m<8, 3><<<gm, 256, smem, s>>>(static_cast<const __nv_bfloat16*>(x), T, K, ad, static_cast<int>(Sm), HS,
+                                          ldb, raw_async);
+  }
+  return cudaGetLastError();
+}
+
 int tt_dg1_splits(int64_t T, int64_t K, int J1) {
   const int E = J1 == 1 ? 4 : 8;
   const int64_t gx = (K + 256 * E - 1) / (256 * E);
@@ -3412,14 +3539,15 @@ cudaError_t launch_tt_dg1(const void* x, int x_dtype, int64_t T, int64_t K, cons
       const size_t raw_bytes = sizeof(float) * 2 * HS * DM_DZT * J1 * R1;
       const int raw_async = smem + raw_bytes <= 220 * 1024 ? 1 : 0;
       if (raw_async) smem += raw_bytes;
+      const DgAdapters ad{{dz1, nullptr, nullptr}, {part, nullptr, nullptr}, {dz1b, nullptr, nullptr}};
       if (R1 == 8) {
         cudaFuncSetAttribute(k_tt_dg1m<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        k_tt_dg1m<8><<<gm, 256, smem, s>>>(static_cast<const __nv_bfloat16*>(x), T, K, dz1, part, static_cast<int>(Sm),
-                                           HS, dz1b, ldb, raw_async);
+        k_tt_dg1m<8><<<gm, 256, smem, s>>>(static_cast<const __nv_bfloat16*>(x), T, K, ad, static_cast<int>(Sm), HS,
+                                           ldb, raw_async);
       } else {
         cudaFuncSetAttribute(k_tt_dg1m<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        k_tt_dg1m<16><<<gm, 256, smem, s>>>(static_cast<const __nv_bfloat16*>(x), T, K, dz1, part, static_cast<int>(Sm),
-                                            HS, dz1b, ldb, raw_async);
+        k_tt_dg1m<16><<<gm, 256, smem, s>>>(static_cast<const __nv_bfloat16*>(x), T, K, ad, static_cast<int>(Sm), HS,
+                                            ldb, raw_async);
       }
       return cudaGetLastError();
     }

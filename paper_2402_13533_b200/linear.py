@@ -34,6 +34,8 @@ __all__ = [
     "tt_merge",
     "lora_merge",
     "attach_tt_adapter",
+    "group_forward",
+    "group_backward",
 ]
 
 
@@ -496,3 +498,89 @@ def attach_tt_adapter(name: str, base: QuantizedLinear, r: int, spec: TTSpec | N
 def quantized_linear(name: str, w, bits: int) -> QuantizedLinear:
     """quantize_model's per-matrix conversion (transformer.py:1122-1127)."""
     return QuantizedLinear(name, quantize_rows(w, bits))
+
+
+# ------------------------------------------------------------------------ shared-input groups
+def _group_c(members):
+    """ctypes arrays for qa_group_*; the returned tuple keeps every referenced object alive."""
+    n = len(members)
+    cores = [m._core_tensors() for m in members]
+    wcs = [m.base.q.as_c() for m in members]
+    tts = [m.spec.as_c(c) for m, c in zip(members, cores)]
+    W = (ctypes.POINTER(_lib.QWeight) * n)(*[ctypes.pointer(w) for w in wcs])
+    Tt = (ctypes.POINTER(_lib.TT) * n)(*[ctypes.pointer(t) for t in tts])
+    return W, Tt, (cores, wcs, tts)
+
+
+def group_forward(members, x, step: int = 0):
+    """Forward of members that read the same input (a decoder layer's wq / wk / wv on norm1 or
+    wu / wg on norm2, transformer.py:862-874) through qa_group_forward: the act-quant codes and
+    every member's Z1 come from one pass over x.  Returns [y_i]; each member keeps its
+    recompute-window state for a following backward on the same x (TTLinear.forward)."""
+    if not members:
+        return []
+    if any(not isinstance(m, TTLinear) or m.merged for m in members) or len(members) > 3:
+        return [m.forward(x, step) for m in members]
+    q0 = members[0].base.q
+    x = _as_device(x, q0.device)
+    lead = tuple(x.shape[:-1])
+    x2 = x.reshape(-1, q0.cols).contiguous()
+    if x2.dtype != torch.bfloat16 or any(m.fan_in != q0.cols for m in members):
+        return [m.forward(x, step) for m in members]
+    T, dev, n = x2.shape[0], q0.device, len(members)
+    W, Tt, keep = _group_c(members)
+    L = _lib.lib()
+    ys = [torch.empty((T, m.fan_out), dtype=torch.bfloat16, device=dev) for m in members]
+    nsv = [L.qa_linear_saved_bytes(ctypes.byref(keep[1][i]), ctypes.byref(keep[2][i]), T) for i in range(n)]
+    saved = [torch.empty(max(b, 4) // 4, dtype=torch.float32, device=dev) for b in nsv]
+    nb = L.qa_group_workspace_bytes(n, W, Tt, T)
+    if nb == 0:
+        raise ModelError(f"invalid group: {L.qa_last_error().decode()}")
+    ws = workspace.get(nb, dev)
+    Y = (ctypes.c_void_p * n)(*[y.data_ptr() for y in ys])
+    S = (ctypes.c_void_p * n)(*[sv.data_ptr() if b else None for sv, b in zip(saved, nsv)])
+    SB = (ctypes.c_size_t * n)(*nsv)
+    _lib.check(L.qa_group_forward(n, W, Tt, x2.data_ptr(), QA_BF16, T, Y, S, SB, ws.data_ptr(), ws.numel(),
+                                  _stream_ptr(dev)), "qa_group_forward")
+    for m, sv, b in zip(members, saved, nsv):
+        m._saved = (weakref.ref(x), m._tag(x), sv) if b else None
+    return [y.reshape(*lead, y.shape[-1]) for y in ys]
+
+
+def group_backward(members, x, dys, grads: dict, step: int = 0):
+    """Backward of a shared-input group (transformer.py:919-944) through qa_group_backward: one
+    pass over x for every member's dG1.  Accumulates the core gradients into `grads` like
+    _accumulate and returns [dx_i] (the caller sums them, as _layer_backward does)."""
+    if not members:
+        return []
+    simple = any(not isinstance(m, TTLinear) or m.merged or isinstance(m, LoraLinear) for m in members)
+    q0 = members[0].base.q if not simple else None
+    if simple or len(members) > 3:
+        return [m.backward(x, dy, grads, step) for m, dy in zip(members, dys)]
+    x = _as_device(x, q0.device)
+    lead = tuple(x.shape[:-1])
+    x2 = x.reshape(-1, q0.cols).contiguous()
+    dys2 = [_as_device(dy, q0.device).reshape(-1, m.fan_out).contiguous() for m, dy in zip(members, dys)]
+    T, dev, n = x2.shape[0], q0.device, len(members)
+    W, Tt, keep = _group_c(members)
+    L = _lib.lib()
+    savedl = [m._take_saved(x) for m in members]
+    dxs = [torch.empty((T, q0.cols), dtype=torch.bfloat16, device=dev) for _ in members]
+    gr = [[torch.empty(m.spec.core_shape(k), dtype=torch.float32, device=dev) for k in range(m.spec.d)]
+          for m in members]
+    nb = L.qa_group_workspace_bytes(n, W, Tt, T)
+    if nb == 0:
+        raise ModelError(f"invalid group: {L.qa_last_error().decode()}")
+    ws = workspace.get(nb, dev)
+    DY = (ctypes.c_void_p * n)(*[d.data_ptr() for d in dys2])
+    DX = (ctypes.c_void_p * n)(*[d.data_ptr() for d in dxs])
+    per = [(ctypes.c_void_p * _lib.QA_TT_MAX_D)(*[g.data_ptr() for g in gm]) for gm in gr]
+    DC = (ctypes.POINTER(ctypes.c_void_p) * n)(*[ctypes.cast(p, ctypes.POINTER(ctypes.c_void_p)) for p in per])
+    S = (ctypes.c_void_p * n)(*[sv.data_ptr() if sv is not None else None for sv in savedl])
+    SB = (ctypes.c_size_t * n)(*[sv.numel() * 4 if sv is not None else 0 for sv in savedl])
+    dy_dtype = _dtype_code(dys2[0])
+    _lib.check(L.qa_group_backward(n, W, Tt, x2.data_ptr(), _dtype_code(x2), DY, dy_dtype, T, DX, DC, 0, S, SB,
+                                   ws.data_ptr(), ws.numel(), _stream_ptr(dev)), "qa_group_backward")
+    for m, g in zip(members, gr):
+        m._scatter_grads(grads, g)
+    return [d.reshape(*lead, q0.cols) for d in dxs]

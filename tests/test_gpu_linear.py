@@ -272,3 +272,31 @@ def test_full_size_properties():
     assert O.rel_err(_np(c), _np(a) + _np(b)) <= 2 * TOL_BF16
     for u, v, w in zip(ga, gb, gc):
         assert O.rel_err(_np(w), _np(u) + _np(v)) <= 2 * TOL_BF16
+
+
+@pytest.mark.parametrize("ns,K,T,r", [((512, 768, 1024), 1024, 200, 8), ((1024, 2048), 512, 77, 8),
+                                      ((512, 256), 1024, 64, 16)])
+def test_shared_input_group_matches_members(ns, K, T, r):
+    """qa_group_forward / qa_group_backward (one x pass per direction for q / k / v-style members,
+    transformer.py:862-874 / 919-944) give each member exactly its single-linear results; r = 16
+    exercises the member-by-member fallback."""
+    x = torch.from_numpy(O.seeded_random(T, K, 41)).cuda().to(torch.bfloat16)
+    members, ref_members = [], []
+    for i, N in enumerate(ns):
+        q = qa.quantize_rows(O.seeded_random(N, K, 50 + i, std=0.02), 8)
+        spec = L.TTSpec.for_shape(N, K, r)
+        cores = [torch.from_numpy(c).cuda() for c in O.tt_init_cores(O.TTShape(spec.m, spec.n, spec.ranks), 60 + i)]
+        members.append(L.TTLinear(f"m{i}", L.QuantizedLinear(f"m{i}.base", q), spec, [c.clone() for c in cores]))
+        ref_members.append(L.TTLinear(f"m{i}", L.QuantizedLinear(f"m{i}.base", q), spec, [c.clone() for c in cores]))
+    dys = [torch.from_numpy(O.seeded_random(T, N, 70 + i)).cuda().to(torch.bfloat16) for i, N in enumerate(ns)]
+    ys = L.group_forward(members, x)
+    g_grads, r_grads = {}, {}
+    dxs = L.group_backward(members, x, dys, g_grads)
+    for i, m in enumerate(ref_members):
+        y_ref = m.forward(x)
+        assert torch.equal(ys[i], y_ref), i
+        dx_ref = m.backward(x, dys[i], r_grads)
+        assert torch.equal(dxs[i], dx_ref), i
+    assert sorted(g_grads) == sorted(r_grads)
+    for k in g_grads:
+        assert torch.equal(g_grads[k], r_grads[k]), k
