@@ -38,7 +38,10 @@ constexpr int THREADS = 256;
 // kind 0 persistent kernels issue tile i-1's y2 extension this many k-blocks into tile i's main
 // loop: late enough for the epilogue's in-place s32 -> fp32 pass, early enough that tile i-1's TMEM
 // buffer is drained before tile i+1 needs it.
-constexpr int kFoldAt = 16;
+#ifndef QA_FOLD_AT
+#define QA_FOLD_AT 16
+#endif
+constexpr int kFoldAt = QA_FOLD_AT;
 constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 4 * BN * 4 /*column terms*/ + 256;
 
 template <int KIND>
@@ -49,6 +52,8 @@ struct Cfg {
 struct KParams {
   int64_t M, N, K;  // K in elements of the main operands
   int num_ext;      // extension k-blocks (bf16, 64 elements each)
+  int prefetch;     // int8 CTA-pair kernel: L2 prefetch of the next tile's operands
+  int tma_store;    // CTA-pair kernel: bf16 output through shared memory + TMA stores (tmC)
   GemmEpilogue e;
 };
 
@@ -586,19 +591,21 @@ __global__ void __launch_bounds__(THREADS, 1)
 constexpr int STAGES2 = 6;
 constexpr int BH_BYTES = 128 * BK_BYTES;  // half of B per CTA
 constexpr int STAGE2_BYTES = A_BYTES + BH_BYTES;
-constexpr int SMEM2_BYTES = 1024 + STAGES2 * STAGE2_BYTES + 4 * BN * 4 + 512;
+constexpr int STG2_BYTES = 4 * 32 * 128;  // TMA-store staging: one 32-row x 64-col bf16 box per epilogue warp
+constexpr int SMEM2_BYTES = 1024 + STAGES2 * STAGE2_BYTES + STG2_BYTES + 4 * BN * 4 + 512;
 
 template <int KIND>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     k_gemm_tc_2sm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                   const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
-                  const KParams p) {
+                  const __grid_constant__ CUtensorMap tmC, const KParams p) {
   constexpr uint32_t TMEM_COLS = 512;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES2 * A_BYTES;
-  float* colA = reinterpret_cast<float*>(smem + STAGES2 * STAGE2_BYTES);
+  uint8_t* sStage = smem + STAGES2 * STAGE2_BYTES;  // 1024-aligned (128B-swizzled TMA boxes)
+  float* colA = reinterpret_cast<float*>(sStage + STG2_BYTES);
   float* colB = colA + BN;
   float* colC = colB + BN;
   int32_t* colD = reinterpret_cast<int32_t*>(colC + BN);
@@ -654,6 +661,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const bool fold_ext = KIND == 0 && num_ext > 0;
+  const bool prefetch_on = p.prefetch != 0;
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (both CTAs)
@@ -671,15 +679,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         ++q;
       };
       for (int i = 0; i < my_tiles; ++i) {
-        int64_t m0, n0, pm0, pn0;
+        int64_t m0, n0, pm0, pn0, xm0 = 0, xn0 = 0;
         coords(i, m0, n0);
+        // int8: one k-block takes ~half the time of a bf16 one, so the 6-stage ring covers L2 but not
+        // DRAM latency; warm L2 with the next tile's k-block alongside each load of this tile
+        const bool pf = KIND == 0 && i + 1 < my_tiles && prefetch_on;
+        if (pf) coords(i + 1, xm0, xn0);
+        auto main_block = [&](int kb) {
+          load(&tmA, &tmB, kb * BK, m0, n0);
+          if (pf) {
+            tma_prefetch_2d(&tmA, kb * BK, static_cast<int32_t>(xm0 + BM * rank));
+            tma_prefetch_2d(&tmB, kb * BK, static_cast<int32_t>(xn0 + 128 * rank));
+          }
+        };
         const int split = (fold_ext && i > 0) ? (num_main < kFoldAt ? num_main : kFoldAt) : num_main;
-        for (int kb = 0; kb < split; ++kb) load(&tmA, &tmB, kb * BK, m0, n0);
+        for (int kb = 0; kb < split; ++kb) main_block(kb);
         if (fold_ext && i > 0) {
           coords(i - 1, pm0, pn0);
           for (int e = 0; e < num_ext; ++e) load(&tmA2, &tmB2, e * 64, pm0, pn0);
         }
-        for (int kb = split; kb < num_main; ++kb) load(&tmA, &tmB, kb * BK, m0, n0);
+        for (int kb = split; kb < num_main; ++kb) main_block(kb);
         if (KIND == 1)
           for (int e = 0; e < num_ext; ++e) load(&tmA2, &tmB2, e * 64, m0, n0);
       }
@@ -815,6 +834,54 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         mbar_wait(&acc_full[b], ph);
         tc_fence_after();
       }
+      if (p.tma_store) {
+        // bf16 tile of this warp (32 rows x 256 cols) in 64-column boxes: TMEM -> registers ->
+        // 128B-swizzled staging -> TMA store (asynchronous, fully coalesced)
+        uint8_t* stg = sStage + quarter * (32 * 128);
+#pragma unroll 1
+        for (int q = 0; q < BN / 64; ++q) {
+          uint32_t v0[32], v1[32];
+          tmem_ld_32x32b_x32(d + (2 * q) * 32u, v0);
+          tmem_ld_32x32b_x32(d + (2 * q + 1) * 32u, v1);
+          tmem_ld_wait();
+          uint32_t pk[32];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t(&v)[32] = h ? v1 : v0;
+#pragma unroll
+            for (int j2 = 0; j2 < 16; ++j2) {
+              float a, bb;
+              if (KIND == 0 && !fold_ext) {
+                const int c = (2 * q + h) * 32 + 2 * j2;
+                const int32_t c0 = static_cast<int32_t>(v[2 * j2]) + ibase - colD[c];
+                const int32_t c1 = static_cast<int32_t>(v[2 * j2 + 1]) + ibase - colD[c + 1];
+                a = fmaf(sx, fmaf(colA[c], static_cast<float>(c0), colB[c] * rsxc), ox * colC[c]);
+                bb = fmaf(sx, fmaf(colA[c + 1], static_cast<float>(c1), colB[c + 1] * rsxc), ox * colC[c + 1]);
+              } else {
+                a = __uint_as_float(v[2 * j2]);
+                bb = __uint_as_float(v[2 * j2 + 1]);
+              }
+              const __nv_bfloat162 b2 = __floats2bfloat162_rn(a, bb);
+              pk[h * 16 + j2] = *reinterpret_cast<const uint32_t*>(&b2);
+            }
+          }
+          if (lane == 0) bulk_wait_read0();  // the previous box has left the staging buffer
+          __syncwarp();
+#pragma unroll
+          for (int c16 = 0; c16 < 8; ++c16)
+            *reinterpret_cast<uint4*>(stg + lane * 128 + ((c16 ^ (lane & 7)) << 4)) =
+                make_uint4(pk[4 * c16], pk[4 * c16 + 1], pk[4 * c16 + 2], pk[4 * c16 + 3]);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmC, stg, static_cast<int32_t>(n0 + 64 * q), static_cast<int32_t>(m0 + BM * rank + quarter * 32));
+            bulk_commit();
+          }
+        }
+        tc_fence_before();
+        arrive_leader(&tmem_empty[b]);
+        continue;
+      }
       uint32_t packed[BN / 2];
 #pragma unroll
       for (int chunk = 0; chunk < BN / 32; ++chunk) {
@@ -875,12 +942,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     }
   }
 
+  if (warp >= 4 && p.tma_store && lane_id() == 0) bulk_wait0();  // stores complete before the CTA exits
   tc_fence_before();
   cluster_sync();
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc_2sm<TMEM_COLS>(tmem_base);
   }
+}
+
+// QA_GEMM_PREFETCH=1 enables the int8 kernel's L2 prefetch of the next tile (measured slower on
+// B200: 509 vs 446 us at 16384 x 4096 x 11008; kept for A/B comparisons).
+bool prefetch_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("QA_GEMM_PREFETCH");
+    return v != nullptr && v[0] == '1';
+  }();
+  return on;
+}
+
+// QA_GEMM_TMA_STORE=0 keeps the direct global stores of the CTA-pair epilogue (A/B comparisons).
+bool tma_store_disabled() {
+  static const bool off = [] {
+    const char* v = getenv("QA_GEMM_TMA_STORE");
+    return v != nullptr && v[0] == '0';
+  }();
+  return off;
 }
 
 // QA_GEMM_2SM=0 keeps the single-CTA persistent kernel (A/B comparisons, triage).
@@ -976,6 +1063,8 @@ int launch(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, in
   p.N = N;
   p.K = K;
   p.num_ext = num_ext;
+  p.prefetch = prefetch_enabled() ? 1 : 0;
+  p.tma_store = 0;
   p.e = epi;
   const double kalg = KIND == 0 && epi.k_real > 0 ? double(epi.k_real) : double(K);
   LaunchScope scope(KIND == 0 ? kGemmI8 : kGemmBF16, 2.0 * double(M) * double(N) * kalg, s);
@@ -1003,7 +1092,12 @@ int launch(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, in
     if (num_ext == 0) tb2h = tbh;
     const int64_t pair_tiles = ((N + BN - 1) / BN) * ((M + 2 * BM - 1) / (2 * BM));
     const int64_t clusters = pair_tiles < num_sms / 2 ? pair_tiles : num_sms / 2;
-    k_gemm_tc_2sm<KIND><<<static_cast<unsigned>(2 * clusters), THREADS, SMEM2_BYTES, s>>>(ta, tbh, ta2, tb2h, p);
+    // bf16-only outputs leave through shared memory + TMA stores (64-column x 32-row boxes)
+    CUtensorMap tc = ta;
+    if (epi.out_bf16 != nullptr && epi.out_f32 == nullptr && epi.addend == nullptr && !tma_store_disabled() &&
+        aligned_operand(epi.out_bf16, epi.ld_out, 2) && make_tmap(&tc, epi.out_bf16, 2, M, N, epi.ld_out, 32))
+      p.tma_store = 1;
+    k_gemm_tc_2sm<KIND><<<static_cast<unsigned>(2 * clusters), THREADS, SMEM2_BYTES, s>>>(ta, tbh, ta2, tb2h, tc, p);
   } else {
     const unsigned grid = static_cast<unsigned>(tiles < num_sms ? tiles : num_sms);
     k_gemm_tc_p<KIND><<<grid, THREADS, SMEM_BYTES, s>>>(ta, tb, ta2, tb2, p);
