@@ -812,17 +812,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         tc_fence_after();
         if (fold_ext) {
 #pragma unroll 1
-          for (int chunk = 0; chunk < BN / 32; ++chunk) {
-            uint32_t v[32];
-            tmem_ld_32x32b_x32(d + chunk * 32u, v);
+          for (int chunk = 0; chunk < BN / 32; chunk += 2) {  // two TMEM loads in flight per wait
+            uint32_t v[2][32];
+            tmem_ld_32x32b_x32(d + chunk * 32u, v[0]);
+            tmem_ld_32x32b_x32(d + (chunk + 1) * 32u, v[1]);
             tmem_ld_wait();
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const int c = chunk * 32 + j;
-              const int32_t accc = static_cast<int32_t>(v[j]) + ibase - colD[c];
-              v[j] = __float_as_uint(fmaf(sx, fmaf(colA[c], static_cast<float>(accc), colB[c] * rsxc), ox * colC[c]));
-            }
-            tmem_st_32x32b_x32(d + chunk * 32u, v);
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                const int c = (chunk + h) * 32 + j;
+                const int32_t accc = static_cast<int32_t>(v[h][j]) + ibase - colD[c];
+                v[h][j] =
+                    __float_as_uint(fmaf(sx, fmaf(colA[c], static_cast<float>(accc), colB[c] * rsxc), ox * colC[c]));
+              }
+            tmem_st_32x32b_x32(d + chunk * 32u, v[0]);
+            tmem_st_32x32b_x32(d + (chunk + 1) * 32u, v[1]);
           }
           tmem_st_wait();
           tc_fence_before();
