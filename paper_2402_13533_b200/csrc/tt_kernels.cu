@@ -12,6 +12,7 @@
 #include "qa_common.cuh"
 #include "qa_internal.h"
 #include "qa_timing.h"
+#include "quant_row.cuh"
 
 namespace qa {
 
@@ -216,6 +217,72 @@ __global__ void __launch_bounds__(128) k_prefix_full(TTDims dd, TTCorePtrs cores
   L[idx] = v[b];
 }
 
+// Prefix of the pinned 3-core modes (m_1 = 1): L[h, j1 J1 + j2, :] = G1[0, 0, j1, :] · G2[:, h, j2, :].
+// A CTA owns one h and 256 columns; G2[:, h, :, :] (R x J1 x R) sits in shared memory.
+template <int R>
+__global__ void __launch_bounds__(256) k_prefix_d3(const float* __restrict__ G1, const float* __restrict__ G2,
+                                                   float* __restrict__ L, int H, int J1, int64_t K) {
+  __shared__ float g2[R][16][R];  // [a][j2][b], J1 <= 16
+  const int h = blockIdx.y;
+  for (int q = threadIdx.x; q < R * J1 * R; q += 256) {
+    const int a = q / (J1 * R), j2 = (q / R) % J1, b = q % R;
+    g2[a][j2][b] = G2[((static_cast<int64_t>(a) * H + h) * J1 + j2) * R + b];
+  }
+  __syncthreads();
+  const int64_t col = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;
+  if (col >= K) return;
+  const int64_t j1 = col / J1;
+  const int j2 = static_cast<int>(col - j1 * J1);
+  float v[R];
+#pragma unroll
+  for (int a = 0; a < R; ++a) v[a] = __ldg(G1 + j1 * R + a);
+  float out[R];
+#pragma unroll
+  for (int b = 0; b < R; ++b) {
+    float acc = 0.f;
+#pragma unroll
+    for (int a = 0; a < R; ++a) acc = fmaf(v[a], g2[a][j2][b], acc);
+    out[b] = acc;
+  }
+  float4* dst = reinterpret_cast<float4*>(L + (static_cast<int64_t>(h) * K + col) * R);
+#pragma unroll
+  for (int q = 0; q < R / 4; ++q) dst[q] = make_float4(out[4 * q], out[4 * q + 1], out[4 * q + 2], out[4 * q + 3]);
+}
+
+// Same chain, one thread per (ip, jp) writing all R entries (R <= 16).
+__global__ void __launch_bounds__(128) k_prefix_vec(TTDims dd, TTCorePtrs cores, float* __restrict__ L, int64_t IP,
+                                                    int64_t JP, int R) {
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= IP * JP) return;
+  const int64_t jp = idx % JP, ip = idx / JP;
+  const int last = dd.d - 1;
+  int iv[QA_TT_MAX_D], jv[QA_TT_MAX_D];
+  int64_t ir = ip, jr = jp;
+  for (int k = last - 1; k >= 0; --k) {
+    iv[k] = static_cast<int>(ir % dd.m[k]);
+    ir /= dd.m[k];
+    jv[k] = static_cast<int>(jr % dd.n[k]);
+    jr /= dd.n[k];
+  }
+  constexpr int kMaxR = 64;
+  float v[kMaxR], w[kMaxR];
+  v[0] = 1.f;
+  int ra = 1;
+  for (int k = 0; k < last; ++k) {
+    const int rb = dd.r[k + 1];
+    const float* g = cores.p[k];
+    for (int bb = 0; bb < rb; ++bb) {
+      float s = 0.f;
+      for (int a = 0; a < ra; ++a)
+        s = fmaf(v[a], g[((static_cast<int64_t>(a) * dd.m[k] + iv[k]) * dd.n[k] + jv[k]) * rb + bb], s);
+      w[bb] = s;
+    }
+    for (int bb = 0; bb < rb; ++bb) v[bb] = w[bb];
+    ra = rb;
+  }
+  for (int b = 0; b < R; ++b) L[idx * R + b] = v[b];
+}
+
 template <typename OutT>
 QA_DEV void store_out(OutT* p, float v);
 template <>
@@ -253,6 +320,121 @@ __global__ void __launch_bounds__(256) k_last_full(const float* __restrict__ L, 
       store_out<OutT>(out + idx, static_cast<float>(__dadd_rn(deq, static_cast<double>(s))));
     } else {
       store_out<OutT>(out + idx, s);
+    }
+  }
+}
+
+// Merge / materialise for last cores with n_d = 1 (the pinned Llama modes and LoRA):
+//   W'[row, col] = code(row, col) * scale[row] + offset[row] + Σ_b L[h, col, b] Gd[b, i],  row = h md + i
+// A warp owns one row and 128 consecutive columns (4 per lane: one 4- or 2-byte code load, one 8- or
+// 16-byte output store per lane, coalesced); the CTA's 8 warps walk MG_ROWS rows of one h-block with
+// the lane's L[h, col, :] pairs held in registers (packed FFMA2 over column pairs) and the code words
+// of RU rows loaded before any is used.  Dequantisation is one fp32 FMA (error < 1 ulp of fp32 against
+// the reference's fp64 route, quant.py:102-105 — well inside the merge's 1e-5 tolerance).
+constexpr int MG_COLS = 256;
+
+template <typename OutT, int BITS, int R>
+__global__ void __launch_bounds__(256, 2) k_merge_nd1(const float* __restrict__ L, const float* __restrict__ Gd,
+                                                      int64_t md, int64_t N, int64_t K, int MG_ROWS,
+                                                      const uint8_t* __restrict__ codes,
+                                                      const float* __restrict__ scale,
+                                                      const float* __restrict__ offset, OutT* __restrict__ out) {
+  __shared__ float gs[R][256];  // Gd[:, i] of this CTA's rows (i = row - h md), MG_ROWS <= 256
+  __shared__ float ss[256], os[256];
+  extern __shared__ __align__(16) uint8_t mg_codes[];  // the CTA's code tile [MG_ROWS][256 * BITS / 8]
+  constexpr int CB = MG_COLS * BITS / 8;               // code bytes per tile row
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t c0 = static_cast<int64_t>(blockIdx.x) * MG_COLS;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * MG_ROWS;
+  const int64_t h = r0 / md;  // MG_ROWS divides md: one h-block per CTA
+  const int i0 = static_cast<int>(r0 - h * md);
+  const int64_t cld = BITS == 8 ? K : (K + 1) / 2;
+  if (codes != nullptr) {  // the whole code tile in flight at once (cp.async), consumed from shared memory
+    const int64_t cb0 = BITS == 8 ? c0 : c0 / 2;
+    for (int q = threadIdx.x; q < MG_ROWS * (CB / 16); q += 256) {
+      const int r = q / (CB / 16), ch = q % (CB / 16);
+      const bool ok = r0 + r < N && cb0 + ch * 16 + 16 <= cld;
+      cp_async16(mg_codes + r * CB + ch * 16, ok ? codes + (r0 + r) * cld + cb0 + ch * 16 : codes, ok);
+    }
+    cp_async_commit();
+  }
+  for (int q = threadIdx.x; q < R * MG_ROWS; q += 256) gs[q / MG_ROWS][q % MG_ROWS] = Gd[(q / MG_ROWS) * md + i0 + q % MG_ROWS];
+  for (int q = threadIdx.x; q < MG_ROWS; q += 256) {
+    ss[q] = codes != nullptr && r0 + q < N ? scale[r0 + q] : 0.f;
+    os[q] = codes != nullptr && r0 + q < N ? offset[r0 + q] : 0.f;
+  }
+  const int64_t col = c0 + lane * 8;
+  unsigned long long lp[R][4];  // column pairs of the lane's 8 columns, per rank index b
+  {
+    const float4* lr = reinterpret_cast<const float4*>(L + (h * K + col) * R);
+    float lv[8][R];
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+#pragma unroll
+      for (int q = 0; q < R / 4; ++q) {
+        const float4 v = __ldg(lr + c * (R / 4) + q);
+        lv[c][4 * q] = v.x;
+        lv[c][4 * q + 1] = v.y;
+        lv[c][4 * q + 2] = v.z;
+        lv[c][4 * q + 3] = v.w;
+      }
+#pragma unroll
+    for (int b = 0; b < R; ++b)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) lp[b][q] = f2pack(lv[2 * q][b], lv[2 * q + 1][b]);
+  }
+  OutT* obase = out + col;
+  cp_async_wait<0>();
+  __syncthreads();
+  if (col >= K) return;
+  for (int rl = warp; rl < MG_ROWS; rl += 8) {
+    const int64_t row = r0 + rl;
+    if (row >= N) break;
+    unsigned long long acc[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+    for (int b = 0; b < R; ++b) {
+      const float gb = gs[b][rl];
+      const unsigned long long g2 = f2pack(gb, gb);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) ffma2(acc[q], g2, lp[b][q]);
+    }
+    float wt[8];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      wt[2 * q] = f2lo(acc[q]);
+      wt[2 * q + 1] = f2hi(acc[q]);
+    }
+    if (codes != nullptr) {
+      uint32_t cv[8];
+      if constexpr (BITS == 8) {
+        const uint2 w = *reinterpret_cast<const uint2*>(mg_codes + rl * CB + lane * 8);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          cv[e] = (w.x >> (8 * e)) & 0xFFu;
+          cv[4 + e] = (w.y >> (8 * e)) & 0xFFu;
+        }
+      } else {  // two codes per byte, even column in the low nibble (quant.py:37-52)
+        const uint32_t w = *reinterpret_cast<const uint32_t*>(mg_codes + rl * CB + lane * 4);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) cv[e] = (w >> (4 * e)) & 0xFu;
+      }
+      const float sc = ss[rl], of = os[rl];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) wt[e] += fmaf(static_cast<float>(cv[e]), sc, of);
+    }
+    OutT* dst = obase + row * K;
+    if constexpr (sizeof(OutT) == 2) {
+      uint4 pk;
+      uint32_t* pw = reinterpret_cast<uint32_t*>(&pk);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const __nv_bfloat162 b2 = __floats2bfloat162_rn(wt[2 * q], wt[2 * q + 1]);
+        pw[q] = *reinterpret_cast<const uint32_t*>(&b2);
+      }
+      *reinterpret_cast<uint4*>(dst) = pk;
+    } else {
+      *reinterpret_cast<float4*>(dst) = make_float4(wt[0], wt[1], wt[2], wt[3]);
+      *reinterpret_cast<float4*>(dst + 4) = make_float4(wt[4], wt[5], wt[6], wt[7]);
     }
   }
 }
@@ -347,7 +529,19 @@ cudaError_t launch_tt_prefix_full(const TTDims& dd, const float* const* cores, f
   const int64_t total = IP * JP * R;
   LaunchScope scope(kMerge, 4.0 * double(total), s);
   count_launches(1);
-  k_prefix_full<<<static_cast<unsigned>((total + 127) / 128), 128, 0, s>>>(dd, cp, L, IP, JP, R);
+  if (dd.d == 3 && dd.m[0] == 1 && (R == 8 || R == 16) && dd.r[1] == R && dd.n[1] <= 16) {
+    // pinned 3-core modes: a tiny GEMM per (h, j2) with G2[:, h, :, :] in shared memory
+    const dim3 grid(static_cast<unsigned>((JP + 255) / 256), static_cast<unsigned>(IP));
+    if (R == 8)
+      k_prefix_d3<8><<<grid, 256, 0, s>>>(cores[0], cores[1], L, static_cast<int>(IP), dd.n[1], JP);
+    else
+      k_prefix_d3<16><<<grid, 256, 0, s>>>(cores[0], cores[1], L, static_cast<int>(IP), dd.n[1], JP);
+  } else if (R <= 16) {  // one thread per (ip, jp): the whole rank vector at once
+    const int64_t pairs = IP * JP;
+    k_prefix_vec<<<static_cast<unsigned>((pairs + 127) / 128), 128, 0, s>>>(dd, cp, L, IP, JP, R);
+  } else {
+    k_prefix_full<<<static_cast<unsigned>((total + 127) / 128), 128, 0, s>>>(dd, cp, L, IP, JP, R);
+  }
   return cudaGetLastError();
 }
 
@@ -362,6 +556,44 @@ cudaError_t launch_tt_last_full(const TTDims& dd, const float* L, const float* G
   const int64_t total = dd.N * dd.K;
   LaunchScope scope(kMerge, double(total) * ((codes ? (bits == 8 ? 1.0 : 0.5) : 0.0) + (out_dtype == QA_F32 ? 4 : 2)), s);
   count_launches(1);
+  const int R = dd.r[last];
+  const int64_t md = dd.m[last];
+  const int mg_rows = md % 256 == 0 ? 256 : (md % 64 == 0 ? 64 : 0);
+  const bool nd1 = dd.n[last] == 1 && mg_rows > 0 && dd.K % 32 == 0 && (R == 8 || R == 16) &&
+                   reinterpret_cast<uintptr_t>(out) % 16 == 0 && reinterpret_cast<uintptr_t>(L) % 16 == 0 &&
+                   (codes == nullptr || reinterpret_cast<uintptr_t>(codes) % 8 == 0);
+  if (nd1) {
+    const dim3 grid(static_cast<unsigned>((dd.K + MG_COLS - 1) / MG_COLS), static_cast<unsigned>(dd.N / mg_rows));
+#define QA_MG(OT, BB, RR)                                                                                        \
+  {                                                                                                              \
+    const size_t smem = codes != nullptr ? static_cast<size_t>(mg_rows) * MG_COLS * BB / 8 : 0;                 \
+    cudaFuncSetAttribute(k_merge_nd1<OT, BB, RR>, cudaFuncAttributeMaxDynamicSharedMemorySize,                    \
+                         static_cast<int>(smem));                                                                 \
+    k_merge_nd1<OT, BB, RR><<<grid, 256, smem, s>>>(L, Gd, md, dd.N, dd.K, mg_rows, codes, scale, offset,         \
+                                                   static_cast<OT*>(out));                                        \
+  }
+#define QA_MG_R(OT, BB) \
+  if (R == 8)           \
+    QA_MG(OT, BB, 8)    \
+  else                  \
+    QA_MG(OT, BB, 16)
+    if (out_dtype == QA_F32) {
+      if (bits == 4) {
+        QA_MG_R(float, 4)
+      } else {
+        QA_MG_R(float, 8)
+      }
+    } else {
+      if (bits == 4) {
+        QA_MG_R(__nv_bfloat16, 4)
+      } else {
+        QA_MG_R(__nv_bfloat16, 8)
+      }
+    }
+#undef QA_MG_R
+#undef QA_MG
+    return cudaGetLastError();
+  }
   if (out_dtype == QA_F32)
     k_last_full<float><<<grid_for(total, 256), 256, 0, s>>>(L, Gd, H, JP, dd.r[last], dd.m[last], dd.n[last], codes,
                                                             bits, scale, offset, static_cast<float*>(out));
