@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-merge", action="store_true")
     ap.add_argument("--no-group", action="store_true", help="run every linear on its own (A/B of the shared x pass)")
     return ap.parse_args()
 
@@ -223,6 +224,53 @@ def run_reference_arm(args):
 
 
 # ----------------------------------------------------------------------------- GPU arm
+
+MERGE_70B = [("wq", 8192, 8192), ("wk", 1024, 8192), ("wv", 1024, 8192), ("wo", 8192, 8192),
+             ("wu", 28672, 8192), ("wg", 28672, 8192), ("wd", 8192, 28672)]
+
+
+def measure_merge(dev, sptr, hbm_gbs, iters=5):
+    """qa_merge (W' = dequantize_rows(q) + W_t, lowrank.py:245-257) over the config-5 70B set, int4, r = 8,
+    bf16 W'; one matrix resident at a time."""
+    import torch
+
+    from paper_2402_13533_b200 import _lib
+    from paper_2402_13533_b200.linear import TTSpec
+    from paper_2402_13533_b200.quant import quantize_rows
+
+    lib = _lib.lib()
+    g = torch.Generator(device=dev).manual_seed(7)
+    tot_ms, tot_bytes = 0.0, 0.0
+    for name, n, k in MERGE_70B:
+        w = torch.randn((n, k), generator=g, device=dev) * 0.02
+        q = quantize_rows(w, 4)
+        del w
+        spec = TTSpec.for_shape(n, k, 8)
+        cores = [torch.randn(spec.core_shape(i), generator=g, device=dev) * 0.01 for i in range(spec.d)]
+        wc, ttc = q.as_c(), spec.as_c(cores)
+        wsm = torch.empty(max(lib.qa_merge_workspace_bytes(ctypes.byref(ttc)), 16), dtype=torch.uint8, device=dev)
+        out = torch.empty((n, k), dtype=torch.bfloat16, device=dev)
+
+        def run():
+            _lib.check(lib.qa_merge(ctypes.byref(wc), ctypes.byref(ttc), out.data_ptr(), _lib.QA_BF16,
+                                    wsm.data_ptr(), wsm.numel(), sptr), "qa_merge")
+
+        run()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(iters):
+            run()
+        e1.record()
+        torch.cuda.synchronize(dev)
+        tot_ms += e0.elapsed_time(e1) / iters
+        tot_bytes += n * k * 0.5 + n * k * 2 + 8 * n + 4 * spec.param_count()
+        del q, out, wsm, cores
+    gbs = tot_bytes / tot_ms / 1e6
+    return {"set": "llama2-70b linears (q/o 8192^2, k/v 1024x8192, gate/up 28672x8192, down 8192x28672), int4, "
+                   "TT r=8, bf16 W'", "ms": tot_ms, "bytes": tot_bytes, "achieved_gbs": gbs,
+            "frac_of_hbm": gbs / hbm_gbs, "kernels": "k_prefix_d3 + k_merge_nd1"}
+
 
 
 def main():
@@ -513,6 +561,12 @@ def main():
                "d2h_bytes_per_step": int(d2h), "steps": k_e2e,
                "note": "C-ABI calls on pinned host inputs; H2D of step i+1 overlaps compute of step i"}
 
+    # the merge kernel (north star step 6) on BASELINE config 5's 70B linear set (int4, TT r = 8), outside
+    # the timed region: algorithmic bytes = codes in + bf16 W' out, CUDA events, warm
+    merge = None
+    if rank == 0 and not args.no_merge:
+        merge = measure_merge(dev, sptr, peaks["hbm_gbs"])
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = run_cpu_baseline(cfg)
@@ -522,7 +576,7 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "int8 (u8xu8->s32) GEMM + bf16", "data": "synthetic",
-            "config": desc, "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
+            "config": desc, "roofline": roofline, "kernels": kernels, "merge": merge, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches * args.steps), "gpu_launches_per_step": int(launches), "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
