@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(256) k_last_full(const float* __restrict__ L, 
 // the lane's L[h, col, :] pairs held in registers (packed FFMA2 over column pairs) and the code words
 // of RU rows loaded before any is used.  Dequantisation is one fp32 FMA (error < 1 ulp of fp32 against
 // the reference's fp64 route, quant.py:102-105 — well inside the merge's 1e-5 tolerance).
-constexpr int MG_COLS = 256;
+constexpr int MG_COLS = 256, MG_GROUPS = 1;  // 4 groups measured slower (243 vs 216 us, 70B gate)
 
 template <typename OutT, int BITS, int R>
 __global__ void __launch_bounds__(256, 2) k_merge_nd1(const float* __restrict__ L, const float* __restrict__ Gd,
@@ -349,14 +349,20 @@ __global__ void __launch_bounds__(256, 2) k_merge_nd1(const float* __restrict__ 
   const int64_t h = r0 / md;  // MG_ROWS divides md: one h-block per CTA
   const int i0 = static_cast<int>(r0 - h * md);
   const int64_t cld = BITS == 8 ? K : (K + 1) / 2;
-  if (codes != nullptr) {  // the whole code tile in flight at once (cp.async), consumed from shared memory
+  // the whole code tile in flight at once (cp.async, MG_GROUPS commit groups of rows), consumed from
+  // shared memory group by group while the later groups are still landing
+  const int grows = MG_ROWS / MG_GROUPS;
+  {
     const int64_t cb0 = BITS == 8 ? c0 : c0 / 2;
-    for (int q = threadIdx.x; q < MG_ROWS * (CB / 16); q += 256) {
-      const int r = q / (CB / 16), ch = q % (CB / 16);
-      const bool ok = r0 + r < N && cb0 + ch * 16 + 16 <= cld;
-      cp_async16(mg_codes + r * CB + ch * 16, ok ? codes + (r0 + r) * cld + cb0 + ch * 16 : codes, ok);
+    for (int gq = 0; gq < MG_GROUPS; ++gq) {
+      if (codes != nullptr)
+        for (int q = threadIdx.x; q < grows * (CB / 16); q += 256) {
+          const int r = gq * grows + q / (CB / 16), ch = q % (CB / 16);
+          const bool ok = r0 + r < N && cb0 + ch * 16 + 16 <= cld;
+          cp_async16(mg_codes + r * CB + ch * 16, ok ? codes + (r0 + r) * cld + cb0 + ch * 16 : codes, ok);
+        }
+      cp_async_commit();
     }
-    cp_async_commit();
   }
   for (int q = threadIdx.x; q < R * MG_ROWS; q += 256) gs[q / MG_ROWS][q % MG_ROWS] = Gd[(q / MG_ROWS) * md + i0 + q % MG_ROWS];
   for (int q = threadIdx.x; q < MG_ROWS; q += 256) {
@@ -384,12 +390,14 @@ __global__ void __launch_bounds__(256, 2) k_merge_nd1(const float* __restrict__ 
       for (int q = 0; q < 4; ++q) lp[b][q] = f2pack(lv[2 * q][b], lv[2 * q + 1][b]);
   }
   OutT* obase = out + col;
-  cp_async_wait<0>();
-  __syncthreads();
-  if (col >= K) return;
+  const bool active = col < K;
   for (int rl = warp; rl < MG_ROWS; rl += 8) {
+    if (rl % grows < 8) {  // first row of a group for this warp: its codes have landed for every thread
+      cp_async_wait_dyn(MG_GROUPS - 1 - rl / grows);
+      __syncthreads();
+    }
     const int64_t row = r0 + rl;
-    if (row >= N) break;
+    if (row >= N || !active) continue;
     unsigned long long acc[4] = {0ull, 0ull, 0ull, 0ull};
 #pragma unroll
     for (int b = 0; b < R; ++b) {
