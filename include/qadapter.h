@@ -94,6 +94,11 @@ QA_API int qa_quantize_rows(const void* w, int w_dtype, int64_t rows, int64_t co
  * transpose != 0 writes outᵀ ([cols, rows], row stride ld_out). */
 QA_API int qa_dequantize_rows(const qa_qweight* w, void* out, int out_dtype, int64_t ld_out, int transpose, void* stream);
 
+/* rowsum[r] = Σ_c code[r, c] of a stored code grid (reference layout, row stride = cols or
+ * ceil(cols/2) bytes): the qa_qweight.rowsum term for bases loaded from a checkpoint's u8q / u4q
+ * entries (checkpoint.py:64-70, 186-197) instead of quantised on the device. */
+QA_API int qa_code_rowsum(const uint8_t* codes, int64_t rows, int64_t cols, int bits, int32_t* rowsum, void* stream);
+
 /* Workspace for qa_linear_forward / qa_linear_backward at `tokens` tokens. */
 QA_API size_t qa_linear_workspace_bytes(const qa_qweight* w, const qa_tt* tt, int64_t tokens);
 

@@ -28,6 +28,7 @@ EXPORTS = (
     "qa_last_error",
     "qa_quantize_rows",
     "qa_dequantize_rows",
+    "qa_code_rowsum",
     "qa_linear_workspace_bytes",
     "qa_linear_forward",
     "qa_linear_backward",
@@ -84,6 +85,8 @@ def _declare(lib):
     lib.qa_quantize_rows.argtypes = [P, I32, I64, I64, I64, I32, P, I64, I64, P, P, P, P, P]
     lib.qa_dequantize_rows.restype = I32
     lib.qa_dequantize_rows.argtypes = [PW, P, I32, I64, I32, P]
+    lib.qa_code_rowsum.restype = I32
+    lib.qa_code_rowsum.argtypes = [P, I64, I64, I32, P, P]
     lib.qa_linear_workspace_bytes.restype = SZ
     lib.qa_linear_workspace_bytes.argtypes = [PW, PT, I64]
     lib.qa_linear_forward.restype = I32

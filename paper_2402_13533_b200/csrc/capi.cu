@@ -280,6 +280,19 @@ int qa_dequantize_rows(const qa_qweight* w, void* out, int out_dtype, int64_t ld
                      "dequantize");
 }
 
+int qa_code_rowsum(const uint8_t* codes, int64_t rows, int64_t cols, int bits, int32_t* rowsum, void* stream) {
+  if (bits != 4 && bits != 8) {
+    set_error("bits must be 4 or 8, got %d", bits);
+    return QA_ERR_BITS;
+  }
+  if (codes == nullptr || rowsum == nullptr || rows < 0 || cols < 1) {
+    set_error("qa_code_rowsum: bad argument");
+    return QA_ERR_ARG;
+  }
+  return cuda_status(launch_code_rowsum(codes, rows, cols, bits, rowsum, static_cast<cudaStream_t>(stream)),
+                     "code rowsum");
+}
+
 size_t qa_linear_workspace_bytes(const qa_qweight* w, const qa_tt* tt, int64_t tokens) {
   if (check_weight(w) != QA_OK) return 0;
   TTDims dd;

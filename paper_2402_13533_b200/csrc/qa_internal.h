@@ -65,6 +65,9 @@ cudaError_t launch_tt_last_full(const TTDims& dd, const float* L, const float* G
 cudaError_t launch_sum_partials(const float* partial, int nparts, int64_t numel, float* out, bool accumulate,
                                 cudaStream_t s);
 
+cudaError_t launch_code_rowsum(const uint8_t* codes, int64_t rows, int64_t cols, int bits, int32_t* rowsum,
+                               cudaStream_t s);
+
 // ------------------------------------------------------------ fast TT family (tt_fast.cu)
 bool fast_tt_supported(int J1, int R1);
 size_t g1i_floats(int64_t K, int J1, int R1);  // workspace for the interleaved G1 copy

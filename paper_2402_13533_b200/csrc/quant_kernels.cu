@@ -318,6 +318,34 @@ cudaError_t launch_unpack_pad(const uint8_t* codes, int64_t rows, int64_t cols, 
   return cudaGetLastError();
 }
 
+// Σ codes per row of a stored code grid (reference layout; 4-bit: low nibble = even column), for
+// bases whose codes arrive from a checkpoint rather than from qa_quantize_rows.
+__global__ void __launch_bounds__(256) k_code_rowsum(const uint8_t* __restrict__ codes, int64_t rows, int64_t cols,
+                                                     int bits, int32_t* __restrict__ rowsum) {
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t ldc = bits == 8 ? cols : (cols + 1) / 2;
+  const uint8_t* r = codes + row * ldc;
+  int32_t sum = 0;
+  for (int64_t c = lane; c < ldc; c += 32) {
+    const uint32_t b = r[c];
+    sum += bits == 8 ? static_cast<int32_t>(b) : static_cast<int32_t>((b & 0xFu) + (2 * c + 1 < cols ? (b >> 4) : 0u));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  if (lane == 0) rowsum[row] = sum;
+}
+
+cudaError_t launch_code_rowsum(const uint8_t* codes, int64_t rows, int64_t cols, int bits, int32_t* rowsum,
+                               cudaStream_t s) {
+  if (rows == 0) return cudaSuccess;
+  LaunchScope scope(kQuantize, double(rows) * (bits == 8 ? cols : (cols + 1) / 2) + 4.0 * rows, s);
+  count_launches(1);
+  k_code_rowsum<<<static_cast<unsigned>((rows + 7) / 8), 256, 0, s>>>(codes, rows, cols, bits, rowsum);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_to_bf16_pad(const void* in, int in_dtype, int64_t rows, int64_t cols, __nv_bfloat16* out,
                                int64_t ld_out, cudaStream_t s, __nv_bfloat16* out_lo) {
   if (rows == 0) return cudaSuccess;
