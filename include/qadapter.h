@@ -165,6 +165,17 @@ QA_API int qa_group_backward(int n, const qa_qweight* const* w, const qa_tt* con
                              float* const* const* dcores, int accumulate, const void* const* saved,
                              const size_t* saved_bytes, void* workspace, size_t workspace_bytes, void* stream);
 
+/* AdamW over a flat buffer of n adapter parameters (trainer.py:84-121 adamw_step): float64 masters and
+ * moments updated with the reference's exact sequence of float64 operations (no contraction), float32
+ * working copies rounded from the masters; step = the optimizer step after increment (t >= 1). */
+QA_API int qa_adamw_step(float* params, double* master, double* m, double* v, const float* grads, int64_t n,
+                         double lr, double beta1, double beta2, double eps, double weight_decay, int64_t step,
+                         void* stream);
+/* flags[s] |= 1 when grads[seg_offsets[s] .. seg_offsets[s+1]) holds a NaN / Inf (the reference raises
+ * naming the first such tensor, trainer.py:107-108); flags must be zeroed by the caller. */
+QA_API int qa_nonfinite_segments(const float* grads, const int64_t* seg_offsets, int nseg, int32_t* flags,
+                                 void* stream);
+
 /* Workspace for qa_merge / qa_tt_materialize. */
 QA_API size_t qa_merge_workspace_bytes(const qa_tt* tt);
 

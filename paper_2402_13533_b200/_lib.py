@@ -38,6 +38,8 @@ EXPORTS = (
     "qa_group_workspace_bytes",
     "qa_group_forward",
     "qa_group_backward",
+    "qa_adamw_step",
+    "qa_nonfinite_segments",
     "qa_merge_workspace_bytes",
     "qa_merge",
     "qa_tt_materialize",
@@ -108,6 +110,11 @@ def _declare(lib):
     lib.qa_group_backward.restype = I32
     lib.qa_group_backward.argtypes = [I32, ctypes.POINTER(PW), ctypes.POINTER(PT), P, I32, PP, I32, I64, PP,
                                       ctypes.POINTER(PP), I32, PP, ctypes.POINTER(SZ), P, SZ, P]
+    D = ctypes.c_double
+    lib.qa_adamw_step.restype = I32
+    lib.qa_adamw_step.argtypes = [P, P, P, P, P, I64, D, D, D, D, D, I64, P]
+    lib.qa_nonfinite_segments.restype = I32
+    lib.qa_nonfinite_segments.argtypes = [P, P, I32, P, P]
     lib.qa_merge_workspace_bytes.restype = SZ
     lib.qa_merge_workspace_bytes.argtypes = [PT]
     lib.qa_merge.restype = I32

@@ -280,6 +280,27 @@ int qa_dequantize_rows(const qa_qweight* w, void* out, int out_dtype, int64_t ld
                      "dequantize");
 }
 
+int qa_adamw_step(float* params, double* master, double* m, double* v, const float* grads, int64_t n, double lr,
+                  double beta1, double beta2, double eps, double weight_decay, int64_t step, void* stream) {
+  if ((n > 0 && (params == nullptr || master == nullptr || m == nullptr || v == nullptr || grads == nullptr)) ||
+      n < 0 || step < 1 || !(beta1 > 0.0 && beta1 < 1.0) || !(beta2 > 0.0 && beta2 < 1.0) || !(lr > 0.0)) {
+    set_error("qa_adamw_step: bad argument");
+    return QA_ERR_ARG;
+  }
+  return cuda_status(launch_adamw(params, master, m, v, grads, n, lr, beta1, beta2, eps, weight_decay, step,
+                                  static_cast<cudaStream_t>(stream)),
+                     "adamw");
+}
+
+int qa_nonfinite_segments(const float* grads, const int64_t* seg_offsets, int nseg, int32_t* flags, void* stream) {
+  if (nseg < 0 || (nseg > 0 && (grads == nullptr || seg_offsets == nullptr || flags == nullptr))) {
+    set_error("qa_nonfinite_segments: bad argument");
+    return QA_ERR_ARG;
+  }
+  return cuda_status(launch_seg_nonfinite(grads, seg_offsets, nseg, flags, static_cast<cudaStream_t>(stream)),
+                     "nonfinite segments");
+}
+
 int qa_code_rowsum(const uint8_t* codes, int64_t rows, int64_t cols, int bits, int32_t* rowsum, void* stream) {
   if (bits != 4 && bits != 8) {
     set_error("bits must be 4 or 8, got %d", bits);

@@ -68,6 +68,11 @@ cudaError_t launch_sum_partials(const float* partial, int nparts, int64_t numel,
 cudaError_t launch_code_rowsum(const uint8_t* codes, int64_t rows, int64_t cols, int bits, int32_t* rowsum,
                                cudaStream_t s);
 
+// AdamW (optim.cu)
+cudaError_t launch_adamw(float* params, double* master, double* m, double* v, const float* g, int64_t n, double lr,
+                         double b1, double b2, double eps, double wd, int64_t step, cudaStream_t s);
+cudaError_t launch_seg_nonfinite(const float* g, const int64_t* seg, int nseg, int32_t* flags, cudaStream_t s);
+
 // ------------------------------------------------------------ fast TT family (tt_fast.cu)
 bool fast_tt_supported(int J1, int R1);
 size_t g1i_floats(int64_t K, int J1, int R1);  // workspace for the interleaved G1 copy
