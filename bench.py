@@ -561,6 +561,38 @@ def main():
                "d2h_bytes_per_step": int(d2h), "steps": k_e2e,
                "note": "C-ABI calls on pinned host inputs; H2D of step i+1 overlaps compute of step i"}
 
+    # decode-size forwards (KV-cached decoding, transformer.py:1043-1080): 1 and 8 tokens through the 7
+    # linears; HBM-bound on the weight codes (gemv.cu)
+    decode = None
+    if rank == 0 and not args.no_merge:
+        decode = {}
+        for td in (1, 8):
+            xd = {kd: torch.randn((td, d), generator=dgen, device=dev).to(torch.bfloat16) for kd, d in INPUT_DIMS.items()}
+            yd = {nm: torch.empty((td, n), dtype=torch.bfloat16, device=dev) for nm, n, _, _ in LINEARS_7B}
+
+            def dstep():
+                for name, _, _, kind in LINEARS_7B:
+                    m = mats[name]
+                    _lib.check(lib.qa_linear_forward(ctypes.byref(m["wc"]), ctypes.byref(m["ttc"]), xd[kind].data_ptr(),
+                                                     BF16, td, yd[name].data_ptr(), None, None, None, ws.data_ptr(),
+                                                     ws_bytes, sptr), "decode forward")
+
+            for _ in range(5):
+                dstep()
+            torch.cuda.synchronize(dev)
+            d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            d0.record(stream)
+            for _ in range(50):
+                dstep()
+            d1.record(stream)
+            torch.cuda.synchronize(dev)
+            ms = d0.elapsed_time(d1) / 50
+            wbytes = sum(mats[nm]["q"].codes.numel() + 8 * n for nm, n, _, _ in LINEARS_7B)
+            decode[f"tokens_{td}"] = {"ms_per_step": ms, "tokens_per_s": td / (ms / 1e3),
+                                      "weight_gbs": wbytes / ms / 1e6, "frac_of_hbm": wbytes / ms / 1e6 / peaks["hbm_gbs"]}
+        decode["note"] = ("forward of the 7 linears for 1 / 8 tokens (int8 codes + TT adapter), dp4a matrix-vector pass; "
+                          "weight_gbs counts the code bytes read per step")
+
     # the merge kernel (north star step 6) on BASELINE config 5's 70B linear set (int4, TT r = 8), outside
     # the timed region: algorithmic bytes = codes in + bf16 W' out, CUDA events, warm
     merge = None
@@ -576,7 +608,7 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "int8 (u8xu8->s32) GEMM + bf16", "data": "synthetic",
-            "config": desc, "roofline": roofline, "kernels": kernels, "merge": merge, "cpu_baseline": cpu, "e2e": e2e,
+            "config": desc, "roofline": roofline, "kernels": kernels, "decode": decode, "merge": merge, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches * args.steps), "gpu_launches_per_step": int(launches), "clocks": clocks,
         }
         print(json.dumps(line), flush=True)

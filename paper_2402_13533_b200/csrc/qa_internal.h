@@ -68,6 +68,13 @@ cudaError_t launch_sum_partials(const float* partial, int nparts, int64_t numel,
 cudaError_t launch_code_rowsum(const uint8_t* codes, int64_t rows, int64_t cols, int bits, int32_t* rowsum,
                                cudaStream_t s);
 
+// decode-size forward (gemv.cu): 1..8 tokens against the stored codes (dp4a), GEMM-identical epilogue
+bool gemv_ok(int64_t T, int64_t K, int bits);
+cudaError_t launch_gemv(const uint8_t* xc, int64_t ldx, int64_t T, const float* sx, const float* ox,
+                        const int32_t* rsx, const uint8_t* wc, int64_t N, int64_t K, int bits, const float* ws,
+                        const float* wo, const int32_t* wrs, const float* zf, int K2, const __nv_bfloat16* V,
+                        int64_t ldv, const float* addend, __nv_bfloat16* out, float* out32, cudaStream_t s);
+
 // AdamW (optim.cu)
 cudaError_t launch_adamw(float* params, double* master, double* m, double* v, const float* g, int64_t n, double lr,
                          double b1, double b2, double eps, double wd, int64_t step, cudaStream_t s);

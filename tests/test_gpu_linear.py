@@ -300,3 +300,26 @@ def test_shared_input_group_matches_members(ns, K, T, r):
     assert sorted(g_grads) == sorted(r_grads)
     for k in g_grads:
         assert torch.equal(g_grads[k], r_grads[k]), k
+
+
+@pytest.mark.parametrize("N,K,bits,r,spec", [(1024, 512, 8, 8, None), (768, 1024, 4, 8, None),
+                                             (512, 256, 8, 8, "lora"), (512, 512, 8, 8, "base"),
+                                             (1024, 1024, 8, 8, "config1")])
+def test_decode_sized_batches(N, K, bits, r, spec):
+    """1..8 tokens (KV-cached decoding, transformer.py:1043-1080) run the dp4a matrix-vector pass
+    (gemv.cu): exact int32 products and the GEMM's epilogue, so y matches the oracle and the tcgen05
+    path on the same rows."""
+    if spec == "lora":
+        spec = L.TTSpec.lora(N, K, r)
+    elif spec == "config1":
+        spec = L.TTSpec.for_shape(N, K, r)
+    q, oq, x, xs, spec_, cores, cores_np = _case(N, K, 9, bits, r, 61, None if spec in (None, "base") else spec)
+    adapter = None if spec == "base" else (spec_, cores)
+    big = L.linear_forward(q, adapter, x)  # 9 tokens: the tensor-core path
+    for T in (1, 2, 3, 5, 8):
+        y = L.linear_forward(q, adapter, x[:T])
+        ref = O.qa_linear_forward(xs[:T], oq, cores_np if adapter is not None else None)
+        assert O.rel_err(_np(y), ref["y"]) <= TOL_BF16, T
+        assert O.rel_err(_np(y), _np(big[:T])) <= 2 ** -7, T
+        y32 = L.linear_forward(q, adapter, x[:T].float())
+        assert O.rel_err(_np(y32), ref["y"]) <= 1e-4, T
