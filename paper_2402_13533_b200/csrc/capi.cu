@@ -358,14 +358,34 @@ int linear_forward_impl(const qa_qweight* w, const qa_tt* tt, const void* x, int
 
   GemmExt ext;
   const bool x_vec = reinterpret_cast<uintptr_t>(x) % 16 == 0;
-  // decode-size batches (KV-cached decoding, transformer.py:1043-1080) take the HBM-bound dp4a pass
-  const bool gemv = gemv_ok(T, K, w->bits) && acc_i32 == nullptr && y2_f32 == nullptr &&
-                    (pd == nullptr || (P.fast && x_vec));
-  float* zf_out = z1_save != nullptr ? z1_save : (gemv && pd != nullptr ? P.zf : nullptr);
+  // decode-size batches (KV-cached decoding, transformer.py:1043-1080): two launches — the act-quant /
+  // adapter prologue and the HBM-bound dp4a matrix-vector pass over the stored codes (gemv.cu)
+  if (gemv_ok(T, K, w->bits) && acc_i32 == nullptr && y2_f32 == nullptr &&
+      (pd == nullptr || (P.fast && x_vec && x_dtype == QA_BF16 && P.C <= 32))) {
+    const float* zl = nullptr;
+    const float* gl = nullptr;
+    int64_t ldz = 0;
+    if (pd == nullptr) {
+      QA_TRY_CUDA(launch_quantize_rows(x, x_dtype, T, K, K, 8, P.xcodes, P.Kp, P.Kp, P.sx, P.ox, P.rsx, nullptr, s),
+                  "act quantize");
+    } else {
+      float* zlw = P.fd == 3 ? P.z2 : (z1_save != nullptr ? z1_save : P.zf);
+      ldz = P.fd == 3 ? int64_t(P.H) * P.C : P.K2;
+      QA_TRY_CUDA(launch_decode_prep(x, T, K, P.xcodes, P.Kp, P.sx, P.ox, P.rsx, tt->cores[0], P.J1, P.R1,
+                                     tt->cores[1], P.fd, P.H, P.C, z1_save, zlw, ldz, s),
+                  "decode prologue");
+      zl = zlw;
+      gl = tt->cores[P.fd - 1];
+    }
+    return cuda_status(launch_gemv(P.xcodes, P.Kp, T, P.sx, P.ox, P.rsx, w->codes, N, K, w->bits, w->scale,
+                                   w->offset, w->rowsum, zl, ldz, gl, P.M, P.C, nullptr,
+                                   static_cast<__nv_bfloat16*>(y), y_f32, s),
+                       "decode gemv");
+  }
   if (P.fast && x_vec) {
     // (2)+(4a) one pass over x: bit-exact per-token act-quant + Z1 = first TT stage
     QA_TRY_CUDA(launch_actquant_z1(x, x_dtype, T, K, true, P.xcodes, P.Kp, P.sx, P.ox, P.rsx, tt->cores[0], P.J1,
-                                   P.R1, gemv ? nullptr : P.zb, P.K2p, zf_out, P.g1i, s),
+                                   P.R1, P.zb, P.K2p, z1_save, P.g1i, s),
                 "act quantize + TT stage 1");
     // (4b) V = cores 2..d contracted; y2 = Z1 · Vᵀ runs as extension k-blocks of the GEMM
     QA_TRY_CUDA(launch_build_v(P.fd, P.R1, P.H, P.J1, P.C, P.M, tt->cores[1], P.fd == 3 ? tt->cores[2] : nullptr,
@@ -380,12 +400,6 @@ int linear_forward_impl(const qa_qweight* w, const qa_tt* tt, const void* x, int
     // (2) per-token activation quantisation: quantize_rows on x[T, K] (codes padded to Kp with zeros)
     QA_TRY_CUDA(launch_quantize_rows(x, x_dtype, T, K, K, 8, P.xcodes, P.Kp, P.Kp, P.sx, P.ox, P.rsx, nullptr, s),
                 "act quantize");
-  }
-  if (gemv) {
-    return cuda_status(launch_gemv(P.xcodes, P.Kp, T, P.sx, P.ox, P.rsx, w->codes, N, K, w->bits, w->scale,
-                                   w->offset, w->rowsum, zf_out, P.K2, pd != nullptr ? P.v : nullptr, P.K2p,
-                                   nullptr, static_cast<__nv_bfloat16*>(y), y_f32, s),
-                       "decode gemv");
   }
   int st = QA_OK;
   const uint8_t* wop = weight_operand(w, P, s, &st);

@@ -12,7 +12,7 @@ namespace qa {
 
 namespace {
 
-constexpr int GV_WARPS = 8, GV_RPW = 4;  // warps per CTA, rows per warp in flight
+constexpr int GV_WARPS = 8, GV_RPW = 2, GV_UNR = 4;  // warps per CTA, rows per warp, chunks in flight per row
 
 template <int M, int BITS>
 __global__ void __launch_bounds__(GV_WARPS * 32) k_gemv(const uint8_t* __restrict__ xc, int64_t ldx, int T,
@@ -21,8 +21,8 @@ __global__ void __launch_bounds__(GV_WARPS * 32) k_gemv(const uint8_t* __restric
                                                         const uint8_t* __restrict__ wc, int64_t N, int64_t K,
                                                         const float* __restrict__ ws, const float* __restrict__ wo,
                                                         const int32_t* __restrict__ wrs,
-                                                        const float* __restrict__ zf, int K2,
-                                                        const __nv_bfloat16* __restrict__ V, int64_t ldv,
+                                                        const float* __restrict__ zl, int64_t ldz,
+                                                        const float* __restrict__ Gl, int64_t Ml, int Cl,
                                                         const float* __restrict__ addend,
                                                         __nv_bfloat16* __restrict__ out, float* __restrict__ out32) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -34,11 +34,20 @@ __global__ void __launch_bounds__(GV_WARPS * 32) k_gemv(const uint8_t* __restric
   for (int r = 0; r < GV_RPW; ++r)
 #pragma unroll
     for (int t = 0; t < M; ++t) acc[r][t] = 0u;
-  for (int64_t q = lane; q < nchunk; q += 32) {
-    uint4 w[GV_RPW];
+  for (int64_t q0 = lane; q0 < nchunk; q0 += 32 * GV_UNR) {
+    uint4 wu[GV_UNR][GV_RPW];
 #pragma unroll
-    for (int r = 0; r < GV_RPW; ++r)
-      w[r] = row0 + r < N ? __ldg(reinterpret_cast<const uint4*>(wc + (row0 + r) * ldw) + q) : make_uint4(0, 0, 0, 0);
+    for (int u = 0; u < GV_UNR; ++u)
+#pragma unroll
+      for (int r = 0; r < GV_RPW; ++r)
+        wu[u][r] = (row0 + r < N && q0 + 32 * u < nchunk)
+                       ? __ldg(reinterpret_cast<const uint4*>(wc + (row0 + r) * ldw) + q0 + 32 * u)
+                       : make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int u = 0; u < GV_UNR; ++u) {
+    const int64_t q = q0 + 32 * u;
+    if (q >= nchunk) break;
+    const uint4(&w)[GV_RPW] = wu[u];
 #pragma unroll
     for (int t = 0; t < M; ++t) {
       if (t >= T) break;
@@ -77,24 +86,24 @@ __global__ void __launch_bounds__(GV_WARPS * 32) k_gemv(const uint8_t* __restric
         }
       }
     }
+    }
   }
-  // adapter: y2[t, n] = Σ_c Z1[t, c] (V_hi[n, c] + V_lo[n, c]), lanes over c (K2 <= 64)
+  // adapter: y2[t, n] = Σ_b Zlast[t, h, b] Glast[b, i], n = h Ml + i (the last TT core, rank Cl <= 32)
   float y2[GV_RPW][M];
 #pragma unroll
   for (int r = 0; r < GV_RPW; ++r)
 #pragma unroll
     for (int t = 0; t < M; ++t) y2[r][t] = 0.f;
-  if (V != nullptr) {
-    for (int c = lane; c < K2; c += 32) {
+  if (Gl != nullptr && lane < Cl) {
 #pragma unroll
-      for (int r = 0; r < GV_RPW; ++r) {
-        if (row0 + r >= N) break;
-        const __nv_bfloat16* vr = V + (row0 + r) * ldv;
-        const float v = __bfloat162float(vr[c]) + __bfloat162float(vr[2 * K2 + c]);
+    for (int r = 0; r < GV_RPW; ++r) {
+      const int64_t n = row0 + r;
+      if (n >= N) break;
+      const int64_t h = n / Ml, i = n - h * Ml;
+      const float g = __ldg(Gl + lane * Ml + i);
 #pragma unroll
-        for (int t = 0; t < M; ++t)
-          if (t < T) y2[r][t] = fmaf(zf[t * K2 + c], v, y2[r][t]);
-      }
+      for (int t = 0; t < M; ++t)
+        if (t < T) y2[r][t] = __ldg(zl + t * ldz + h * Cl + lane) * g;
     }
   }
 #pragma unroll
@@ -148,8 +157,8 @@ bool gemv_ok(int64_t T, int64_t K, int bits) {
 
 cudaError_t launch_gemv(const uint8_t* xc, int64_t ldx, int64_t T, const float* sx, const float* ox,
                         const int32_t* rsx, const uint8_t* wc, int64_t N, int64_t K, int bits, const float* ws,
-                        const float* wo, const int32_t* wrs, const float* zf, int K2, const __nv_bfloat16* V,
-                        int64_t ldv, const float* addend, __nv_bfloat16* out, float* out32, cudaStream_t s) {
+                        const float* wo, const int32_t* wrs, const float* zl, int64_t ldz, const float* Gl,
+                        int64_t Ml, int Cl, const float* addend, __nv_bfloat16* out, float* out32, cudaStream_t s) {
   if (T == 0 || N == 0) return cudaSuccess;
   LaunchScope scope(kGemmI8, 2.0 * double(T) * N * K, s);
   count_launches(1);
@@ -158,10 +167,10 @@ cudaError_t launch_gemv(const uint8_t* xc, int64_t ldx, int64_t T, const float* 
   {                                                                                                                 \
     if (bits == 8)                                                                                                  \
       k_gemv<MM, 8><<<grid, GV_WARPS * 32, 0, s>>>(xc, ldx, static_cast<int>(T), sx, ox, rsx, wc, N, K, ws, wo, wrs, \
-                                                   zf, K2, V, ldv, addend, out, out32);                             \
+                                                   zl, ldz, Gl, Ml, Cl, addend, out, out32);                        \
     else                                                                                                            \
       k_gemv<MM, 4><<<grid, GV_WARPS * 32, 0, s>>>(xc, ldx, static_cast<int>(T), sx, ox, rsx, wc, N, K, ws, wo, wrs, \
-                                                   zf, K2, V, ldv, addend, out, out32);                             \
+                                                   zl, ldz, Gl, Ml, Cl, addend, out, out32);                        \
   }
   if (T == 1)
     QA_GV(1)

@@ -72,8 +72,12 @@ cudaError_t launch_code_rowsum(const uint8_t* codes, int64_t rows, int64_t cols,
 bool gemv_ok(int64_t T, int64_t K, int bits);
 cudaError_t launch_gemv(const uint8_t* xc, int64_t ldx, int64_t T, const float* sx, const float* ox,
                         const int32_t* rsx, const uint8_t* wc, int64_t N, int64_t K, int bits, const float* ws,
-                        const float* wo, const int32_t* wrs, const float* zf, int K2, const __nv_bfloat16* V,
-                        int64_t ldv, const float* addend, __nv_bfloat16* out, float* out32, cudaStream_t s);
+                        const float* wo, const int32_t* wrs, const float* zl, int64_t ldz, const float* Gl,
+                        int64_t Ml, int Cl, const float* addend, __nv_bfloat16* out, float* out32, cudaStream_t s);
+// decode prologue (tt_fast.cu): act-quant of T <= 8 bf16 rows + Z1 + the last core's input Zlast
+cudaError_t launch_decode_prep(const void* x, int64_t T, int64_t K, uint8_t* codes, int64_t ldc, float* sx, float* ox,
+                               int32_t* rsx, const float* G1, int J1, int R1, const float* G2, int d, int H, int C,
+                               float* z1out, float* zlast, int64_t ldz, cudaStream_t s);
 
 // AdamW (optim.cu)
 cudaError_t launch_adamw(float* params, double* master, double* m, double* v, const float* g, int64_t n, double lr,

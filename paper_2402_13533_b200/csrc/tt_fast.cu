@@ -1552,6 +1552,175 @@ __global__ void __launch_bounds__(AQR_W * 32, 1) k_aq_ring(const __nv_bfloat16* 
   if (mygroups > 0) finish_sums(mygroups - 1);
 }
 
+// ---------------------------------------------------------------------------------------------
+// Decode-size prologue (1..8 tokens, KV-cached decoding): one CTA per token row does the bit-exact
+// act-quant (aq_codes8b + fp64 replay), Z1 = x·G1 in fp32 and the last core's input Zlast (d = 3:
+// Z2 = Z1·Gm, [H][C]; d = 2: Z1), so the matrix-vector pass (gemv.cu) needs no V / fragment build.
+template <int J1, int R1>
+__global__ void __launch_bounds__(1024) k_decode_prep(const __nv_bfloat16* __restrict__ x, int64_t K,
+                                                     uint8_t* __restrict__ codes, int64_t ldc, float* __restrict__ sx,
+                                                     float* __restrict__ ox, int32_t* __restrict__ rsx,
+                                                     const float* __restrict__ G1, const float* __restrict__ G2,
+                                                     int d, int H, int C, float* __restrict__ z1out,
+                                                     float* __restrict__ zlast, int64_t ldz) {
+  constexpr int K2 = J1 * R1;
+  extern __shared__ __align__(16) uint8_t dp_smem[];
+  constexpr int NW = 32;  // warps
+  __shared__ float red[NW][K2 + 1];
+  __shared__ float s_lo[NW], s_hi[NW];
+  __shared__ int32_t s_sum[NW];
+  __shared__ float z1s[K2];
+  const int t = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + t * K);
+  uint4* row = reinterpret_cast<uint4*>(dp_smem);
+  const int nchunk = static_cast<int>(K / 8);
+  __nv_bfloat162 lo2 = __floats2bfloat162_rn(INFINITY, INFINITY), hi2 = __floats2bfloat162_rn(-INFINITY, -INFINITY);
+  float z[K2];
+#pragma unroll
+  for (int i = 0; i < K2; ++i) z[i] = 0.f;
+  for (int c = tid; c < nchunk; c += NW * 32) {
+    const uint4 v = __ldg(xr + c);
+    row[c] = v;
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const __nv_bfloat162 b2 = *reinterpret_cast<const __nv_bfloat162*>(&w[i]);
+      lo2 = __hmin2(lo2, b2);
+      hi2 = __hmax2(hi2, b2);
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {  // element 8c + e: j1 = (8c + e) / J1, J = e % J1
+      const float xv = __uint_as_float((e & 1) ? (w[e >> 1] & 0xFFFF0000u) : (w[e >> 1] << 16));
+      const int64_t j1 = (8 * static_cast<int64_t>(c) + e) / J1;
+      const int J = e % J1;
+#pragma unroll
+      for (int a = 0; a < R1; ++a) z[a * J1 + J] = fmaf(xv, __ldg(G1 + j1 * R1 + a), z[a * J1 + J]);
+    }
+  }
+  float lo = fminf(__low2float(lo2), __high2float(lo2)), hi = fmaxf(__low2float(hi2), __high2float(hi2));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+#pragma unroll
+  for (int i = 0; i < K2; ++i) {
+    float v = z[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[warp][i] = v;
+  }
+  if (lane == 0) {
+    s_lo[warp] = lo;
+    s_hi[warp] = hi;
+  }
+  __syncthreads();
+  lo = s_lo[0];
+  hi = s_hi[0];
+#pragma unroll
+  for (int w2 = 1; w2 < NW; ++w2) {
+    lo = fminf(lo, s_lo[w2]);
+    hi = fmaxf(hi, s_hi[w2]);
+  }
+  if (tid < K2) {
+    float v = red[0][tid];
+#pragma unroll
+    for (int w2 = 1; w2 < NW; ++w2) v += red[w2][tid];
+    z1s[tid] = v;
+    if (z1out != nullptr) z1out[t * K2 + tid] = v;
+  }
+  // codes of this row (bracketed rule, bit-exact with quant.py:73-99)
+  const double lo64 = static_cast<double>(lo);
+  const double step64 = __ddiv_rn(__dsub_rn(static_cast<double>(hi), lo64), 255.0);
+  const bool flat = !(step64 > 0.0);
+  const float inv = flat ? 0.f : static_cast<float>(1.0 / step64);
+  const float nb = -lo * inv;
+  const bool sub = fabsf(nb) > 512.0f;  // uniform across the CTA
+  const float alo = sub ? 0.5f - kTieBand : nb + 0.5f - kTieBand, ahi = sub ? 0.5f + kTieBand : nb + 0.5f + kTieBand;
+  const unsigned long long inv2 = f2pack(inv, inv), nlo2 = f2pack(-lo, -lo), alo2 = f2pack(alo, alo),
+                           ahi2 = f2pack(ahi, ahi);
+  uint8_t* crow = codes + t * ldc;
+  uint32_t sum = 0;
+  for (int c = tid; c < nchunk; c += NW * 32) {
+    const uint4 v = row[c];
+    uint32_t c0, c1, d0, d1;
+    if (sub)
+      aq_codes8b<true>(v, inv2, alo2, ahi2, nlo2, c0, c1, d0, d1);
+    else
+      aq_codes8b<false>(v, inv2, alo2, ahi2, nlo2, c0, c1, d0, d1);
+    if (flat) c0 = c1 = d0 = d1 = 0u;
+    if (d0 != 0u) c0 = aq_replay_word(v, 0, c0, d0, lo64, step64);
+    if (d1 != 0u) c1 = aq_replay_word(v, 4, c1, d1, lo64, step64);
+    sum = __dp4a(c0, 0x01010101u, __dp4a(c1, 0x01010101u, sum));
+    *reinterpret_cast<uint2*>(crow + 8 * static_cast<int64_t>(c)) = make_uint2(c0, c1);
+  }
+  for (int64_t k = K + tid; k < ldc; k += NW * 32) crow[k] = 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  if (lane == 0) s_sum[warp] = static_cast<int32_t>(sum);
+  __syncthreads();
+  if (tid == 0) {
+    int32_t sm = 0;
+#pragma unroll
+    for (int w2 = 0; w2 < NW; ++w2) sm += s_sum[w2];
+    rsx[t] = sm;
+    sx[t] = flat ? 0.0f : __double2float_rn(step64);
+    ox[t] = lo;
+  }
+  // Zlast: d = 3 -> Z2[i2, b] = Σ_{a, j2} Z1[a, j2] G2[a, i2, j2, b]; d = 2 -> Z1.  G2 is staged in
+  // shared memory (over the row buffer, no longer needed) with coalesced loads first.
+  if (d == 3) {
+    float* g2s = reinterpret_cast<float*>(dp_smem);  // [R1][H][J1][C], same order as the core
+    const int64_t n2 = static_cast<int64_t>(R1) * H * J1 * C;
+    __syncthreads();  // every thread is done with the row buffer
+    for (int64_t q = tid; q < n2; q += NW * 32) g2s[q] = __ldg(G2 + q);
+    __syncthreads();
+    for (int o = tid; o < H * C; o += NW * 32) {
+      const int i2 = o / C, b = o % C;
+      float v = 0.f;
+#pragma unroll 8
+      for (int aj = 0; aj < K2; ++aj) {
+        const int a = aj / J1, j2 = aj % J1;
+        v = fmaf(z1s[aj], g2s[((a * H + i2) * J1 + j2) * C + b], v);
+      }
+      zlast[t * ldz + o] = v;
+    }
+  } else {
+    if (tid < K2) zlast[t * ldz + tid] = z1s[tid];
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_decode_prep(const void* x, int64_t T, int64_t K, uint8_t* codes, int64_t ldc, float* sx, float* ox,
+                               int32_t* rsx, const float* G1, int J1, int R1, const float* G2, int d, int H, int C,
+                               float* z1out, float* zlast, int64_t ldz, cudaStream_t s) {
+  if (T == 0) return cudaSuccess;
+  LaunchScope scope(kQuantize, double(T) * K * 3 + 12.0 * T, s);
+  count_launches(1);
+  size_t smem = static_cast<size_t>(K) * 2;
+  if (d == 3) smem = std::max(smem, sizeof(float) * static_cast<size_t>(R1) * H * J1 * C);
+#define QA_DPR(JJ, RR)                                                                                             \
+  {                                                                                                                \
+    cudaFuncSetAttribute(k_decode_prep<JJ, RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)); \
+    k_decode_prep<JJ, RR><<<static_cast<unsigned>(T), 1024, smem, s>>>(static_cast<const __nv_bfloat16*>(x), K, codes,   \
+                                                                     ldc, sx, ox, rsx, G1, G2, d, H, C, z1out,       \
+                                                                     zlast, ldz);                                    \
+  }
+  if (J1 == 4 && R1 == 8)
+    QA_DPR(4, 8)
+  else if (J1 == 4)
+    QA_DPR(4, 16)
+  else if (R1 == 8)
+    QA_DPR(1, 8)
+  else
+    QA_DPR(1, 16)
+#undef QA_DPR
+  return cudaGetLastError();
+}
+
+namespace {
+
 // V[n, c] (bf16, zero padded to ldv): contraction of cores 2..d with the left rank open.
 //   d = 2: V[i, a] = G2[a, i];  d = 3: V[(i2, i3), (a, j2)] = Σ_b G2[a, i2, j2, b] G3[b, i3]
 __global__ void __launch_bounds__(256) k_build_v(int d, int R1, int H, int J1, int C, int M,
