@@ -190,13 +190,20 @@ __global__ void __launch_bounds__(256) k_dequant_t64(const uint8_t* __restrict__
 #pragma unroll
     for (int i = 0; i < 16; ++i) c[i] = (w[i >> 3] >> (4 * (i & 7))) & 0xFu;
   }
-  const double s = static_cast<double>(scale[n]), o = static_cast<double>(offset[n]);
+  if (out_lo == nullptr) {
+    // bf16 operand of the dX GEMM: one fp32 FMA per code (its rounding sits 2^-16 below the bf16 step)
+    const float s = scale[n], o = offset[n];
 #pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    const double v = __dadd_rn(__dmul_rn(static_cast<double>(c[i]), s), o);
-    const __nv_bfloat16 hi = __float2bfloat16_rn(__double2float_rn(v));
-    sh[seg * 16 + i][r] = hi;
-    if (out_lo != nullptr) sl[seg * 16 + i][r] = __float2bfloat16_rn(__double2float_rn(v - double(__bfloat162float(hi))));
+    for (int i = 0; i < 16; ++i) sh[seg * 16 + i][r] = __float2bfloat16_rn(fmaf(static_cast<float>(c[i]), s, o));
+  } else {  // hi / lo split for fp32 callers: the reference's fp64 value (quant.py:102-105)
+    const double s = static_cast<double>(scale[n]), o = static_cast<double>(offset[n]);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const double v = __dadd_rn(__dmul_rn(static_cast<double>(c[i]), s), o);
+      const __nv_bfloat16 hi = __float2bfloat16_rn(__double2float_rn(v));
+      sh[seg * 16 + i][r] = hi;
+      sl[seg * 16 + i][r] = __float2bfloat16_rn(__double2float_rn(v - double(__bfloat162float(hi))));
+    }
   }
   __syncthreads();
 #pragma unroll
