@@ -2551,11 +2551,12 @@ struct DgAdapters {
 
 template <int R1, int NA = 1>
 __global__ void __launch_bounds__(256, 1) k_tt_dg1m(const __nv_bfloat16* __restrict__ x, int64_t T, int64_t K,
-                                                    const DgAdapters ad, int S, int HS, int64_t ldb, int raw_async) {
+                                                    const DgAdapters ad, int S, int HS, int64_t ldb, int raw_async,
+                                                    int nstg) {
   constexpr int J1 = 4, K2 = J1 * R1, NN = R1 / 8;
   extern __shared__ __align__(16) uint8_t dm_smem[];
   auto xs = reinterpret_cast<__nv_bfloat16(*)[DM_ST][DM_LDX]>(dm_smem);  // [NSTG]
-  constexpr size_t XS_BYTES = sizeof(__nv_bfloat16) * DM_NSTG * DM_ST * DM_LDX;
+  const size_t XS_BYTES = sizeof(__nv_bfloat16) * nstg * DM_ST * DM_LDX;  // nstg in {3, 4}
   auto dzs = reinterpret_cast<__nv_bfloat16(*)[DM_DZT][R1][J1]>(dm_smem + XS_BYTES);  // [NA][2 planes]
   // raw fp32 dZ1 partials of the next 64-token blocks, prefetched by cp.async: [2][NA][HS][DZT][K2]
   float* raw = reinterpret_cast<float*>(dm_smem + XS_BYTES + sizeof(__nv_bfloat16) * NA * 2 * DM_DZT * R1 * J1);
@@ -2590,7 +2591,7 @@ __global__ void __launch_bounds__(256, 1) k_tt_dg1m(const __nv_bfloat16* __restr
   };
   auto issue = [&](int64_t k) {
     if (k < nst) {
-      const int slot = static_cast<int>(k % DM_NSTG);
+      const int slot = static_cast<int>(k % nstg);
       for (int i = tid; i < DM_ST * (DM_COLS / 8); i += 256) {
         const int r = i / (DM_COLS / 8), ch = i % (DM_COLS / 8);
         const int64_t t = t0 + k * DM_ST + r, col = c0 + ch * 8;
@@ -2600,13 +2601,13 @@ __global__ void __launch_bounds__(256, 1) k_tt_dg1m(const __nv_bfloat16* __restr
     }
   };
   if (raw_async) issue_raw(0);
-  for (int k = 0; k < DM_NSTG - 1; ++k) {
+  for (int k = 0; k < nstg - 1; ++k) {
     issue(k);
     cp_async_commit();
   }
   for (int64_t k = 0; k < nst; ++k) {
-    const int slot = static_cast<int>(k % DM_NSTG);
-    cp_async_wait<DM_NSTG - 2>();
+    const int slot = static_cast<int>(k % nstg);
+    cp_async_wait_dyn(nstg - 2);
     __syncthreads();  // stage k (and its dZ1 block) visible to all warps; stage k - 1's readers are done
     if (k % SPB == 0) {  // dZ1 rows of the next 64 tokens: HS partials summed, hi / lo planes, [t][a][J]
       const int64_t blk = k / SPB, tb = t0 + k * DM_ST;
@@ -2646,7 +2647,7 @@ __global__ void __launch_bounds__(256, 1) k_tt_dg1m(const __nv_bfloat16* __restr
         }
       __syncthreads();
     }
-    issue(k + DM_NSTG - 1);  // into the slot stage k - 1 used
+    issue(k + nstg - 1);  // into the slot stage k - 1 used
     if (raw_async && k % SPB == 1) issue_raw(k / SPB + 1);  // complete by the next block's first stage
     cp_async_commit();
     const int zr = static_cast<int>(k % SPB) * DM_ST;
@@ -3659,19 +3660,23 @@ cudaError_t launch_tt_dg1_group(const void* x, int64_t T, int64_t K, const float
     ad.part[a] = part[a];
     ad.dz1b[a] = dz1b != nullptr ? dz1b[a] : nullptr;
   }
-  size_t smem = sizeof(__nv_bfloat16) * (DM_NSTG * DM_ST * DM_LDX + NA * 2 * DM_DZT * R1 * J1);
+  // a 4-stage x ring when the prefetched dZ1 partials fit beside it, else 3 stages (the prefetch matters more)
   const size_t raw_bytes = sizeof(float) * 2 * NA * HS * DM_DZT * J1 * R1;
+  const size_t planes = sizeof(__nv_bfloat16) * NA * 2 * DM_DZT * R1 * J1;
+  int nstg = DM_NSTG;
+  if (sizeof(__nv_bfloat16) * nstg * DM_ST * DM_LDX + planes + raw_bytes > 220 * 1024) nstg = 3;
+  size_t smem = sizeof(__nv_bfloat16) * nstg * DM_ST * DM_LDX + planes;
   const int raw_async = smem + raw_bytes <= 220 * 1024 ? 1 : 0;
   if (raw_async) smem += raw_bytes;
   const dim3 gm(static_cast<unsigned>(gx), static_cast<unsigned>(Sm));
   if (NA == 2) {
     cudaFuncSetAttribute(k_tt_dg1m<8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     k_tt_dg1m<8, 2><<<gm, 256, smem, s>>>(static_cast<const __nv_bfloat16*>(x), T, K, ad, static_cast<int>(Sm), HS,
-                                          ldb, raw_async);
+                                          ldb, raw_async, nstg);
   } else {
     cudaFuncSetAttribute(k_tt_dg1m<8, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     k_tt_dg1m<8, 3><<<gm, 256, smem, s>>>(static_cast<const __nv_bfloat16*>(x), T, K, ad, static_cast<int>(Sm), HS,
-                                          ldb, raw_async);
+                                          ldb, raw_async, nstg);
   }
   return cudaGetLastError();
 }
@@ -3704,19 +3709,22 @@ cudaError_t launch_tt_dg1(const void* x, int x_dtype, int64_t T, int64_t K, cons
     if (Sm <= S) {  // the caller's partial buffer holds S splits
       if (splits_used != nullptr) *splits_used = static_cast<int>(Sm);
       const dim3 gm(static_cast<unsigned>(gx), static_cast<unsigned>(Sm));
-      size_t smem = sizeof(__nv_bfloat16) * (DM_NSTG * DM_ST * DM_LDX + 2 * DM_DZT * R1 * J1);
       const size_t raw_bytes = sizeof(float) * 2 * HS * DM_DZT * J1 * R1;
+      const size_t planes = sizeof(__nv_bfloat16) * 2 * DM_DZT * R1 * J1;
+      int nstg = DM_NSTG;
+      if (sizeof(__nv_bfloat16) * nstg * DM_ST * DM_LDX + planes + raw_bytes > 220 * 1024) nstg = 3;
+      size_t smem = sizeof(__nv_bfloat16) * nstg * DM_ST * DM_LDX + planes;
       const int raw_async = smem + raw_bytes <= 220 * 1024 ? 1 : 0;
       if (raw_async) smem += raw_bytes;
       const DgAdapters ad{{dz1, nullptr, nullptr}, {part, nullptr, nullptr}, {dz1b, nullptr, nullptr}};
       if (R1 == 8) {
         cudaFuncSetAttribute(k_tt_dg1m<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         k_tt_dg1m<8><<<gm, 256, smem, s>>>(static_cast<const __nv_bfloat16*>(x), T, K, ad, static_cast<int>(Sm), HS,
-                                           ldb, raw_async);
+                                           ldb, raw_async, nstg);
       } else {
         cudaFuncSetAttribute(k_tt_dg1m<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         k_tt_dg1m<16><<<gm, 256, smem, s>>>(static_cast<const __nv_bfloat16*>(x), T, K, ad, static_cast<int>(Sm), HS,
-                                            ldb, raw_async);
+                                            ldb, raw_async, nstg);
       }
       return cudaGetLastError();
     }

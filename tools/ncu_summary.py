@@ -53,6 +53,9 @@ def summarise_launches(path: str, last: int = 0) -> str:
     start = next(i for i, l in enumerate(lines) if "Kernel Name" in l)
     rows = list(csv.reader(io.StringIO("\n".join(lines[start:]))))
     hdr = rows[0]
+    if "Metric Name" in hdr:  # keep the duration rows only (the list may carry other metrics)
+        mi = hdr.index("Metric Name")
+        rows = [hdr] + [r for r in rows[1:] if len(r) > mi and r[mi] == "gpu__time_duration.sum"]
     if last:
         rows = [hdr] + [r for r in rows[1:] if len(r) > 1][-last:]
     ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
