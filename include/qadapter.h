@@ -205,6 +205,41 @@ QA_API int qa_timing_read(const char* kernel_class, double* total_ms, int64_t* l
 QA_API int qa_gemm_bf16(const void* a, int64_t lda, const void* b, int64_t ldb, int64_t m, int64_t n, int64_t k,
                         void* out_bf16, float* out_f32, int64_t ld_out, void* stream);
 
+/* ---------------------------------------------------------------- decoder-layer glue (config 4)
+ * The elementwise / row-reduction steps of _layer_forward / _layer_backward (transformer.py:858-946) around
+ * the linears, bf16 activations, each one pass over its operands. Row kernels need dim = 256 * {1,2,4,..,32};
+ * every buffer 16-byte aligned. */
+
+/* rmsnorm (transformer.py:478-484): y = (s * inv) * gain, inv = rsqrt(mean(s^2) + eps) per row, with
+ * s = a, or s = bf16(a + b) written to `sum` (the residual add res1 = x + attn folded in; b and sum both
+ * NULL or both set). inv [rows] f32 is nullable (needed by the backward). */
+QA_API int qa_rmsnorm_forward(const void* a, const void* b, void* sum, const float* gain, int64_t rows,
+                              int64_t dim, float eps, void* y, float* inv, void* stream);
+
+/* _rmsnorm_backward (transformer.py:487-496) for a frozen gain: dx = g*inv - x*(Σ g*x)*inv^3/dim (+ dres),
+ * g = gain * Σ_{i<ndy} dys[i] — the summed input gradients of a shared-input group (:922-923, :942-944) and
+ * the residual gradient dres (nullable) folded in. */
+QA_API int qa_rmsnorm_backward(const void* x, const float* gain, const float* inv, int ndy, const void* const* dys,
+                               const void* dres, int64_t rows, int64_t dim, void* dx, void* stream);
+
+/* _rope_rotate (transformer.py:506-519) in place on q and k (k nullable): adjacent pairs of each head
+ * vector rotate by pos = row % seq with the f32 [seq, head_dim/2] tables of _rope_tables (:499-503);
+ * inverse != 0 applies sign -1 (the backward). */
+QA_API int qa_rope(void* q, void* k, int64_t rows, int64_t dim, int head_dim, int seq, const float* cos_t,
+                   const float* sin_t, int inverse, void* stream);
+
+/* act = up * silu(gate) (transformer.py:872-874), n elements (multiple of 8). */
+QA_API int qa_swiglu_forward(const void* up, const void* gate, void* act, int64_t n, void* stream);
+
+/* dup = dact * silu(gate), dgate = dact * up * s * (1 + gate * (1 - s)), s = sigmoid(gate). */
+QA_API int qa_swiglu_backward(const void* up, const void* gate, const void* dact, void* dup, void* dgate, int64_t n,
+                              void* stream);
+
+/* cross_entropy_loss / cross_entropy_grad (transformer.py:569-588) over bf16 logits [rows, vocab]:
+ * loss_rows[r] = logsumexp - logit[target] (the loss is their mean), dlogits = (softmax - onehot) / rows. */
+QA_API int qa_cross_entropy(const void* logits, const int64_t* targets, int64_t rows, int64_t vocab,
+                            float* loss_rows, void* dlogits, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

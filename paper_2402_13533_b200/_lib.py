@@ -29,6 +29,12 @@ EXPORTS = (
     "qa_quantize_rows",
     "qa_dequantize_rows",
     "qa_code_rowsum",
+    "qa_rmsnorm_forward",
+    "qa_rmsnorm_backward",
+    "qa_rope",
+    "qa_swiglu_forward",
+    "qa_swiglu_backward",
+    "qa_cross_entropy",
     "qa_linear_workspace_bytes",
     "qa_linear_forward",
     "qa_linear_backward",
@@ -89,6 +95,19 @@ def _declare(lib):
     lib.qa_dequantize_rows.argtypes = [PW, P, I32, I64, I32, P]
     lib.qa_code_rowsum.restype = I32
     lib.qa_code_rowsum.argtypes = [P, I64, I64, I32, P, P]
+    F32 = ctypes.c_float
+    lib.qa_rmsnorm_forward.restype = I32
+    lib.qa_rmsnorm_forward.argtypes = [P, P, P, P, I64, I64, F32, P, P, P]
+    lib.qa_rmsnorm_backward.restype = I32
+    lib.qa_rmsnorm_backward.argtypes = [P, P, P, I32, ctypes.POINTER(P), P, I64, I64, P, P]
+    lib.qa_rope.restype = I32
+    lib.qa_rope.argtypes = [P, P, I64, I64, I32, I32, P, P, I32, P]
+    lib.qa_swiglu_forward.restype = I32
+    lib.qa_swiglu_forward.argtypes = [P, P, P, I64, P]
+    lib.qa_swiglu_backward.restype = I32
+    lib.qa_swiglu_backward.argtypes = [P, P, P, P, P, I64, P]
+    lib.qa_cross_entropy.restype = I32
+    lib.qa_cross_entropy.argtypes = [P, P, I64, I64, P, P, P]
     lib.qa_linear_workspace_bytes.restype = SZ
     lib.qa_linear_workspace_bytes.argtypes = [PW, PT, I64]
     lib.qa_linear_forward.restype = I32

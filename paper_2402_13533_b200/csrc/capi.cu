@@ -301,6 +301,109 @@ int qa_nonfinite_segments(const float* grads, const int64_t* seg_offsets, int ns
                      "nonfinite segments");
 }
 
+namespace {
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+bool glue_dim_ok(int64_t D) {
+  if (D < 256 || D % 256 != 0) return false;
+  const int64_t v = D / 256;
+  return v <= 32 && (v & (v - 1)) == 0;
+}
+}  // namespace
+
+int qa_rmsnorm_forward(const void* a, const void* b, void* sum, const float* gain, int64_t rows, int64_t dim,
+                       float eps, void* y, float* inv, void* stream) {
+  if (rows < 0 || a == nullptr || gain == nullptr || y == nullptr || (b == nullptr) != (sum == nullptr) ||
+      !aligned16(a) || !aligned16(y) || !aligned16(gain) || (b != nullptr && (!aligned16(b) || !aligned16(sum)))) {
+    set_error("qa_rmsnorm_forward: bad argument");
+    return QA_ERR_ARG;
+  }
+  if (!glue_dim_ok(dim)) {
+    set_error("qa_rmsnorm_forward: dim %lld must be 256 * {1,2,4,...,32}", (long long)dim);
+    return QA_ERR_UNSUPPORTED;
+  }
+  return cuda_status(launch_rmsnorm_fwd(static_cast<const __nv_bfloat16*>(a), static_cast<const __nv_bfloat16*>(b),
+                                        static_cast<__nv_bfloat16*>(sum), gain, static_cast<__nv_bfloat16*>(y), inv,
+                                        rows, static_cast<int>(dim), eps, static_cast<cudaStream_t>(stream)),
+                     "rmsnorm forward");
+}
+
+int qa_rmsnorm_backward(const void* x, const float* gain, const float* inv, int ndy, const void* const* dys,
+                        const void* dres, int64_t rows, int64_t dim, void* dx, void* stream) {
+  if (rows < 0 || x == nullptr || gain == nullptr || inv == nullptr || dx == nullptr || dys == nullptr || ndy < 1 ||
+      ndy > 3 || !aligned16(x) || !aligned16(dx) || !aligned16(gain) || (dres != nullptr && !aligned16(dres))) {
+    set_error("qa_rmsnorm_backward: bad argument");
+    return QA_ERR_ARG;
+  }
+  GlueDys d{};
+  d.n = ndy;
+  for (int i = 0; i < ndy; ++i) {
+    if (dys[i] == nullptr || !aligned16(dys[i])) {
+      set_error("qa_rmsnorm_backward: bad dy[%d]", i);
+      return QA_ERR_ARG;
+    }
+    d.p[i] = static_cast<const __nv_bfloat16*>(dys[i]);
+  }
+  if (!glue_dim_ok(dim)) {
+    set_error("qa_rmsnorm_backward: dim %lld must be 256 * {1,2,4,...,32}", (long long)dim);
+    return QA_ERR_UNSUPPORTED;
+  }
+  return cuda_status(launch_rmsnorm_bwd(static_cast<const __nv_bfloat16*>(x), gain, inv, d,
+                                        static_cast<const __nv_bfloat16*>(dres), static_cast<__nv_bfloat16*>(dx),
+                                        rows, static_cast<int>(dim), static_cast<cudaStream_t>(stream)),
+                     "rmsnorm backward");
+}
+
+int qa_rope(void* q, void* k, int64_t rows, int64_t dim, int head_dim, int seq, const float* cos_t,
+            const float* sin_t, int inverse, void* stream) {
+  if (rows < 0 || q == nullptr || cos_t == nullptr || sin_t == nullptr || seq < 1 || head_dim < 8 ||
+      head_dim % 8 != 0 || dim % head_dim != 0 || !aligned16(q) || (k != nullptr && !aligned16(k)) ||
+      !aligned16(cos_t) || !aligned16(sin_t)) {
+    set_error("qa_rope: bad argument (head_dim must be a multiple of 8 dividing dim)");
+    return QA_ERR_ARG;
+  }
+  return cuda_status(launch_rope(static_cast<__nv_bfloat16*>(q), static_cast<__nv_bfloat16*>(k), rows,
+                                 static_cast<int>(dim), head_dim, seq, cos_t, sin_t, inverse ? -1.f : 1.f,
+                                 static_cast<cudaStream_t>(stream)),
+                     "rope");
+}
+
+int qa_swiglu_forward(const void* up, const void* gate, void* act, int64_t n, void* stream) {
+  if (n < 0 || n % 8 != 0 || up == nullptr || gate == nullptr || act == nullptr || !aligned16(up) ||
+      !aligned16(gate) || !aligned16(act)) {
+    set_error("qa_swiglu_forward: bad argument (n must be a multiple of 8, 16-byte aligned buffers)");
+    return QA_ERR_ARG;
+  }
+  return cuda_status(launch_swiglu_fwd(static_cast<const __nv_bfloat16*>(up), static_cast<const __nv_bfloat16*>(gate),
+                                       static_cast<__nv_bfloat16*>(act), n, static_cast<cudaStream_t>(stream)),
+                     "swiglu forward");
+}
+
+int qa_swiglu_backward(const void* up, const void* gate, const void* dact, void* dup, void* dgate, int64_t n,
+                       void* stream) {
+  if (n < 0 || n % 8 != 0 || up == nullptr || gate == nullptr || dact == nullptr || dup == nullptr ||
+      dgate == nullptr || !aligned16(up) || !aligned16(gate) || !aligned16(dact) || !aligned16(dup) ||
+      !aligned16(dgate)) {
+    set_error("qa_swiglu_backward: bad argument (n must be a multiple of 8, 16-byte aligned buffers)");
+    return QA_ERR_ARG;
+  }
+  return cuda_status(launch_swiglu_bwd(static_cast<const __nv_bfloat16*>(up), static_cast<const __nv_bfloat16*>(gate),
+                                       static_cast<const __nv_bfloat16*>(dact), static_cast<__nv_bfloat16*>(dup),
+                                       static_cast<__nv_bfloat16*>(dgate), n, static_cast<cudaStream_t>(stream)),
+                     "swiglu backward");
+}
+
+int qa_cross_entropy(const void* logits, const int64_t* targets, int64_t rows, int64_t vocab, float* loss_rows,
+                     void* dlogits, void* stream) {
+  if (rows < 0 || vocab < 8 || vocab % 8 != 0 || vocab > INT32_MAX || logits == nullptr || targets == nullptr ||
+      loss_rows == nullptr || dlogits == nullptr || !aligned16(logits) || !aligned16(dlogits)) {
+    set_error("qa_cross_entropy: bad argument (vocab must be a multiple of 8, 16-byte aligned buffers)");
+    return QA_ERR_ARG;
+  }
+  return cuda_status(launch_xent(static_cast<const __nv_bfloat16*>(logits), targets, rows, static_cast<int>(vocab),
+                                 loss_rows, static_cast<__nv_bfloat16*>(dlogits), static_cast<cudaStream_t>(stream)),
+                     "cross entropy");
+}
+
 int qa_code_rowsum(const uint8_t* codes, int64_t rows, int64_t cols, int bits, int32_t* rowsum, void* stream) {
   if (bits != 4 && bits != 8) {
     set_error("bits must be 4 or 8, got %d", bits);

@@ -84,6 +84,25 @@ cudaError_t launch_adamw(float* params, double* master, double* m, double* v, co
                          double b1, double b2, double eps, double wd, int64_t step, cudaStream_t s);
 cudaError_t launch_seg_nonfinite(const float* g, const int64_t* seg, int nseg, int32_t* flags, cudaStream_t s);
 
+// decoder glue (glue.cu): D = 256 * {1,2,4,8,16,32} for the row kernels
+struct GlueDys {
+  const __nv_bfloat16* p[3];
+  int n;
+};
+cudaError_t launch_rmsnorm_fwd(const __nv_bfloat16* a, const __nv_bfloat16* b, __nv_bfloat16* sum,
+                               const float* gain, __nv_bfloat16* y, float* inv, int64_t rows, int D, float eps,
+                               cudaStream_t st);
+cudaError_t launch_rmsnorm_bwd(const __nv_bfloat16* x, const float* gain, const float* inv, const GlueDys& dys,
+                               const __nv_bfloat16* dres, __nv_bfloat16* dx, int64_t rows, int D, cudaStream_t st);
+cudaError_t launch_rope(__nv_bfloat16* x0, __nv_bfloat16* x1, int64_t rows, int D, int head_dim, int seq,
+                        const float* cos_t, const float* sin_t, float sign, cudaStream_t st);
+cudaError_t launch_swiglu_fwd(const __nv_bfloat16* up, const __nv_bfloat16* gate, __nv_bfloat16* act, int64_t n,
+                              cudaStream_t st);
+cudaError_t launch_swiglu_bwd(const __nv_bfloat16* up, const __nv_bfloat16* gate, const __nv_bfloat16* dact,
+                              __nv_bfloat16* dup, __nv_bfloat16* dgate, int64_t n, cudaStream_t st);
+cudaError_t launch_xent(const __nv_bfloat16* logits, const int64_t* targets, int64_t rows, int V, float* loss_rows,
+                        __nv_bfloat16* dlogits, cudaStream_t st);
+
 // ------------------------------------------------------------ fast TT family (tt_fast.cu)
 bool fast_tt_supported(int J1, int R1);
 size_t g1i_floats(int64_t K, int J1, int R1);  // workspace for the interleaved G1 copy
