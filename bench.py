@@ -57,6 +57,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-merge", action="store_true")
+    ap.add_argument("--no-decoder", action="store_true", help="skip the config-4 decoder-stack measurement")
     ap.add_argument("--no-group", action="store_true", help="run every linear on its own (A/B of the shared x pass)")
     return ap.parse_args()
 
@@ -271,6 +272,39 @@ def measure_merge(dev, sptr, hbm_gbs, iters=5):
                    "TT r=8, bf16 W'", "ms": tot_ms, "bytes": tot_bytes, "achieved_gbs": gbs,
             "frac_of_hbm": gbs / hbm_gbs, "kernels": "k_prefix_d3 + k_merge_nd1"}
 
+
+
+def measure_decoder(dev, layers=32, batch=4, seq=2048, steps=3, warmup=2):
+    """BASELINE config 4 on one GPU: the 32-layer Llama-2-7B-shaped decoder (vocab 32000), int8
+    bases + TT r = 8 adapters on every linear and the head, PER_LAYER recompute, [4, 2048] tokens (the per-GPU
+    share of the [32, 2048] global batch).  Outside the config-2 timed region; CUDA events, warm."""
+    import torch
+
+    from paper_2402_13533_b200.decoder import DecoderConfig, build_decoder
+
+    cfg = DecoderConfig(vocab=32000, dim=4096, heads=32, layers=layers, ffn_dim=11008, max_seq=seq)
+    model = build_decoder(cfg, rank=8, bits=8, seed=1, device=dev)
+    g = torch.Generator(device=dev).manual_seed(2)
+    tokens = torch.randint(0, cfg.vocab, (batch, seq), generator=g, device=dev)
+    targets = torch.randint(0, cfg.vocab, (batch, seq), generator=g, device=dev)
+    for _ in range(warmup):
+        model.train_step_grads(tokens, targets)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        loss, grads = model.train_step_grads(tokens, targets)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / steps
+    out = {"workload": f"llama2-7b decoder, {layers} layers + head, vocab 32000, int8 bases, TT r=8 on all linears "
+                       f"and the head, PER_LAYER recompute, [{batch}, {seq}] tokens",
+           "baseline_config": 4, "ms_per_step": ms, "tokens_per_s": batch * seq / (ms / 1e3), "steps": steps,
+           "loss": loss, "adapter_tensors": len(grads),
+           "note": "fwd storing layer inputs + cross-entropy + bwd re-running each layer; attention = torch SDPA"}
+    del model, grads
+    torch.cuda.empty_cache()
+    return out
 
 
 def main():
@@ -599,6 +633,10 @@ def main():
     if rank == 0 and not args.no_merge:
         merge = measure_merge(dev, sptr, peaks["hbm_gbs"])
 
+    decoder = None
+    if rank == 0 and world == 1 and not args.no_decoder:
+        decoder = measure_decoder(dev)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = run_cpu_baseline(cfg)
@@ -608,7 +646,8 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "int8 (u8xu8->s32) GEMM + bf16", "data": "synthetic",
-            "config": desc, "roofline": roofline, "kernels": kernels, "decode": decode, "merge": merge, "cpu_baseline": cpu, "e2e": e2e,
+            "config": desc, "roofline": roofline, "kernels": kernels, "decode": decode, "merge": merge, "decoder": decoder,
+            "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches * args.steps), "gpu_launches_per_step": int(launches), "clocks": clocks,
         }
         print(json.dumps(line), flush=True)

@@ -3,7 +3,7 @@
 # (gpurun brings back <= 64 MiB).
 python bench.py > gpurun_out/bench_full.log 2>&1; echo bench rc=$?
 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.log 2>&1; echo ref rc=$?
-B="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-merge"
+B="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-merge --no-decoder"
 $B > gpurun_out/plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $B > gpurun_out/ncu1.log 2>&1
 echo launches rc=$?
