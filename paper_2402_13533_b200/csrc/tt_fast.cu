@@ -1553,32 +1553,81 @@ __global__ void __launch_bounds__(AQR_W * 32, 1) k_aq_ring(const __nv_bfloat16* 
 }
 
 // ---------------------------------------------------------------------------------------------
+#ifdef QA_DP_TRACE
+__device__ unsigned long long g_dp_trace[16];
+#define DP_MARK(i)                                                                   \
+  if (threadIdx.x == 0 && blockIdx.x == 0) {                                         \
+    unsigned long long tt_;                                                          \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt_));                          \
+    g_dp_trace[i] = tt_;                                                             \
+  }
+#else
+#define DP_MARK(i)
+#endif
+
+// Warp transpose-reduction of NV values per lane (NV a power of two <= 32): afterwards lane l holds
+// Σ_lanes v[l % NV] in v[0] — 31 shuffles for NV = 32 instead of 32 x 5 for 32 separate reductions.
+template <int NV>
+__device__ __forceinline__ void warp_transpose_reduce(float (&v)[NV]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 16; o >= NV; o >>= 1)
+#pragma unroll
+    for (int j = 0; j < NV; ++j) v[j] += __shfl_xor_sync(0xffffffffu, v[j], o);
+#pragma unroll
+  for (int o = NV / 2; o >= 1; o >>= 1) {
+    const bool upper = (lane & o) != 0;
+#pragma unroll
+    for (int j = 0; j < o; ++j) {
+      const float send = upper ? v[j] : v[j + o];
+      const float keep = upper ? v[j + o] : v[j];
+      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+}
+
 // Decode-size prologue (1..8 tokens, KV-cached decoding): one CTA per token row does the bit-exact
 // act-quant (aq_codes8b + fp64 replay), Z1 = x·G1 in fp32 and the last core's input Zlast (d = 3:
 // Z2 = Z1·Gm, [H][C]; d = 2: Z1), so the matrix-vector pass (gemv.cu) needs no V / fragment build.
+// The CTA is sized to the row (one 16-byte chunk per thread up to 1024 threads) and releases the
+// dependent matrix-vector launch at once (programmatic dependent launch): its CTAs stream the weight
+// codes into L2 while this prologue runs and wait on griddepcontrol before reading its outputs.
 template <int J1, int R1>
-__global__ void __launch_bounds__(1024) k_decode_prep(const __nv_bfloat16* __restrict__ x, int64_t K,
-                                                     uint8_t* __restrict__ codes, int64_t ldc, float* __restrict__ sx,
-                                                     float* __restrict__ ox, int32_t* __restrict__ rsx,
-                                                     const float* __restrict__ G1, const float* __restrict__ G2,
-                                                     int d, int H, int C, float* __restrict__ z1out,
-                                                     float* __restrict__ zlast, int64_t ldz) {
+__global__ void __launch_bounds__(512) k_decode_prep(const __nv_bfloat16* __restrict__ x, int64_t K,
+                                                    uint8_t* __restrict__ codes, int64_t ldc, float* __restrict__ sx,
+                                                    float* __restrict__ ox, int32_t* __restrict__ rsx,
+                                                    const float* __restrict__ G1, const float* __restrict__ G2,
+                                                    int d, int H, int C, float* __restrict__ z1out,
+                                                    float* __restrict__ zlast, int64_t ldz, bool vec) {
+  DP_MARK(0)
+  asm volatile("griddepcontrol.launch_dependents;");
   constexpr int K2 = J1 * R1;
+  constexpr int NV = K2 < 32 ? K2 : 32;  // values per transpose-reduction round
+  constexpr int NJ = 8 / J1;             // G1 rows (j1) per 16-byte chunk of x
+  constexpr int GH = NJ * R1 > 64 ? 2 : 1;  // G1 floats of a chunk loaded in GH halves (<= 64 registers)
   extern __shared__ __align__(16) uint8_t dp_smem[];
-  constexpr int NW = 32;  // warps
-  __shared__ float red[NW][K2 + 1];
-  __shared__ float s_lo[NW], s_hi[NW];
-  __shared__ int32_t s_sum[NW];
+  __shared__ float red[16][K2 + 1];
+  __shared__ float s_lo[16], s_hi[16];
+  __shared__ int32_t s_sum[16];
   __shared__ float z1s[K2];
   const int t = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int NT = blockDim.x, NW = NT >> 5;
   const uint4* xr = reinterpret_cast<const uint4*>(x + t * K);
   uint4* row = reinterpret_cast<uint4*>(dp_smem);
   const int nchunk = static_cast<int>(K / 8);
+  // the middle core (d = 3) does not depend on x: start its copy into shared memory now
+  float* g2s = reinterpret_cast<float*>(dp_smem + ((K * 2 + 15) / 16) * 16);  // [R1][H][J1][C]
+  const int n2 = d == 3 ? R1 * H * J1 * C : 0;
+  if (vec && n2 > 0) {
+    for (int q = tid; q < n2 / 4; q += NT) cp_async16(g2s + 4 * q, G2 + 4 * q, true);
+    cp_async_commit();
+  }
   __nv_bfloat162 lo2 = __floats2bfloat162_rn(INFINITY, INFINITY), hi2 = __floats2bfloat162_rn(-INFINITY, -INFINITY);
   float z[K2];
 #pragma unroll
   for (int i = 0; i < K2; ++i) z[i] = 0.f;
-  for (int c = tid; c < nchunk; c += NW * 32) {
+#pragma unroll 2
+  for (int c = tid; c < nchunk; c += NT) {
     const uint4 v = __ldg(xr + c);
     row[c] = v;
     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
@@ -1588,15 +1637,35 @@ __global__ void __launch_bounds__(1024) k_decode_prep(const __nv_bfloat16* __res
       lo2 = __hmin2(lo2, b2);
       hi2 = __hmax2(hi2, b2);
     }
+    // elements 8c + e: j1 = 8c / J1 + e / J1, J = e % J1; the chunk's G1 rows are NJ * R1 contiguous floats
+    const float* gbase = G1 + static_cast<int64_t>(c) * NJ * R1;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {  // element 8c + e: j1 = (8c + e) / J1, J = e % J1
-      const float xv = __uint_as_float((e & 1) ? (w[e >> 1] & 0xFFFF0000u) : (w[e >> 1] << 16));
-      const int64_t j1 = (8 * static_cast<int64_t>(c) + e) / J1;
-      const int J = e % J1;
+    for (int hh = 0; hh < GH; ++hh) {
+      constexpr int GF = NJ * R1 / GH;
+      float gv[GF];
+      if (vec) {
 #pragma unroll
-      for (int a = 0; a < R1; ++a) z[a * J1 + J] = fmaf(xv, __ldg(G1 + j1 * R1 + a), z[a * J1 + J]);
+        for (int q = 0; q < GF / 4; ++q) {
+          const float4 f = __ldg(reinterpret_cast<const float4*>(gbase + hh * GF) + q);
+          gv[4 * q] = f.x;
+          gv[4 * q + 1] = f.y;
+          gv[4 * q + 2] = f.z;
+          gv[4 * q + 3] = f.w;
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < GF; ++q) gv[q] = __ldg(gbase + hh * GF + q);
+      }
+#pragma unroll
+      for (int e = hh * (8 / GH); e < (hh + 1) * (8 / GH); ++e) {
+        const float xv = __uint_as_float((e & 1) ? (w[e >> 1] & 0xFFFF0000u) : (w[e >> 1] << 16));
+        const int jl = e / J1 - hh * (NJ / GH), J = e % J1;
+#pragma unroll
+        for (int a = 0; a < R1; ++a) z[a * J1 + J] = fmaf(xv, gv[jl * R1 + a], z[a * J1 + J]);
+      }
     }
   }
+  DP_MARK(1)
   float lo = fminf(__low2float(lo2), __high2float(lo2)), hi = fmaxf(__low2float(hi2), __high2float(hi2));
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -1604,31 +1673,33 @@ __global__ void __launch_bounds__(1024) k_decode_prep(const __nv_bfloat16* __res
     hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
   }
 #pragma unroll
-  for (int i = 0; i < K2; ++i) {
-    float v = z[i];
+  for (int g = 0; g < K2 / NV; ++g) {
+    float v[NV];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) red[warp][i] = v;
+    for (int i = 0; i < NV; ++i) v[i] = z[g * NV + i];
+    warp_transpose_reduce<NV>(v);
+    if (lane < NV) red[warp][g * NV + lane] = v[0];
   }
   if (lane == 0) {
     s_lo[warp] = lo;
     s_hi[warp] = hi;
   }
+  DP_MARK(2)
   __syncthreads();
+  DP_MARK(3)
   lo = s_lo[0];
   hi = s_hi[0];
-#pragma unroll
   for (int w2 = 1; w2 < NW; ++w2) {
     lo = fminf(lo, s_lo[w2]);
     hi = fmaxf(hi, s_hi[w2]);
   }
   if (tid < K2) {
     float v = red[0][tid];
-#pragma unroll
     for (int w2 = 1; w2 < NW; ++w2) v += red[w2][tid];
     z1s[tid] = v;
     if (z1out != nullptr) z1out[t * K2 + tid] = v;
   }
+  DP_MARK(4)
   // codes of this row (bracketed rule, bit-exact with quant.py:73-99)
   const double lo64 = static_cast<double>(lo);
   const double step64 = __ddiv_rn(__dsub_rn(static_cast<double>(hi), lo64), 255.0);
@@ -1641,7 +1712,7 @@ __global__ void __launch_bounds__(1024) k_decode_prep(const __nv_bfloat16* __res
                            ahi2 = f2pack(ahi, ahi);
   uint8_t* crow = codes + t * ldc;
   uint32_t sum = 0;
-  for (int c = tid; c < nchunk; c += NW * 32) {
+  for (int c = tid; c < nchunk; c += NT) {
     const uint4 v = row[c];
     uint32_t c0, c1, d0, d1;
     if (sub)
@@ -1654,37 +1725,49 @@ __global__ void __launch_bounds__(1024) k_decode_prep(const __nv_bfloat16* __res
     sum = __dp4a(c0, 0x01010101u, __dp4a(c1, 0x01010101u, sum));
     *reinterpret_cast<uint2*>(crow + 8 * static_cast<int64_t>(c)) = make_uint2(c0, c1);
   }
-  for (int64_t k = K + tid; k < ldc; k += NW * 32) crow[k] = 0;
+  DP_MARK(5)
+  for (int64_t k = K + tid; k < ldc; k += NT) crow[k] = 0;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
   if (lane == 0) s_sum[warp] = static_cast<int32_t>(sum);
   __syncthreads();
+  DP_MARK(6)
   if (tid == 0) {
     int32_t sm = 0;
-#pragma unroll
     for (int w2 = 0; w2 < NW; ++w2) sm += s_sum[w2];
     rsx[t] = sm;
     sx[t] = flat ? 0.0f : __double2float_rn(step64);
     ox[t] = lo;
   }
-  // Zlast: d = 3 -> Z2[i2, b] = Σ_{a, j2} Z1[a, j2] G2[a, i2, j2, b]; d = 2 -> Z1.  G2 is staged in
-  // shared memory (over the row buffer, no longer needed) with coalesced loads first.
+  // Zlast: d = 3 -> Z2[i2, b] = Σ_{a, j2} Z1[a, j2] G2[a, i2, j2, b], four lanes per output (K2 / 4 terms
+  // each, then two shuffles); d = 2 -> Z1.
   if (d == 3) {
-    float* g2s = reinterpret_cast<float*>(dp_smem);  // [R1][H][J1][C], same order as the core
-    const int64_t n2 = static_cast<int64_t>(R1) * H * J1 * C;
-    __syncthreads();  // every thread is done with the row buffer
-    for (int64_t q = tid; q < n2; q += NW * 32) g2s[q] = __ldg(G2 + q);
+    DP_MARK(7)
+    if (vec) {
+      cp_async_wait<0>();
+    } else {
+      for (int q = tid; q < n2; q += NT) g2s[q] = __ldg(G2 + q);
+    }
     __syncthreads();
-    for (int o = tid; o < H * C; o += NW * 32) {
-      const int i2 = o / C, b = o % C;
+    DP_MARK(8)
+    const int HC = H * C;
+    const int passes = (HC * 4 + NT - 1) / NT;
+    for (int p = 0; p < passes; ++p) {
+      const int o = (p * NT + tid) >> 2, part = tid & 3;
+      const int oc = o < HC ? o : HC - 1;
+      const int i2 = oc / C, b = oc % C;
       float v = 0.f;
-#pragma unroll 8
-      for (int aj = 0; aj < K2; ++aj) {
+#pragma unroll
+      for (int q = 0; q < K2 / 4; ++q) {
+        const int aj = part * (K2 / 4) + q;
         const int a = aj / J1, j2 = aj % J1;
         v = fmaf(z1s[aj], g2s[((a * H + i2) * J1 + j2) * C + b], v);
       }
-      zlast[t * ldz + o] = v;
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      if (part == 0 && o < HC) zlast[t * ldz + o] = v;
     }
+    DP_MARK(9)
   } else {
     if (tid < K2) zlast[t * ldz + tid] = z1s[tid];
   }
@@ -1692,20 +1775,31 @@ __global__ void __launch_bounds__(1024) k_decode_prep(const __nv_bfloat16* __res
 
 }  // namespace
 
+#ifdef QA_DP_TRACE
+extern "C" __attribute__((visibility("default"))) int qa_debug_dp_trace(unsigned long long* out) {
+  return static_cast<int>(cudaMemcpyFromSymbol(out, g_dp_trace, sizeof(g_dp_trace)));
+}
+#endif
+
 cudaError_t launch_decode_prep(const void* x, int64_t T, int64_t K, uint8_t* codes, int64_t ldc, float* sx, float* ox,
                                int32_t* rsx, const float* G1, int J1, int R1, const float* G2, int d, int H, int C,
                                float* z1out, float* zlast, int64_t ldz, cudaStream_t s) {
   if (T == 0) return cudaSuccess;
   LaunchScope scope(kQuantize, double(T) * K * 3 + 12.0 * T, s);
   count_launches(1);
-  size_t smem = static_cast<size_t>(K) * 2;
-  if (d == 3) smem = std::max(smem, sizeof(float) * static_cast<size_t>(R1) * H * J1 * C);
+  const int64_t nch = K / 8;  // one 16-byte chunk per thread, 128..512 threads
+  const int threads = static_cast<int>(nch >= 512 ? 512 : (nch <= 128 ? 128 : (nch + 31) / 32 * 32));
+  const size_t n2 = d == 3 ? static_cast<size_t>(R1) * H * J1 * C : 0;
+  const size_t smem = (static_cast<size_t>(K) * 2 + 15) / 16 * 16 + sizeof(float) * n2;
+  // vector / cp.async paths need 16-byte aligned cores (G1 rows of a chunk start at multiples of 32 floats)
+  const bool vec = (reinterpret_cast<uintptr_t>(G1) % 16 == 0) && (G2 == nullptr || reinterpret_cast<uintptr_t>(G2) % 16 == 0) &&
+                   n2 % 4 == 0;
 #define QA_DPR(JJ, RR)                                                                                             \
   {                                                                                                                \
     cudaFuncSetAttribute(k_decode_prep<JJ, RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)); \
-    k_decode_prep<JJ, RR><<<static_cast<unsigned>(T), 1024, smem, s>>>(static_cast<const __nv_bfloat16*>(x), K, codes,   \
-                                                                     ldc, sx, ox, rsx, G1, G2, d, H, C, z1out,       \
-                                                                     zlast, ldz);                                    \
+    k_decode_prep<JJ, RR><<<static_cast<unsigned>(T), threads, smem, s>>>(static_cast<const __nv_bfloat16*>(x), K, codes, \
+                                                                        ldc, sx, ox, rsx, G1, G2, d, H, C, z1out,    \
+                                                                        zlast, ldz, vec);                            \
   }
   if (J1 == 4 && R1 == 8)
     QA_DPR(4, 8)
