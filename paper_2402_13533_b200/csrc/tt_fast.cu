@@ -1820,27 +1820,33 @@ namespace {
 __global__ void __launch_bounds__(256) k_build_v(int d, int R1, int H, int J1, int C, int M,
                                                  const float* __restrict__ G2, const float* __restrict__ G3,
                                                  __nv_bfloat16* __restrict__ V, int64_t N, int64_t ldv) {
-  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (idx >= N * ldv) return;
-  const int64_t n = idx / ldv;
-  const int c = static_cast<int>(idx - n * ldv);
+  // one thread per (row n, column cc < K2): v is computed once and written to its three slots
   // [V_hi | V_hi | V_lo] against [Z_hi | Z_lo | Z_hi]: the three leading terms of the bf16 split
-  // product, so y2 carries ~16 mantissa bits although the MMA operands are bf16
+  // product, so y2 carries ~16 mantissa bits although the MMA operands are bf16; padding [3 K2, ldv) = 0
   const int K2 = R1 * J1;
-  float v = 0.f;
-  if (c < 3 * K2) {
-    const int cc = c % K2;
-    const int a = cc / J1, j2 = cc % J1;
-    if (d == 2) {
-      v = G2[static_cast<int64_t>(a) * N + n];
-    } else {
-      const int i2 = static_cast<int>(n / M), i3 = static_cast<int>(n % M);
-      const float* g2 = G2 + ((static_cast<int64_t>(a) * H + i2) * J1 + j2) * C;
-      for (int b = 0; b < C; ++b) v = fmaf(g2[b], G3[static_cast<int64_t>(b) * M + i3], v);
-    }
-    if (c >= 2 * K2) v -= __bfloat162float(__float2bfloat16_rn(v));
+  const int per_row = static_cast<int>(ldv) - 2 * K2;  // threads per row: K2 value columns + the padding
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= N * per_row) return;
+  const int n32 = static_cast<int>(idx / per_row);  // N * ldv < 2^31 (launcher)
+  const int c = static_cast<int>(idx - static_cast<int64_t>(n32) * per_row);
+  __nv_bfloat16* vr = V + static_cast<int64_t>(n32) * ldv;
+  if (c >= K2) {
+    vr[c + 2 * K2] = __float2bfloat16_rn(0.f);
+    return;
   }
-  V[idx] = __float2bfloat16_rn(v);
+  const int a = c / J1, j2 = c - a * J1;
+  float v = 0.f;
+  if (d == 2) {
+    v = G2[static_cast<int64_t>(a) * N + n32];
+  } else {
+    const int i2 = n32 / M, i3 = n32 - i2 * M;
+    const float* g2 = G2 + ((static_cast<int64_t>(a) * H + i2) * J1 + j2) * C;
+    for (int b = 0; b < C; ++b) v = fmaf(__ldg(g2 + b), __ldg(G3 + static_cast<int64_t>(b) * M + i3), v);
+  }
+  const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+  vr[c] = hi;
+  vr[c + K2] = hi;
+  vr[c + 2 * K2] = __float2bfloat16_rn(v - __bfloat162float(hi));
 }
 
 // B_ext[k = (j1, J), c = (a, J')] = G1[j1, a] δ(J, J')  (bf16, zero padded to ldb)
@@ -2576,16 +2582,19 @@ __global__ void __launch_bounds__(256) k_grad_reduce3(const ReduceArgs a) {
   int si = 0;
   while (si < 3 && b >= a.blocks[si]) b -= a.blocks[si++];
   if (si == 3) {  // B_ext rows
-    const int64_t idx = b * 256 + threadIdx.x;
-    if (a.bext == nullptr || idx >= a.K * a.ldb) return;
-    const int64_t k = idx / a.ldb;
-    const int c = static_cast<int>(idx - k * a.ldb);
+    // 32-bit index math (K * ldb < 2^31, checked by the launcher)
+    const int idx = static_cast<int>(b) * 256 + static_cast<int>(threadIdx.x);
+    if (a.bext == nullptr || idx >= static_cast<int>(a.K * a.ldb)) return;
+    const int ldb = static_cast<int>(a.ldb);
+    const int k = idx / ldb;
+    const int c = idx - k * ldb;
     const int K2 = a.R1 * a.J1;
     float v = 0.f;
     if (c < 3 * K2) {  // [B_hi | B_hi | B_lo] against [dZ1_hi | dZ1_lo | dZ1_hi]
       const int cc = c % K2;
       const int aa = cc / a.J1, Jp = cc % a.J1;
-      if (static_cast<int>(k % a.J1) == Jp) v = a.G1[(k / a.J1) * a.R1 + aa];
+      const int j1 = k / a.J1;
+      if (k - j1 * a.J1 == Jp) v = __ldg(a.G1 + static_cast<int64_t>(j1) * a.R1 + aa);
       if (c >= 2 * K2) v -= __bfloat162float(__float2bfloat16_rn(v));
     }
     a.bext[idx] = __float2bfloat16_rn(v);
@@ -3549,7 +3558,9 @@ cudaError_t launch_build_v(int d, int R1, int H, int J1, int C, int M, const flo
   const int64_t total = N * ldv;
   LaunchScope scope(kTT, double(total) * 2 + double(N) * R1 * J1 * C * 2, s);
   count_launches(1);
-  k_build_v<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(d, R1, H, J1, C, M, G2, G3, V, N, ldv);
+  const int64_t threads = N * (ldv - 2 * int64_t(R1) * J1);
+  if (total >= (int64_t(1) << 31) || ldv < 3 * int64_t(R1) * J1) return cudaErrorInvalidValue;
+  k_build_v<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, s>>>(d, R1, H, J1, C, M, G2, G3, V, N, ldv);
   return cudaGetLastError();
 }
 
@@ -3670,7 +3681,10 @@ cudaError_t launch_grad_reduce3(const float* const* parts, const int* nparts, co
   a.bext = bext;
   a.K = K;
   a.ldb = ldb;
-  if (bext != nullptr) total += (K * ldb + 255) / 256;
+  if (bext != nullptr) {
+    if (K * ldb >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
+    total += (K * ldb + 255) / 256;
+  }
   if (total == 0) return cudaSuccess;
   LaunchScope scope(kTT, bytes + (bext ? 2.0 * double(K) * ldb : 0.0), s);
   count_launches(1);
