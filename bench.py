@@ -287,22 +287,24 @@ def measure_decoder(dev, layers=32, batch=4, seq=2048, steps=3, warmup=2):
     g = torch.Generator(device=dev).manual_seed(2)
     tokens = torch.randint(0, cfg.vocab, (batch, seq), generator=g, device=dev)
     targets = torch.randint(0, cfg.vocab, (batch, seq), generator=g, device=dev)
+    state = None
     for _ in range(warmup):
-        model.train_step_grads(tokens, targets)
+        _, state = model.train_step(tokens, targets, state)
     torch.cuda.synchronize(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(steps):
-        loss, grads = model.train_step_grads(tokens, targets)
+        loss, state = model.train_step(tokens, targets, state)
     e1.record()
     torch.cuda.synchronize(dev)
     ms = e0.elapsed_time(e1) / steps
     out = {"workload": f"llama2-7b decoder, {layers} layers + head, vocab 32000, int8 bases, TT r=8 on all linears "
                        f"and the head, PER_LAYER recompute, [{batch}, {seq}] tokens",
            "baseline_config": 4, "ms_per_step": ms, "tokens_per_s": batch * seq / (ms / 1e3), "steps": steps,
-           "loss": loss, "adapter_tensors": len(grads),
-           "note": "fwd storing layer inputs + cross-entropy + bwd re-running each layer; attention = torch SDPA"}
-    del model, grads
+           "loss": loss, "adapter_tensors": len(state.names),
+           "note": "trainer.train_step: fwd storing layer inputs + cross-entropy + bwd re-running each layer + "
+                   "AdamW on the adapter cores; attention = torch SDPA"}
+    del model, state
     torch.cuda.empty_cache()
     return out
 

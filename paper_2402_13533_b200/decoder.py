@@ -23,6 +23,7 @@ import torch
 import torch.nn.functional as F
 
 from . import glue
+from .optim import AdamWConfig, AdamWState, adamw_step
 from .linear import QuantizedLinear, TTLinear, TTSpec, attach_tt_adapter, group_backward, group_forward
 from .quant import quantize_rows
 
@@ -130,6 +131,40 @@ class DecoderStack:
     def adapters(self):
         out = [m for layer in self.layers for m in layer.mats.values()]
         return out + [self.head]
+
+    def trainable(self) -> dict:
+        """name -> Param of every adapter core (configure_trainable("lora_finetune"), trainer.py:133-147)."""
+        return {p.name: p for m in self.adapters() for p in m.params() if p.trainable}
+
+    def train_step(self, tokens, targets, state: AdamWState | None = None, config: AdamWConfig | None = None,
+                   micro_batches: int = 1):
+        """trainer.train_step (trainer.py:165-199) with the PER_LAYER policy: per micro-batch (np.array_split
+        of the rows) forward, cross-entropy and backward with recompute, gradients summed and divided by the
+        micro-batch count, then one AdamW update of the adapter cores.  Returns (mean loss, state)."""
+        params = self.trainable()
+        if state is None:
+            state = AdamWState(params)
+        if micro_batches < 1:
+            raise ValueError("micro_batches must be >= 1")
+        total: dict = {}
+        loss_sum = 0.0
+        b = tokens.shape[0]
+        sizes = [b // micro_batches + (1 if i < b % micro_batches else 0) for i in range(micro_batches)]
+        start = 0
+        for n in sizes:
+            loss, grads = self.train_step_grads(tokens[start:start + n], targets[start:start + n])
+            start += n
+            loss_sum += loss
+            for k, g in grads.items():
+                if k in total:
+                    total[k] += g
+                else:
+                    total[k] = g
+        if micro_batches > 1:
+            for g in total.values():
+                g /= micro_batches
+        adamw_step(state, params, total, config or AdamWConfig())
+        return loss_sum / micro_batches, state
 
     def rope_tables(self, length, device):
         """_rope_tables (transformer.py:499-503): angles in float64, tables stored as float32."""

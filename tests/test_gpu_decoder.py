@@ -164,3 +164,29 @@ def test_decoder_rejects_long_sequences(setup):
     long = torch.zeros((1, CFG.max_seq + 1), dtype=torch.long, device="cuda")
     with pytest.raises(ValueError):
         model.train_step_grads(long, long)
+
+
+def test_decoder_train_step_updates_adapters_only(setup):
+    """train_step = grads + AdamW (trainer.py:94-121): every adapter core moves, bases / norms / embedding do not,
+    and the update equals adamw_step applied to the same gradients."""
+    from paper_2402_13533_b200.optim import AdamWConfig, AdamWState, adamw_step
+
+    model, tokens, targets = setup
+    params = model.trainable()
+    before = {k: p.data.clone() for k, p in params.items()}
+    embed0 = model.embed.clone()
+    codes0 = model.layers[0].mats["wq"].base.q.codes.clone()
+    cfg = AdamWConfig(lr=1e-3)
+    _, grads = model.train_step_grads(tokens, targets)
+    shadow = {k: type(p)(p.name, p.data.clone(), True) for k, p in params.items()}
+    st2 = AdamWState(shadow)
+    adamw_step(st2, shadow, grads, cfg)
+    for k, p in params.items():  # restore, then run the fused step from the same state
+        p.data.copy_(before[k])
+    loss, st = model.train_step(tokens, targets, config=cfg)
+    assert st.step == 1 and loss > 0
+    for k, p in params.items():
+        assert not torch.equal(p.data, before[k]), k
+        assert torch.equal(p.data, shadow[k].data), k
+    assert torch.equal(model.embed, embed0)
+    assert torch.equal(model.layers[0].mats["wq"].base.q.codes, codes0)

@@ -1,7 +1,7 @@
 """BASELINE config 4 on one GPU: the 32-layer Llama-2-7B-shaped decoder stack (hidden 4096, 32 heads, FFN 11008,
 vocab 32000), int8 bases + TT adapters (r = 8) on every linear and the head, PER_LAYER recompute; 4 x 2048
 tokens per GPU (the [32, 2048] global batch over 8 GPUs).  One step = forward storing each layer's input,
-cross-entropy, backward re-running each layer (paper_2402_13533_b200.decoder).
+cross-entropy, backward re-running each layer, AdamW on the adapter cores (DecoderStack.train_step).
 
     python tools/decoder_bench.py [--layers 32] [--batch 4] [--seq 2048] [--steps 3] [--warmup 2]
 
@@ -36,28 +36,29 @@ def main():
     g = torch.Generator(device="cuda").manual_seed(2)
     tokens = torch.randint(0, cfg.vocab, (a.batch, a.seq), generator=g, device="cuda")
     targets = torch.randint(0, cfg.vocab, (a.batch, a.seq), generator=g, device="cuda")
+    state = None
     for _ in range(a.warmup):
-        model.train_step_grads(tokens, targets)
+        _, state = model.train_step(tokens, targets, state)
     torch.cuda.synchronize()
     torch.cuda.reset_peak_memory_stats()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     losses = []
     for _ in range(a.steps):
-        loss, grads = model.train_step_grads(tokens, targets)
+        loss, state = model.train_step(tokens, targets, state)
         losses.append(loss)
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / a.steps
     T = a.batch * a.seq
     print(json.dumps({
-        "metric": "decoder fwd+bwd (per-layer recompute) tokens/s", "value": T / (ms / 1e3), "unit": "tokens/s",
+        "metric": "decoder training step (per-layer recompute + AdamW) tokens/s", "value": T / (ms / 1e3), "unit": "tokens/s",
         "ms_per_step": ms, "steps": a.steps, "warmup": a.warmup, "dtype": "int8 weights x bf16 activations",
         "config": {"workload": f"llama2-7b decoder, {a.layers} layers, vocab 32000, TT r=8 on all linears + head, "
                                f"int8 bases, PER_LAYER recompute, [{a.batch}, {a.seq}] tokens/GPU",
                    "baseline_config": 4},
         "peak_mem_gb": torch.cuda.max_memory_allocated() / 1e9, "loss": losses[-1],
-        "adapter_tensors": len(grads)}))
+        "adapter_tensors": len(state.names)}))
 
 
 if __name__ == "__main__":
