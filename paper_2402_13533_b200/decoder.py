@@ -146,23 +146,23 @@ class DecoderStack:
             state = AdamWState(params)
         if micro_batches < 1:
             raise ValueError("micro_batches must be >= 1")
-        total: dict = {}
+        # cores live in the optimizer's flat float32 buffer and the kernels accumulate their gradients
+        # straight into its flat gradient buffer (no per-tensor gather / copy-back around the update)
+        if getattr(state, "_bound_to", None) is not self:
+            state._grad_views = state.bind(params)
+            state._bound_to = self
+        state.gflat.zero_()
+        total = dict(state._grad_views)
         loss_sum = 0.0
         b = tokens.shape[0]
         sizes = [b // micro_batches + (1 if i < b % micro_batches else 0) for i in range(micro_batches)]
         start = 0
         for n in sizes:
-            loss, grads = self.train_step_grads(tokens[start:start + n], targets[start:start + n])
+            loss, _ = self.train_step_grads(tokens[start:start + n], targets[start:start + n], grads=total)
             start += n
             loss_sum += loss
-            for k, g in grads.items():
-                if k in total:
-                    total[k] += g
-                else:
-                    total[k] = g
         if micro_batches > 1:
-            for g in total.values():
-                g /= micro_batches
+            state.gflat.div_(micro_batches)
         adamw_step(state, params, total, config or AdamWConfig())
         return loss_sum / micro_batches, state
 
@@ -174,10 +174,11 @@ class DecoderStack:
         ang = torch.arange(length, dtype=torch.float64, device=device)[:, None] * freqs[None, :]
         return torch.cos(ang).float().contiguous(), torch.sin(ang).float().contiguous()
 
-    def train_step_grads(self, tokens, targets, policy: str = "per_layer"):
+    def train_step_grads(self, tokens, targets, policy: str = "per_layer", grads: dict | None = None):
         """One forward + cross-entropy + backward (model_forward / cross_entropy_grad / model_backward).
         policy "per_layer" keeps only each layer's input and recomputes; "store_all" keeps every layer's
-        activations.  Returns (loss, grads dict of the adapter cores)."""
+        activations.  Gradients accumulate into `grads` (new dict if None; preallocated float32 tensors are
+        accumulated into by the kernels).  Returns (loss, grads dict of the adapter cores)."""
         cfg = self.config
         if tokens.dim() != 2:
             raise ValueError(f"tokens must be 2-D, got shape {tuple(tokens.shape)}")
@@ -189,7 +190,7 @@ class DecoderStack:
         keep_all = policy == "store_all"
         shape = (b, l, cfg.heads)
         rope = self.rope_tables(l, tokens.device)
-        grads: dict = {}
+        grads = {} if grads is None else grads
         stored = []
         x = self.embed[tokens.reshape(-1)]
         for layer in self.layers:

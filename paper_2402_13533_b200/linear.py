@@ -206,9 +206,11 @@ def linear_forward_saving(q: QuantizedMatrix, adapter, x):
 
 
 def linear_backward(q: QuantizedMatrix, adapter, x, dy, *, want_dx: bool = True, want_grads: bool = True,
-                    debug: bool = False, saved: torch.Tensor | None = None):
+                    debug: bool = False, saved: torch.Tensor | None = None, grad_out=None):
     """dx = dy·deq(W) + dy·W_t and the adapter-core gradients through qa_linear_backward.
 
+    grad_out: float32 tensors shaped like the cores; the gradients are then added into them in the kernels
+    (the C ABI's accumulate flag) and None is returned in their place.
     Returns (dx or None, [dG_k] or None[, dx_f32 when debug])."""
     dy = _as_device(dy, q.device)
     lead = tuple(dy.shape[:-1])
@@ -232,8 +234,10 @@ def linear_backward(q: QuantizedMatrix, adapter, x, dy, *, want_dx: bool = True,
         _check_cores(spec, cores)
         ttc = spec.as_c(cores)
         if want_grads:
-            grads = [torch.empty(spec.core_shape(k), dtype=torch.float32, device=dev) for k in range(spec.d)]
+            grads = grad_out if grad_out is not None else \
+                [torch.empty(spec.core_shape(k), dtype=torch.float32, device=dev) for k in range(spec.d)]
             gptrs = (ctypes.c_void_p * _lib.QA_TT_MAX_D)(*[g.data_ptr() for g in grads])
+    accumulate = 1 if (grad_out is not None and grads is not None) else 0
     L = _lib.lib()
     nbytes = L.qa_linear_workspace_bytes(ctypes.byref(wc), ctypes.byref(ttc) if ttc else None, T)
     if nbytes == 0:
@@ -244,19 +248,21 @@ def linear_backward(q: QuantizedMatrix, adapter, x, dy, *, want_dx: bool = True,
                                         dy2.data_ptr(), _dtype_code(dy2), T,
                                         dx.data_ptr() if dx is not None else None,
                                         ctypes.cast(gptrs, ctypes.POINTER(ctypes.c_void_p)) if gptrs is not None
-                                        else None, 0, saved.data_ptr(), saved.numel() * 4, ws.data_ptr(),
+                                        else None, accumulate, saved.data_ptr(), saved.numel() * 4, ws.data_ptr(),
                                         ws.numel(), _stream_ptr(dev))
         _lib.check(st, "qa_linear_backward_saved")
         out_dx = None if dx is None else dx.reshape(*lead, q.cols)
+        grads = None if accumulate else grads
         return (out_dx, grads, None) if debug else (out_dx, grads)
     st = L.qa_linear_backward(ctypes.byref(wc), ctypes.byref(ttc) if ttc else None,
                               x2.data_ptr() if x2 is not None else None,
                               _dtype_code(x2) if x2 is not None else QA_F32, dy2.data_ptr(), _dtype_code(dy2), T,
                               dx.data_ptr() if dx is not None else None,
                               dx32.data_ptr() if dx32 is not None else None,
-                              ctypes.cast(gptrs, ctypes.POINTER(ctypes.c_void_p)) if gptrs is not None else None, 0,
-                              ws.data_ptr(), ws.numel(), _stream_ptr(dev))
+                              ctypes.cast(gptrs, ctypes.POINTER(ctypes.c_void_p)) if gptrs is not None else None,
+                              accumulate, ws.data_ptr(), ws.numel(), _stream_ptr(dev))
     _lib.check(st, "qa_linear_backward")
+    grads = None if accumulate else grads
     out_dx = None
     if want_dx:
         out_dx = (dx32 if dy2.dtype == torch.float32 else dx).reshape(*lead, q.cols)
@@ -379,6 +385,18 @@ class TTLinear:
         for p, g in zip(self.cores, dcores):
             _accumulate(grads, p, g)
 
+    def _grad_dest(self, grads: dict):
+        """Preallocated float32 gradient buffers for every core (e.g. views of an optimizer's flat gradient
+        buffer), or None: then the kernels accumulate into them directly instead of returning new tensors."""
+        out = []
+        for p in self.cores:
+            g = grads.get(p.name)
+            if not p.trainable or not (isinstance(g, torch.Tensor) and g.is_cuda and g.dtype == torch.float32 and
+                                       g.is_contiguous() and g.shape == p.data.shape):
+                return None
+            out.append(g)
+        return out if out else None
+
     def _tag(self, x):
         return (x.data_ptr(), tuple(x.shape), x._version, tuple(p.data._version for p in self._params_for_tag()))
 
@@ -411,8 +429,11 @@ class TTLinear:
         if self.merged:
             raise ModelError(f"{self.name}: merged adapter is inference-only")
         saved = self._take_saved(x)
-        dx, dcores = linear_backward(self.base.q, (self.spec, self._core_tensors()), x, dy, saved=saved)
-        self._scatter_grads(grads, dcores)
+        dest = self._grad_dest(grads)
+        dx, dcores = linear_backward(self.base.q, (self.spec, self._core_tensors()), x, dy, saved=saved,
+                                     grad_out=dest)
+        if dest is None:
+            self._scatter_grads(grads, dcores)
         return dx
 
     def astype(self, dtype):
@@ -455,6 +476,9 @@ class LoraLinear(TTLinear):
 
     def _core_tensors(self):
         return self._lora_cores(self.down.data, self.up.data)
+
+    def _grad_dest(self, grads: dict):
+        return None  # the trainable tensors are .down / .up (transposed cores)
 
     def _scatter_grads(self, grads: dict, dcores):
         r, k = self.down.data.shape
@@ -566,8 +590,11 @@ def group_backward(members, x, dys, grads: dict, step: int = 0):
     L = _lib.lib()
     savedl = [m._take_saved(x) for m in members]
     dxs = [torch.empty((T, q0.cols), dtype=torch.bfloat16, device=dev) for _ in members]
-    gr = [[torch.empty(m.spec.core_shape(k), dtype=torch.float32, device=dev) for k in range(m.spec.d)]
-          for m in members]
+    dests = [m._grad_dest(grads) for m in members]
+    accumulate = 1 if all(d is not None for d in dests) else 0
+    gr = dests if accumulate else \
+        [[torch.empty(m.spec.core_shape(k), dtype=torch.float32, device=dev) for k in range(m.spec.d)]
+         for m in members]
     nb = L.qa_group_workspace_bytes(n, W, Tt, T)
     if nb == 0:
         raise ModelError(f"invalid group: {L.qa_last_error().decode()}")
@@ -579,8 +606,9 @@ def group_backward(members, x, dys, grads: dict, step: int = 0):
     S = (ctypes.c_void_p * n)(*[sv.data_ptr() if sv is not None else None for sv in savedl])
     SB = (ctypes.c_size_t * n)(*[sv.numel() * 4 if sv is not None else 0 for sv in savedl])
     dy_dtype = _dtype_code(dys2[0])
-    _lib.check(L.qa_group_backward(n, W, Tt, x2.data_ptr(), _dtype_code(x2), DY, dy_dtype, T, DX, DC, 0, S, SB,
-                                   ws.data_ptr(), ws.numel(), _stream_ptr(dev)), "qa_group_backward")
-    for m, g in zip(members, gr):
-        m._scatter_grads(grads, g)
+    _lib.check(L.qa_group_backward(n, W, Tt, x2.data_ptr(), _dtype_code(x2), DY, dy_dtype, T, DX, DC, accumulate, S,
+                                   SB, ws.data_ptr(), ws.numel(), _stream_ptr(dev)), "qa_group_backward")
+    if not accumulate:
+        for m, g in zip(members, gr):
+            m._scatter_grads(grads, g)
     return [d.reshape(*lead, q0.cols) for d in dxs]

@@ -57,6 +57,24 @@ class AdamWState:
         self.flags = torch.zeros(max(len(self.names), 1), dtype=torch.int32, device=dev)
         self.index = {k: i for i, k in enumerate(self.names)}
 
+    def bind(self, params: dict) -> dict:
+        """Make every parameter's data a view of the flat float32 working copy (values unchanged) and return
+        name -> view of the flat gradient buffer.  A training loop that zeroes `gflat`, lets the backward
+        accumulate into those views and calls adamw_step skips the per-tensor gather and copy-back."""
+        self.flat.copy_(self.master.to(torch.float32))
+        views = {}
+        for k in self.names:
+            i = self.index[k]
+            a, b = self.offsets[i], self.offsets[i + 1]
+            shape = params[k].data.shape
+            params[k].data = self.flat[a:b].view(shape)
+            views[k] = self.gflat[a:b].view(shape)
+        return views
+
+    def _is_view(self, t: torch.Tensor, base: torch.Tensor, i: int) -> bool:
+        return (t.data_ptr() == base.data_ptr() + base.element_size() * self.offsets[i]
+                and t.numel() == self.sizes[i] and t.is_contiguous())
+
 
 def adamw_step(state: AdamWState, params: dict, grads: dict, config: AdamWConfig):
     """trainer.py:94-121 on the device."""
@@ -71,10 +89,11 @@ def adamw_step(state: AdamWState, params: dict, grads: dict, config: AdamWConfig
     dev = state.flat.device
     sp = _stream_ptr(dev)
     # gather the gradients into the flat buffer (tensors without a gradient keep a zero slice and are
-    # not touched below)
+    # not touched below); gradients that already are its slices (AdamWState.bind) need no copy
     for k in names:
         i = state.index[k]
-        state.gflat[state.offsets[i]:state.offsets[i + 1]].copy_(grads[k].reshape(-1).to(torch.float32))
+        if not state._is_view(grads[k], state.gflat, i):
+            state.gflat[state.offsets[i]:state.offsets[i + 1]].copy_(grads[k].reshape(-1).to(torch.float32))
     state.flags.zero_()
     _lib.check(L.qa_nonfinite_segments(state.gflat.data_ptr(), state.seg.data_ptr(), len(state.names),
                                        state.flags.data_ptr(), sp), "qa_nonfinite_segments")
@@ -103,6 +122,7 @@ def adamw_step(state: AdamWState, params: dict, grads: dict, config: AdamWConfig
     for k in todo:
         i = state.index[k]
         p = params[k]
-        p.data.copy_(state.flat[state.offsets[i]:state.offsets[i + 1]].reshape(p.data.shape).to(p.data.dtype))
+        if not state._is_view(p.data, state.flat, i):
+            p.data.copy_(state.flat[state.offsets[i]:state.offsets[i + 1]].reshape(p.data.shape).to(p.data.dtype))
     if stop is not None:
         raise TrainError(f"non-finite gradient for tensor {stop}")

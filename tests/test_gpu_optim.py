@@ -49,3 +49,21 @@ def test_adamw_nonfinite_gradient_names_tensor():
     assert not torch.equal(params[names[0]].data, before[names[0]])
     assert torch.equal(params[names[1]].data, before[names[1]])
     assert torch.equal(params[names[2]].data, before[names[2]])
+
+
+def test_adamw_bound_flat_buffers_match_reference():
+    """AdamWState.bind: parameters become views of the flat working copy and gradients are written into the
+    flat gradient views (the decoder's path, no gather / copy-back) — still bit-identical to the reference."""
+    g, names = _load()
+    params = {k: Param(k, torch.from_numpy(g[f"init__{k}"]).cuda()) for k in names}
+    state = optim.AdamWState(params)
+    views = state.bind(params)
+    for k in names:
+        assert np.array_equal(params[k].data.cpu().numpy(), g[f"init__{k}"])
+    cfg = optim.AdamWConfig(lr=1e-3, weight_decay=0.05)
+    for t in range(3):
+        for k in names:
+            views[k].copy_(torch.from_numpy(g[f"g{t}__{k}"]))
+        optim.adamw_step(state, params, views, cfg)
+        for k in names:
+            assert np.array_equal(params[k].data.cpu().numpy(), g[f"p{t}__{k}"]), (t, k)
