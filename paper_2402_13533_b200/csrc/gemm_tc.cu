@@ -54,6 +54,7 @@ struct KParams {
   int num_ext;      // extension k-blocks (bf16, 64 elements each)
   int prefetch;     // int8 CTA-pair kernel: L2 prefetch of the next tile's operands
   int tma_store;    // CTA-pair kernel: bf16 output through shared memory + TMA stores (tmC)
+  int group_m;      // CTA-pair kernel: tile raster in groups of group_m M-tiles (M fastest inside a group)
   GemmEpilogue e;
 };
 
@@ -630,10 +631,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   const int64_t total = ((p.M + BM2 - 1) / BM2) * n_tn;
   const int64_t cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
   const int my_tiles = cluster < total ? static_cast<int>((total - cluster + nclusters - 1) / nclusters) : 0;
+  const int64_t n_tm = (p.M + BM2 - 1) / BM2;
+  // Grouped raster: the ~74 tiles in flight at a time cover a group_m x (74 / group_m) block of the tile
+  // grid instead of ~1-2 whole tile rows, so the A and B panels they read stay in L2 (row order re-read
+  // every B panel from DRAM once per wave when N / 256 * panel bytes exceeded L2).
   auto coords = [&](int i, int64_t& m0, int64_t& n0) {
     const int64_t t = cluster + static_cast<int64_t>(i) * nclusters;
-    m0 = (t / n_tn) * BM2;
-    n0 = (t % n_tn) * BN;
+    if (p.group_m > 1) {
+      const int64_t per_group = static_cast<int64_t>(p.group_m) * n_tn;
+      const int64_t grp = t / per_group, r = t - grp * per_group;
+      const int64_t gm0 = grp * p.group_m;
+      const int64_t rows = n_tm - gm0 < p.group_m ? n_tm - gm0 : p.group_m;
+      m0 = (gm0 + r % rows) * BM2;
+      n0 = (r / rows) * BN;
+    } else {
+      m0 = (t / n_tn) * BM2;
+      n0 = (t % n_tn) * BN;
+    }
   };
 
   if (warp == 0 && lane == 0) {
@@ -975,6 +989,24 @@ bool tma_store_disabled() {
   return off;
 }
 
+// Raster group of the CTA-pair kernel (M-tiles per group, 1 = row order). Row order keeps every B panel
+// of a tile row in L2 across the ~1-2 tile rows in flight; that breaks once the B panels of one row exceed
+// L2 (dX of the 16384 x 11008 x 4096 down projection re-read B from DRAM every wave: 3.46 GB for 224 MB of
+// operands), while a group of 8 M-tiles keeps both the group's A panels and the in-flight B panels
+// resident (0.92 GB there). Measured: grouping raises DRAM reads where row order already fits, so only
+// shapes whose B row exceeds 64 MB and whose group A panels stay under 32 MB are grouped.
+// QA_GEMM_GROUP_M=<g> forces g.
+int gemm_group_m(int64_t N, int64_t K, int elem_bytes) {
+  static const int forced = [] {
+    const char* v = getenv("QA_GEMM_GROUP_M");
+    return v != nullptr ? atoi(v) : 0;
+  }();
+  if (forced >= 1) return forced;
+  const double panel = 256.0 * double(K) * elem_bytes;  // one 256-row (or 256-column) k-panel
+  const double b_row = double((N + 255) / 256) * panel;
+  return (b_row > 64e6 && 8.0 * panel < 32e6) ? 8 : 1;
+}
+
 // QA_GEMM_2SM=0 keeps the single-CTA persistent kernel (A/B comparisons, triage).
 bool pair_disabled() {
   static const bool off = [] {
@@ -1070,6 +1102,7 @@ int launch(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, in
   p.num_ext = num_ext;
   p.prefetch = prefetch_enabled() ? 1 : 0;
   p.tma_store = 0;
+  p.group_m = gemm_group_m(N, K, KIND == 0 ? 1 : 2);
   p.e = epi;
   const double kalg = KIND == 0 && epi.k_real > 0 ? double(epi.k_real) : double(K);
   LaunchScope scope(KIND == 0 ? kGemmI8 : kGemmBF16, 2.0 * double(M) * double(N) * kalg, s);
