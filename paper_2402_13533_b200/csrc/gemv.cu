@@ -274,7 +274,28 @@ __global__ void __launch_bounds__(GM_WARPS * 32) k_gemv_mma(const uint8_t* __res
     wof = wo[n];
     rs = wrs[n];
   }
+  // adapter operands in shared memory: the last core's columns of this CTA's 16 rows (weights, read
+  // before the wait) and Zlast[t, h, :] of the row block (one h: 16 | Ml), read right after it
+  __shared__ float sG[16][32], sZ[8][32];
+  const int64_t h0 = Gl != nullptr ? n0 / Ml : 0;
+  if (Gl != nullptr)
+    for (int idx = threadIdx.x; idx < 16 * Cl; idx += GM_WARPS * 32) {
+      const int r = idx / Cl, b = idx - (idx / Cl) * Cl;
+      const int64_t nr = n0 + r < N ? n0 + r : N - 1;
+      sG[r][b] = __ldg(Gl + b * Ml + (nr - h0 * Ml));
+    }
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (Gl != nullptr && static_cast<int>(threadIdx.x) < T * Cl) {
+    const int tt = threadIdx.x / Cl, b = threadIdx.x - (threadIdx.x / Cl) * Cl;
+    sZ[tt][b] = ld_dep_f32(zl + tt * ldz + h0 * Cl + b);
+  }
+  float sxt = 0.f, oxr = 0.f;
+  int32_t rx = 0;
+  if (live) {
+    sxt = ld_dep_f32(sx + t);
+    oxr = ld_dep_f32(ox + t);
+    rx = ld_dep_s32(rsx + t);
+  }
   const bool tok = g < T;
   const uint8_t* px = xc + (tok ? g : 0) * ldx + tq * 16;
   int acc[4] = {0, 0, 0, 0};
@@ -304,29 +325,17 @@ __global__ void __launch_bounds__(GM_WARPS * 32) k_gemv_mma(const uint8_t* __res
   uint32_t a = 0;
 #pragma unroll
   for (int w = 0; w < GM_WARPS; ++w) a += static_cast<uint32_t>(red[w][rr][t]);
-  // adapter: y2[t, n] = Σ_b Zlast[t, h, b] Glast[b, i], n = h Ml + i (loads issued together)
+  // adapter: y2[t, n] = Σ_b Zlast[t, h, b] Glast[b, i], n = h Ml + i
   float y2 = 0.f;
-  if (Gl != nullptr) {
-    const int64_t hz = n / Ml, i = n - hz * Ml;
-    const float* z = zl + t * ldz + hz * Cl;
-    float zv[32], gl[32];
-#pragma unroll
-    for (int b = 0; b < 32; ++b) {
-      zv[b] = b < Cl ? ld_dep_f32(z + b) : 0.f;
-      gl[b] = b < Cl ? __ldg(Gl + b * Ml + i) : 0.f;
-    }
-#pragma unroll
-    for (int b = 0; b < 32; ++b) y2 = fmaf(zv[b], gl[b], y2);
-  }
+  if (Gl != nullptr)
+    for (int b = 0; b < Cl; ++b) y2 = fmaf(sZ[t][b], sG[rr][b], y2);
   // the tcgen05 GEMM's exact int32 centring + fp32 dequant epilogue (gemm_tc.cu)
   const int zp_row = 128, zp_col = BITS == 8 ? 128 : 8;
   const int kr = static_cast<int>(K);
   const float owt = wof + static_cast<float>(zp_col) * sw;
   const float colC = fmaf(sw, static_cast<float>(rs - zp_col * kr), static_cast<float>(kr) * owt);
   const int32_t colD = zp_row * rs;
-  const float sxt = ld_dep_f32(sx + t);
-  const float oxt = ld_dep_f32(ox + t) + static_cast<float>(zp_row) * sxt;
-  const int32_t rx = ld_dep_s32(rsx + t);
+  const float oxt = oxr + static_cast<float>(zp_row) * sxt;
   const float rsxc = static_cast<float>(rx - zp_row * kr);
   const int32_t ibase = zp_row * zp_col * kr - zp_col * rx;
   const int32_t accc = static_cast<int32_t>(a) + ibase - colD;
@@ -385,7 +394,8 @@ cudaError_t launch_gemv(const uint8_t* xc, int64_t ldx, int64_t T, const float* 
     const char* v = getenv("QA_GEMV_MMA");
     return v != nullptr && v[0] == '0';
   }();
-  if (K % 64 == 0 && !dp4a_only) {
+  // the tensor-core pass keeps one Zlast block per 16-row tile (16 | Ml, or a single block) and Cl <= 32
+  if (K % 64 == 0 && !dp4a_only && (Gl == nullptr || ((Ml % 16 == 0 || Ml >= N) && Cl <= 32))) {
     cfg.gridDim = dim3(static_cast<unsigned>((N + 15) / 16));
     cfg.blockDim = dim3(GM_WARPS * 32);
     if (bits == 8)
