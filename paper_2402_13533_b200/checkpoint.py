@@ -30,7 +30,8 @@ from . import _lib
 from .linear import LoraLinear, QuantizedLinear, TTLinear, TTSpec
 from .quant import QuantizedMatrix, _stream_ptr
 
-__all__ = ["CheckpointError", "MAGIC", "VERSION", "ALIGN", "Checkpoint", "read_checkpoint", "load_quantized",
+__all__ = ["CheckpointError", "MAGIC", "VERSION", "ALIGN", "Checkpoint", "read_checkpoint", "quantized_from_arrays",
+           "load_quantized",
            "load_lora", "load_tt", "save_checkpoint", "collect_backends"]
 
 MAGIC = b"LRLM"
@@ -121,6 +122,26 @@ def _upload(arr: np.ndarray, dtype, device) -> torch.Tensor:
     return host.to(device=device, dtype=dtype, non_blocking=True)
 
 
+def quantized_from_arrays(codes, scale, offset, rows: int, cols: int, bits: int, device="cuda") -> QuantizedMatrix:
+    """A quantised base from the reference's host arrays (QuantizedMatrix fields, quant.py:55-70: u8 codes,
+    4-bit packed two per byte, f32 scale / offset) into device buffers, codes byte for byte; the epilogue's
+    Σcodes term from qa_code_rowsum."""
+    if bits not in (4, 8):
+        raise CheckpointError(f"bits must be 4 or 8, got {bits}")
+    packed = (cols + 1) // 2 if bits == 4 else cols
+    codes = np.asarray(codes, dtype=np.uint8)
+    if codes.size != rows * packed:
+        raise CheckpointError(f"{codes.size} code bytes for a {rows}x{cols} {bits}-bit grid")
+    dev = torch.device(device)
+    c = _upload(codes.reshape(rows, packed), torch.uint8, dev)
+    sc = _upload(np.asarray(scale, dtype=np.float32).reshape(rows), torch.float32, dev)
+    of = _upload(np.asarray(offset, dtype=np.float32).reshape(rows), torch.float32, dev)
+    rowsum = torch.empty(rows, dtype=torch.int32, device=dev)
+    _lib.check(_lib.lib().qa_code_rowsum(c.data_ptr(), rows, cols, bits, rowsum.data_ptr(), _stream_ptr(dev)),
+               "qa_code_rowsum")
+    return QuantizedMatrix(rows, cols, bits, c, sc, of, rowsum)
+
+
 def load_quantized(ck: Checkpoint, name: str, device="cuda") -> QuantizedMatrix:
     """A u8q / u4q base straight into device buffers (checkpoint.py:186-197): codes byte for byte."""
     codes, ent = ck.raw(name, ("u8q", "u4q"))
@@ -129,14 +150,8 @@ def load_quantized(ck: Checkpoint, name: str, device="cuda") -> QuantizedMatrix:
     packed = (cols + 1) // 2 if bits == 4 else cols
     if codes.size != rows * packed:
         raise CheckpointError(f"{name}: {codes.size} code bytes for a {rows}x{cols} {ent['dtype']} grid")
-    dev = torch.device(device)
-    c = _upload(codes.reshape(rows, packed), torch.uint8, dev)
-    scale = _upload(ck.raw(name + ".scale", "f32")[0], torch.float32, dev)
-    offset = _upload(ck.raw(name + ".offset", "f32")[0], torch.float32, dev)
-    rowsum = torch.empty(rows, dtype=torch.int32, device=dev)
-    _lib.check(_lib.lib().qa_code_rowsum(c.data_ptr(), rows, cols, bits, rowsum.data_ptr(), _stream_ptr(dev)),
-               "qa_code_rowsum")
-    return QuantizedMatrix(rows, cols, bits, c, scale, offset, rowsum)
+    return quantized_from_arrays(codes, ck.raw(name + ".scale", "f32")[0], ck.raw(name + ".offset", "f32")[0],
+                                 rows, cols, bits, device)
 
 
 def load_lora(ck: Checkpoint, slot: str, device="cuda") -> LoraLinear:
