@@ -22,7 +22,7 @@ from dataclasses import dataclass
 import torch
 import torch.nn.functional as F
 
-from . import glue
+from . import dp, glue
 from .optim import AdamWConfig, AdamWState, adamw_step
 from .linear import QuantizedLinear, TTLinear, TTSpec, attach_tt_adapter, group_backward, group_forward
 from .quant import quantize_rows
@@ -137,10 +137,14 @@ class DecoderStack:
         return {p.name: p for m in self.adapters() for p in m.params() if p.trainable}
 
     def train_step(self, tokens, targets, state: AdamWState | None = None, config: AdamWConfig | None = None,
-                   micro_batches: int = 1):
+                   micro_batches: int = 1, process_group=None):
         """trainer.train_step (trainer.py:165-199) with the PER_LAYER policy: per micro-batch (np.array_split
         of the rows) forward, cross-entropy and backward with recompute, gradients summed and divided by the
-        micro-batch count, then one AdamW update of the adapter cores.  Returns (mean loss, state)."""
+        micro-batch count, then one AdamW update of the adapter cores.  With a torch.distributed process
+        group of G > 1 ranks (data parallelism, each rank holding its shard of the batch), the flat gradient
+        buffer is all-reduced and divided by G before the update (the fixed-order average of
+        distsim.federated_round, distsim.py:309-314), so every replica applies the same update.
+        Returns (mean loss of this rank's shard, state)."""
         params = self.trainable()
         if state is None:
             state = AdamWState(params)
@@ -163,6 +167,8 @@ class DecoderStack:
             loss_sum += loss
         if micro_batches > 1:
             state.gflat.div_(micro_batches)
+        if process_group is not None:
+            dp.allreduce_mean_(state.gflat, process_group)
         adamw_step(state, params, total, config or AdamWConfig())
         return loss_sum / micro_batches, state
 
