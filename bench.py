@@ -773,12 +773,25 @@ def main():
             xd = {kd: torch.randn((td, d), generator=dgen, device=dev).to(torch.bfloat16) for kd, d in INPUT_DIMS.items()}
             yd = {nm: torch.empty((td, n), dtype=torch.bfloat16, device=dev) for nm, n, _, _ in LINEARS_7B}
 
-            def dstep():
-                for name, _, _, kind in LINEARS_7B:
-                    m = mats[name]
-                    _lib.check(lib.qa_linear_forward(ctypes.byref(m["wc"]), ctypes.byref(m["ttc"]), xd[kind].data_ptr(),
-                                                     BF16, td, yd[name].data_ptr(), None, None, None, ws.data_ptr(),
-                                                     ws_bytes, sptr), "decode forward")
+            dgroups = {}
+            for gnames in GROUPS_FWD:
+                if len(gnames) > 1:
+                    gd = groups[gnames]
+                    dgroups[gnames] = (ctypes.c_void_p * gd["n"])(*[yd[g].data_ptr() for g in gnames])
+
+            def dstep():  # as a decoder layer calls them: q/k/v and up/gate as shared-input groups
+                for gnames in GROUPS_FWD:
+                    if len(gnames) == 1:
+                        m = mats[gnames[0]]
+                        _lib.check(lib.qa_linear_forward(ctypes.byref(m["wc"]), ctypes.byref(m["ttc"]),
+                                                         xd[m["kind"]].data_ptr(), BF16, td, yd[gnames[0]].data_ptr(),
+                                                         None, None, None, ws.data_ptr(), ws_bytes, sptr),
+                                   "decode forward")
+                    else:
+                        gd = groups[gnames]
+                        _lib.check(lib.qa_group_forward(gd["n"], gd["W"], gd["T"], xd[gd["kind"]].data_ptr(), BF16, td,
+                                                        dgroups[gnames], None, None, ws.data_ptr(), ws_bytes, sptr),
+                                   "decode group forward")
 
             for _ in range(5):
                 dstep()
@@ -793,8 +806,9 @@ def main():
             wbytes = sum(mats[nm]["q"].codes.numel() + 8 * n for nm, n, _, _ in LINEARS_7B)
             decode[f"tokens_{td}"] = {"ms_per_step": ms, "tokens_per_s": td / (ms / 1e3),
                                       "weight_gbs": wbytes / ms / 1e6, "frac_of_hbm": wbytes / ms / 1e6 / peaks["hbm_gbs"]}
-        decode["note"] = ("forward of the 7 linears for 1 / 8 tokens (int8 codes + TT adapter), dp4a matrix-vector pass; "
-                          "weight_gbs counts the code bytes read per step")
+        decode["note"] = ("forward of the 7 linears for 1 / 8 tokens (int8 codes + TT adapter; q/k/v and up/gate as "
+                          "shared-input groups): act-quant prologue + tensor-core matrix-vector pass per linear, chained "
+                          "with programmatic dependent launches; weight_gbs counts the code bytes read per step")
 
     # the merge kernel (north star step 6) on BASELINE config 5's 70B linear set (int4, TT r = 8), outside
     # the timed region: algorithmic bytes = codes in + bf16 W' out, CUDA events, warm

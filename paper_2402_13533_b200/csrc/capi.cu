@@ -436,7 +436,7 @@ namespace qa {
 namespace {
 int linear_forward_impl(const qa_qweight* w, const qa_tt* tt, const void* x, int x_dtype, int64_t tokens, void* y,
                         int32_t* acc_i32, float* y_f32, float* y2_f32, float* z1_save, void* workspace,
-                        size_t workspace_bytes, void* stream) {
+                        size_t workspace_bytes, void* stream, bool chain_prologue = false) {
   QA_TRY(check_weight(w));
   if (tokens == 0) return QA_OK;  // empty batch: nothing to do (pointers may be null)
   if (x == nullptr || tokens < 0 || (x_dtype != QA_F32 && x_dtype != QA_BF16) || w->rowsum == nullptr) {
@@ -475,7 +475,7 @@ int linear_forward_impl(const qa_qweight* w, const qa_tt* tt, const void* x, int
       float* zlw = P.fd == 3 ? P.z2 : (z1_save != nullptr ? z1_save : P.zf);
       ldz = P.fd == 3 ? int64_t(P.H) * P.C : P.K2;
       QA_TRY_CUDA(launch_decode_prep(x, T, K, P.xcodes, P.Kp, P.sx, P.ox, P.rsx, tt->cores[0], P.J1, P.R1,
-                                     tt->cores[1], P.fd, P.H, P.C, z1_save, zlw, ldz, s),
+                                     tt->cores[1], P.fd, P.H, P.C, z1_save, zlw, ldz, s, chain_prologue),
                   "decode prologue");
       zl = zlw;
       gl = tt->cores[P.fd - 1];
@@ -925,14 +925,21 @@ int qa_group_forward(int n, const qa_qweight* const* w, const qa_tt* const* tt, 
     return QA_ERR_WORKSPACE;
   }
   QA_TRY(plan_group(n, w, tt, tokens, workspace, false, x, &G));
-  const bool fast = G.fast && x_dtype == QA_BF16;
+  // decode-size batches: every member through its prologue + matrix-vector pass, chained so that member
+  // i + 1's prologue (its own workspace region, reading only x and its cores) runs while member i's pass
+  // streams its weights (programmatic dependent launches, decode prologue / gemv.cu)
+  bool decode = x_dtype == QA_BF16 && reinterpret_cast<uintptr_t>(x) % 16 == 0;
+  for (int i = 0; i < n && decode; ++i)
+    decode = gemv_ok(tokens, w[i]->cols, w[i]->bits) && (tt[i] == nullptr || (G.P[i].fast && G.P[i].C <= 32));
+  const bool fast = G.fast && x_dtype == QA_BF16 && !decode;
   if (!fast) {  // the members' single-linear forwards
     for (int i = 0; i < n; ++i) {
       const size_t need = G.P[i].fast ? sizeof(float) * static_cast<size_t>(tokens) * G.P[i].K2 : 0;
       float* sv = (saved != nullptr && saved[i] != nullptr && need > 0 && saved_bytes != nullptr &&
                    saved_bytes[i] >= need) ? static_cast<float*>(saved[i]) : nullptr;
       QA_TRY(linear_forward_impl(w[i], tt[i], x, x_dtype, tokens, y[i], nullptr, nullptr, nullptr, sv,
-                                 reinterpret_cast<char*>(G.P[i].xcodes) - 0, G.P[i].bytes, stream));
+                                 reinterpret_cast<char*>(G.P[i].xcodes) - 0, G.P[i].bytes, stream,
+                                 decode && i > 0 && tt[i] != nullptr));
     }
     return QA_OK;
   }

@@ -237,6 +237,8 @@ __global__ void __launch_bounds__(GM_WARPS * 32) k_gemv_mma(const uint8_t* __res
   using W = typename GmW<BITS>::T;
   constexpr int SB = BITS == 8 ? 64 : 32;  // weight bytes per row per 64-column step
   __shared__ int red[GM_WARPS][16][8];
+  // let a chained next prologue (a programmatic dependent, see launch_decode_prep) start right away
+  asm volatile("griddepcontrol.launch_dependents;");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
   const int64_t n0 = static_cast<int64_t>(blockIdx.x) * 16;
   const int64_t ldw = BITS == 8 ? K : K / 2;
@@ -348,6 +350,15 @@ __global__ void __launch_bounds__(GM_WARPS * 32) k_gemv_mma(const uint8_t* __res
 
 }  // namespace
 
+// QA_PDL=0 launches the decode kernels without programmatic dependent launch (A/B, triage).
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("QA_PDL");
+    return !(v != nullptr && v[0] == '0');
+  }();
+  return on;
+}
+
 bool gemv_ok(int64_t T, int64_t K, int bits) {
   static const bool off = [] {
     const char* v = getenv("QA_GEMV");
@@ -371,12 +382,8 @@ cudaError_t launch_gemv(const uint8_t* xc, int64_t ldx, int64_t T, const float* 
   cfg.blockDim = dim3(GV_WARPS * 32);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = s;
-  static const bool pdl = [] {
-    const char* v = getenv("QA_PDL");
-    return !(v != nullptr && v[0] == '0');
-  }();
   cfg.attrs = attr;
-  cfg.numAttrs = pdl ? 1 : 0;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
   const int Ti = static_cast<int>(T);
   cudaError_t e = cudaSuccess;
 #define QA_GV(MM)                                                                                                 \

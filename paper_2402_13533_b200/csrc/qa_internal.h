@@ -70,6 +70,7 @@ cudaError_t launch_code_rowsum(const uint8_t* codes, int64_t rows, int64_t cols,
 
 // decode-size forward (gemv.cu): 1..8 tokens against the stored codes (dp4a), GEMM-identical epilogue
 bool gemv_ok(int64_t T, int64_t K, int bits);
+bool pdl_enabled();
 cudaError_t launch_gemv(const uint8_t* xc, int64_t ldx, int64_t T, const float* sx, const float* ox,
                         const int32_t* rsx, const uint8_t* wc, int64_t N, int64_t K, int bits, const float* ws,
                         const float* wo, const int32_t* wrs, const float* zl, int64_t ldz, const float* Gl,
@@ -77,7 +78,7 @@ cudaError_t launch_gemv(const uint8_t* xc, int64_t ldx, int64_t T, const float* 
 // decode prologue (tt_fast.cu): act-quant of T <= 8 bf16 rows + Z1 + the last core's input Zlast
 cudaError_t launch_decode_prep(const void* x, int64_t T, int64_t K, uint8_t* codes, int64_t ldc, float* sx, float* ox,
                                int32_t* rsx, const float* G1, int J1, int R1, const float* G2, int d, int H, int C,
-                               float* z1out, float* zlast, int64_t ldz, cudaStream_t s);
+                               float* z1out, float* zlast, int64_t ldz, cudaStream_t s, bool chain = false);
 
 // AdamW (optim.cu)
 cudaError_t launch_adamw(float* params, double* master, double* m, double* v, const float* g, int64_t n, double lr,

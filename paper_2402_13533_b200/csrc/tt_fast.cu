@@ -1771,6 +1771,9 @@ __global__ void __launch_bounds__(512) k_decode_prep(const __nv_bfloat16* __rest
   } else {
     if (tid < K2) zlast[t * ldz + tid] = z1s[tid];
   }
+  // when chained behind the previous member's matrix-vector pass: do not complete before it (no-op when
+  // launched normally)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 }  // namespace
@@ -1783,7 +1786,7 @@ extern "C" __attribute__((visibility("default"))) int qa_debug_dp_trace(unsigned
 
 cudaError_t launch_decode_prep(const void* x, int64_t T, int64_t K, uint8_t* codes, int64_t ldc, float* sx, float* ox,
                                int32_t* rsx, const float* G1, int J1, int R1, const float* G2, int d, int H, int C,
-                               float* z1out, float* zlast, int64_t ldz, cudaStream_t s) {
+                               float* z1out, float* zlast, int64_t ldz, cudaStream_t s, bool chain) {
   if (T == 0) return cudaSuccess;
   LaunchScope scope(kQuantize, double(T) * K * 3 + 12.0 * T, s);
   count_launches(1);
@@ -1794,12 +1797,27 @@ cudaError_t launch_decode_prep(const void* x, int64_t T, int64_t K, uint8_t* cod
   // vector / cp.async paths need 16-byte aligned cores (G1 rows of a chunk start at multiples of 32 floats)
   const bool vec = (reinterpret_cast<uintptr_t>(G1) % 16 == 0) && (G2 == nullptr || reinterpret_cast<uintptr_t>(G2) % 16 == 0) &&
                    n2 % 4 == 0;
+  // chain: launched as a programmatic dependent of the previous group member's matrix-vector pass (which
+  // releases its dependents at once); this prologue reads only x and its own cores and writes its own
+  // workspace, and it waits for that pass before exiting (griddepcontrol.wait at its end), so stream order
+  // still holds for every later kernel
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(T));
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = chain && pdl_enabled() ? 1 : 0;
+  const __nv_bfloat16* xb = static_cast<const __nv_bfloat16*>(x);
+  cudaError_t e = cudaSuccess;
 #define QA_DPR(JJ, RR)                                                                                             \
   {                                                                                                                \
     cudaFuncSetAttribute(k_decode_prep<JJ, RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)); \
-    k_decode_prep<JJ, RR><<<static_cast<unsigned>(T), threads, smem, s>>>(static_cast<const __nv_bfloat16*>(x), K, codes, \
-                                                                        ldc, sx, ox, rsx, G1, G2, d, H, C, z1out,    \
-                                                                        zlast, ldz, vec);                            \
+    e = cudaLaunchKernelEx(&cfg, k_decode_prep<JJ, RR>, xb, K, codes, ldc, sx, ox, rsx, G1, G2, d, H, C, z1out,    \
+                           zlast, ldz, vec);                                                                        \
   }
   if (J1 == 4 && R1 == 8)
     QA_DPR(4, 8)
@@ -1810,6 +1828,7 @@ cudaError_t launch_decode_prep(const void* x, int64_t T, int64_t K, uint8_t* cod
   else
     QA_DPR(1, 16)
 #undef QA_DPR
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

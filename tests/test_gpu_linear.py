@@ -275,7 +275,10 @@ def test_full_size_properties():
 
 
 @pytest.mark.parametrize("ns,K,T,r", [((512, 768, 1024), 1024, 200, 8), ((1024, 2048), 512, 77, 8),
-                                      ((512, 256), 1024, 64, 16)])
+                                      ((512, 256), 1024, 64, 16),
+                                      # decode sizes: the members' prologue + matrix-vector passes, chained
+                                      ((512, 768, 1024), 1024, 1, 8), ((1024, 2048), 512, 5, 8),
+                                      ((4096, 4096, 4096), 4096, 8, 8)])
 def test_shared_input_group_matches_members(ns, K, T, r):
     """qa_group_forward / qa_group_backward (one x pass per direction for q / k / v-style members,
     transformer.py:862-874 / 919-944) give each member exactly its single-linear results; r = 16

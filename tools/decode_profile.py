@@ -15,7 +15,7 @@ from paper_2402_13533_b200 import _lib  # noqa: E402
 from paper_2402_13533_b200.linear import TTSpec  # noqa: E402
 from paper_2402_13533_b200.quant import quantize_rows  # noqa: E402
 
-T = int(sys.argv[1]) if len(sys.argv) > 1 else 1
+T = int(sys.argv[1]) if len(sys.argv) > 1 and sys.argv[1].isdigit() else 1
 SHAPES = [("wq", 4096, 4096), ("wk", 4096, 4096), ("wv", 4096, 4096), ("wo", 4096, 4096),
           ("wu", 11008, 4096), ("wg", 11008, 4096), ("wd", 4096, 11008)]
 dev = torch.device("cuda", 0)
@@ -36,7 +36,25 @@ ws = torch.empty(nb, dtype=torch.uint8, device=dev)
 s = torch.cuda.current_stream(dev).cuda_stream
 
 
+GROUP = "--group" in sys.argv
+GROUPS = [(0, 1, 2), (3,), (4, 5), (6,)]  # q/k/v and up/gate share their input
+gsets = []
+for gi in GROUPS:
+    n = len(gi)
+    W = (ctypes.POINTER(_lib.QWeight) * n)(*[ctypes.pointer(mats[i][2]) for i in gi])
+    Tt = (ctypes.POINTER(_lib.TT) * n)(*[ctypes.pointer(mats[i][3]) for i in gi])
+    Y = (ctypes.c_void_p * n)(*[mats[i][5].data_ptr() for i in gi])
+    nb = max(nb, lib.qa_group_workspace_bytes(n, W, Tt, T))
+    gsets.append((n, W, Tt, Y, mats[gi[0]][4]))
+ws = torch.empty(nb, dtype=torch.uint8, device=dev)
+
+
 def step():
+    if GROUP:
+        for n, W, Tt, Y, x in gsets:
+            _lib.check(lib.qa_group_forward(n, W, Tt, x.data_ptr(), 1, T, Y, None, None, ws.data_ptr(), nb, s),
+                       "group forward")
+        return
     for q, cores, wc, ttc, x, y in mats:
         _lib.check(lib.qa_linear_forward(ctypes.byref(wc), ctypes.byref(ttc), x.data_ptr(), 1, T, y.data_ptr(), None,
                                           None, None, ws.data_ptr(), nb, s), "forward")
