@@ -939,11 +939,14 @@ QA_DEV uint32_t aqc_codes_row(const uint8_t* xrow, uint8_t* crow, int64_t nseg, 
 #ifndef QA_AQC_MINB
 #define QA_AQC_MINB 3  // <= 85 registers: 3 CTAs (24 warps) per SM; measured best of {1, 3, 4}
 #endif
+#ifndef QA_AQC_MINB_GROUP
+#define QA_AQC_MINB_GROUP 2  // NA = 2, 3 adapters sharing x: NA sets of Z1 accumulators need <= 128 registers
+#endif
 // NA adapters share the pass over x (the q / k / v or up / gate linears of a decoder layer read the
 // same input, transformer.py:862-874): one set of codes, NA sets of Z1 (fragments of adapter a at
 // frag + a * ad.frag_stride).
 template <int J1, int R1, bool CODES, bool FRAG_SMEM, int NA = 1>
-__global__ void __launch_bounds__(AQC_WARPS * 32, NA == 1 ? QA_AQC_MINB : 2) k_aq_cta(const __nv_bfloat16* __restrict__ x, int64_t T, int64_t K,
+__global__ void __launch_bounds__(AQC_WARPS * 32, NA == 1 ? QA_AQC_MINB : QA_AQC_MINB_GROUP) k_aq_cta(const __nv_bfloat16* __restrict__ x, int64_t T, int64_t K,
                                                             uint8_t* __restrict__ codes, int64_t ldc,
                                                             float* __restrict__ sx, float* __restrict__ ox,
                                                             int32_t* __restrict__ rsx, const uint4* __restrict__ frag_g,
