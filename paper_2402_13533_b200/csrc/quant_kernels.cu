@@ -226,6 +226,26 @@ __global__ void __launch_bounds__(256) k_unpack_pad(const uint8_t* __restrict__ 
   }
 }
 
+// 4-bit codes -> one byte per code for the int8 GEMM operand, 16 codes per thread: 8 packed bytes in
+// (low nibble = even column, quant.py:37-52), 16 bytes out; padding [cols, ld_out) written as 0.
+__global__ void __launch_bounds__(256) k_unpack4_v16(const uint8_t* __restrict__ codes, int64_t ldc, int64_t cols,
+                                                     uint8_t* __restrict__ out, int64_t ld_out) {
+  const int64_t row = blockIdx.y;
+  const int64_t nch = ld_out / 16, nin = cols / 16;
+  for (int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; c < nch;
+       c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    uint4 o = make_uint4(0u, 0u, 0u, 0u);
+    if (c < nin) {
+      const uint2 w = __ldg(reinterpret_cast<const uint2*>(codes + row * ldc) + c);
+      const uint32_t lo0 = w.x & 0x0F0F0F0Fu, hi0 = (w.x >> 4) & 0x0F0F0F0Fu;
+      const uint32_t lo1 = w.y & 0x0F0F0F0Fu, hi1 = (w.y >> 4) & 0x0F0F0F0Fu;
+      o = make_uint4(__byte_perm(lo0, hi0, 0x5140), __byte_perm(lo0, hi0, 0x7362), __byte_perm(lo1, hi1, 0x5140),
+                     __byte_perm(lo1, hi1, 0x7362));
+    }
+    reinterpret_cast<uint4*>(out + row * ld_out)[c] = o;
+  }
+}
+
 template <typename InT>
 __global__ void __launch_bounds__(256) k_to_bf16_pad(const InT* __restrict__ in, int64_t rows, int64_t cols,
                                                      __nv_bfloat16* __restrict__ out, int64_t ld_out,
@@ -320,6 +340,12 @@ cudaError_t launch_unpack_pad(const uint8_t* codes, int64_t rows, int64_t cols, 
   const int64_t ldc = bits == 8 ? cols : (cols + 1) / 2;
   LaunchScope scope(kDequant, double(rows) * (ldc + ld_out), s);
   count_launches(1);
+  if (bits == 4 && cols % 16 == 0 && ld_out % 16 == 0 && reinterpret_cast<uintptr_t>(codes) % 8 == 0 &&
+      reinterpret_cast<uintptr_t>(out) % 16 == 0) {
+    const dim3 g16(static_cast<unsigned>((ld_out / 16 + 255) / 256), static_cast<unsigned>(rows));
+    k_unpack4_v16<<<g16, 256, 0, s>>>(codes, ldc, cols, out, ld_out);
+    return cudaGetLastError();
+  }
   const dim3 grid(static_cast<unsigned>(std::min<int64_t>((ld_out + 255) / 256, 64)), static_cast<unsigned>(rows));
   k_unpack_pad<<<grid, 256, 0, s>>>(codes, ldc, rows, cols, bits, out, ld_out);
   return cudaGetLastError();
