@@ -3651,7 +3651,13 @@ void tt_bwd_fused_plan(int64_t T, int H, int C, int* HR, int* HS, int* TS) {
   *HR = (H + *HS - 1) / *HS;
   const bool ws = C == 8 && !ws_bwd_disabled();  // k_tt_bwd_ws: 16-token tiles, one CTA per SM
   const int64_t tiles = (T + (ws ? WS_TT : FB_TT) - 1) / (ws ? WS_TT : FB_TT);
-  const int per_sm = ws ? 1 : (C == 8 ? 2 : 1);
+  // rank 16: two CTAs per SM (120 registers; measured 9.7 -> 8.7 ms of TT side kernels at config 3 vs
+  // one; three or four were not better). QA_FB16_PER_SM overrides.
+  static const int per_sm16 = [] {
+    const char* v = getenv("QA_FB16_PER_SM");
+    return v != nullptr ? atoi(v) : 2;
+  }();
+  const int per_sm = ws ? 1 : (C == 8 ? 2 : (per_sm16 >= 1 ? per_sm16 : 1));
   int64_t ts = (static_cast<int64_t>(per_sm) * 148 + *HS - 1) / *HS;
   if (ts > tiles) ts = tiles;
   *TS = static_cast<int>(ts < 1 ? 1 : ts);
