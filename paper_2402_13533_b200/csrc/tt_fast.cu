@@ -3773,6 +3773,29 @@ cudaError_t launch_actquant_z1_group(const void* x, int64_t T, int64_t K, bool w
   return cudaGetLastError();
 }
 
+// x-pass occupancy: two CTAs per SM with a 2-stage x ring when ring + dZ1 planes + prefetched dZ1 partials fit
+// in half an SM's shared memory (measured on the 7B set: TT side kernels 1.21 -> 1.14 ms), else one CTA per
+// SM with the deepest ring that fits. QA_DG1_PER_SM / QA_DG1_NSTG force either (A/B).
+struct Dg1Shape {
+  int per_sm, nstg;
+};
+Dg1Shape dg1_shape(size_t planes, size_t raw_bytes) {
+  static const int f_per_sm = [] {
+    const char* e = getenv("QA_DG1_PER_SM");
+    return e != nullptr ? atoi(e) : 0;
+  }();
+  static const int f_nstg = [] {
+    const char* e = getenv("QA_DG1_NSTG");
+    return e != nullptr ? atoi(e) : 0;
+  }();
+  const size_t ring2 = sizeof(__nv_bfloat16) * 2 * DM_ST * DM_LDX;
+  Dg1Shape d{1, DM_NSTG};
+  if (ring2 + planes + raw_bytes <= 112 * 1024) d = Dg1Shape{2, 2};
+  if (f_per_sm >= 1) d.per_sm = f_per_sm;
+  if (f_nstg >= 2) d.nstg = f_nstg;
+  return d;
+}
+
 cudaError_t launch_tt_dg1_group(const void* x, int64_t T, int64_t K, const float* const* dz1, float* const* part,
                                 int S, int HS, __nv_bfloat16* const* dz1b, int64_t ldb, int NA, int* splits_used,
                                 cudaStream_t s) {
@@ -3785,7 +3808,10 @@ cudaError_t launch_tt_dg1_group(const void* x, int64_t T, int64_t K, const float
   count_launches(1);
   const int64_t gx = (K + DM_COLS - 1) / DM_COLS;
   const int64_t stages = (T + DM_ST - 1) / DM_ST;
-  int64_t Sm = (148 + gx - 1) / gx;
+  const size_t raw_bytes = sizeof(float) * 2 * NA * HS * DM_DZT * J1 * R1;
+  const size_t planes = sizeof(__nv_bfloat16) * NA * 2 * DM_DZT * R1 * J1;
+  const Dg1Shape shp = dg1_shape(planes, raw_bytes);
+  int64_t Sm = (148 * shp.per_sm + gx - 1) / gx;
   if (Sm > stages) Sm = stages;
   if (Sm > S) Sm = S;
   if (Sm < 1) Sm = 1;
@@ -3796,10 +3822,9 @@ cudaError_t launch_tt_dg1_group(const void* x, int64_t T, int64_t K, const float
     ad.part[a] = part[a];
     ad.dz1b[a] = dz1b != nullptr ? dz1b[a] : nullptr;
   }
-  // a 4-stage x ring when the prefetched dZ1 partials fit beside it, else 3 stages (the prefetch matters more)
-  const size_t raw_bytes = sizeof(float) * 2 * NA * HS * DM_DZT * J1 * R1;
-  const size_t planes = sizeof(__nv_bfloat16) * NA * 2 * DM_DZT * R1 * J1;
-  int nstg = DM_NSTG;
+  // one CTA per SM: a 4-stage x ring when the prefetched dZ1 partials fit beside it, else 3 stages (the
+  // prefetch matters more)
+  int nstg = shp.nstg;
   if (sizeof(__nv_bfloat16) * nstg * DM_ST * DM_LDX + planes + raw_bytes > 220 * 1024) nstg = 3;
   size_t smem = sizeof(__nv_bfloat16) * nstg * DM_ST * DM_LDX + planes;
   const int raw_async = smem + raw_bytes <= 220 * 1024 ? 1 : 0;
@@ -3839,15 +3864,17 @@ cudaError_t launch_tt_dg1(const void* x, int x_dtype, int64_t T, int64_t K, cons
   if (x_dtype == QA_BF16 && J1 == 4 && K % 8 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0 && !dg1_mma_disabled()) {
     const int64_t gx = (K + DM_COLS - 1) / DM_COLS;
     const int64_t stages = (T + DM_ST - 1) / DM_ST;
-    int64_t Sm = (148 + gx - 1) / gx;
+    const size_t raw_bytes = sizeof(float) * 2 * HS * DM_DZT * J1 * R1;
+    const size_t planes = sizeof(__nv_bfloat16) * 2 * DM_DZT * R1 * J1;
+    const Dg1Shape shp = dg1_shape(planes, raw_bytes);
+    int64_t Sm = (148 * shp.per_sm + gx - 1) / gx;
     if (Sm > stages) Sm = stages;
+    if (Sm > S) Sm = S;
     if (Sm < 1) Sm = 1;
     if (Sm <= S) {  // the caller's partial buffer holds S splits
       if (splits_used != nullptr) *splits_used = static_cast<int>(Sm);
       const dim3 gm(static_cast<unsigned>(gx), static_cast<unsigned>(Sm));
-      const size_t raw_bytes = sizeof(float) * 2 * HS * DM_DZT * J1 * R1;
-      const size_t planes = sizeof(__nv_bfloat16) * 2 * DM_DZT * R1 * J1;
-      int nstg = DM_NSTG;
+      int nstg = shp.nstg;
       if (sizeof(__nv_bfloat16) * nstg * DM_ST * DM_LDX + planes + raw_bytes > 220 * 1024) nstg = 3;
       size_t smem = sizeof(__nv_bfloat16) * nstg * DM_ST * DM_LDX + planes;
       const int raw_async = smem + raw_bytes <= 220 * 1024 ? 1 : 0;
