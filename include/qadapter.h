@@ -152,8 +152,10 @@ QA_API int qa_linear_backward_saved(const qa_qweight* w, const qa_tt* tt, const 
  * each member's outputs exactly as its own qa_linear_forward_save / qa_linear_backward_saved would
  * (per-member y, dx and core gradients), but read x once per direction when every member is a
  * pinned-mode tensor-train adapter (first core input-only with 4-wide last input mode, rank 8);
- * otherwise they run the members one after another.  saved[i] / saved_bytes[i] as in
- * qa_linear_forward_save (entries or the arrays themselves may be NULL). */
+ * otherwise they run the members one after another.  Decode-size batches (1..8 tokens) run each member's
+ * act-quant prologue + matrix-vector pass, the next member's prologue overlapping the current pass
+ * (programmatic dependent launches; stream order still holds for later work).  saved[i] / saved_bytes[i]
+ * as in qa_linear_forward_save (entries or the arrays themselves may be NULL). */
 QA_API size_t qa_group_workspace_bytes(int n, const qa_qweight* const* w, const qa_tt* const* tt, int64_t tokens);
 QA_API int qa_group_forward(int n, const qa_qweight* const* w, const qa_tt* const* tt, const void* x, int x_dtype,
                             int64_t tokens, void* const* y, void* const* saved, const size_t* saved_bytes,
