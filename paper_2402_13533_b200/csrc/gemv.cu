@@ -1,9 +1,12 @@
 // Decode-size forward (1..8 tokens, KV-cached decoding, transformer.py:1043-1080): the int8 product is a
 // matrix-vector pass over the stored codes, so it is HBM-bound on the weight bytes, not tensor-bound.
-// One warp per output row at a time: lanes stream 16-byte code chunks of the row (512 B per warp
-// load), multiply them against the tokens' activation codes with dp4a (u8 x u8 -> exact int32),
-// reduce across the warp, and apply the same exact-int32 centring + fp32 dequant epilogue as the
-// tcgen05 GEMM (gemm_tc.cu), plus the adapter term y2 = Z1 · Vᵀ from the fp32 Z1 and the hi + lo V split.
+//   k_gemv_mma (K % 64 == 0, the production pass): mma.sync m16n8k32 u8 x u8 -> exact s32 with 16 weight
+//     rows x 8 token columns per warp instruction, 8 warps splitting K, launched as a programmatic dependent
+//     of the act-quant prologue (weights loaded / prefetched before griddepcontrol.wait).
+//   k_gemv (other K): one warp per output row at a time, lanes stream 16-byte code chunks and multiply them
+//     against the activation codes with dp4a.
+// Both apply the tcgen05 GEMM's exact-int32 centring + fp32 dequant epilogue (gemm_tc.cu) plus the adapter
+// term y2 = Σ_b Zlast[t, h, b] · Glast[b, i] from the prologue's fp32 Zlast and the last core.
 #include "qa_common.cuh"
 #include "qa_internal.h"
 #include "qa_timing.h"
