@@ -914,20 +914,27 @@ QA_DEV uint32_t aqc_codes_row(const uint8_t* xrow, uint8_t* crow, int64_t nseg, 
   const float alo = SUB ? 0.5f - kTieBand : r.nbh - kTieBand, ahi = SUB ? 0.5f + kTieBand : r.nbh + kTieBand;
   const unsigned long long alo2 = f2pack(alo, alo), ahi2 = f2pack(ahi, ahi);
   uint32_t sum = 0;
-  int64_t st = warp;
-  for (; st + (AQC_UNROLL - 1) * AQC_WARPS < nseg; st += AQC_UNROLL * AQC_WARPS) {
+  // this warp's segments warp + i W, i < n, visited last-first: pass 1 read them first-first, so the most
+  // recently loaded (likeliest still in L2) come first when rows are long (K = 11008: 8 rows x 22 KB per CTA)
+  const int64_t n = nseg > static_cast<int64_t>(warp) ? (nseg - warp + AQC_WARPS - 1) / AQC_WARPS : 0;
+  int64_t i = n - 1;
+  for (; i >= AQC_UNROLL - 1; i -= AQC_UNROLL) {
     uint4 p[AQC_UNROLL][2];
 #pragma unroll
     for (int u = 0; u < AQC_UNROLL; ++u) {
-      p[u][0] = __ldg(reinterpret_cast<const uint4*>(xrow + 128 * (st + u * AQC_WARPS) + off0));
-      p[u][1] = __ldg(reinterpret_cast<const uint4*>(xrow + 128 * (st + u * AQC_WARPS) + off1));
+      const int64_t st = warp + (i - u) * AQC_WARPS;
+      p[u][0] = __ldg(reinterpret_cast<const uint4*>(xrow + 128 * st + off0));
+      p[u][1] = __ldg(reinterpret_cast<const uint4*>(xrow + 128 * st + off1));
     }
 #pragma unroll
-    for (int u = 0; u < AQC_UNROLL; ++u)
+    for (int u = 0; u < AQC_UNROLL; ++u) {
+      const int64_t st = warp + (i - u) * AQC_WARPS;
       sum += aqc_codes_seg<J1, SUB>(p[u][0], p[u][1], inv2, alo2, ahi2, nlo2, r.lo64, r.step64, flat,
-                                    crow + 64 * (st + u * AQC_WARPS) + off0 / 2, store);
+                                    crow + 64 * st + off0 / 2, store);
+    }
   }
-  for (; st < nseg; st += AQC_WARPS) {
+  for (; i >= 0; --i) {
+    const int64_t st = warp + i * AQC_WARPS;
     const uint4 p0 = __ldg(reinterpret_cast<const uint4*>(xrow + 128 * st + off0));
     const uint4 p1 = __ldg(reinterpret_cast<const uint4*>(xrow + 128 * st + off1));
     sum += aqc_codes_seg<J1, SUB>(p0, p1, inv2, alo2, ahi2, nlo2, r.lo64, r.step64, flat, crow + 64 * st + off0 / 2,
