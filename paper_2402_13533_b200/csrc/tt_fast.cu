@@ -867,7 +867,10 @@ __global__ void __launch_bounds__((AQP_NC + 1) * 32, 1)
 //            replayed in fp64 in place.
 // Splitting the row over the CTA's warps keeps the live footprint per in-flight byte small (the
 // whole row must be seen before its first code), so many CTAs per SM can stream at once.
-constexpr int AQC_WARPS = 8, AQC_UNROLL = 4;
+#ifndef QA_AQC_UNROLL
+#define QA_AQC_UNROLL 4
+#endif
+constexpr int AQC_WARPS = 8, AQC_UNROLL = QA_AQC_UNROLL;
 
 struct AqAdapters {  // per-adapter outputs of the shared x pass (unused entries null)
   __nv_bfloat16* zb[3];
