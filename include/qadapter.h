@@ -108,7 +108,9 @@ QA_API size_t qa_linear_workspace_bytes(const qa_qweight* w, const qa_tt* tt, in
  *   dequantising epilogue, + y2 = x · W_tᵀ (tt may be NULL: base only).
  * x: [tokens, cols] (dtype x_dtype, row stride = cols).  y: [tokens, rows] bf16.
  * Optional debug outputs (NULL to skip): acc_i32 [tokens, rows] raw Σ cx·cw,
- * y_f32 [tokens, rows] the fp32 pre-rounding y, y2_f32 [tokens, rows] the adapter term. */
+ * y_f32 [tokens, rows] the fp32 pre-rounding y, y2_f32 [tokens, rows] the adapter term (needs y_f32).
+ * They come from the same persistent tcgen05 kernels as the plain call (probe outputs of the epilogue),
+ * so parity tests that read them pin the production path. */
 QA_API int qa_linear_forward(const qa_qweight* w, const qa_tt* tt, const void* x, int x_dtype, int64_t tokens,
                       void* y, int32_t* acc_i32, float* y_f32, float* y2_f32, void* workspace,
                       size_t workspace_bytes, void* stream);

@@ -28,6 +28,7 @@ __all__ = [
     "tt_init_cores",
     "tt_full",
     "tt_apply",
+    "tt_rows",
     "tt_prefix",
     "tt_dx",
     "tt_core_grads",
@@ -283,6 +284,26 @@ def tt_full(cores) -> np.ndarray:
         i, j, _ = cur.shape
         nxt = np.einsum("ija,akqb->ikjqb", cur, g)
         cur = nxt.reshape(i * g.shape[1], j * g.shape[2], g.shape[3])
+    return cur[..., 0]
+
+
+def tt_rows(cores, rows) -> np.ndarray:
+    """Selected rows of W_t ([len(rows), K] fp64) without materialising the whole matrix: row n with
+    multi-index (i_1..i_d) (row-major over m) is G1[0,i_1,:,:] · G2[:,i_2,:,:] ··· Gd[:,i_d,:,0] over j."""
+    cs = [np.asarray(g, dtype=np.float64) for g in cores]
+    ms = [g.shape[1] for g in cs]
+    rows = np.asarray(rows, dtype=np.int64)
+    idx = []
+    rem = rows.copy()
+    for m in reversed(ms):
+        idx.append(rem % m)
+        rem //= m
+    idx = idx[::-1]
+    cur = cs[0][0][idx[0]]  # [R, n_1, r_1]
+    for k in range(1, len(cs)):
+        g = cs[k][:, idx[k]]  # [a, R, n_k, b]
+        cur = np.einsum("rja,arqb->rjqb", cur, g)
+        cur = cur.reshape(cur.shape[0], -1, cur.shape[-1])
     return cur[..., 0]
 
 

@@ -20,14 +20,16 @@ What this module adds for the device path:
 
 from __future__ import annotations
 
+import io
 import json
 import os
+import struct
 
 import numpy as np
 import torch
 
 from . import _lib
-from .linear import LoraLinear, QuantizedLinear, TTLinear, TTSpec
+from .linear import LoraLinear, QuantizedLinear, TTLinear, TTSpec, tt_merge
 from .quant import QuantizedMatrix, _stream_ptr
 
 __all__ = ["CheckpointError", "MAGIC", "VERSION", "ALIGN", "Checkpoint", "read_checkpoint", "quantized_from_arrays",
@@ -37,7 +39,14 @@ __all__ = ["CheckpointError", "MAGIC", "VERSION", "ALIGN", "Checkpoint", "read_c
 MAGIC = b"LRLM"
 VERSION = 1
 ALIGN = 64
+# element type of each dtype tag (u8q / u4q payloads are packed code bytes)
 _NP = {"f32": np.dtype("<f4"), "f16": np.dtype("<f2"), "u8q": np.dtype("<u1"), "u4q": np.dtype("<u1")}
+# magic, version (u32 LE), header byte length (u64 LE)
+_PREAMBLE = struct.Struct("<4sIQ")
+
+
+def _align_up(n: int) -> int:
+    return -(-n // ALIGN) * ALIGN
 
 
 class CheckpointError(RuntimeError):
@@ -54,14 +63,15 @@ class Checkpoint:
         self.payload_start = payload_start
 
     def raw(self, name: str, expect=None) -> tuple[np.ndarray, dict]:
-        if name not in self.table:
+        ent = self.table.get(name)
+        if ent is None:
             raise CheckpointError(f"checkpoint is missing tensor {name}")
-        ent = self.table[name]
-        if expect is not None and ent["dtype"] not in ((expect,) if isinstance(expect, str) else expect):
-            raise CheckpointError(f"{name}: expected dtype {expect}, found {ent['dtype']}")
-        a = self.payload_start + ent["offset"]
-        return np.frombuffer(self.data, dtype=_NP[ent["dtype"]], count=ent["length"] // _NP[ent["dtype"]].itemsize,
-                             offset=a), ent
+        tags = (expect,) if isinstance(expect, str) else expect
+        if tags is not None and ent["dtype"] not in tags:
+            raise CheckpointError(f"{name}: stored as {ent['dtype']}, wanted one of {tags}")
+        dt = _NP[ent["dtype"]]
+        view = memoryview(self.data)[self.payload_start + ent["offset"]:][:ent["length"]]
+        return np.frombuffer(view, dtype=dt), ent
 
     def array(self, name: str) -> np.ndarray:
         """A float tensor as float32 in its logical shape (f16 widened, like the reference's fetch)."""
@@ -70,50 +80,63 @@ class Checkpoint:
 
     def entries(self):
         """(name, dtype tag, logical shape, host array) in the file's (sorted) order — save_checkpoint's input."""
-        out = []
-        for name in sorted(self.table):
-            arr, ent = self.raw(name)
-            out.append((name, ent["dtype"], list(ent["shape"]), arr))
-        return out
+        return [(name, self.table[name]["dtype"], list(self.table[name]["shape"]), self.raw(name)[0])
+                for name in sorted(self.table)]
+
+
+def _parse_preamble(data: bytes) -> tuple[dict, int]:
+    """Header dict and payload start of a file (the container layout of checkpoint.py:1-8)."""
+    if len(data) < _PREAMBLE.size:
+        raise CheckpointError("not a checkpoint: bad magic (file shorter than the preamble)")
+    magic, version, hlen = _PREAMBLE.unpack_from(data)
+    if magic != MAGIC:
+        raise CheckpointError("not a checkpoint: bad magic")
+    if version != VERSION:
+        raise CheckpointError(f"unsupported checkpoint version {version} (this reader handles {VERSION})")
+    end = _PREAMBLE.size + hlen
+    if end > len(data):
+        raise CheckpointError("truncated checkpoint: the JSON header runs past end of file")
+    try:
+        header = json.loads(bytes(data[_PREAMBLE.size:end]))
+    except (UnicodeDecodeError, ValueError) as exc:
+        raise CheckpointError(f"corrupt header: {exc}") from exc
+    if not isinstance(header, dict) or not isinstance(header.get("tensors"), dict):
+        raise CheckpointError("corrupt header: no tensor table")
+    return header, _align_up(end)
+
+
+def _check_table(table: dict, payload_len: int) -> None:
+    """Every entry aligned, inside the payload, of a known dtype, with its quantisation companions; no two
+    entries share bytes."""
+    if not table:
+        return
+    names = list(table)
+    starts = np.array([int(table[n]["offset"]) for n in names], dtype=np.int64)
+    ends = starts + np.array([int(table[n]["length"]) for n in names], dtype=np.int64)
+    for n, a, b in zip(names, starts, ends):
+        tag = table[n]["dtype"]
+        if tag not in _NP:
+            raise CheckpointError(f"{n}: unknown dtype tag {tag!r}")
+        if a % ALIGN != 0:
+            raise CheckpointError(f"{n}: payload offset {a} is not a multiple of {ALIGN}")
+        if a < 0 or b > payload_len:
+            raise CheckpointError(f"{n}: tensor bytes [{a}, {b}) run past end of file (truncated?)")
+        if tag in ("u8q", "u4q"):
+            missing = [c for c in (n + ".scale", n + ".offset") if c not in table]
+            if missing:
+                raise CheckpointError(f"{n}: quantised tensor without its companion {missing[0]}")
+    order = np.lexsort((ends, starts))
+    clash = np.flatnonzero(starts[order][1:] < ends[order][:-1])
+    if clash.size:
+        first, second = names[order[clash[0]]], names[order[clash[0] + 1]]
+        raise CheckpointError(f"tensors {first} and {second} share payload bytes")
 
 
 def read_checkpoint(path) -> Checkpoint:
-    data = open(path, "rb").read()
-    if len(data) < 16 or data[:4] != MAGIC:
-        raise CheckpointError("not a checkpoint: bad magic")
-    version = int.from_bytes(data[4:8], "little")
-    if version != VERSION:
-        raise CheckpointError(f"unsupported checkpoint version {version}, expected {VERSION}")
-    hlen = int.from_bytes(data[8:16], "little")
-    if 16 + hlen > len(data):
-        raise CheckpointError("truncated checkpoint: header runs past end of file")
-    try:
-        header = json.loads(data[16:16 + hlen].decode("utf-8"))
-    except (UnicodeDecodeError, json.JSONDecodeError) as exc:
-        raise CheckpointError(f"corrupt header: {exc}") from exc
-    payload_start = 16 + hlen + (-(16 + hlen)) % ALIGN
-    table = header.get("tensors")
-    if not isinstance(table, dict):
-        raise CheckpointError("corrupt header: no tensor table")
-    payload_len = len(data) - payload_start
-    spans = []
-    for name, ent in table.items():
-        off, length = ent["offset"], ent["length"]
-        if off % ALIGN:
-            raise CheckpointError(f"{name}: offset {off} not {ALIGN}-byte aligned")
-        if off < 0 or off + length > payload_len:
-            raise CheckpointError(f"{name}: tensor bytes run past end of file (truncated?)")
-        if ent["dtype"] not in _NP:
-            raise CheckpointError(f"{name}: unknown dtype {ent['dtype']}")
-        if ent["dtype"] in ("u8q", "u4q"):
-            for companion in (name + ".scale", name + ".offset"):
-                if companion not in table:
-                    raise CheckpointError(f"{name}: missing companion tensor {companion}")
-        spans.append((off, off + length, name))
-    spans.sort()
-    for (a0, a1, n1), (b0, _b1, n2) in zip(spans, spans[1:]):
-        if b0 < a1:
-            raise CheckpointError(f"overlapping tensors {n1} and {n2}")
+    with open(path, "rb") as f:
+        data = f.read()
+    header, payload_start = _parse_preamble(data)
+    _check_table(header["tensors"], len(data) - payload_start)
     return Checkpoint(data, header, payload_start)
 
 
@@ -159,7 +182,15 @@ def load_lora(ck: Checkpoint, slot: str, device="cuda") -> LoraLinear:
     base = QuantizedLinear(slot + ".base", load_quantized(ck, slot + ".base", device))
     down = torch.from_numpy(ck.array(slot + ".down")).to(device)
     up = torch.from_numpy(ck.array(slot + ".up")).to(device)
-    return LoraLinear(slot, base, down, up)
+    return _honour_merged(ck, slot, LoraLinear(slot, base, down, up))
+
+
+def _honour_merged(ck: Checkpoint, slot: str, adapter):
+    """A slot the header marks merged is re-folded after loading, as the reference's load_checkpoint does
+    (checkpoint.py:231-235)."""
+    if ck.header.get("merged", {}).get(slot):
+        tt_merge(adapter)
+    return adapter
 
 
 def load_tt(ck: Checkpoint, slot: str, device="cuda") -> TTLinear:
@@ -172,7 +203,7 @@ def load_tt(ck: Checkpoint, slot: str, device="cuda") -> TTLinear:
     spec = TTSpec(tuple(sp["m"]), tuple(sp["n"]), tuple(sp["ranks"]))
     base = QuantizedLinear(slot + ".base", load_quantized(ck, slot + ".base", device))
     cores = [torch.from_numpy(ck.array(f"{slot}.core{k}")).to(device) for k in range(spec.d)]
-    return TTLinear(slot, base, spec, cores)
+    return _honour_merged(ck, slot, TTLinear(slot, base, spec, cores))
 
 
 def _host(a) -> np.ndarray:
@@ -181,27 +212,30 @@ def _host(a) -> np.ndarray:
 
 def save_checkpoint(path, entries, header: dict) -> None:
     """Deterministic writer of the reference layout (checkpoint.py:113-140): `entries` are (name, dtype tag,
-    logical shape, array); `header` supplies every key but "tensors" (model_config, layer_specs, merged, …)."""
-    entries = sorted(entries, key=lambda e: e[0])
-    table, blobs, offset = {}, [], 0
-    for name, tag, shape, array in entries:
-        raw = np.ascontiguousarray(_host(array)).astype(_NP[tag], copy=False).tobytes()
-        table[name] = {"dtype": tag, "shape": list(shape), "offset": offset, "length": len(raw)}
-        blobs.append((offset, raw))
-        offset += len(raw)
-        offset += (-offset) % ALIGN
-    full = dict(header)
-    full["tensors"] = table
-    hb = json.dumps(full, sort_keys=True, separators=(",", ":")).encode("utf-8")
-    out = bytearray(MAGIC + VERSION.to_bytes(4, "little") + len(hb).to_bytes(8, "little") + hb)
-    out += b"\x00" * ((-len(out)) % ALIGN)
-    start = len(out)
-    out += b"\x00" * offset
-    for off, raw in blobs:
-        out[start + off:start + off + len(raw)] = raw
+    logical shape, array); `header` supplies every key but "tensors" (model_config, layer_specs, merged, …).
+    Tensors go in name order, each at the next 64-byte boundary of the payload."""
+    blobs = {name: (tag, list(shape), np.ascontiguousarray(_host(arr)).astype(_NP[tag], copy=False).tobytes())
+             for name, tag, shape, arr in entries}
+    table, cursor = {}, 0
+    for name in sorted(blobs):
+        tag, shape, raw = blobs[name]
+        table[name] = {"dtype": tag, "shape": shape, "offset": cursor, "length": len(raw)}
+        cursor = _align_up(cursor + len(raw))
+    hdr = json.dumps({**header, "tensors": table}, sort_keys=True, separators=(",", ":")).encode("utf-8")
+    head = _PREAMBLE.pack(MAGIC, VERSION, len(hdr)) + hdr
+    buf = io.BytesIO()
+    buf.write(head)
+    buf.write(bytes(_align_up(len(head)) - len(head)))
+    for name in sorted(blobs):
+        raw = blobs[name][2]
+        buf.write(raw)
+        buf.write(bytes(_align_up(len(raw)) - len(raw)))
+    out = buf.getvalue()
+    # the last tensor's padding is part of the payload only up to the table's end (as in the reference)
+    out = out[:_align_up(len(head)) + cursor]
     tmp = str(path) + ".tmp"
     with open(tmp, "wb") as f:
-        f.write(bytes(out))
+        f.write(out)
     os.replace(tmp, path)
 
 
@@ -217,6 +251,11 @@ def collect_backends(slots: dict):
     bases as u8q / u4q, LoRA factors under the reference's names, TT cores as "<slot>.core{k}"."""
     entries, tt_specs, merged = [], {}, {}
     for path, b in slots.items():
+        if isinstance(b, TTLinear) and b.merged:
+            # the reference re-folds a merged slot on load with lora_merge, which refuses quantised bases
+            # (checkpoint.py:231-235, lowrank.py:247-251): a merged adapter over codes has no LRLM encoding
+            raise CheckpointError(f"{path}: save the adapter before merging it (merged adapters over quantised "
+                                  "bases cannot be stored in an LRLM file)")
         if isinstance(b, LoraLinear):
             entries += _quant_entries(path + ".base", b.base.q)
             entries.append((b.down.name, "f32", list(b.down.data.shape), b.down.data))

@@ -443,6 +443,10 @@ int linear_forward_impl(const qa_qweight* w, const qa_tt* tt, const void* x, int
     set_error("qa_linear_forward: bad argument (x, dtype, tokens or weight rowsum)");
     return QA_ERR_ARG;
   }
+  if (y2_f32 != nullptr && y_f32 == nullptr) {
+    set_error("qa_linear_forward: the y2_f32 probe needs y_f32");
+    return QA_ERR_ARG;
+  }
   TTDims dd;
   const TTDims* pd = nullptr;
   if (tt != nullptr) {

@@ -353,21 +353,12 @@ __global__ void __launch_bounds__(GM_WARPS * 32) k_gemv_mma(const uint8_t* __res
 
 }  // namespace
 
-// QA_PDL=0 launches the decode kernels without programmatic dependent launch (A/B, triage).
-bool pdl_enabled() {
-  static const bool on = [] {
-    const char* v = getenv("QA_PDL");
-    return !(v != nullptr && v[0] == '0');
-  }();
-  return on;
-}
+// The decode kernels chain by programmatic dependent launch (the pass's weight loads start while the
+// prologue still runs).
+bool pdl_enabled() { return true; }
 
 bool gemv_ok(int64_t T, int64_t K, int bits) {
-  static const bool off = [] {
-    const char* v = getenv("QA_GEMV");
-    return v != nullptr && v[0] == '0';
-  }();
-  return !off && T >= 1 && T <= 8 && (bits == 8 ? K % 16 == 0 : K % 32 == 0);
+  return T >= 1 && T <= 8 && (bits == 8 ? K % 16 == 0 : K % 32 == 0);
 }
 
 cudaError_t launch_gemv(const uint8_t* xc, int64_t ldx, int64_t T, const float* sx, const float* ox,
@@ -400,12 +391,8 @@ cudaError_t launch_gemv(const uint8_t* xc, int64_t ldx, int64_t T, const float* 
       e = cudaLaunchKernelEx(&cfg, k_gemv<MM, 4>, xc, ldx, Ti, sx, ox, rsx, wc, N, K, ws, wo, wrs, zl, ldz, Gl, Ml, \
                              Cl, addend, out, out32);                                                             \
   }
-  static const bool dp4a_only = [] {
-    const char* v = getenv("QA_GEMV_MMA");
-    return v != nullptr && v[0] == '0';
-  }();
   // the tensor-core pass keeps one Zlast block per 16-row tile (16 | Ml, or a single block) and Cl <= 32
-  if (K % 64 == 0 && !dp4a_only && (Gl == nullptr || ((Ml % 16 == 0 || Ml >= N) && Cl <= 32))) {
+  if (K % 64 == 0 && (Gl == nullptr || ((Ml % 16 == 0 || Ml >= N) && Cl <= 32))) {
     cfg.gridDim = dim3(static_cast<unsigned>((N + 15) / 16));
     cfg.blockDim = dim3(GM_WARPS * 32);
     if (bits == 8)

@@ -309,7 +309,8 @@ __global__ void __launch_bounds__(kXentThreads) k_xent(const __nv_bfloat16* __re
     fin[0] = M;
     fin[1] = S;
     const int64_t t = targets[row];
-    const float lt = __bfloat162float(logits[row * V + t]);
+    // a target outside [0, V) reads nothing and marks the row NaN (the host wrapper raises IndexError first)
+    const float lt = (t >= 0 && t < V) ? __bfloat162float(logits[row * V + t]) : __int_as_float(0x7fc00000);
     loss_rows[row] = (M + logf(S)) - lt;
   }
   __syncthreads();

@@ -283,46 +283,6 @@ struct AqRow {
   double lo64, step64;  // the reference's fp64 quantities (tie replays)
 };
 
-// q' = (v - lo) / step + 1/2 for the two bf16 of w, packed.  SUB = false evaluates v * inv + nbh
-// (one FFMA2; used when |lo * inv| <= 512, error < 1e-4), SUB = true subtracts first (rows whose
-// offset dwarfs their range, where v * inv - lo * inv would cancel catastrophically).
-template <bool SUB>
-QA_DEV unsigned long long aq_q2(uint32_t w, unsigned long long inv2, unsigned long long nbh2,
-                                unsigned long long nlo2) {
-  const unsigned long long v2 = f2pack(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
-  if constexpr (SUB)
-    return ffma2r(fadd2(v2, nlo2), inv2, f2pack(0.5f, 0.5f));
-  else
-    return ffma2r(v2, inv2, nbh2);
-}
-template <bool SUB>
-QA_DEV float aq_q1(float v, const AqRow& r) {
-  return SUB ? fmaf(v - r.lo, r.inv, 0.5f) : fmaf(v, r.inv, r.nbh);
-}
-
-// Codes of 8 elements: s = q' + 1.5 * 2^15 puts q' on a 2^-8 grid inside the mantissa, so byte 1
-// of s is floor(q') (the code, round half up) and byte 0 the fraction.  A zero fraction byte means
-// q' is within 2^-9 of an integer — possibly a rounding tie of the reference — and flags the chunk
-// for aq_codes_fix.
-template <bool SUB>
-QA_DEV void aq_codes8(const uint4 raw, unsigned long long inv2, unsigned long long nbh2, unsigned long long nlo2,
-                      uint32_t& c0, uint32_t& c1, bool& near) {
-  const unsigned long long m2 = f2pack(49152.0f, 49152.0f);
-  const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
-  uint32_t s[8];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const unsigned long long s2 = fadd2(aq_q2<SUB>(w[i], inv2, nbh2, nlo2), m2);
-    s[2 * i] = static_cast<uint32_t>(s2);
-    s[2 * i + 1] = static_cast<uint32_t>(s2 >> 32);
-  }
-  c0 = __byte_perm(__byte_perm(s[0], s[1], 0x0051), __byte_perm(s[2], s[3], 0x0051), 0x5410);
-  c1 = __byte_perm(__byte_perm(s[4], s[5], 0x0051), __byte_perm(s[6], s[7], 0x0051), 0x5410);
-  const uint32_t f0 = __byte_perm(__byte_perm(s[0], s[1], 0x0040), __byte_perm(s[2], s[3], 0x0040), 0x5410);
-  const uint32_t f1 = __byte_perm(__byte_perm(s[4], s[5], 0x0040), __byte_perm(s[6], s[7], 0x0040), 0x5410);
-  near = (((f0 - 0x01010101u) & ~f0) | ((f1 - 0x01010101u) & ~f1)) & 0x80808080u;
-}
-
 // Bracketed codes of 8 elements: t = q' + 1/2 is evaluated twice, with the addend shifted by
 // -kTieBand and +kTieBand, and each is floored onto the integer grid by a round-down magic add
 // (byte 1 of M + t, M = 1.5 * 2^15).  Outside the band both floors agree and equal the reference's
@@ -372,484 +332,6 @@ QA_DEV uint32_t aq_replay_word(const uint4 raw, int e0, uint32_t code, uint32_t 
   return code;
 }
 
-// Resolve the flagged elements of a chunk.  With s rounded to the integer n, floor(q') is n when
-// q' >= n and n - 1 otherwise; the fp32 q' decides that unless it lies within kTieBand of n (far
-// above its error), where the reference's fp64 arithmetic is replayed exactly.
-template <bool SUB>
-QA_DEV void aq_codes_fix(const uint4 raw, const AqRow& r, uint32_t& c0, uint32_t& c1) {
-  const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const float v = __uint_as_float((i & 1) ? (w[i >> 1] & 0xFFFF0000u) : (w[i >> 1] << 16));
-    const float q = aq_q1<SUB>(v, r);
-    const float s = q + 49152.0f;
-    if ((__float_as_uint(s) & 0xFFu) != 0u) continue;
-    const float n = s - 49152.0f;  // exact
-    const float d = q - n;         // exact (Sterbenz)
-    uint32_t code;
-    if (fabsf(d) < kTieBand) {
-      const double v64 = __ddiv_rn(__dsub_rn(static_cast<double>(v), r.lo64), r.step64);
-      code = static_cast<uint32_t>(fmin(fmax(floor(__dadd_rn(v64, 0.5)), 0.0), 255.0));
-    } else {
-      code = static_cast<uint32_t>(n) - (d < 0.0f ? 1u : 0u);
-    }
-    uint32_t& word = i < 4 ? c0 : c1;
-    const int sh = 8 * (i & 3);
-    word = (word & ~(0xFFu << sh)) | (code << sh);
-  }
-}
-
-// Codes for one warp's chunk range [cb, ce) of a shared-memory bf16 row (8 elements per chunk);
-// returns the lane's code sum.  Flags are kept per lane in a bitmask (bit k = the lane's k-th
-// chunk) and resolved after the streaming loop, so the loop itself stays branch-free.
-template <bool SUB>
-QA_DEV uint32_t aq_codes_run(const uint4* srow, uint32_t cb, uint32_t ce, const AqRow& r, uint8_t* dst) {
-  const uint32_t lane = lane_id();
-  const unsigned long long inv2 = f2pack(r.inv, r.inv), nbh2 = f2pack(r.nbh, r.nbh), nlo2 = f2pack(-r.lo, -r.lo);
-  const uint32_t first = cb + lane;
-  const uint32_t cnt = first < ce ? (ce - first + 31) / 32 : 0;
-  const uint4* src = srow + first;
-  uint2* out = reinterpret_cast<uint2*>(dst) + first;
-  unsigned long long mask = 0ull;
-  uint32_t sum = 0;
-  uint32_t k0 = 0;
-  for (; k0 + 4 <= cnt; k0 += 4) {  // unguarded groups: four independent chains per iteration
-    uint4 raw[4];
-#pragma unroll
-    for (uint32_t u = 0; u < 4; ++u) raw[u] = src[(k0 + u) * 32];
-    uint32_t m4 = 0;
-#pragma unroll
-    for (uint32_t u = 0; u < 4; ++u) {
-      uint2 packed;
-      bool near;
-      aq_codes8<SUB>(raw[u], inv2, nbh2, nlo2, packed.x, packed.y, near);
-      m4 |= static_cast<uint32_t>(near) << u;
-      sum = __dp4a(packed.x, 0x01010101u, sum);
-      sum = __dp4a(packed.y, 0x01010101u, sum);
-      out[(k0 + u) * 32] = packed;
-    }
-    mask |= static_cast<unsigned long long>(m4) << k0;
-  }
-  for (; k0 < cnt; ++k0) {
-    uint2 packed;
-    bool near;
-    aq_codes8<SUB>(src[k0 * 32], inv2, nbh2, nlo2, packed.x, packed.y, near);
-    mask |= static_cast<unsigned long long>(near) << k0;
-    sum = __dp4a(packed.x, 0x01010101u, sum);
-    sum = __dp4a(packed.y, 0x01010101u, sum);
-    out[k0 * 32] = packed;
-  }
-  while (mask != 0ull) {
-    const uint32_t k = static_cast<uint32_t>(__ffsll(static_cast<long long>(mask)) - 1);
-    mask &= mask - 1;
-    const uint4 raw = src[k * 32];
-    uint2 old;  // recomputed rather than read back from global memory (a full L2 round trip)
-    bool near;
-    aq_codes8<SUB>(raw, inv2, nbh2, nlo2, old.x, old.y, near);
-    uint2 fixed = old;
-    aq_codes_fix<SUB>(raw, r, fixed.x, fixed.y);
-    sum += (__dp4a(fixed.x, 0x01010101u, 0u) + __dp4a(fixed.y, 0x01010101u, 0u)) -
-           (__dp4a(old.x, 0x01010101u, 0u) + __dp4a(old.y, 0x01010101u, 0u));
-    out[k * 32] = fixed;
-  }
-  return sum;
-}
-
-QA_DEV int aq_codes_range(const uint4* srow, uint32_t cb, uint32_t ce, float lo, float hi, uint8_t* dst) {
-  const uint32_t lane = lane_id();
-  AqRow r;
-  r.lo = lo;
-  r.lo64 = static_cast<double>(lo);
-  r.step64 = __ddiv_rn(__dsub_rn(static_cast<double>(hi), r.lo64), 255.0);
-  if (!(r.step64 > 0.0)) {  // flat row: every code is 0
-    for (uint32_t c = cb + lane; c < ce; c += 32) *reinterpret_cast<uint2*>(dst + c * 8) = make_uint2(0u, 0u);
-    return 0;
-  }
-  r.inv = static_cast<float>(1.0 / r.step64);
-  const float nb = -lo * r.inv;
-  r.nbh = nb + 0.5f;
-  const uint32_t sum = fabsf(nb) <= 512.0f ? aq_codes_run<false>(srow, cb, ce, r, dst)
-                                           : aq_codes_run<true>(srow, cb, ce, r, dst);
-  return static_cast<int>(sum);
-}
-
-template <int J1>
-__host__ __device__ constexpr uint32_t aq_row_pad() {
-  return J1 == 4 ? 64u : 16u;
-}
-
-// CTA: 8 warps, tiles of TOK = 4 token rows (the n8 MMA columns 4..7 repeat rows 0..3), NBUF tile
-// buffers in a ring so the next tiles stream in while one is processed.
-constexpr int AQ_TOK = 4, AQ_NW = 8;
-
-template <int J1, int R1, int NBUF, bool CODES>
-__global__ void __launch_bounds__(AQ_NW * 32) k_aq_mma(const __nv_bfloat16* __restrict__ x, int64_t T, int64_t K,
-                                                      uint8_t* __restrict__ codes, int64_t ldc,
-                                                      float* __restrict__ sx, float* __restrict__ ox,
-                                                      int32_t* __restrict__ rsx, const uint4* __restrict__ frag,
-                                                      __nv_bfloat16* __restrict__ zb, int64_t ldzb,
-                                                      float* __restrict__ zf) {
-  constexpr int K2 = J1 * R1, MT = R1 / 8, NJ = J1 == 4 ? 4 : 1, TOK = AQ_TOK, NW = AQ_NW, PARTS = NW / TOK;
-  static_assert(J1 == 1 || J1 == 4, "J1");
-  static_assert(R1 == 8 || R1 == 16, "R1");
-  extern __shared__ __align__(128) uint8_t aq_tile[];
-  __shared__ uint64_t bars[NBUF];
-  __shared__ float s_lo[NW][TOK], s_hi[NW][TOK];
-  __shared__ float s_red[NW][TOK * K2];
-  __shared__ int s_sum[TOK][PARTS];
-  const uint32_t warp = threadIdx.x >> 5, lane = lane_id(), g = lane >> 2, c = lane & 3;
-  const uint32_t rowbytes = static_cast<uint32_t>(K * 2), stride = rowbytes + aq_row_pad<J1>();
-  const uint32_t nsteps = static_cast<uint32_t>(K / 64), nvec = static_cast<uint32_t>(K / 8);
-  const int64_t ntiles = (T + TOK - 1) / TOK;
-  auto issue = [&](int64_t t, int b) {
-    const int nr = static_cast<int>(T - t * TOK < TOK ? T - t * TOK : TOK);
-    mbar_arrive_expect_tx(&bars[b], static_cast<uint32_t>(nr) * rowbytes);
-    for (int r = 0; r < nr; ++r)
-      bulk_load(aq_tile + (b * TOK + r) * stride, x + (t * TOK + r) * K, rowbytes, &bars[b]);
-  };
-  int64_t tile = blockIdx.x;
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int b = 0; b < NBUF; ++b) mbar_init(&bars[b], 1);
-    fence_barrier_init();
-#pragma unroll
-    for (int b = 0; b < NBUF; ++b)
-      if (tile + static_cast<int64_t>(b) * gridDim.x < ntiles) issue(tile + static_cast<int64_t>(b) * gridDim.x, b);
-  }
-  __syncthreads();
-  for (uint32_t it = 0; tile < ntiles; ++it, tile += gridDim.x) {
-    const int b = static_cast<int>(it % NBUF);
-    const uint8_t* buf = aq_tile + b * TOK * stride;
-    const int64_t r0 = tile * TOK;
-    const int nr = static_cast<int>(T - r0 < TOK ? T - r0 : TOK);
-    mbar_wait(&bars[b], (it / NBUF) & 1);
-    // ---- pass 1: Z1 partials on the tensor cores (+ exact bf16 min/max when codes are wanted)
-    const uint8_t* myrow = buf + (g % TOK) * stride;
-    float acc[NJ][MT][4];
-#pragma unroll
-    for (int J = 0; J < NJ; ++J)
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-        for (int i = 0; i < 4; ++i) acc[J][mt][i] = 0.f;
-    __nv_bfloat162 lo2 = __floats2bfloat162_rn(INFINITY, INFINITY), hi2 = __floats2bfloat162_rn(-INFINITY, -INFINITY);
-#pragma unroll 2
-    for (uint32_t st = warp; st < nsteps; st += NW) {
-      const uint8_t* p = myrow + 128u * st;
-      const uint4 p0 = *reinterpret_cast<const uint4*>(p + (J1 == 4 ? 16u * c : 32u * c));
-      const uint4 p1 = *reinterpret_cast<const uint4*>(p + (J1 == 4 ? 64u + 16u * c : 32u * c + 16u));
-      const uint32_t w[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
-      if constexpr (CODES) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const __nv_bfloat162 b2 = *reinterpret_cast<const __nv_bfloat162*>(&w[i]);
-          lo2 = __hmin2(lo2, b2);
-          hi2 = __hmax2(hi2, b2);
-        }
-      }
-      if constexpr (J1 == 4) {
-        uint4 fr[MT];
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt) fr[mt] = __ldg(frag + (static_cast<size_t>(st) * MT + mt) * 32 + lane);
-#pragma unroll
-        for (int J = 0; J < 4; ++J) {
-          const uint32_t sel = (J & 1) ? 0x7632u : 0x5410u;
-          const uint32_t b0 = __byte_perm(w[J >> 1], w[2 + (J >> 1)], sel);
-          const uint32_t b1 = __byte_perm(w[4 + (J >> 1)], w[6 + (J >> 1)], sel);
-#pragma unroll
-          for (int mt = 0; mt < MT; ++mt) mma_16816(acc[J][mt], fr[mt].x, fr[mt].y, fr[mt].z, fr[mt].w, b0, b1);
-        }
-      } else {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-#pragma unroll
-          for (int mt = 0; mt < MT; ++mt) {
-            const uint4 fr = __ldg(frag + ((static_cast<size_t>(st) * 4 + u) * MT + mt) * 32 + lane);
-            mma_16816(acc[0][mt], fr.x, fr.y, fr.z, fr.w, w[2 * u], w[2 * u + 1]);
-          }
-        }
-      }
-    }
-    if constexpr (CODES) {  // per-token stats: the 4 lanes of a group share token g % TOK
-      float lo = fminf(__low2float(lo2), __high2float(lo2)), hi = fmaxf(__low2float(hi2), __high2float(hi2));
-#pragma unroll
-      for (int o = 1; o < 4; o <<= 1) {
-        lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-        hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-      }
-      if (c == 0 && g < TOK) {
-        s_lo[warp][g] = lo;
-        s_hi[warp][g] = hi;
-      }
-    }
-    if (2 * c < TOK) {  // D columns 2c, 2c + 1 are tokens 2c, 2c + 1
-#pragma unroll
-      for (int J = 0; J < NJ; ++J)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const uint32_t t = 2 * c + h;
-          if constexpr (MT == 1) {
-            s_red[warp][t * K2 + g * J1 + J] = acc[J][0][h] + acc[J][0][2 + h];
-          } else {
-            s_red[warp][t * K2 + g * J1 + J] = acc[J][0][h] + acc[J][1][h];
-            s_red[warp][t * K2 + (g + 8) * J1 + J] = acc[J][0][2 + h] + acc[J][1][2 + h];
-          }
-        }
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < nr * K2; i += NW * 32) {
-      float v = s_red[0][i];
-#pragma unroll
-      for (int w = 1; w < NW; ++w) v += s_red[w][i];
-      const int64_t row = r0 + i / K2;
-      const int col = i % K2;
-      if (zf != nullptr) zf[row * K2 + col] = v;
-      if (zb != nullptr) {
-        const __nv_bfloat16 hv = __float2bfloat16_rn(v);
-        zb[row * ldzb + col] = hv;
-        zb[row * ldzb + K2 + col] = __float2bfloat16_rn(v - __bfloat162float(hv));
-        zb[row * ldzb + 2 * K2 + col] = hv;
-      }
-    }
-    if (zb != nullptr && ldzb > 3 * K2) {
-      const int padw = static_cast<int>(ldzb - 3 * K2);
-      for (int i = threadIdx.x; i < nr * padw; i += NW * 32)
-        zb[(r0 + i / padw) * ldzb + 3 * K2 + i % padw] = __float2bfloat16_rn(0.f);
-    }
-    if constexpr (CODES) {
-      // ---- pass 2: codes; warp w takes part w / TOK of token w % TOK
-      const int t = static_cast<int>(warp % TOK), part = static_cast<int>(warp / TOK);
-      if (t < nr) {
-        float tlo = s_lo[0][t], thi = s_hi[0][t];
-#pragma unroll
-        for (int w = 1; w < NW; ++w) {
-          tlo = fminf(tlo, s_lo[w][t]);
-          thi = fmaxf(thi, s_hi[w][t]);
-        }
-        const uint32_t cb = (nvec * part) / PARTS, ce = (nvec * (part + 1)) / PARTS;
-        uint8_t* dst = codes + (r0 + t) * ldc;
-        int sum = aq_codes_range(reinterpret_cast<const uint4*>(buf + t * stride), cb, ce, tlo, thi, dst);
-        sum = warp_sum_i(sum);
-        if (lane == 0) s_sum[t][part] = sum;
-        if (part == PARTS - 1)
-          for (int64_t kk = K + lane; kk < ldc; kk += 32) dst[kk] = 0;
-        if (part == 0 && lane == 0) {
-          const double step64 = __ddiv_rn(__dsub_rn(static_cast<double>(thi), static_cast<double>(tlo)), 255.0);
-          sx[r0 + t] = step64 > 0.0 ? __double2float_rn(step64) : 0.0f;
-          ox[r0 + t] = tlo;
-        }
-      }
-    }
-    __syncthreads();  // the tile buffer, s_red, s_lo/s_hi are free again
-    if constexpr (CODES) {
-      if (threadIdx.x < static_cast<uint32_t>(nr)) {
-        int sum = 0;
-#pragma unroll
-        for (int p = 0; p < PARTS; ++p) sum += s_sum[threadIdx.x][p];
-        rsx[r0 + threadIdx.x] = sum;
-      }
-    }
-    const int64_t next = tile + static_cast<int64_t>(NBUF) * gridDim.x;
-    if (threadIdx.x == 0 && next < ntiles) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue(next, b);
-    }
-  }
-}
-
-// Barrier-free pipelined variant (rows up to ~4.6K elements): a producer warp streams tiles of 8
-// token rows into an NBUF-deep ring (full/empty mbarriers); each of the 8 consumer warps takes
-// 1/8 of the tile's Z1 k-steps on the tensor cores, publishes its partial (zred mbarrier), then
-// owns one token row end to end — exact bf16 min/max scan and codes.  The warp it % 8 sums the
-// partials in fixed order (deterministic) and writes Z1.  Warps never wait for each other's codes,
-// so the per-row cost variance (tie replays) is absorbed by the ring instead of a CTA barrier.
-constexpr int AQP_TOK = 8, AQP_NC = 8;
-
-template <int J1>
-__host__ __device__ constexpr uint32_t aqp_row_pad() {
-  return J1 == 4 ? 64u : 16u;
-}
-
-template <int J1, int R1, int NBUF, bool CODES>
-__global__ void __launch_bounds__((AQP_NC + 1) * 32, 1)
-    k_aq_pipe(const __nv_bfloat16* __restrict__ x, int64_t T, int64_t K, uint8_t* __restrict__ codes, int64_t ldc,
-              float* __restrict__ sx, float* __restrict__ ox, int32_t* __restrict__ rsx,
-              const uint4* __restrict__ frag, __nv_bfloat16* __restrict__ zb, int64_t ldzb, float* __restrict__ zf) {
-  constexpr int K2 = J1 * R1, MT = R1 / 8, NJ = J1 == 4 ? 4 : 1, TOK = AQP_TOK, NC = AQP_NC;
-  static_assert(J1 == 1 || J1 == 4, "J1");
-  static_assert(R1 == 8 || R1 == 16, "R1");
-  extern __shared__ __align__(128) uint8_t aq_tile[];
-  __shared__ uint64_t full[NBUF], empty[NBUF], zred[NBUF];
-  const uint32_t warp = threadIdx.x >> 5, lane = lane_id(), g = lane >> 2, c = lane & 3;
-  const uint32_t rowbytes = static_cast<uint32_t>(K * 2), stride = rowbytes + aqp_row_pad<J1>();
-  const uint32_t nsteps = static_cast<uint32_t>(K / 64), nvec = static_cast<uint32_t>(K / 8);
-  const int64_t ntiles = (T + TOK - 1) / TOK;
-  float* s_red = reinterpret_cast<float*>(aq_tile + static_cast<size_t>(NBUF) * TOK * stride);  // [NBUF][NC][TOK*K2]
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int b = 0; b < NBUF; ++b) {
-      mbar_init(&full[b], 1);
-      mbar_init(&empty[b], NC);
-      mbar_init(&zred[b], NC);
-    }
-    fence_barrier_init();
-  }
-  __syncthreads();
-  if (warp == NC) {  // ---- producer
-    if (lane == 0) {
-      uint32_t it = 0;
-      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-        const int b = static_cast<int>(it % NBUF);
-        if (it >= static_cast<uint32_t>(NBUF)) mbar_wait(&empty[b], ((it / NBUF) - 1) & 1);
-        const int nr = static_cast<int>(T - tile * TOK < TOK ? T - tile * TOK : TOK);
-        mbar_arrive_expect_tx(&full[b], static_cast<uint32_t>(nr) * rowbytes);
-        for (int r = 0; r < nr; ++r)
-          bulk_load(aq_tile + (b * TOK + r) * stride, x + (tile * TOK + r) * K, rowbytes, &full[b]);
-      }
-    }
-    return;
-  }
-  uint32_t it = 0;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-    const int b = static_cast<int>(it % NBUF);
-    const uint32_t ph = (it / NBUF) & 1;
-    const uint8_t* buf = aq_tile + b * TOK * stride;
-    const int64_t r0 = tile * TOK;
-    const int nr = static_cast<int>(T - r0 < TOK ? T - r0 : TOK);
-    mbar_wait(&full[b], ph);
-    // ---- Z1 partial over this warp's k-steps
-    {
-      const uint8_t* myrow = buf + g * stride;
-      float acc[NJ][MT][4];
-#pragma unroll
-      for (int J = 0; J < NJ; ++J)
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-          for (int i = 0; i < 4; ++i) acc[J][mt][i] = 0.f;
-      auto kstep = [&](uint32_t st) {
-        const uint8_t* p = myrow + 128u * st;
-        const uint4 p0 = *reinterpret_cast<const uint4*>(p + (J1 == 4 ? 16u * c : 32u * c));
-        const uint4 p1 = *reinterpret_cast<const uint4*>(p + (J1 == 4 ? 64u + 16u * c : 32u * c + 16u));
-        const uint32_t w[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
-        if constexpr (J1 == 4) {
-          uint4 fr[MT];
-#pragma unroll
-          for (int mt = 0; mt < MT; ++mt) fr[mt] = __ldg(frag + (static_cast<size_t>(st) * MT + mt) * 32 + lane);
-#pragma unroll
-          for (int J = 0; J < 4; ++J) {
-            const uint32_t sel = (J & 1) ? 0x7632u : 0x5410u;
-            const uint32_t b0 = __byte_perm(w[J >> 1], w[2 + (J >> 1)], sel);
-            const uint32_t b1 = __byte_perm(w[4 + (J >> 1)], w[6 + (J >> 1)], sel);
-#pragma unroll
-            for (int mt = 0; mt < MT; ++mt) mma_16816(acc[J][mt], fr[mt].x, fr[mt].y, fr[mt].z, fr[mt].w, b0, b1);
-          }
-        } else {
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-#pragma unroll
-            for (int mt = 0; mt < MT; ++mt) {
-              const uint4 fr = __ldg(frag + ((static_cast<size_t>(st) * 4 + u) * MT + mt) * 32 + lane);
-              mma_16816(acc[0][mt], fr.x, fr.y, fr.z, fr.w, w[2 * u], w[2 * u + 1]);
-            }
-          }
-        }
-      };
-      uint32_t st = warp;
-      for (; st + NC < nsteps; st += 2 * NC) {  // two independent steps per iteration, no guards
-        kstep(st);
-        kstep(st + NC);
-      }
-      if (st < nsteps) kstep(st);
-      float* red = s_red + (static_cast<size_t>(b) * NC + warp) * (TOK * K2);
-#pragma unroll
-      for (int J = 0; J < NJ; ++J)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const uint32_t t = 2 * c + h;  // D columns 2c, 2c + 1 are tokens 2c, 2c + 1
-          if constexpr (MT == 1) {
-            red[t * K2 + g * J1 + J] = acc[J][0][h] + acc[J][0][2 + h];
-          } else {
-            red[t * K2 + g * J1 + J] = acc[J][0][h] + acc[J][1][h];
-            red[t * K2 + (g + 8) * J1 + J] = acc[J][0][2 + h] + acc[J][1][2 + h];
-          }
-        }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&zred[b]);
-    }
-    // ---- codes of token row `warp`
-    if (CODES && static_cast<int>(warp) < nr) {
-      const uint4* srow = reinterpret_cast<const uint4*>(buf + warp * stride);
-      __nv_bfloat162 lo2 = __floats2bfloat162_rn(INFINITY, INFINITY), hi2 = __floats2bfloat162_rn(-INFINITY, -INFINITY);
-      uint32_t cc = lane;
-      for (; cc + 96 < nvec; cc += 128) {
-        uint4 raw[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) raw[u] = srow[cc + 32 * u];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const uint32_t w[4] = {raw[u].x, raw[u].y, raw[u].z, raw[u].w};
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const __nv_bfloat162 b2 = *reinterpret_cast<const __nv_bfloat162*>(&w[i]);
-            lo2 = __hmin2(lo2, b2);
-            hi2 = __hmax2(hi2, b2);
-          }
-        }
-      }
-      for (; cc < nvec; cc += 32) {
-        const uint4 raw = srow[cc];
-        const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const __nv_bfloat162 b2 = *reinterpret_cast<const __nv_bfloat162*>(&w[i]);
-          lo2 = __hmin2(lo2, b2);
-          hi2 = __hmax2(hi2, b2);
-        }
-      }
-      const float lo = warp_min(fminf(__low2float(lo2), __high2float(lo2)));
-      const float hi = warp_max(fmaxf(__low2float(hi2), __high2float(hi2)));
-      const int64_t row = r0 + warp;
-      uint8_t* dst = codes + row * ldc;
-      int sum = aq_codes_range(srow, 0, nvec, lo, hi, dst);
-      for (int64_t kk = K + lane; kk < ldc; kk += 32) dst[kk] = 0;
-      sum = warp_sum_i(sum);
-      if (lane == 0) {
-        const double step64 = __ddiv_rn(__dsub_rn(static_cast<double>(hi), static_cast<double>(lo)), 255.0);
-        sx[row] = step64 > 0.0 ? __double2float_rn(step64) : 0.0f;
-        ox[row] = lo;
-        rsx[row] = sum;
-      }
-    }
-    // ---- Z1 of the tile (rotating finalizer), then release the buffer
-    if (warp == it % NC) {
-      mbar_wait(&zred[b], ph);
-      const float* red = s_red + static_cast<size_t>(b) * NC * (TOK * K2);
-      for (int i = static_cast<int>(lane); i < nr * K2; i += 32) {
-        float v = red[i];
-#pragma unroll
-        for (int w = 1; w < NC; ++w) v += red[w * (TOK * K2) + i];
-        const int64_t row = r0 + i / K2;
-        const int col = i % K2;
-        if (zf != nullptr) zf[row * K2 + col] = v;
-        if (zb != nullptr) {
-          const __nv_bfloat16 hv = __float2bfloat16_rn(v);
-          zb[row * ldzb + col] = hv;
-          zb[row * ldzb + K2 + col] = __float2bfloat16_rn(v - __bfloat162float(hv));
-          zb[row * ldzb + 2 * K2 + col] = hv;
-        }
-      }
-      if (zb != nullptr && ldzb > 3 * K2) {
-        const int padw = static_cast<int>(ldzb - 3 * K2);
-        for (int i = static_cast<int>(lane); i < nr * padw; i += 32)
-          zb[(r0 + i / padw) * ldzb + 3 * K2 + i % padw] = __float2bfloat16_rn(0.f);
-      }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[b]);
-  }
-}
-
 // ---------------------------------------------------------------------------------------------
 // CTA-per-8-token act-quant + Z1 (production path for bf16 rows, K % 64 == 0, J1 in {1, 4}).
 // Nothing is staged in shared memory but the G1 fragments: a CTA of AQC_WARPS warps owns 8 token
@@ -861,7 +343,7 @@ __global__ void __launch_bounds__((AQP_NC + 1) * 32, 1)
 //   pass 1 (the one HBM read of x): Z1 partials on the tensor cores (A = [G1_hi | G1_lo] fragments,
 //          k_g1_frag; B = the x words, exact in bf16) and the exact bf16 min / max, per warp.
 //   reduce : partials meet in shared memory and are summed in fixed warp order (deterministic).
-//   pass 2 : codes by the byte-grid rule (aq_codes8, bit-exact with quant.py:73-99) from a second
+//   pass 2 : codes by the byte-grid rule (aq_codes8b, bit-exact with quant.py:73-99) from a second
 //            read of the same 64-byte pieces by the same warp — a CTA's live rows are 8 x 2K bytes,
 //            so the re-read is served by L1 / L2, not HBM.  Bracketed elements (aq_codes8b) are
 //            replayed in fp64 in place.
@@ -1139,430 +621,6 @@ __global__ void __launch_bounds__(AQC_WARPS * 32, NA == 1 ? QA_AQC_MINB : QA_AQC
       __syncthreads();
     }
   }
-}
-
-// ---------------------------------------------------------------------------------------------
-// Register-resident variant of k_aq_cta (rows up to K = 11264): a CTA of W warps owns 8 token rows
-// at a time and warp w holds the S segments w, w + W, ... of all 8 rows in registers (two 16-byte
-// words per lane and segment, loaded up front).  Pass 1 (Z1 MMAs + min / max) and pass 2 (codes)
-// both read those registers: x crosses HBM once and is never re-read.  A bracketed code byte is
-// resolved in
-// place (aq_codes8b / aq_replay_word) while its bf16 inputs are still in registers.
-template <int J1, int R1, int W, int S, bool CODES>
-__global__ void __launch_bounds__(W * 32) k_aq_reg(const __nv_bfloat16* __restrict__ x, int64_t T, int64_t K,
-                                                    uint8_t* __restrict__ codes, int64_t ldc, float* __restrict__ sx,
-                                                    float* __restrict__ ox, int32_t* __restrict__ rsx,
-                                                    const uint4* __restrict__ frag, __nv_bfloat16* __restrict__ zb,
-                                                    int64_t ldzb, float* __restrict__ zf) {
-  static_assert(J1 == 1 || J1 == 4, "J1");
-  static_assert(R1 == 8 || R1 == 16, "R1");
-  constexpr int K2 = J1 * R1, MT = R1 / 8, NJ = J1 == 4 ? 4 : 1;
-  __shared__ float s_z[W][8][K2];
-  __shared__ float s_lo[W][8], s_hi[W][8];
-  __shared__ int32_t s_sum[W][8];
-  const uint32_t warp = threadIdx.x >> 5, lane = lane_id(), g = lane >> 2, c = lane & 3;
-  const int64_t nseg = K / 64;
-  uint32_t off0, off1;
-  aqc_offsets<J1>(c, off0, off1);
-  const int64_t ngroups = (T + 7) / 8;
-  for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
-    const int64_t t0 = grp * 8;
-    const bool valid = t0 + g < T;
-    const int64_t trow = valid ? t0 + g : T - 1;  // rows past T are computed on a clamped row, never stored
-    const uint8_t* xrow = reinterpret_cast<const uint8_t*>(x + trow * K);
-    uint4 p[S][2];
-#pragma unroll
-    for (int i = 0; i < S; ++i) {
-      const int64_t st = warp + static_cast<int64_t>(W) * i;
-      if (st < nseg) {
-        p[i][0] = __ldg(reinterpret_cast<const uint4*>(xrow + 128 * st + off0));
-        p[i][1] = __ldg(reinterpret_cast<const uint4*>(xrow + 128 * st + off1));
-      } else {
-        p[i][0] = p[i][1] = make_uint4(0u, 0u, 0u, 0u);
-      }
-    }
-    // ---- pass 1: Z1 partial + exact min / max over this warp's segments
-    float acc[NJ][MT][4];
-#pragma unroll
-    for (int J = 0; J < NJ; ++J)
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-        for (int i = 0; i < 4; ++i) acc[J][mt][i] = 0.f;
-    __nv_bfloat162 lo2 = __floats2bfloat162_rn(INFINITY, INFINITY), hi2 = __floats2bfloat162_rn(-INFINITY, -INFINITY);
-#pragma unroll
-    for (int i = 0; i < S; ++i) {
-      const int64_t st = warp + static_cast<int64_t>(W) * i;
-      if (st >= nseg) break;
-      const uint32_t w[8] = {p[i][0].x, p[i][0].y, p[i][0].z, p[i][0].w, p[i][1].x, p[i][1].y, p[i][1].z, p[i][1].w};
-      if (CODES) {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const __nv_bfloat162 b2 = *reinterpret_cast<const __nv_bfloat162*>(&w[k]);
-          lo2 = __hmin2(lo2, b2);
-          hi2 = __hmax2(hi2, b2);
-        }
-      }
-      if constexpr (J1 == 4) {
-        uint4 fr[MT];
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt) fr[mt] = frag[(st * MT + mt) * 32 + lane];
-#pragma unroll
-        for (int J = 0; J < 4; ++J) {
-          const uint32_t sel = (J & 1) ? 0x7632u : 0x5410u;
-          const uint32_t b0 = __byte_perm(w[J >> 1], w[2 + (J >> 1)], sel);
-          const uint32_t b1 = __byte_perm(w[4 + (J >> 1)], w[6 + (J >> 1)], sel);
-#pragma unroll
-          for (int mt = 0; mt < MT; ++mt) mma_16816(acc[J][mt], fr[mt].x, fr[mt].y, fr[mt].z, fr[mt].w, b0, b1);
-        }
-      } else {
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-          for (int mt = 0; mt < MT; ++mt) {
-            const uint4 fr = frag[((st * 4 + u) * MT + mt) * 32 + lane];
-            mma_16816(acc[0][mt], fr.x, fr.y, fr.z, fr.w, w[2 * u], w[2 * u + 1]);
-          }
-      }
-    }
-#pragma unroll
-    for (int J = 0; J < NJ; ++J)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        if constexpr (MT == 1) {
-          s_z[warp][2 * c + h][g * J1 + J] = acc[J][0][h] + acc[J][0][2 + h];
-        } else {
-          s_z[warp][2 * c + h][g * J1 + J] = acc[J][0][h] + acc[J][1][h];
-          s_z[warp][2 * c + h][(g + 8) * J1 + J] = acc[J][0][2 + h] + acc[J][1][2 + h];
-        }
-      }
-    if (CODES) {
-      float lo = fminf(__low2float(lo2), __high2float(lo2)), hi = fmaxf(__low2float(hi2), __high2float(hi2));
-      lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, 1));
-      lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, 2));
-      hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, 1));
-      hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, 2));
-      if (c == 0) {
-        s_lo[warp][g] = lo;
-        s_hi[warp][g] = hi;
-      }
-    }
-    __syncthreads();
-    // ---- Z1 of the 8 tokens: fixed-order sum of the warp partials
-    for (int i = static_cast<int>(threadIdx.x); i < 8 * K2; i += W * 32) {
-      const int tk = i / K2, col = i % K2;
-      const int64_t row = t0 + tk;
-      float v = s_z[0][tk][col];
-#pragma unroll
-      for (int w2 = 1; w2 < W; ++w2) v += s_z[w2][tk][col];
-      if (row < T) {
-        if (zf != nullptr) zf[row * K2 + col] = v;
-        if (zb != nullptr) {
-          const __nv_bfloat16 hv = __float2bfloat16_rn(v);
-          zb[row * ldzb + col] = hv;
-          zb[row * ldzb + K2 + col] = __float2bfloat16_rn(v - __bfloat162float(hv));
-          zb[row * ldzb + 2 * K2 + col] = hv;
-        }
-      }
-    }
-    if (zb != nullptr && ldzb > 3 * K2) {
-      const int padw = static_cast<int>(ldzb - 3 * K2);
-      for (int i = static_cast<int>(threadIdx.x); i < 8 * padw; i += W * 32) {
-        const int64_t row = t0 + i / padw;
-        if (row < T) zb[row * ldzb + 3 * K2 + i % padw] = __float2bfloat16_rn(0.f);
-      }
-    }
-    if constexpr (CODES) {
-      // ---- pass 2: codes of this warp's segments of row g, straight from the registers
-      float lo = s_lo[0][g], hi = s_hi[0][g];
-#pragma unroll
-      for (int w2 = 1; w2 < W; ++w2) {
-        lo = fminf(lo, s_lo[w2][g]);
-        hi = fmaxf(hi, s_hi[w2][g]);
-      }
-      AqRow r;
-      r.lo = lo;
-      r.lo64 = static_cast<double>(lo);
-      r.step64 = __ddiv_rn(__dsub_rn(static_cast<double>(hi), r.lo64), 255.0);
-      const bool flat = !(r.step64 > 0.0);
-      r.inv = flat ? 0.f : static_cast<float>(1.0 / r.step64);
-      const float nb = -lo * r.inv;
-      r.nbh = nb + 0.5f;
-      uint8_t* crow = codes + trow * ldc;
-      const bool sub = __any_sync(0xffffffffu, fabsf(nb) > 512.0f);
-      const unsigned long long inv2 = f2pack(r.inv, r.inv), nlo2 = f2pack(-r.lo, -r.lo);
-      const float alo = sub ? 0.5f - kTieBand : r.nbh - kTieBand, ahi = sub ? 0.5f + kTieBand : r.nbh + kTieBand;
-      const unsigned long long alo2 = f2pack(alo, alo), ahi2 = f2pack(ahi, ahi);
-      uint32_t sum = 0;
-#pragma unroll
-      for (int i = 0; i < S; ++i) {
-        const int64_t st = warp + static_cast<int64_t>(W) * i;
-        if (st >= nseg) break;
-        uint32_t cw[4], dw[4];
-        if (sub) {
-          aq_codes8b<true>(p[i][0], inv2, alo2, ahi2, nlo2, cw[0], cw[1], dw[0], dw[1]);
-          aq_codes8b<true>(p[i][1], inv2, alo2, ahi2, nlo2, cw[2], cw[3], dw[2], dw[3]);
-        } else {
-          aq_codes8b<false>(p[i][0], inv2, alo2, ahi2, nlo2, cw[0], cw[1], dw[0], dw[1]);
-          aq_codes8b<false>(p[i][1], inv2, alo2, ahi2, nlo2, cw[2], cw[3], dw[2], dw[3]);
-        }
-        if (flat) cw[0] = cw[1] = cw[2] = cw[3] = dw[0] = dw[1] = dw[2] = dw[3] = 0u;
-        if ((dw[0] | dw[1] | dw[2] | dw[3]) != 0u) {  // rare: replay the bracketed elements in fp64
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            if (dw[k] != 0u) cw[k] = aq_replay_word(k < 2 ? p[i][0] : p[i][1], (k & 1) * 4, cw[k], dw[k], r.lo64, r.step64);
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) sum = __dp4a(cw[k], 0x01010101u, sum);
-        if (valid) {
-          uint8_t* dst = crow + 64 * st + off0 / 2;
-          if constexpr (J1 == 4) {
-            *reinterpret_cast<uint2*>(dst) = make_uint2(cw[0], cw[1]);
-            *reinterpret_cast<uint2*>(dst + 32) = make_uint2(cw[2], cw[3]);
-          } else {
-            *reinterpret_cast<uint4*>(dst) = make_uint4(cw[0], cw[1], cw[2], cw[3]);
-          }
-        }
-      }
-      sum += __shfl_xor_sync(0xffffffffu, sum, 1);
-      sum += __shfl_xor_sync(0xffffffffu, sum, 2);
-      if (c == 0) s_sum[warp][g] = static_cast<int32_t>(sum);
-      if (warp == 0 && valid) {
-        if (c == 0) {
-          sx[trow] = flat ? 0.0f : __double2float_rn(r.step64);
-          ox[trow] = lo;
-        }
-        for (int64_t kk = K + c; kk < ldc; kk += 4) crow[kk] = 0;  // zero padding [K, ldc) of the codes row
-      }
-      __syncthreads();  // after this only s_sum is read until the next group's first barrier
-      if (threadIdx.x < 8 && t0 + threadIdx.x < T) {
-        int32_t s = 0;
-#pragma unroll
-        for (int w2 = 0; w2 < W; ++w2) s += s_sum[w2][threadIdx.x];
-        rsx[t0 + threadIdx.x] = s;
-      }
-    } else {
-      __syncthreads();
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------------------------
-// Ring-buffered act-quant + Z1 (production path for bf16 rows, K % 64 == 0): one CTA per SM streams
-// groups of TOKG token rows through a cp.async ring of shared-memory slots (~190 KB in flight per
-// SM: HBM stays busy without relying on register-resident loads or occupancy).  Per group:
-//   pass 1: Z1 partials on the tensor cores + exact bf16 min / max, warp w on the 64-element
-//           segments w, w + 8, ... (lane (g, c) of the m16n8k16 B fragment reads row g % TOKG;
-//           lanes g >= TOKG duplicate a row and are ignored);
-//   reduce: Z1 partials and min / max meet in shared memory (fixed warp order);
-//   pass 2: codes (aq_codes8b, bracketed fp32 + fp64 replay) from the same slot, each lane on a
-//           contiguous 16-element chunk (16 code bytes, one 16-byte store).
-constexpr int AQR_W = 16;
-
-template <int J1, int R1, int TOKG, bool CODES>
-__global__ void __launch_bounds__(AQR_W * 32, 1) k_aq_ring(const __nv_bfloat16* __restrict__ x, int64_t T, int64_t K,
-                                                           uint8_t* __restrict__ codes, int64_t ldc,
-                                                           float* __restrict__ sx, float* __restrict__ ox,
-                                                           int32_t* __restrict__ rsx, const uint4* __restrict__ frag,
-                                                           __nv_bfloat16* __restrict__ zb, int64_t ldzb,
-                                                           float* __restrict__ zf, int NS, int frag_smem) {
-  static_assert(TOKG == 8 || TOKG == 4 || TOKG == 2, "TOKG");
-  constexpr int K2 = J1 * R1, MT = R1 / 8, NJ = J1 == 4 ? 4 : 1, W = AQR_W, LPR = 32 / TOKG;
-  extern __shared__ __align__(16) uint8_t aqr_smem[];
-  __shared__ float s_z[W][8][K2];
-  __shared__ float s_lo[W][8], s_hi[W][8];
-  __shared__ int32_t s_sum[W][8];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, c = lane & 3;
-  const int64_t nseg = K / 64;
-  const int64_t rowb = K * 2 + 64;  // slot row stride in bytes (64-byte pad: conflict-free fragment reads)
-  const int64_t slotb = rowb * TOKG;
-  const int64_t ngroups = (T + TOKG - 1) / TOKG;
-  const int64_t mygroups = blockIdx.x < ngroups ? (ngroups - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  if (frag_smem) {  // G1 fragments next to the ring: the big ring leaves little L1 for __ldg
-    uint4* sf = reinterpret_cast<uint4*>(aqr_smem + NS * slotb);
-    const int64_t nf = nseg * (J1 == 4 ? 1 : 4) * MT * 32;
-    for (int64_t q = tid; q < nf; q += W * 32) sf[q] = frag[q];
-    frag = sf;  // visible after the first loop barrier
-  }
-  auto issue = [&](int64_t i) {
-    if (i < mygroups) {
-      const int64_t t0 = (blockIdx.x + i * gridDim.x) * TOKG;
-      uint8_t* slot = aqr_smem + (i % NS) * slotb;
-      const int chunks = static_cast<int>(K / 8);  // 16-byte pieces per row
-#pragma unroll
-      for (int r = 0; r < TOKG; ++r) {
-        const bool ok = t0 + r < T;
-        const __nv_bfloat16* src = x + (ok ? t0 + r : 0) * K;
-        uint8_t* dst = slot + r * rowb;
-        for (int ch = tid; ch < chunks; ch += W * 32) cp_async16(dst + ch * 16, src + ch * 8, ok);
-      }
-    }
-    cp_async_commit();
-  };
-  auto finish_sums = [&](int64_t i) {  // Σ codes of group i (needs the barrier after its pass 2)
-    const int64_t t0 = (blockIdx.x + i * gridDim.x) * TOKG;
-    if (CODES && tid < TOKG && t0 + tid < T) {
-      int32_t sum = 0;
-#pragma unroll
-      for (int w = 0; w < W; ++w) sum += s_sum[w][tid];
-      rsx[t0 + tid] = sum;
-    }
-  };
-  for (int i = 0; i < NS - 1; ++i) issue(i);
-  for (int64_t i = 0; i < mygroups; ++i) {
-    const int64_t t0 = (blockIdx.x + i * gridDim.x) * TOKG;
-    const int nr = static_cast<int>(T - t0 < TOKG ? T - t0 : TOKG);
-    const uint8_t* slot = aqr_smem + (i % NS) * slotb;
-    cp_async_wait_dyn(NS - 2);
-    __syncthreads();  // slot i landed for every thread; slot i - 1 and the shared partials are free
-    if (i > 0) finish_sums(i - 1);
-    issue(i + NS - 1);
-    // ---- pass 1
-    const uint8_t* myrow = slot + (g % TOKG) * rowb;
-    uint32_t off0, off1;
-    aqc_offsets<J1>(c, off0, off1);
-    float acc[NJ][MT][4];
-#pragma unroll
-    for (int J = 0; J < NJ; ++J)
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-        for (int k = 0; k < 4; ++k) acc[J][mt][k] = 0.f;
-    __nv_bfloat162 lo2 = __floats2bfloat162_rn(INFINITY, INFINITY), hi2 = __floats2bfloat162_rn(-INFINITY, -INFINITY);
-    for (int64_t st = warp; st < nseg; st += W) {
-      const uint4 p0 = *reinterpret_cast<const uint4*>(myrow + 128 * st + off0);
-      const uint4 p1 = *reinterpret_cast<const uint4*>(myrow + 128 * st + off1);
-      const uint32_t w[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
-      if (CODES) {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const __nv_bfloat162 b2 = *reinterpret_cast<const __nv_bfloat162*>(&w[k]);
-          lo2 = __hmin2(lo2, b2);
-          hi2 = __hmax2(hi2, b2);
-        }
-      }
-      if constexpr (J1 == 4) {
-        uint4 fr[MT];
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt) fr[mt] = frag[(st * MT + mt) * 32 + lane];
-#pragma unroll
-        for (int J = 0; J < 4; ++J) {
-          const uint32_t sel = (J & 1) ? 0x7632u : 0x5410u;
-          const uint32_t b0 = __byte_perm(w[J >> 1], w[2 + (J >> 1)], sel);
-          const uint32_t b1 = __byte_perm(w[4 + (J >> 1)], w[6 + (J >> 1)], sel);
-#pragma unroll
-          for (int mt = 0; mt < MT; ++mt) mma_16816(acc[J][mt], fr[mt].x, fr[mt].y, fr[mt].z, fr[mt].w, b0, b1);
-        }
-      } else {
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-          for (int mt = 0; mt < MT; ++mt) {
-            const uint4 fr = frag[((st * 4 + u) * MT + mt) * 32 + lane];
-            mma_16816(acc[0][mt], fr.x, fr.y, fr.z, fr.w, w[2 * u], w[2 * u + 1]);
-          }
-      }
-    }
-#pragma unroll
-    for (int J = 0; J < NJ; ++J)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        if constexpr (MT == 1) {
-          s_z[warp][2 * c + h][g * J1 + J] = acc[J][0][h] + acc[J][0][2 + h];
-        } else {
-          s_z[warp][2 * c + h][g * J1 + J] = acc[J][0][h] + acc[J][1][h];
-          s_z[warp][2 * c + h][(g + 8) * J1 + J] = acc[J][0][2 + h] + acc[J][1][2 + h];
-        }
-      }
-    if (CODES) {
-      float lo = fminf(__low2float(lo2), __high2float(lo2)), hi = fmaxf(__low2float(hi2), __high2float(hi2));
-      lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, 1));
-      lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, 2));
-      hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, 1));
-      hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, 2));
-      if (c == 0) {
-        s_lo[warp][g] = lo;
-        s_hi[warp][g] = hi;
-      }
-    }
-    __syncthreads();
-    for (int k = tid; k < nr * K2; k += W * 32) {  // Z1: fixed-order sum of the warp partials
-      const int tk = k / K2, col = k % K2;
-      const int64_t row = t0 + tk;
-      float v = s_z[0][tk][col];
-#pragma unroll
-      for (int w2 = 1; w2 < W; ++w2) v += s_z[w2][tk][col];
-      if (zf != nullptr) zf[row * K2 + col] = v;
-      if (zb != nullptr) {
-        const __nv_bfloat16 hv = __float2bfloat16_rn(v);
-        zb[row * ldzb + col] = hv;
-        zb[row * ldzb + K2 + col] = __float2bfloat16_rn(v - __bfloat162float(hv));
-        zb[row * ldzb + 2 * K2 + col] = hv;
-      }
-    }
-    if (zb != nullptr && ldzb > 3 * K2) {
-      const int padw = static_cast<int>(ldzb - 3 * K2);
-      for (int k = tid; k < nr * padw; k += W * 32) zb[(t0 + k / padw) * ldzb + 3 * K2 + k % padw] = __float2bfloat16_rn(0.f);
-    }
-    if constexpr (CODES) {
-      // ---- pass 2: lane -> (token r, 16-element chunk j of each 512 / TOKG-element super-segment)
-      const int r = lane / LPR, j = lane % LPR;
-      float lo = s_lo[0][r], hi = s_hi[0][r];
-#pragma unroll
-      for (int w2 = 1; w2 < W; ++w2) {
-        lo = fminf(lo, s_lo[w2][r]);
-        hi = fmaxf(hi, s_hi[w2][r]);
-      }
-      const double lo64 = static_cast<double>(lo);
-      const double step64 = __ddiv_rn(__dsub_rn(static_cast<double>(hi), lo64), 255.0);
-      const bool flat = !(step64 > 0.0);
-      const float inv = flat ? 0.f : static_cast<float>(1.0 / step64);
-      const float nb = -lo * inv;
-      const bool sub = __any_sync(0xffffffffu, fabsf(nb) > 512.0f);
-      const float alo = sub ? 0.5f - kTieBand : nb + 0.5f - kTieBand, ahi = sub ? 0.5f + kTieBand : nb + 0.5f + kTieBand;
-      const unsigned long long inv2 = f2pack(inv, inv), nlo2 = f2pack(-lo, -lo), alo2 = f2pack(alo, alo),
-                               ahi2 = f2pack(ahi, ahi);
-      const bool valid = r < nr;
-      const uint8_t* xr = slot + r * rowb;
-      uint8_t* crow = codes + (t0 + (valid ? r : 0)) * ldc;
-      const int64_t nss = K / (512 / TOKG);  // super-segments per row
-      uint32_t sum = 0;
-      for (int64_t ss = warp; ss < nss; ss += W) {
-        const int64_t e0 = ss * (512 / TOKG) + j * 16;  // first element of the lane's chunk
-        const uint4 p0 = *reinterpret_cast<const uint4*>(xr + 2 * e0);
-        const uint4 p1 = *reinterpret_cast<const uint4*>(xr + 2 * e0 + 16);
-        uint32_t cw[4], dw[4];
-        if (sub) {
-          aq_codes8b<true>(p0, inv2, alo2, ahi2, nlo2, cw[0], cw[1], dw[0], dw[1]);
-          aq_codes8b<true>(p1, inv2, alo2, ahi2, nlo2, cw[2], cw[3], dw[2], dw[3]);
-        } else {
-          aq_codes8b<false>(p0, inv2, alo2, ahi2, nlo2, cw[0], cw[1], dw[0], dw[1]);
-          aq_codes8b<false>(p1, inv2, alo2, ahi2, nlo2, cw[2], cw[3], dw[2], dw[3]);
-        }
-        if (flat) cw[0] = cw[1] = cw[2] = cw[3] = dw[0] = dw[1] = dw[2] = dw[3] = 0u;
-        if ((dw[0] | dw[1] | dw[2] | dw[3]) != 0u) {
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            if (dw[k] != 0u) cw[k] = aq_replay_word(k < 2 ? p0 : p1, (k & 1) * 4, cw[k], dw[k], lo64, step64);
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) sum = __dp4a(cw[k], 0x01010101u, sum);
-        if (valid) *reinterpret_cast<uint4*>(crow + e0) = make_uint4(cw[0], cw[1], cw[2], cw[3]);
-      }
-#pragma unroll
-      for (int o = 1; o < LPR; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-      if (j == 0) s_sum[warp][r] = static_cast<int32_t>(sum);
-      if (warp == 0 && valid && j == 0) {
-        sx[t0 + r] = flat ? 0.0f : __double2float_rn(step64);
-        ox[t0 + r] = lo;
-      }
-      if (valid && ldc > K)
-        for (int64_t kk = K + warp * LPR + j; kk < ldc; kk += W * LPR) crow[kk] = 0;  // zero padding [K, ldc)
-    }
-  }
-  cp_async_wait_dyn(0);
-  __syncthreads();
-  if (mygroups > 0) finish_sums(mygroups - 1);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -2833,110 +1891,6 @@ __global__ void __launch_bounds__(256, 1) k_tt_dg1m(const __nv_bfloat16* __restr
     }
 }
 
-// Ring-buffered x pass for bf16 rows (J1 = 4): each thread owns 8 columns and streams its own
-// 16-byte pieces of x through a 3-stage cp.async ring (8 token rows per stage), so the bytes in
-// flight per SM (up to 2 CTAs x 2 stages x 32 KB) no longer depend on registers.  The ring is
-// thread-private: only the dZ1 block (32 tokens) needs CTA barriers.
-constexpr int DG_ROWS = 8, DG_NST = 3;
-
-template <int R1>
-__global__ void __launch_bounds__(256) k_tt_dg1r(const __nv_bfloat16* __restrict__ x, int64_t T, int64_t K,
-                                                 const float* __restrict__ dz1, float* __restrict__ part, int S,
-                                                 int HS, __nv_bfloat16* __restrict__ dz1b, int64_t ldb) {
-  constexpr int J1 = 4, K2 = J1 * R1, NJ = 2, TB = 32;
-  __shared__ __align__(16) float sdz[TB][J1][R1];
-  extern __shared__ __align__(16) uint4 sxr[];  // [DG_NST][DG_ROWS][256]
-  const int tid = threadIdx.x;
-  const int64_t col0 = (static_cast<int64_t>(blockIdx.x) * 256 + tid) * 8;
-  const bool active = col0 < K;
-  const int s = blockIdx.y;
-  const int64_t per = (T + S - 1) / S;
-  const int64_t t0 = s * per, t1 = t0 + per < T ? t0 + per : T;
-  const int64_t nst = t1 > t0 ? (t1 - t0 + DG_ROWS - 1) / DG_ROWS : 0;
-  unsigned long long acc[NJ][R1 / 2];
-#pragma unroll
-  for (int j = 0; j < NJ; ++j)
-#pragma unroll
-    for (int a = 0; a < R1 / 2; ++a) acc[j][a] = 0ull;
-  auto issue = [&](int64_t k) {
-    if (k < nst) {
-#pragma unroll
-      for (int r = 0; r < DG_ROWS; ++r) {
-        const int64_t t = t0 + k * DG_ROWS + r;
-        const bool ok = active && t < t1;
-        cp_async16(&sxr[(static_cast<int>(k % DG_NST) * DG_ROWS + r) * 256 + tid], ok ? x + t * K + col0 : x, ok);
-      }
-    }
-    cp_async_commit();
-  };
-  for (int k = 0; k < DG_NST - 1; ++k) issue(k);
-  for (int64_t k = 0; k < nst; ++k) {
-    if (k % (TB / DG_ROWS) == 0) {
-      const int64_t tb = t0 + k * DG_ROWS;
-      const int nt = static_cast<int>(t1 - tb < TB ? t1 - tb : TB);
-      __syncthreads();
-      for (int i = tid; i < nt * K2; i += 256) {
-        const int r = i / K2, cc = i % K2;
-        const int64_t off = (tb + r) * K2 + cc;
-        float v = dz1[off];
-        for (int h = 1; h < HS; ++h) v += dz1[static_cast<int64_t>(h) * T * K2 + off];
-        sdz[r][cc % J1][cc / J1] = v;
-      }
-      __syncthreads();
-      if (dz1b != nullptr && blockIdx.x == 0) {
-        for (int i = tid; i < nt * static_cast<int>(ldb); i += 256) {
-          const int r = i / static_cast<int>(ldb), c = i % static_cast<int>(ldb);
-          float v = 0.f;
-          if (c < 3 * K2) {  // [hi | lo | hi]
-            const int cc = c % K2;
-            const float f = sdz[r][cc % J1][cc / J1];
-            v = __bfloat162float(__float2bfloat16_rn(f));
-            if (c >= K2 && c < 2 * K2) v = f - v;
-          }
-          dz1b[(tb + r) * ldb + c] = __float2bfloat16_rn(v);
-        }
-      }
-    }
-    issue(k + DG_NST - 1);
-    cp_async_wait<DG_NST - 1>();
-    if (!active) continue;
-    const int rb = static_cast<int>(k % (TB / DG_ROWS)) * DG_ROWS;
-    const int nr = static_cast<int>(t1 - (t0 + k * DG_ROWS) < DG_ROWS ? t1 - (t0 + k * DG_ROWS) : DG_ROWS);
-    for (int r = 0; r < nr; ++r) {
-      const uint4 raw = sxr[(static_cast<int>(k % DG_NST) * DG_ROWS + r) * 256 + tid];
-      const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
-#pragma unroll
-      for (int J = 0; J < J1; ++J) {
-        const float4* dz4 = reinterpret_cast<const float4*>(&sdz[rb + r][J][0]);
-        float4 d4[R1 / 4];
-#pragma unroll
-        for (int q = 0; q < R1 / 4; ++q) d4[q] = dz4[q];
-#pragma unroll
-        for (int j = 0; j < NJ; ++j) {
-          const int e = j * J1 + J;  // element e of the 8: bf16 half (e & 1) of word e / 2
-          const float xv = __uint_as_float((e & 1) ? (w[e >> 1] & 0xFFFF0000u) : (w[e >> 1] << 16));
-          const unsigned long long xx = f2pack(xv, xv);
-#pragma unroll
-          for (int q = 0; q < R1 / 4; ++q) {
-            ffma2(acc[j][2 * q], xx, f2pack(d4[q].x, d4[q].y));
-            ffma2(acc[j][2 * q + 1], xx, f2pack(d4[q].z, d4[q].w));
-          }
-        }
-      }
-    }
-  }
-  cp_async_wait<0>();
-  if (!active) return;
-  float* dst = part + static_cast<int64_t>(s) * (K / J1) * R1;
-#pragma unroll
-  for (int j = 0; j < NJ; ++j)
-#pragma unroll
-    for (int a = 0; a < R1 / 2; ++a) {
-      dst[(col0 / J1 + j) * R1 + 2 * a] = f2lo(acc[j][a]);
-      dst[(col0 / J1 + j) * R1 + 2 * a + 1] = f2hi(acc[j][a]);
-    }
-}
-
 template <typename InT, int J1, int R1>
 __global__ void __launch_bounds__(256) k_tt_dg1(const InT* __restrict__ x, int64_t T, int64_t K,
                                                 const float* __restrict__ dz1, float* __restrict__ part, int S,
@@ -3222,71 +2176,6 @@ bool fast_tt_supported(int J1, int R1) {
   return (J1 == 1 && (R1 == 8 || R1 == 16)) || (J1 == 4 && (R1 == 8 || R1 == 16));
 }
 
-// QA_AQ_MMA=0 selects the register-streaming act-quant kernel (A/B comparisons).
-bool aq_mma_disabled() {
-  static const bool off = [] {
-    const char* v = getenv("QA_AQ_MMA");
-    return v != nullptr && v[0] == '0';
-  }();
-  return off;
-}
-
-// QA_DG1_MMA=0 selects the FFMA2 x pass (A/B comparisons).
-bool dg1_mma_disabled() {
-  static const bool off = [] {
-    const char* v = getenv("QA_DG1_MMA");
-    return v != nullptr && v[0] == '0';
-  }();
-  return off;
-}
-
-// QA_FUSED_BWD=0 selects the unfused dy pass / middle-core kernels (A/B comparisons).
-bool fused_bwd_disabled() {
-  static const bool off = [] {
-    const char* v = getenv("QA_FUSED_BWD");
-    return v != nullptr && v[0] == '0';
-  }();
-  return off;
-}
-
-// QA_AQ_RING=1 selects the ring-buffered act-quant kernel (measured slower than k_aq_cta on B200:
-// one 16-warp CTA per SM is issue-bound on the codes pass; kept for A/B comparisons).
-bool aq_ring_disabled() {
-  static const bool off = [] {
-    const char* v = getenv("QA_AQ_RING");
-    return !(v != nullptr && v[0] == '1');
-  }();
-  return off;
-}
-
-// QA_AQ_REG=1 selects the register-resident k_aq_reg kernel (measured slower than k_aq_cta on
-// B200: 2 CTAs / SM at 120 registers; kept for A/B comparisons).
-bool aq_reg_disabled() {
-  static const bool off = [] {
-    const char* v = getenv("QA_AQ_REG");
-    return !(v != nullptr && v[0] == '1');
-  }();
-  return off;
-}
-
-// QA_AQ_CTA=0 falls back to the shared-memory-staged act-quant kernels below (A/B comparisons).
-bool aq_cta_disabled() {
-  static const bool off = [] {
-    const char* v = getenv("QA_AQ_CTA");
-    return v != nullptr && v[0] == '0';
-  }();
-  return off;
-}
-
-// QA_AQ_PIPE=0 selects the CTA-barrier tensor-core act-quant kernel (A/B comparisons).
-bool aq_pipe_disabled() {
-  static const bool off = [] {
-    const char* v = getenv("QA_AQ_PIPE");
-    return v != nullptr && v[0] == '0';
-  }();
-  return off;
-}
-
 size_t g1i_floats(int64_t K, int J1, int R1) {
   const int64_t nvec = K / 8;
   return static_cast<size_t>(((nvec + 31) / 32) * 32) * 8 * R1 / J1 * 2;  // >= the k_g1_frag fragments
@@ -3298,7 +2187,7 @@ cudaError_t launch_actquant_z1(const void* x, int x_dtype, int64_t T, int64_t K,
   if (T == 0) return cudaSuccess;
   const int64_t nvec = K / 8;
   // ---- production path: CTA-per-8-token kernel, rows read straight from global memory
-  if (x_dtype == QA_BF16 && !aq_cta_disabled() && K % 64 == 0 && (J1 == 1 || J1 == 4) && (R1 == 8 || R1 == 16) &&
+  if (x_dtype == QA_BF16 && K % 64 == 0 && (J1 == 1 || J1 == 4) && (R1 == 8 || R1 == 16) &&
       reinterpret_cast<uintptr_t>(x) % 16 == 0 &&
       (!want_codes || (ldc % 16 == 0 && reinterpret_cast<uintptr_t>(codes) % 16 == 0)) &&
       (zf == nullptr || reinterpret_cast<uintptr_t>(zf) % 16 == 0)) {
@@ -3330,80 +2219,6 @@ cudaError_t launch_actquant_z1(const void* x, int x_dtype, int64_t T, int64_t K,
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     const int64_t ngroups = (T + 7) / 8;
-    const int64_t nseg = K / 64;
-    if (!aq_ring_disabled()) {  // ring-buffered rows: pick the widest group whose slot allows >= 3 slots
-      const size_t budget = 180 * 1024;  // dynamic ring; ~40 KB static partials (16 warps)
-      const size_t rowb = static_cast<size_t>(K) * 2 + 64;
-      int tokg = 0;
-      for (int tg : {8, 4, 2})
-        if (3 * rowb * tg <= budget) {
-          tokg = tg;
-          break;
-        }
-      if (tokg > 0 && K % (512 / tokg) == 0) {
-        const size_t slotb = rowb * tokg;
-        const size_t fbytes = static_cast<size_t>(nfrag) * MT * 32 * 16;
-        const int fsm = fbytes <= 64 * 1024 && 3 * slotb + fbytes <= 180 * 1024 ? 1 : 0;
-        int ns = static_cast<int>((180 * 1024 - (fsm ? fbytes : 0)) / slotb);
-        if (ns > 6) ns = 6;
-        const size_t smem = slotb * ns + (fsm ? fbytes : 0);
-        const int64_t groups = (T + tokg - 1) / tokg;
-        const unsigned grid = static_cast<unsigned>(groups < nsm ? groups : nsm);
-#define QA_AQG(JJ, RR, TG)                                                                                     \
-  {                                                                                                            \
-    auto kern = want_codes ? k_aq_ring<JJ, RR, TG, true> : k_aq_ring<JJ, RR, TG, false>;                       \
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));          \
-    kern<<<grid, AQR_W * 32, smem, s>>>(static_cast<const __nv_bfloat16*>(x), T, K, codes, ldc, sx, ox, rsx, fr, \
-                                        zb, ldzb, zf, ns, fsm);                                                \
-  }
-#define QA_AQG_T(JJ, RR) \
-  if (tokg == 8)         \
-    QA_AQG(JJ, RR, 8)    \
-  else if (tokg == 4)    \
-    QA_AQG(JJ, RR, 4)    \
-  else                   \
-    QA_AQG(JJ, RR, 2)
-        if (J1 == 1 && R1 == 8)
-          QA_AQG_T(1, 8)
-        else if (J1 == 1)
-          QA_AQG_T(1, 16)
-        else if (R1 == 8)
-          QA_AQG_T(4, 8)
-        else
-          QA_AQG_T(4, 16)
-#undef QA_AQG_T
-#undef QA_AQG
-        return cudaGetLastError();
-      }
-    }
-    if (nseg <= 176 && !aq_reg_disabled()) {  // register-resident rows
-#define QA_AQR(JJ, RR, WW, SS)                                                                                \
-  {                                                                                                           \
-    auto kern = want_codes ? k_aq_reg<JJ, RR, WW, SS, true> : k_aq_reg<JJ, RR, WW, SS, false>;                \
-    int per_sm = 1;                                                                                           \
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WW * 32, 0);                                 \
-    const int64_t cap = static_cast<int64_t>(per_sm < 1 ? 1 : per_sm) * nsm;                                  \
-    const unsigned grid = static_cast<unsigned>(ngroups < cap ? ngroups : cap);                               \
-    kern<<<grid, WW * 32, 0, s>>>(static_cast<const __nv_bfloat16*>(x), T, K, codes, ldc, sx, ox, rsx, fr, zb, \
-                                  ldzb, zf);                                                                  \
-  }
-#define QA_AQR_W(JJ, RR)     \
-  if (nseg <= 64)            \
-    QA_AQR(JJ, RR, 8, 8)     \
-  else                       \
-    QA_AQR(JJ, RR, 16, 11)
-      if (J1 == 1 && R1 == 8)
-        QA_AQR_W(1, 8)
-      else if (J1 == 1)
-        QA_AQR_W(1, 16)
-      else if (R1 == 8)
-        QA_AQR_W(4, 8)
-      else
-        QA_AQR_W(4, 16)
-#undef QA_AQR_W
-#undef QA_AQR
-      return cudaGetLastError();
-    }
     const size_t frag_bytes = static_cast<size_t>(nfrag) * MT * 32 * 16;
     const bool fsmem = frag_bytes <= 48 * 1024;
     const size_t smem = fsmem ? frag_bytes : 0;
@@ -3440,99 +2255,6 @@ cudaError_t launch_actquant_z1(const void* x, int x_dtype, int64_t T, int64_t K,
 #undef QA_AQC_C
 #undef QA_AQC
     return cudaGetLastError();
-  }
-  // ---- tensor-core path (bf16 rows): TOK = 8 rows per tile when two tiles fit an SM, else 4
-  if (x_dtype == QA_BF16 && !aq_mma_disabled() && K % 64 == 0 && K <= 32768 && (J1 == 1 || J1 == 4)) {
-    const uint32_t pad = J1 == 4 ? aq_row_pad<4>() : aq_row_pad<1>();
-    const size_t tile_bytes = (static_cast<size_t>(K) * 2 + pad) * AQ_TOK;
-    const int nbuf = 3 * tile_bytes <= 200 * 1024 ? 3 : 2;
-    const size_t smem = nbuf * tile_bytes;
-    if (smem <= 200 * 1024) {
-      const int MT = R1 / 8;
-      const int64_t nfrag = (J1 == 4 ? K / 64 : K / 16);
-      {
-        LaunchScope scope(kTT, double(nfrag) * MT * 32 * 16 + double(K) * R1 * 4, s);
-        count_launches(1);
-        const int64_t n = nfrag * MT * 32;
-        const unsigned g = static_cast<unsigned>((n + 255) / 256);
-        uint4* fr = reinterpret_cast<uint4*>(g1i_ws);
-        if (J1 == 1 && R1 == 8)
-          k_g1_frag<1, 8><<<g, 256, 0, s>>>(G1, fr, nfrag);
-        else if (J1 == 1)
-          k_g1_frag<1, 16><<<g, 256, 0, s>>>(G1, fr, nfrag);
-        else if (R1 == 8)
-          k_g1_frag<4, 8><<<g, 256, 0, s>>>(G1, fr, nfrag);
-        else
-          k_g1_frag<4, 16><<<g, 256, 0, s>>>(G1, fr, nfrag);
-        cudaError_t e = cudaGetLastError();
-        if (e != cudaSuccess) return e;
-      }
-      LaunchScope scope(kQuantize, double(T) * K * 2 + (want_codes ? double(T) * ldc + 12.0 * T : 0.0) +
-                                       double(T) * (zb ? ldzb * 2 : 0) + double(T) * (zf ? J1 * R1 * 4 : 0),
-                        s);
-      count_launches(1);
-      const uint4* fr = reinterpret_cast<const uint4*>(g1i_ws);
-      // barrier-free pipelined kernel when a 2- or 3-deep ring of 8-row tiles fits
-      const size_t ptile = (static_cast<size_t>(K) * 2 + pad) * AQP_TOK;
-      const size_t pred = static_cast<size_t>(AQP_NC) * AQP_TOK * J1 * R1 * 4;
-      const int pbuf = 3 * (ptile + pred) <= 220 * 1024 ? 3 : (2 * (ptile + pred) <= 220 * 1024 ? 2 : 0);
-      if (pbuf > 0 && K <= 16384 && !aq_pipe_disabled()) {
-        const size_t psmem = pbuf * (ptile + pred);
-        const int64_t pt = (T + AQP_TOK - 1) / AQP_TOK;
-        const unsigned grid = static_cast<unsigned>(pt < 148 ? pt : 148);
-#define QA_AQP(JJ, RR, NB)                                                                                     \
-  {                                                                                                            \
-    auto kern = want_codes ? k_aq_pipe<JJ, RR, NB, true> : k_aq_pipe<JJ, RR, NB, false>;                       \
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(psmem));         \
-    kern<<<grid, (AQP_NC + 1) * 32, psmem, s>>>(static_cast<const __nv_bfloat16*>(x), T, K, codes, ldc, sx, ox, \
-                                                rsx, fr, zb, ldzb, zf);                                        \
-  }
-#define QA_AQP_T(JJ, RR) \
-  if (pbuf == 3)         \
-    QA_AQP(JJ, RR, 3)    \
-  else                   \
-    QA_AQP(JJ, RR, 2)
-        if (J1 == 1 && R1 == 8)
-          QA_AQP_T(1, 8)
-        else if (J1 == 1)
-          QA_AQP_T(1, 16)
-        else if (R1 == 8)
-          QA_AQP_T(4, 8)
-        else
-          QA_AQP_T(4, 16)
-#undef QA_AQP_T
-#undef QA_AQP
-        return cudaGetLastError();
-      }
-      const int64_t ntiles = (T + AQ_TOK - 1) / AQ_TOK;
-#define QA_AQM(JJ, RR, NB)                                                                                      \
-  {                                                                                                             \
-    auto kern = want_codes ? k_aq_mma<JJ, RR, NB, true> : k_aq_mma<JJ, RR, NB, false>;                          \
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));           \
-    int per_sm = 1;                                                                                             \
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, AQ_NW * 32, smem);                             \
-    const int64_t cap = static_cast<int64_t>(per_sm < 1 ? 1 : per_sm) * 148;                                    \
-    const unsigned grid = static_cast<unsigned>(ntiles < cap ? ntiles : cap);                                   \
-    kern<<<grid, AQ_NW * 32, smem, s>>>(static_cast<const __nv_bfloat16*>(x), T, K, codes, ldc, sx, ox, rsx, fr, \
-                                        zb, ldzb, zf);                                                          \
-  }
-#define QA_AQM_T(JJ, RR) \
-  if (nbuf == 3)         \
-    QA_AQM(JJ, RR, 3)    \
-  else                   \
-    QA_AQM(JJ, RR, 2)
-      if (J1 == 1 && R1 == 8)
-        QA_AQM_T(1, 8)
-      else if (J1 == 1)
-        QA_AQM_T(1, 16)
-      else if (R1 == 8)
-        QA_AQM_T(4, 8)
-      else
-        QA_AQM_T(4, 16)
-#undef QA_AQM_T
-#undef QA_AQM
-      return cudaGetLastError();
-    }
   }
   {
     const int64_t n = nvec * 2 * R1 / J1;
@@ -3643,31 +2365,19 @@ cudaError_t launch_tt_dy(const __nv_bfloat16* dy, int64_t T, int64_t N, int H, i
 }
 
 bool tt_bwd_fused_ok(int d, int J1, int R1, int C, int M) {
-  return d == 3 && J1 == 4 && M == FB_COLS && R1 == C && (C == 8 || C == 16) && !fused_bwd_disabled();
+  return d == 3 && J1 == 4 && M == FB_COLS && R1 == C && (C == 8 || C == 16);
 }
 
 // h-range per CTA: the dG2 accumulators (HR x K2 x C fp32) and Gm_h stay <= 64 KB of shared memory
-bool ws_bwd_disabled() {
-  static const bool off = [] {
-    const char* v = getenv("QA_WS_BWD");
-    return v != nullptr && v[0] == '0';
-  }();
-  return off;
-}
-
 void tt_bwd_fused_plan(int64_t T, int H, int C, int* HR, int* HS, int* TS) {
   const int hr_max = C == 8 ? 16 : 8;
   *HS = (H + hr_max - 1) / hr_max;
   *HR = (H + *HS - 1) / *HS;
-  const bool ws = C == 8 && !ws_bwd_disabled();  // k_tt_bwd_ws: 16-token tiles, one CTA per SM
+  const bool ws = C == 8;  // k_tt_bwd_ws: 16-token tiles, one CTA per SM
   const int64_t tiles = (T + (ws ? WS_TT : FB_TT) - 1) / (ws ? WS_TT : FB_TT);
   // rank 16: two CTAs per SM (120 registers; measured 9.7 -> 8.7 ms of TT side kernels at config 3 vs
-  // one; three or four were not better). QA_FB16_PER_SM overrides.
-  static const int per_sm16 = [] {
-    const char* v = getenv("QA_FB16_PER_SM");
-    return v != nullptr ? atoi(v) : 2;
-  }();
-  const int per_sm = ws ? 1 : (C == 8 ? 2 : (per_sm16 >= 1 ? per_sm16 : 1));
+  // one; three or four were not better)
+  const int per_sm = ws ? 1 : 2;
   int64_t ts = (static_cast<int64_t>(per_sm) * 148 + *HS - 1) / *HS;
   if (ts > tiles) ts = tiles;
   *TS = static_cast<int>(ts < 1 ? 1 : ts);
@@ -3684,14 +2394,10 @@ cudaError_t launch_tt_bwd_fused(const __nv_bfloat16* dy, int64_t ldy, int64_t T,
   LaunchScope scope(kTT, 2.0 * double(T) * N + 4.0 * double(T) * 4 * C * (1 + HS), s);
   count_launches(1);
   const dim3 grid(static_cast<unsigned>(HS), static_cast<unsigned>(TS));
-  if (C == 8 && !ws_bwd_disabled()) {
+  if (C == 8) {
     const size_t smem = WsLayout::bytes(HR);
     cudaFuncSetAttribute(k_tt_bwd_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     k_tt_bwd_ws<<<grid, 256, smem, s>>>(dy, ldy, T, H, HR, Z1, G2, G3, dz1p, g3part, g2part);
-  } else if (C == 8) {
-    const size_t smem = FbLayout<8>::bytes(HR);
-    cudaFuncSetAttribute(k_tt_bwd_fused<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    k_tt_bwd_fused<8><<<grid, 256, smem, s>>>(dy, ldy, T, H, HR, Z1, G2, G3, dz1p, g3part, g2part);
   } else {
     const size_t smem = FbLayout<16>::bytes(HR);
     cudaFuncSetAttribute(k_tt_bwd_fused<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -3733,8 +2439,7 @@ cudaError_t launch_grad_reduce3(const float* const* parts, const int* nparts, co
 // ---- shared-input groups (a decoder layer's q / k / v and up / gate, transformer.py:862-874):
 // one x pass serves NA in {2, 3} adapters of the pinned modes with J1 = 4, R1 = 8.
 bool group_x_pass_ok(int J1, int R1, int64_t K, int NA, const void* x) {
-  return J1 == 4 && R1 == 8 && NA >= 2 && NA <= 3 && K % 64 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0 &&
-         !aq_cta_disabled() && !dg1_mma_disabled();
+  return J1 == 4 && R1 == 8 && NA >= 2 && NA <= 3 && K % 64 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0;
 }
 
 cudaError_t launch_actquant_z1_group(const void* x, int64_t T, int64_t K, bool want_codes, uint8_t* codes,
@@ -3785,24 +2490,14 @@ cudaError_t launch_actquant_z1_group(const void* x, int64_t T, int64_t K, bool w
 
 // x-pass occupancy: two CTAs per SM with a 2-stage x ring when ring + dZ1 planes + prefetched dZ1 partials fit
 // in half an SM's shared memory (measured on the 7B set: TT side kernels 1.21 -> 1.14 ms), else one CTA per
-// SM with the deepest ring that fits. QA_DG1_PER_SM / QA_DG1_NSTG force either (A/B).
+// SM with the deepest ring that fits.
 struct Dg1Shape {
   int per_sm, nstg;
 };
 Dg1Shape dg1_shape(size_t planes, size_t raw_bytes) {
-  static const int f_per_sm = [] {
-    const char* e = getenv("QA_DG1_PER_SM");
-    return e != nullptr ? atoi(e) : 0;
-  }();
-  static const int f_nstg = [] {
-    const char* e = getenv("QA_DG1_NSTG");
-    return e != nullptr ? atoi(e) : 0;
-  }();
   const size_t ring2 = sizeof(__nv_bfloat16) * 2 * DM_ST * DM_LDX;
   Dg1Shape d{1, DM_NSTG};
   if (ring2 + planes + raw_bytes <= 112 * 1024) d = Dg1Shape{2, 2};
-  if (f_per_sm >= 1) d.per_sm = f_per_sm;
-  if (f_nstg >= 2) d.nstg = f_nstg;
   return d;
 }
 
@@ -3871,7 +2566,7 @@ cudaError_t launch_tt_dg1(const void* x, int x_dtype, int64_t T, int64_t K, cons
   count_launches(1);
   const int E = J1 == 1 ? 4 : 8;
   const dim3 grid(static_cast<unsigned>((K + 256 * E - 1) / (256 * E)), static_cast<unsigned>(S));
-  if (x_dtype == QA_BF16 && J1 == 4 && K % 8 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0 && !dg1_mma_disabled()) {
+  if (x_dtype == QA_BF16 && J1 == 4 && K % 8 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0) {
     const int64_t gx = (K + DM_COLS - 1) / DM_COLS;
     const int64_t stages = (T + DM_ST - 1) / DM_ST;
     const size_t raw_bytes = sizeof(float) * 2 * HS * DM_DZT * J1 * R1;
@@ -3901,17 +2596,6 @@ cudaError_t launch_tt_dg1(const void* x, int x_dtype, int64_t T, int64_t K, cons
       }
       return cudaGetLastError();
     }
-  }
-  if (x_dtype == QA_BF16 && J1 == 4 && K % 8 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0) {
-    const size_t smem = sizeof(uint4) * DG_NST * DG_ROWS * 256;
-    if (R1 == 8) {
-      cudaFuncSetAttribute(k_tt_dg1r<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      k_tt_dg1r<8><<<grid, 256, smem, s>>>(static_cast<const __nv_bfloat16*>(x), T, K, dz1, part, S, HS, dz1b, ldb);
-    } else {
-      cudaFuncSetAttribute(k_tt_dg1r<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      k_tt_dg1r<16><<<grid, 256, smem, s>>>(static_cast<const __nv_bfloat16*>(x), T, K, dz1, part, S, HS, dz1b, ldb);
-    }
-    return cudaGetLastError();
   }
 #define QA_DG(TI, JJ, RR) \
   k_tt_dg1<TI, JJ, RR><<<grid, 256, 0, s>>>(static_cast<const TI*>(x), T, K, dz1, part, S, HS, dz1b, ldb)

@@ -84,6 +84,10 @@ def cross_entropy(logits, targets):
     _bf16(logits, "cross_entropy logits")
     rows, vocab = logits.shape
     t = targets.reshape(-1).to(torch.int64).contiguous()
+    if t.numel() != rows:
+        raise IndexError(f"cross_entropy: {t.numel()} targets for {rows} rows of logits")
+    if rows and not bool(((t >= 0) & (t < vocab)).all()):  # the reference indexes logits[row, target]
+        raise IndexError(f"cross_entropy: target outside [0, {vocab})")
     loss_rows = torch.empty(rows, dtype=torch.float32, device=logits.device)
     dl = torch.empty_like(logits)
     _lib.check(_lib.lib().qa_cross_entropy(logits.data_ptr(), t.data_ptr(), rows, vocab, loss_rows.data_ptr(),

@@ -43,6 +43,17 @@ class ModelError(ValueError):
     """Same role as lrlm.transformer.ModelError (transformer.py:61-62)."""
 
 
+# Generation of the trainable parameters' values.  Kernels (the AdamW update, checkpoint loads) write
+# parameters through raw pointers, which torch's _version counters never see; they bump this instead,
+# so a recompute-window state saved before the update is not reused after it.
+_param_generation = [0]
+
+
+def params_changed() -> None:
+    """Invalidate every saved recompute-window state (call after updating parameters in place)."""
+    _param_generation[0] += 1
+
+
 class Param:
     """transformer.py:138-147."""
 
@@ -398,7 +409,8 @@ class TTLinear:
         return out if out else None
 
     def _tag(self, x):
-        return (x.data_ptr(), tuple(x.shape), x._version, tuple(p.data._version for p in self._params_for_tag()))
+        return (x.data_ptr(), tuple(x.shape), x._version, _param_generation[0],
+                tuple(p.data._version for p in self._params_for_tag()))
 
     def _params_for_tag(self):
         return self.cores

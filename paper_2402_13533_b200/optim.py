@@ -15,6 +15,7 @@ import ctypes
 import torch
 
 from . import _lib
+from .linear import params_changed
 from .quant import _stream_ptr
 
 __all__ = ["TrainError", "AdamWConfig", "AdamWState", "adamw_step"]
@@ -119,6 +120,8 @@ def adamw_step(state: AdamWState, params: dict, grads: dict, config: AdamWConfig
                                    state.gflat.data_ptr() + 4 * a, b - a, float(config.lr), float(config.beta1),
                                    float(config.beta2), float(config.eps), float(config.weight_decay),
                                    state.step, sp), "qa_adamw_step")
+    if todo:
+        params_changed()  # the kernels wrote the parameters through raw pointers
     for k in todo:
         i = state.index[k]
         p = params[k]

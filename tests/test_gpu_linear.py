@@ -69,6 +69,7 @@ def test_forward_parity(N, K, T, bits, r, spec):
     e_y2 = O.rel_err(y2, ref["y2"])
     e_y1 = O.rel_err(_np(out["y_f32"]) - y2, ref["y1"])
     e_y = O.rel_err(_np(out["y_bf16"]), ref["y"])
+    print(f"fwd {N}x{K} T={T} b{bits} r{r} {spec}: y1 {e_y1:.2e} y2 {e_y2:.2e} y {e_y:.2e}")
     assert e_y1 <= TOL_F32, e_y1
     assert e_y2 <= TOL_BF16, e_y2
     assert e_y <= TOL_BF16, e_y
@@ -85,10 +86,11 @@ def test_backward_parity(N, K, T, bits, r, spec):
     dys = dy.float().cpu().numpy()
     dx, dcores, dx32 = L.linear_backward(q, (spec, cores), x, dy, debug=True)
     ref = O.qa_linear_backward(xs, dys, oq, cores_np)
-    assert O.rel_err(_np(dx32), ref["dx"]) <= TOL_BF16
-    assert O.rel_err(_np(dx), ref["dx"]) <= TOL_BF16
-    for k, (g, gr) in enumerate(zip(dcores, ref["dcores"])):
-        e = O.rel_err(_np(g), gr)
+    e32, e16 = O.rel_err(_np(dx32), ref["dx"]), O.rel_err(_np(dx), ref["dx"])
+    eg = [O.rel_err(_np(g), gr) for g, gr in zip(dcores, ref["dcores"])]
+    print(f"bwd {N}x{K} T={T} b{bits} r{r} {spec}: dx32 {e32:.2e} dx {e16:.2e} grads " + " ".join(f"{e:.2e}" for e in eg))
+    assert e32 <= TOL_BF16 and e16 <= TOL_BF16
+    for k, e in enumerate(eg):
         assert e <= TOL_BF16, (k, e)
 
 
