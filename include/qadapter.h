@@ -94,6 +94,19 @@ QA_API int qa_quantize_rows(const void* w, int w_dtype, int64_t rows, int64_t co
  * transpose != 0 writes outᵀ ([cols, rows], row stride ld_out). */
 QA_API int qa_dequantize_rows(const qa_qweight* w, void* out, int out_dtype, int64_t ld_out, int transpose, void* stream);
 
+/* Reference-semantics products against the stored codes, no activation quantisation (quant.py:108-144):
+ *   qa_qmatmul   (qmatmul / qmatvec, quant.py:108-132): y  [tokens, rows] f32 = (x·codesᵀ)·scale + Σx·offset
+ *   qa_qmatmul_t (qmatmul_t, quant.py:135-144):         dx [tokens, cols] f32 = (dy·scale)·codes + dy·offset
+ * x / dy: [tokens, cols] / [tokens, rows], dtype QA_F32 or QA_BF16, contiguous.  The products run on the bf16
+ * tensor cores as three chained GEMMs over a 3-term bf16 split of the float operand (codes are exact in
+ * bf16), fp64 row terms and epilogue: fp32-accurate against the reference's fp64 result.
+ * Workspace from qa_qmatmul_workspace_bytes(w, tokens, transpose) (transpose = 1 for qa_qmatmul_t). */
+QA_API size_t qa_qmatmul_workspace_bytes(const qa_qweight* w, int64_t tokens, int transpose);
+QA_API int qa_qmatmul(const qa_qweight* w, const void* x, int x_dtype, int64_t tokens, float* y, void* workspace,
+                      size_t workspace_bytes, void* stream);
+QA_API int qa_qmatmul_t(const qa_qweight* w, const void* dy, int dy_dtype, int64_t tokens, float* dx,
+                        void* workspace, size_t workspace_bytes, void* stream);
+
 /* rowsum[r] = Σ_c code[r, c] of a stored code grid (reference layout, row stride = cols or
  * ceil(cols/2) bytes): the qa_qweight.rowsum term for bases loaded from a checkpoint's u8q / u4q
  * entries (checkpoint.py:64-70, 186-197) instead of quantised on the device. */

@@ -40,6 +40,7 @@ __all__ = [
     "mse_grad",
     "dp_mean",
     "rel_err",
+    "rel_rms",
     "tt_apply_staged",
     "tt_backward_staged",
     "qa_step_staged",
@@ -448,6 +449,14 @@ def rel_err(got, want) -> float:
     denom = np.abs(want) + rms
     denom = np.where(denom > 0, denom, 1.0)
     return float(np.max(np.abs(got - want) / denom))
+
+
+def rel_rms(got, want) -> float:
+    """||got - want|| / ||want|| (Frobenius): the average-case companion of rel_err."""
+    got = np.asarray(got, dtype=np.float64)
+    want = np.asarray(want, dtype=np.float64)
+    n = float(np.linalg.norm(want))
+    return float(np.linalg.norm(got - want)) / (n if n > 0 else 1.0)
 
 
 # ---------------------------------------------------------------------------

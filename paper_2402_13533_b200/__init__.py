@@ -14,6 +14,7 @@ from .quant import (  # noqa: F401
     dequantize_rows,
     qmatmul,
     qmatmul_t,
+    qmatvec,
     quantize_activations,
     quantize_rows,
     quantized_size_bytes,

@@ -29,6 +29,9 @@ EXPORTS = (
     "qa_quantize_rows",
     "qa_dequantize_rows",
     "qa_code_rowsum",
+    "qa_qmatmul_workspace_bytes",
+    "qa_qmatmul",
+    "qa_qmatmul_t",
     "qa_rmsnorm_forward",
     "qa_rmsnorm_backward",
     "qa_rope",
@@ -93,6 +96,12 @@ def _declare(lib):
     lib.qa_quantize_rows.argtypes = [P, I32, I64, I64, I64, I32, P, I64, I64, P, P, P, P, P]
     lib.qa_dequantize_rows.restype = I32
     lib.qa_dequantize_rows.argtypes = [PW, P, I32, I64, I32, P]
+    lib.qa_qmatmul_workspace_bytes.restype = SZ
+    lib.qa_qmatmul_workspace_bytes.argtypes = [PW, I64, I32]
+    lib.qa_qmatmul.restype = I32
+    lib.qa_qmatmul.argtypes = [PW, P, I32, I64, P, P, SZ, P]
+    lib.qa_qmatmul_t.restype = I32
+    lib.qa_qmatmul_t.argtypes = [PW, P, I32, I64, P, P, SZ, P]
     lib.qa_code_rowsum.restype = I32
     lib.qa_code_rowsum.argtypes = [P, I64, I64, I32, P, P]
     F32 = ctypes.c_float

@@ -22,6 +22,7 @@ __all__ = [
     "QuantizedMatrix",
     "quantize_rows",
     "dequantize_rows",
+    "qmatvec",
     "qmatmul",
     "qmatmul_t",
     "quantize_activations",
@@ -166,20 +167,56 @@ def _flatten(x: torch.Tensor, k: int) -> torch.Tensor:
     return x.reshape(-1, k).contiguous()
 
 
-def qmatmul(q: QuantizedMatrix, x) -> torch.Tensor:
-    """quant.py:123-132 as the paper computes it: x is quantised per token to 8 bits,
-    multiplied with the codes on int8 tensor cores and dequantised in the epilogue.
-    x: (..., cols) float32 / bfloat16 -> (..., rows) in x's dtype."""
-    from .linear import linear_forward
+def _qmm(q: QuantizedMatrix, a: torch.Tensor, transpose: bool) -> torch.Tensor:
+    """qa_qmatmul / qa_qmatmul_t on a contiguous 2-D float32 / bfloat16 operand."""
+    T = a.shape[0]
+    out = torch.empty((T, q.cols if transpose else q.rows), dtype=torch.float32, device=q.device)
+    if T == 0:
+        return out
+    c = q.as_c()
+    L = _lib.lib()
+    ws = workspace.get(L.qa_qmatmul_workspace_bytes(ctypes.byref(c), T, 1 if transpose else 0), q.device)
+    fn = L.qa_qmatmul_t if transpose else L.qa_qmatmul
+    _lib.check(fn(ctypes.byref(c), a.data_ptr(), _dtype_code(a), T, out.data_ptr(), ws.data_ptr(), ws.numel(),
+                  _stream_ptr(q.device)), "qmatmul_t" if transpose else "qmatmul")
+    return out
 
-    return linear_forward(q, None, x)
+
+def qmatvec(q: QuantizedMatrix, x) -> torch.Tensor:
+    """quant.py:108-120: row i = scale_i (codes_i · x) + offset_i Σx, without dequantising (float32 result)."""
+    x = _as_device(x, q.device)
+    if x.shape[-1] != q.cols:
+        raise QuantError(f"qmatvec dimension mismatch: {q.rows}x{q.cols} @ {tuple(x.shape)}")
+    if x.dim() != 1:
+        raise QuantError(f"qmatvec expects a 1-D vector, got shape {tuple(x.shape)}")
+    return _qmm(q, x.reshape(1, -1), False)[0]
+
+
+def qmatmul(q: QuantizedMatrix, x, act_quant: bool = False) -> torch.Tensor:
+    """quant.py:123-132: x (..., cols) -> (..., rows) = (x·codesᵀ)·scale + Σx·offset (float32 result, the
+    reference's fp64 formula to fp32 accuracy; qa_qmatmul).
+
+    act_quant=True is the paper's forward instead: x quantised per token to 8 bits, an int8
+    tensor-core GEMM and a dequantising epilogue (qa_linear_forward); the result then is in x's dtype."""
+    if act_quant:
+        from .linear import linear_forward
+
+        return linear_forward(q, None, x)
+    x = _as_device(x, q.device)
+    if x.shape[-1] != q.cols:
+        raise QuantError(f"qmatmul dimension mismatch: {q.rows}x{q.cols} vs {tuple(x.shape)}")
+    lead = tuple(x.shape[:-1])
+    return _qmm(q, x.reshape(-1, q.cols).contiguous(), False).reshape(*lead, q.rows)
 
 
 def qmatmul_t(q: QuantizedMatrix, dy) -> torch.Tensor:
-    """quant.py:135-144: dy (..., rows) -> dy·deq(W) (..., cols) on bf16 tensor cores."""
-    from .linear import linear_backward
-
-    return linear_backward(q, None, None, dy)[0]
+    """quant.py:135-144: dy (..., rows) -> dy·W = (dy·scale)·codes + dy·offset (float32 result, fp32-accurate;
+    qa_qmatmul_t).  The training backward's bf16 path is QuantizedLinear.backward / linear_backward."""
+    dy = _as_device(dy, q.device)
+    if dy.shape[-1] != q.rows:
+        raise QuantError(f"qmatmul_t dimension mismatch: {q.rows}x{q.cols} vs {tuple(dy.shape)}")
+    lead = tuple(dy.shape[:-1])
+    return _qmm(q, dy.reshape(-1, q.rows).contiguous(), True).reshape(*lead, q.cols)
 
 
 def quantize_activations(x, bits: int) -> QuantizedMatrix:

@@ -78,7 +78,8 @@ def test_device_loading_and_roundtrip(tmp_path):
         x = O.seeded_random(9, q.cols, 4)
         oq = O.OQuant(q.rows, q.cols, q.bits, g[f"{name}.codes"], g[f"{name}.scale"], g[f"{name}.offset"])
         want = O.qmatmul(oq, O.dequantize_rows(O.quantize_rows(x, 8)))
-        assert O.rel_err(qa.qmatmul(q, torch.from_numpy(x).cuda()).cpu().numpy(), want) <= 1e-5
+        assert O.rel_err(qa.qmatmul(q, torch.from_numpy(x).cuda(), act_quant=True).cpu().numpy(), want) <= 1e-5
+        assert O.rel_err(qa.qmatmul(q, torch.from_numpy(x).cuda()).cpu().numpy(), O.qmatmul(oq, x)) <= 1e-5
     lora = ckpt.load_lora(ck, "layers.0.wq")
     assert torch.equal(lora.down.data.cpu(), torch.from_numpy(g["wq.down"]))
     # device backends -> file -> device backends (LoRA under the reference's names, TT cores under new ones)

@@ -21,6 +21,15 @@ pytestmark = pytest.mark.gpu
 
 TOL_F32 = 1e-5
 TOL_BF16 = 1e-2
+# adapter term y2 (probe output of the production GEMM): fp32-class — measured 5e-7..4e-5
+TOL_Y2 = 1e-4
+# adapter-core gradients. Generic stage kernels accumulate fp32 products of exact operands: measured
+# <= 1.1e-6.  The fast family (first core input-only, last core output-only, LoRA) runs its dy pass on
+# mma.sync with the intermediates Z2 / dZ2 / dZ1 as bf16 operands: measured 3.4e-3..6.1e-3 max-normalised,
+# so it keeps the bf16 bar plus an average-case bar (Frobenius-relative) that a lost split term would break.
+TOL_GRAD_GENERIC = 1e-4
+TOL_GRAD_FAST = 1e-2
+TOL_GRAD_FAST_RMS = 3e-3
 
 
 def _np(t):
@@ -71,7 +80,7 @@ def test_forward_parity(N, K, T, bits, r, spec):
     e_y = O.rel_err(_np(out["y_bf16"]), ref["y"])
     print(f"fwd {N}x{K} T={T} b{bits} r{r} {spec}: y1 {e_y1:.2e} y2 {e_y2:.2e} y {e_y:.2e}")
     assert e_y1 <= TOL_F32, e_y1
-    assert e_y2 <= TOL_BF16, e_y2
+    assert e_y2 <= TOL_Y2, e_y2
     assert e_y <= TOL_BF16, e_y
     # production path (persistent GEMM, adapter folded in TMEM) against the oracle and the debug path
     y_prod = L.linear_forward(q, (spec, cores), x)
@@ -88,10 +97,16 @@ def test_backward_parity(N, K, T, bits, r, spec):
     ref = O.qa_linear_backward(xs, dys, oq, cores_np)
     e32, e16 = O.rel_err(_np(dx32), ref["dx"]), O.rel_err(_np(dx), ref["dx"])
     eg = [O.rel_err(_np(g), gr) for g, gr in zip(dcores, ref["dcores"])]
-    print(f"bwd {N}x{K} T={T} b{bits} r{r} {spec}: dx32 {e32:.2e} dx {e16:.2e} grads " + " ".join(f"{e:.2e}" for e in eg))
+    eg_rms = [O.rel_rms(_np(g), gr) for g, gr in zip(dcores, ref["dcores"])]
+    print(f"bwd {N}x{K} T={T} b{bits} r{r} {spec}: dx32 {e32:.2e} dx {e16:.2e} grads "
+          + " ".join(f"{e:.2e}/{f:.2e}" for e, f in zip(eg, eg_rms)))
     assert e32 <= TOL_BF16 and e16 <= TOL_BF16
-    for k, e in enumerate(eg):
-        assert e <= TOL_BF16, (k, e)
+    fast = spec.m[0] == 1 and spec.n[-1] == 1
+    for k, (e, f) in enumerate(zip(eg, eg_rms)):
+        if fast:
+            assert e <= TOL_GRAD_FAST and f <= TOL_GRAD_FAST_RMS, (k, e, f)
+        else:
+            assert e <= TOL_GRAD_GENERIC, (k, e)
 
 
 @pytest.mark.parametrize("N,K,T,bits,r,spec", CASES[4:])  # the fast TT family
@@ -123,18 +138,50 @@ def test_recompute_window_handoff_is_bit_identical(N, K, T, bits, r, spec):
 
 
 def test_base_only_paths_match_reference_functions():
-    # qmatmul with per-token act-quant == qmatmul(qw, deq(Q(x))) ; qmatmul_t == reference qmatmul_t
+    # qmatmul(act_quant=True) == qmatmul(qw, deq(Q(x))) (the paper's forward); the plain qmatmul / qmatmul_t /
+    # qmatvec are the reference's own formulas (no activation quantisation) to fp32 accuracy
     W = O.seeded_random(384, 640, 5, std=0.02)
     X = O.seeded_random(200, 640, 6)
     dY = O.seeded_random(200, 384, 7)
     for bits in (4, 8):
         q, oq = qa.quantize_rows(W, bits), O.quantize_rows(W, bits)
-        y = qa.qmatmul(q, torch.from_numpy(X).cuda())
+        y = qa.qmatmul(q, torch.from_numpy(X).cuda(), act_quant=True)
         assert y.dtype == torch.float32
         want = O.qmatmul(oq, O.dequantize_rows(O.quantize_rows(X, 8)))
         assert O.rel_err(_np(y), want) <= TOL_F32
+        y = qa.qmatmul(q, torch.from_numpy(X).cuda())
+        assert O.rel_err(_np(y), O.qmatmul(oq, X)) <= TOL_F32
+        yb = qa.qmatmul(q, torch.from_numpy(X).cuda().to(torch.bfloat16))
+        assert O.rel_err(_np(yb), O.qmatmul(oq, O.to_bf16(X))) <= TOL_F32
+        v = qa.qmatvec(q, torch.from_numpy(X[3]).cuda())
+        assert v.shape == (384,) and O.rel_err(_np(v), O.qmatmul(oq, X[3])) <= TOL_F32
         dx = qa.qmatmul_t(q, torch.from_numpy(dY).cuda())
-        assert O.rel_err(_np(dx), O.qmatmul_t(oq, dY)) <= TOL_BF16
+        assert O.rel_err(_np(dx), O.qmatmul_t(oq, dY)) <= TOL_F32
+        # the training backward's bf16 path (QuantizedLinear.backward): deq(W) rounded to bf16
+        dxb = L.QuantizedLinear("w", q).backward(None, torch.from_numpy(dY).cuda(), {})
+        assert O.rel_err(_np(dxb), O.qmatmul_t(oq, dY)) <= TOL_BF16
+
+
+def test_qmatmul_against_reference_golden(golden_dir):
+    """quant.qmatmul / qmatmul_t outputs written by the reference itself (oracle/gen_golden.py), odd K = 13."""
+    g = np.load(os.path.join(golden_dir, "qmatmul_cases.npz"))
+    for bits in (4, 8):
+        q = qa.quantize_rows(g[f"b{bits}__w"], bits)
+        y = qa.qmatmul(q, torch.from_numpy(g[f"b{bits}__x"]).cuda())
+        assert O.rel_err(_np(y), g[f"b{bits}__qmatmul"]) <= TOL_F32
+        dx = qa.qmatmul_t(q, torch.from_numpy(g[f"b{bits}__dy"]).cuda())
+        assert O.rel_err(_np(dx), g[f"b{bits}__qmatmul_t"]) <= TOL_F32
+    c = np.load(os.path.join(golden_dir, "config1.npz"))
+    W = O.seeded_random(1024, 1024, 1, std=0.02)
+    X = O.seeded_random(512, 1024, 2)
+    qw = qa.quantize_rows(W, 8)
+    xd = qa.dequantize_rows(qa.quantize_rows(X, 8), torch.float32)[:16]
+    assert O.rel_err(_np(qa.qmatmul(qw, xd)), c["y1_first16"]) <= TOL_F32
+    assert O.rel_err(_np(qa.qmatmul_t(qw, torch.from_numpy(c["dy_first16"]).cuda())), c["dx_base_first16"]) <= TOL_F32
+    with pytest.raises(qa.QuantError):
+        qa.qmatmul(qw, torch.zeros(2, 1000, device="cuda"))
+    with pytest.raises(qa.QuantError):
+        qa.qmatmul_t(qw, torch.zeros(2, 1000, device="cuda"))
 
 
 def test_lora_backend_is_drop_in_for_reference_loralinear(golden_dir):

@@ -13,8 +13,9 @@ nothing — and on all tokens for the adapter-core gradients (the staged oracle 
 Tolerances, |got - want| <= tol (|want| + rms(want)) (oracle.rel_err):
   exact : int32 accumulators
   1e-5  : y1 (fp32 epilogue of exact integers)
-  1e-4  : y2 (3-term bf16 split of Z1 and V, fp32 accumulation) and the adapter-core gradients
-  1e-2  : bf16 outputs (y, dx; dx also carries deq(W) rounded to bf16)
+  1e-4  : y2 (3-term bf16 split of Z1 and V, fp32 accumulation)
+  1e-2  : bf16 outputs (y, dx; dx also carries deq(W) rounded to bf16) and the adapter-core gradients (bf16
+          intermediates in the fused dy pass), the latter also <= 3e-3 Frobenius-relative
 """
 
 import numpy as np
@@ -29,7 +30,11 @@ pytestmark = pytest.mark.gpu
 
 TOL_Y1 = 1e-5
 TOL_Y2 = 1e-4
-TOL_GRAD = 1e-2  # calibration run: measured values are printed
+# adapter-core gradients of the fast TT family: the fused dy pass feeds Z2 / dZ2 / dZ1 to mma.sync as bf16
+# operands (measured 4.2e-3..7.2e-3 max-normalised at these shapes), so the bf16 bar applies, plus an
+# average-case (Frobenius-relative) bar that a lost hi/lo split term would break
+TOL_GRAD = 1e-2
+TOL_GRAD_RMS = 3e-3
 TOL_BF16 = 1e-2
 BF16_ULP = 2.0 ** -7  # one bf16 ulp relative to the value (8-bit significand)
 
@@ -122,9 +127,9 @@ def _grads_check(members, cores_list, x, dys, grads):
     for m, cn, dy in zip(members, cores_list, dys):
         _, ref = O.tt_backward_staged(xs, _np(dy), cn)
         for k, p in enumerate(m.cores):
-            e = O.rel_err(_np(grads[p.name]), ref[k])
-            print(f"  {p.name} grad err {e:.2e}")
-            assert e <= TOL_GRAD, (p.name, e)
+            e, f = O.rel_err(_np(grads[p.name]), ref[k]), O.rel_rms(_np(grads[p.name]), ref[k])
+            print(f"  {p.name} grad err {e:.2e} rms {f:.2e}")
+            assert e <= TOL_GRAD and f <= TOL_GRAD_RMS, (p.name, e, f)
 
 
 def _dx_check(members, cores_list, dys, dxs, rows):
