@@ -1,0 +1,144 @@
+"""The drop-in proof: the reference's OWN model code — lrlm's build_model, model_forward /
+model_backward under PER_LAYER, greedy_decode with its KV cache — driving the device backends through
+lifecycle.HostLinear, compared with the all-CPU reference run of the same model.
+
+lrlm is imported from baseline/_ref (the unmodified reference installed there by
+`pip install --no-deps --target baseline/_ref`); the tests are skipped when it is absent.
+
+Expected agreement:
+  act_quant=False (reference arithmetic): loss and logits to ~1e-6; the LoRA factor gradients carry the fast
+    adapter backward's bf16 intermediates (tests/test_gpu_linear.py TOL_GRAD_FAST), so they meet 1e-2;
+  act_quant=True (the paper's per-token activation quantisation): the forward moves by the act-quant
+    error (~0.5% of each base product), measured loss within 2e-3 relative and gradients within 5e-2.
+"""
+
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF = os.path.join(ROOT, "baseline", "_ref")
+if os.path.isdir(REF) and REF not in sys.path:
+    sys.path.append(REF)
+lrlm = pytest.importorskip("lrlm", reason="the reference (lrlm) is not installed in baseline/_ref")
+from lrlm import lowrank, trainer  # noqa: E402
+from lrlm import transformer as tfm  # noqa: E402
+
+import oracle as O  # noqa: E402
+from paper_2402_13533_b200 import lifecycle as LC  # noqa: E402
+from paper_2402_13533_b200.linear import ModelError  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+MATS = ("wq", "wk", "wv", "wo", "wu", "wg", "wd")
+
+
+def _models(act_quant, r=4, seed=3, bits=8):
+    cfg = tfm.ModelConfig(vocab=512, dim=256, heads=4, layers=2, ffn_dim=512, max_seq=64)
+    dense = tfm.build_model(cfg, seed=seed)
+    ref = lowrank.attach_adapters(tfm.quantize_model(dense, bits), r=r, targets=MATS + ("wh",), seed=7)
+    trainer.configure_trainable(ref, "lora_finetune")
+    dev = LC.attach_adapters(LC.quantize_model(dense, bits, act_quant=act_quant), r=r, targets=MATS + ("wh",), seed=7,
+                             act_quant=act_quant)
+    LC.configure_trainable(dev, "lora_finetune")
+    # the same codes and the same initial factors as the reference's own quantize_model / attach_adapters
+    for (name, a), (_, b) in zip(sorted(ref.named_parameters().items()), sorted(dev.named_parameters().items())):
+        assert a.name == b.name and a.trainable == b.trainable
+        assert np.array_equal(a.data, b.data), name
+    rq, dq = ref.layers[1].wu.base.q, dev.layers[1].wu.q
+    assert rq.codes.tobytes() == dq.codes.cpu().numpy().tobytes()
+    # non-zero `up` factors so every factor receives a gradient
+    for i, name in enumerate(sorted(ref.trainable_parameters())):
+        if name.endswith(".up"):
+            v = O.seeded_random(*ref.named_parameters()[name].data.shape, 900 + i, std=0.02)
+            ref.named_parameters()[name].data[...] = v
+            dev.named_parameters()[name].data[...] = v
+    return cfg, ref, dev
+
+
+def _run(model, tokens, targets):
+    logits, tape = tfm.model_forward(model, tokens, tfm.PER_LAYER)
+    loss = tfm.cross_entropy_loss(logits, targets)
+    grads = tfm.model_backward(model, tape, tfm.cross_entropy_grad(logits, targets))
+    return logits, loss, grads
+
+
+@pytest.mark.parametrize("act_quant", [False, True])
+def test_reference_model_code_drives_device_backends(act_quant):
+    cfg, ref, dev = _models(act_quant)
+    rng = np.random.default_rng(5)
+    tokens = rng.integers(0, cfg.vocab, size=(2, 48))
+    targets = rng.integers(0, cfg.vocab, size=(2, 48))
+    l_ref, loss_ref, g_ref = _run(ref, tokens, targets)
+    l_dev, loss_dev, g_dev = _run(dev, tokens, targets)
+    assert sorted(g_ref) == sorted(g_dev) == sorted(ref.trainable_parameters())
+    e_logits = O.rel_err(l_dev, l_ref)
+    e_loss = abs(loss_dev - loss_ref) / abs(loss_ref)
+    e_g = {k: O.rel_err(g_dev[k], g_ref[k]) for k in g_ref}
+    worst = max(e_g, key=e_g.get)
+    print(f"act_quant={act_quant}: logits {e_logits:.2e} loss {e_loss:.2e} worst grad {worst} {e_g[worst]:.2e} "
+          f"median {np.median(list(e_g.values())):.2e}")
+    if act_quant:
+        assert e_loss <= 2e-3 and e_g[worst] <= 5e-2
+    else:
+        assert e_logits <= 1e-4 and e_loss <= 1e-5 and e_g[worst] <= 1e-2
+    # the reference's AdamW updates the host factors in place; the next forward uploads them
+    cfg_t = trainer.TrainConfig(lr=1e-2)
+    trainer.adamw_step(trainer.AdamWState(dev.trainable_parameters()), dev.trainable_parameters(), g_dev, cfg_t)
+    trainer.adamw_step(trainer.AdamWState(ref.trainable_parameters()), ref.trainable_parameters(), g_ref, cfg_t)
+    l2_ref, _ = tfm.model_forward(ref, tokens)
+    l2_dev, _ = tfm.model_forward(dev, tokens)
+    assert O.rel_err(l2_dev, l2_ref) <= (1e-2 if act_quant else 1e-3)
+
+
+def test_reference_greedy_decode_with_kv_cache_on_device_backends():
+    """lrlm's own greedy_decode (KvCache + kv_decode_step, transformer.py:1015-1111) over the device backends:
+    1-token forwards take the act-quant prologue + matrix-vector pass; with the reference arithmetic the
+    generated ids equal the CPU run's."""
+    cfg, ref, dev = _models(False)
+    prompt = [5, 77, 301, 12]
+    want, passes = tfm.greedy_decode(ref, prompt, max_new=6)
+    got, passes_dev = tfm.greedy_decode(dev, prompt, max_new=6)
+    assert got == want and passes_dev == passes
+    logits_ref, cache = tfm.kv_decode_step(ref, tfm.KvCache(ref), 5)
+    logits_dev, _ = tfm.kv_decode_step(dev, tfm.KvCache(dev), 5)
+    assert O.rel_err(logits_dev, logits_ref) <= 1e-4
+
+
+def test_lifecycle_rejections_and_merge():
+    cfg = tfm.ModelConfig(vocab=256, dim=128, heads=2, layers=1, ffn_dim=256, max_seq=32)
+    dense = tfm.build_model(cfg, seed=1)
+    with pytest.raises(ModelError, match="embedding"):
+        LC.quantize_model(dense, 8, targets=("we",))
+    with pytest.raises(ModelError, match="unknown matrix"):
+        LC.quantize_model(dense, 8, targets=("wz",))
+    q = LC.quantize_model(dense, 4)
+    with pytest.raises(ModelError, match="only dense"):
+        LC.quantize_model(q, 8)
+    with pytest.raises(ModelError, match="embedding"):
+        LC.attach_adapters(q, r=4, targets=("we",))
+    with pytest.raises(ModelError, match="rank"):
+        LC.attach_adapters(q, r=128, targets=("wq",))
+    with pytest.raises(ModelError, match="quantized base"):
+        LC.attach_adapters(dense, r=4, targets=("wq",))
+    with pytest.raises(ModelError, match="requires adapters"):
+        LC.configure_trainable(q, "lora_finetune")
+    m = LC.attach_adapters(q, r=4, targets=("wq", "wv", "wh"), seed=2, kind="tt",
+                           spec_for=lambda n, k, r: LC.TTSpec.for_shape(n, k, r) if n % 256 == 0 else
+                           LC.TTSpec((1, n // 64, 64), (k // 4, 4, 1), (1, r, r, 1)))
+    LC.configure_trainable(m, "lora_finetune")
+    assert sorted(m.trainable_parameters()) == sorted(
+        [f"layers.0.{w}.core{k}" for w in ("wq", "wv") for k in range(3)] + [f"head.core{k}" for k in range(3)])
+    x = np.random.default_rng(0).standard_normal((3, 128)).astype(np.float32)
+    m.layers[0].wq.params()[2].data[...] = O.seeded_random(*m.layers[0].wq.params()[2].data.shape[:2], 4,
+                                                           std=0.02).reshape(m.layers[0].wq.params()[2].data.shape)
+    y_before = m.layers[0].wq.forward(x)
+    merged = LC.merge_model(m)
+    y_after = merged.layers[0].wq.forward(x)
+    assert O.rel_err(y_after, y_before) <= 2e-2  # dense bf16 forward on W' vs act-quant forward
+    with pytest.raises(ModelError, match="already merged"):
+        LC.merge_model(merged)
+    with pytest.raises(ModelError, match="inference-only"):
+        merged.layers[0].wq.backward(x, np.ones((3, 128), np.float32), {})
