@@ -37,18 +37,30 @@ LINEARS_7B = [  # (name, fan_out, fan_in, input) in forward order (transformer.p
     ("wo", 4096, 4096, "ctx"), ("wu", 11008, 4096, "ffn"), ("wg", 11008, 4096, "ffn"),
     ("wd", 4096, 11008, "act"),
 ]
+LINEARS_70B = [  # config 5: hidden 8192, FFN 28672, GQA 8 KV heads of 128 (k / v project to 1024)
+    ("wq", 8192, 8192, "attn"), ("wk", 1024, 8192, "attn"), ("wv", 1024, 8192, "attn"),
+    ("wo", 8192, 8192, "ctx"), ("wu", 28672, 8192, "ffn"), ("wg", 28672, 8192, "ffn"),
+    ("wd", 8192, 28672, "act"),
+]
 BACKWARD_ORDER = ["wd", "wu", "wg", "wo", "wq", "wk", "wv"]  # transformer.py:919-944
 # members that read the same input run as one shared-input group (qa_group_forward / _backward):
 # wq / wk / wv on norm1 and wu / wg on norm2 (transformer.py:862-874)
 GROUPS_FWD = [("wq", "wk", "wv"), ("wo",), ("wu", "wg"), ("wd",)]
 GROUPS_BWD = [("wd",), ("wu", "wg"), ("wo",), ("wq", "wk", "wv")]
 INPUT_DIMS = {"attn": 4096, "ctx": 4096, "ffn": 4096, "act": 11008}
+INPUT_DIMS_70B = {"attn": 8192, "ctx": 8192, "ffn": 8192, "act": 28672}
 
 CONFIGS = {
     "2": {"bits": 8, "rank": 8, "batch": 8, "seq": 2048},
     "3": {"bits": 4, "rank": 16, "batch": 16, "seq": 4096},  # global tokens; sharded over ranks
     "4": {"bits": 8, "rank": 8, "batch": 4, "seq": 2048},  # decoder stack: 4 sequences per GPU (32 over 8 GPUs)
+    "5": {"bits": 4, "rank": 8, "batch": 8, "seq": 4096},  # 70B linear set, [8, 4096] tokens per GPU
 }
+
+
+def linear_set(cfg_name):
+    """(linears, input dims) of a config: the 7B set for configs 1-4, the 70B set for config 5."""
+    return (LINEARS_70B, INPUT_DIMS_70B) if cfg_name == "5" else (LINEARS_7B, INPUT_DIMS)
 DECODER_LAYERS = 32
 
 
@@ -75,8 +87,10 @@ def workload_config(cfg_name, world):
     else:
         tokens = c["batch"] * c["seq"]
         scaling = "weak"
+    lset = ("llama2-70b linear set q/o 8192x8192, k/v 1024x8192 (GQA), gate/up 28672x8192, down 8192x28672"
+            if cfg_name == "5" else "llama2-7b linear set q/k/v/o 4096x4096, gate/up 11008x4096, down 4096x11008")
     desc = {
-        "workload": (f"llama2-7b linear set q/k/v/o 4096x4096, gate/up 11008x4096, down 4096x11008; int{c['bits']} "
+        "workload": (f"{lset}; int{c['bits']} "
                      f"per-row weights; TT adapter r={c['rank']} m=(1,N/256,256) n=(K/4,4,1); "
                      f"{tokens} bf16 tokens/GPU; fwd + bwd-with-recompute (+ NCCL grad all-reduce); q/k/v and "
                      f"up/gate as shared-input groups (one x pass per direction, transformer.py:862-874)"),
@@ -84,7 +98,8 @@ def workload_config(cfg_name, world):
         "tokens_per_gpu": tokens,
         "bits": c["bits"],
         "rank": c["rank"],
-        "l2": "inputs larger than L2 (>= 763 MB of layer inputs + 1.4 GB of upstream grads per step)",
+        "l2": ("inputs larger than L2 (>= 763 MB of layer inputs + 1.4 GB of upstream grads per step)"
+               if cfg_name != "5" else "inputs larger than L2 (3.4 GB of layer inputs + 4.8 GB of upstream grads)"),
         "parallelism": f"dp{world}",
     }
     return c, tokens, scaling, desc
