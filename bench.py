@@ -154,13 +154,14 @@ def measured_peaks():
 # ----------------------------------------------------------------------------- CPU baseline / reference arm
 
 
-def cpu_reference_step_fn(cfg, sample_tokens, seed=0):
+def cpu_reference_step_fn(cfg, sample_tokens, seed=0, linset=None):
     """The oracle's staged numpy port of the same 7-linear step on `sample_tokens` tokens
     (TEST/BASELINE INFRASTRUCTURE: used only for the CPU baseline and --impl reference)."""
     import numpy as np
 
     import oracle as O
 
+    LINEARS_7B, INPUT_DIMS = linset or (globals()["LINEARS_7B"], globals()["INPUT_DIMS"])
     rng = np.random.default_rng(seed)
     mats = {}
     for name, n, k, _ in LINEARS_7B:
@@ -181,6 +182,64 @@ def cpu_reference_step_fn(cfg, sample_tokens, seed=0):
     return step
 
 
+def lrlm_available() -> bool:
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(ref) and ref not in sys.path:
+        sys.path.append(ref)
+    try:
+        import lrlm  # noqa: F401  (the unmodified reference, pip-installed into baseline/_ref)
+    except ImportError:
+        return False
+    return True
+
+
+def lrlm_reference_step_fn(cfg_name, sample_tokens, seed=0):
+    """The reference's OWN CPU code for the path (lrlm, baseline/_ref), through its public API: per linear,
+    quant.quantize_rows on the [T, K] activations (the per-token act-quant the paper adds, quant.py:73-99), then
+    transformer.LoraLinear over a QuantizedLinear base (its adapter; transformer.py:276-327) forward on the
+    dequantised activations and backward with recompute (qmatmul / qmatmul_t, quant.py:123-144).  Weights are
+    quantised outside the timed region."""
+    import numpy as np
+    from lrlm import linalg, quant
+    from lrlm import transformer as tfm
+
+    cfg = CONFIGS[cfg_name]
+    linears, dims = linear_set(cfg_name)
+    r = cfg["rank"]
+    mats = {}
+    for i, (name, n, k, _) in enumerate(linears):
+        q = quant.quantize_rows(linalg.seeded_random(n, k, seed + 10 * i + 1, std=0.02), cfg["bits"])
+        down = linalg.seeded_random(r, k, seed + 10 * i + 2, std=0.02)
+        up = linalg.seeded_random(n, r, seed + 10 * i + 3, std=0.02)
+        mats[name] = tfm.LoraLinear(name, tfm.QuantizedLinear(name + ".base", q), down, up)
+    rng = np.random.default_rng(seed)
+    xs = {kind: rng.standard_normal((sample_tokens, d), dtype=np.float32) for kind, d in dims.items()}
+    dys = {name: rng.standard_normal((sample_tokens, n), dtype=np.float32) for name, n, _, _ in linears}
+    inputs = {name: kind for name, _, _, kind in linears}
+
+    def step():
+        grads = {}
+        for name, _, _, _ in linears:
+            x = xs[inputs[name]]
+            xq = quant.dequantize_rows(quant.quantize_rows(x, 8))
+            mats[name].forward(xq)
+            mats[name].backward(xq, dys[name], grads)
+
+    return step
+
+
+def reference_cpu_step(cfg_name, sample_tokens):
+    """(step, kind, description) of the CPU reference: lrlm itself when baseline/_ref holds it, else the
+    oracle's staged numpy port of the same step."""
+    if lrlm_available():
+        return (lrlm_reference_step_fn(cfg_name, sample_tokens), "reference",
+                "lrlm (baseline/_ref, unmodified): quant.quantize_rows per-token act-quant + LoraLinear(QuantizedLinear) "
+                f"fwd + bwd at rank {CONFIGS[cfg_name]['rank']} on each linear")
+    return (cpu_reference_step_fn(CONFIGS[cfg_name], sample_tokens, linset=linear_set(cfg_name)), "port",
+            "oracle staged numpy fp64 port of the reference path (quant.py quantize_rows/qmatmul/qmatmul_t + TT "
+            "adapter)")
+
+
 def cpu_threads():
     try:
         import threadpoolctl
@@ -194,8 +253,8 @@ def cpu_threads():
     return os.cpu_count() or 1, "numpy BLAS"
 
 
-def run_cpu_baseline(cfg, sample_tokens=256, repeats=3):
-    step = cpu_reference_step_fn(cfg, sample_tokens)
+def run_cpu_baseline(cfg_name, sample_tokens=256, repeats=3):
+    step, kind, what = reference_cpu_step(cfg_name, sample_tokens)
     step()  # warm (BLAS thread start-up, page faults)
     times = []
     for _ in range(repeats):
@@ -208,10 +267,9 @@ def run_cpu_baseline(cfg, sample_tokens=256, repeats=3):
         "value": sample_tokens / sec,
         "unit": UNIT,
         "cores": threads,
-        "kind": "port",
-        "sample": (f"{sample_tokens} tokens through all 7 linears (fwd + bwd) with the oracle's staged numpy fp64 "
-                   f"port of the reference path (quant.py quantize_rows/qmatmul/qmatmul_t + TT adapter), median "
-                   f"of {repeats}, {blas}, {threads} threads; weights quantised outside the timed region"),
+        "kind": kind,
+        "sample": (f"{sample_tokens} tokens through all 7 linears (fwd + bwd): {what}; median of {repeats}, {blas}, "
+                   f"{threads} threads; weights quantised outside the timed region"),
     }
 
 
@@ -223,8 +281,8 @@ def run_reference_arm(args):
     if args.config == "4":
         return run_reference_arm_decoder(args)
     cfg, tokens, scaling, desc = workload_config(args.config, world)
-    sample = 256
-    step = cpu_reference_step_fn(cfg, sample)
+    sample = 64 if args.config == "5" else 1024
+    step, kind, what = reference_cpu_step(args.config, sample)
     for _ in range(args.warmup):
         step()
     t0 = time.perf_counter()
@@ -237,13 +295,13 @@ def run_reference_arm(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
         "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": desc,
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{sample} tokens/step through the 7 linears, oracle staged numpy fp64 port "
-                                   f"({blas}); the reference lrlm itself cannot travel to the GPU box"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": f"{sample} tokens/step through the 7 linears: {what} ({blas})"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
 
 def decoder_cpu_rate(sample=64, repeats=2):
     """CPU stand-in for config 4 (a 32-layer decoder is hours of numpy per step): the oracle's staged fp64 port
@@ -442,6 +500,43 @@ def measure_merge(dev, sptr, hbm_gbs, iters=5):
 
 
 
+def measure_weight_quantize(dev, sptr, hbm_gbs, linears, bits, iters=5):
+    """qa_quantize_rows (quant.py:73-99, north-star step 1) over the config's linear set from f32 weights,
+    outside the timed region: algorithmic bytes = f32 in + codes out + scale / offset / Σcodes."""
+    import torch
+
+    from paper_2402_13533_b200 import _lib
+
+    lib = _lib.lib()
+    g = torch.Generator(device=dev).manual_seed(11)
+    tot_ms, tot_bytes = 0.0, 0.0
+    for name, n, k, _ in linears:
+        w = torch.randn((n, k), generator=g, device=dev) * 0.02
+        ld = k if bits == 8 else (k + 1) // 2
+        codes = torch.empty((n, ld), dtype=torch.uint8, device=dev)
+        sc, of = torch.empty(n, device=dev), torch.empty(n, device=dev)
+        rs = torch.empty(n, dtype=torch.int32, device=dev)
+
+        def run():
+            _lib.check(lib.qa_quantize_rows(w.data_ptr(), _lib.QA_F32, n, k, k, bits, codes.data_ptr(), ld, k,
+                                            sc.data_ptr(), of.data_ptr(), rs.data_ptr(), None, sptr), "quantize")
+
+        run()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(iters):
+            run()
+        e1.record()
+        torch.cuda.synchronize(dev)
+        tot_ms += e0.elapsed_time(e1) / iters
+        tot_bytes += n * k * 4 + n * ld + 12 * n
+        del w, codes
+    gbs = tot_bytes / tot_ms / 1e6
+    return {"set": f"the config's {len(linears)} linears from f32, int{bits}", "ms": tot_ms, "bytes": tot_bytes,
+            "achieved_gbs": gbs, "frac_of_hbm": gbs / hbm_gbs, "kernels": "k_quantize_rows"}
+
+
 def roofline_from_classes(per_class, ms_total, steps, clocks, with_traffic=True):
     """Roofline of the dominant kernel class and every class's share / fraction of its own roofline, from the
     library's live per-launch CUDA-event durations of the timed region (qa_timing_*)."""
@@ -554,8 +649,8 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_2402_13533_b200 import _lib
-    from paper_2402_13533_b200.linear import TTSpec
+    from paper_2402_13533_b200 import _lib, dp
+    from paper_2402_13533_b200.linear import QuantizedLinear, TTLinear, TTSpec
     from paper_2402_13533_b200.quant import quantize_rows
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -568,16 +663,20 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     cfg, T, scaling, desc = workload_config(args.config, world)
+    LINEARS, IN_DIMS = linear_set(args.config)
     lib = _lib.lib()
     stream = torch.cuda.current_stream(dev)
     sptr = stream.cuda_stream
+    if world > 1 and rank == 0:
+        print(f"[bench] {world} ranks, NCCL {'.'.join(map(str, torch.cuda.nccl.version()))}, backend "
+              f"{dist.get_backend()}", file=sys.stderr, flush=True)
 
     # --- frozen quantised base + TT adapters (identical on every rank: same seed)
     gen = torch.Generator(device=dev).manual_seed(1234)
     mats = {}
     ws_bytes = 0
     grad_numel = 0
-    for name, n, k, kind in LINEARS_7B:
+    for name, n, k, kind in LINEARS:
         w = torch.randn((n, k), generator=gen, device=dev, dtype=torch.float32) * 0.02
         q = quantize_rows(w, cfg["bits"])
         del w
@@ -603,7 +702,7 @@ def main():
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     flat_grad = torch.zeros(grad_numel, dtype=torch.float32, device=dev)
     off = 0
-    for name, n, k, kind in LINEARS_7B:
+    for name, n, k, kind in LINEARS:
         m = mats[name]
         views = []
         for i in range(m["spec"].d):
@@ -612,17 +711,23 @@ def main():
             off += numel
         m["gptr"] = (ctypes.c_void_p * _lib.QA_TT_MAX_D)(*[v.data_ptr() for v in views])
 
+    # every rank must hold the same frozen codes and adapter cores before the step (the state_signature check
+    # of distsim.federated_round, distsim.py:293-296)
+    if world > 1:
+        dp.check_replicas([TTLinear(nm, QuantizedLinear(nm + ".base", mats[nm]["q"]), mats[nm]["spec"],
+                                    mats[nm]["cores"]) for nm, _, _, _ in LINEARS])
+
     # --- per-rank synthetic activations / upstream grads (rank-dependent seed: different token shards)
     dgen = torch.Generator(device=dev).manual_seed(99 + rank)
 
     def make_inputs():
-        xs = {kd: torch.randn((T, d), generator=dgen, device=dev).to(torch.bfloat16) for kd, d in INPUT_DIMS.items()}
-        dys = {nm: torch.randn((T, n), generator=dgen, device=dev).to(torch.bfloat16) for nm, n, _, _ in LINEARS_7B}
+        xs = {kd: torch.randn((T, d), generator=dgen, device=dev).to(torch.bfloat16) for kd, d in IN_DIMS.items()}
+        dys = {nm: torch.randn((T, n), generator=dgen, device=dev).to(torch.bfloat16) for nm, n, _, _ in LINEARS}
         return xs, dys
 
     xs, dys = make_inputs()
-    ys = {nm: torch.empty((T, n), dtype=torch.bfloat16, device=dev) for nm, n, _, _ in LINEARS_7B}
-    dxs = {nm: torch.empty((T, k), dtype=torch.bfloat16, device=dev) for nm, _, k, _ in LINEARS_7B}
+    ys = {nm: torch.empty((T, n), dtype=torch.bfloat16, device=dev) for nm, n, _, _ in LINEARS}
+    dxs = {nm: torch.empty((T, k), dtype=torch.bfloat16, device=dev) for nm, _, k, _ in LINEARS}
     BF16 = _lib.QA_BF16
 
     for gnames, gd in groups.items():  # saved-state, gradient and dy/dx pointer arrays
@@ -638,7 +743,7 @@ def main():
     def step(xs, dys):
         if not args.no_group:
             return step_grouped(xs, dys)
-        for name, _, _, kind in LINEARS_7B:
+        for name, _, _, kind in LINEARS:
             m = mats[name]
             st = lib.qa_linear_forward_save(ctypes.byref(m["wc"]), ctypes.byref(m["ttc"]), xs[kind].data_ptr(), BF16,
                                             T, ys[name].data_ptr(), m["saved"].data_ptr(), m["nsaved"],
@@ -655,8 +760,7 @@ def main():
             if st:
                 _lib.check(st, f"backward {name}")
         if world > 1:
-            dist.all_reduce(flat_grad, op=dist.ReduceOp.SUM)
-            flat_grad.div_(world)
+            dp.allreduce_mean_(flat_grad)
 
     def step_grouped(xs, dys):
         for gnames in GROUPS_FWD:
@@ -688,8 +792,7 @@ def main():
             if st:
                 _lib.check(st, f"backward {gnames}")
         if world > 1:
-            dist.all_reduce(flat_grad, op=dist.ReduceOp.SUM)
-            flat_grad.div_(world)
+            dp.allreduce_mean_(flat_grad)
 
     def barrier():
         if world > 1:
@@ -782,11 +885,11 @@ def main():
     # decode-size forwards (KV-cached decoding, transformer.py:1043-1080): 1 and 8 tokens through the 7
     # linears; HBM-bound on the weight codes (gemv.cu)
     decode = None
-    if rank == 0 and not args.no_merge:
+    if rank == 0 and not args.no_merge and args.config != "5":
         decode = {}
         for td in (1, 8):
-            xd = {kd: torch.randn((td, d), generator=dgen, device=dev).to(torch.bfloat16) for kd, d in INPUT_DIMS.items()}
-            yd = {nm: torch.empty((td, n), dtype=torch.bfloat16, device=dev) for nm, n, _, _ in LINEARS_7B}
+            xd = {kd: torch.randn((td, d), generator=dgen, device=dev).to(torch.bfloat16) for kd, d in IN_DIMS.items()}
+            yd = {nm: torch.empty((td, n), dtype=torch.bfloat16, device=dev) for nm, n, _, _ in LINEARS}
 
             dgroups = {}
             for gnames in GROUPS_FWD:
@@ -818,7 +921,7 @@ def main():
             d1.record(stream)
             torch.cuda.synchronize(dev)
             ms = d0.elapsed_time(d1) / 50
-            wbytes = sum(mats[nm]["q"].codes.numel() + 8 * n for nm, n, _, _ in LINEARS_7B)
+            wbytes = sum(mats[nm]["q"].codes.numel() + 8 * n for nm, n, _, _ in LINEARS)
             decode[f"tokens_{td}"] = {"ms_per_step": ms, "tokens_per_s": td / (ms / 1e3),
                                       "weight_gbs": wbytes / ms / 1e6, "frac_of_hbm": wbytes / ms / 1e6 / peaks["hbm_gbs"]}
         decode["note"] = ("forward of the 7 linears for 1 / 8 tokens (int8 codes + TT adapter; q/k/v and up/gate as "
@@ -831,20 +934,25 @@ def main():
     if rank == 0 and not args.no_merge:
         merge = measure_merge(dev, sptr, peaks["hbm_gbs"])
 
+    wquant = None
+    if rank == 0 and not args.no_merge:
+        wquant = measure_weight_quantize(dev, sptr, peaks["hbm_gbs"], LINEARS, cfg["bits"])
+
     decoder = None
-    if rank == 0 and world == 1 and not args.no_decoder:
+    if rank == 0 and world == 1 and not args.no_decoder and args.config != "5":
         decoder = measure_decoder(dev)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = run_cpu_baseline(cfg)
+        cpu = run_cpu_baseline(args.config, 64 if args.config == "5" else 1024)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "int8 (u8xu8->s32) GEMM + bf16", "data": "synthetic",
-            "config": desc, "roofline": roofline, "kernels": kernels, "decode": decode, "merge": merge, "decoder": decoder,
+            "config": desc, "roofline": roofline, "kernels": kernels, "decode": decode, "merge": merge,
+            "weight_quantize": wquant, "decoder": decoder,
             "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches * args.steps), "gpu_launches_per_step": int(launches), "clocks": clocks,
         }

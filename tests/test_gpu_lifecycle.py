@@ -91,7 +91,7 @@ def test_reference_model_code_drives_device_backends(act_quant):
     trainer.adamw_step(trainer.AdamWState(ref.trainable_parameters()), ref.trainable_parameters(), g_ref, cfg_t)
     l2_ref, _ = tfm.model_forward(ref, tokens)
     l2_dev, _ = tfm.model_forward(dev, tokens)
-    assert O.rel_err(l2_dev, l2_ref) <= (0.15 if act_quant else 1e-4)
+    assert O.rel_err(l2_dev, l2_ref) <= (0.15 if act_quant else 1e-3)
 
 
 def test_reference_greedy_decode_with_kv_cache_on_device_backends():
