@@ -1119,6 +1119,9 @@ int qa_merge(const qa_qweight* w, const qa_tt* tt, void* out, int out_dtype, voi
     return QA_ERR_WORKSPACE;
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (merge_fast_ok(dd, w->codes, out))  // one pass: the prefix contraction formed in registers
+    return cuda_status(launch_merge_fast(dd, tt->cores, w->codes, w->bits, w->scale, w->offset, out, out_dtype, s),
+                       "merge");
   float* L = static_cast<float*>(workspace);
   QA_TRY_CUDA(launch_tt_prefix_full(dd, tt->cores, L, s), "tt prefix");
   return cuda_status(launch_tt_last_full(dd, L, tt->cores[dd.d - 1], w->codes, w->bits, w->scale, w->offset, out,
@@ -1138,6 +1141,9 @@ int qa_tt_materialize(const qa_tt* tt, float* out, void* workspace, size_t works
     return QA_ERR_WORKSPACE;
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (merge_fast_ok(dd, nullptr, out))
+    return cuda_status(launch_merge_fast(dd, tt->cores, nullptr, 8, nullptr, nullptr, out, QA_F32, s),
+                       "tt materialize");
   float* L = static_cast<float*>(workspace);
   QA_TRY_CUDA(launch_tt_prefix_full(dd, tt->cores, L, s), "tt prefix");
   return cuda_status(launch_tt_last_full(dd, L, tt->cores[dd.d - 1], nullptr, 8, nullptr, nullptr, out, QA_F32, s),

@@ -61,6 +61,11 @@ cudaError_t launch_tt_last_full(const TTDims& dd, const float* L, const float* G
                                 int bits, const float* scale, const float* offset, void* out, int out_dtype,
                                 cudaStream_t s);
 
+// Fused merge / materialise for the fast TT family (no prefix pass): out = W_t (+ deq(codes) when codes != NULL)
+bool merge_fast_ok(const TTDims& dd, const void* codes, const void* out);
+cudaError_t launch_merge_fast(const TTDims& dd, const float* const* cores, const uint8_t* codes, int bits,
+                              const float* scale, const float* offset, void* out, int out_dtype, cudaStream_t s);
+
 // out[i] (+)= Σ_p partial[p][i] in fixed order (deterministic reduction of per-CTA partials)
 cudaError_t launch_sum_partials(const float* partial, int nparts, int64_t numel, float* out, bool accumulate,
                                 cudaStream_t s);

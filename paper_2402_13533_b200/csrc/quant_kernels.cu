@@ -106,6 +106,113 @@ __global__ void __launch_bounds__(256) k_quantize_rows(const InT* __restrict__ w
   }
 }
 
+// One CTA per row with the whole row in registers (production weight quantiser for rows of 8-element
+// aligned chunks, cols <= 256 * 8 * CH): every thread issues its CH chunk loads (16 or 32 bytes each) at once,
+// so a CTA keeps its row's bytes in flight; min / max meet through warp shuffles and shared memory; the
+// codes come from the registers — each input byte crosses HBM exactly once.  Same code rule as
+// k_quantize_rows (code_of / codes8: fp32 with an fp64 replay inside the tie band).
+constexpr int QR_THREADS = 256;
+
+template <typename InT, int BITS, int CH>
+__global__ void __launch_bounds__(QR_THREADS) k_quantize_rows_reg(const InT* __restrict__ w, int64_t cols,
+                                                                   int64_t ldw, uint8_t* __restrict__ codes,
+                                                                   int64_t ldc, int64_t pad_cols,
+                                                                   float* __restrict__ scale,
+                                                                   float* __restrict__ offset,
+                                                                   int32_t* __restrict__ rowsum,
+                                                                   int32_t* __restrict__ flag) {
+  __shared__ float s_lo[QR_THREADS / 32], s_hi[QR_THREADS / 32];
+  __shared__ int s_bad[QR_THREADS / 32], s_sum[QR_THREADS / 32];
+  const int64_t row = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const InT* src = w + row * ldw;
+  const int nchunk = static_cast<int>(cols / 8);
+  float v[CH][8];
+  float lo = INFINITY, hi = -INFINITY;
+  bool bad = false;
+#pragma unroll
+  for (int j = 0; j < CH; ++j) {
+    const int c = tid + j * QR_THREADS;
+    if (c < nchunk) {
+      load8<InT>(src + static_cast<int64_t>(c) * 8, v[j]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[j][i] = 0.f;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < CH; ++j) {
+    if (tid + j * QR_THREADS < nchunk) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        lo = fminf(lo, v[j][i]);
+        hi = fmaxf(hi, v[j][i]);
+        bad |= !isfinite(v[j][i]);
+      }
+    }
+  }
+  lo = warp_min(lo);
+  hi = warp_max(hi);
+  const int wbad = __any_sync(0xffffffffu, bad);
+  if (lane == 0) {
+    s_lo[wid] = lo;
+    s_hi[wid] = hi;
+    s_bad[wid] = wbad;
+  }
+  __syncthreads();
+  lo = s_lo[0];
+  hi = s_hi[0];
+  int any_bad = s_bad[0];
+#pragma unroll
+  for (int i = 1; i < QR_THREADS / 32; ++i) {
+    lo = fminf(lo, s_lo[i]);
+    hi = fmaxf(hi, s_hi[i]);
+    any_bad |= s_bad[i];
+  }
+  if (any_bad && tid == 0 && flag != nullptr) atomicOr(flag, 1);
+  constexpr int kTop = (1 << BITS) - 1;
+  const double lo64 = static_cast<double>(lo);
+  const double step64 = __ddiv_rn(__dsub_rn(static_cast<double>(hi), lo64), static_cast<double>(kTop));
+  const bool flat = !(step64 > 0.0) || any_bad;
+  const float inv = flat ? 0.0f : static_cast<float>(1.0 / step64);
+  uint8_t* dst = codes + row * ldc;
+  int sum = 0;
+#pragma unroll
+  for (int j = 0; j < CH; ++j) {
+    const int c = tid + j * QR_THREADS;
+    if (c >= nchunk) continue;
+    if (BITS == 8) {
+      uint2 packed = make_uint2(0u, 0u);
+      if (!flat) codes8(v[j], lo, inv, lo64, step64, packed.x, packed.y, sum);
+      *reinterpret_cast<uint2*>(dst + static_cast<int64_t>(c) * 8) = packed;
+    } else {
+      uint32_t packed = 0u;
+      if (!flat) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const uint32_t q = code_of<4>(v[j][i], lo, inv, lo64, step64);
+          sum += static_cast<int>(q);
+          packed |= q << (4 * i);
+        }
+      }
+      *reinterpret_cast<uint32_t*>(dst + static_cast<int64_t>(c) * 4) = packed;
+    }
+  }
+  if (BITS == 8)
+    for (int64_t k = cols + tid; k < pad_cols; k += QR_THREADS) dst[k] = 0;
+  sum = warp_sum_i(sum);
+  if (lane == 0) s_sum[wid] = sum;
+  __syncthreads();
+  if (tid == 0) {
+    int t = 0;
+#pragma unroll
+    for (int i = 0; i < QR_THREADS / 32; ++i) t += s_sum[i];
+    scale[row] = flat ? 0.0f : __double2float_rn(step64);
+    offset[row] = lo;
+    if (rowsum != nullptr) rowsum[row] = t;
+  }
+}
+
 QA_DEV uint32_t unpack_code(const uint8_t* row, int64_t k, int bits) {
   if (bits == 8) return row[k];
   const uint32_t b = row[k >> 1];
@@ -276,6 +383,39 @@ cudaError_t launch_quantize_rows(const void* w, int w_dtype, int64_t rows, int64
   const bool vec_out = bits == 8 ? ((reinterpret_cast<uintptr_t>(codes) % 8 == 0) && (ld_codes % 8 == 0))
                                  : ((reinterpret_cast<uintptr_t>(codes) % 4 == 0) && (ld_codes % 4 == 0));
   const int vec_ok = vec_in && vec_out;
+  // production path: one CTA per row, the row in registers (cols a multiple of 8, up to 32768)
+  const int64_t per_pass = int64_t(QR_THREADS) * 8;
+  const int ch = vec_ok && cols % 8 == 0 ? static_cast<int>((cols + per_pass - 1) / per_pass) : 0;
+  if (ch >= 1 && ch <= 16) {
+    const int chp = ch <= 1 ? 1 : ch <= 2 ? 2 : ch <= 4 ? 4 : ch <= 8 ? 8 : 16;
+#define QA_QR(TI, BB, CC)                                                                                         \
+  k_quantize_rows_reg<TI, BB, CC><<<static_cast<unsigned>(rows), QR_THREADS, 0, s>>>(                              \
+      static_cast<const TI*>(w), cols, ld_w, codes, ld_codes, pad_cols, scale, offset, rowsum, flag)
+#define QA_QR_C(TI, BB)      \
+  switch (chp) {             \
+    case 1: QA_QR(TI, BB, 1); break;  \
+    case 2: QA_QR(TI, BB, 2); break;  \
+    case 4: QA_QR(TI, BB, 4); break;  \
+    case 8: QA_QR(TI, BB, 8); break;  \
+    default: QA_QR(TI, BB, 16); break; \
+  }
+    if (w_dtype == QA_F32) {
+      if (bits == 8) {
+        QA_QR_C(float, 8)
+      } else {
+        QA_QR_C(float, 4)
+      }
+    } else {
+      if (bits == 8) {
+        QA_QR_C(__nv_bfloat16, 8)
+      } else {
+        QA_QR_C(__nv_bfloat16, 4)
+      }
+    }
+#undef QA_QR_C
+#undef QA_QR
+    return cudaGetLastError();
+  }
   if (w_dtype == QA_F32) {
     if (bits == 8)
       k_quantize_rows<float, 8><<<grid, warps * 32, 0, s>>>(static_cast<const float*>(w), rows, cols, ld_w, codes,

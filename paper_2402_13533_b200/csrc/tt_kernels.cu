@@ -447,6 +447,136 @@ __global__ void __launch_bounds__(256, 2) k_merge_nd1(const float* __restrict__ 
   }
 }
 
+// Fused merge / materialise for the fast TT family (first core input-only, last core output-only: the pinned
+// Llama modes m = (1, H, M), n = (J0, J1, 1), and LoRA, m = (1, N), n = (K, 1)):
+//   W'[row, col] = code·scale[row] + offset[row] + Σ_b L[col, b] · Gd[b, i],   row = h·md + i
+//   d = 3: L[col, b] = Σ_a G1[j0, a] · G2[a, h, j1, b]  (col = j0·J1 + j1);  d = 2: L[col, b] = G1[col, b]
+// A CTA owns RT rows of one h-block and 128 columns; every lane holds its 4 columns' L (R x 4 fp32, formed
+// in registers from G1 and the h-slice of G2 staged in shared memory — no prefix pass, no L buffer) and walks
+// the rows of its warp: Gd[:, i] as two broadcast 16-byte shared loads, 2R packed FMAs, the 4 codes (2 or 4
+// bytes, prefetched UN rows ahead), one fp32 FMA dequantisation per element (< 1 ulp of the reference's fp64
+// route, quant.py:102-105), one 8- or 16-byte store (a warp writes 256 / 512 contiguous bytes per row).
+constexpr int MF_COLS = 128, MF_UN = 4;
+
+template <typename OutT, int BITS, int R, bool D3>
+__global__ void __launch_bounds__(256, R == 8 ? 4 : 2) k_merge_fast(const float* __restrict__ G1, const float* __restrict__ G2,
+                                                       const float* __restrict__ Gd, int R1, int J1, int H,
+                                                       int64_t md, int64_t N, int64_t K, int RT,
+                                                       const uint8_t* __restrict__ codes,
+                                                       const float* __restrict__ scale,
+                                                       const float* __restrict__ offset, OutT* __restrict__ out) {
+  extern __shared__ __align__(16) float mf_smem[];
+  float* gs = mf_smem;             // [RT][R]: Gd[:, i] per tile row
+  float* g2s = mf_smem + RT * R;   // [R1][J1][R]: G2[:, h, :, :] (d = 3)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t c0 = static_cast<int64_t>(blockIdx.x) * MF_COLS;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * RT;
+  const int64_t h = r0 / md;
+  const int64_t i0 = r0 - h * md;
+  for (int q = threadIdx.x; q < RT * R; q += 256) {
+    const int rl = q / R, b = q - rl * R;
+    gs[q] = Gd[static_cast<int64_t>(b) * md + i0 + rl];
+  }
+  if (D3)
+    for (int q = threadIdx.x; q < R1 * J1 * R; q += 256) {
+      const int a = q / (J1 * R), rem = q - a * J1 * R;
+      g2s[q] = G2[(static_cast<int64_t>(a) * H + h) * J1 * R + rem];
+    }
+  __syncthreads();
+  const int64_t col = c0 + lane * 4;
+  const bool active = col < K;
+  // L of the lane's 4 columns, as column pairs per rank: lp[b][0] = (col, col+1), lp[b][1] = (col+2, col+3)
+  unsigned long long lp[R][2];
+  {
+    float lv[4][R];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+#pragma unroll
+      for (int b = 0; b < R; ++b) lv[c][b] = 0.f;
+      const int64_t cc = active ? col + c : 0;
+      if (D3) {
+        const int64_t j0 = cc / J1;
+        const int j1 = static_cast<int>(cc - j0 * J1);
+        for (int a = 0; a < R1; ++a) {
+          const float g1 = __ldg(G1 + j0 * R1 + a);
+          const float* g2 = g2s + (a * J1 + j1) * R;
+#pragma unroll
+          for (int b = 0; b < R; ++b) lv[c][b] = fmaf(g1, g2[b], lv[c][b]);
+        }
+      } else {
+        const float4* g1 = reinterpret_cast<const float4*>(G1 + cc * R);
+#pragma unroll
+        for (int q = 0; q < R / 4; ++q) {
+          const float4 v = __ldg(g1 + q);
+          lv[c][4 * q] = v.x;
+          lv[c][4 * q + 1] = v.y;
+          lv[c][4 * q + 2] = v.z;
+          lv[c][4 * q + 3] = v.w;
+        }
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < R; ++b) {
+      lp[b][0] = f2pack(lv[0][b], lv[1][b]);
+      lp[b][1] = f2pack(lv[2][b], lv[3][b]);
+    }
+  }
+  if (!active) return;
+  const int64_t cld = BITS == 8 ? K : (K + 1) / 2;
+  const uint8_t* cbase = codes != nullptr ? codes + (BITS == 8 ? col : col / 2) : nullptr;
+  OutT* obase = out + col;
+  const int nrows = static_cast<int>(N - r0 < RT ? N - r0 : RT);
+  for (int rb = warp * MF_UN; rb < nrows; rb += 8 * MF_UN) {
+    uint32_t cw[MF_UN];
+#pragma unroll
+    for (int u = 0; u < MF_UN; ++u) {
+      const int rl = rb + u;
+      cw[u] = 0u;
+      if (cbase != nullptr && rl < nrows) {
+        const uint8_t* p = cbase + (r0 + rl) * cld;
+        cw[u] = BITS == 8 ? __ldg(reinterpret_cast<const uint32_t*>(p))
+                          : static_cast<uint32_t>(__ldg(reinterpret_cast<const uint16_t*>(p)));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < MF_UN; ++u) {
+      const int rl = rb + u;
+      if (rl >= nrows) break;
+      unsigned long long acc0 = 0ull, acc1 = 0ull;
+      const float4* gr = reinterpret_cast<const float4*>(gs + rl * R);
+#pragma unroll
+      for (int q = 0; q < R / 4; ++q) {
+        const float4 g = gr[q];
+        const float gg[4] = {g.x, g.y, g.z, g.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const unsigned long long g2 = f2pack(gg[e], gg[e]);
+          ffma2(acc0, g2, lp[4 * q + e][0]);
+          ffma2(acc1, g2, lp[4 * q + e][1]);
+        }
+      }
+      float wt[4] = {f2lo(acc0), f2hi(acc0), f2lo(acc1), f2hi(acc1)};
+      const int64_t row = r0 + rl;
+      if (cbase != nullptr) {
+        const float sc = __ldg(scale + row), of = __ldg(offset + row);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t c = BITS == 8 ? (cw[u] >> (8 * e)) & 0xFFu : (cw[u] >> (4 * e)) & 0xFu;
+          wt[e] += fmaf(static_cast<float>(c), sc, of);
+        }
+      }
+      OutT* dst = obase + row * K;
+      if constexpr (sizeof(OutT) == 2) {
+        const __nv_bfloat162 a = __floats2bfloat162_rn(wt[0], wt[1]), b = __floats2bfloat162_rn(wt[2], wt[3]);
+        *reinterpret_cast<uint2*>(dst) =
+            make_uint2(*reinterpret_cast<const uint32_t*>(&a), *reinterpret_cast<const uint32_t*>(&b));
+      } else {
+        *reinterpret_cast<float4*>(dst) = make_float4(wt[0], wt[1], wt[2], wt[3]);
+      }
+    }
+  }
+}
+
 unsigned grid_for(int64_t total, int threads) {
   const int64_t blocks = (total + threads - 1) / threads;
   return static_cast<unsigned>(blocks < 148 * 64 ? (blocks > 0 ? blocks : 1) : 148 * 64);
@@ -550,6 +680,64 @@ cudaError_t launch_tt_prefix_full(const TTDims& dd, const float* const* cores, f
   } else {
     k_prefix_full<<<static_cast<unsigned>((total + 127) / 128), 128, 0, s>>>(dd, cp, L, IP, JP, R);
   }
+  return cudaGetLastError();
+}
+
+bool merge_fast_ok(const TTDims& dd, const void* codes, const void* out) {
+  const int d = dd.d;
+  if ((d != 2 && d != 3) || dd.m[0] != 1 || dd.n[d - 1] != 1) return false;
+  const int R = dd.r[d - 1];
+  const int64_t md = dd.m[d - 1];
+  if ((R != 8 && R != 16) || md % 64 != 0 || dd.K % 8 != 0) return false;
+  if (d == 3 && (dd.r[1] > 16 || dd.n[1] > 16)) return false;
+  return reinterpret_cast<uintptr_t>(out) % 16 == 0 && (codes == nullptr || reinterpret_cast<uintptr_t>(codes) % 4 == 0);
+}
+
+cudaError_t launch_merge_fast(const TTDims& dd, const float* const* cores, const uint8_t* codes, int bits,
+                              const float* scale, const float* offset, void* out, int out_dtype, cudaStream_t s) {
+  const int d = dd.d;
+  const int R = dd.r[d - 1];
+  const int64_t md = dd.m[d - 1];
+  const int RT = md % 256 == 0 ? 256 : 64;
+  const int R1 = d == 3 ? dd.r[1] : 0, J1 = d == 3 ? dd.n[1] : 1, H = d == 3 ? dd.m[1] : 1;
+  const int64_t total = dd.N * dd.K;
+  LaunchScope scope(kMerge, double(total) * ((codes ? (bits == 8 ? 1.0 : 0.5) : 0.0) + (out_dtype == QA_F32 ? 4 : 2)), s);
+  count_launches(1);
+  const dim3 grid(static_cast<unsigned>((dd.K + MF_COLS - 1) / MF_COLS), static_cast<unsigned>(dd.N / RT));
+  const size_t smem = sizeof(float) * (static_cast<size_t>(RT) * R + static_cast<size_t>(R1) * J1 * R);
+  const float* G1 = cores[0];
+  const float* G2 = d == 3 ? cores[1] : nullptr;
+  const float* Gd = cores[d - 1];
+#define QA_MF(OT, BB, RR, DD)                                                                                     \
+  k_merge_fast<OT, BB, RR, DD><<<grid, 256, smem, s>>>(G1, G2, Gd, R1, J1, H, md, dd.N, dd.K, RT, codes, scale,     \
+                                                      offset, static_cast<OT*>(out))
+#define QA_MF_D(OT, BB, RR) \
+  if (d == 3)               \
+    QA_MF(OT, BB, RR, true); \
+  else                      \
+    QA_MF(OT, BB, RR, false);
+#define QA_MF_R(OT, BB) \
+  if (R == 8) {         \
+    QA_MF_D(OT, BB, 8)  \
+  } else {              \
+    QA_MF_D(OT, BB, 16) \
+  }
+  if (out_dtype == QA_F32) {
+    if (bits == 4) {
+      QA_MF_R(float, 4)
+    } else {
+      QA_MF_R(float, 8)
+    }
+  } else {
+    if (bits == 4) {
+      QA_MF_R(__nv_bfloat16, 4)
+    } else {
+      QA_MF_R(__nv_bfloat16, 8)
+    }
+  }
+#undef QA_MF_R
+#undef QA_MF_D
+#undef QA_MF
   return cudaGetLastError();
 }
 

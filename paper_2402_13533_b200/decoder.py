@@ -24,10 +24,11 @@ import torch.nn.functional as F
 
 from . import dp, glue
 from .optim import AdamWConfig, AdamWState, adamw_step
-from .linear import QuantizedLinear, TTLinear, TTSpec, attach_tt_adapter, group_backward, group_forward
+from .linear import ModelError, QuantizedLinear, TTLinear, TTSpec, attach_tt_adapter, group_backward, group_forward
 from .quant import quantize_rows
 
-__all__ = ["DecoderConfig", "DecoderLayer", "DecoderStack", "build_decoder"]
+__all__ = ["DecoderConfig", "DecoderLayer", "DecoderStack", "KvCache", "build_decoder", "kv_decode_step",
+           "greedy_decode"]
 
 
 @dataclass(frozen=True)
@@ -180,6 +181,25 @@ class DecoderStack:
         ang = torch.arange(length, dtype=torch.float64, device=device)[:, None] * freqs[None, :]
         return torch.cos(ang).float().contiguous(), torch.sin(ang).float().contiguous()
 
+    def forward(self, tokens):
+        """model_forward (transformer.py:949-981) for inference: logits [batch, seq, vocab] (bf16), no tape."""
+        cfg = self.config
+        tokens = torch.as_tensor(tokens, device=self.embed.device)
+        if tokens.dim() == 1:
+            tokens = tokens[None]
+        b, l = tokens.shape
+        if l > cfg.max_seq:
+            raise ModelError(f"sequence length {l} exceeds max_seq {cfg.max_seq}")
+        if int(tokens.min()) < 0 or int(tokens.max()) >= cfg.vocab:
+            raise ModelError(f"token id out of range [0, {cfg.vocab})")
+        shape = (b, l, cfg.heads)
+        rope = self.rope_tables(l, tokens.device)
+        x = self.embed[tokens.reshape(-1)]
+        for layer in self.layers:
+            x, _ = layer.forward(x, shape, rope, keep=False)
+        (logits,) = _group_fwd([self.head], x)
+        return logits.view(b, l, -1)
+
     def train_step_grads(self, tokens, targets, policy: str = "per_layer", grads: dict | None = None):
         """One forward + cross-entropy + backward (model_forward / cross_entropy_grad / model_backward).
         policy "per_layer" keeps only each layer's input and recomputes; "store_all" keeps every layer's
@@ -213,6 +233,92 @@ class DecoderStack:
             dx = layer.backward(entry, dx, shape, rope, grads)
             del entry
         return float(loss), grads
+
+
+class KvCache:
+    """Per-layer key / value grids in HBM, one row appended per decode step (transformer.py:1015-1027): bf16
+    [max_seq, dim] per layer, as the projections produce them (k after RoPE)."""
+
+    def __init__(self, model: "DecoderStack"):
+        cfg = model.config
+        dev = model.embed.device
+        self.max_seq = cfg.max_seq
+        self.length = 0
+        self.k = [torch.zeros((cfg.max_seq, cfg.dim), dtype=torch.bfloat16, device=dev) for _ in range(cfg.layers)]
+        self.v = [torch.zeros((cfg.max_seq, cfg.dim), dtype=torch.bfloat16, device=dev) for _ in range(cfg.layers)]
+        self.rope = model.rope_tables(cfg.max_seq, dev)
+
+    @property
+    def current_len(self) -> int:
+        return self.length
+
+
+def kv_decode_step(model: "DecoderStack", cache: KvCache, token: int, step: int = 0):
+    """kv_decode_step (transformer.py:1043-1080) on the device: exactly one token through the stack — each linear
+    a decode-size forward (act-quant prologue + tensor-core matrix-vector pass; q/k/v and up/gate as shared-input
+    groups), RoPE at this position, attention of the new query over the cached keys / values (torch SDPA), the
+    cache grown by one row.  Returns (logits [vocab] f32, cache)."""
+    cfg = model.config
+    if cache.length >= cache.max_seq:
+        raise ModelError(f"kv cache overflow: length {cache.length} at max_seq {cache.max_seq}")
+    if not 0 <= int(token) < cfg.vocab:
+        raise ModelError(f"token id {token} out of range")
+    pos = cache.length
+    heads, d = cfg.heads, cfg.head_dim
+    cos, sin = cache.rope[0][pos:pos + 1], cache.rope[1][pos:pos + 1]
+    x = model.embed[int(token)].reshape(1, cfg.dim).contiguous()
+    for li, layer in enumerate(model.layers):
+        m = layer.mats
+        norm1, _ = glue.rmsnorm(x, layer.norm1)
+        q, k, v = _group_fwd([m["wq"], m["wk"], m["wv"]], norm1)
+        glue.rope_(q, k, cos, sin, heads, 1)
+        cache.k[li][pos].copy_(k[0])
+        cache.v[li][pos].copy_(v[0])
+        keys = cache.k[li][:pos + 1].view(pos + 1, heads, d).transpose(0, 1)
+        vals = cache.v[li][:pos + 1].view(pos + 1, heads, d).transpose(0, 1)
+        ctx = F.scaled_dot_product_attention(q.view(heads, 1, d), keys, vals)
+        ctx = ctx.reshape(1, cfg.dim).contiguous()
+        (attn,) = _group_fwd([m["wo"]], ctx)
+        norm2, _, res1 = glue.rmsnorm(x, layer.norm2, b=attn)
+        up, gate = _group_fwd([m["wu"], m["wg"]], norm2)
+        (ffn,) = _group_fwd([m["wd"]], glue.swiglu(up, gate))
+        x = res1 + ffn
+    cache.length += 1
+    (logits,) = _group_fwd([model.head], x)
+    return logits[0].float(), cache
+
+
+def greedy_decode(model: "DecoderStack", prompt, max_new: int, use_cache: bool = True):
+    """greedy_decode (transformer.py:1083-1111): greedy continuation of the prompt; returns (generated ids, token
+    passes).  use_cache=False re-runs the full forward over the growing sequence for every new token."""
+    prompt = [int(t) for t in torch.as_tensor(prompt).reshape(-1).tolist()]
+    if not prompt:
+        raise ModelError("prompt must hold at least one token")
+    generated: list[int] = []
+    passes = 0
+    if use_cache:
+        cache = KvCache(model)
+        logits = None
+        for tok in prompt:
+            logits, cache = kv_decode_step(model, cache, tok)
+            passes += 1
+        for _ in range(max_new):
+            nxt = int(torch.argmax(logits))
+            generated.append(nxt)
+            if len(generated) == max_new:
+                break
+            logits, cache = kv_decode_step(model, cache, nxt)
+            passes += 1
+    else:
+        seq = list(prompt)
+        dev = model.embed.device
+        for _ in range(max_new):
+            logits = model.forward(torch.tensor([seq], dtype=torch.int64, device=dev))
+            passes += len(seq)
+            nxt = int(torch.argmax(logits[0, -1]))
+            generated.append(nxt)
+            seq.append(nxt)
+    return generated, passes
 
 
 def build_decoder(cfg: DecoderConfig, rank: int = 8, bits: int = 8, seed: int = 0, device="cuda") -> DecoderStack:

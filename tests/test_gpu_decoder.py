@@ -230,3 +230,31 @@ def test_decoder_matches_reference_model_backward():
     errs = {k: _norm_rel(grads[k].cpu().numpy(), want[k]) for k in want}
     bad = {k: e for k, e in errs.items() if not e < 5e-2}
     assert not bad, (bad, max(errs.values()))
+
+
+def test_kv_decode_matches_full_forward_and_greedy(setup):
+    """kv_decode_step (transformer.py:1043-1080) on the device: the logits of each cached one-token step equal the
+    matching position of a full forward over the prefix (the reference's own contract for the cache), within the
+    bf16 activation noise of two different attention kernels; greedy_decode with and without the cache agree."""
+    model, tokens, _ = setup
+    seq = tokens[0, :12].tolist()
+    full = model.forward(torch.tensor([seq], device="cuda"))[0].float()
+    cache = decoder.KvCache(model)
+    errs = []
+    for i, t in enumerate(seq):
+        logits, cache = decoder.kv_decode_step(model, cache, t)
+        assert logits.shape == (CFG.vocab,) and logits.dtype == torch.float32
+        errs.append(O.rel_err(logits.cpu().numpy(), full[i].cpu().numpy()))
+    print("kv decode vs full forward:", " ".join(f"{e:.1e}" for e in errs))
+    assert max(errs) <= 3e-2, errs
+    assert cache.current_len == 12
+    with pytest.raises(decoder.ModelError, match="out of range"):
+        decoder.kv_decode_step(model, cache, CFG.vocab)
+    gen, passes = decoder.greedy_decode(model, seq[:4], max_new=5)
+    gen2, passes2 = decoder.greedy_decode(model, seq[:4], max_new=5, use_cache=False)
+    assert passes == 4 + 4 and passes2 == sum(4 + i for i in range(5))
+    assert gen == gen2
+    over = decoder.KvCache(model)
+    over.length = CFG.max_seq
+    with pytest.raises(decoder.ModelError, match="overflow"):
+        decoder.kv_decode_step(model, over, 1)

@@ -254,3 +254,29 @@ def test_single_cta_persistent_kernel_multi_tile():
     dx = lin.backward(x, dy, grads)
     _dx_check([lin], [cores_np], [dy], [dx], rows)
     _grads_check([lin], [cores_np], x, [dy], grads)
+
+
+@pytest.mark.parametrize("shape", [(28672, 8192, 4), (1024, 8192, 4), (4096, 11008, 8)])
+@pytest.mark.parametrize("kind", ["tt", "lora"])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_merge_matches_oracle_at_benchmark_shapes(shape, kind, dtype):
+    """qa_merge as the bench times it (config 5's 70B gate and GQA k/v shapes, int4; the 7B down projection,
+    int8): the fused fast-family merge (prefix contraction in registers) for the pinned TT modes and LoRA,
+    against dequantize_rows + W_t (lowrank.py:245-257 via :249-252) on sampled rows.  fp32 output within 1e-5,
+    bf16 output within one bf16 ulp."""
+    N, K, bits = shape
+    g = torch.Generator(device="cuda").manual_seed(N + K)
+    q = qa.quantize_rows(torch.randn(N, K, generator=g, device="cuda") * 0.02, bits)
+    spec = L.TTSpec.for_shape(N, K, 8) if kind == "tt" else L.TTSpec.lora(N, K, 8)
+    cores_np = O.tt_init_cores(O.TTShape(spec.m, spec.n, spec.ranks), 7, std=0.05)
+    lin = L.TTLinear("w", L.QuantizedLinear("w.base", q), spec, [torch.from_numpy(c).cuda() for c in cores_np])
+    merged = L.tt_merge(lin, dtype)
+    rows = _sample(N, 24, 5)
+    want = O.dequantize_rows(_oq(q, rows)) + O.tt_rows(cores_np, rows)
+    got = _np(merged[torch.from_numpy(rows).cuda()])
+    e = O.rel_err(got, want)
+    print(f"merge {kind} {N}x{K} int{bits} {dtype}: {e:.2e}")
+    assert e <= (1e-5 if dtype == torch.float32 else BF16_ULP / 2), e
+    # W_t alone (qa_tt_materialize, same fused kernel without codes)
+    wt = L.tt_materialize(spec, lin._core_tensors())
+    assert O.rel_err(_np(wt[torch.from_numpy(rows).cuda()]), O.tt_rows(cores_np, rows)) <= 1e-5
