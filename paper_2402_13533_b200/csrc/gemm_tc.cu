@@ -699,8 +699,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           __syncwarp();
 #pragma unroll
           for (int c16 = 0; c16 < 8; ++c16)
-            *reinterpret_cast<uint4*>(stg + lane * 128 + ((c16 ^ (lane & 7)) << 4)) =
-                make_uint4(pk[4 * c16], pk[4 * c16 + 1], pk[4 * c16 + 2], pk[4 * c16 + 3]);
+            sts128(smem_u32(stg) + lane * 128 + ((c16 ^ (lane & 7)) << 4),
+                   make_uint4(pk[4 * c16], pk[4 * c16 + 1], pk[4 * c16 + 2], pk[4 * c16 + 3]));
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {

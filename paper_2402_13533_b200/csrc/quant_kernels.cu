@@ -111,9 +111,7 @@ __global__ void __launch_bounds__(256) k_quantize_rows(const InT* __restrict__ w
 // so a CTA keeps its row's bytes in flight; min / max meet through warp shuffles and shared memory; the
 // codes come from the registers — each input byte crosses HBM exactly once.  Same code rule as
 // k_quantize_rows (code_of / codes8: fp32 with an fp64 replay inside the tie band).
-constexpr int QR_THREADS = 256;
-
-template <typename InT, int BITS, int CH>
+template <typename InT, int BITS, int CH, int QR_THREADS>
 __global__ void __launch_bounds__(QR_THREADS) k_quantize_rows_reg(const InT* __restrict__ w, int64_t cols,
                                                                    int64_t ldw, uint8_t* __restrict__ codes,
                                                                    int64_t ldc, int64_t pad_cols,
@@ -383,21 +381,30 @@ cudaError_t launch_quantize_rows(const void* w, int w_dtype, int64_t rows, int64
   const bool vec_out = bits == 8 ? ((reinterpret_cast<uintptr_t>(codes) % 8 == 0) && (ld_codes % 8 == 0))
                                  : ((reinterpret_cast<uintptr_t>(codes) % 4 == 0) && (ld_codes % 4 == 0));
   const int vec_ok = vec_in && vec_out;
-  // production path: one CTA per row, the row in registers (cols a multiple of 8, up to 32768)
-  const int64_t per_pass = int64_t(QR_THREADS) * 8;
+  // production path: one CTA per row, the row in registers (cols a multiple of 8, up to 32768); rows up to
+  // 16384 columns take 128-thread CTAs with up to 16 chunks per thread (more bytes in flight per register)
+  const int qthreads = cols <= 128 * 8 * 16 ? 128 : 256;
+  const int64_t per_pass = int64_t(qthreads) * 8;
   const int ch = vec_ok && cols % 8 == 0 ? static_cast<int>((cols + per_pass - 1) / per_pass) : 0;
   if (ch >= 1 && ch <= 16) {
     const int chp = ch <= 1 ? 1 : ch <= 2 ? 2 : ch <= 4 ? 4 : ch <= 8 ? 8 : 16;
-#define QA_QR(TI, BB, CC)                                                                                         \
-  k_quantize_rows_reg<TI, BB, CC><<<static_cast<unsigned>(rows), QR_THREADS, 0, s>>>(                              \
+#define QA_QR(TI, BB, CC, TH)                                                                                     \
+  k_quantize_rows_reg<TI, BB, CC, TH><<<static_cast<unsigned>(rows), TH, 0, s>>>(                                  \
       static_cast<const TI*>(w), cols, ld_w, codes, ld_codes, pad_cols, scale, offset, rowsum, flag)
-#define QA_QR_C(TI, BB)      \
-  switch (chp) {             \
-    case 1: QA_QR(TI, BB, 1); break;  \
-    case 2: QA_QR(TI, BB, 2); break;  \
-    case 4: QA_QR(TI, BB, 4); break;  \
-    case 8: QA_QR(TI, BB, 8); break;  \
-    default: QA_QR(TI, BB, 16); break; \
+#define QA_QR_C(TI, BB)                                                 \
+  if (qthreads == 128) {                                                \
+    switch (chp) {                                                      \
+      case 1: QA_QR(TI, BB, 1, 128); break;                             \
+      case 2: QA_QR(TI, BB, 2, 128); break;                             \
+      case 4: QA_QR(TI, BB, 4, 128); break;                             \
+      case 8: QA_QR(TI, BB, 8, 128); break;                             \
+      default: QA_QR(TI, BB, 16, 128); break;                           \
+    }                                                                   \
+  } else {                                                              \
+    switch (chp) {                                                      \
+      case 1: case 2: case 4: case 8: QA_QR(TI, BB, 8, 256); break;     \
+      default: QA_QR(TI, BB, 16, 256); break;                           \
+    }                                                                   \
   }
     if (w_dtype == QA_F32) {
       if (bits == 8) {

@@ -456,10 +456,10 @@ __global__ void __launch_bounds__(256, 2) k_merge_nd1(const float* __restrict__ 
 // the rows of its warp: Gd[:, i] as two broadcast 16-byte shared loads, 2R packed FMAs, the 4 codes (2 or 4
 // bytes, prefetched UN rows ahead), one fp32 FMA dequantisation per element (< 1 ulp of the reference's fp64
 // route, quant.py:102-105), one 8- or 16-byte store (a warp writes 256 / 512 contiguous bytes per row).
-constexpr int MF_COLS = 128, MF_UN = 4;
+constexpr int MF_COLS = 128, MF_UN = 8;
 
 template <typename OutT, int BITS, int R, bool D3>
-__global__ void __launch_bounds__(256, R == 8 ? 4 : 2) k_merge_fast(const float* __restrict__ G1, const float* __restrict__ G2,
+__global__ void __launch_bounds__(256, R == 8 ? 3 : 2) k_merge_fast(const float* __restrict__ G1, const float* __restrict__ G2,
                                                        const float* __restrict__ Gd, int R1, int J1, int H,
                                                        int64_t md, int64_t N, int64_t K, int RT,
                                                        const uint8_t* __restrict__ codes,
@@ -526,8 +526,8 @@ __global__ void __launch_bounds__(256, R == 8 ? 4 : 2) k_merge_fast(const float*
   const uint8_t* cbase = codes != nullptr ? codes + (BITS == 8 ? col : col / 2) : nullptr;
   OutT* obase = out + col;
   const int nrows = static_cast<int>(N - r0 < RT ? N - r0 : RT);
-  for (int rb = warp * MF_UN; rb < nrows; rb += 8 * MF_UN) {
-    uint32_t cw[MF_UN];
+  // the code words of the warp's next MF_UN rows are in flight while the current ones are processed
+  auto load_codes = [&](int rb, uint32_t (&cw)[MF_UN]) {
 #pragma unroll
     for (int u = 0; u < MF_UN; ++u) {
       const int rl = rb + u;
@@ -538,6 +538,11 @@ __global__ void __launch_bounds__(256, R == 8 ? 4 : 2) k_merge_fast(const float*
                           : static_cast<uint32_t>(__ldg(reinterpret_cast<const uint16_t*>(p)));
       }
     }
+  };
+  uint32_t cw[MF_UN], cn[MF_UN];
+  load_codes(warp * MF_UN, cw);
+  for (int rb = warp * MF_UN; rb < nrows; rb += 8 * MF_UN) {
+    load_codes(rb + 8 * MF_UN, cn);
 #pragma unroll
     for (int u = 0; u < MF_UN; ++u) {
       const int rl = rb + u;
@@ -574,6 +579,8 @@ __global__ void __launch_bounds__(256, R == 8 ? 4 : 2) k_merge_fast(const float*
         *reinterpret_cast<float4*>(dst) = make_float4(wt[0], wt[1], wt[2], wt[3]);
       }
     }
+#pragma unroll
+    for (int u = 0; u < MF_UN; ++u) cw[u] = cn[u];
   }
 }
 
