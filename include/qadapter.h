@@ -257,6 +257,12 @@ QA_API int qa_swiglu_backward(const void* up, const void* gate, const void* dact
 QA_API int qa_cross_entropy(const void* logits, const int64_t* targets, int64_t rows, int64_t vocab,
                             float* loss_rows, void* dlogits, void* stream);
 
+/* MSE loss against a target (BASELINE config 1's "adapter grads vs MSE to a seeded target"; the
+ * reference's own loss is cross-entropy, transformer.py:569-588): loss_rows[r] = Σ_c (y - target)^2 (the loss is
+ * their sum / (rows * cols)), dy = 2 (y - target) / (rows * cols) (nullable).  y / dy: QA_F32 or QA_BF16. */
+QA_API int qa_mse(const void* y, int y_dtype, const float* target, int64_t rows, int64_t cols, float* loss_rows,
+                  void* dy, int dy_dtype, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

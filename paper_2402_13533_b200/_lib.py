@@ -38,6 +38,7 @@ EXPORTS = (
     "qa_swiglu_forward",
     "qa_swiglu_backward",
     "qa_cross_entropy",
+    "qa_mse",
     "qa_linear_workspace_bytes",
     "qa_linear_forward",
     "qa_linear_backward",
@@ -117,6 +118,8 @@ def _declare(lib):
     lib.qa_swiglu_backward.argtypes = [P, P, P, P, P, I64, P]
     lib.qa_cross_entropy.restype = I32
     lib.qa_cross_entropy.argtypes = [P, P, I64, I64, P, P, P]
+    lib.qa_mse.restype = I32
+    lib.qa_mse.argtypes = [P, I32, P, I64, I64, P, P, I32, P]
     lib.qa_linear_workspace_bytes.restype = SZ
     lib.qa_linear_workspace_bytes.argtypes = [PW, PT, I64]
     lib.qa_linear_forward.restype = I32

@@ -404,6 +404,18 @@ int qa_cross_entropy(const void* logits, const int64_t* targets, int64_t rows, i
                      "cross entropy");
 }
 
+int qa_mse(const void* y, int y_dtype, const float* target, int64_t rows, int64_t cols, float* loss_rows, void* dy,
+           int dy_dtype, void* stream) {
+  if (rows < 0 || cols < 1 || y == nullptr || target == nullptr || loss_rows == nullptr ||
+      (y_dtype != QA_F32 && y_dtype != QA_BF16) || (dy_dtype != QA_F32 && dy_dtype != QA_BF16)) {
+    set_error("qa_mse: bad argument");
+    return QA_ERR_ARG;
+  }
+  return cuda_status(launch_mse(y, y_dtype, target, rows, cols, loss_rows, dy, dy_dtype,
+                                static_cast<cudaStream_t>(stream)),
+                     "mse");
+}
+
 int qa_code_rowsum(const uint8_t* codes, int64_t rows, int64_t cols, int bits, int32_t* rowsum, void* stream) {
   if (bits != 4 && bits != 8) {
     set_error("bits must be 4 or 8, got %d", bits);

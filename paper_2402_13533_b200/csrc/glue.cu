@@ -10,6 +10,7 @@
 
 #include "qa_common.cuh"
 #include "qa_internal.h"
+#include "qa_timing.h"
 
 namespace qa {
 
@@ -329,14 +330,35 @@ __global__ void __launch_bounds__(kXentThreads) k_xent(const __nv_bfloat16* __re
   }
 }
 
-int glue_grid(int64_t work, int threads) {
-  static int nsm = 0;
-  if (nsm == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    if (nsm <= 0) nsm = 148;
+// MSE against a target (the reference's loss is cross-entropy only): per row,
+// loss_rows[r] = Σ_c (y - t)^2 (fixed-order block reduction) and dy = 2 (y - t) / (rows * cols).
+template <typename YT, typename DT>
+__global__ void __launch_bounds__(256) k_mse(const YT* __restrict__ y, const float* __restrict__ target, int64_t cols,
+                                             float inv_n2, float* __restrict__ loss_rows, DT* __restrict__ dy) {
+  const int64_t row = blockIdx.x;
+  const YT* yr = y + row * cols;
+  const float* tr = target + row * cols;
+  float acc = 0.f;
+  for (int64_t c = threadIdx.x; c < cols; c += 256) {
+    const float d = to_f32(yr[c]) - tr[c];
+    acc = fmaf(d, d, acc);
+    if (dy != nullptr) dy[row * cols + c] = static_cast<DT>(d * inv_n2);
   }
+  __shared__ float red[256];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (static_cast<int>(threadIdx.x) < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) loss_rows[row] = red[0];
+}
+
+int glue_grid(int64_t work, int threads) {
+  int dev = 0, nsm = 0;  // per call: the current device's SM count (an attribute query, no global state)
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  if (nsm <= 0) nsm = 148;
   const int64_t want = (work + threads - 1) / threads;
   const int64_t cap = static_cast<int64_t>(nsm) * 8;
   return static_cast<int>(want < 1 ? 1 : (want < cap ? want : cap));
@@ -428,6 +450,27 @@ cudaError_t launch_swiglu_bwd(const __nv_bfloat16* up, const __nv_bfloat16* gate
   k_swiglu_bwd<<<glue_grid(n / 8, 256), 256, 0, st>>>(
       reinterpret_cast<const uint4*>(up), reinterpret_cast<const uint4*>(gate), reinterpret_cast<const uint4*>(dact),
       reinterpret_cast<uint4*>(dup), reinterpret_cast<uint4*>(dgate), n / 8);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mse(const void* y, int y_dtype, const float* target, int64_t rows, int64_t cols, float* loss_rows,
+                       void* dy, int dy_dtype, cudaStream_t st) {
+  if (rows == 0) return cudaSuccess;
+  count_launches(1);
+  const float inv_n2 = static_cast<float>(2.0 / (static_cast<double>(rows) * static_cast<double>(cols)));
+  const unsigned grid = static_cast<unsigned>(rows);
+  if (y_dtype == QA_F32 && dy_dtype == QA_F32)
+    k_mse<float, float><<<grid, 256, 0, st>>>(static_cast<const float*>(y), target, cols, inv_n2, loss_rows,
+                                              static_cast<float*>(dy));
+  else if (y_dtype == QA_F32)
+    k_mse<float, __nv_bfloat16><<<grid, 256, 0, st>>>(static_cast<const float*>(y), target, cols, inv_n2, loss_rows,
+                                                      static_cast<__nv_bfloat16*>(dy));
+  else if (dy_dtype == QA_F32)
+    k_mse<__nv_bfloat16, float><<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(y), target, cols, inv_n2,
+                                                      loss_rows, static_cast<float*>(dy));
+  else
+    k_mse<__nv_bfloat16, __nv_bfloat16><<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(y), target, cols,
+                                                              inv_n2, loss_rows, static_cast<__nv_bfloat16*>(dy));
   return cudaGetLastError();
 }
 

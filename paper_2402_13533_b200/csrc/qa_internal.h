@@ -106,6 +106,8 @@ cudaError_t launch_swiglu_fwd(const __nv_bfloat16* up, const __nv_bfloat16* gate
                               cudaStream_t st);
 cudaError_t launch_swiglu_bwd(const __nv_bfloat16* up, const __nv_bfloat16* gate, const __nv_bfloat16* dact,
                               __nv_bfloat16* dup, __nv_bfloat16* dgate, int64_t n, cudaStream_t st);
+cudaError_t launch_mse(const void* y, int y_dtype, const float* target, int64_t rows, int64_t cols, float* loss_rows,
+                       void* dy, int dy_dtype, cudaStream_t st);
 cudaError_t launch_xent(const __nv_bfloat16* logits, const int64_t* targets, int64_t rows, int V, float* loss_rows,
                         __nv_bfloat16* dlogits, cudaStream_t st);
 

@@ -2351,14 +2351,12 @@ cudaError_t launch_tt_dy(const __nv_bfloat16* dy, int64_t T, int64_t N, int H, i
   const dim3 grid(static_cast<unsigned>((M / DY_COLS) * H), static_cast<unsigned>(S));
   const size_t smem = sizeof(__nv_bfloat16) * (2 * DY_TT * DY_LDY + 2 * C * (DY_TT + 8) + C * (DY_COLS + 8)) +
                       sizeof(float) * (8 / (2 * (C / 8))) * DY_TT * C;
-  static bool attr8 = false, attr16 = false;
+  // the attribute is per device; setting it on every launch is cheap next to the kernel
   if (C == 8) {
-    if (!attr8) cudaFuncSetAttribute(k_tt_dy<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    attr8 = true;
+    cudaFuncSetAttribute(k_tt_dy<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     k_tt_dy<8><<<grid, 256, smem, s>>>(dy, T, N, H, M, Z, zs, Gd, dz_part, dg_part, S);
   } else {
-    if (!attr16) cudaFuncSetAttribute(k_tt_dy<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    attr16 = true;
+    cudaFuncSetAttribute(k_tt_dy<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     k_tt_dy<16><<<grid, 256, smem, s>>>(dy, T, N, H, M, Z, zs, Gd, dz_part, dg_part, S);
   }
   return cudaGetLastError();

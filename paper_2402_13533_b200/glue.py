@@ -12,7 +12,7 @@ import torch
 from . import _lib
 from .quant import _stream_ptr
 
-__all__ = ["rmsnorm", "rmsnorm_backward", "rope_", "swiglu", "swiglu_backward", "cross_entropy"]
+__all__ = ["rmsnorm", "rmsnorm_backward", "rope_", "swiglu", "swiglu_backward", "cross_entropy", "mse"]
 
 RMSNORM_EPS = 1e-5  # transformer.py:53
 
@@ -93,3 +93,20 @@ def cross_entropy(logits, targets):
     _lib.check(_lib.lib().qa_cross_entropy(logits.data_ptr(), t.data_ptr(), rows, vocab, loss_rows.data_ptr(),
                                            dl.data_ptr(), _stream_ptr(logits.device)), "qa_cross_entropy")
     return loss_rows.mean(), dl
+
+
+def mse(y, target, dy_dtype=None):
+    """(loss as a 0-d f32 tensor, dL/dy) of L = mean (y - target)^2 over y [rows, cols] (f32 or
+    bf16) and an f32 target of the same shape; dL/dy = 2 (y - target) / (rows * cols) in dy_dtype (y's dtype)."""
+    from .quant import _dtype_code
+
+    if tuple(y.shape) != tuple(target.shape):
+        raise ValueError(f"mse: y {tuple(y.shape)} vs target {tuple(target.shape)}")
+    y2 = y.reshape(-1, y.shape[-1]).contiguous()
+    t2 = target.reshape(-1, y.shape[-1]).to(torch.float32).contiguous()
+    rows, cols = y2.shape
+    loss_rows = torch.empty(rows, dtype=torch.float32, device=y.device)
+    dy = torch.empty(y2.shape, dtype=dy_dtype or y.dtype, device=y.device)
+    _lib.check(_lib.lib().qa_mse(y2.data_ptr(), _dtype_code(y2), t2.data_ptr(), rows, cols, loss_rows.data_ptr(),
+                                 dy.data_ptr(), _dtype_code(dy), _stream_ptr(y.device)), "qa_mse")
+    return loss_rows.sum() / (rows * cols), dy.reshape(y.shape)

@@ -232,11 +232,24 @@ def test_decoder_matches_reference_model_backward():
     assert not bad, (bad, max(errs.values()))
 
 
-def test_kv_decode_matches_full_forward_and_greedy(setup):
+def _f32_sdpa(q, k, v, is_causal=False):
+    s = (q.float() @ k.float().transpose(-1, -2)) / (q.shape[-1] ** 0.5)
+    if is_causal:
+        lq, lk = q.shape[-2], k.shape[-2]
+        s = s + torch.triu(torch.full((lq, lk), float("-inf"), device=q.device), 1)
+    return (torch.softmax(s, -1) @ v.float()).to(q.dtype)
+
+
+def test_kv_decode_matches_full_forward_and_greedy(setup, monkeypatch):
     """kv_decode_step (transformer.py:1043-1080) on the device: the logits of each cached one-token step equal the
-    matching position of a full forward over the prefix (the reference's own contract for the cache), within the
-    bf16 activation noise of two different attention kernels; greedy_decode with and without the cache agree."""
+    matching position of a full forward over the prefix (the reference's own contract for the cache).  Both paths
+    run the same float32 attention here, so what remains is the one-token linears' decode kernels against the
+    tcgen05 path (identical int32 products and epilogue): measured bit-identical logits at every position.  With
+    the library attention (flash causal vs one-query kernels) their bf16 noise compounds through the layers'
+    act-quant to ~5e-2.
+    greedy_decode with and without the cache agree."""
     model, tokens, _ = setup
+    monkeypatch.setattr(decoder.F, "scaled_dot_product_attention", _f32_sdpa)
     seq = tokens[0, :12].tolist()
     full = model.forward(torch.tensor([seq], device="cuda"))[0].float()
     cache = decoder.KvCache(model)
@@ -246,7 +259,7 @@ def test_kv_decode_matches_full_forward_and_greedy(setup):
         assert logits.shape == (CFG.vocab,) and logits.dtype == torch.float32
         errs.append(O.rel_err(logits.cpu().numpy(), full[i].cpu().numpy()))
     print("kv decode vs full forward:", " ".join(f"{e:.1e}" for e in errs))
-    assert max(errs) <= 3e-2, errs
+    assert max(errs) <= 1e-3, errs
     assert cache.current_len == 12
     with pytest.raises(decoder.ModelError, match="out of range"):
         decoder.kv_decode_step(model, cache, CFG.vocab)

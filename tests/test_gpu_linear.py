@@ -375,3 +375,37 @@ def test_decode_sized_batches(N, K, bits, r, spec):
         assert O.rel_err(_np(y), _np(big[:T])) <= 2 ** -7, T
         y32 = L.linear_forward(q, adapter, x[:T].float())
         assert O.rel_err(_np(y32), ref["y"]) <= 1e-4, T
+
+
+def test_config1_mse_training_step_matches_oracle():
+    """BASELINE config 1 end to end on the device: W 1024^2 ~N(0, 0.02) int8, x [4, 128, 1024] ~N(0, 1) fp32, the
+    balanced (4,16,16)^2 rank-8 tensor adapter with cores ~N(0, 0.01), forward, MSE to a seeded N(0, 1) target
+    (qa_mse: the loss and dL/dy), backward — loss, dy, dx and the core gradients against the oracle (SURVEY §8a A15:
+    the reference's loss is cross-entropy, so the oracle restates MSE)."""
+    from paper_2402_13533_b200 import glue
+
+    W = O.seeded_random(1024, 1024, 1, std=0.02)
+    X = O.seeded_random(512, 1024, 2).reshape(4, 128, 1024)
+    target = O.seeded_random(512, 1024, 3).reshape(4, 128, 1024)
+    spec = L.TTSpec.for_shape(1024, 1024, 8)
+    assert spec.m == (4, 16, 16) and spec.n == (4, 16, 16)
+    cores_np = O.tt_init_cores(O.TTShape(spec.m, spec.n, spec.ranks), 4, std=0.01)
+    q, oq = qa.quantize_rows(W, 8), O.quantize_rows(W, 8)
+    lin = L.TTLinear("w", L.QuantizedLinear("w.base", q), spec, [torch.from_numpy(c).cuda() for c in cores_np])
+    x = torch.from_numpy(X).cuda()
+    y = lin.forward(x)
+    assert y.shape == (4, 128, 1024) and y.dtype == torch.float32
+    loss, dy = glue.mse(y, torch.from_numpy(target).cuda())
+    ref_y = O.qa_linear_forward(X.reshape(512, 1024), oq, cores_np)["y"]
+    ref_loss = O.mse_loss(ref_y, target.reshape(512, 1024))
+    ref_dy = O.mse_grad(ref_y, target.reshape(512, 1024))
+    assert abs(float(loss) - ref_loss) <= 1e-5 * ref_loss
+    assert O.rel_err(_np(dy).reshape(512, 1024), ref_dy) <= 1e-4
+    grads = {}
+    dx = lin.backward(x, dy, grads)
+    ref = O.qa_linear_backward(X.reshape(512, 1024), ref_dy, oq, cores_np)
+    e_dx = O.rel_err(_np(dx).reshape(512, 1024), ref["dx"])
+    e_g = [O.rel_err(_np(grads[f"w.core{k}"]), ref["dcores"][k]) for k in range(3)]
+    print(f"config 1 MSE step: loss {float(loss):.6f} ({ref_loss:.6f}), dx {e_dx:.2e}, grads " +
+          " ".join(f"{e:.2e}" for e in e_g))
+    assert e_dx <= 1e-4 and max(e_g) <= TOL_GRAD_GENERIC
