@@ -700,16 +700,16 @@ def main():
         ws_bytes = max(ws_bytes, lib.qa_group_workspace_bytes(n, W, Tt, T))
         groups[gnames] = dict(n=n, W=W, T=Tt)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    # one flat buffer of every adapter-core gradient (linear order, then core order): the kernels write into its
+    # views and one collective averages it (dp.flat_views / dp.average_flat_, covered by tests/test_dp_gloo.py)
     flat_grad = torch.zeros(grad_numel, dtype=torch.float32, device=dev)
-    off = 0
+    grad_layout = [(f"{name}.core{i}", mats[name]["spec"].core_shape(i)) for name, _, _, _ in LINEARS
+                   for i in range(mats[name]["spec"].d)]
+    gviews = dp.flat_views(flat_grad, grad_layout)
     for name, n, k, kind in LINEARS:
         m = mats[name]
-        views = []
-        for i in range(m["spec"].d):
-            numel = int(torch.tensor(m["spec"].core_shape(i)).prod())
-            views.append(flat_grad[off: off + numel])
-            off += numel
-        m["gptr"] = (ctypes.c_void_p * _lib.QA_TT_MAX_D)(*[v.data_ptr() for v in views])
+        m["gptr"] = (ctypes.c_void_p * _lib.QA_TT_MAX_D)(
+            *[gviews[f"{name}.core{i}"].data_ptr() for i in range(m["spec"].d)])
 
     # every rank must hold the same frozen codes and adapter cores before the step (the state_signature check
     # of distsim.federated_round, distsim.py:293-296)
@@ -760,7 +760,7 @@ def main():
             if st:
                 _lib.check(st, f"backward {name}")
         if world > 1:
-            dp.allreduce_mean_(flat_grad)
+            dp.average_flat_(flat_grad)
 
     def step_grouped(xs, dys):
         for gnames in GROUPS_FWD:
@@ -792,7 +792,7 @@ def main():
             if st:
                 _lib.check(st, f"backward {gnames}")
         if world > 1:
-            dp.allreduce_mean_(flat_grad)
+            dp.average_flat_(flat_grad)
 
     def barrier():
         if world > 1:

@@ -154,6 +154,8 @@ class DecoderStack:
         # cores live in the optimizer's flat float32 buffer and the kernels accumulate their gradients
         # straight into its flat gradient buffer (no per-tensor gather / copy-back around the update)
         if getattr(state, "_bound_to", None) is not self:
+            if process_group is not None:  # replicas must start identical (distsim.py:293-296)
+                dp.check_replicas(self.adapters(), process_group)
             state._grad_views = state.bind(params)
             state._bound_to = self
         state.gflat.zero_()
@@ -166,10 +168,7 @@ class DecoderStack:
             loss, _ = self.train_step_grads(tokens[start:start + n], targets[start:start + n], grads=total)
             start += n
             loss_sum += loss
-        if micro_batches > 1:
-            state.gflat.div_(micro_batches)
-        if process_group is not None:
-            dp.allreduce_mean_(state.gflat, process_group)
+        dp.average_flat_(state.gflat, micro_batches, process_group)
         adamw_step(state, params, total, config or AdamWConfig())
         return loss_sum / micro_batches, state
 

@@ -24,6 +24,8 @@ __all__ = [
     "shard_tokens",
     "flatten_grads",
     "allreduce_mean_",
+    "average_flat_",
+    "flat_views",
     "average_grads",
     "state_signature",
     "check_replicas",
@@ -76,6 +78,30 @@ def allreduce_mean_(flat: torch.Tensor, group=None) -> torch.Tensor:
         dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
         flat.mul_(1.0 / world)
     return flat
+
+
+def flat_views(flat: torch.Tensor, named_shapes) -> dict:
+    """Views of one contiguous gradient buffer, laid out in the given (name, shape) order — the layout the
+    bench and the training step reduce with a single collective."""
+    views, off = {}, 0
+    for name, shape in named_shapes:
+        n = 1
+        for d in shape:
+            n *= int(d)
+        views[name] = flat[off:off + n].view(*shape)
+        off += n
+    if off != flat.numel():
+        raise ValueError(f"layout covers {off} of {flat.numel()} elements")
+    return views
+
+
+def average_flat_(flat: torch.Tensor, micro_batches: int = 1, group=None) -> torch.Tensor:
+    """The gradient exchange of one training step on a flat buffer, in place: the micro-batch average of
+    trainer.train_step (trainer.py:193-195), then the mean over the data-parallel replicas
+    (distsim.federated_round, distsim.py:309-314)."""
+    if micro_batches > 1:
+        flat.div_(micro_batches)
+    return allreduce_mean_(flat, group)
 
 
 def average_grads(grads: dict, group=None) -> dict:

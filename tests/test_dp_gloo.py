@@ -91,7 +91,47 @@ def _worker_divergence(rank, port, out):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("worker", [_worker_grads, _worker_divergence])
+def _worker_bench_layout(rank, port, out):
+    """The exact exchange of bench.py and DecoderStack.train_step: every adapter-core gradient of the linear set
+    lives in ONE flat buffer (dp.flat_views, linear order then core order), each rank fills its views from its
+    own token shard — micro-batch by micro-batch, accumulating like the kernels' accumulate flag — and
+    dp.average_flat_ (micro-batch mean, then the NCCL / gloo mean over replicas) leaves every view equal to the
+    reference's average over all chunks (trainer.py:193-195, distsim.py:309-314)."""
+    _setup(rank, port)
+    try:
+        rng = np.random.default_rng(1)
+        linears = [("wq", O.TTShape((1, 2, 8), (4, 2, 1), (1, 3, 3, 1))),
+                   ("wu", O.TTShape((1, 3, 8), (4, 2, 1), (1, 3, 3, 1))),
+                   ("wd", O.TTShape((1, 2, 8), (6, 2, 1), (1, 3, 3, 1)))]
+        cores = {nm: [rng.standard_normal(sh.core_shape(k)) for k in range(sh.d)] for nm, sh in linears}
+        tokens, micro = 16, 2
+        xs = {nm: rng.standard_normal((tokens, sh.K)) for nm, sh in linears}
+        dys = {nm: rng.standard_normal((tokens, sh.N)) for nm, sh in linears}
+        layout = [(f"{nm}.core{k}", sh.core_shape(k)) for nm, sh in linears for k in range(sh.d)]
+        flat = torch.zeros(sum(int(np.prod(s)) for _, s in layout), dtype=torch.float32)
+        views = dp.flat_views(flat, layout)
+        for nm, sh in linears:
+            x = dp.shard_tokens(torch.from_numpy(xs[nm]), rank, WORLD)
+            dy = dp.shard_tokens(torch.from_numpy(dys[nm]), rank, WORLD)
+            for mb in range(micro):  # micro-batches of this rank's shard
+                part = slice(mb * x.shape[0] // micro, (mb + 1) * x.shape[0] // micro)
+                _, g = O.tt_backward_staged(x[part].numpy(), dy[part].numpy(), cores[nm])
+                for k, gk in enumerate(g):
+                    views[f"{nm}.core{k}"] += torch.from_numpy(gk.astype(np.float32))
+        dp.average_flat_(flat, micro)
+        for nm, sh in linears:
+            _, gfull = O.tt_backward_staged(xs[nm], dys[nm], cores[nm])
+            for k, gk in enumerate(gfull):  # mean over WORLD * micro equal chunks
+                np.testing.assert_allclose(views[f"{nm}.core{k}"].numpy(), gk / (WORLD * micro), rtol=1e-5,
+                                           atol=1e-6)
+        with pytest.raises(ValueError):
+            dp.flat_views(flat, layout[:-1])
+        out[rank] = 1
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("worker", [_worker_grads, _worker_divergence, _worker_bench_layout])
 def test_two_rank_gloo(worker):
     port = _free_port()
     out = mp.Manager().dict()
