@@ -466,66 +466,74 @@ __global__ void __launch_bounds__(256, R == 8 ? 3 : 2) k_merge_fast(const float*
                                                        const float* __restrict__ scale,
                                                        const float* __restrict__ offset, OutT* __restrict__ out) {
   extern __shared__ __align__(16) float mf_smem[];
-  float* gs = mf_smem;             // [RT][R]: Gd[:, i] per tile row
-  float* g2s = mf_smem + RT * R;   // [R1][J1][R]: G2[:, h, :, :] (d = 3)
+  float* gs = mf_smem;               // [RT][R]: Gd[:, i] per tile row
+  float* ls = gs + RT * R;           // [MF_COLS][R]: L of the tile's columns (formed once per CTA)
+  float* so = ls + MF_COLS * R;      // [RT][2]: scale, offset per tile row
+  float* g2s = so + 2 * RT;          // [R1][J1][R]: G2[:, h, :, :] (d = 3)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t c0 = static_cast<int64_t>(blockIdx.x) * MF_COLS;
   const int64_t r0 = static_cast<int64_t>(blockIdx.y) * RT;
   const int64_t h = r0 / md;
   const int64_t i0 = r0 - h * md;
+  const int nrows = static_cast<int>(N - r0 < RT ? N - r0 : RT);
   for (int q = threadIdx.x; q < RT * R; q += 256) {
     const int rl = q / R, b = q - rl * R;
     gs[q] = Gd[static_cast<int64_t>(b) * md + i0 + rl];
   }
-  if (D3)
+  for (int q = threadIdx.x; q < RT; q += 256) {
+    const bool ok = codes != nullptr && q < nrows;
+    so[2 * q] = ok ? scale[r0 + q] : 0.f;
+    so[2 * q + 1] = ok ? offset[r0 + q] : 0.f;
+  }
+  if (D3) {
     for (int q = threadIdx.x; q < R1 * J1 * R; q += 256) {
       const int a = q / (J1 * R), rem = q - a * J1 * R;
       g2s[q] = G2[(static_cast<int64_t>(a) * H + h) * J1 * R + rem];
     }
+    __syncthreads();
+    // L[col, b] = Σ_a G1[j0, a] G2[a, h, j1, b] for the tile's columns, one (column, b) per thread pass
+    for (int q = threadIdx.x; q < MF_COLS * R; q += 256) {
+      const int cl = q / R, b = q - cl * R;
+      const int64_t cc = c0 + cl < K ? c0 + cl : 0;
+      const int64_t j0 = cc / J1;
+      const int j1 = static_cast<int>(cc - j0 * J1);
+      float acc = 0.f;
+      for (int a = 0; a < R1; ++a) acc = fmaf(__ldg(G1 + j0 * R1 + a), g2s[(a * J1 + j1) * R + b], acc);
+      ls[q] = acc;
+    }
+  } else {
+    for (int q = threadIdx.x; q < MF_COLS * R; q += 256) {
+      const int cl = q / R;
+      ls[q] = c0 + cl < K ? __ldg(G1 + (c0 + cl) * R + (q - cl * R)) : 0.f;
+    }
+  }
   __syncthreads();
   const int64_t col = c0 + lane * 4;
-  const bool active = col < K;
-  // L of the lane's 4 columns, as column pairs per rank: lp[b][0] = (col, col+1), lp[b][1] = (col+2, col+3)
+  if (col >= K) return;
+  // the lane's 4 columns as column pairs per rank: lp[b][0] = (col, col+1), lp[b][1] = (col+2, col+3)
   unsigned long long lp[R][2];
   {
+    const float4* l4 = reinterpret_cast<const float4*>(ls + lane * 4 * R);
     float lv[4][R];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < 4; ++c)
 #pragma unroll
-      for (int b = 0; b < R; ++b) lv[c][b] = 0.f;
-      const int64_t cc = active ? col + c : 0;
-      if (D3) {
-        const int64_t j0 = cc / J1;
-        const int j1 = static_cast<int>(cc - j0 * J1);
-        for (int a = 0; a < R1; ++a) {
-          const float g1 = __ldg(G1 + j0 * R1 + a);
-          const float* g2 = g2s + (a * J1 + j1) * R;
-#pragma unroll
-          for (int b = 0; b < R; ++b) lv[c][b] = fmaf(g1, g2[b], lv[c][b]);
-        }
-      } else {
-        const float4* g1 = reinterpret_cast<const float4*>(G1 + cc * R);
-#pragma unroll
-        for (int q = 0; q < R / 4; ++q) {
-          const float4 v = __ldg(g1 + q);
-          lv[c][4 * q] = v.x;
-          lv[c][4 * q + 1] = v.y;
-          lv[c][4 * q + 2] = v.z;
-          lv[c][4 * q + 3] = v.w;
-        }
+      for (int q = 0; q < R / 4; ++q) {
+        const float4 v = l4[c * (R / 4) + q];
+        lv[c][4 * q] = v.x;
+        lv[c][4 * q + 1] = v.y;
+        lv[c][4 * q + 2] = v.z;
+        lv[c][4 * q + 3] = v.w;
       }
-    }
 #pragma unroll
     for (int b = 0; b < R; ++b) {
       lp[b][0] = f2pack(lv[0][b], lv[1][b]);
       lp[b][1] = f2pack(lv[2][b], lv[3][b]);
     }
   }
-  if (!active) return;
   const int64_t cld = BITS == 8 ? K : (K + 1) / 2;
   const uint8_t* cbase = codes != nullptr ? codes + (BITS == 8 ? col : col / 2) : nullptr;
   OutT* obase = out + col;
-  const int nrows = static_cast<int>(N - r0 < RT ? N - r0 : RT);
   // the code words of the warp's next MF_UN rows are in flight while the current ones are processed
   auto load_codes = [&](int rb, uint32_t (&cw)[MF_UN]) {
 #pragma unroll
@@ -539,6 +547,7 @@ __global__ void __launch_bounds__(256, R == 8 ? 3 : 2) k_merge_fast(const float*
       }
     }
   };
+  const unsigned long long nm2 = f2pack(-8388608.f, -8388608.f);
   uint32_t cw[MF_UN], cn[MF_UN];
   load_codes(warp * MF_UN, cw);
   for (int rb = warp * MF_UN; rb < nrows; rb += 8 * MF_UN) {
@@ -547,7 +556,24 @@ __global__ void __launch_bounds__(256, R == 8 ? 3 : 2) k_merge_fast(const float*
     for (int u = 0; u < MF_UN; ++u) {
       const int rl = rb + u;
       if (rl >= nrows) break;
-      unsigned long long acc0 = 0ull, acc1 = 0ull;
+      // dequantised codes (code -> fp32 by the exponent-field trick, then code * scale + offset): the
+      // accumulators start from them and the W_t FMAs add on top
+      const float2 sv = *reinterpret_cast<const float2*>(so + 2 * rl);
+      const unsigned long long sc2 = f2pack(sv.x, sv.x), of2 = f2pack(sv.y, sv.y);
+      unsigned long long acc0, acc1;
+      {
+        const uint32_t w = cw[u];
+        uint32_t e0, e1, e2, e3;
+        if (BITS == 8) {
+          e0 = w & 0xFFu, e1 = (w >> 8) & 0xFFu, e2 = (w >> 16) & 0xFFu, e3 = w >> 24;
+        } else {
+          e0 = w & 0xFu, e1 = (w >> 4) & 0xFu, e2 = (w >> 8) & 0xFu, e3 = (w >> 12) & 0xFu;
+        }
+        const unsigned long long f01 = fadd2(f2pack(__uint_as_float(0x4B000000u | e0), __uint_as_float(0x4B000000u | e1)), nm2);
+        const unsigned long long f23 = fadd2(f2pack(__uint_as_float(0x4B000000u | e2), __uint_as_float(0x4B000000u | e3)), nm2);
+        acc0 = ffma2r(f01, sc2, of2);
+        acc1 = ffma2r(f23, sc2, of2);
+      }
       const float4* gr = reinterpret_cast<const float4*>(gs + rl * R);
 #pragma unroll
       for (int q = 0; q < R / 4; ++q) {
@@ -560,23 +586,14 @@ __global__ void __launch_bounds__(256, R == 8 ? 3 : 2) k_merge_fast(const float*
           ffma2(acc1, g2, lp[4 * q + e][1]);
         }
       }
-      float wt[4] = {f2lo(acc0), f2hi(acc0), f2lo(acc1), f2hi(acc1)};
-      const int64_t row = r0 + rl;
-      if (cbase != nullptr) {
-        const float sc = __ldg(scale + row), of = __ldg(offset + row);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const uint32_t c = BITS == 8 ? (cw[u] >> (8 * e)) & 0xFFu : (cw[u] >> (4 * e)) & 0xFu;
-          wt[e] += fmaf(static_cast<float>(c), sc, of);
-        }
-      }
-      OutT* dst = obase + row * K;
+      OutT* dst = obase + (r0 + rl) * K;
       if constexpr (sizeof(OutT) == 2) {
-        const __nv_bfloat162 a = __floats2bfloat162_rn(wt[0], wt[1]), b = __floats2bfloat162_rn(wt[2], wt[3]);
+        const __nv_bfloat162 a = __floats2bfloat162_rn(f2lo(acc0), f2hi(acc0));
+        const __nv_bfloat162 b = __floats2bfloat162_rn(f2lo(acc1), f2hi(acc1));
         *reinterpret_cast<uint2*>(dst) =
             make_uint2(*reinterpret_cast<const uint32_t*>(&a), *reinterpret_cast<const uint32_t*>(&b));
       } else {
-        *reinterpret_cast<float4*>(dst) = make_float4(wt[0], wt[1], wt[2], wt[3]);
+        *reinterpret_cast<float4*>(dst) = make_float4(f2lo(acc0), f2hi(acc0), f2lo(acc1), f2hi(acc1));
       }
     }
 #pragma unroll
@@ -711,7 +728,8 @@ cudaError_t launch_merge_fast(const TTDims& dd, const float* const* cores, const
   LaunchScope scope(kMerge, double(total) * ((codes ? (bits == 8 ? 1.0 : 0.5) : 0.0) + (out_dtype == QA_F32 ? 4 : 2)), s);
   count_launches(1);
   const dim3 grid(static_cast<unsigned>((dd.K + MF_COLS - 1) / MF_COLS), static_cast<unsigned>(dd.N / RT));
-  const size_t smem = sizeof(float) * (static_cast<size_t>(RT) * R + static_cast<size_t>(R1) * J1 * R);
+  const size_t smem =
+      sizeof(float) * (static_cast<size_t>(RT) * R + MF_COLS * R + 2 * RT + static_cast<size_t>(R1) * J1 * R);
   const float* G1 = cores[0];
   const float* G2 = d == 3 ? cores[1] : nullptr;
   const float* Gd = cores[d - 1];
