@@ -897,36 +897,50 @@ def main():
                     gd = groups[gnames]
                     dgroups[gnames] = (ctypes.c_void_p * gd["n"])(*[yd[g].data_ptr() for g in gnames])
 
-            def dstep():  # as a decoder layer calls them: q/k/v and up/gate as shared-input groups
+            def dstep(sp):  # as a decoder layer calls them: q/k/v and up/gate as shared-input groups
                 for gnames in GROUPS_FWD:
                     if len(gnames) == 1:
                         m = mats[gnames[0]]
                         _lib.check(lib.qa_linear_forward(ctypes.byref(m["wc"]), ctypes.byref(m["ttc"]),
                                                          xd[m["kind"]].data_ptr(), BF16, td, yd[gnames[0]].data_ptr(),
-                                                         None, None, None, ws.data_ptr(), ws_bytes, sptr),
+                                                         None, None, None, ws.data_ptr(), ws_bytes, sp),
                                    "decode forward")
                     else:
                         gd = groups[gnames]
                         _lib.check(lib.qa_group_forward(gd["n"], gd["W"], gd["T"], xd[gd["kind"]].data_ptr(), BF16, td,
-                                                        dgroups[gnames], None, None, ws.data_ptr(), ws_bytes, sptr),
+                                                        dgroups[gnames], None, None, ws.data_ptr(), ws_bytes, sp),
                                    "decode group forward")
 
-            for _ in range(5):
-                dstep()
-            torch.cuda.synchronize(dev)
-            d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            d0.record(stream)
-            for _ in range(50):
-                dstep()
-            d1.record(stream)
-            torch.cuda.synchronize(dev)
-            ms = d0.elapsed_time(d1) / 50
+            def timed(fn, n=50):
+                for _ in range(5):
+                    fn()
+                torch.cuda.synchronize(dev)
+                d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                d0.record(stream)
+                for _ in range(n):
+                    fn()
+                d1.record(stream)
+                torch.cuda.synchronize(dev)
+                return d0.elapsed_time(d1) / n
+
+            ms_eager = timed(lambda: dstep(sptr))
+            # the step captured once as a CUDA graph (programmatic-dependent edges included) and replayed: the
+            # decode loop of a serving engine, without the host's per-call launch latency
+            graph = torch.cuda.CUDAGraph()
+            gs = torch.cuda.Stream(dev)
+            gs.wait_stream(stream)
+            with torch.cuda.graph(graph, stream=gs):
+                dstep(gs.cuda_stream)
+            stream.wait_stream(gs)
+            ms = timed(graph.replay)
             wbytes = sum(mats[nm]["q"].codes.numel() + 8 * n for nm, n, _, _ in LINEARS)
             decode[f"tokens_{td}"] = {"ms_per_step": ms, "tokens_per_s": td / (ms / 1e3),
-                                      "weight_gbs": wbytes / ms / 1e6, "frac_of_hbm": wbytes / ms / 1e6 / peaks["hbm_gbs"]}
+                                      "weight_gbs": wbytes / ms / 1e6, "frac_of_hbm": wbytes / ms / 1e6 / peaks["hbm_gbs"],
+                                      "ms_per_step_host_issued": ms_eager}
         decode["note"] = ("forward of the 7 linears for 1 / 8 tokens (int8 codes + TT adapter; q/k/v and up/gate as "
                           "shared-input groups): act-quant prologue + tensor-core matrix-vector pass per linear, chained "
-                          "with programmatic dependent launches; weight_gbs counts the code bytes read per step")
+                          "with programmatic dependent launches, replayed as one CUDA graph (ms_per_step_host_issued: "
+                          "the same calls issued from the host each step); weight_gbs counts the code bytes read per step")
 
     # the merge kernel (north star step 6) on BASELINE config 5's 70B linear set (int4, TT r = 8), outside
     # the timed region: algorithmic bytes = codes in + bf16 W' out, CUDA events, warm

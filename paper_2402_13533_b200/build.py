@@ -18,7 +18,7 @@ from concurrent.futures import ThreadPoolExecutor
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libqadapter.so")
-SOURCES = ["quant_kernels.cu", "tt_kernels.cu", "tt_fast.cu", "gemm_tc.cu", "gemv.cu", "optim.cu", "glue.cu", "qmm.cu", "timing.cu", "capi.cu"]
+SOURCES = ["quant_kernels.cu", "tt_kernels.cu", "tt_dense.cu", "tt_fast.cu", "gemm_tc.cu", "gemv.cu", "optim.cu", "glue.cu", "qmm.cu", "timing.cu", "capi.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -55,12 +55,17 @@ struct LinearPlan {
   float* ox = nullptr;
   int32_t* rsx = nullptr;
   uint8_t* wcodes = nullptr;
-  float* z[QA_TT_MAX_D + 1] = {};  // Z_1..Z_{d-1}
-  float* y2 = nullptr;             // [T, N]
-  float* dz[2] = {};               // ping-pong dZ buffers (max Z size)
-  float* dxad = nullptr;           // [T, K]
-  float* partial = nullptr;
   int nchunks = 1;
+  // generic TT modes (tt_dense.cu): plane widths and buffers
+  int64_t Kg = 0, Ng = 0, Tg = 0, K2g = 0, N2g = 0, T2g = 0;
+  float* lpre = nullptr;          // prefix contraction of cores 0..d-2
+  float* wt32 = nullptr;          // W_t [N, K] fp32
+  __nv_bfloat16* b2 = nullptr;    // W_t (or W_tᵀ) term planes
+  __nv_bfloat16* a2 = nullptr;    // x (or dy) term planes
+  __nv_bfloat16* dyT = nullptr;   // dyᵀ term planes [N, T2g]
+  __nv_bfloat16* xT = nullptr;    // xᵀ term planes [K, T2g]
+  float* dw32 = nullptr;          // dW_t = dyᵀ x [N, K]
+  float* proj = nullptr;          // projection scratch
   __nv_bfloat16* wdt = nullptr;   // deq(W)ᵀ [K, Np]
   __nv_bfloat16* dyb = nullptr;   // dy padded [T, Np]
   __nv_bfloat16* wdt_lo = nullptr;  // fp32-input path: bf16 residuals of deq(W)ᵀ and dy
@@ -154,19 +159,27 @@ bool plan_linear(const qa_qweight* w, const TTDims* dd, int64_t T, void* ws, Lin
       P->g3p = b.take<float>(int64_t(P->HS) * P->TS * P->C * P->M);
     }
   } else if (dd != nullptr) {
-    int64_t zmax = 0;
-    for (int k = 1; k < dd->d; ++k) {
-      P->z[k] = b.take<float>(T * dd->zsize[k]);
-      zmax = std::max(zmax, dd->zsize[k]);
+    // generic modes: W_t materialised (fp32), its bf16 term planes as the GEMMs' extension operand, the
+    // activation planes beside it; dW_t = dyᵀ x and its projection onto the cores for the gradients
+    int64_t IP = 1, JP = 1;
+    for (int k = 0; k + 1 < dd->d; ++k) {
+      IP *= dd->m[k];
+      JP *= dd->n[k];
     }
-    P->y2 = b.take<float>(T * P->N);
-    P->dz[0] = b.take<float>(T * zmax);
-    P->dz[1] = b.take<float>(T * zmax);
-    P->dxad = b.take<float>(T * P->K);
-    int64_t gmax = 0;
-    for (int k = 0; k < dd->d; ++k) gmax = std::max(gmax, dd->core_numel(k));
-    P->nchunks = tt_grad_chunks(T);
-    P->partial = b.take<float>(gmax * P->nchunks);
+    P->Kg = round_up(P->K, 8);
+    P->Ng = round_up(P->N, 8);
+    P->Tg = round_up(T, 8);
+    P->K2g = round_up(3 * P->Kg, 64);
+    P->N2g = round_up(3 * P->Ng, 64);
+    P->T2g = round_up(3 * P->Tg, 64);
+    P->lpre = b.take<float>(IP * JP * dd->r[dd->d - 1]);
+    P->wt32 = b.take<float>(P->N * P->K);
+    P->b2 = b.take<__nv_bfloat16>(std::max(P->N * P->K2g, P->K * P->N2g));
+    P->a2 = b.take<__nv_bfloat16>(T * std::max(P->K2g, P->N2g));
+    P->dyT = b.take<__nv_bfloat16>(P->N * P->T2g);
+    P->xT = b.take<__nv_bfloat16>(P->K * P->T2g);
+    P->dw32 = b.take<float>(P->N * P->K);
+    P->proj = b.take<float>(static_cast<int64_t>(tt_project_ws_floats(*dd)));
   }
   P->wdt = b.take<__nv_bfloat16>(P->K * P->Np);
   P->dyb = b.take<__nv_bfloat16>(T * P->Np);
@@ -524,22 +537,20 @@ int linear_forward_impl(const qa_qweight* w, const qa_tt* tt, const void* x, int
   const uint8_t* wop = weight_operand(w, P, s, &st);
   QA_TRY(st);
 
-  // (4) generic TT adapter y2 = x · W_tᵀ via the left-to-right stage chain
+  // (4) generic TT adapter: y2 = x · W_tᵀ with W_t materialised once per call (O(N K r), token-independent) and
+  // the product run as fp32-class extension k-blocks of the int8 GEMM: [x_hi | x_lo | x_hi] · [W_hi | W_hi | W_lo]
   float* y2 = nullptr;
   if (pd != nullptr && ext.K2 == 0) {
-    y2 = y2_f32 != nullptr ? y2_f32 : P.y2;
-    const void* zin = x;
-    int zin_dtype = x_dtype;
-    int64_t zin_ld = K;
-    for (int k = 0; k < dd.d; ++k) {
-      float* zout = (k == dd.d - 1) ? y2 : P.z[k + 1];
-      QA_TRY_CUDA(launch_tt_stage_fwd(zin, zin_dtype, zin_ld, tt->cores[k], zout, dd.zsize[k + 1], T, dd.I(k),
-                                      dd.r[k], dd.n[k], dd.J(k + 1), dd.m[k], dd.r[k + 1], s),
-                  "tt stage fwd");
-      zin = zout;
-      zin_dtype = QA_F32;
-      zin_ld = dd.zsize[k + 1];
-    }
+    QA_TRY_CUDA(launch_tt_prefix_full(dd, tt->cores, P.lpre, s), "tt prefix");
+    QA_TRY_CUDA(launch_tt_last_full(dd, P.lpre, tt->cores[dd.d - 1], nullptr, 8, nullptr, nullptr, P.wt32, QA_F32, s),
+                "tt materialize");
+    QA_TRY_CUDA(launch_split3_rows(P.wt32, QA_F32, N, K, K, P.b2, P.K2g, P.Kg, kPlanesHiHiLo, s), "W_t planes");
+    QA_TRY_CUDA(launch_split3_rows(x, x_dtype, T, K, K, P.a2, P.K2g, P.Kg, kPlanesHiLoHi, s), "x planes");
+    ext.A2 = P.a2;
+    ext.lda2 = P.K2g;
+    ext.B2 = P.b2;
+    ext.ldb2 = P.K2g;
+    ext.K2 = P.K2g;
   }
 
   // (3) int8 tcgen05 GEMM with the dequantising epilogue (+ y2)
@@ -611,7 +622,6 @@ int linear_backward_impl(const qa_qweight* w, const qa_tt* tt, const void* x, in
   const int64_t T = tokens, N = P.N, K = P.K;
   const bool want_dx = dx != nullptr || dx_f32 != nullptr;
 
-  float* dxad = nullptr;
   GemmExt ext;
   // bf16 view of dy: the dX GEMM operand and the fast dy pass read it through 16-byte copies
   const void* dyb16 = dy;
@@ -734,38 +744,29 @@ int linear_backward_impl(const qa_qweight* w, const qa_tt* tt, const void* x, in
     }
     }  // !P.fused
   } else if (pd != nullptr) {
-    // (5) recompute Z_1..Z_{d-1} from the stored layer input
-    for (int k = 0; k + 1 < dd.d; ++k) {
-      const void* zin = k == 0 ? x : static_cast<const void*>(P.z[k]);
-      QA_TRY_CUDA(launch_tt_stage_fwd(zin, k == 0 ? x_dtype : QA_F32, k == 0 ? K : dd.zsize[k], tt->cores[k],
-                                      P.z[k + 1], dd.zsize[k + 1], T, dd.I(k), dd.r[k], dd.n[k], dd.J(k + 1),
-                                      dd.m[k], dd.r[k + 1], s),
-                  "tt recompute");
+    // generic modes (tt_dense.cu): W_t materialised once; the adapter dx = dy · W_t rides as extension k-blocks of
+    // the dX GEMM, dW_t = dyᵀ · x runs on tcgen05 and is projected onto every core (no per-token stage chain)
+    QA_TRY_CUDA(launch_tt_prefix_full(dd, tt->cores, P.lpre, s), "tt prefix");
+    QA_TRY_CUDA(launch_tt_last_full(dd, P.lpre, tt->cores[dd.d - 1], nullptr, 8, nullptr, nullptr, P.wt32, QA_F32, s),
+                "tt materialize");
+    if (dcores != nullptr) {
+      QA_TRY_CUDA(launch_split3_t(dy, dy_dtype, T, N, N, P.dyT, P.T2g, P.Tg, kPlanesHiLoHi, s), "dy planes");
+      QA_TRY_CUDA(launch_split3_t(x, x_dtype, T, K, K, P.xT, P.T2g, P.Tg, kPlanesHiHiLo, s), "x planes");
+      GemmEpilogue eg;
+      eg.out_f32 = P.dw32;
+      eg.ld_f32 = K;
+      QA_TRY(gemm_tc(1, P.dyT, P.T2g, P.xT, P.T2g, N, K, P.T2g, eg, s));
+      QA_TRY_CUDA(launch_tt_project(dd, tt->cores, P.dw32, P.proj, dcores, accumulate != 0, s), "project dW_t");
     }
-    // walk the stages right to left: dG_k from (Z_k, dZ_{k+1}); dZ_k = stage_bwd(dZ_{k+1})
-    const void* cur = dy;
-    int cur_dtype = dy_dtype;
-    int64_t cur_ld = N;
-    for (int k = dd.d - 1; k >= 0; --k) {
-      const void* zin = k == 0 ? x : static_cast<const void*>(P.z[k]);
-      const int zin_dtype = k == 0 ? x_dtype : QA_F32;
-      const int64_t zin_ld = k == 0 ? K : dd.zsize[k];
-      if (dcores != nullptr && dcores[k] != nullptr) {
-        QA_TRY_CUDA(launch_tt_core_grad(zin, zin_dtype, zin_ld, cur, cur_dtype, cur_ld, P.partial, P.nchunks,
-                                        dcores[k], accumulate != 0, T, dd.I(k), dd.r[k], dd.n[k], dd.J(k + 1),
-                                        dd.m[k], dd.r[k + 1], s),
-                    "tt core grad");
-      }
-      if (k == 0 && !want_dx) break;
-      float* next = k == 0 ? P.dxad : P.dz[k & 1];
-      QA_TRY_CUDA(launch_tt_stage_bwd(cur, cur_dtype, cur_ld, tt->cores[k], next, dd.zsize[k], T, dd.I(k), dd.r[k],
-                                      dd.n[k], dd.J(k + 1), dd.m[k], dd.r[k + 1], s),
-                  "tt stage bwd");
-      cur = next;
-      cur_dtype = QA_F32;
-      cur_ld = dd.zsize[k];
+    if (want_dx) {
+      QA_TRY_CUDA(launch_split3_t(P.wt32, QA_F32, N, K, K, P.b2, P.N2g, P.Ng, kPlanesHiHiLo, s), "W_t planes");
+      QA_TRY_CUDA(launch_split3_rows(dy, dy_dtype, T, N, N, P.a2, P.N2g, P.Ng, kPlanesHiLoHi, s), "dy planes");
+      ext.A2 = P.a2;
+      ext.lda2 = P.N2g;
+      ext.B2 = P.b2;
+      ext.ldb2 = P.N2g;
+      ext.K2 = P.N2g;
     }
-    if (want_dx) dxad = P.dxad;
   }
 
   if (want_dx) {
@@ -781,11 +782,9 @@ int linear_backward_impl(const qa_qweight* w, const qa_tt* tt, const void* x, in
                 "dequantize T");
     const void* a = dyb16;
     const int64_t lda = ld_dyb;
-    const float* addend = dxad;
+    const float* addend = nullptr;
     if (f32_path) {
       GemmEpilogue e1;
-      e1.addend = dxad;
-      e1.ld_add = K;
       e1.out_f32 = P.dxacc;
       e1.ld_f32 = K;
       QA_TRY(gemm_tc(1, P.dyb_lo, P.Np, P.wdt, P.Np, T, K, P.Np, e1, s));

@@ -61,6 +61,18 @@ cudaError_t launch_tt_last_full(const TTDims& dd, const float* L, const float* G
                                 int bits, const float* scale, const float* offset, void* out, int out_dtype,
                                 cudaStream_t s);
 
+// generic TT modes through the materialised W_t (tt_dense.cu): bf16 term planes of a matrix / of its transpose
+// (order bit p set = plane p holds the lo term), and the projection of dW_t onto every core's gradient
+cudaError_t launch_split3_rows(const void* in, int in_dtype, int64_t rows, int64_t cols, int64_t ldin,
+                               __nv_bfloat16* out, int64_t ld_out, int64_t plane_w, int order, cudaStream_t s);
+cudaError_t launch_split3_t(const void* in, int in_dtype, int64_t rows, int64_t cols, int64_t ldin,
+                            __nv_bfloat16* out, int64_t ld_out, int64_t plane_w, int order, cudaStream_t s);
+size_t tt_project_ws_floats(const TTDims& dd);
+cudaError_t launch_tt_project(const TTDims& dd, const float* const* cores, const float* dW, float* ws,
+                              float* const* dcores, bool accumulate, cudaStream_t s);
+constexpr int kPlanesHiLoHi = 2;  // planes (hi, lo, hi): the activation side
+constexpr int kPlanesHiHiLo = 4;  // planes (hi, hi, lo): the weight side
+
 // Fused merge / materialise for the fast TT family (no prefix pass): out = W_t (+ deq(codes) when codes != NULL)
 bool merge_fast_ok(const TTDims& dd, const void* codes, const void* out);
 cudaError_t launch_merge_fast(const TTDims& dd, const float* const* cores, const uint8_t* codes, int bits,
