@@ -457,8 +457,9 @@ MERGE_70B = [("wq", 8192, 8192), ("wk", 1024, 8192), ("wv", 1024, 8192), ("wo", 
 
 
 def measure_merge(dev, sptr, hbm_gbs, iters=5):
-    """qa_merge (W' = dequantize_rows(q) + W_t, lowrank.py:245-257) over the config-5 70B set, int4, r = 8,
-    bf16 W'; one matrix resident at a time."""
+    """qa_merge (W' = dequantize_rows(q) + W_t, lowrank.py:245-257) over the config-5 70B set, int4, r = 8; one
+    matrix resident at a time.  The headline is the fp32 W' the reference's lora_merge returns (numpy float32
+    dense weights, lowrank.py:254-257); the bf16 W' (the serving dtype) is reported beside it."""
     import torch
 
     from paper_2402_13533_b200 import _lib
@@ -466,38 +467,42 @@ def measure_merge(dev, sptr, hbm_gbs, iters=5):
     from paper_2402_13533_b200.quant import quantize_rows
 
     lib = _lib.lib()
-    g = torch.Generator(device=dev).manual_seed(7)
-    tot_ms, tot_bytes = 0.0, 0.0
-    for name, n, k in MERGE_70B:
-        w = torch.randn((n, k), generator=g, device=dev) * 0.02
-        q = quantize_rows(w, 4)
-        del w
-        spec = TTSpec.for_shape(n, k, 8)
-        cores = [torch.randn(spec.core_shape(i), generator=g, device=dev) * 0.01 for i in range(spec.d)]
-        wc, ttc = q.as_c(), spec.as_c(cores)
-        wsm = torch.empty(max(lib.qa_merge_workspace_bytes(ctypes.byref(ttc)), 16), dtype=torch.uint8, device=dev)
-        out = torch.empty((n, k), dtype=torch.bfloat16, device=dev)
+    res = {}
+    for odt, code, tag in ((torch.float32, _lib.QA_F32, "f32"), (torch.bfloat16, _lib.QA_BF16, "bf16")):
+        g = torch.Generator(device=dev).manual_seed(7)
+        tot_ms, tot_bytes = 0.0, 0.0
+        for name, n, k in MERGE_70B:
+            w = torch.randn((n, k), generator=g, device=dev) * 0.02
+            q = quantize_rows(w, 4)
+            del w
+            spec = TTSpec.for_shape(n, k, 8)
+            cores = [torch.randn(spec.core_shape(i), generator=g, device=dev) * 0.01 for i in range(spec.d)]
+            wc, ttc = q.as_c(), spec.as_c(cores)
+            wsm = torch.empty(max(lib.qa_merge_workspace_bytes(ctypes.byref(ttc)), 16), dtype=torch.uint8,
+                              device=dev)
+            out = torch.empty((n, k), dtype=odt, device=dev)
 
-        def run():
-            _lib.check(lib.qa_merge(ctypes.byref(wc), ctypes.byref(ttc), out.data_ptr(), _lib.QA_BF16,
-                                    wsm.data_ptr(), wsm.numel(), sptr), "qa_merge")
+            def run():
+                _lib.check(lib.qa_merge(ctypes.byref(wc), ctypes.byref(ttc), out.data_ptr(), code, wsm.data_ptr(),
+                                        wsm.numel(), sptr), "qa_merge")
 
-        run()
-        torch.cuda.synchronize(dev)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(iters):
             run()
-        e1.record()
-        torch.cuda.synchronize(dev)
-        tot_ms += e0.elapsed_time(e1) / iters
-        tot_bytes += n * k * 0.5 + n * k * 2 + 8 * n + 4 * spec.param_count()
-        del q, out, wsm, cores
-    gbs = tot_bytes / tot_ms / 1e6
-    return {"set": "llama2-70b linears (q/o 8192^2, k/v 1024x8192, gate/up 28672x8192, down 8192x28672), int4, "
-                   "TT r=8, bf16 W'", "ms": tot_ms, "bytes": tot_bytes, "achieved_gbs": gbs,
-            "frac_of_hbm": gbs / hbm_gbs, "kernels": "k_prefix_d3 + k_merge_nd1"}
-
+            torch.cuda.synchronize(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(iters):
+                run()
+            e1.record()
+            torch.cuda.synchronize(dev)
+            tot_ms += e0.elapsed_time(e1) / iters
+            tot_bytes += n * k * 0.5 + n * k * out.element_size() + 8 * n + 4 * spec.param_count()
+            del q, out, wsm, cores
+        gbs = tot_bytes / tot_ms / 1e6
+        res[tag] = {"ms": tot_ms, "bytes": tot_bytes, "achieved_gbs": gbs, "frac_of_hbm": gbs / hbm_gbs}
+    out = {"set": "llama2-70b linears (q/o 8192^2, k/v 1024x8192, gate/up 28672x8192, down 8192x28672), int4, "
+                  "TT r=8, fp32 W' (the reference's dtype)", **res["f32"], "kernels": "k_merge_fast"}
+    out["bf16_out"] = res["bf16"]
+    return out
 
 
 def measure_weight_quantize(dev, sptr, hbm_gbs, linears, bits, iters=5):

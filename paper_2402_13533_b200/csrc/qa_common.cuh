@@ -332,6 +332,12 @@ QA_DEV void cp_async16(void* smem, const void* gmem, bool pred) {
                "r"(pred ? 16 : 0)
                : "memory");
 }
+// 4- or 8-byte asynchronous global -> shared copy (cached in L1: .ca is the only form below 16 bytes)
+template <int BYTES>
+QA_DEV void cp_async_ca(uint32_t smem, const void* gmem) {
+  static_assert(BYTES == 4 || BYTES == 8 || BYTES == 16, "cp.async size");
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem), "l"(gmem), "n"(BYTES) : "memory");
+}
 QA_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 QA_DEV void cp_async_wait() {

@@ -9,6 +9,7 @@
 // (I = Π_{q<k} m_q, Q = Π_{q>k} n_q).  The core gradient reduction is two-phase with a fixed
 // summation order, so results are bit-reproducible run to run (the reference's determinism
 // contract, distsim.py:312).
+#include <cmath>
 #include "qa_common.cuh"
 #include "qa_internal.h"
 #include "qa_timing.h"
@@ -451,153 +452,241 @@ __global__ void __launch_bounds__(256, 2) k_merge_nd1(const float* __restrict__ 
 // Llama modes m = (1, H, M), n = (J0, J1, 1), and LoRA, m = (1, N), n = (K, 1)):
 //   W'[row, col] = code·scale[row] + offset[row] + Σ_b L[col, b] · Gd[b, i],   row = h·md + i
 //   d = 3: L[col, b] = Σ_a G1[j0, a] · G2[a, h, j1, b]  (col = j0·J1 + j1);  d = 2: L[col, b] = G1[col, b]
-// A CTA owns RT rows of one h-block and 128 columns; every lane holds its 4 columns' L (R x 4 fp32, formed
-// in registers from G1 and the h-slice of G2 staged in shared memory — no prefix pass, no L buffer) and walks
-// the rows of its warp: Gd[:, i] as two broadcast 16-byte shared loads, 2R packed FMAs, the 4 codes (2 or 4
-// bytes, prefetched UN rows ahead), one fp32 FMA dequantisation per element (< 1 ulp of the reference's fp64
-// route, quant.py:102-105), one 8- or 16-byte store (a warp writes 256 / 512 contiguous bytes per row).
-constexpr int MF_COLS = 128, MF_UN = 8;
+// A CTA owns RT rows of one h-block (RT divides md, so every row of the tile exists) and 32·CPL columns,
+// CPL = 64 / R (8 for r = 8, 4 for r = 16).  The prologue stages Gd[:, i] and scale / offset per tile row and
+// forms L for the tile's columns (one thread per column, all R values); then every lane holds its CPL columns'
+// L as R x CPL/2 packed pairs (64 registers) and walks RT/4 consecutive rows of its warp with no predicates:
+// the code word (prefetched MF_UN rows ahead), codes -> fp32 by one byte permute into the 2^23 exponent field
+// and a packed subtract, one packed FMA dequantisation per column pair (< 1 ulp of the reference's fp64
+// route, quant.py:102-105), R packed FMAs per column pair on a broadcast Gd value, one 16-byte store (a warp
+// writes 512 contiguous bytes per row in bf16).
+template <int R>
+__host__ __device__ constexpr int mf_cpl() { return 64 / R; }
+template <int R>
+__host__ __device__ constexpr int mf_cols() { return 32 * mf_cpl<R>(); }
+
+// code bytes of a lane's CPL columns in one row (2, 4 or 8), and the code-row ring per warp: MF_SLOTS batches of
+// MF_UN rows in flight as cp.async copies (no registers held), so each SM keeps 16-64 KB of code reads in flight
+// while the stores stream out
+template <int BITS, int CPL>
+__host__ __device__ constexpr int mf_lane_bytes() { return CPL * BITS / 8; }
+constexpr int MF_SLOTS = 4, MF_UN = 8;
+
+constexpr int MF_THREADS = 128;  // 4 warps: 4 CTAs (16 warps) per SM at <= 128 registers
 
 template <typename OutT, int BITS, int R, bool D3>
-__global__ void __launch_bounds__(256, R == 8 ? 3 : 2) k_merge_fast(const float* __restrict__ G1, const float* __restrict__ G2,
-                                                       const float* __restrict__ Gd, int R1, int J1, int H,
-                                                       int64_t md, int64_t N, int64_t K, int RT,
-                                                       const uint8_t* __restrict__ codes,
-                                                       const float* __restrict__ scale,
-                                                       const float* __restrict__ offset, OutT* __restrict__ out) {
+__global__ void __launch_bounds__(MF_THREADS, 4) k_merge_fast(const float* __restrict__ G1, const float* __restrict__ G2,
+                                                             const float* __restrict__ Gd, int R1, int J1, int H,
+                                                             int64_t md, int64_t N, int64_t K, int RT,
+                                                             const uint8_t* __restrict__ codes,
+                                                             const float* __restrict__ scale,
+                                                             const float* __restrict__ offset, OutT* __restrict__ out) {
+  constexpr int CPL = mf_cpl<R>(), COLS = mf_cols<R>(), NP = CPL / 2, NWARP = MF_THREADS / 32;
+  constexpr int LB = mf_lane_bytes<BITS, CPL>();  // code bytes per lane and row
+  constexpr int CB = LB < 4 ? 4 : LB;               // bytes per copy (an even lane copies its pair when LB = 2)
+  constexpr int NW = LB > 4 ? 2 : 1;
+  constexpr int SLOT = MF_UN * 32 * LB;
   extern __shared__ __align__(16) float mf_smem[];
-  float* gs = mf_smem;               // [RT][R]: Gd[:, i] per tile row
-  float* ls = gs + RT * R;           // [MF_COLS][R]: L of the tile's columns (formed once per CTA)
-  float* so = ls + MF_COLS * R;      // [RT][2]: scale, offset per tile row
-  float* g2s = so + 2 * RT;          // [R1][J1][R]: G2[:, h, :, :] (d = 3)
+  float* gs = mf_smem;           // [RT][R]: Gd[:, i] per tile row
+  float* ls = gs + RT * R;       // [COLS][R]: L of the tile's columns (formed once per CTA)
+  float* so = ls + COLS * R;     // [RT][2]: scale, offset per tile row
+  float* g2s = so + 2 * RT;      // [R1][J1][R]: G2[:, h, :, :] (d = 3)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t c0 = static_cast<int64_t>(blockIdx.x) * MF_COLS;
+  // [NWARP][MF_SLOTS][MF_UN][32 lanes][LB]: this warp's code ring
+  const uint32_t ring = smem_u32(g2s + R1 * J1 * R) + static_cast<uint32_t>(warp * MF_SLOTS * SLOT);
+  const int64_t c0 = static_cast<int64_t>(blockIdx.x) * COLS;
   const int64_t r0 = static_cast<int64_t>(blockIdx.y) * RT;
   const int64_t h = r0 / md;
   const int64_t i0 = r0 - h * md;
-  const int nrows = static_cast<int>(N - r0 < RT ? N - r0 : RT);
-  for (int q = threadIdx.x; q < RT * R; q += 256) {
-    const int rl = q / R, b = q - rl * R;
-    gs[q] = Gd[static_cast<int64_t>(b) * md + i0 + rl];
+  const int64_t col = c0 + lane * CPL;
+  const bool live = col < K;
+  const int64_t cld = BITS == 8 ? K : K / 2;
+  const int rpw = RT / NWARP;  // consecutive rows of this warp
+  const int rw0 = warp * rpw;
+  const uint8_t* cp = codes != nullptr && live && (LB >= 4 || (lane & 1) == 0)
+                          ? codes + (r0 + rw0) * cld + (BITS == 8 ? col : col / 2)
+                          : nullptr;
+  const int nb = rpw / MF_UN;
+  // batch i of this warp's rows into ring slot i % MF_SLOTS; every lane commits a (possibly empty) group
+  auto issue = [&](int i) {
+    if (cp != nullptr && i < nb) {
+      const uint32_t slot = ring + static_cast<uint32_t>((i % MF_SLOTS) * SLOT + lane * LB);
+#pragma unroll
+      for (int u = 0; u < MF_UN; ++u) cp_async_ca<CB>(slot + u * 32 * LB, cp + (static_cast<int64_t>(i) * MF_UN + u) * cld);
+    }
+    cp_async_commit();
+  };
+  // Prologue, one round trip: Gd[:, i] / scale / offset / G2[:, h] as cp.async copies (committed first), the
+  // first code batches behind them, and this thread's G1 rows in registers, all in flight at once.
+#pragma unroll
+  for (int b = 0; b < R; ++b)  // coalesced along the rows of Gd
+    for (int rl = threadIdx.x; rl < RT; rl += MF_THREADS)
+      cp_async_ca<4>(smem_u32(gs + rl * R + b), Gd + static_cast<int64_t>(b) * md + i0 + rl);
+  for (int rl = threadIdx.x; rl < RT; rl += MF_THREADS) {
+    if (codes != nullptr) {
+      cp_async_ca<4>(smem_u32(so + 2 * rl), scale + r0 + rl);
+      cp_async_ca<4>(smem_u32(so + 2 * rl + 1), offset + r0 + rl);
+    } else {
+      *reinterpret_cast<float2*>(so + 2 * rl) = make_float2(0.f, 0.f);
+    }
   }
-  for (int q = threadIdx.x; q < RT; q += 256) {
-    const bool ok = codes != nullptr && q < nrows;
-    so[2 * q] = ok ? scale[r0 + q] : 0.f;
-    so[2 * q + 1] = ok ? offset[r0 + q] : 0.f;
-  }
-  if (D3) {
-    for (int q = threadIdx.x; q < R1 * J1 * R; q += 256) {
+  if (D3)
+    for (int q = threadIdx.x; q < R1 * J1 * R; q += MF_THREADS) {
       const int a = q / (J1 * R), rem = q - a * J1 * R;
-      g2s[q] = G2[(static_cast<int64_t>(a) * H + h) * J1 * R + rem];
+      cp_async_ca<4>(smem_u32(g2s + q), G2 + (static_cast<int64_t>(a) * H + h) * J1 * R + rem);
     }
-    __syncthreads();
-    // L[col, b] = Σ_a G1[j0, a] G2[a, h, j1, b] for the tile's columns, one (column, b) per thread pass
-    for (int q = threadIdx.x; q < MF_COLS * R; q += 256) {
-      const int cl = q / R, b = q - cl * R;
-      const int64_t cc = c0 + cl < K ? c0 + cl : 0;
+  cp_async_commit();
+#pragma unroll
+  for (int i = 0; i < MF_SLOTS - 1; ++i) issue(i);
+  // G1 rows of this thread's L columns (one thread per column; R1 <= 16 values each for d = 3, R for d = 2)
+  constexpr int NCT = COLS / MF_THREADS;
+  constexpr int G1N = D3 ? 16 : R;
+  float g1v[NCT][G1N];
+  int j1c[NCT];
+#pragma unroll
+  for (int k = 0; k < NCT; ++k) {
+    const int cl = static_cast<int>(threadIdx.x) + k * MF_THREADS;
+    const int64_t cc = c0 + cl < K ? c0 + cl : 0;
+    if (D3) {
       const int64_t j0 = cc / J1;
-      const int j1 = static_cast<int>(cc - j0 * J1);
-      float acc = 0.f;
-      for (int a = 0; a < R1; ++a) acc = fmaf(__ldg(G1 + j0 * R1 + a), g2s[(a * J1 + j1) * R + b], acc);
-      ls[q] = acc;
+      j1c[k] = static_cast<int>(cc - j0 * J1);
+#pragma unroll
+      for (int a = 0; a < G1N; ++a) g1v[k][a] = a < R1 ? __ldg(G1 + j0 * R1 + a) : 0.f;
+    } else {
+      j1c[k] = 0;
+#pragma unroll
+      for (int b = 0; b < G1N; ++b) g1v[k][b] = __ldg(G1 + cc * R + b);
     }
-  } else {
-    for (int q = threadIdx.x; q < MF_COLS * R; q += 256) {
-      const int cl = q / R;
-      ls[q] = c0 + cl < K ? __ldg(G1 + (c0 + cl) * R + (q - cl * R)) : 0.f;
+  }
+  cp_async_wait<MF_SLOTS - 1>();  // the prologue group (the code batches may still be in flight)
+  __syncthreads();
+  // L for the tile's columns, every rank index (same summation order as the prefix)
+#pragma unroll
+  for (int k = 0; k < NCT; ++k) {
+    const int cl = static_cast<int>(threadIdx.x) + k * MF_THREADS;
+    float acc[R];
+    if (D3) {
+#pragma unroll
+      for (int b = 0; b < R; ++b) acc[b] = 0.f;
+#pragma unroll
+      for (int a = 0; a < G1N; ++a) {
+        if (a >= R1) break;
+        const float4* g2 = reinterpret_cast<const float4*>(g2s + (a * J1 + j1c[k]) * R);
+#pragma unroll
+        for (int b4 = 0; b4 < R / 4; ++b4) {
+          const float4 t = g2[b4];
+          acc[4 * b4] = fmaf(g1v[k][a], t.x, acc[4 * b4]);
+          acc[4 * b4 + 1] = fmaf(g1v[k][a], t.y, acc[4 * b4 + 1]);
+          acc[4 * b4 + 2] = fmaf(g1v[k][a], t.z, acc[4 * b4 + 2]);
+          acc[4 * b4 + 3] = fmaf(g1v[k][a], t.w, acc[4 * b4 + 3]);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int b = 0; b < R; ++b) acc[b] = g1v[k][b];
     }
+#pragma unroll
+    for (int b = 0; b < R; b += 4)
+      *reinterpret_cast<float4*>(ls + cl * R + b) = make_float4(acc[b], acc[b + 1], acc[b + 2], acc[b + 3]);
   }
   __syncthreads();
-  const int64_t col = c0 + lane * 4;
-  if (col >= K) return;
-  // the lane's 4 columns as column pairs per rank: lp[b][0] = (col, col+1), lp[b][1] = (col+2, col+3)
-  unsigned long long lp[R][2];
-  {
-    const float4* l4 = reinterpret_cast<const float4*>(ls + lane * 4 * R);
-    float lv[4][R];
+  const unsigned live_mask = __ballot_sync(0xffffffffu, live);
+  if (!live) return;
+  // the lane's CPL columns as column pairs per rank: lp[b][p] = (col + 2p, col + 2p + 1)
+  unsigned long long lp[R][NP];
 #pragma unroll
-    for (int c = 0; c < 4; ++c)
+  for (int p = 0; p < NP; ++p)
 #pragma unroll
-      for (int q = 0; q < R / 4; ++q) {
-        const float4 v = l4[c * (R / 4) + q];
-        lv[c][4 * q] = v.x;
-        lv[c][4 * q + 1] = v.y;
-        lv[c][4 * q + 2] = v.z;
-        lv[c][4 * q + 3] = v.w;
-      }
-#pragma unroll
-    for (int b = 0; b < R; ++b) {
-      lp[b][0] = f2pack(lv[0][b], lv[1][b]);
-      lp[b][1] = f2pack(lv[2][b], lv[3][b]);
+    for (int b4 = 0; b4 < R / 4; ++b4) {
+      const float4 u = *reinterpret_cast<const float4*>(ls + (lane * CPL + 2 * p) * R + 4 * b4);
+      const float4 v = *reinterpret_cast<const float4*>(ls + (lane * CPL + 2 * p + 1) * R + 4 * b4);
+      lp[4 * b4][p] = f2pack(u.x, v.x);
+      lp[4 * b4 + 1][p] = f2pack(u.y, v.y);
+      lp[4 * b4 + 2][p] = f2pack(u.z, v.z);
+      lp[4 * b4 + 3][p] = f2pack(u.w, v.w);
     }
-  }
-  const int64_t cld = BITS == 8 ? K : (K + 1) / 2;
-  const uint8_t* cbase = codes != nullptr ? codes + (BITS == 8 ? col : col / 2) : nullptr;
-  OutT* obase = out + col;
-  // the code words of the warp's next MF_UN rows are in flight while the current ones are processed
-  auto load_codes = [&](int rb, uint32_t (&cw)[MF_UN]) {
-#pragma unroll
-    for (int u = 0; u < MF_UN; ++u) {
-      const int rl = rb + u;
-      cw[u] = 0u;
-      if (cbase != nullptr && rl < nrows) {
-        const uint8_t* p = cbase + (r0 + rl) * cld;
-        cw[u] = BITS == 8 ? __ldg(reinterpret_cast<const uint32_t*>(p))
-                          : static_cast<uint32_t>(__ldg(reinterpret_cast<const uint16_t*>(p)));
-      }
-    }
-  };
+  OutT* dst = out + (r0 + rw0) * K + col;
   const unsigned long long nm2 = f2pack(-8388608.f, -8388608.f);
-  uint32_t cw[MF_UN], cn[MF_UN];
-  load_codes(warp * MF_UN, cw);
-  for (int rb = warp * MF_UN; rb < nrows; rb += 8 * MF_UN) {
-    load_codes(rb + 8 * MF_UN, cn);
+  for (int bi = 0; bi < nb; ++bi) {
+    issue(bi + MF_SLOTS - 1);
+    cp_async_wait<MF_SLOTS - 1>();
+    if (LB < 4) __syncwarp(live_mask);  // the pair's bytes were copied by the even lane
+    const int rb = bi * MF_UN;
+    const uint32_t slot = ring + static_cast<uint32_t>((bi % MF_SLOTS) * SLOT + lane * LB);
+    uint32_t cw[MF_UN][NW];
 #pragma unroll
     for (int u = 0; u < MF_UN; ++u) {
-      const int rl = rb + u;
-      if (rl >= nrows) break;
-      // dequantised codes (code -> fp32 by the exponent-field trick, then code * scale + offset): the
-      // accumulators start from them and the W_t FMAs add on top
+      if (codes == nullptr) {
+        cw[u][0] = 0u;
+        if (NW == 2) cw[u][NW - 1] = 0u;
+      } else if constexpr (LB == 8) {
+        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(cw[u][0]), "=r"(cw[u][NW - 1]) : "r"(slot + u * 32 * LB));
+      } else if constexpr (LB == 4) {
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cw[u][0]) : "r"(slot + u * 32 * LB));
+      } else {
+        uint16_t v;
+        asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(slot + u * 32 * LB));
+        cw[u][0] = v;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < MF_UN; ++u) {
+      const int rl = rw0 + rb + u;
       const float2 sv = *reinterpret_cast<const float2*>(so + 2 * rl);
       const unsigned long long sc2 = f2pack(sv.x, sv.x), of2 = f2pack(sv.y, sv.y);
-      unsigned long long acc0, acc1;
-      {
-        const uint32_t w = cw[u];
-        uint32_t e0, e1, e2, e3;
+      // codes of column 2p in `ev` byte p, of column 2p + 1 in `od` byte p
+      uint32_t ev[NW], od[NW];
+#pragma unroll
+      for (int q = 0; q < NW; ++q) {
         if (BITS == 8) {
-          e0 = w & 0xFFu, e1 = (w >> 8) & 0xFFu, e2 = (w >> 16) & 0xFFu, e3 = w >> 24;
+          ev[q] = __byte_perm(cw[u][q], 0u, 0x4420);
+          od[q] = __byte_perm(cw[u][q], 0u, 0x4431);
         } else {
-          e0 = w & 0xFu, e1 = (w >> 4) & 0xFu, e2 = (w >> 8) & 0xFu, e3 = (w >> 12) & 0xFu;
+          ev[q] = cw[u][q] & 0x0F0F0F0Fu;
+          od[q] = (cw[u][q] >> 4) & 0x0F0F0F0Fu;
         }
-        const unsigned long long f01 = fadd2(f2pack(__uint_as_float(0x4B000000u | e0), __uint_as_float(0x4B000000u | e1)), nm2);
-        const unsigned long long f23 = fadd2(f2pack(__uint_as_float(0x4B000000u | e2), __uint_as_float(0x4B000000u | e3)), nm2);
-        acc0 = ffma2r(f01, sc2, of2);
-        acc1 = ffma2r(f23, sc2, of2);
+      }
+      unsigned long long acc[NP];
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        constexpr int kPerWord = BITS == 8 ? 2 : 4;  // column pairs per code word
+        const int q = p / kPerWord, byte = p % kPerWord;
+        const uint32_t e = __byte_perm(ev[q], 0x4B000000u, 0x7650 + byte);
+        const uint32_t o = __byte_perm(od[q], 0x4B000000u, 0x7650 + byte);
+        acc[p] = ffma2r(fadd2(f2pack(__uint_as_float(e), __uint_as_float(o)), nm2), sc2, of2);
       }
       const float4* gr = reinterpret_cast<const float4*>(gs + rl * R);
 #pragma unroll
-      for (int q = 0; q < R / 4; ++q) {
-        const float4 g = gr[q];
+      for (int b4 = 0; b4 < R / 4; ++b4) {
+        const float4 g = gr[b4];
         const float gg[4] = {g.x, g.y, g.z, g.w};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const unsigned long long g2 = f2pack(gg[e], gg[e]);
-          ffma2(acc0, g2, lp[4 * q + e][0]);
-          ffma2(acc1, g2, lp[4 * q + e][1]);
+#pragma unroll
+          for (int p = 0; p < NP; ++p) ffma2(acc[p], g2, lp[4 * b4 + e][p]);
         }
       }
-      OutT* dst = obase + (r0 + rl) * K;
+      OutT* d = dst + static_cast<int64_t>(rb + u) * K;
       if constexpr (sizeof(OutT) == 2) {
-        const __nv_bfloat162 a = __floats2bfloat162_rn(f2lo(acc0), f2hi(acc0));
-        const __nv_bfloat162 b = __floats2bfloat162_rn(f2lo(acc1), f2hi(acc1));
-        *reinterpret_cast<uint2*>(dst) =
-            make_uint2(*reinterpret_cast<const uint32_t*>(&a), *reinterpret_cast<const uint32_t*>(&b));
+        uint32_t pk[NP];
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          const __nv_bfloat162 t = __floats2bfloat162_rn(f2lo(acc[p]), f2hi(acc[p]));
+          pk[p] = *reinterpret_cast<const uint32_t*>(&t);
+        }
+        if constexpr (NP == 4)
+          *reinterpret_cast<uint4*>(d) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        else
+          *reinterpret_cast<uint2*>(d) = make_uint2(pk[0], pk[1]);
       } else {
-        *reinterpret_cast<float4*>(dst) = make_float4(f2lo(acc0), f2hi(acc0), f2lo(acc1), f2hi(acc1));
+#pragma unroll
+        for (int p = 0; p < NP; p += 2)
+          *reinterpret_cast<float4*>(d + 2 * p) =
+              make_float4(f2lo(acc[p]), f2hi(acc[p]), f2lo(acc[p + 1]), f2hi(acc[p + 1]));
       }
     }
-#pragma unroll
-    for (int u = 0; u < MF_UN; ++u) cw[u] = cn[u];
+    if (LB < 4) __syncwarp(live_mask);  // before the even lane refills the slot its pair has just read
   }
 }
 
@@ -714,7 +803,7 @@ bool merge_fast_ok(const TTDims& dd, const void* codes, const void* out) {
   const int64_t md = dd.m[d - 1];
   if ((R != 8 && R != 16) || md % 64 != 0 || dd.K % 8 != 0) return false;
   if (d == 3 && (dd.r[1] > 16 || dd.n[1] > 16)) return false;
-  return reinterpret_cast<uintptr_t>(out) % 16 == 0 && (codes == nullptr || reinterpret_cast<uintptr_t>(codes) % 4 == 0);
+  return reinterpret_cast<uintptr_t>(out) % 16 == 0 && (codes == nullptr || reinterpret_cast<uintptr_t>(codes) % 8 == 0);
 }
 
 cudaError_t launch_merge_fast(const TTDims& dd, const float* const* cores, const uint8_t* codes, int bits,
@@ -722,25 +811,35 @@ cudaError_t launch_merge_fast(const TTDims& dd, const float* const* cores, const
   const int d = dd.d;
   const int R = dd.r[d - 1];
   const int64_t md = dd.m[d - 1];
+  const int cols = R == 8 ? mf_cols<8>() : mf_cols<16>();
+  const int64_t ctiles = (dd.K + cols - 1) / cols;
+  // 256-row tiles: the per-CTA prologue (L for the tile's columns) amortised over more rows; 64-row tiles
+  // (more CTAs for the 1024-row k / v matrices) measured slower even where 256 leaves SMs idle
   const int RT = md % 256 == 0 ? 256 : 64;
   const int R1 = d == 3 ? dd.r[1] : 0, J1 = d == 3 ? dd.n[1] : 1, H = d == 3 ? dd.m[1] : 1;
   const int64_t total = dd.N * dd.K;
   LaunchScope scope(kMerge, double(total) * ((codes ? (bits == 8 ? 1.0 : 0.5) : 0.0) + (out_dtype == QA_F32 ? 4 : 2)), s);
   count_launches(1);
-  const dim3 grid(static_cast<unsigned>((dd.K + MF_COLS - 1) / MF_COLS), static_cast<unsigned>(dd.N / RT));
+  const dim3 grid(static_cast<unsigned>(ctiles), static_cast<unsigned>(dd.N / RT));
   const size_t smem =
-      sizeof(float) * (static_cast<size_t>(RT) * R + MF_COLS * R + 2 * RT + static_cast<size_t>(R1) * J1 * R);
+      sizeof(float) * (static_cast<size_t>(RT) * R + static_cast<size_t>(cols) * R + 2 * RT +
+                       static_cast<size_t>(R1) * J1 * R) +
+      static_cast<size_t>(MF_THREADS / 32) * MF_SLOTS * MF_UN * 32 * (cols / 32) * bits / 8;
   const float* G1 = cores[0];
   const float* G2 = d == 3 ? cores[1] : nullptr;
   const float* Gd = cores[d - 1];
 #define QA_MF(OT, BB, RR, DD)                                                                                     \
-  k_merge_fast<OT, BB, RR, DD><<<grid, 256, smem, s>>>(G1, G2, Gd, R1, J1, H, md, dd.N, dd.K, RT, codes, scale,     \
-                                                      offset, static_cast<OT*>(out))
+  {                                                                                                              \
+    cudaFuncSetAttribute(k_merge_fast<OT, BB, RR, DD>, cudaFuncAttributeMaxDynamicSharedMemorySize,                 \
+                         static_cast<int>(smem));                                                                   \
+    k_merge_fast<OT, BB, RR, DD><<<grid, MF_THREADS, smem, s>>>(G1, G2, Gd, R1, J1, H, md, dd.N, dd.K, RT, codes,   \
+                                                               scale, offset, static_cast<OT*>(out));              \
+  }
 #define QA_MF_D(OT, BB, RR) \
   if (d == 3)               \
-    QA_MF(OT, BB, RR, true); \
+    QA_MF(OT, BB, RR, true)  \
   else                      \
-    QA_MF(OT, BB, RR, false);
+    QA_MF(OT, BB, RR, false)
 #define QA_MF_R(OT, BB) \
   if (R == 8) {         \
     QA_MF_D(OT, BB, 8)  \

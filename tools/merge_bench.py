@@ -78,7 +78,7 @@ def main():
     if os.path.exists(p):
         peak = json.load(open(p)).get("hbm_gbs")
     gbs = tot_bytes / tot_ms / 1e6
-    print(json.dumps({"kernel": "merge (k_prefix_full + k_last_full)", "set": a.set, "bits": bits, "out": a.out,
+    print(json.dumps({"kernel": "merge (k_merge_fast)", "set": a.set, "bits": bits, "out": a.out,
                       "total_ms": tot_ms, "total_bytes": tot_bytes, "achieved_gbs": gbs,
                       "frac_of_hbm": gbs / peak if peak else None, "per_matrix": rows}))
 
