@@ -669,7 +669,7 @@ __global__ void __launch_bounds__(512) k_decode_prep(const __nv_bfloat16* __rest
                                                     float* __restrict__ ox, int32_t* __restrict__ rsx,
                                                     const float* __restrict__ G1, const float* __restrict__ G2,
                                                     int d, int H, int C, float* __restrict__ z1out,
-                                                    float* __restrict__ zlast, int64_t ldz, bool vec) {
+                                                    float* __restrict__ zlast, int64_t ldz, bool vec, bool early) {
   DP_MARK(0)
   asm volatile("griddepcontrol.launch_dependents;");
   constexpr int K2 = J1 * R1;
@@ -693,13 +693,22 @@ __global__ void __launch_bounds__(512) k_decode_prep(const __nv_bfloat16* __rest
     for (int q = tid; q < n2 / 4; q += NT) cp_async16(g2s + 4 * q, G2 + 4 * q, true);
     cp_async_commit();
   }
+  // early: launched as a programmatic dependent of whatever kernel produces x — the cores (weights) are
+  // pulled into L2 while that kernel finishes, then x is read only after it has completed
+  if (early) {
+    for (int c = tid; c < nchunk; c += NT)
+      for (int off = 0; off < NJ * R1; off += 32)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(G1 + static_cast<int64_t>(c) * NJ * R1 + off));
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
   __nv_bfloat162 lo2 = __floats2bfloat162_rn(INFINITY, INFINITY), hi2 = __floats2bfloat162_rn(-INFINITY, -INFINITY);
   float z[K2];
 #pragma unroll
   for (int i = 0; i < K2; ++i) z[i] = 0.f;
 #pragma unroll 2
   for (int c = tid; c < nchunk; c += NT) {
-    const uint4 v = __ldg(xr + c);
+    uint4 v;  // not ld.global.nc: x may come from the kernel this one was launched behind
+    asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(xr + c));
     row[c] = v;
     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
@@ -881,14 +890,17 @@ cudaError_t launch_decode_prep(const void* x, int64_t T, int64_t K, uint8_t* cod
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cfg.attrs = attr;
-  cfg.numAttrs = chain && pdl_enabled() ? 1 : 0;
+  // every prologue is a programmatic dependent: a chained member (x already complete) overlaps the previous
+  // member's pass; the first one (early) prefetches its cores and waits for x's producer before reading it
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  const bool early = !chain;
   const __nv_bfloat16* xb = static_cast<const __nv_bfloat16*>(x);
   cudaError_t e = cudaSuccess;
 #define QA_DPR(JJ, RR)                                                                                             \
   {                                                                                                                \
     cudaFuncSetAttribute(k_decode_prep<JJ, RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)); \
     e = cudaLaunchKernelEx(&cfg, k_decode_prep<JJ, RR>, xb, K, codes, ldc, sx, ox, rsx, G1, G2, d, H, C, z1out,    \
-                           zlast, ldz, vec);                                                                        \
+                           zlast, ldz, vec, early);                                                                 \
   }
   if (J1 == 4 && R1 == 8)
     QA_DPR(4, 8)

@@ -377,6 +377,32 @@ def test_decode_sized_batches(N, K, bits, r, spec):
         assert O.rel_err(_np(y32), ref["y"]) <= 1e-4, T
 
 
+@pytest.mark.parametrize("bits", [8, 4])
+def test_decode_sized_group_matches_members(bits):
+    """A shared-input group at decode size (q / k / v of one decoder layer, transformer.py:862-874 with 1..8
+    tokens; member i + 1's prologue chained behind member i's matrix-vector pass): each member's y equals its own
+    single-linear decode pass bit for bit and the oracle to bf16, int8 and int4 bases."""
+    K = 1024
+    members, refs = [], []
+    for i, N in enumerate((1024, 512, 512)):
+        W = O.seeded_random(N, K, 80 + i, std=0.02)
+        q, oq = qa.quantize_rows(W, bits), O.quantize_rows(W, bits)
+        spec = L.TTSpec.for_shape(N, K, 8)
+        cores_np = O.tt_init_cores(O.TTShape(spec.m, spec.n, spec.ranks), 90 + i, std=0.05)
+        cores = [torch.from_numpy(c).cuda() for c in cores_np]
+        members.append(L.TTLinear(f"m{i}", L.QuantizedLinear(f"m{i}.base", q), spec, cores))
+        refs.append((oq, cores_np))
+    xs = O.seeded_random(8, K, 99)
+    x = torch.from_numpy(xs).cuda().to(torch.bfloat16)
+    xs_b = _np(x).astype(np.float64)
+    for T in (1, 3, 8):
+        ys = L.group_forward(members, x[:T])
+        for i, m in enumerate(members):
+            assert torch.equal(ys[i], m.forward(x[:T])), (T, i)
+            ref = O.qa_linear_forward(xs_b[:T], refs[i][0], refs[i][1])
+            assert O.rel_err(_np(ys[i]), ref["y"]) <= TOL_BF16, (T, i)
+
+
 def test_config1_mse_training_step_matches_oracle():
     """BASELINE config 1 end to end on the device: W 1024^2 ~N(0, 0.02) int8, x [4, 128, 1024] ~N(0, 1) fp32, the
     balanced (4,16,16)^2 rank-8 tensor adapter with cores ~N(0, 0.01), forward, MSE to a seeded N(0, 1) target
