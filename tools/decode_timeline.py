@@ -69,7 +69,7 @@ per = len(ev) // 5
 last = ev[-per:]
 t0 = last[0]["ts"]
 for e in last:
-    name = e["name"].split("(")[0].replace("void ", "").replace("qa::(anonymous namespace)::", "")
+    name = e["name"].replace("qa::(anonymous namespace)::", "").replace("void ", "").split("(")[0]
     print(f"{e['ts'] - t0:8.2f} .. {e['ts'] + e['dur'] - t0:8.2f}  ({e['dur']:6.2f} us)  {name}")
 print(f"step span {last[-1]['ts'] + last[-1]['dur'] - t0:.2f} us; previous step ended "
       f"{t0 - (ev[-per - 1]['ts'] + ev[-per - 1]['dur']):.2f} us before this one began")
