@@ -2502,12 +2502,15 @@ cudaError_t launch_actquant_z1_group(const void* x, int64_t T, int64_t K, bool w
 // in half an SM's shared memory (measured on the 7B set: TT side kernels 1.21 -> 1.14 ms), else one CTA per
 // SM with the deepest ring that fits.
 struct Dg1Shape {
-  int per_sm, nstg;
+  int per_sm, nstg, raw;  // raw: the dZ1 partials prefetched into shared memory (else read from L2 in place)
 };
 Dg1Shape dg1_shape(size_t planes, size_t raw_bytes) {
   const size_t ring2 = sizeof(__nv_bfloat16) * 2 * DM_ST * DM_LDX;
-  Dg1Shape d{1, DM_NSTG};
-  if (ring2 + planes + raw_bytes <= 112 * 1024) d = Dg1Shape{2, 2};
+  Dg1Shape d{1, DM_NSTG, -1};
+  if (ring2 + planes + raw_bytes <= 112 * 1024)
+    d = Dg1Shape{2, 2, 1};
+  else if (ring2 + planes <= 112 * 1024)  // shared-input groups: two CTAs per SM beat the prefetch
+    d = Dg1Shape{2, 2, 0};
   return d;
 }
 
@@ -2540,9 +2543,9 @@ cudaError_t launch_tt_dg1_group(const void* x, int64_t T, int64_t K, const float
   // one CTA per SM: a 4-stage x ring when the prefetched dZ1 partials fit beside it, else 3 stages (the
   // prefetch matters more)
   int nstg = shp.nstg;
-  if (sizeof(__nv_bfloat16) * nstg * DM_ST * DM_LDX + planes + raw_bytes > 220 * 1024) nstg = 3;
+  if (shp.raw < 0 && sizeof(__nv_bfloat16) * nstg * DM_ST * DM_LDX + planes + raw_bytes > 220 * 1024) nstg = 3;
   size_t smem = sizeof(__nv_bfloat16) * nstg * DM_ST * DM_LDX + planes;
-  const int raw_async = smem + raw_bytes <= 220 * 1024 ? 1 : 0;
+  const int raw_async = shp.raw >= 0 ? shp.raw : (smem + raw_bytes <= 220 * 1024 ? 1 : 0);
   if (raw_async) smem += raw_bytes;
   const dim3 gm(static_cast<unsigned>(gx), static_cast<unsigned>(Sm));
   if (NA == 2) {
@@ -2590,9 +2593,9 @@ cudaError_t launch_tt_dg1(const void* x, int x_dtype, int64_t T, int64_t K, cons
       if (splits_used != nullptr) *splits_used = static_cast<int>(Sm);
       const dim3 gm(static_cast<unsigned>(gx), static_cast<unsigned>(Sm));
       int nstg = shp.nstg;
-      if (sizeof(__nv_bfloat16) * nstg * DM_ST * DM_LDX + planes + raw_bytes > 220 * 1024) nstg = 3;
+      if (shp.raw < 0 && sizeof(__nv_bfloat16) * nstg * DM_ST * DM_LDX + planes + raw_bytes > 220 * 1024) nstg = 3;
       size_t smem = sizeof(__nv_bfloat16) * nstg * DM_ST * DM_LDX + planes;
-      const int raw_async = smem + raw_bytes <= 220 * 1024 ? 1 : 0;
+      const int raw_async = shp.raw >= 0 ? shp.raw : (smem + raw_bytes <= 220 * 1024 ? 1 : 0);
       if (raw_async) smem += raw_bytes;
       const DgAdapters ad{{dz1, nullptr, nullptr}, {part, nullptr, nullptr}, {dz1b, nullptr, nullptr}};
       if (R1 == 8) {
