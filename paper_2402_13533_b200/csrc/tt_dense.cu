@@ -144,18 +144,21 @@ __global__ void __launch_bounds__(256) k_proj_right(const float* __restrict__ dW
   }
 }
 
-// The same with one 256-thread CTA per (I, ik, J, j), for long inner sums (few outputs, e.g. the first core)
+// The same for long inner sums over few outputs (e.g. the first core): CTAs (o, s) split output o's sum into
+// gridDim.y slices, each writing its partial to Y plane s (summed in fixed order by k_proj_left)
 template <int RB>
 __global__ void __launch_bounds__(256) k_proj_right_cta(const float* __restrict__ dW, int64_t K, int64_t OUT_COLS,
                                                         int64_t SM, int64_t SN, const float* __restrict__ R, int rb,
-                                                        float* __restrict__ Y) {
+                                                        float* __restrict__ Y, int64_t plane) {
   __shared__ float red[8][RB];
   const int64_t o = blockIdx.x;
   const int64_t orow = o / OUT_COLS, ocol = o - orow * OUT_COLS;
+  const int64_t total = SM * SN, per = (total + gridDim.y - 1) / gridDim.y;
+  const int64_t e0 = blockIdx.y * per, e1 = e0 + per < total ? e0 + per : total;
   float acc[RB];
 #pragma unroll
   for (int b = 0; b < RB; ++b) acc[b] = 0.f;
-  for (int64_t e = threadIdx.x; e < SM * SN; e += 256) {
+  for (int64_t e = e0 + threadIdx.x; e < e1; e += 256) {
     const int64_t Ip = e / SN, Jp = e - Ip * SN;
     const float w = dW[(orow * SM + Ip) * K + ocol * SN + Jp];
 #pragma unroll
@@ -174,14 +177,15 @@ __global__ void __launch_bounds__(256) k_proj_right_cta(const float* __restrict_
     float v = 0.f;
 #pragma unroll
     for (int w = 0; w < 8; ++w) v += red[w][threadIdx.x];
-    Y[o * rb + threadIdx.x] = v;
+    Y[blockIdx.y * plane + o * rb + threadIdx.x] = v;
   }
 }
 
-// dG[a, ik, j, b] (+)= Σ_{I, J} L[I, J, a] · Y[I, ik, J, j, b]   (one warp per output element)
+// dG[a, ik, j, b] (+)= Σ_{I, J} L[I, J, a] · Y[I, ik, J, j, b]   (one warp per output element; Y may come as
+// nplanes partial planes, summed first in fixed order)
 __global__ void __launch_bounds__(256) k_proj_left(const float* __restrict__ Y, const float* __restrict__ L, int64_t PM,
                                                    int64_t PN, int ra, int mk, int nk, int rb, float* __restrict__ dG,
-                                                   int accumulate) {
+                                                   int accumulate, int nplanes, int64_t plane) {
   const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int64_t total = static_cast<int64_t>(ra) * mk * nk * rb;
@@ -195,10 +199,25 @@ __global__ void __launch_bounds__(256) k_proj_left(const float* __restrict__ Y, 
     const int64_t I = e / PN, J = e - I * PN;
     const float l = L != nullptr ? L[(I * PN + J) * ra + a] : 1.f;
     // Y index: ((I * mk + ik) * (PN * nk) + J * nk + j) * rb + b
-    acc = fmaf(l, Y[(((I * mk + ik) * PN + J) * nk + j) * rb + b], acc);
+    const int64_t yi = (((I * mk + ik) * PN + J) * nk + j) * rb + b;
+    float y = Y[yi];
+    for (int p = 1; p < nplanes; ++p) y += Y[p * plane + yi];
+    acc = fmaf(l, y, acc);
   }
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   if (lane == 0) dG[wid] = accumulate ? dG[wid] + acc : acc;
+}
+
+constexpr int kProjMaxPlanes = 64;  // partial Y planes of a split projection
+
+// Slices of a projection's inner sum: long sums (SM·SN >= 2048 terms) over few outputs are split so that ~4 CTAs
+// per SM run, each slice >= 1024 terms; the rest run unsplit (one warp per output).
+int proj_planes(int64_t outs, int64_t terms) {
+  if (terms < 2048) return 1;
+  int64_t sl = (4 * 148 + outs - 1) / outs;
+  const int64_t by_len = (terms + 1023) / 1024;
+  if (sl > by_len) sl = by_len;
+  return static_cast<int>(sl < 1 ? 1 : (sl > kProjMaxPlanes ? kProjMaxPlanes : sl));
 }
 
 unsigned blocks_for(int64_t work, int threads) {
@@ -252,7 +271,8 @@ size_t tt_project_ws_floats(const TTDims& dd) {
     }
     const size_t L = static_cast<size_t>(PM * PN * dd.r[k]);
     const size_t R = static_cast<size_t>(SM * SN * dd.r[k + 1]);
-    const size_t Y = static_cast<size_t>(PM * dd.m[k] * PN * dd.n[k]) * dd.r[k + 1];
+    const int64_t outs = PM * dd.m[k] * PN * dd.n[k];
+    const size_t Y = static_cast<size_t>(outs) * dd.r[k + 1] * (k + 1 < dd.d ? proj_planes(outs, SM * SN) : 1);
     const size_t tot = L + R + Y + 3 * 64;
     if (tot > best) best = tot;
   }
@@ -291,17 +311,20 @@ cudaError_t launch_tt_project(const TTDims& dd, const float* const* cores, const
     const float* Rp = R;
     const int64_t outs = (PM * mk) * (PN * nk);
     const unsigned gr = static_cast<unsigned>((outs * 32 + 255) / 256);
+    const int64_t plane = outs * rb;
+    int nplanes = 1;
     if (k + 1 == dd.d) {
       // Y[I, ik, J, j, 0] = dW[(I, ik), (J, j)] (SM = SN = 1, R = 1)
       cudaError_t e = cudaMemcpyAsync(Y, dW, sizeof(float) * outs, cudaMemcpyDeviceToDevice, s);
       if (e != cudaSuccess) return e;
     } else {
-      // long inner sums over few outputs take a CTA each, the rest a warp each
+      // long inner sums over few outputs take CTAs (split into proj_planes slices), the rest a warp each
       const bool cta = SM * SN >= 2048;
-      const unsigned gc = static_cast<unsigned>(outs);
+      nplanes = proj_planes(outs, SM * SN);
+      const dim3 gc(static_cast<unsigned>(outs), static_cast<unsigned>(nplanes));
 #define QA_PR(RBV)                                                                                   \
   if (cta)                                                                                           \
-    k_proj_right_cta<RBV><<<gc, 256, 0, s>>>(dW, dd.K, PN * nk, SM, SN, Rp, rb, Y);                  \
+    k_proj_right_cta<RBV><<<gc, 256, 0, s>>>(dW, dd.K, PN * nk, SM, SN, Rp, rb, Y, plane);           \
   else                                                                                               \
     k_proj_right<RBV><<<gr, 256, 0, s>>>(dW, dd.K, PM * mk, PN * nk, SM, SN, Rp, rb, Y);
       if (rb <= 8) {
@@ -317,7 +340,8 @@ cudaError_t launch_tt_project(const TTDims& dd, const float* const* cores, const
     }
     const int64_t gouts = static_cast<int64_t>(ra) * mk * nk * rb;
     k_proj_left<<<static_cast<unsigned>((gouts * 32 + 255) / 256), 256, 0, s>>>(Y, k > 0 ? L : nullptr, PM, PN, ra, mk,
-                                                                                nk, rb, dcores[k], accumulate ? 1 : 0);
+                                                                                nk, rb, dcores[k], accumulate ? 1 : 0,
+                                                                                nplanes, plane);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
