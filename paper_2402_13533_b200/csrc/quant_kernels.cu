@@ -270,19 +270,22 @@ __global__ void __launch_bounds__(256) k_dequantize(const uint8_t* __restrict__ 
 }
 
 // Transposed bf16 dequantisation for the dX GEMM operand: outᵀ[k, n] = bf16(code·scale + offset),
-// 64 x 64 tiles, 16-byte code loads and 16-byte stores (full tiles; edges go through k_dequantize).
+// 64 x 64 tiles, 16-byte code loads and 16-byte stores (full tiles; edges go through k_dequantize).  The
+// shared tile is [k][n] with its 16-byte n-chunks XOR-swizzled by k / 16, so the transposing 2-byte stores
+// of a warp (8 rows n x 4 column blocks k) land on distinct banks and the row reads stay conflict-free.
 template <int BITS>
 __global__ void __launch_bounds__(256) k_dequant_t64(const uint8_t* __restrict__ codes, int64_t ldc,
                                                      const float* __restrict__ scale,
                                                      const float* __restrict__ offset,
                                                      __nv_bfloat16* __restrict__ out, int64_t ld_out,
                                                      __nv_bfloat16* __restrict__ out_lo) {
-  __shared__ __align__(16) __nv_bfloat16 sh[64][72];
-  __shared__ __align__(16) __nv_bfloat16 sl[64][72];
+  __shared__ __align__(16) __nv_bfloat16 sh[64][64];
+  __shared__ __align__(16) __nv_bfloat16 sl[64][64];
   const int64_t n0 = static_cast<int64_t>(blockIdx.y) * 64, k0 = static_cast<int64_t>(blockIdx.x) * 64;
   const int t = threadIdx.x;
   const int r = t >> 2, seg = t & 3;  // row n0 + r, columns k0 + 16 seg .. + 15
   const int64_t n = n0 + r;
+  const int col = (((r >> 3) ^ seg) << 3) | (r & 7);  // swizzled position of n in rows k = 16 seg + i
   uint32_t c[16];
   if (BITS == 8) {
     const uint4 u = __ldg(reinterpret_cast<const uint4*>(codes + n * ldc + k0 + seg * 16));
@@ -299,25 +302,26 @@ __global__ void __launch_bounds__(256) k_dequant_t64(const uint8_t* __restrict__
     // bf16 operand of the dX GEMM: one fp32 FMA per code (its rounding sits 2^-16 below the bf16 step)
     const float s = scale[n], o = offset[n];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) sh[seg * 16 + i][r] = __float2bfloat16_rn(fmaf(static_cast<float>(c[i]), s, o));
+    for (int i = 0; i < 16; ++i) sh[seg * 16 + i][col] = __float2bfloat16_rn(fmaf(static_cast<float>(c[i]), s, o));
   } else {  // hi / lo split for fp32 callers: the reference's fp64 value (quant.py:102-105)
     const double s = static_cast<double>(scale[n]), o = static_cast<double>(offset[n]);
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       const double v = __dadd_rn(__dmul_rn(static_cast<double>(c[i]), s), o);
       const __nv_bfloat16 hi = __float2bfloat16_rn(__double2float_rn(v));
-      sh[seg * 16 + i][r] = hi;
-      sl[seg * 16 + i][r] = __float2bfloat16_rn(__double2float_rn(v - double(__bfloat162float(hi))));
+      sh[seg * 16 + i][col] = hi;
+      sl[seg * 16 + i][col] = __float2bfloat16_rn(__double2float_rn(v - double(__bfloat162float(hi))));
     }
   }
   __syncthreads();
 #pragma unroll
   for (int pass = 0; pass < 2; ++pass) {
     const int kk = (t >> 3) + pass * 32, ch = t & 7;
-    *reinterpret_cast<uint4*>(out + (k0 + kk) * ld_out + n0 + ch * 8) = *reinterpret_cast<const uint4*>(&sh[kk][ch * 8]);
+    const int pch = (ch ^ ((kk >> 4) & 3)) << 3;  // physical chunk of logical chunk ch in row kk
+    *reinterpret_cast<uint4*>(out + (k0 + kk) * ld_out + n0 + ch * 8) = *reinterpret_cast<const uint4*>(&sh[kk][pch]);
     if (out_lo != nullptr)
       *reinterpret_cast<uint4*>(out_lo + (k0 + kk) * ld_out + n0 + ch * 8) =
-          *reinterpret_cast<const uint4*>(&sl[kk][ch * 8]);
+          *reinterpret_cast<const uint4*>(&sl[kk][pch]);
   }
 }
 
