@@ -515,14 +515,17 @@ int linear_forward_impl(const qa_qweight* w, const qa_tt* tt, const void* x, int
                        "decode gemv");
   }
   if (P.fast && x_vec) {
+    // (4b, core-only half) one launch: the G1 fragments of the x pass and V = cores 2..d contracted (y2 = Z1 · Vᵀ
+    // runs as extension k-blocks of the GEMM)
+    const bool frags = actquant_frag_path(x_dtype, K, P.J1, P.R1, x, true, P.Kp, P.xcodes, z1_save);
+    const VJob vj{P.fd, P.R1, P.H, P.J1, P.C, P.M, tt->cores[1], P.fd == 3 ? tt->cores[2] : nullptr, P.v, N, P.K2p};
+    const float* g1 = tt->cores[0];
+    float* fr = P.g1i;
+    QA_TRY_CUDA(launch_adapter_prep(P.J1, P.R1, frags ? 1 : 0, &g1, &fr, K, 1, &vj, s), "adapter prep");
     // (2)+(4a) one pass over x: bit-exact per-token act-quant + Z1 = first TT stage
     QA_TRY_CUDA(launch_actquant_z1(x, x_dtype, T, K, true, P.xcodes, P.Kp, P.sx, P.ox, P.rsx, tt->cores[0], P.J1,
-                                   P.R1, P.zb, P.K2p, z1_save, P.g1i, s),
+                                   P.R1, P.zb, P.K2p, z1_save, P.g1i, s, frags),
                 "act quantize + TT stage 1");
-    // (4b) V = cores 2..d contracted; y2 = Z1 · Vᵀ runs as extension k-blocks of the GEMM
-    QA_TRY_CUDA(launch_build_v(P.fd, P.R1, P.H, P.J1, P.C, P.M, tt->cores[1], P.fd == 3 ? tt->cores[2] : nullptr,
-                               P.v, N, P.K2p, s),
-                "build V");
     ext.A2 = P.zb;
     ext.lda2 = P.K2p;
     ext.B2 = P.v;
@@ -971,14 +974,23 @@ int qa_group_forward(int n, const qa_qweight* const* w, const qa_tt* const* tt, 
     zf[i] = (saved != nullptr && saved[i] != nullptr && saved_bytes != nullptr && saved_bytes[i] >= need)
                 ? static_cast<float*>(saved[i]) : nullptr;
   }
-  // one pass over x: shared codes + each member's Z1
+  // every member's G1 fragments and V in one launch, then one pass over x: shared codes + each member's Z1
+  {
+    VJob vj[kMaxGroup];
+    float* fr[kMaxGroup];
+    const int64_t frag_floats = (K / 64) * 32 * 4;  // uint4 per lane per 64-element segment (J1 = 4, R1 = 8)
+    for (int i = 0; i < n; ++i) {
+      const LinearPlan& P = G.P[i];
+      vj[i] = VJob{P.fd, P.R1, P.H, P.J1, P.C, P.M, tt[i]->cores[1], tt[i]->cores[2], P.v, P.N, P.K2p};
+      fr[i] = G.frag + i * frag_floats;
+    }
+    QA_TRY_CUDA(launch_adapter_prep(4, 8, n, G1, fr, K, n, vj, s), "group adapter prep");
+  }
   QA_TRY_CUDA(launch_actquant_z1_group(x, T, K, true, P0.xcodes, P0.Kp, P0.sx, P0.ox, P0.rsx, G1, n, zb, P0.K2p, zf,
-                                       G.frag, s),
+                                       G.frag, s, true),
               "group act quantize + TT stage 1");
   for (int i = 0; i < n; ++i) {
     LinearPlan& P = G.P[i];
-    QA_TRY_CUDA(launch_build_v(P.fd, P.R1, P.H, P.J1, P.C, P.M, tt[i]->cores[1], tt[i]->cores[2], P.v, P.N, P.K2p, s),
-                "build V");
     int st = QA_OK;
     const uint8_t* wop = weight_operand(w[i], P, s, &st);
     QA_TRY(st);

@@ -128,7 +128,31 @@ bool fast_tt_supported(int J1, int R1);
 size_t g1i_floats(int64_t K, int J1, int R1);  // workspace for the interleaved G1 copy
 cudaError_t launch_actquant_z1(const void* x, int x_dtype, int64_t T, int64_t K, bool want_codes, uint8_t* codes,
                                int64_t ldc, float* sx, float* ox, int32_t* rsx, const float* G1, int J1, int R1,
-                               __nv_bfloat16* zb, int64_t ldzb, float* zf, float* g1i_ws, cudaStream_t s);
+                               __nv_bfloat16* zb, int64_t ldzb, float* zf, float* g1i_ws, cudaStream_t s,
+                               bool frag_ready = false);
+// launch_actquant_z1 takes its tensor-core path (the one reading G1 fragments) for these arguments
+bool actquant_frag_path(int x_dtype, int64_t K, int J1, int R1, const void* x, bool want_codes, int64_t ldc,
+                        const void* codes, const void* zf);
+// One launch for the core-only inputs of a forward (tt_fast.cu k_adapter_prep): the G1 MMA fragments of nf
+// members (same J1 / R1) and the V operands of nv members.
+struct VJob {
+  int d, R1, H, J1, C, M;
+  const float* G2;
+  const float* G3;
+  __nv_bfloat16* V;
+  int64_t N, ldv;
+};
+struct AdapterPrep {
+  const float* G1[3];
+  uint4* frag[3];
+  int nf;
+  int64_t nfrag, per_f;  // fragment steps per member, blocks per member
+  VJob v[3];
+  int nv;
+  int64_t vstart[4];  // first block of each V job
+};
+cudaError_t launch_adapter_prep(int J1, int R1, int nf, const float* const* G1, float* const* frag, int64_t K,
+                                int nv, const VJob* v, cudaStream_t s);
 cudaError_t launch_build_v(int d, int R1, int H, int J1, int C, int M, const float* G2, const float* G3,
                            __nv_bfloat16* V, int64_t N, int64_t ldv, cudaStream_t s);
 cudaError_t launch_build_bext(int R1, int J1, const float* G1, __nv_bfloat16* B, int64_t K, int64_t ldb,
@@ -159,7 +183,7 @@ bool group_x_pass_ok(int J1, int R1, int64_t K, int NA, const void* x);
 cudaError_t launch_actquant_z1_group(const void* x, int64_t T, int64_t K, bool want_codes, uint8_t* codes,
                                      int64_t ldc, float* sx, float* ox, int32_t* rsx, const float* const* G1, int NA,
                                      __nv_bfloat16* const* zb, int64_t ldzb, float* const* zf, float* frag_ws,
-                                     cudaStream_t s);
+                                     cudaStream_t s, bool frag_ready = false);
 cudaError_t launch_tt_dg1_group(const void* x, int64_t T, int64_t K, const float* const* dz1, float* const* part,
                                 int S, int HS, __nv_bfloat16* const* dz1b, int64_t ldb, int NA, int* splits_used,
                                 cudaStream_t s);

@@ -241,10 +241,8 @@ __global__ void __launch_bounds__(256, 2) k_actquant_z1(const InT* __restrict__ 
 //   pass 2: per-token codes (reference rule, bit-exact) from the same shared-memory rows.
 // G1 reaches the MMAs as pre-built fragments (k_g1_frag): one 16-byte load per lane per k-step.
 template <int J1, int R1>
-__global__ void __launch_bounds__(256) k_g1_frag(const float* __restrict__ G1, uint4* __restrict__ frag,
-                                                 int64_t nsteps) {
+QA_DEV void g1_frag_at(const float* __restrict__ G1, uint4* __restrict__ frag, int64_t nsteps, int64_t idx) {
   constexpr int MT = R1 / 8;  // m16 tiles: R1 = 8 -> rows (hi a | lo a); R1 = 16 -> tile 0 hi, tile 1 lo
-  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (idx >= nsteps * MT * 32) return;
   const int lane = static_cast<int>(idx % 32), mt = static_cast<int>((idx / 32) % MT);
   const int64_t s = idx / (32 * MT);
@@ -275,6 +273,12 @@ __global__ void __launch_bounds__(256) k_g1_frag(const float* __restrict__ G1, u
     w[q] = packed;
   }
   frag[idx] = make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+template <int J1, int R1>
+__global__ void __launch_bounds__(256) k_g1_frag(const float* __restrict__ G1, uint4* __restrict__ frag,
+                                                 int64_t nsteps) {
+  g1_frag_at<J1, R1>(G1, frag, nsteps, static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x);
 }
 
 // Per-row constants of the act-quant rule for the byte-grid code path below.
@@ -919,15 +923,14 @@ namespace {
 
 // V[n, c] (bf16, zero padded to ldv): contraction of cores 2..d with the left rank open.
 //   d = 2: V[i, a] = G2[a, i];  d = 3: V[(i2, i3), (a, j2)] = Σ_b G2[a, i2, j2, b] G3[b, i3]
-__global__ void __launch_bounds__(256) k_build_v(int d, int R1, int H, int J1, int C, int M,
-                                                 const float* __restrict__ G2, const float* __restrict__ G3,
-                                                 __nv_bfloat16* __restrict__ V, int64_t N, int64_t ldv) {
+QA_DEV void build_v_at(int d, int R1, int H, int J1, int C, int M, const float* __restrict__ G2,
+                       const float* __restrict__ G3, __nv_bfloat16* __restrict__ V, int64_t N, int64_t ldv,
+                       int64_t idx) {
   // one thread per (row n, column cc < K2): v is computed once and written to its three slots
   // [V_hi | V_hi | V_lo] against [Z_hi | Z_lo | Z_hi]: the three leading terms of the bf16 split
   // product, so y2 carries ~16 mantissa bits although the MMA operands are bf16; padding [3 K2, ldv) = 0
   const int K2 = R1 * J1;
   const int per_row = static_cast<int>(ldv) - 2 * K2;  // threads per row: K2 value columns + the padding
-  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (idx >= N * per_row) return;
   const int n32 = static_cast<int>(idx / per_row);  // N * ldv < 2^31 (launcher)
   const int c = static_cast<int>(idx - static_cast<int64_t>(n32) * per_row);
@@ -949,6 +952,30 @@ __global__ void __launch_bounds__(256) k_build_v(int d, int R1, int H, int J1, i
   vr[c] = hi;
   vr[c + K2] = hi;
   vr[c + 2 * K2] = __float2bfloat16_rn(v - __bfloat162float(hi));
+}
+
+__global__ void __launch_bounds__(256) k_build_v(int d, int R1, int H, int J1, int C, int M,
+                                                 const float* __restrict__ G2, const float* __restrict__ G3,
+                                                 __nv_bfloat16* __restrict__ V, int64_t N, int64_t ldv) {
+  build_v_at(d, R1, H, J1, C, M, G2, G3, V, N, ldv, static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x);
+}
+
+// Everything the forward of a linear (or of a shared-input group) derives from the cores alone, in one launch:
+// the G1 MMA fragments of every member (k_g1_frag) and every member's V (k_build_v); blocks [0, fb) build
+// fragments (member = block / per_f), the rest V (member from the prefix vstart).
+template <int J1, int R1>
+__global__ void __launch_bounds__(256) k_adapter_prep(const AdapterPrep P) {
+  const int64_t b = blockIdx.x;
+  const int64_t fb = P.nf * P.per_f;
+  if (b < fb) {
+    const int m = static_cast<int>(b / P.per_f);
+    g1_frag_at<J1, R1>(P.G1[m], P.frag[m], P.nfrag, (b - m * P.per_f) * 256 + threadIdx.x);
+    return;
+  }
+  int m = 0;
+  while (m + 1 < P.nv && b >= P.vstart[m + 1]) ++m;
+  const VJob& v = P.v[m];
+  build_v_at(v.d, v.R1, v.H, v.J1, v.C, v.M, v.G2, v.G3, v.V, v.N, v.ldv, (b - P.vstart[m]) * 256 + threadIdx.x);
 }
 
 // B_ext[k = (j1, J), c = (a, J')] = G1[j1, a] δ(J, J')  (bf16, zero padded to ldb)
@@ -2193,19 +2220,25 @@ size_t g1i_floats(int64_t K, int J1, int R1) {
   return static_cast<size_t>(((nvec + 31) / 32) * 32) * 8 * R1 / J1 * 2;  // >= the k_g1_frag fragments
 }
 
+bool actquant_frag_path(int x_dtype, int64_t K, int J1, int R1, const void* x, bool want_codes, int64_t ldc,
+                        const void* codes, const void* zf) {
+  return x_dtype == QA_BF16 && K % 64 == 0 && (J1 == 1 || J1 == 4) && (R1 == 8 || R1 == 16) &&
+         reinterpret_cast<uintptr_t>(x) % 16 == 0 &&
+         (!want_codes || (ldc % 16 == 0 && reinterpret_cast<uintptr_t>(codes) % 16 == 0)) &&
+         (zf == nullptr || reinterpret_cast<uintptr_t>(zf) % 16 == 0);
+}
+
 cudaError_t launch_actquant_z1(const void* x, int x_dtype, int64_t T, int64_t K, bool want_codes, uint8_t* codes,
                                int64_t ldc, float* sx, float* ox, int32_t* rsx, const float* G1, int J1, int R1,
-                               __nv_bfloat16* zb, int64_t ldzb, float* zf, float* g1i_ws, cudaStream_t s) {
+                               __nv_bfloat16* zb, int64_t ldzb, float* zf, float* g1i_ws, cudaStream_t s,
+                               bool frag_ready) {
   if (T == 0) return cudaSuccess;
   const int64_t nvec = K / 8;
   // ---- production path: CTA-per-8-token kernel, rows read straight from global memory
-  if (x_dtype == QA_BF16 && K % 64 == 0 && (J1 == 1 || J1 == 4) && (R1 == 8 || R1 == 16) &&
-      reinterpret_cast<uintptr_t>(x) % 16 == 0 &&
-      (!want_codes || (ldc % 16 == 0 && reinterpret_cast<uintptr_t>(codes) % 16 == 0)) &&
-      (zf == nullptr || reinterpret_cast<uintptr_t>(zf) % 16 == 0)) {
+  if (actquant_frag_path(x_dtype, K, J1, R1, x, want_codes, ldc, codes, zf)) {
     const int MT = R1 / 8;
     const int64_t nfrag = (J1 == 4 ? K / 64 : K / 16);
-    {
+    if (!frag_ready) {
       LaunchScope scope(kTT, double(nfrag) * MT * 32 * 16 + double(K) * R1 * 4, s);
       count_launches(1);
       const int64_t n = nfrag * MT * 32;
@@ -2316,6 +2349,44 @@ cudaError_t launch_actquant_z1(const void* x, int x_dtype, int64_t T, int64_t K,
   }
 #undef QA_AQ_T
 #undef QA_AQ
+  return cudaGetLastError();
+}
+
+cudaError_t launch_adapter_prep(int J1, int R1, int nf, const float* const* G1, float* const* frag, int64_t K,
+                                int nv, const VJob* v, cudaStream_t s) {
+  AdapterPrep P{};
+  P.nf = nf;
+  P.nfrag = J1 == 4 ? K / 64 : K / 16;
+  P.per_f = (P.nfrag * (R1 / 8) * 32 + 255) / 256;
+  double bytes = 0.0;
+  for (int i = 0; i < nf; ++i) {
+    P.G1[i] = G1[i];
+    P.frag[i] = reinterpret_cast<uint4*>(frag[i]);
+    bytes += double(P.nfrag) * (R1 / 8) * 32 * 16 + double(K) * R1 * 4;
+  }
+  P.nv = nv;
+  int64_t blk = nf * P.per_f;
+  for (int i = 0; i < nv; ++i) {
+    P.v[i] = v[i];
+    P.vstart[i] = blk;
+    const int K2 = v[i].R1 * v[i].J1;
+    if (v[i].N * v[i].ldv >= (int64_t(1) << 31) || v[i].ldv < 3 * int64_t(K2)) return cudaErrorInvalidValue;
+    blk += (v[i].N * (v[i].ldv - 2 * K2) + 255) / 256;
+    bytes += double(v[i].N) * v[i].ldv * 2 + double(v[i].N) * K2 * v[i].C * 2;
+  }
+  P.vstart[nv] = blk;
+  if (blk == 0) return cudaSuccess;
+  LaunchScope scope(kTT, bytes, s);
+  count_launches(1);
+  const unsigned g = static_cast<unsigned>(blk);
+  if (J1 == 1 && R1 == 8)
+    k_adapter_prep<1, 8><<<g, 256, 0, s>>>(P);
+  else if (J1 == 1)
+    k_adapter_prep<1, 16><<<g, 256, 0, s>>>(P);
+  else if (R1 == 8)
+    k_adapter_prep<4, 8><<<g, 256, 0, s>>>(P);
+  else
+    k_adapter_prep<4, 16><<<g, 256, 0, s>>>(P);
   return cudaGetLastError();
 }
 
@@ -2455,12 +2526,12 @@ bool group_x_pass_ok(int J1, int R1, int64_t K, int NA, const void* x) {
 cudaError_t launch_actquant_z1_group(const void* x, int64_t T, int64_t K, bool want_codes, uint8_t* codes,
                                      int64_t ldc, float* sx, float* ox, int32_t* rsx, const float* const* G1, int NA,
                                      __nv_bfloat16* const* zb, int64_t ldzb, float* const* zf, float* frag_ws,
-                                     cudaStream_t s) {
+                                     cudaStream_t s, bool frag_ready) {
   if (T == 0) return cudaSuccess;
   const int64_t nfrag = K / 64;  // J1 = 4, R1 = 8: one uint4 per lane per 64-element segment
   const int64_t stride = nfrag * 32;
   uint4* fr = reinterpret_cast<uint4*>(frag_ws);
-  for (int a = 0; a < NA; ++a) {
+  for (int a = 0; a < NA && !frag_ready; ++a) {
     LaunchScope scope(kTT, double(stride) * 16 + double(K) * 8 * 4, s);
     count_launches(1);
     k_g1_frag<4, 8><<<static_cast<unsigned>((stride + 255) / 256), 256, 0, s>>>(G1[a], fr + a * stride, nfrag);
