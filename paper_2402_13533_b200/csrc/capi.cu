@@ -1089,16 +1089,33 @@ int qa_group_backward(int n, const qa_qweight* const* w, const qa_tt* const* tt,
   int s_dg1 = G.P[0].S_dg1;
   QA_TRY_CUDA(launch_tt_dg1_group(x, T, K, dz1, g1p, G.P[0].S_dg1, G.P[0].HS, dz1b, G.P[0].K2p, n, &s_dg1, s),
               "group TT x pass");
+  {  // every member's core-gradient partials (fixed order) and B_ext in one launch
+    const float* parts[3 * kMaxGroup];
+    int nparts[3 * kMaxGroup];
+    int64_t numel[3 * kMaxGroup];
+    float* outs[3 * kMaxGroup];
+    const float* g1s[kMaxGroup];
+    __nv_bfloat16* bexts[kMaxGroup];
+    for (int i = 0; i < n; ++i) {
+      const LinearPlan& P = G.P[i];
+      const float* pp[3] = {P.g1p, P.g2p, P.g3p};
+      const int np[3] = {s_dg1, P.TS, P.HS * P.TS};
+      for (int k = 0; k < 3; ++k) {
+        parts[3 * i + k] = pp[k];
+        nparts[3 * i + k] = np[k];
+        numel[3 * i + k] = G.dd[i].core_numel(k);
+        outs[3 * i + k] = dcores[i][k];
+      }
+      g1s[i] = tt[i]->cores[0];
+      bexts[i] = dx != nullptr && dx[i] != nullptr ? P.bext : nullptr;
+    }
+    QA_TRY_CUDA(launch_grad_reduce_n(n, parts, nparts, numel, outs, accumulate != 0, G.P[0].R1, G.P[0].J1, g1s, bexts,
+                                     K, G.P[0].K2p, s),
+                "reduce core gradients + B_ext");
+  }
   for (int i = 0; i < n; ++i) {
     LinearPlan& P = G.P[i];
-    const float* parts[3] = {P.g1p, P.g2p, P.g3p};
-    const int nparts[3] = {s_dg1, P.TS, P.HS * P.TS};
-    const int64_t numel[3] = {G.dd[i].core_numel(0), G.dd[i].core_numel(1), G.dd[i].core_numel(2)};
-    float* outs[3] = {dcores[i][0], dcores[i][1], dcores[i][2]};
     const bool want_dx = dx != nullptr && dx[i] != nullptr;
-    QA_TRY_CUDA(launch_grad_reduce3(parts, nparts, numel, outs, accumulate != 0, P.R1, P.J1, tt[i]->cores[0],
-                                    want_dx ? P.bext : nullptr, K, P.K2p, s),
-                "reduce core gradients + B_ext");
     if (!want_dx) continue;
     QA_TRY_CUDA(launch_dequantize(w[i]->codes, w[i]->scale, w[i]->offset, P.N, K, w[i]->bits, P.wdt, QA_BF16, P.Np,
                                   true, s, nullptr),

@@ -191,6 +191,10 @@ cudaError_t launch_tt_dg1_group(const void* x, int64_t T, int64_t K, const float
 cudaError_t launch_grad_reduce3(const float* const* parts, const int* nparts, const int64_t* numel,
                                 float* const* outs, bool accumulate, int R1, int J1, const float* G1,
                                 __nv_bfloat16* bext, int64_t K, int64_t ldb, cudaStream_t s);
+// the same for the n <= 3 members of a shared-input group in one launch (arrays of 3 n sets, n B_ext jobs)
+cudaError_t launch_grad_reduce_n(int n, const float* const* parts, const int* nparts, const int64_t* numel,
+                                 float* const* outs, bool accumulate, int R1, int J1, const float* const* G1,
+                                 __nv_bfloat16* const* bext, int64_t K, int64_t ldb, cudaStream_t s);
 
 // ------------------------------------------------------------ tcgen05 GEMM
 struct GemmEpilogue {

@@ -1695,13 +1695,16 @@ struct ReduceSet {
   int64_t numel;
   float* out;
 };
+constexpr int kRedMembers = 3;  // members of a shared-input group reduced in one launch
 struct ReduceArgs {
-  ReduceSet set[3];
-  int64_t blocks[3];
+  ReduceSet set[3 * kRedMembers];
+  int64_t blocks[3 * kRedMembers];
+  int nsets;
   int accumulate;
   int R1, J1;
-  const float* G1;
-  __nv_bfloat16* bext;
+  const float* G1s[kRedMembers];  // B_ext jobs: member j's first core and output (null: none)
+  __nv_bfloat16* bexts[kRedMembers];
+  int64_t bext_blocks;            // blocks per B_ext job
   int64_t K, ldb;
 };
 
@@ -1709,11 +1712,15 @@ __global__ void __launch_bounds__(256) k_grad_reduce3(const ReduceArgs a) {
   __shared__ float red[8][33];
   int64_t b = blockIdx.x;
   int si = 0;
-  while (si < 3 && b >= a.blocks[si]) b -= a.blocks[si++];
-  if (si == 3) {  // B_ext rows
+  while (si < a.nsets && b >= a.blocks[si]) b -= a.blocks[si++];
+  if (si == a.nsets) {  // B_ext rows of job b / bext_blocks
+    const int jb = static_cast<int>(b / a.bext_blocks);
+    b -= jb * a.bext_blocks;
+    const float* G1 = a.G1s[jb];
+    __nv_bfloat16* bext = a.bexts[jb];
     // 32-bit index math (K * ldb < 2^31, checked by the launcher)
     const int idx = static_cast<int>(b) * 256 + static_cast<int>(threadIdx.x);
-    if (a.bext == nullptr || idx >= static_cast<int>(a.K * a.ldb)) return;
+    if (bext == nullptr || idx >= static_cast<int>(a.K * a.ldb)) return;
     const int ldb = static_cast<int>(a.ldb);
     const int k = idx / ldb;
     const int c = idx - k * ldb;
@@ -1723,10 +1730,10 @@ __global__ void __launch_bounds__(256) k_grad_reduce3(const ReduceArgs a) {
       const int cc = c % K2;
       const int aa = cc / a.J1, Jp = cc % a.J1;
       const int j1 = k / a.J1;
-      if (k - j1 * a.J1 == Jp) v = __ldg(a.G1 + static_cast<int64_t>(j1) * a.R1 + aa);
+      if (k - j1 * a.J1 == Jp) v = __ldg(G1 + static_cast<int64_t>(j1) * a.R1 + aa);
       if (c >= 2 * K2) v -= __bfloat162float(__float2bfloat16_rn(v));
     }
-    a.bext[idx] = __float2bfloat16_rn(v);
+    bext[idx] = __float2bfloat16_rn(v);
     return;
   }
   const ReduceSet& S = a.set[si];
@@ -2487,13 +2494,15 @@ cudaError_t launch_tt_bwd_fused(const __nv_bfloat16* dy, int64_t ldy, int64_t T,
   return cudaGetLastError();
 }
 
-cudaError_t launch_grad_reduce3(const float* const* parts, const int* nparts, const int64_t* numel,
-                                float* const* outs, bool accumulate, int R1, int J1, const float* G1,
-                                __nv_bfloat16* bext, int64_t K, int64_t ldb, cudaStream_t s) {
-  ReduceArgs a;
+cudaError_t launch_grad_reduce_n(int n, const float* const* parts, const int* nparts, const int64_t* numel,
+                                 float* const* outs, bool accumulate, int R1, int J1, const float* const* G1,
+                                 __nv_bfloat16* const* bext, int64_t K, int64_t ldb, cudaStream_t s) {
+  if (n < 1 || n > kRedMembers) return cudaErrorInvalidValue;
+  ReduceArgs a{};
   int64_t total = 0;
   double bytes = 0.0;
-  for (int i = 0; i < 3; ++i) {
+  a.nsets = 3 * n;
+  for (int i = 0; i < 3 * n; ++i) {
     a.set[i] = ReduceSet{parts[i], nparts[i], numel[i], outs[i]};
     a.blocks[i] = (parts[i] != nullptr && outs[i] != nullptr) ? (numel[i] + 31) / 32 : 0;
     total += a.blocks[i];
@@ -2502,19 +2511,32 @@ cudaError_t launch_grad_reduce3(const float* const* parts, const int* nparts, co
   a.accumulate = accumulate ? 1 : 0;
   a.R1 = R1;
   a.J1 = J1;
-  a.G1 = G1;
-  a.bext = bext;
   a.K = K;
   a.ldb = ldb;
-  if (bext != nullptr) {
+  a.bext_blocks = (K * ldb + 255) / 256;
+  int nb = 0;  // B_ext jobs run after the sets, in member order (a member without one leaves an idle range)
+  for (int j = 0; j < n; ++j) {
+    a.G1s[j] = G1[j];
+    a.bexts[j] = bext != nullptr ? bext[j] : nullptr;
+    if (a.bexts[j] != nullptr) nb = j + 1;
+  }
+  if (nb > 0) {
     if (K * ldb >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
-    total += (K * ldb + 255) / 256;
+    total += nb * a.bext_blocks;
+    for (int j = 0; j < nb; ++j)
+      if (a.bexts[j] != nullptr) bytes += 2.0 * double(K) * ldb;
   }
   if (total == 0) return cudaSuccess;
-  LaunchScope scope(kTT, bytes + (bext ? 2.0 * double(K) * ldb : 0.0), s);
+  LaunchScope scope(kTT, bytes, s);
   count_launches(1);
   k_grad_reduce3<<<static_cast<unsigned>(total), 256, 0, s>>>(a);
   return cudaGetLastError();
+}
+
+cudaError_t launch_grad_reduce3(const float* const* parts, const int* nparts, const int64_t* numel,
+                                float* const* outs, bool accumulate, int R1, int J1, const float* G1,
+                                __nv_bfloat16* bext, int64_t K, int64_t ldb, cudaStream_t s) {
+  return launch_grad_reduce_n(1, parts, nparts, numel, outs, accumulate, R1, J1, &G1, &bext, K, ldb, s);
 }
 
 // ---- shared-input groups (a decoder layer's q / k / v and up / gate, transformer.py:862-874):
