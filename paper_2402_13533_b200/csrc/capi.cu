@@ -531,6 +531,7 @@ int linear_forward_impl(const qa_qweight* w, const qa_tt* tt, const void* x, int
     ext.B2 = P.v;
     ext.ldb2 = P.K2p;
     ext.K2 = P.K2p;
+    ext.k2_valid = 3 * int64_t(P.K2);  // [hi | lo | hi] planes of K2 columns, zero beyond
   } else {
     // (2) per-token activation quantisation: quantize_rows on x[T, K] (codes padded to Kp with zeros)
     QA_TRY_CUDA(launch_quantize_rows(x, x_dtype, T, K, K, 8, P.xcodes, P.Kp, P.Kp, P.sx, P.ox, P.rsx, nullptr, s),
@@ -554,6 +555,7 @@ int linear_forward_impl(const qa_qweight* w, const qa_tt* tt, const void* x, int
     ext.B2 = P.b2;
     ext.ldb2 = P.K2g;
     ext.K2 = P.K2g;
+    ext.k2_valid = 3 * P.Kg;
   }
 
   // (3) int8 tcgen05 GEMM with the dequantising epilogue (+ y2)
@@ -677,6 +679,7 @@ int linear_backward_impl(const qa_qweight* w, const qa_tt* tt, const void* x, in
         ext.B2 = P.bext;
         ext.ldb2 = P.K2p;
         ext.K2 = P.K2p;
+        ext.k2_valid = 3 * int64_t(P.K2);  // [hi | lo | hi] planes of K2 columns, zero beyond
       }
     }
     const float* zd = zf;
@@ -744,6 +747,7 @@ int linear_backward_impl(const qa_qweight* w, const qa_tt* tt, const void* x, in
       ext.B2 = P.bext;
       ext.ldb2 = P.K2p;
       ext.K2 = P.K2p;
+      ext.k2_valid = 3 * int64_t(P.K2);  // [hi | lo | hi] planes of K2 columns, zero beyond
     }
     }  // !P.fused
   } else if (pd != nullptr) {
@@ -769,6 +773,7 @@ int linear_backward_impl(const qa_qweight* w, const qa_tt* tt, const void* x, in
       ext.B2 = P.b2;
       ext.ldb2 = P.N2g;
       ext.K2 = P.N2g;
+      ext.k2_valid = 3 * P.Ng;
     }
   }
 
@@ -1012,6 +1017,7 @@ int qa_group_forward(int n, const qa_qweight* const* w, const qa_tt* const* tt, 
     ext.B2 = P.v;
     ext.ldb2 = P.K2p;
     ext.K2 = P.K2p;
+    ext.k2_valid = 3 * int64_t(P.K2);  // [hi | lo | hi] planes of K2 columns, zero beyond
     QA_TRY(gemm_tc(0, P0.xcodes, P0.Kp, wop, P.Kp, T, P.N, P0.Kp, e, s, &ext));
   }
   return QA_OK;
@@ -1129,6 +1135,7 @@ int qa_group_backward(int n, const qa_qweight* const* w, const qa_tt* const* tt,
     ext.B2 = P.bext;
     ext.ldb2 = P.K2p;
     ext.K2 = P.K2p;
+    ext.k2_valid = 3 * int64_t(P.K2);  // [hi | lo | hi] planes of K2 columns, zero beyond
     QA_TRY(gemm_tc(1, dy[i], P.N, P.wdt, P.Np, T, K, P.Np, e, s, &ext));
   }
   return QA_OK;

@@ -52,6 +52,7 @@ constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 4 * BN 
 struct KParams {
   int64_t M, N, K;  // K in elements of the main operands
   int num_ext;      // extension k-blocks (bf16, 64 elements each)
+  int ext_last;     // 16-element MMA steps of the last extension k-block that hold nonzero columns (1..4)
   int tma_store;    // CTA-pair kernel: bf16 output through shared memory + TMA stores (tmC)
   int group_m;      // CTA-pair kernel: tile raster in groups of group_m M-tiles (M fastest inside a group)
   GemmEpilogue e;
@@ -207,7 +208,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       constexpr uint32_t idesc = KIND == 0 ? make_idesc(2, 0, 0, BM, BN) : make_idesc(1, 1, 1, BM, BN);
       constexpr uint32_t idesc_ext = make_idesc(1, 1, 1, BM, BN);
       uint32_t q = 0;
-      auto block = [&](uint32_t dcol, bool ext, bool first) {
+      auto block = [&](uint32_t dcol, bool ext, bool first, int nk = BK_BYTES / 32) {
         const int s = q % STAGES;
         mbar_wait(&full[s], (q / STAGES) & 1);
         tc_fence_after();
@@ -215,6 +216,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint64_t b0 = smem_desc_kmajor_sw128(sB + s * B_BYTES);
 #pragma unroll
         for (int k = 0; k < BK_BYTES / 32; ++k) {
+          if (k >= nk) break;  // the zero-padded tail of the last extension k-block
           const uint64_t adv = static_cast<uint64_t>((k * 32) >> 4);
           const uint32_t acc = (first && k == 0) ? 0u : 1u;
           if (!ext && KIND == 0)
@@ -229,7 +231,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t pb = i & 1;
         mbar_wait(&y1_ready[pb], (i >> 1) & 1);
         tc_fence_after();
-        for (int e = 0; e < num_ext; ++e) block(tmem_base + pb * 256, true, false);
+        for (int e = 0; e < num_ext; ++e) block(tmem_base + pb * 256, true, false, e + 1 == num_ext ? p.ext_last : 4);
         mma_commit(&y_full[pb]);
       };
       for (int i = 0; i < my_tiles; ++i) {
@@ -242,7 +244,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (fold_ext && i > 0) fold(i - 1);
         for (int kb = split; kb < num_main; ++kb) block(d, false, false);
         if (KIND == 1)
-          for (int e = 0; e < num_ext; ++e) block(d, true, false);
+          for (int e = 0; e < num_ext; ++e) block(d, true, false, e + 1 == num_ext ? p.ext_last : 4);
         mma_commit(&acc_full[b]);
       }
       if (fold_ext && my_tiles > 0) fold(my_tiles - 1);
@@ -535,7 +537,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       constexpr uint32_t idesc = KIND == 0 ? make_idesc(2, 0, 0, BM2, BN) : make_idesc(1, 1, 1, BM2, BN);
       constexpr uint32_t idesc_ext = make_idesc(1, 1, 1, BM2, BN);
       uint32_t q = 0;
-      auto block = [&](uint32_t dcol, bool ext, bool first) {
+      auto block = [&](uint32_t dcol, bool ext, bool first, int nk = BK_BYTES / 32) {
         const int s = q % STAGES2;
         mbar_wait(&full[s], (q / STAGES2) & 1);
         tc_fence_after();
@@ -543,6 +545,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         const uint64_t b0 = smem_desc_kmajor_sw128(sB + s * BH_BYTES);
 #pragma unroll
         for (int k = 0; k < BK_BYTES / 32; ++k) {
+          if (k >= nk) break;  // the zero-padded tail of the last extension k-block
           const uint64_t adv = static_cast<uint64_t>((k * 32) >> 4);
           const uint32_t acc = (first && k == 0) ? 0u : 1u;
           if (!ext && KIND == 0)
@@ -557,7 +560,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         const uint32_t pb = i & 1;
         mbar_wait(&y1_ready[pb], (i >> 1) & 1);
         tc_fence_after();
-        for (int e = 0; e < num_ext; ++e) block(tmem_base + pb * 256, true, false);
+        for (int e = 0; e < num_ext; ++e) block(tmem_base + pb * 256, true, false, e + 1 == num_ext ? p.ext_last : 4);
         mma_commit_2sm(&y_full[pb]);
       };
       for (int i = 0; i < my_tiles; ++i) {
@@ -570,7 +573,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         if (fold_ext && i > 0) fold(i - 1);
         for (int kb = split; kb < num_main; ++kb) block(d, false, false);
         if (KIND == 1)
-          for (int e = 0; e < num_ext; ++e) block(d, true, false);
+          for (int e = 0; e < num_ext; ++e) block(d, true, false, e + 1 == num_ext ? p.ext_last : 4);
         mma_commit_2sm(&acc_full[b]);
       }
       if (fold_ext && my_tiles > 0) fold(my_tiles - 1);
@@ -906,6 +909,11 @@ int launch(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, in
   p.N = N;
   p.K = K;
   p.num_ext = num_ext;
+  p.ext_last = 4;
+  if (num_ext > 0 && ext->k2_valid > 0 && ext->k2_valid <= ext->K2) {
+    const int64_t tail = ext->k2_valid - int64_t(num_ext - 1) * 64;  // nonzero columns of the last k-block
+    p.ext_last = tail <= 0 ? 4 : static_cast<int>((tail + 15) / 16 < 4 ? (tail + 15) / 16 : 4);
+  }
   p.tma_store = 0;
   p.group_m = gemm_group_m(N, K, KIND == 0 ? 1 : 2);
   p.e = epi;

@@ -227,6 +227,7 @@ struct GemmExt {
   const void* B2 = nullptr;
   int64_t ldb2 = 0;
   int64_t K2 = 0;  // multiple of 64 expected (zero padded)
+  int64_t k2_valid = 0;  // columns [k2_valid, K2) are zero in both operands (0: unknown); their MMAs are skipped
 };
 
 // C[M, N] = A[M, K] · B[N, K]ᵀ, both operands K-major with row strides lda / ldb (elements).
