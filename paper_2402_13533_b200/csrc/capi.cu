@@ -503,8 +503,10 @@ int linear_forward_impl(const qa_qweight* w, const qa_tt* tt, const void* x, int
     } else {
       float* zlw = P.fd == 3 ? P.z2 : (z1_save != nullptr ? z1_save : P.zf);
       ldz = P.fd == 3 ? int64_t(P.H) * P.C : P.K2;
-      QA_TRY_CUDA(launch_decode_prep(x, T, K, P.xcodes, P.Kp, P.sx, P.ox, P.rsx, tt->cores[0], P.J1, P.R1,
-                                     tt->cores[1], P.fd, P.H, P.C, z1_save, zlw, ldz, s, chain_prologue),
+      DecodePrepMembers dm{};
+      dm.n = 1;
+      dm.m[0] = DecodePrepMember{tt->cores[0], tt->cores[1], P.fd, P.H, P.C, z1_save, zlw, ldz};
+      QA_TRY_CUDA(launch_decode_prep(x, T, K, P.xcodes, P.Kp, P.sx, P.ox, P.rsx, P.J1, P.R1, dm, s, chain_prologue),
                   "decode prologue");
       zl = zlw;
       gl = tt->cores[P.fd - 1];
@@ -954,6 +956,37 @@ int qa_group_forward(int n, const qa_qweight* const* w, const qa_tt* const* tt, 
   bool decode = x_dtype == QA_BF16 && reinterpret_cast<uintptr_t>(x) % 16 == 0;
   for (int i = 0; i < n && decode; ++i)
     decode = gemv_ok(tokens, w[i]->cols, w[i]->bits) && (tt[i] == nullptr || (G.P[i].fast && G.P[i].C <= 32));
+  // decode with every member adapted alike: one prologue launch (member 0's CTAs write the shared activation
+  // codes) and one matrix-vector launch over all members' rows
+  bool decode_group = decode && n <= 3;
+  for (int i = 0; i < n && decode_group; ++i) {
+    const LinearPlan& P = G.P[i];
+    decode_group = tt[i] != nullptr && P.fast && P.J1 == G.P[0].J1 && P.R1 == G.P[0].R1 &&
+                   w[i]->bits == w[0]->bits && gemv_mma_ok(w[i]->cols, P.N, tt[i]->cores[P.fd - 1], P.M, P.C);
+  }
+  if (decode_group) {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const LinearPlan& P0 = G.P[0];
+    const int64_t T = tokens, K = w[0]->cols;
+    DecodePrepMembers dm{};
+    GemvMembers gm{};
+    dm.n = gm.n = n;
+    for (int i = 0; i < n; ++i) {
+      const LinearPlan& P = G.P[i];
+      const size_t need = sizeof(float) * static_cast<size_t>(tokens) * P.K2;
+      float* sv = (saved != nullptr && saved[i] != nullptr && saved_bytes != nullptr && saved_bytes[i] >= need)
+                      ? static_cast<float*>(saved[i]) : nullptr;
+      float* zlw = P.fd == 3 ? P.z2 : (sv != nullptr ? sv : P.zf);
+      const int64_t ldz = P.fd == 3 ? int64_t(P.H) * P.C : P.K2;
+      dm.m[i] = DecodePrepMember{tt[i]->cores[0], tt[i]->cores[1], P.fd, P.H, P.C, sv, zlw, ldz};
+      gm.m[i] = GemvMember{w[i]->codes, P.N, w[i]->scale, w[i]->offset, w[i]->rowsum, zlw, ldz,
+                           tt[i]->cores[P.fd - 1], P.M, P.C, nullptr, static_cast<__nv_bfloat16*>(y[i]), nullptr, 0};
+    }
+    QA_TRY_CUDA(launch_decode_prep(x, T, K, P0.xcodes, P0.Kp, P0.sx, P0.ox, P0.rsx, P0.J1, P0.R1, dm, s, false),
+                "group decode prologue");
+    return cuda_status(launch_gemv_members(P0.xcodes, P0.Kp, T, P0.sx, P0.ox, P0.rsx, K, w[0]->bits, gm, s),
+                       "group decode gemv");
+  }
   const bool fast = G.fast && x_dtype == QA_BF16 && !decode;
   if (!fast) {  // the members' single-linear forwards
     for (int i = 0; i < n; ++i) {

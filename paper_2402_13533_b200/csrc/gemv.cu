@@ -226,24 +226,36 @@ __device__ __forceinline__ void gm_step(int (&acc)[4], const typename GmW<BITS>:
   }
 }
 
+// The members of a shared-input group (q / k / v, up / gate) in one launch: CTA b belongs to the member whose
+// [cta0, next cta0) range holds it, and reads that member's weights, epilogue terms and adapter input.
 template <int BITS>
 __global__ void __launch_bounds__(GM_WARPS * 32) k_gemv_mma(const uint8_t* __restrict__ xc, int64_t ldx, int T,
                                                             const float* __restrict__ sx, const float* __restrict__ ox,
-                                                            const int32_t* __restrict__ rsx,
-                                                            const uint8_t* __restrict__ wc, int64_t N, int64_t K,
-                                                            const float* __restrict__ ws, const float* __restrict__ wo,
-                                                            const int32_t* __restrict__ wrs,
-                                                            const float* __restrict__ zl, int64_t ldz,
-                                                            const float* __restrict__ Gl, int64_t Ml, int Cl,
-                                                            const float* __restrict__ addend,
-                                                            __nv_bfloat16* __restrict__ out, float* __restrict__ out32) {
+                                                            const int32_t* __restrict__ rsx, int64_t K,
+                                                            const GemvMembers mem) {
   using W = typename GmW<BITS>::T;
   constexpr int SB = BITS == 8 ? 64 : 32;  // weight bytes per row per 64-column step
   __shared__ int red[GM_WARPS][16][8];
   // let a chained next prologue (a programmatic dependent, see launch_decode_prep) start right away
   asm volatile("griddepcontrol.launch_dependents;");
+  int mi = 0;
+  while (mi + 1 < mem.n && static_cast<int>(blockIdx.x) >= mem.m[mi + 1].cta0) ++mi;
+  const GemvMember& M = mem.m[mi];
+  const uint8_t* __restrict__ wc = M.wc;
+  const int64_t N = M.N;
+  const float* __restrict__ ws = M.ws;
+  const float* __restrict__ wo = M.wo;
+  const int32_t* __restrict__ wrs = M.wrs;
+  const float* __restrict__ zl = M.zl;
+  const int64_t ldz = M.ldz;
+  const float* __restrict__ Gl = M.Gl;
+  const int64_t Ml = M.Ml;
+  const int Cl = M.Cl;
+  const float* __restrict__ addend = M.addend;
+  __nv_bfloat16* __restrict__ out = M.out;
+  float* __restrict__ out32 = M.out32;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
-  const int64_t n0 = static_cast<int64_t>(blockIdx.x) * 16;
+  const int64_t n0 = static_cast<int64_t>(blockIdx.x - M.cta0) * 16;
   const int64_t ldw = BITS == 8 ? K : K / 2;
   const int64_t nsteps = K / 64;
   const int64_t per = (nsteps + GM_WARPS - 1) / GM_WARPS;
@@ -357,6 +369,41 @@ __global__ void __launch_bounds__(GM_WARPS * 32) k_gemv_mma(const uint8_t* __res
 // prologue still runs).
 bool pdl_enabled() { return true; }
 
+bool gemv_mma_ok(int64_t K, int64_t N, const float* Gl, int64_t Ml, int Cl) {
+  return K % 64 == 0 && (Gl == nullptr || ((Ml % 16 == 0 || Ml >= N) && Cl <= 32));
+}
+
+cudaError_t launch_gemv_members(const uint8_t* xc, int64_t ldx, int64_t T, const float* sx, const float* ox,
+                                const int32_t* rsx, int64_t K, int bits, GemvMembers mem, cudaStream_t s) {
+  if (T == 0 || mem.n < 1) return cudaSuccess;
+  int ctas = 0;
+  double flops = 0.0;
+  for (int i = 0; i < mem.n; ++i) {
+    if (!gemv_mma_ok(K, mem.m[i].N, mem.m[i].Gl, mem.m[i].Ml, mem.m[i].Cl)) return cudaErrorInvalidValue;
+    mem.m[i].cta0 = ctas;
+    ctas += static_cast<int>((mem.m[i].N + 15) / 16);
+    flops += 2.0 * double(T) * mem.m[i].N * K;
+  }
+  LaunchScope scope(kGemmI8, flops, s);
+  count_launches(1);
+  // programmatic dependent launch: the CTAs may start while the preceding prologue still runs
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(ctas));
+  cfg.blockDim = dim3(GM_WARPS * 32);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  const int Ti = static_cast<int>(T);
+  cudaError_t e = bits == 8 ? cudaLaunchKernelEx(&cfg, k_gemv_mma<8>, xc, ldx, Ti, sx, ox, rsx, K, mem)
+                            : cudaLaunchKernelEx(&cfg, k_gemv_mma<4>, xc, ldx, Ti, sx, ox, rsx, K, mem);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
 bool gemv_ok(int64_t T, int64_t K, int bits) {
   return T >= 1 && T <= 8 && (bits == 8 ? K % 16 == 0 : K % 32 == 0);
 }
@@ -366,6 +413,13 @@ cudaError_t launch_gemv(const uint8_t* xc, int64_t ldx, int64_t T, const float* 
                         const float* wo, const int32_t* wrs, const float* zl, int64_t ldz, const float* Gl,
                         int64_t Ml, int Cl, const float* addend, __nv_bfloat16* out, float* out32, cudaStream_t s) {
   if (T == 0 || N == 0) return cudaSuccess;
+  // the tensor-core pass keeps one Zlast block per 16-row tile (16 | Ml, or a single block) and Cl <= 32
+  if (gemv_mma_ok(K, N, Gl, Ml, Cl)) {
+    GemvMembers mem{};
+    mem.n = 1;
+    mem.m[0] = GemvMember{wc, N, ws, wo, wrs, zl, ldz, Gl, Ml, Cl, addend, out, out32, 0};
+    return launch_gemv_members(xc, ldx, T, sx, ox, rsx, K, bits, mem, s);
+  }
   LaunchScope scope(kGemmI8, 2.0 * double(T) * N * K, s);
   count_launches(1);
   // programmatic dependent launch: the CTAs may start while the preceding prologue still runs
@@ -390,19 +444,6 @@ cudaError_t launch_gemv(const uint8_t* xc, int64_t ldx, int64_t T, const float* 
     else                                                                                                          \
       e = cudaLaunchKernelEx(&cfg, k_gemv<MM, 4>, xc, ldx, Ti, sx, ox, rsx, wc, N, K, ws, wo, wrs, zl, ldz, Gl, Ml, \
                              Cl, addend, out, out32);                                                             \
-  }
-  // the tensor-core pass keeps one Zlast block per 16-row tile (16 | Ml, or a single block) and Cl <= 32
-  if (K % 64 == 0 && (Gl == nullptr || ((Ml % 16 == 0 || Ml >= N) && Cl <= 32))) {
-    cfg.gridDim = dim3(static_cast<unsigned>((N + 15) / 16));
-    cfg.blockDim = dim3(GM_WARPS * 32);
-    if (bits == 8)
-      e = cudaLaunchKernelEx(&cfg, k_gemv_mma<8>, xc, ldx, Ti, sx, ox, rsx, wc, N, K, ws, wo, wrs, zl, ldz, Gl, Ml, Cl,
-                             addend, out, out32);
-    else
-      e = cudaLaunchKernelEx(&cfg, k_gemv_mma<4>, xc, ldx, Ti, sx, ox, rsx, wc, N, K, ws, wo, wrs, zl, ldz, Gl, Ml, Cl,
-                             addend, out, out32);
-    if (e != cudaSuccess) return e;
-    return cudaGetLastError();
   }
   if (T == 1)
     QA_GV(1)

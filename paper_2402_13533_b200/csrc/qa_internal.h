@@ -92,10 +92,48 @@ cudaError_t launch_gemv(const uint8_t* xc, int64_t ldx, int64_t T, const float* 
                         const int32_t* rsx, const uint8_t* wc, int64_t N, int64_t K, int bits, const float* ws,
                         const float* wo, const int32_t* wrs, const float* zl, int64_t ldz, const float* Gl,
                         int64_t Ml, int Cl, const float* addend, __nv_bfloat16* out, float* out32, cudaStream_t s);
-// decode prologue (tt_fast.cu): act-quant of T <= 8 bf16 rows + Z1 + the last core's input Zlast
+// Decode-size forward (1..8 tokens, gemv.cu / tt_fast.cu): one prologue launch and one matrix-vector launch per
+// linear or shared-input group.  Members share x (the activation codes of member 0's workspace) and K.
+struct GemvMember {
+  const uint8_t* wc;  // codes [N][K or K/2]
+  int64_t N;
+  const float* ws;    // scale, offset, Σcodes per row
+  const float* wo;
+  const int32_t* wrs;
+  const float* zl;    // the adapter's last-core input Zlast [T][ldz] (null: no adapter)
+  int64_t ldz;
+  const float* Gl;    // last core [Cl][Ml]
+  int64_t Ml;
+  int Cl;
+  const float* addend;  // optional fp32 [T][N] added to y
+  __nv_bfloat16* out;
+  float* out32;
+  int cta0;           // first CTA of this member (filled by the launcher)
+};
+struct GemvMembers {
+  GemvMember m[3];
+  int n;
+};
+bool gemv_mma_ok(int64_t K, int64_t N, const float* Gl, int64_t Ml, int Cl);
+cudaError_t launch_gemv_members(const uint8_t* xc, int64_t ldx, int64_t T, const float* sx, const float* ox,
+                                const int32_t* rsx, int64_t K, int bits, GemvMembers mem, cudaStream_t s);
+struct DecodePrepMember {
+  const float* G1;
+  const float* G2;  // middle core (d = 3)
+  int d, H, C;
+  float* z1out;     // optional Z1 export
+  float* zlast;     // Zlast [T][ldz]
+  int64_t ldz;
+};
+struct DecodePrepMembers {
+  DecodePrepMember m[3];
+  int n;
+};
 cudaError_t launch_decode_prep(const void* x, int64_t T, int64_t K, uint8_t* codes, int64_t ldc, float* sx, float* ox,
-                               int32_t* rsx, const float* G1, int J1, int R1, const float* G2, int d, int H, int C,
-                               float* z1out, float* zlast, int64_t ldz, cudaStream_t s, bool chain = false);
+                               int32_t* rsx, int J1, int R1, const DecodePrepMembers& mem, cudaStream_t s,
+                               bool chain);
+// decode prologue (tt_fast.cu): act-quant of T <= 8 bf16 rows + Z1 + the last core's input Zlast
+
 
 // AdamW (optim.cu)
 cudaError_t launch_adamw(float* params, double* master, double* m, double* v, const float* g, int64_t n, double lr,

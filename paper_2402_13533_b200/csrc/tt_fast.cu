@@ -671,11 +671,18 @@ template <int J1, int R1>
 __global__ void __launch_bounds__(512) k_decode_prep(const __nv_bfloat16* __restrict__ x, int64_t K,
                                                     uint8_t* __restrict__ codes, int64_t ldc, float* __restrict__ sx,
                                                     float* __restrict__ ox, int32_t* __restrict__ rsx,
-                                                    const float* __restrict__ G1, const float* __restrict__ G2,
-                                                    int d, int H, int C, float* __restrict__ z1out,
-                                                    float* __restrict__ zlast, int64_t ldz, bool vec, bool early) {
+                                                    const DecodePrepMembers mem, bool vec, bool early) {
   DP_MARK(0)
   asm volatile("griddepcontrol.launch_dependents;");
+  // CTA (token, member): every member's Z1 / Zlast; member 0 also writes the shared activation codes
+  const DecodePrepMember& me = mem.m[blockIdx.y];
+  const float* __restrict__ G1 = me.G1;
+  const float* __restrict__ G2 = me.G2;
+  const int d = me.d, H = me.H, C = me.C;
+  float* __restrict__ z1out = me.z1out;
+  float* __restrict__ zlast = me.zlast;
+  const int64_t ldz = me.ldz;
+  const bool coder = blockIdx.y == 0;
   constexpr int K2 = J1 * R1;
   constexpr int NV = K2 < 32 ? K2 : 32;  // values per transpose-reduction round
   constexpr int NJ = 8 / J1;             // G1 rows (j1) per 16-byte chunk of x
@@ -784,6 +791,7 @@ __global__ void __launch_bounds__(512) k_decode_prep(const __nv_bfloat16* __rest
     if (z1out != nullptr) z1out[t * K2 + tid] = v;
   }
   DP_MARK(4)
+  if (coder) {
   // codes of this row (bracketed rule, bit-exact with quant.py:73-99)
   const double lo64 = static_cast<double>(lo);
   const double step64 = __ddiv_rn(__dsub_rn(static_cast<double>(hi), lo64), 255.0);
@@ -823,6 +831,7 @@ __global__ void __launch_bounds__(512) k_decode_prep(const __nv_bfloat16* __rest
     sx[t] = flat ? 0.0f : __double2float_rn(step64);
     ox[t] = lo;
   }
+  }  // coder
   // Zlast: d = 3 -> Z2[i2, b] = Σ_{a, j2} Z1[a, j2] G2[a, i2, j2, b], four lanes per output (K2 / 4 terms
   // each, then two shuffles); d = 2 -> Z1.
   if (d == 3) {
@@ -869,33 +878,34 @@ extern "C" __attribute__((visibility("default"))) int qa_debug_dp_trace(unsigned
 #endif
 
 cudaError_t launch_decode_prep(const void* x, int64_t T, int64_t K, uint8_t* codes, int64_t ldc, float* sx, float* ox,
-                               int32_t* rsx, const float* G1, int J1, int R1, const float* G2, int d, int H, int C,
-                               float* z1out, float* zlast, int64_t ldz, cudaStream_t s, bool chain) {
-  if (T == 0) return cudaSuccess;
+                               int32_t* rsx, int J1, int R1, const DecodePrepMembers& mem, cudaStream_t s,
+                               bool chain) {
+  if (T == 0 || mem.n < 1) return cudaSuccess;
   LaunchScope scope(kQuantize, double(T) * K * 3 + 12.0 * T, s);
   count_launches(1);
   const int64_t nch = K / 8;  // one 16-byte chunk per thread, 128..512 threads
   const int threads = static_cast<int>(nch >= 512 ? 512 : (nch <= 128 ? 128 : (nch + 31) / 32 * 32));
-  const size_t n2 = d == 3 ? static_cast<size_t>(R1) * H * J1 * C : 0;
+  size_t n2 = 0;
+  bool vec = true;  // vector / cp.async paths need 16-byte aligned cores (G1 rows of a chunk start at multiples of 32 floats)
+  for (int i = 0; i < mem.n; ++i) {
+    const DecodePrepMember& m = mem.m[i];
+    const size_t n2i = m.d == 3 ? static_cast<size_t>(R1) * m.H * J1 * m.C : 0;
+    n2 = n2i > n2 ? n2i : n2;
+    vec = vec && reinterpret_cast<uintptr_t>(m.G1) % 16 == 0 &&
+          (m.G2 == nullptr || reinterpret_cast<uintptr_t>(m.G2) % 16 == 0) && n2i % 4 == 0;
+  }
   const size_t smem = (static_cast<size_t>(K) * 2 + 15) / 16 * 16 + sizeof(float) * n2;
-  // vector / cp.async paths need 16-byte aligned cores (G1 rows of a chunk start at multiples of 32 floats)
-  const bool vec = (reinterpret_cast<uintptr_t>(G1) % 16 == 0) && (G2 == nullptr || reinterpret_cast<uintptr_t>(G2) % 16 == 0) &&
-                   n2 % 4 == 0;
-  // chain: launched as a programmatic dependent of the previous group member's matrix-vector pass (which
-  // releases its dependents at once); this prologue reads only x and its own cores and writes its own
-  // workspace, and it waits for that pass before exiting (griddepcontrol.wait at its end), so stream order
-  // still holds for every later kernel
+  // every prologue is a programmatic dependent: a chained member (x already complete) overlaps the previous
+  // member's pass; the first one (early) prefetches its cores and waits for x's producer before reading it
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(static_cast<unsigned>(T));
+  cfg.gridDim = dim3(static_cast<unsigned>(T), static_cast<unsigned>(mem.n));
   cfg.blockDim = dim3(threads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cfg.attrs = attr;
-  // every prologue is a programmatic dependent: a chained member (x already complete) overlaps the previous
-  // member's pass; the first one (early) prefetches its cores and waits for x's producer before reading it
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
   const bool early = !chain;
   const __nv_bfloat16* xb = static_cast<const __nv_bfloat16*>(x);
@@ -903,8 +913,7 @@ cudaError_t launch_decode_prep(const void* x, int64_t T, int64_t K, uint8_t* cod
 #define QA_DPR(JJ, RR)                                                                                             \
   {                                                                                                                \
     cudaFuncSetAttribute(k_decode_prep<JJ, RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)); \
-    e = cudaLaunchKernelEx(&cfg, k_decode_prep<JJ, RR>, xb, K, codes, ldc, sx, ox, rsx, G1, G2, d, H, C, z1out,    \
-                           zlast, ldz, vec, early);                                                                 \
+    e = cudaLaunchKernelEx(&cfg, k_decode_prep<JJ, RR>, xb, K, codes, ldc, sx, ox, rsx, mem, vec, early);          \
   }
   if (J1 == 4 && R1 == 8)
     QA_DPR(4, 8)
