@@ -191,7 +191,9 @@ __global__ void __launch_bounds__(GV_WARPS * 32, 1) k_gemv(const uint8_t* __rest
 // reduction is order-free, each thread feeds the mma the contiguous bytes it loaded (8-bit: 16 B of
 // a row = two k32 steps; 4-bit: 8 packed bytes unpacked to even / odd columns) with the activation
 // bytes of the same columns. A CTA owns 16 rows; its 8 warps split K and meet in shared memory.
-constexpr int GM_WARPS = 8, GM_MAXS = 4;  // warps (K split) per CTA, 64-column steps held in registers
+// warps (K split) per CTA and 64-column steps held in registers: 8 steps = a 4096-wide row slice per warp in one
+// round trip, at two CTAs per SM (measured: 93.5 -> 76.2 us for the 7-linear decode step against 4 steps)
+constexpr int GM_WARPS = 8, GM_MAXS = 8;
 
 __device__ __forceinline__ void mma_u8_16832(int (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                                              uint32_t b0, uint32_t b1) {
@@ -229,7 +231,7 @@ __device__ __forceinline__ void gm_step(int (&acc)[4], const typename GmW<BITS>:
 // The members of a shared-input group (q / k / v, up / gate) in one launch: CTA b belongs to the member whose
 // [cta0, next cta0) range holds it, and reads that member's weights, epilogue terms and adapter input.
 template <int BITS>
-__global__ void __launch_bounds__(GM_WARPS * 32) k_gemv_mma(const uint8_t* __restrict__ xc, int64_t ldx, int T,
+__global__ void __launch_bounds__(GM_WARPS * 32, 2) k_gemv_mma(const uint8_t* __restrict__ xc, int64_t ldx, int T,
                                                             const float* __restrict__ sx, const float* __restrict__ ox,
                                                             const int32_t* __restrict__ rsx, int64_t K,
                                                             const GemvMembers mem) {
