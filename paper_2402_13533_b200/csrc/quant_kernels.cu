@@ -385,30 +385,32 @@ cudaError_t launch_quantize_rows(const void* w, int w_dtype, int64_t rows, int64
   const bool vec_out = bits == 8 ? ((reinterpret_cast<uintptr_t>(codes) % 8 == 0) && (ld_codes % 8 == 0))
                                  : ((reinterpret_cast<uintptr_t>(codes) % 4 == 0) && (ld_codes % 4 == 0));
   const int vec_ok = vec_in && vec_out;
-  // production path: one CTA per row, the row in registers (cols a multiple of 8, up to 32768); rows up to
-  // 16384 columns take 128-thread CTAs with up to 16 chunks per thread (more bytes in flight per register)
-  const int qthreads = cols <= 128 * 8 * 16 ? 128 : 256;
-  const int64_t per_pass = int64_t(qthreads) * 8;
-  const int ch = vec_ok && cols % 8 == 0 ? static_cast<int>((cols + per_pass - 1) / per_pass) : 0;
-  if (ch >= 1 && ch <= 16) {
-    const int chp = ch <= 1 ? 1 : ch <= 2 ? 2 : ch <= 4 ? 4 : ch <= 8 ? 8 : 16;
+  // production path: one CTA per row, the row in registers (cols a multiple of 8, up to 32768): the (threads,
+  // chunks per thread) shape that covers the row with the fewest idle chunk slots, fewer threads on a tie
+  // (K = 11008 takes 256 x 6 instead of 128 x 16: 1.9 -> 4+ TB/s)
+  static constexpr int kShapes[][2] = {{128, 1}, {128, 2}, {128, 4}, {128, 8}, {256, 6}, {256, 8}, {512, 6}, {512, 8}};
+  const int64_t nchunk = cols / 8;
+  int pick = -1;
+  if (vec_ok && cols % 8 == 0)
+    for (int i = 0; i < 8; ++i) {
+      const int64_t cap = int64_t(kShapes[i][0]) * kShapes[i][1];
+      if (cap < nchunk) continue;
+      if (pick < 0 || cap < int64_t(kShapes[pick][0]) * kShapes[pick][1]) pick = i;
+    }
+  if (pick >= 0) {
 #define QA_QR(TI, BB, CC, TH)                                                                                     \
   k_quantize_rows_reg<TI, BB, CC, TH><<<static_cast<unsigned>(rows), TH, 0, s>>>(                                  \
       static_cast<const TI*>(w), cols, ld_w, codes, ld_codes, pad_cols, scale, offset, rowsum, flag)
-#define QA_QR_C(TI, BB)                                                 \
-  if (qthreads == 128) {                                                \
-    switch (chp) {                                                      \
-      case 1: QA_QR(TI, BB, 1, 128); break;                             \
-      case 2: QA_QR(TI, BB, 2, 128); break;                             \
-      case 4: QA_QR(TI, BB, 4, 128); break;                             \
-      case 8: QA_QR(TI, BB, 8, 128); break;                             \
-      default: QA_QR(TI, BB, 16, 128); break;                           \
-    }                                                                   \
-  } else {                                                              \
-    switch (chp) {                                                      \
-      case 1: case 2: case 4: case 8: QA_QR(TI, BB, 8, 256); break;     \
-      default: QA_QR(TI, BB, 16, 256); break;                           \
-    }                                                                   \
+#define QA_QR_C(TI, BB)                          \
+  switch (pick) {                                \
+    case 0: QA_QR(TI, BB, 1, 128); break;        \
+    case 1: QA_QR(TI, BB, 2, 128); break;        \
+    case 2: QA_QR(TI, BB, 4, 128); break;        \
+    case 3: QA_QR(TI, BB, 8, 128); break;        \
+    case 4: QA_QR(TI, BB, 6, 256); break;        \
+    case 5: QA_QR(TI, BB, 8, 256); break;        \
+    case 6: QA_QR(TI, BB, 6, 512); break;        \
+    default: QA_QR(TI, BB, 8, 512); break;       \
   }
     if (w_dtype == QA_F32) {
       if (bits == 8) {

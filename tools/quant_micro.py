@@ -1,5 +1,5 @@
-"""Weight quantiser in isolation (for ncu): qa_quantize_rows over the 7B gate matrix (11008 x 4096, f32 -> int8)
-and the 70B gate matrix (28672 x 8192, f32 -> int4), a few warm launches each.   python tools/quant_micro.py"""
+"""Weight quantiser in isolation (for ncu): qa_quantize_rows over the 7B shapes (f32 -> int8) and the 70B gate / q
+shapes (f32 -> int4), a few warm launches each.   python tools/quant_micro.py"""
 import os
 import sys
 
@@ -12,7 +12,7 @@ dev = torch.device("cuda", 0)
 lib = _lib.lib()
 s = torch.cuda.current_stream(dev).cuda_stream
 g = torch.Generator(device=dev).manual_seed(3)
-for n, k, bits in ((11008, 4096, 8), (28672, 8192, 4)):
+for n, k, bits in ((4096, 4096, 8), (11008, 4096, 8), (4096, 11008, 8), (28672, 8192, 4), (8192, 8192, 4)):
     w = torch.randn((n, k), generator=g, device=dev) * 0.02
     ld = k if bits == 8 else (k + 1) // 2
     codes = torch.empty((n, ld), dtype=torch.uint8, device=dev)
