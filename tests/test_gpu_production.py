@@ -280,3 +280,28 @@ def test_merge_matches_oracle_at_benchmark_shapes(shape, kind, dtype):
     # W_t alone (qa_tt_materialize, same fused kernel without codes)
     wt = L.tt_materialize(spec, lin._core_tensors())
     assert O.rel_err(_np(wt[torch.from_numpy(rows).cuda()]), O.tt_rows(cores_np, rows)) <= 1e-5
+
+
+@pytest.mark.parametrize("T", [1, 8])
+def test_decode_at_benchmark_shapes(T):
+    """The decode step the bench times (KV-cached decoding, transformer.py:1043-1080) at the 7B shapes: the
+    up / gate group (one prologue launch for both members, one matrix-vector launch over their 22016 rows, each
+    warp holding a 4096-column slice in registers) and the down projection (K = 11008: three register rounds per
+    warp), against the oracle on all tokens and sampled output columns (y within the bf16 bar)."""
+    rng = np.random.default_rng(5)
+    up = _member(11008, 4096, 8, 8, 301, std=0.05, device_w=True)
+    gate = _member(11008, 4096, 8, 8, 303, std=0.05, device_w=True)
+    down = _member(4096, 11008, 8, 8, 305, std=0.05, device_w=True)
+    x = _tokens(T, 4096, 307)
+    xd = _tokens(T, 11008, 309)
+    ys = L.group_forward([up[4], gate[4]], x)
+    yd = down[4].forward(xd)
+    for (W, q, spec, cores_np, lin), y, xin in ((up, ys[0], x), (gate, ys[1], x), (down, yd, xd)):
+        cols = np.sort(rng.choice(q.rows, 512, replace=False))
+        _check_weight_rows(W, q, cols[:64])
+        _, y1, y2 = _ref_forward_rows(_np(xin), q, cores_np, cols)
+        e = O.rel_err(_np(y[:, torch.from_numpy(cols).cuda()]), y1 + y2)
+        print(f"decode {q.rows}x{q.cols} T={T}: y err {e:.2e}")
+        assert e <= TOL_BF16, e
+        # bit-identical to the single-linear decode pass
+        assert torch.equal(y, lin.forward(xin))
