@@ -226,6 +226,21 @@ def test_merge_parity_and_merged_inference(bits):
     assert O.rel_err(_np(y), xs.astype(np.float64) @ O.qa_merge(oq, cores_np).T) <= TOL_BF16
 
 
+@pytest.mark.parametrize("N,K,bits,r", [(320, 520, 8, 8), (320, 520, 4, 16), (1280, 264, 4, 8)])
+def test_fused_merge_ragged_tiles(N, K, bits, r):
+    """The fused merge kernel (k_merge_fast) off the bench shapes: LoRA with N = 320 (64-row tiles, md % 256 != 0),
+    K = 520 / 264 (a partial last column tile), int4 packing with an odd number of column pairs per tile edge and
+    rank 16 (4 columns per lane, 2-byte code words copied by lane pairs): fp32 and bf16 W' against the oracle's
+    dequantise + W_t route (lowrank.py:249-257)."""
+    spec = L.TTSpec.lora(N, K, r)
+    q, oq, x, xs, spec, cores, cores_np = _case(N, K, 16, bits, r, 41, spec)
+    want = O.qa_merge(oq, cores_np)
+    for dt, tol in ((torch.float32, TOL_F32), (torch.bfloat16, 2.0 ** -8)):
+        ad = L.TTLinear("w", L.QuantizedLinear("w.base", q), spec, [c.clone() for c in cores])
+        got = L.tt_merge(ad, dtype=dt)
+        assert got.dtype == dt and O.rel_err(_np(got), want) <= tol, (dt, O.rel_err(_np(got), want))
+
+
 def test_edge_cases():
     q = qa.quantize_rows(O.seeded_random(256, 512, 3, std=0.02), 8)
     spec = L.TTSpec.for_shape(256, 512, 4)
