@@ -1152,13 +1152,29 @@ int qa_group_backward(int n, const qa_qweight* const* w, const qa_tt* const* tt,
                                      K, G.P[0].K2p, s),
                 "reduce core gradients + B_ext");
   }
+  {  // every member's transient deq(W)ᵀ in one launch
+    DequantJobs dj{};
+    int nj = 0;
+    for (int i = 0; i < n; ++i) {
+      if (dx == nullptr || dx[i] == nullptr) continue;
+      const LinearPlan& P = G.P[i];
+      dj.codes[nj] = w[i]->codes;
+      dj.scale[nj] = w[i]->scale;
+      dj.offset[nj] = w[i]->offset;
+      dj.rows[nj] = P.N;
+      dj.cols[nj] = K;
+      dj.ldc[nj] = w[i]->bits == 8 ? K : (K + 1) / 2;
+      dj.ld_out[nj] = P.Np;
+      dj.bits[nj] = w[i]->bits;
+      dj.out[nj] = P.wdt;
+      ++nj;
+    }
+    if (nj > 0) QA_TRY_CUDA(launch_dequantize_t_multi(nj, dj, s), "dequantize T");
+  }
   for (int i = 0; i < n; ++i) {
     LinearPlan& P = G.P[i];
     const bool want_dx = dx != nullptr && dx[i] != nullptr;
     if (!want_dx) continue;
-    QA_TRY_CUDA(launch_dequantize(w[i]->codes, w[i]->scale, w[i]->offset, P.N, K, w[i]->bits, P.wdt, QA_BF16, P.Np,
-                                  true, s, nullptr),
-                "dequantize T");
     GemmEpilogue e;
     e.out_bf16 = static_cast<__nv_bfloat16*>(dx[i]);
     e.ld_out = K;

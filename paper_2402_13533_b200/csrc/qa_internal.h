@@ -21,6 +21,19 @@ cudaError_t launch_quantize_rows(const void* w, int w_dtype, int64_t rows, int64
 cudaError_t launch_dequantize(const uint8_t* codes, const float* scale, const float* offset, int64_t rows,
                               int64_t cols, int bits, void* out, int out_dtype, int64_t ld_out, bool transpose,
                               cudaStream_t s, __nv_bfloat16* out_lo = nullptr);
+// Transposed bf16 dequantisation of up to kDqJobs matrices (a shared-input group's members) in one launch.
+constexpr int kDqJobs = 3;
+struct DequantJobs {
+  const uint8_t* codes[kDqJobs];
+  const float* scale[kDqJobs];
+  const float* offset[kDqJobs];
+  int64_t rows[kDqJobs], cols[kDqJobs], ldc[kDqJobs], ld_out[kDqJobs];
+  int bits[kDqJobs];
+  __nv_bfloat16* out[kDqJobs];
+  int64_t first[kDqJobs + 1];  // first tile of each job (filled by the launcher)
+  int n;
+};
+cudaError_t launch_dequantize_t_multi(int n, const DequantJobs& jobs, cudaStream_t s);
 // 4-bit packed / unpadded codes -> u8 codes [rows, ld_out] with zero padding in [cols, ld_out).
 cudaError_t launch_unpack_pad(const uint8_t* codes, int64_t rows, int64_t cols, int bits, uint8_t* out,
                               int64_t ld_out, cudaStream_t s);

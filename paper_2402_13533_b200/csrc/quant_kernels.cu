@@ -274,14 +274,12 @@ __global__ void __launch_bounds__(256) k_dequantize(const uint8_t* __restrict__ 
 // shared tile is [k][n] with its 16-byte n-chunks XOR-swizzled by k / 16, so the transposing 2-byte stores
 // of a warp (8 rows n x 4 column blocks k) land on distinct banks and the row reads stay conflict-free.
 template <int BITS>
-__global__ void __launch_bounds__(256) k_dequant_t64(const uint8_t* __restrict__ codes, int64_t ldc,
-                                                     const float* __restrict__ scale,
-                                                     const float* __restrict__ offset,
-                                                     __nv_bfloat16* __restrict__ out, int64_t ld_out,
-                                                     __nv_bfloat16* __restrict__ out_lo) {
+QA_DEV void dequant_t64_tile(const uint8_t* __restrict__ codes, int64_t ldc, const float* __restrict__ scale,
+                             const float* __restrict__ offset, __nv_bfloat16* __restrict__ out, int64_t ld_out,
+                             __nv_bfloat16* __restrict__ out_lo, int64_t bx, int64_t by) {
   __shared__ __align__(16) __nv_bfloat16 sh[64][64];
   __shared__ __align__(16) __nv_bfloat16 sl[64][64];
-  const int64_t n0 = static_cast<int64_t>(blockIdx.y) * 64, k0 = static_cast<int64_t>(blockIdx.x) * 64;
+  const int64_t n0 = by * 64, k0 = bx * 64;
   const int t = threadIdx.x;
   const int r = t >> 2, seg = t & 3;  // row n0 + r, columns k0 + 16 seg .. + 15
   const int64_t n = n0 + r;
@@ -323,6 +321,26 @@ __global__ void __launch_bounds__(256) k_dequant_t64(const uint8_t* __restrict__
       *reinterpret_cast<uint4*>(out_lo + (k0 + kk) * ld_out + n0 + ch * 8) =
           *reinterpret_cast<const uint4*>(&sl[kk][pch]);
   }
+}
+
+template <int BITS>
+__global__ void __launch_bounds__(256) k_dequant_t64(const uint8_t* __restrict__ codes, int64_t ldc,
+                                                     const float* __restrict__ scale,
+                                                     const float* __restrict__ offset,
+                                                     __nv_bfloat16* __restrict__ out, int64_t ld_out,
+                                                     __nv_bfloat16* __restrict__ out_lo) {
+  dequant_t64_tile<BITS>(codes, ldc, scale, offset, out, ld_out, out_lo, blockIdx.x, blockIdx.y);
+}
+
+// The same for up to kDqJobs matrices in one launch (the members of a shared-input group): block b takes tile
+// b - first[j] of job j, row-major over its (cols / 64) x (rows / 64) tiles.
+template <int BITS>
+__global__ void __launch_bounds__(256) k_dequant_t64_multi(const DequantJobs J) {
+  int j = 0;
+  while (j + 1 < J.n && static_cast<int64_t>(blockIdx.x) >= J.first[j + 1]) ++j;
+  const int64_t t = blockIdx.x - J.first[j];
+  const int64_t tx = J.cols[j] / 64;
+  dequant_t64_tile<BITS>(J.codes[j], J.ldc[j], J.scale[j], J.offset[j], J.out[j], J.ld_out[j], nullptr, t % tx, t / tx);
 }
 
 __global__ void __launch_bounds__(256) k_unpack_pad(const uint8_t* __restrict__ codes, int64_t ldc, int64_t rows,
@@ -485,6 +503,40 @@ cudaError_t launch_dequantize(const uint8_t* codes, const float* scale, const fl
       k_dequantize<__nv_bfloat16, false><<<grid, 256, 0, s>>>(codes, ldc, scale, offset, rows, cols, bits,
                                                               static_cast<__nv_bfloat16*>(out), ld_out, out_lo);
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dequantize_t_multi(int n, const DequantJobs& jobs_in, cudaStream_t s) {
+  DequantJobs J = jobs_in;
+  J.n = n;
+  bool fast = n >= 1 && n <= kDqJobs;
+  int bits = fast ? J.bits[0] : 8;
+  int64_t tiles = 0;
+  double bytes = 0.0;
+  for (int i = 0; i < n && fast; ++i) {
+    fast = J.bits[i] == bits && J.rows[i] % 64 == 0 && J.cols[i] % 64 == 0 && J.ld_out[i] % 8 == 0 &&
+           reinterpret_cast<uintptr_t>(J.out[i]) % 16 == 0 && reinterpret_cast<uintptr_t>(J.codes[i]) % 16 == 0 &&
+           J.ldc[i] % 16 == 0;
+    J.first[i] = tiles;
+    tiles += (J.rows[i] / 64) * (J.cols[i] / 64);
+    bytes += double(J.rows[i]) * J.ldc[i] + 2.0 * double(J.rows[i]) * J.cols[i];
+  }
+  if (!fast) {  // member by member (the general kernels)
+    for (int i = 0; i < n; ++i) {
+      cudaError_t e = launch_dequantize(J.codes[i], J.scale[i], J.offset[i], J.rows[i], J.cols[i], J.bits[i], J.out[i],
+                                        QA_BF16, J.ld_out[i], true, s);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
+  if (tiles == 0) return cudaSuccess;
+  J.first[n] = tiles;
+  LaunchScope scope(kDequant, bytes, s);
+  count_launches(1);
+  if (bits == 8)
+    k_dequant_t64_multi<8><<<static_cast<unsigned>(tiles), 256, 0, s>>>(J);
+  else
+    k_dequant_t64_multi<4><<<static_cast<unsigned>(tiles), 256, 0, s>>>(J);
   return cudaGetLastError();
 }
 
