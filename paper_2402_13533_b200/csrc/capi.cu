@@ -1109,12 +1109,30 @@ int qa_group_backward(int n, const qa_qweight* const* w, const qa_tt* const* tt,
                                          G.frag, s),
                 "group TT stage 1 recompute");
   }
-  // one pass over each dy
+  // one pass over each dy; rank-8 members with the same output blocking share one launch
+  bool one_dy_launch = n <= kBwdJobs;
+  for (int i = 0; i < n && one_dy_launch; ++i) one_dy_launch = G.P[i].C == 8 && G.P[i].H == G.P[0].H;
+  if (one_dy_launch) {
+    BwdJobs bj{};
+    for (int i = 0; i < n; ++i) {
+      const LinearPlan& P = G.P[i];
+      bj.dy[i] = static_cast<const __nv_bfloat16*>(dy[i]);
+      bj.ldy[i] = P.N;
+      bj.Z1[i] = zfs[i];
+      bj.G2[i] = tt[i]->cores[1];
+      bj.G3[i] = tt[i]->cores[2];
+      bj.dz1p[i] = P.dz1p;
+      bj.g3part[i] = P.g3p;
+      bj.g2part[i] = P.g2p;
+    }
+    QA_TRY_CUDA(launch_tt_bwd_ws_group(bj, n, T, G.P[0].H, s), "group TT fused dy pass");
+  } else {
   for (int i = 0; i < n; ++i) {
     LinearPlan& P = G.P[i];
     QA_TRY_CUDA(launch_tt_bwd_fused(static_cast<const __nv_bfloat16*>(dy[i]), P.N, T, P.H, P.C, zfs[i], tt[i]->cores[1],
                                     tt[i]->cores[2], P.dz1p, P.g3p, P.g2p, s),
                 "TT fused dy pass");
+  }
   }
   // one pass over x for every member's dG1 (+ the dZ1 split rows of the dX GEMMs)
   const float* dz1[kMaxGroup];

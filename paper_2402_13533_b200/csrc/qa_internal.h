@@ -229,6 +229,19 @@ void tt_bwd_fused_plan(int64_t T, int H, int C, int* HR, int* HS, int* TS);
 cudaError_t launch_tt_bwd_fused(const __nv_bfloat16* dy, int64_t ldy, int64_t T, int H, int C, const float* Z1,
                                 const float* G2, const float* G3, float* dz1p, float* g3part, float* g2part,
                                 cudaStream_t s);
+// rank-8 dy passes of the members of a shared-input group (same H) in one launch (grid z = member)
+constexpr int kBwdJobs = 3;
+struct BwdJobs {
+  const __nv_bfloat16* dy[kBwdJobs];
+  int64_t ldy[kBwdJobs];
+  const float* Z1[kBwdJobs];
+  const float* G2[kBwdJobs];
+  const float* G3[kBwdJobs];
+  float* dz1p[kBwdJobs];
+  float* g3part[kBwdJobs];
+  float* g2part[kBwdJobs];
+};
+cudaError_t launch_tt_bwd_ws_group(const BwdJobs& jobs, int n, int64_t T, int H, cudaStream_t s);
 // shared-input groups: one x pass for NA in {2, 3} adapters (J1 = 4, R1 = 8)
 bool group_x_pass_ok(int J1, int R1, int64_t K, int NA, const void* x);
 cudaError_t launch_actquant_z1_group(const void* x, int64_t T, int64_t K, bool want_codes, uint8_t* codes,

@@ -1467,12 +1467,19 @@ struct WsLayout {
   __host__ __device__ static size_t bytes(int hr) { return gmp + sizeof(__nv_bfloat16) * 2 * size_t(hr) * 32 * 8; }
 };
 
-__global__ void __launch_bounds__(256, 1) k_tt_bwd_ws(const __nv_bfloat16* __restrict__ dy, int64_t ldy, int64_t T,
-                                                      int H, int HR, const float* __restrict__ Z1,
-                                                      const float* __restrict__ G2, const float* __restrict__ G3,
-                                                      float* __restrict__ dz1p, float* __restrict__ g3part,
-                                                      float* __restrict__ g2part) {
+// blockIdx.z selects the member of a shared-input group (same H / HR / token split): its dy, Z1, cores and
+// partial buffers come from the job table, so the members' dy passes run as one launch
+__global__ void __launch_bounds__(256, 1) k_tt_bwd_ws(const BwdJobs jobs, int64_t T, int H, int HR) {
   constexpr int C = 8, K2 = 32, J1 = 4;
+  const int mz = blockIdx.z;
+  const __nv_bfloat16* __restrict__ dy = jobs.dy[mz];
+  const int64_t ldy = jobs.ldy[mz];
+  const float* __restrict__ Z1 = jobs.Z1[mz];
+  const float* __restrict__ G2 = jobs.G2[mz];
+  const float* __restrict__ G3 = jobs.G3[mz];
+  float* __restrict__ dz1p = jobs.dz1p[mz];
+  float* __restrict__ g3part = jobs.g3part[mz];
+  float* __restrict__ g2part = jobs.g2part[mz];
   extern __shared__ __align__(16) uint8_t ws_smem[];
   auto sdy = reinterpret_cast<__nv_bfloat16(*)[2][WS_TT][FB_LDY]>(ws_smem + WsLayout::dy);
   auto sg3 = reinterpret_cast<__nv_bfloat16(*)[FB_LDY]>(ws_smem + WsLayout::g3);
@@ -2480,10 +2487,38 @@ void tt_bwd_fused_plan(int64_t T, int H, int C, int* HR, int* HS, int* TS) {
   *TS = static_cast<int>(ts < 1 ? 1 : ts);
 }
 
+cudaError_t launch_tt_bwd_ws_group(const BwdJobs& jobs, int n, int64_t T, int H, cudaStream_t s) {
+  if (T == 0 || n < 1) return cudaSuccess;
+  if (n > kBwdJobs) return cudaErrorInvalidValue;
+  int HR, HS, TS;
+  tt_bwd_fused_plan(T, H, 8, &HR, &HS, &TS);
+  const int64_t N = static_cast<int64_t>(H) * FB_COLS;
+  // algorithmic HBM bytes: dy (bf16) + Z1 in, the dZ1 partials out (the kTT class counts bytes)
+  LaunchScope scope(kTT, n * (2.0 * double(T) * N + 4.0 * double(T) * 4 * 8 * (1 + HS)), s);
+  count_launches(1);
+  const dim3 grid(static_cast<unsigned>(HS), static_cast<unsigned>(TS), static_cast<unsigned>(n));
+  const size_t smem = WsLayout::bytes(HR);
+  cudaFuncSetAttribute(k_tt_bwd_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  k_tt_bwd_ws<<<grid, 256, smem, s>>>(jobs, T, H, HR);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_tt_bwd_fused(const __nv_bfloat16* dy, int64_t ldy, int64_t T, int H, int C, const float* Z1,
                                 const float* G2, const float* G3, float* dz1p, float* g3part, float* g2part,
                                 cudaStream_t s) {
   if (T == 0) return cudaSuccess;
+  if (C == 8) {
+    BwdJobs j{};
+    j.dy[0] = dy;
+    j.ldy[0] = ldy;
+    j.Z1[0] = Z1;
+    j.G2[0] = G2;
+    j.G3[0] = G3;
+    j.dz1p[0] = dz1p;
+    j.g3part[0] = g3part;
+    j.g2part[0] = g2part;
+    return launch_tt_bwd_ws_group(j, 1, T, H, s);
+  }
   int HR, HS, TS;
   tt_bwd_fused_plan(T, H, C, &HR, &HS, &TS);
   const int64_t N = static_cast<int64_t>(H) * FB_COLS;
@@ -2491,11 +2526,7 @@ cudaError_t launch_tt_bwd_fused(const __nv_bfloat16* dy, int64_t ldy, int64_t T,
   LaunchScope scope(kTT, 2.0 * double(T) * N + 4.0 * double(T) * 4 * C * (1 + HS), s);
   count_launches(1);
   const dim3 grid(static_cast<unsigned>(HS), static_cast<unsigned>(TS));
-  if (C == 8) {
-    const size_t smem = WsLayout::bytes(HR);
-    cudaFuncSetAttribute(k_tt_bwd_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    k_tt_bwd_ws<<<grid, 256, smem, s>>>(dy, ldy, T, H, HR, Z1, G2, G3, dz1p, g3part, g2part);
-  } else {
+  {
     const size_t smem = FbLayout<16>::bytes(HR);
     cudaFuncSetAttribute(k_tt_bwd_fused<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     k_tt_bwd_fused<16><<<grid, 256, smem, s>>>(dy, ldy, T, H, HR, Z1, G2, G3, dz1p, g3part, g2part);
