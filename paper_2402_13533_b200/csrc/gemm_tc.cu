@@ -58,6 +58,30 @@ struct KParams {
   GemmEpilogue e;
 };
 
+// Column terms of the kind-0 epilogue, one 32-byte record per column pair (c, c+1):
+//   {A_c, A_c+1, B_c, B_c+1} {C_c, C_c+1, D_c, D_c+1}, A = col scale, B = col offset (zero point folded in),
+//   C = the column's constant term, D = zp_row * col_sum (int32 bits)
+// so an epilogue thread reads both columns' terms with two broadcast 16-byte shared loads.
+QA_DEV void put_col_terms(float* colP, int c, float a, float b, float cc, int32_t dd) {
+  float* q = colP + (c >> 1) * 8 + (c & 1);
+  q[0] = a;
+  q[2] = b;
+  q[4] = cc;
+  q[6] = __int_as_float(dd);
+}
+
+// y1 = sx * (A * acc' + B * rsx') + ox * C of two adjacent columns, acc' = acc + ibase - D exact in int32.
+// Each lane of the f32x2 instructions rounds exactly as the scalar fmaf form does.
+QA_DEV float2 dequant_pair(uint32_t a0, uint32_t a1, uint32_t caddr, int32_t ibase, float sx, float ox, float rsxc) {
+  const uint4 ab = lds128(caddr), cd = lds128(caddr + 16);
+  const float2 acc = make_float2(static_cast<float>(static_cast<int32_t>(a0) + ibase - static_cast<int32_t>(cd.z)),
+                                 static_cast<float>(static_cast<int32_t>(a1) + ibase - static_cast<int32_t>(cd.w)));
+  const float2 t = __fmul2_rn(make_float2(__uint_as_float(ab.z), __uint_as_float(ab.w)), make_float2(rsxc, rsxc));
+  const float2 u = __ffma2_rn(make_float2(__uint_as_float(ab.x), __uint_as_float(ab.y)), acc, t);
+  const float2 w = __fmul2_rn(make_float2(ox, ox), make_float2(__uint_as_float(cd.x), __uint_as_float(cd.y)));
+  return __ffma2_rn(make_float2(sx, sx), u, w);
+}
+
 // Probe outputs of the persistent kernels (parity tests pin the production path through them):
 //   out_acc : the raw s32 accumulators, read from TMEM before the epilogue touches them;
 //   out_y2  : (kind 0 with the adapter fold) pass A writes y1 to out_f32 and stores 0 into TMEM instead
@@ -117,11 +141,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_BYTES;
-  float* colA = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES);
-  float* colB = colA + BN;
-  float* colC = colB + BN;
-  int32_t* colD = reinterpret_cast<int32_t*>(colC + BN);
-  uint64_t* full = reinterpret_cast<uint64_t*>(colD + BN);
+  float* colP = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES);  // column terms, ColPair layout
+  uint64_t* full = reinterpret_cast<uint64_t*>(colP + 4 * BN);
   uint64_t* empty = full + STAGES;
   uint64_t* acc_full = empty + STAGES;  // [2]
   uint64_t* y1_ready = acc_full + 2;    // [2]
@@ -253,6 +274,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ------------------------------------------------------------ epilogue
     const int et = static_cast<int>(threadIdx.x) - 128;
     const GemmEpilogue& e = p.e;
+    const uint32_t cp = smem_u32(colP);
     const uint32_t quarter = warp & 3u;
     const uint32_t lane_base = (quarter * 32u) << 16;
     const bool vec_out = e.out_bf16 != nullptr && (e.ld_out % 8 == 0) &&
@@ -276,15 +298,10 @@ __global__ void __launch_bounds__(THREADS, 1)
             const float sw = e.col_scale[n];
             const float ow = e.col_offset[n] + static_cast<float>(e.zp_col) * sw;
             const int32_t rs = e.col_sum[n];
-            colA[c] = sw;
-            colB[c] = ow;
-            colC[c] = fmaf(sw, static_cast<float>(rs - e.zp_col * e.k_real), kf * ow);
-            colD[c] = e.zp_row * rs;
+            put_col_terms(colP, c, sw, ow, fmaf(sw, static_cast<float>(rs - e.zp_col * e.k_real), kf * ow),
+                          e.zp_row * rs);
           } else {
-            colA[c] = 0.f;
-            colB[c] = 0.f;
-            colC[c] = 0.f;
-            colD[c] = 0;
+            put_col_terms(colP, c, 0.f, 0.f, 0.f, 0);
           }
         }
         named_bar_sync(1, 128);
@@ -309,11 +326,10 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
             for (int h = 0; h < 2; ++h)
 #pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                const int c = (chunk + h) * 32 + j;
-                const int32_t accc = static_cast<int32_t>(v[h][j]) + ibase - colD[c];
-                v[h][j] =
-                    __float_as_uint(fmaf(sx, fmaf(colA[c], static_cast<float>(accc), colB[c] * rsxc), ox * colC[c]));
+              for (int j = 0; j < 32; j += 2) {
+                const float2 y = dequant_pair(v[h][j], v[h][j + 1], cp + ((chunk + h) * 32 + j) * 16, ibase, sx, ox, rsxc);
+                v[h][j] = __float_as_uint(y.x);
+                v[h][j + 1] = __float_as_uint(y.y);
               }
             if (probe) probe_y1(e, row_ok, row, n0 + chunk * 32, p.N, v[0], v[1]);
             tmem_st_32x32b_x32(d + chunk * 32u, v[0]);
@@ -345,13 +361,14 @@ __global__ void __launch_bounds__(THREADS, 1)
             if (j < ncols) e.out_acc[row * e.ld_acc + nb + j] = static_cast<int32_t>(v[j]);
         float y[32];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
+        for (int j = 0; j < 32; j += 2) {
           if (KIND == 0 && !fold_ext) {  // no adapter: dequantise the s32 accumulator here
-            const int c = chunk * 32 + j;
-            const int32_t accc = static_cast<int32_t>(v[j]) + ibase - colD[c];
-            y[j] = fmaf(sx, fmaf(colA[c], static_cast<float>(accc), colB[c] * rsxc), ox * colC[c]);
+            const float2 yy = dequant_pair(v[j], v[j + 1], cp + (chunk * 32 + j) * 16, ibase, sx, ox, rsxc);
+            y[j] = yy.x;
+            y[j + 1] = yy.y;
           } else {
             y[j] = __uint_as_float(v[j]);
+            y[j + 1] = __uint_as_float(v[j + 1]);
           }
         }
         if (fold_ext && probe && row_ok) probe_y2(e, row, nb, ncols, y);
@@ -427,11 +444,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES2 * A_BYTES;
   uint8_t* sStage = smem + STAGES2 * STAGE2_BYTES;  // 1024-aligned (128B-swizzled TMA boxes)
-  float* colA = reinterpret_cast<float*>(sStage + STG2_BYTES);
-  float* colB = colA + BN;
-  float* colC = colB + BN;
-  int32_t* colD = reinterpret_cast<int32_t*>(colC + BN);
-  uint64_t* full = reinterpret_cast<uint64_t*>(colD + BN);
+  float* colP = reinterpret_cast<float*>(sStage + STG2_BYTES);  // column terms, ColPair layout
+  uint64_t* full = reinterpret_cast<uint64_t*>(colP + 4 * BN);
   uint64_t* empty = full + STAGES2;
   uint64_t* acc_full = empty + STAGES2;
   uint64_t* y1_ready = acc_full + 2;
@@ -582,6 +596,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     // ------------------------------------------------------------ epilogue (both CTAs, own 128 rows)
     const int et = static_cast<int>(threadIdx.x) - 128;
     const GemmEpilogue& e = p.e;
+    const uint32_t cp = smem_u32(colP);
     const uint32_t quarter = warp & 3u;
     const uint32_t lane_base = (quarter * 32u) << 16;
     const bool vec_out = e.out_bf16 != nullptr && (e.ld_out % 8 == 0) &&
@@ -615,15 +630,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             const float sw = e.col_scale[n];
             const float ow = e.col_offset[n] + static_cast<float>(e.zp_col) * sw;
             const int32_t rs = e.col_sum[n];
-            colA[c] = sw;
-            colB[c] = ow;
-            colC[c] = fmaf(sw, static_cast<float>(rs - e.zp_col * e.k_real), kf * ow);
-            colD[c] = e.zp_row * rs;
+            put_col_terms(colP, c, sw, ow, fmaf(sw, static_cast<float>(rs - e.zp_col * e.k_real), kf * ow),
+                          e.zp_row * rs);
           } else {
-            colA[c] = 0.f;
-            colB[c] = 0.f;
-            colC[c] = 0.f;
-            colD[c] = 0;
+            put_col_terms(colP, c, 0.f, 0.f, 0.f, 0);
           }
         }
         named_bar_sync(1, 128);
@@ -647,11 +657,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 #pragma unroll
             for (int h = 0; h < 2; ++h)
 #pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                const int c = (chunk + h) * 32 + j;
-                const int32_t accc = static_cast<int32_t>(v[h][j]) + ibase - colD[c];
-                v[h][j] =
-                    __float_as_uint(fmaf(sx, fmaf(colA[c], static_cast<float>(accc), colB[c] * rsxc), ox * colC[c]));
+              for (int j = 0; j < 32; j += 2) {
+                const float2 y = dequant_pair(v[h][j], v[h][j + 1], cp + ((chunk + h) * 32 + j) * 16, ibase, sx, ox, rsxc);
+                v[h][j] = __float_as_uint(y.x);
+                v[h][j + 1] = __float_as_uint(y.y);
               }
             if (probe) probe_y1(e, row_ok, row, n0 + chunk * 32, p.N, v[0], v[1]);
             tmem_st_32x32b_x32(d + chunk * 32u, v[0]);
@@ -685,11 +694,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             for (int j2 = 0; j2 < 16; ++j2) {
               float a, bb;
               if (KIND == 0 && !fold_ext) {
-                const int c = (2 * q + h) * 32 + 2 * j2;
-                const int32_t c0 = static_cast<int32_t>(v[2 * j2]) + ibase - colD[c];
-                const int32_t c1 = static_cast<int32_t>(v[2 * j2 + 1]) + ibase - colD[c + 1];
-                a = fmaf(sx, fmaf(colA[c], static_cast<float>(c0), colB[c] * rsxc), ox * colC[c]);
-                bb = fmaf(sx, fmaf(colA[c + 1], static_cast<float>(c1), colB[c + 1] * rsxc), ox * colC[c + 1]);
+                const float2 y = dequant_pair(v[2 * j2], v[2 * j2 + 1], cp + ((2 * q + h) * 32 + 2 * j2) * 16, ibase,
+                                              sx, ox, rsxc);
+                a = y.x;
+                bb = y.y;
               } else {
                 a = __uint_as_float(v[2 * j2]);
                 bb = __uint_as_float(v[2 * j2 + 1]);
@@ -729,13 +737,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             if (j < ncols) e.out_acc[row * e.ld_acc + nb + j] = static_cast<int32_t>(v[j]);
         float y[32];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
+        for (int j = 0; j < 32; j += 2) {
           if (KIND == 0 && !fold_ext) {
-            const int c = chunk * 32 + j;
-            const int32_t accc = static_cast<int32_t>(v[j]) + ibase - colD[c];
-            y[j] = fmaf(sx, fmaf(colA[c], static_cast<float>(accc), colB[c] * rsxc), ox * colC[c]);
+            const float2 yy = dequant_pair(v[j], v[j + 1], cp + (chunk * 32 + j) * 16, ibase, sx, ox, rsxc);
+            y[j] = yy.x;
+            y[j + 1] = yy.y;
           } else {
             y[j] = __uint_as_float(v[j]);
+            y[j + 1] = __uint_as_float(v[j + 1]);
           }
         }
         if (fold_ext && probe && row_ok) probe_y2(e, row, nb, ncols, y);
