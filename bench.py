@@ -824,8 +824,10 @@ def main():
     lib.qa_timing_enable(1)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
+    h0 = time.perf_counter()
     for _ in range(args.steps):
         step(xs, dys)
+    host_issue_ms = (time.perf_counter() - h0) * 1e3 / max(args.steps, 1)
     e1.record(stream)
     torch.cuda.synchronize(dev)
     barrier()
@@ -833,6 +835,15 @@ def main():
     launches = (lib.qa_launch_count() - n_launch0) // max(args.steps, 1)
     per_class = {c: _lib.timing_read(c) for c in ("gemm_i8", "gemm_bf16", "quantize", "tt", "dequant")}
     lib.qa_timing_enable(0)
+    # diagnostic (outside the timed region): the same steps without the per-launch timing events
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    for _ in range(args.steps):
+        step(xs, dys)
+    e3.record(stream)
+    torch.cuda.synchronize(dev)
+    diag = {"host_issue_ms_per_step": host_issue_ms,
+            "ms_per_step_without_launch_events": e2.elapsed_time(e3) / max(args.steps, 1)}
     clocks = clocks_sampler_stop(sampler, clk_path, local) if sampler else None
     ms_total = max_over_ranks(e0.elapsed_time(e1))
     ms_step = ms_total / args.steps
@@ -974,6 +985,7 @@ def main():
             "weight_quantize": wquant, "decoder": decoder,
             "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches * args.steps), "gpu_launches_per_step": int(launches), "clocks": clocks,
+            "diagnostics": diag,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -36,10 +36,12 @@ def main():
     lib = _lib.lib()
     g = torch.Generator(device=dev).manual_seed(1)
     q = quantize_rows(torch.randn((a.N, a.K), generator=g, device=dev) * 0.02, a.bits)
-    spec = TTSpec.for_shape(a.N, a.K, a.rank)
+    spec = TTSpec.for_shape(a.N, a.K, a.rank if a.rank > 0 else 8)
     cores = [torch.randn(spec.core_shape(i), generator=g, device=dev) * 0.01 for i in range(spec.d)]
-    wc, ttc = q.as_c(), spec.as_c(cores)
-    nb = lib.qa_linear_workspace_bytes(ctypes.byref(wc), ctypes.byref(ttc), a.T)
+    wc = q.as_c()
+    ttc = spec.as_c(cores) if a.rank > 0 else None  # --rank 0: the base linear alone (no adapter)
+    ttp = ctypes.byref(ttc) if ttc is not None else None
+    nb = lib.qa_linear_workspace_bytes(ctypes.byref(wc), ttp, a.T)
     ws = torch.empty(nb, dtype=torch.uint8, device=dev)
     x = torch.randn((a.T, a.K), generator=g, device=dev).to(torch.bfloat16)
     dy = torch.randn((a.T, a.N), generator=g, device=dev).to(torch.bfloat16)
@@ -51,10 +53,10 @@ def main():
 
     def run():
         if a.only in ("fwd", "both"):
-            _lib.check(lib.qa_linear_forward(ctypes.byref(wc), ctypes.byref(ttc), x.data_ptr(), _lib.QA_BF16, a.T,
+            _lib.check(lib.qa_linear_forward(ctypes.byref(wc), ttp, x.data_ptr(), _lib.QA_BF16, a.T,
                                              y.data_ptr(), None, None, None, ws.data_ptr(), nb, sptr), "fwd")
         if a.only in ("bwd", "both"):
-            _lib.check(lib.qa_linear_backward(ctypes.byref(wc), ctypes.byref(ttc), x.data_ptr(), _lib.QA_BF16,
+            _lib.check(lib.qa_linear_backward(ctypes.byref(wc), ttp, x.data_ptr(), _lib.QA_BF16,
                                               dy.data_ptr(), _lib.QA_BF16, a.T, dx.data_ptr(), None,
                                               ctypes.cast(gptr, ctypes.POINTER(ctypes.c_void_p)), 0, ws.data_ptr(),
                                               nb, sptr), "bwd")
