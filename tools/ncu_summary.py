@@ -79,8 +79,36 @@ def summarise_launches(path: str, last: int = 0) -> str:
     return "\n".join(out) + "\n"
 
 
+def per_launch(path: str, last: int) -> str:
+    """Duration, DRAM read / write and rate of each of the last `last` launches of a launch-list CSV taken with
+    --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum."""
+    lines = open(path).read().splitlines()
+    start = next(i for i, l in enumerate(lines) if "Kernel Name" in l)
+    rows = list(csv.reader(io.StringIO("\n".join(lines[start:]))))
+    hdr = rows[0]
+    ii, ki, mi = hdr.index("ID"), hdr.index("Kernel Name"), hdr.index("Metric Name")
+    vi, ui = hdr.index("Metric Value"), hdr.index("Metric Unit")
+    launches = collections.OrderedDict()
+    for r in rows[1:]:
+        if len(r) <= vi:
+            continue
+        d = launches.setdefault(r[ii], {"name": r[ki].split("(")[0]})
+        scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "byte": 1e-6,
+                 "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}.get(r[ui], 1.0)
+        d[r[mi]] = float(r[vi].replace(",", "")) * scale
+    out = ["per launch, one timed step (cold cache, serialised): duration, DRAM read / write, DRAM rate"]
+    for d in list(launches.values())[-last:]:
+        us = d.get("gpu__time_duration.sum", 0.0)
+        rd, wr = d.get("dram__bytes_read.sum", 0.0), d.get("dram__bytes_write.sum", 0.0)
+        rate = (rd + wr) / us if us else 0.0  # MB / us = TB/s
+        out.append(f"{us:8.1f} us  rd {rd:9.1f} MB  wr {wr:8.1f} MB  {rate:5.2f} TB/s  {d['name']}")
+    return "\n".join(out) + "\n"
+
+
 if __name__ == "__main__":
     if sys.argv[1] == "--launches":
         sys.stdout.write(summarise_launches(sys.argv[2], int(sys.argv[3]) if len(sys.argv) > 3 else 0))
+    elif sys.argv[1] == "--per-launch":
+        sys.stdout.write(per_launch(sys.argv[2], int(sys.argv[3])))
     else:
         sys.stdout.write(summarise_report(sys.argv[1]))

@@ -10,7 +10,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
   --log-file ${O}_launches.csv $B > ${O}_ncu_l.log 2>&1; echo launches rc=$?
 rm -f /tmp/p_*.ncu-rep
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_gemm_tc -s 42 -c 14 -f -o /tmp/p_gemm $B > ${O}_ncu_g.log 2>&1; echo gemm rc=$?
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_aq|k_tt_|k_grad|k_dequant|k_g1_frag|k_build_v" -s 126 -c 42 -f -o /tmp/p_side $B > ${O}_ncu_s.log 2>&1; echo side rc=$?
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_aq|k_tt_|k_grad|k_dequant|k_g1_frag|k_build_v" -s 60 -c 20 -f -o /tmp/p_side $B > ${O}_ncu_s.log 2>&1; echo side rc=$?
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_merge_fast -s 12 -c 1 -f -o /tmp/p_merge32 python tools/merge_bench.py --set 70b --out f32 --iters 1 > ${O}_ncu_m.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_merge_fast -s 12 -c 1 -f -o /tmp/p_merge16 python tools/merge_bench.py --set 70b --out bf16 --iters 1 >> ${O}_ncu_m.log 2>&1; echo merge rc=$?
 python tools/quant_micro.py > ${O}_quant.log 2>&1
