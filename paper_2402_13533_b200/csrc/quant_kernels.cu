@@ -274,28 +274,48 @@ __global__ void __launch_bounds__(256) k_dequantize(const uint8_t* __restrict__ 
 // shared tile is [k][n] with its 16-byte n-chunks XOR-swizzled by k / 16, so the transposing 2-byte stores
 // of a warp (8 rows n x 4 column blocks k) land on distinct banks and the row reads stay conflict-free.
 template <int BITS>
-QA_DEV void dequant_t64_tile(const uint8_t* __restrict__ codes, int64_t ldc, const float* __restrict__ scale,
-                             const float* __restrict__ offset, __nv_bfloat16* __restrict__ out, int64_t ld_out,
-                             __nv_bfloat16* __restrict__ out_lo, int64_t bx, int64_t by) {
-  __shared__ __align__(16) __nv_bfloat16 sh[64][64];
-  __shared__ __align__(16) __nv_bfloat16 sl[64][64];
+struct T64Codes {  // one thread's 16 codes of a 64 x 64 tile: row n0 + t / 4, columns k0 + 16 (t % 4) ..
+  uint32_t w[BITS == 8 ? 4 : 2];
+};
+
+template <int BITS>
+QA_DEV T64Codes<BITS> dequant_t64_load(const uint8_t* __restrict__ codes, int64_t ldc, int64_t bx, int64_t by) {
+  const int t = threadIdx.x, r = t >> 2, seg = t & 3;
+  const int64_t n = by * 64 + r, k0 = bx * 64;
+  T64Codes<BITS> c;
+  if (BITS == 8) {
+    const uint4 u = __ldg(reinterpret_cast<const uint4*>(codes + n * ldc + k0 + seg * 16));
+    c.w[0] = u.x;
+    c.w[1] = u.y;
+    c.w[2] = u.z;
+    c.w[3] = u.w;
+  } else {
+    const uint2 u = __ldg(reinterpret_cast<const uint2*>(codes + n * ldc + (k0 + seg * 16) / 2));
+    c.w[0] = u.x;
+    c.w[1] = u.y;
+  }
+  return c;
+}
+
+// Transposed bf16 dequantisation for the dX GEMM operand: outᵀ[k, n] = bf16(code·scale + offset),
+// 64 x 64 tiles, 16-byte code loads and 16-byte stores (full tiles; edges go through k_dequantize).  The
+// shared tile is [k][n] with its 16-byte n-chunks XOR-swizzled by k / 16, so the transposing 2-byte stores
+// of a warp (8 rows n x 4 column blocks k) land on distinct banks and the row reads stay conflict-free.
+// sh / sl: [64][64] shared tiles (sl only for the hi / lo split of fp32 callers).
+template <int BITS>
+QA_DEV void dequant_t64_store(const T64Codes<BITS>& cw, const float* __restrict__ scale,
+                              const float* __restrict__ offset, __nv_bfloat16* __restrict__ out, int64_t ld_out,
+                              __nv_bfloat16* __restrict__ out_lo, int64_t bx, int64_t by, __nv_bfloat16 (*sh)[64],
+                              __nv_bfloat16 (*sl)[64]) {
   const int64_t n0 = by * 64, k0 = bx * 64;
   const int t = threadIdx.x;
   const int r = t >> 2, seg = t & 3;  // row n0 + r, columns k0 + 16 seg .. + 15
   const int64_t n = n0 + r;
   const int col = (((r >> 3) ^ seg) << 3) | (r & 7);  // swizzled position of n in rows k = 16 seg + i
   uint32_t c[16];
-  if (BITS == 8) {
-    const uint4 u = __ldg(reinterpret_cast<const uint4*>(codes + n * ldc + k0 + seg * 16));
-    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
-    for (int i = 0; i < 16; ++i) c[i] = (w[i >> 2] >> (8 * (i & 3))) & 0xFFu;
-  } else {
-    const uint2 u = __ldg(reinterpret_cast<const uint2*>(codes + n * ldc + (k0 + seg * 16) / 2));
-    const uint32_t w[2] = {u.x, u.y};
-#pragma unroll
-    for (int i = 0; i < 16; ++i) c[i] = (w[i >> 3] >> (4 * (i & 7))) & 0xFu;
-  }
+  for (int i = 0; i < 16; ++i)
+    c[i] = BITS == 8 ? (cw.w[i >> 2] >> (8 * (i & 3))) & 0xFFu : (cw.w[i >> 3] >> (4 * (i & 7))) & 0xFu;
   if (out_lo == nullptr) {
     // bf16 operand of the dX GEMM: one fp32 FMA per code (its rounding sits 2^-16 below the bf16 step)
     const float s = scale[n], o = offset[n];
@@ -329,18 +349,44 @@ __global__ void __launch_bounds__(256) k_dequant_t64(const uint8_t* __restrict__
                                                      const float* __restrict__ offset,
                                                      __nv_bfloat16* __restrict__ out, int64_t ld_out,
                                                      __nv_bfloat16* __restrict__ out_lo) {
-  dequant_t64_tile<BITS>(codes, ldc, scale, offset, out, ld_out, out_lo, blockIdx.x, blockIdx.y);
+  __shared__ __align__(16) __nv_bfloat16 sh[64][64];
+  __shared__ __align__(16) __nv_bfloat16 sl[64][64];
+  const T64Codes<BITS> c = dequant_t64_load<BITS>(codes, ldc, blockIdx.x, blockIdx.y);
+  dequant_t64_store<BITS>(c, scale, offset, out, ld_out, out_lo, blockIdx.x, blockIdx.y, sh, sl);
 }
 
-// The same for up to kDqJobs matrices in one launch (the members of a shared-input group): block b takes tile
-// b - first[j] of job j, row-major over its (cols / 64) x (rows / 64) tiles.
+// The same for up to kDqJobs matrices in one launch (the members of a shared-input group), DQ_TPB tiles per block:
+// block b takes tiles DQ_TPB b .. of the concatenated row-major tile lists (job j from tile first[j]); every tile's
+// code loads are issued before the first tile is converted (DQ_TPB x 16 bytes in flight per thread).
+#ifndef QA_DQ_TPB
+#define QA_DQ_TPB 2
+#endif
+constexpr int DQ_TPB = QA_DQ_TPB;
+
 template <int BITS>
 __global__ void __launch_bounds__(256) k_dequant_t64_multi(const DequantJobs J) {
-  int j = 0;
-  while (j + 1 < J.n && static_cast<int64_t>(blockIdx.x) >= J.first[j + 1]) ++j;
-  const int64_t t = blockIdx.x - J.first[j];
-  const int64_t tx = J.cols[j] / 64;
-  dequant_t64_tile<BITS>(J.codes[j], J.ldc[j], J.scale[j], J.offset[j], J.out[j], J.ld_out[j], nullptr, t % tx, t / tx);
+  __shared__ __align__(16) __nv_bfloat16 sh[64][64];
+  int jt[DQ_TPB];
+  int64_t tx[DQ_TPB], ty[DQ_TPB];
+  T64Codes<BITS> c[DQ_TPB];
+#pragma unroll
+  for (int u = 0; u < DQ_TPB; ++u) {
+    const int64_t g = static_cast<int64_t>(blockIdx.x) * DQ_TPB + u;
+    int j = 0;
+    while (j + 1 < J.n && g >= J.first[j + 1]) ++j;
+    jt[u] = g < J.first[J.n] ? j : -1;
+    const int64_t t = g - J.first[j], ncol = J.cols[j] / 64;
+    tx[u] = t % ncol;
+    ty[u] = t / ncol;
+    if (jt[u] >= 0) c[u] = dequant_t64_load<BITS>(J.codes[j], J.ldc[j], tx[u], ty[u]);
+  }
+#pragma unroll
+  for (int u = 0; u < DQ_TPB; ++u) {
+    if (jt[u] < 0) break;  // block-uniform
+    if (u > 0) __syncthreads();  // the previous tile's shared-memory reads are done
+    const int j = jt[u];
+    dequant_t64_store<BITS>(c[u], J.scale[j], J.offset[j], J.out[j], J.ld_out[j], nullptr, tx[u], ty[u], sh, nullptr);
+  }
 }
 
 __global__ void __launch_bounds__(256) k_unpack_pad(const uint8_t* __restrict__ codes, int64_t ldc, int64_t rows,
@@ -488,7 +534,26 @@ cudaError_t launch_dequantize(const uint8_t* codes, const float* scale, const fl
                         reinterpret_cast<uintptr_t>(out) % 16 == 0 &&
                         (out_lo == nullptr || reinterpret_cast<uintptr_t>(out_lo) % 16 == 0) &&
                         reinterpret_cast<uintptr_t>(codes) % 16 == 0 && (ldc % 16 == 0);
-    if (fast_t) {
+    if (fast_t && out_lo == nullptr) {  // the dX GEMM operand: the multi-tile kernel with one job
+      DequantJobs J{};
+      J.n = 1;
+      J.codes[0] = codes;
+      J.scale[0] = scale;
+      J.offset[0] = offset;
+      J.rows[0] = rows;
+      J.cols[0] = cols;
+      J.ldc[0] = ldc;
+      J.ld_out[0] = ld_out;
+      J.bits[0] = bits;
+      J.out[0] = static_cast<__nv_bfloat16*>(out);
+      J.first[0] = 0;
+      J.first[1] = (rows / 64) * (cols / 64);
+      const unsigned blocks = static_cast<unsigned>((J.first[1] + DQ_TPB - 1) / DQ_TPB);
+      if (bits == 8)
+        k_dequant_t64_multi<8><<<blocks, 256, 0, s>>>(J);
+      else
+        k_dequant_t64_multi<4><<<blocks, 256, 0, s>>>(J);
+    } else if (fast_t) {
       const dim3 g64(static_cast<unsigned>(cols / 64), static_cast<unsigned>(rows / 64));
       if (bits == 8)
         k_dequant_t64<8><<<g64, 256, 0, s>>>(codes, ldc, scale, offset, static_cast<__nv_bfloat16*>(out), ld_out,
@@ -533,10 +598,11 @@ cudaError_t launch_dequantize_t_multi(int n, const DequantJobs& jobs_in, cudaStr
   J.first[n] = tiles;
   LaunchScope scope(kDequant, bytes, s);
   count_launches(1);
+  const unsigned blocks = static_cast<unsigned>((tiles + DQ_TPB - 1) / DQ_TPB);
   if (bits == 8)
-    k_dequant_t64_multi<8><<<static_cast<unsigned>(tiles), 256, 0, s>>>(J);
+    k_dequant_t64_multi<8><<<blocks, 256, 0, s>>>(J);
   else
-    k_dequant_t64_multi<4><<<static_cast<unsigned>(tiles), 256, 0, s>>>(J);
+    k_dequant_t64_multi<4><<<blocks, 256, 0, s>>>(J);
   return cudaGetLastError();
 }
 
