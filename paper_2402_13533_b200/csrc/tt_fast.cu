@@ -1734,22 +1734,30 @@ __global__ void __launch_bounds__(256) k_grad_reduce3(const ReduceArgs a) {
     b -= jb * a.bext_blocks;
     const float* G1 = a.G1s[jb];
     __nv_bfloat16* bext = a.bexts[jb];
-    // 32-bit index math (K * ldb < 2^31, checked by the launcher)
-    const int idx = static_cast<int>(b) * 256 + static_cast<int>(threadIdx.x);
-    if (bext == nullptr || idx >= static_cast<int>(a.K * a.ldb)) return;
+    // 8 consecutive columns of one row per thread (ldb % 8 == 0), one 16-byte store; 32-bit index math
+    // (K * ldb < 2^31, checked by the launcher)
+    const int e0 = (static_cast<int>(b) * 256 + static_cast<int>(threadIdx.x)) * 8;
+    if (bext == nullptr || e0 >= static_cast<int>(a.K * a.ldb)) return;
     const int ldb = static_cast<int>(a.ldb);
-    const int k = idx / ldb;
-    const int c = idx - k * ldb;
+    const int k = e0 / ldb;
+    const int c0 = e0 - k * ldb;
     const int K2 = a.R1 * a.J1;
-    float v = 0.f;
-    if (c < 3 * K2) {  // [B_hi | B_hi | B_lo] against [dZ1_hi | dZ1_lo | dZ1_hi]
-      const int cc = c % K2;
-      const int aa = cc / a.J1, Jp = cc % a.J1;
-      const int j1 = k / a.J1;
-      if (k - j1 * a.J1 == Jp) v = __ldg(G1 + static_cast<int64_t>(j1) * a.R1 + aa);
-      if (c >= 2 * K2) v -= __bfloat162float(__float2bfloat16_rn(v));
+    const int j1 = k / a.J1, J = k - j1 * a.J1;
+    uint32_t w[4];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int c = c0 + q;
+      float v = 0.f;
+      if (c < 3 * K2) {  // [B_hi | B_hi | B_lo] against [dZ1_hi | dZ1_lo | dZ1_hi]
+        const int cc = c % K2;
+        const int aa = cc / a.J1, Jp = cc % a.J1;
+        if (J == Jp) v = __ldg(G1 + static_cast<int64_t>(j1) * a.R1 + aa);
+        if (c >= 2 * K2) v -= __bfloat162float(__float2bfloat16_rn(v));
+      }
+      const uint32_t h = __bfloat16_as_ushort(__float2bfloat16_rn(v));
+      w[q >> 1] = (q & 1) ? (w[q >> 1] | (h << 16)) : h;
     }
-    bext[idx] = __float2bfloat16_rn(v);
+    *reinterpret_cast<uint4*>(bext + e0) = make_uint4(w[0], w[1], w[2], w[3]);
     return;
   }
   const ReduceSet& S = a.set[si];
@@ -1757,18 +1765,18 @@ __global__ void __launch_bounds__(256) k_grad_reduce3(const ReduceArgs a) {
   const int64_t gi = b * 32 + lane;
   float s = 0.f;
   if (gi < S.numel) {
+    // this warp's partials c = warp, warp + 8, ... summed in that order; eight loads in flight per batch
+    const float* __restrict__ pp = S.part + gi;
+    const int64_t st = S.numel;
     int c = warp;
-    for (; c + 24 < S.nparts; c += 32) {
-      const float a0 = S.part[static_cast<int64_t>(c) * S.numel + gi];
-      const float a1 = S.part[static_cast<int64_t>(c + 8) * S.numel + gi];
-      const float a2 = S.part[static_cast<int64_t>(c + 16) * S.numel + gi];
-      const float a3 = S.part[static_cast<int64_t>(c + 24) * S.numel + gi];
-      s += a0;
-      s += a1;
-      s += a2;
-      s += a3;
+    for (; c + 56 < S.nparts; c += 64) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldg(pp + static_cast<int64_t>(c + 8 * u) * st);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s += v[u];
     }
-    for (; c < S.nparts; c += 8) s += S.part[static_cast<int64_t>(c) * S.numel + gi];
+    for (; c < S.nparts; c += 8) s += __ldg(pp + static_cast<int64_t>(c) * st);
   }
   red[warp][lane] = s;
   __syncthreads();
@@ -2573,7 +2581,8 @@ cudaError_t launch_grad_reduce_n(int n, const float* const* parts, const int* np
   a.J1 = J1;
   a.K = K;
   a.ldb = ldb;
-  a.bext_blocks = (K * ldb + 255) / 256;
+  if (ldb % 8 != 0) return cudaErrorInvalidValue;  // B_ext rows are written 8 columns (16 bytes) per thread
+  a.bext_blocks = (K * ldb / 8 + 255) / 256;
   int nb = 0;  // B_ext jobs run after the sets, in member order (a member without one leaves an idle range)
   for (int j = 0; j < n; ++j) {
     a.G1s[j] = G1[j];
