@@ -956,6 +956,21 @@ int launch(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, in
 
 }  // namespace
 
+// bf16 rows [T, *] (row stride ld elements) as the 3-D view {64 elements, T rows, cols / 64 column blocks}: box
+// {64, box_rows, box_cb} with 128-byte swizzle, so one load fills a [column block][row][128 B] tile; rows past T
+// are zero-filled.
+bool make_tmap_rows3d(CUtensorMap* m, const void* x, int64_t T, int64_t cols, int64_t ld, int box_rows, int box_cb) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (enc == nullptr || cols % 64 != 0 || (ld * 2) % 16 != 0 || reinterpret_cast<uintptr_t>(x) % 16 != 0) return false;
+  const cuuint64_t dims[3] = {64, static_cast<cuuint64_t>(T), static_cast<cuuint64_t>(cols / 64)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld * 2), 128};
+  const cuuint32_t box[3] = {64, static_cast<cuuint32_t>(box_rows), static_cast<cuuint32_t>(box_cb)};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(x), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 int gemm_tc(int kind, const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
             const GemmEpilogue& epi, cudaStream_t s, const GemmExt* ext) {
   if (M == 0 || N == 0) return QA_OK;

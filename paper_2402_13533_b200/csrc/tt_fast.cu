@@ -1455,21 +1455,36 @@ __global__ void __launch_bounds__(256) k_tt_bwd_fused(const __nv_bfloat16* __res
 // of a block stays in registers: the m16n8 D fragments of Z2_h and dZ2_h are re-used as the
 // m16n8k8 A fragments (dZ1 += dZ2_h · Gm_hᵀ) and, transposed with movmatrix, as the B fragments
 // of dG3 += dy_hᵀ · Z2_h and dG2_h += Z1ᵀ · dZ2_h.  dG3 / dG2 accumulate in registers per warp.
-constexpr int WS_TT = 16, WS_NHW = 2, WS_LDZ1 = 40;
+constexpr int WS_TT = 16, WS_NHW = 2, WS_LDZ1 = 40, WS_DYBLK = WS_TT * 256 * 2;
 
-struct WsLayout {
-  static constexpr size_t dy = 0;                                                         // bf16 [8][2][TT][LDY]
-  static constexpr size_t g3 = dy + sizeof(__nv_bfloat16) * 8 * 2 * WS_TT * FB_LDY;     // bf16 [8][LDY]
+struct WsLayout {  // offsets from the 1024-byte aligned base (bytes() includes the alignment slack)
+  static constexpr size_t dy = 0;                       // bf16 [8][2][4 column blocks][TT][64], 128-byte swizzle
+  static constexpr size_t dybar = dy + 8 * 2 * WS_DYBLK;                                 // u64 [8][2]
+  static constexpr size_t g3 = dybar + 8 * 2 * sizeof(uint64_t);                        // bf16 [8][LDY]
   static constexpr size_t z1p = g3 + sizeof(__nv_bfloat16) * 8 * FB_LDY;                // bf16 [2][TT][LDZ1]
   static constexpr size_t z1raw = z1p + sizeof(__nv_bfloat16) * 2 * WS_TT * WS_LDZ1;    // f32 [2][TT][32]
   static constexpr size_t dzs = z1raw + sizeof(float) * 2 * WS_TT * 32;                 // f32 [8][TT][33]
   static constexpr size_t gmp = dzs + sizeof(float) * 8 * WS_TT * 33;                   // bf16 [2][HR][32][8]
-  __host__ __device__ static size_t bytes(int hr) { return gmp + sizeof(__nv_bfloat16) * 2 * size_t(hr) * 32 * 8; }
+  __host__ __device__ static size_t bytes(int hr) {
+    return 1024 + gmp + sizeof(__nv_bfloat16) * 2 * size_t(hr) * 32 * 8;
+  }
 };
+
+// dy maps of the (up to kBwdJobs) jobs: rows [T, N] as {64 elements, T, N / 64}, box {64, WS_TT, 4}
+struct DyMaps {
+  CUtensorMap m[kBwdJobs];
+};
+
+// dy element (row r, column c, c % 8 == 0) of a warp's 16 x 256 block written by the 3-D TMA box: column block
+// c / 64 of 2 KB, 128-byte rows, 16-byte chunks XOR-swizzled by r % 8
+QA_DEV uint32_t ws_dy_addr(uint32_t blk, int r, int c) {
+  return blk + (c >> 6) * (WS_TT * 128) + r * 128 + ((((c >> 3) & 7) ^ (r & 7)) << 4);
+}
 
 // blockIdx.z selects the member of a shared-input group (same H / HR / token split): its dy, Z1, cores and
 // partial buffers come from the job table, so the members' dy passes run as one launch
-__global__ void __launch_bounds__(256, 1) k_tt_bwd_ws(const BwdJobs jobs, int64_t T, int H, int HR) {
+__global__ void __launch_bounds__(256, 1) k_tt_bwd_ws(const BwdJobs jobs, const __grid_constant__ DyMaps maps,
+                                                      int64_t T, int H, int HR) {
   constexpr int C = 8, K2 = 32, J1 = 4;
   const int mz = blockIdx.z;
   const __nv_bfloat16* __restrict__ dy = jobs.dy[mz];
@@ -1480,8 +1495,11 @@ __global__ void __launch_bounds__(256, 1) k_tt_bwd_ws(const BwdJobs jobs, int64_
   float* __restrict__ dz1p = jobs.dz1p[mz];
   float* __restrict__ g3part = jobs.g3part[mz];
   float* __restrict__ g2part = jobs.g2part[mz];
-  extern __shared__ __align__(16) uint8_t ws_smem[];
-  auto sdy = reinterpret_cast<__nv_bfloat16(*)[2][WS_TT][FB_LDY]>(ws_smem + WsLayout::dy);
+  extern __shared__ __align__(16) uint8_t ws_smem_raw[];
+  uint8_t* ws_smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(ws_smem_raw) + 1023) & ~uintptr_t(1023));
+  const CUtensorMap* tmdy = &maps.m[mz];
+  uint64_t* dybar = reinterpret_cast<uint64_t*>(ws_smem + WsLayout::dybar);  // [warp][slot]
+  const uint32_t sdy0 = smem_u32(ws_smem + WsLayout::dy);
   auto sg3 = reinterpret_cast<__nv_bfloat16(*)[FB_LDY]>(ws_smem + WsLayout::g3);
   auto sz1p = reinterpret_cast<__nv_bfloat16(*)[WS_TT][WS_LDZ1]>(ws_smem + WsLayout::z1p);
   auto sz1raw = reinterpret_cast<float(*)[WS_TT][K2]>(ws_smem + WsLayout::z1raw);
@@ -1508,15 +1526,18 @@ __global__ void __launch_bounds__(256, 1) k_tt_bwd_ws(const BwdJobs jobs, int64_
     gm(0, hl, aj)[c] = hi;
     gm(1, hl, aj)[c] = __float2bfloat16_rn(v - __bfloat162float(hi));
   }
+  if (tid < 16) mbar_init(&dybar[tid], 1);
+  fence_barrier_init();
+  // one TMA box per (tile, h block) item: the warp's 16 x 256 dy block into its slot (rows past T zero-filled)
   auto load_item = [&](int64_t it, int slot) {
     const int64_t t0 = (tile0 + it / nmine) * WS_TT;
     const int h = h0 + warp + 8 * static_cast<int>(it % nmine);
-#pragma unroll
-    for (int r = 0; r < WS_TT; ++r) {  // one 512-byte row per warp instruction
-      const int64_t t = t0 + r;
-      const bool ok = t < T;
-      cp_async16(&sdy[warp][slot][r][lane * 8], dy + (ok ? t : 0) * ldy + static_cast<int64_t>(h) * FB_COLS + lane * 8,
-                 ok);
+    __syncwarp();  // every lane's reads of the slot (item it - 2) are done ...
+    if (lane == 0) {
+      fence_proxy_async_smem();  // ... and ordered before the asynchronous-proxy write
+      mbar_arrive_expect_tx(&dybar[warp * 2 + slot], WS_DYBLK);
+      tma_load_3d(ws_smem + WsLayout::dy + (warp * 2 + slot) * WS_DYBLK, tmdy, &dybar[warp * 2 + slot], 0,
+                  static_cast<int32_t>(t0), 4 * h);
     }
   };
   auto load_z1raw = [&](int64_t tile) {
@@ -1538,6 +1559,7 @@ __global__ void __launch_bounds__(256, 1) k_tt_bwd_ws(const BwdJobs jobs, int64_
 #pragma unroll
       for (int k = 0; k < 4; ++k) g2acc[i][m][k] = 0.f;
 
+  __syncthreads();  // barrier inits visible to every warp
   load_z1raw(tile0);
   if (nit > 0) load_item(0, 0);
   cp_async_commit();
@@ -1577,14 +1599,9 @@ __global__ void __launch_bounds__(256, 1) k_tt_bwd_ws(const BwdJobs jobs, int64_
     for (int i = 0; i < WS_NHW; ++i, ++it) {
       if (i >= nmine) break;
       const int slot = static_cast<int>(it & 1), hl = warp + 8 * i;
-      if (i == 0)
-        cp_async_wait<1>();
-      else
-        cp_async_wait<0>();
-      __syncwarp();
+      mbar_wait(&dybar[warp * 2 + slot], static_cast<uint32_t>((it >> 1) & 1));
       if (it + 1 < nit) load_item(it + 1, slot ^ 1);
-      cp_async_commit();
-      const __nv_bfloat16(*dyw)[FB_LDY] = sdy[warp][slot];
+      const uint32_t dyw = sdy0 + (warp * 2 + slot) * WS_DYBLK;
       // Z2_h = Z1 · Gm_h
       float z2[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -1601,7 +1618,7 @@ __global__ void __launch_bounds__(256, 1) k_tt_bwd_ws(const BwdJobs jobs, int64_
 #pragma unroll
       for (int k = 0; k < 16; ++k) {
         uint32_t a0, a1, a2, a3, b0, b1;
-        ldsm_x4(&dyw[lane & 15][k * 16 + (lane >> 4) * 8], a0, a1, a2, a3);
+        ldsm_x4_a(ws_dy_addr(dyw, lane & 15, k * 16 + (lane >> 4) * 8), a0, a1, a2, a3);
         ldsm_x2(&sg3[lane & 7][k * 16 + ((lane >> 3) & 1) * 8], b0, b1);
         if (k & 1)
           mma_16816(e1, a0, a1, a2, a3, b0, b1);
@@ -1617,7 +1634,7 @@ __global__ void __launch_bounds__(256, 1) k_tt_bwd_ws(const BwdJobs jobs, int64_
 #pragma unroll
         for (int m = 0; m < 16; ++m) {
           uint32_t a0, a1, a2, a3;
-          ldsm_x4_t(&dyw[(q >> 1) * 8 + (lane & 7)][m * 16 + (q & 1) * 8], a0, a1, a2, a3);
+          ldsm_x4_t_a(ws_dy_addr(dyw, (q >> 1) * 8 + (lane & 7), m * 16 + (q & 1) * 8), a0, a1, a2, a3);
           mma_16816(acc3[m], a0, a1, a2, a3, b0, b1);
         }
       }
@@ -2525,9 +2542,12 @@ cudaError_t launch_tt_bwd_ws_group(const BwdJobs& jobs, int n, int64_t T, int H,
   LaunchScope scope(kTT, n * (2.0 * double(T) * N + 4.0 * double(T) * 4 * 8 * (1 + HS)), s);
   count_launches(1);
   const dim3 grid(static_cast<unsigned>(HS), static_cast<unsigned>(TS), static_cast<unsigned>(n));
+  DyMaps maps;
+  for (int i = 0; i < n; ++i)
+    if (!make_tmap_rows3d(&maps.m[i], jobs.dy[i], T, N, jobs.ldy[i], WS_TT, 4)) return cudaErrorInvalidValue;
   const size_t smem = WsLayout::bytes(HR);
   cudaFuncSetAttribute(k_tt_bwd_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  k_tt_bwd_ws<<<grid, 256, smem, s>>>(jobs, T, H, HR);
+  k_tt_bwd_ws<<<grid, 256, smem, s>>>(jobs, maps, T, H, HR);
   return cudaGetLastError();
 }
 
