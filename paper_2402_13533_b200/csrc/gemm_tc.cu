@@ -956,6 +956,11 @@ int launch(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, in
 
 }  // namespace
 
+// bf16 rows [rows, cols] (row stride ld elements): boxes of 64 columns x box_rows rows, 128-byte swizzle
+bool make_tmap_bf16_rows(CUtensorMap* m, const void* x, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+  return make_tmap(m, x, 2, rows, cols, ld, box_rows);
+}
+
 // bf16 rows [T, *] (row stride ld elements) as the 3-D view {64 elements, T rows, cols / 64 column blocks}: box
 // {64, box_rows, box_cb} with 128-byte swizzle, so one load fills a [column block][row][128 B] tile; rows past T
 // are zero-filled.

@@ -243,6 +243,7 @@ struct BwdJobs {
 };
 cudaError_t launch_tt_bwd_ws_group(const BwdJobs& jobs, int n, int64_t T, int H, cudaStream_t s);
 bool make_tmap_rows3d(CUtensorMap* m, const void* x, int64_t T, int64_t cols, int64_t ld, int box_rows, int box_cb);
+bool make_tmap_bf16_rows(CUtensorMap* m, const void* x, int64_t rows, int64_t cols, int64_t ld, int box_rows);
 // shared-input groups: one x pass for NA in {2, 3} adapters (J1 = 4, R1 = 8)
 bool group_x_pass_ok(int J1, int R1, int64_t K, int NA, const void* x);
 cudaError_t launch_actquant_z1_group(const void* x, int64_t T, int64_t K, bool want_codes, uint8_t* codes,

@@ -1820,6 +1820,13 @@ __global__ void __launch_bounds__(256) k_grad_reduce3(const ReduceArgs a) {
 // 16-token stages; dZ1 is staged per 64 tokens (HS partials summed in fixed order), and CTAs of
 // column block 0 also emit the [hi | lo | hi | 0] split rows the dX GEMM's extension reads.
 constexpr int DM_COLS = 1024, DM_LDX = DM_COLS + 32, DM_ST = 16, DM_NSTG = 4, DM_DZT = 64;
+constexpr int DM_XST = DM_ST * DM_COLS * 2;  // bytes of one x stage (16 tokens x 1024 columns, one TMA box)
+
+// x stage element (row r, column c) of the 3-D TMA box {64, 16, 16}: column block c / 64 of 2 KB, 128-byte rows,
+// 16-byte chunks XOR-swizzled by r % 8
+QA_DEV uint32_t dm_x_addr(uint32_t stage, int r, int c) {
+  return stage + (c >> 6) * (DM_ST * 128) + r * 128 + ((((c >> 3) & 7) ^ (r & 7)) << 4) + ((c & 7) << 1);
+}
 
 // NA adapters sharing x (a decoder layer's q / k / v or up / gate) run in one pass: per adapter its
 // own dZ1 planes, B fragments and accumulators.
@@ -1830,13 +1837,17 @@ struct DgAdapters {
 };
 
 template <int R1, int NA = 1>
-__global__ void __launch_bounds__(256, 2) k_tt_dg1m(const __nv_bfloat16* __restrict__ x, int64_t T, int64_t K,
+__global__ void __launch_bounds__(256, 2) k_tt_dg1m(const __grid_constant__ CUtensorMap tmx,
+                                                    const __nv_bfloat16* __restrict__ x, int64_t T, int64_t K,
                                                     const DgAdapters ad, int S, int HS, int64_t ldb, int raw_async,
-                                                    int nstg) {
+                                                    int nstg, int x3d) {
   constexpr int J1 = 4, K2 = J1 * R1, NN = R1 / 8;
   extern __shared__ __align__(16) uint8_t dm_smem[];
-  auto xs = reinterpret_cast<__nv_bfloat16(*)[DM_ST][DM_LDX]>(dm_smem);  // [NSTG]
-  const size_t XS_BYTES = sizeof(__nv_bfloat16) * nstg * DM_ST * DM_LDX;  // nstg in {3, 4}
+  // x ring: nstg TMA stages (1024-byte aligned) and their mbarriers inside the XS_BYTES region
+  const size_t XS_BYTES = sizeof(__nv_bfloat16) * nstg * DM_ST * DM_LDX;  // >= 1024 + nstg * (DM_XST + 8)
+  uint8_t* xring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dm_smem) + 1023) & ~uintptr_t(1023));
+  uint64_t* xbar = reinterpret_cast<uint64_t*>(xring + static_cast<size_t>(nstg) * DM_XST);
+  const uint32_t xring_s = smem_u32(xring);
   auto dzs = reinterpret_cast<__nv_bfloat16(*)[DM_DZT][R1][J1]>(dm_smem + XS_BYTES);  // [NA][2 planes]
   // raw fp32 dZ1 partials of the next 64-token blocks, prefetched by cp.async: [2][NA][HS][DZT][K2]
   float* raw = reinterpret_cast<float*>(dm_smem + XS_BYTES + sizeof(__nv_bfloat16) * NA * 2 * DM_DZT * R1 * J1);
@@ -1869,14 +1880,28 @@ __global__ void __launch_bounds__(256, 2) k_tt_dg1m(const __nv_bfloat16* __restr
       }
     }
   };
+  if (tid == 0) {
+    for (int i = 0; i < nstg; ++i) mbar_init(&xbar[i], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  // stage k: 16 tokens x 1024 columns as up to 16 TMA boxes of 64 columns (128-byte swizzle) issued by one thread;
+  // columns past K and rows past T are zero-filled, blocks wholly past K are not loaded (their j1 rows are never
+  // stored), rows of the next split past t1 meet zero dZ1 rows
+  const int ncb = static_cast<int>((K - c0 + 63) / 64 < 16 ? (K - c0 + 63) / 64 : 16);
   auto issue = [&](int64_t k) {
-    if (k < nst) {
+    if (k < nst && tid == 0) {
       const int slot = static_cast<int>(k % nstg);
-      for (int i = tid; i < DM_ST * (DM_COLS / 8); i += 256) {
-        const int r = i / (DM_COLS / 8), ch = i % (DM_COLS / 8);
-        const int64_t t = t0 + k * DM_ST + r, col = c0 + ch * 8;
-        const bool ok = t < t1 && col < K;
-        cp_async16(&xs[slot][r][ch * 8], ok ? x + t * K + col : x, ok);
+      fence_proxy_async_smem();  // the slot's previous readers (behind the CTA barrier) before the async write
+      if (x3d) {  // K % 64 == 0: the whole stage as one box {64, 16, 16} of the view {64, T, K / 64}
+        mbar_arrive_expect_tx(&xbar[slot], DM_XST);
+        tma_load_3d(xring + static_cast<size_t>(slot) * DM_XST, &tmx, &xbar[slot], 0,
+                    static_cast<int32_t>(t0 + k * DM_ST), static_cast<int32_t>(c0 / 64));
+      } else {
+        mbar_arrive_expect_tx(&xbar[slot], static_cast<uint32_t>(ncb) * DM_ST * 128);
+        for (int cb = 0; cb < ncb; ++cb)
+          tma_load_2d(xring + static_cast<size_t>(slot) * DM_XST + cb * (DM_ST * 128), &tmx, &xbar[slot],
+                      static_cast<int32_t>(c0 + 64 * cb), static_cast<int32_t>(t0 + k * DM_ST));
       }
     }
   };
@@ -1888,6 +1913,7 @@ __global__ void __launch_bounds__(256, 2) k_tt_dg1m(const __nv_bfloat16* __restr
   for (int64_t k = 0; k < nst; ++k) {
     const int slot = static_cast<int>(k % nstg);
     cp_async_wait_dyn(nstg - 2);
+    mbar_wait(&xbar[slot], static_cast<uint32_t>((k / nstg) & 1));
     __syncthreads();  // stage k (and its dZ1 block) visible to all warps; stage k - 1's readers are done
     if (k % SPB == 0) {  // dZ1 rows of the next 64 tokens: HS partials summed, hi / lo planes, [t][a][J]
       const int64_t blk = k / SPB, tb = t0 + k * DM_ST;
@@ -1951,25 +1977,29 @@ __global__ void __launch_bounds__(256, 2) k_tt_dg1m(const __nv_bfloat16* __restr
     if (raw_async && k % SPB == 1) issue_raw(k / SPB + 1);  // complete by the next block's first stage
     cp_async_commit();
     const int zr = static_cast<int>(k % SPB) * DM_ST;
+    const uint32_t xst = xring_s + static_cast<uint32_t>(slot) * DM_XST;
 #pragma unroll
     for (int ks = 0; ks < DM_ST / 4; ++ks) {  // 4 tokens x 4 J per k-step
-      const int tr = ks * 4 + (tq >> 1), J = 2 * (tq & 1);
+      // the k-step's tokens: stage rows r0 (k 0..7) and r0 + 1 (k 8..15) for lane pair s = tq / 2 at rows 4 apart,
+      // so a quarter-warp's two rows have swizzle keys differing in bit 2 (conflict-free 32-bit reads); the B
+      // fragments read the dZ1 rows of the same tokens
+      const int r0 = 8 * (ks >> 1) + 4 * (tq >> 1) + 2 * (ks & 1), J = 2 * (tq & 1);
       uint32_t bh[NA * NN][2], bl[NA * NN][2];
 #pragma unroll
       for (int n = 0; n < NA * NN; ++n) {
         const int aa = n / NN, nn = n % NN;
-        bh[n][0] = *reinterpret_cast<const uint32_t*>(&dzs[2 * aa][zr + tr][nn * 8 + g][J]);
-        bh[n][1] = *reinterpret_cast<const uint32_t*>(&dzs[2 * aa][zr + tr + 2][nn * 8 + g][J]);
-        bl[n][0] = *reinterpret_cast<const uint32_t*>(&dzs[2 * aa + 1][zr + tr][nn * 8 + g][J]);
-        bl[n][1] = *reinterpret_cast<const uint32_t*>(&dzs[2 * aa + 1][zr + tr + 2][nn * 8 + g][J]);
+        bh[n][0] = *reinterpret_cast<const uint32_t*>(&dzs[2 * aa][zr + r0][nn * 8 + g][J]);
+        bh[n][1] = *reinterpret_cast<const uint32_t*>(&dzs[2 * aa][zr + r0 + 1][nn * 8 + g][J]);
+        bl[n][0] = *reinterpret_cast<const uint32_t*>(&dzs[2 * aa + 1][zr + r0][nn * 8 + g][J]);
+        bl[n][1] = *reinterpret_cast<const uint32_t*>(&dzs[2 * aa + 1][zr + r0 + 1][nn * 8 + g][J]);
       }
 #pragma unroll
       for (int m = 0; m < 2; ++m) {
         const int jl = (warp * 2 + m) * 16 + g;
-        const uint32_t a0 = *reinterpret_cast<const uint32_t*>(&xs[slot][tr][4 * jl + J]);
-        const uint32_t a1 = *reinterpret_cast<const uint32_t*>(&xs[slot][tr][4 * (jl + 8) + J]);
-        const uint32_t a2 = *reinterpret_cast<const uint32_t*>(&xs[slot][tr + 2][4 * jl + J]);
-        const uint32_t a3 = *reinterpret_cast<const uint32_t*>(&xs[slot][tr + 2][4 * (jl + 8) + J]);
+        const uint32_t a0 = lds32(dm_x_addr(xst, r0, 4 * jl + J));
+        const uint32_t a1 = lds32(dm_x_addr(xst, r0, 4 * (jl + 8) + J));
+        const uint32_t a2 = lds32(dm_x_addr(xst, r0 + 1, 4 * jl + J));
+        const uint32_t a3 = lds32(dm_x_addr(xst, r0 + 1, 4 * (jl + 8) + J));
 #pragma unroll
         for (int n = 0; n < NA * NN; ++n) {
           mma_16816(acc[m][n], a0, a1, a2, a3, bh[n][0], bh[n][1]);
@@ -2730,14 +2760,18 @@ cudaError_t launch_tt_dg1_group(const void* x, int64_t T, int64_t K, const float
   const int raw_async = shp.raw >= 0 ? shp.raw : (smem + raw_bytes <= 220 * 1024 ? 1 : 0);
   if (raw_async) smem += raw_bytes;
   const dim3 gm(static_cast<unsigned>(gx), static_cast<unsigned>(Sm));
+  CUtensorMap tmx;
+  const int x3d = K % 64 == 0 ? 1 : 0;
+  if (!(x3d ? make_tmap_rows3d(&tmx, x, T, K, K, DM_ST, DM_COLS / 64) : make_tmap_bf16_rows(&tmx, x, T, K, K, DM_ST)))
+    return cudaErrorInvalidValue;
   if (NA == 2) {
     cudaFuncSetAttribute(k_tt_dg1m<8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    k_tt_dg1m<8, 2><<<gm, 256, smem, s>>>(static_cast<const __nv_bfloat16*>(x), T, K, ad, static_cast<int>(Sm), HS,
-                                          ldb, raw_async, nstg);
+    k_tt_dg1m<8, 2><<<gm, 256, smem, s>>>(tmx, static_cast<const __nv_bfloat16*>(x), T, K, ad, static_cast<int>(Sm), HS,
+                                          ldb, raw_async, nstg, x3d);
   } else {
     cudaFuncSetAttribute(k_tt_dg1m<8, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    k_tt_dg1m<8, 3><<<gm, 256, smem, s>>>(static_cast<const __nv_bfloat16*>(x), T, K, ad, static_cast<int>(Sm), HS,
-                                          ldb, raw_async, nstg);
+    k_tt_dg1m<8, 3><<<gm, 256, smem, s>>>(tmx, static_cast<const __nv_bfloat16*>(x), T, K, ad, static_cast<int>(Sm), HS,
+                                          ldb, raw_async, nstg, x3d);
   }
   return cudaGetLastError();
 }
@@ -2780,14 +2814,19 @@ cudaError_t launch_tt_dg1(const void* x, int x_dtype, int64_t T, int64_t K, cons
       const int raw_async = shp.raw >= 0 ? shp.raw : (smem + raw_bytes <= 220 * 1024 ? 1 : 0);
       if (raw_async) smem += raw_bytes;
       const DgAdapters ad{{dz1, nullptr, nullptr}, {part, nullptr, nullptr}, {dz1b, nullptr, nullptr}};
+      CUtensorMap tmx;
+      const int x3d = K % 64 == 0 ? 1 : 0;
+      if (!(x3d ? make_tmap_rows3d(&tmx, x, T, K, K, DM_ST, DM_COLS / 64)
+                : make_tmap_bf16_rows(&tmx, x, T, K, K, DM_ST)))
+        return cudaErrorInvalidValue;
       if (R1 == 8) {
         cudaFuncSetAttribute(k_tt_dg1m<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        k_tt_dg1m<8><<<gm, 256, smem, s>>>(static_cast<const __nv_bfloat16*>(x), T, K, ad, static_cast<int>(Sm), HS,
-                                           ldb, raw_async, nstg);
+        k_tt_dg1m<8><<<gm, 256, smem, s>>>(tmx, static_cast<const __nv_bfloat16*>(x), T, K, ad, static_cast<int>(Sm), HS,
+                                           ldb, raw_async, nstg, x3d);
       } else {
         cudaFuncSetAttribute(k_tt_dg1m<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        k_tt_dg1m<16><<<gm, 256, smem, s>>>(static_cast<const __nv_bfloat16*>(x), T, K, ad, static_cast<int>(Sm), HS,
-                                            ldb, raw_async, nstg);
+        k_tt_dg1m<16><<<gm, 256, smem, s>>>(tmx, static_cast<const __nv_bfloat16*>(x), T, K, ad, static_cast<int>(Sm), HS,
+                                            ldb, raw_async, nstg, x3d);
       }
       return cudaGetLastError();
     }
