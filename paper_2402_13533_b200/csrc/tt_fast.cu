@@ -1450,7 +1450,8 @@ __global__ void __launch_bounds__(256) k_tt_bwd_fused(const __nv_bfloat16* __res
 // ---------------------------------------------------------------------------------------------
 // Warp-specialised fused backward for C = 8 (the benchmark's rank).  Same contractions as
 // k_tt_bwd_fused, but each warp owns whole output blocks h (local h = warp, warp + 8) and streams
-// its own 16-token x 256-column dy blocks through a private 2-slot cp.async ring, so the only CTA
+// its own 16-token x 256-column dy blocks through a private 2-slot ring (one TMA box per block, completion on the
+// slot's mbarrier; lane 0 issues the next block as soon as the current one has landed), so the only CTA
 // barriers are at 16-token tile boundaries (Z1 planes in, dZ1 partials out).  Every intermediate
 // of a block stays in registers: the m16n8 D fragments of Z2_h and dZ2_h are re-used as the
 // m16n8k8 A fragments (dZ1 += dZ2_h · Gm_hᵀ) and, transposed with movmatrix, as the B fragments
@@ -1816,8 +1817,8 @@ __global__ void __launch_bounds__(256) k_grad_reduce3(const ReduceArgs a) {
 // needs, per lane, the bf16 pair x[t, 4 j1 + J .. + 1] — one 32-bit shared-memory load — and the
 // B fragment the pair dZ1[t, a, J .. J + 1] of the [t][a][J] staged dZ1 rows.  x is exact in bf16;
 // dZ1 enters as hi + lo bf16 (two MMAs), so the sums keep fp32-class accuracy.  A CTA owns 1024
-// columns (16 m-tiles, 2 per warp) of a token range, streamed through a 4-stage cp.async ring of
-// 16-token stages; dZ1 is staged per 64 tokens (HS partials summed in fixed order), and CTAs of
+// columns (16 m-tiles, 2 per warp) of a token range, streamed through a ring of 16-token stages (one TMA box per
+// stage, mbarrier completion); dZ1 is staged per 64 tokens (HS partials summed in fixed order), and CTAs of
 // column block 0 also emit the [hi | lo | hi | 0] split rows the dX GEMM's extension reads.
 constexpr int DM_COLS = 1024, DM_LDX = DM_COLS + 32, DM_ST = 16, DM_NSTG = 4, DM_DZT = 64;
 constexpr int DM_XST = DM_ST * DM_COLS * 2;  // bytes of one x stage (16 tokens x 1024 columns, one TMA box)
